@@ -1,0 +1,464 @@
+"""Restatement of the reference's hot-path protocols, generic over a backend.
+
+TEST INFRASTRUCTURE ONLY. Each function cites the reference lines it follows
+(/root/reference/proj/src/...). The backend is any object with the slotforge
+op set (encrypt, zeros, add, sub, mul, mul_plain, mac_plain, rotate,
+level_drop, exact_transform, with_layout, ledger): the numpy SimBackend
+(oracle/slot_sim.py) pins these restatements against the reference's golden
+vectors, and the CKKS CPU oracle (oracle/ckks.py) runs the same op sequence on
+real ciphertexts so the GPU product can be held to it bit for bit.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from .errors import CacheEmpty, CacheFull, LayoutMismatch, ShapeMismatch
+from .layout import (Layout, log2_exact, make_interleaved, make_mask, padded_dim, stride_mask,
+                     validate_layout, block_mask)
+
+
+# --------------------------------------------------------------------------- vmm.cpp
+
+def ceil_sqrt(k: int) -> int:
+    """vmm.cpp:10-15."""
+    b = int(math.isqrt(k))
+    while b * b < k:
+        b += 1
+    while b > 1 and (b - 1) * (b - 1) >= k:
+        b -= 1
+    return b
+
+
+def bsgs_split(k: int):
+    """vmm.cpp:23-28: baby = ceil(sqrt(k)), giant = ceil(k / baby)."""
+    if k < 1:
+        raise ShapeMismatch("bsgs_split: k must be >= 1")
+    b = ceil_sqrt(k)
+    return b, (k + b - 1) // b
+
+
+@dataclass
+class Shape:
+    """vmm.cpp:124-153 (InterleavedShape)."""
+    N: int
+    d_in: int
+    d_out: int
+    t_in: int
+    t_out: int
+    k: int
+    alpha_up: int
+    ladder_T: int
+    tau_in: int
+    tau_out: int
+    tau_u: int
+    carry: int
+    delta: int
+
+
+def interleaved_shape(N: int, rows: int, cols: int, tau_in: int, tau_out: int) -> Shape:
+    d_in, d_out = padded_dim(rows), padded_dim(cols)
+    if d_in > N or d_out > N:
+        raise ShapeMismatch("vmm_interleaved: padded dimension exceeds N")
+    t_in, t_out = N // d_in, N // d_out
+    if not (0 <= tau_in < t_in):
+        raise ShapeMismatch("vmm_interleaved: input offset out of range")
+    if not (0 <= tau_out < t_out):
+        raise ShapeMismatch("vmm_interleaved: output offset out of range")
+    tau_u = tau_in % t_out
+    return Shape(N, d_in, d_out, t_in, t_out, max(d_in * d_out // N, 1), max(1, t_out // t_in),
+                 max(t_in, t_out), tau_in, tau_out, tau_u, 1 if tau_out < tau_u else 0,
+                 (tau_out - tau_u) % t_out)
+
+
+def interleaved_diag(s: Shape, W: np.ndarray, g: int, j: np.ndarray) -> np.ndarray:
+    """vmm.cpp:159-168 vectorised over slot indices j (pre-giant frame)."""
+    N = s.N
+    i0 = (j + g * s.t_in * s.t_out - s.tau_in) % N
+    row = (i0 // s.t_in + (i0 % s.t_in) * s.alpha_up) % s.d_in
+    rel = (j - s.tau_u) % N
+    u = rel % s.t_out
+    within = u // s.t_in + (u % s.t_in) * s.alpha_up
+    col = (rel // s.t_out + s.carry) % s.d_out
+    rows, cols = W.shape
+    ok = (g * s.t_out + within < s.d_in) & (row < rows) & (col < cols)
+    out = np.zeros(len(j))
+    out[ok] = W[row[ok], col[ok]]
+    return out
+
+
+def interleaved_plain(s: Shape, W: np.ndarray, g: int, giant_shift: int) -> np.ndarray:
+    """vmm.cpp:170-175: p[i] = diag(g, (i - giant_shift) mod N)."""
+    i = np.arange(s.N, dtype=np.int64)
+    return interleaved_diag(s, W, g, (i - giant_shift) % s.N)
+
+
+def vmm_interleaved(be, x, W: np.ndarray, bsgs: bool = False, out_offset: int = 0,
+                    mask_output: bool = False):
+    """vmm.cpp:179-236 (the scheme of record)."""
+    N = be.N
+    if x.layout is None or x.layout.kind != "interleaved":
+        raise LayoutMismatch("vmm_interleaved: input must carry an interleaved layout")
+    if x.layout.deferred_mask:
+        raise LayoutMismatch("vmm_interleaved: mask (or fuse) deferred garbage before feeding a VMM")
+    W = np.asarray(W, dtype=np.float64)
+    s = interleaved_shape(N, W.shape[0], W.shape[1], x.layout.offset, out_offset)
+    if x.layout.d != s.d_in:
+        raise ShapeMismatch(f"vmm_interleaved: layout d={x.layout.d} but weights want {s.d_in}")
+    # 1. ladder (vmm.cpp:190-193)
+    stair = x
+    step = 1
+    while step < s.t_in:
+        stair = be.add(stair, be.rotate(stair, step * (s.ladder_T - 1)))
+        step <<= 1
+    unit = s.t_in * s.t_out
+    # 2. multiply-accumulate (vmm.cpp:196-224)
+    if not bsgs:
+        terms = [(be.rotate(stair, g * unit), interleaved_plain(s, W, g, 0)) for g in range(s.k)]
+        acc = be.mac_plain(terms)
+    else:
+        b, giants = bsgs_split(s.k)
+        baby = [stair] + [be.rotate(stair, g1 * unit, hoisted=True) for g1 in range(1, b)]
+        acc = None
+        for g2 in range(giants):
+            shift = g2 * b * unit
+            terms = [(baby[g1], interleaved_plain(s, W, g2 * b + g1, shift))
+                     for g1 in range(b) if g2 * b + g1 < s.k]
+            partial = be.mac_plain(terms)
+            aligned = be.rotate(partial, shift)
+            acc = aligned if g2 == 0 else be.add(acc, aligned)
+    # 3. reduce (vmm.cpp:226-230)
+    m = 0
+    while (1 << m) < s.t_out:
+        st = 1 << m
+        acc = be.add(acc, be.rotate(acc, -st if (s.delta >> m) & 1 else st))
+        m += 1
+    # 4. mask or defer (vmm.cpp:233-234)
+    if mask_output:
+        acc = be.mul_plain(acc, stride_mask(N, s.t_out, s.tau_out))
+    return be.with_layout(acc, Layout("interleaved", s.d_out, s.t_out, s.tau_out, 1, not mask_output))
+
+
+def predict_interleaved_cost(N: int, rows: int, cols: int, bsgs: bool = False, mask_output: bool = False):
+    """vmm.cpp:473-488 -> (rotations, ct_pt_mults, depth)."""
+    d_in, d_out = padded_dim(rows), padded_dim(cols)
+    t_in, t_out = N // d_in, N // d_out
+    k = max(d_in * d_out // N, 1)
+    rot = log2_exact(t_in) + log2_exact(t_out)
+    if bsgs:
+        b, g = bsgs_split(k)
+        rot += (b - 1) + (g - 1)
+    else:
+        rot += k - 1
+    return rot, k + (1 if mask_output else 0), 1 + (1 if mask_output else 0)
+
+
+def valid_mask(ly: Layout, N: int) -> np.ndarray:
+    """vmm.cpp:45-56."""
+    return make_mask(ly, N, "valid")
+
+
+def apply_deferred_mask(be, x):
+    """vmm.cpp:58-64."""
+    if x.layout is None or not x.layout.deferred_mask:
+        return x
+    out = be.mul_plain(x, valid_mask(x.layout, be.N))
+    return be.with_layout(out, x.layout.with_(deferred_mask=False))
+
+
+def rope_plaintexts(n: int, d_head: int, ly: Layout, N: int, base: float = 10000.0):
+    """vmm.cpp:66-83: p0 = cos, p1 = sin on even elements, p2 = -sin on odd."""
+    validate_layout(ly, N)
+    if ly.kind != "interleaved":
+        raise LayoutMismatch("rope_plaintexts: interleaved layout required")
+    if d_head <= 0 or d_head % 2:
+        raise ShapeMismatch("rope_plaintexts: d_head must be positive and even")
+    p0, p1, p2 = np.zeros(N), np.zeros(N), np.zeros(N)
+    for e in range(ly.d):
+        pair = (e % d_head) // 2
+        ang = float(n) * math.pow(base, -2.0 * pair / float(d_head))
+        i = e * ly.t + ly.offset
+        p0[i] = math.cos(ang)
+        if e % 2 == 0:
+            p1[i] = math.sin(ang)
+        else:
+            p2[i] = -math.sin(ang)
+    return p0, p1, p2
+
+
+def fused_extract(be, x, succ: str, rope: Optional[dict] = None, coeff=None):
+    """vmm.cpp:85-109. succ in {rope, silu_mask, norm_mask, vcache_mask};
+    rope = {n, d_head, s, base}."""
+    N = be.N
+    if x.layout is None:
+        raise LayoutMismatch("fused_extract: input must carry a layout")
+    ly = x.layout
+    if succ == "rope":
+        if rope is None:
+            raise ShapeMismatch("fused_extract: rope successor needs RoPEParams")
+        p0, p1, p2 = rope_plaintexts(rope["n"], rope["d_head"], ly, N, rope.get("base", 10000.0))
+        s = rope["s"]
+        y = be.mul_plain(x, p0)
+        y = be.add(y, be.rotate(be.mul_plain(x, p1), -s))
+        y = be.add(y, be.rotate(be.mul_plain(x, p2), s))
+        return be.with_layout(y, ly.with_(deferred_mask=False))
+    m = valid_mask(ly, N)
+    if coeff is not None:
+        m = m * np.asarray(coeff)
+    y = be.mul_plain(x, m)
+    return be.with_layout(y, ly.with_(deferred_mask=False))
+
+
+# ----------------------------------------------------------------- kv_attention.cpp
+
+@dataclass
+class AttentionConfig:
+    """kv_attention.hpp:32-42."""
+    N: int
+    d: int
+    H: int = 1
+    n0: int = 0
+    n_max: int = 0
+
+    @property
+    def d_head(self):
+        return self.d // self.H
+
+    @property
+    def t(self):
+        return self.N // self.d
+
+    @property
+    def group_tokens(self):
+        return self.N // self.H
+
+
+def validate_attention_config(cfg: AttentionConfig, N_backend: int):
+    """kv_attention.cpp:80-88."""
+    from .layout import is_pow2
+    if cfg.N != N_backend:
+        raise ShapeMismatch("attention config N != backend slot count")
+    if not (is_pow2(cfg.N) and is_pow2(cfg.d) and is_pow2(cfg.H)):
+        raise ShapeMismatch("attention config: N, d and H must be powers of two")
+    if cfg.H > cfg.d or cfg.d > cfg.N:
+        raise ShapeMismatch("attention config: need H <= d <= N")
+    if cfg.n0 < 0 or cfg.n_max < max(cfg.n0, 1):
+        raise ShapeMismatch("attention config: need 0 <= n0 <= n_max, n_max >= 1")
+
+
+@dataclass
+class KVCache:
+    """kv_attention.hpp:49-54 (copy-on-write value; appends return a new one)."""
+    n_prime: int = 0
+    k_cts: list = field(default_factory=list)
+    v_cts: list = field(default_factory=list)  # [group][variant]
+
+    def copy(self):
+        return KVCache(self.n_prime, list(self.k_cts), [list(g) for g in self.v_cts])
+
+
+def v_variant_count(cfg):
+    return cfg.d_head if cfg.H == 1 else 2 * cfg.d_head - 1
+
+
+def v_variant_index(cfg, w):
+    dh = cfg.d_head
+    if cfg.H == 1:
+        if not (0 <= w < dh):
+            raise ShapeMismatch("v_variant_index: merged variant out of range")
+        return w
+    if w <= -dh or w >= dh:
+        raise ShapeMismatch("v_variant_index: variant out of range")
+    return w + dh - 1
+
+
+def v_variant_of(cfg, e, u_local):
+    raw = e - u_local // cfg.t
+    return raw % cfg.d_head if cfg.H == 1 else raw
+
+
+def _require_clean_interleaved(x, cfg, offset, who):
+    """kv_attention.cpp:15-27."""
+    if x.layout is None or x.layout.kind != "interleaved":
+        raise LayoutMismatch(f"{who}: input must carry an interleaved layout")
+    if x.layout.d != cfg.d:
+        raise ShapeMismatch(f"{who}: layout width {x.layout.d} != configured {cfg.d}")
+    if x.layout.offset != offset:
+        raise LayoutMismatch(f"{who}: expected slot offset {offset}, got {x.layout.offset}")
+    if x.layout.deferred_mask:
+        raise LayoutMismatch(f"{who}: input garbage must be cleared first")
+
+
+def replicate_lanes(be, q, t):
+    """kv_attention.cpp:30-34."""
+    r = q
+    step = 1
+    while step < t:
+        r = be.add(r, be.rotate(r, -step))
+        step <<= 1
+    return r
+
+
+def fold_within_head(be, c, d_head, t):
+    """kv_attention.cpp:38-41."""
+    l = 0
+    while (1 << l) < d_head:
+        c = be.add(c, be.rotate(c, (1 << l) * t))
+        l += 1
+    return c
+
+
+def fold_lanes(be, c, t):
+    """kv_attention.cpp:44-47."""
+    step = 1
+    while step < t:
+        c = be.add(c, be.rotate(c, step))
+        step <<= 1
+    return c
+
+
+def touched_variants(cfg, tokens):
+    """kv_attention.cpp:53-57."""
+    u_max = (tokens - 1) // cfg.t
+    if cfg.H == 1:
+        return 0, cfg.d_head
+    return -u_max, cfg.d_head
+
+
+def rope_apply(be, x, cfg, position, base=10000.0):
+    """kv_attention.cpp:111-117 (s = t)."""
+    if x.layout is None or x.layout.kind != "interleaved" or x.layout.d != cfg.d:
+        raise LayoutMismatch("rope_apply: input must be interleaved at the configured width")
+    return fused_extract(be, x, "rope", dict(n=position, d_head=cfg.d_head, s=cfg.t, base=base))
+
+
+def k_append(be, cache: KVCache, k_new, cfg):
+    """kv_attention.cpp:131-143."""
+    if cache.n_prime >= cfg.n_max:
+        raise CacheFull("k_append: cache at capacity")
+    t = cfg.t
+    _require_clean_interleaved(k_new, cfg, cache.n_prime % t, "k_append")
+    out = cache.copy()
+    if cache.n_prime % t == 0:
+        out.k_cts.append(k_new)
+    else:
+        out.k_cts[-1] = be.add(out.k_cts[-1], k_new)
+    out.n_prime = cache.n_prime + 1
+    return out
+
+
+def v_piece_mask(cfg, e, position):
+    """The mask of kv_attention.cpp:157-160: ones at (h*d_head+e)*t + pos%t."""
+    m = np.zeros(cfg.N)
+    j0 = position % cfg.t
+    for h in range(cfg.H):
+        m[(h * cfg.d_head + e) * cfg.t + j0] = 1.0
+    return m
+
+
+def make_v_pieces(be, v_open, cfg, position):
+    """kv_attention.cpp:145-163."""
+    if position < 0 or position >= cfg.n_max:
+        raise ShapeMismatch("make_v_pieces: position outside cache capacity")
+    if v_open.layout is None or v_open.layout.kind != "interleaved" or v_open.layout.d != cfg.d:
+        raise LayoutMismatch("make_v_pieces: input must be interleaved at the configured width")
+    if v_open.layout.offset != position % cfg.t:
+        raise LayoutMismatch("make_v_pieces: value ct offset does not match the token position")
+    return [fused_extract(be, v_open, "vcache_mask", coeff=v_piece_mask(cfg, e, position))
+            for e in range(cfg.d_head)]
+
+
+def v_append(be, cache: KVCache, parts, cfg):
+    """kv_attention.cpp:165-182."""
+    if cache.n_prime >= cfg.n_max:
+        raise CacheFull("v_append: cache at capacity")
+    dh = cfg.d_head
+    if len(parts) != dh:
+        raise ShapeMismatch(f"v_append: expected d/H pieces, got {len(parts)}")
+    gt = cfg.group_tokens
+    g = cache.n_prime // gt
+    u_local = cache.n_prime - g * gt
+    out = cache.copy()
+    if g == len(out.v_cts):
+        z = be.zeros()
+        out.v_cts.append([z] * v_variant_count(cfg))
+    for e in range(dh):
+        idx = v_variant_index(cfg, v_variant_of(cfg, e, u_local))
+        out.v_cts[g][idx] = be.add(out.v_cts[g][idx], parts[e])
+    return out
+
+
+def _ceil_div(a, b):
+    return (a + b - 1) // b
+
+
+def qk_dot(be, q, cache: KVCache, cfg):
+    """kv_attention.cpp:184-214."""
+    if cache.n_prime == 0:
+        raise CacheEmpty("qk_dot: no cached keys")
+    _require_clean_interleaved(q, cfg, 0, "qk_dot")
+    t, dh, gt = cfg.t, cfg.d_head, cfg.group_tokens
+    if len(cache.k_cts) != _ceil_div(cache.n_prime, t):
+        raise ShapeMismatch("qk_dot: key ct count does not match n_prime")
+    q_rep = replicate_lanes(be, q, t)
+    head_mask = make_mask(make_interleaved(cfg.d, cfg.N, 0, cfg.H), cfg.N, "replicate_extract")
+    maps = [None] * _ceil_div(cache.n_prime, gt)
+    for j, kc in enumerate(cache.k_cts):
+        prod = be.mul(q_rep, kc)
+        prod = fold_within_head(be, prod, dh, t)
+        masked = be.mul_plain(prod, head_mask)
+        local = (j * t) % gt
+        packed = be.rotate(masked, -local) if local else masked
+        m = (j * t) // gt
+        maps[m] = packed if maps[m] is None else be.add(maps[m], packed)
+    return [be.with_layout(m, None) for m in maps]
+
+
+def softmax_times_v(be, probs, cache: KVCache, cfg):
+    """kv_attention.cpp:216-241."""
+    if cache.n_prime == 0:
+        raise CacheEmpty("softmax_times_v: no cached values")
+    t, gt = cfg.t, cfg.group_tokens
+    n_maps = _ceil_div(cache.n_prime, gt)
+    if len(probs) != n_maps:
+        raise ShapeMismatch(f"softmax_times_v: expected {n_maps} probability maps, got {len(probs)}")
+    if len(cache.v_cts) < n_maps:
+        raise ShapeMismatch("softmax_times_v: value cache is missing groups")
+    acc = None
+    for g in range(n_maps):
+        tokens = min(gt, cache.n_prime - g * gt)
+        lo, hi = touched_variants(cfg, tokens)
+        for w in range(lo, hi):
+            scores = be.rotate(probs[g], -w * t) if w else probs[g]
+            prod = be.mul(scores, cache.v_cts[g][v_variant_index(cfg, w)])
+            acc = prod if acc is None else be.add(acc, prod)
+    folded = fold_lanes(be, acc, t)
+    out = be.mul_plain(folded, stride_mask(cfg.N, t, 0))
+    return be.with_layout(out, make_interleaved(cfg.d, cfg.N, 0, cfg.H))
+
+
+def plain_softmax(s):
+    s = np.asarray(s, dtype=np.float64)
+    if len(s) == 0:
+        return s
+    p = np.exp(s - s.max())
+    return p / p.sum()
+
+
+def exact_softmax_maps(be, maps, cfg, n_prime):
+    """kv_attention.cpp:395-412: oracle softmax (zero cost, level preserving)."""
+    gt = cfg.group_tokens
+    if len(maps) != _ceil_div(n_prime, gt):
+        raise ShapeMismatch("exact_softmax_maps: map count does not match n_prime")
+    slots = [be.decrypt(m) for m in maps]
+    out = [np.zeros(cfg.N) for _ in maps]
+    v = np.arange(n_prime)
+    for h in range(cfg.H):
+        sc = np.array([slots[i // gt][h * gt + i % gt] for i in v])
+        p = plain_softmax(sc)
+        for i in v:
+            out[i // gt][h * gt + i % gt] = p[i]
+    return [be.exact_transform(m, (lambda _s, o=o: o)) for m, o in zip(maps, out)]

@@ -1,0 +1,40 @@
+# Recipe: compile the reference's own hot-path sources and tests, unmodified,
+# from where they lie under /root/reference, into oracle/_ref/ (git-ignored,
+# NOT gpurun-ignored). TEST INFRASTRUCTURE: oracle/_ref is the checker and the
+# `--impl reference` CPU arm, never the product.
+#   make -f oracle/ref.mk            -> libslotforge_ref.so + 4 test binaries + golden dumper
+#   make -f oracle/ref.mk check      -> runs the reference's own tests
+REF      ?= /root/reference/proj
+OUT      ?= oracle/_ref
+JSON_INC ?= $(shell python3 -c "import os,sys; p=os.path.join(sys.prefix,'lib','python%d.%d'%sys.version_info[:2],'site-packages','include','cudnn_frontend','thirdparty'); print(p)")
+CXX      ?= g++
+CXXFLAGS ?= -std=c++20 -O2 -fPIC -ffp-contract=off -w
+INC      := -I$(REF)/include -Ioracle/shim -I$(JSON_INC)
+SRCS     := engine layouts vmm kv_attention
+OBJS     := $(SRCS:%=$(OUT)/%.o)
+TESTS    := test_engine test_layouts test_vmm test_kv
+
+all: $(OUT)/libslotforge_ref.so $(TESTS:%=$(OUT)/%) $(OUT)/ref_golden $(OUT)/ref_bench
+
+$(OUT)/%.o: $(REF)/src/%.cpp oracle/shim/Eigen/Dense | $(OUT)
+	$(CXX) $(CXXFLAGS) $(INC) -c $< -o $@
+
+$(OUT)/libslotforge_ref.so: $(OBJS)
+	$(CXX) -shared -o $@ $^
+
+$(OUT)/test_%: $(REF)/tests/test_%.cpp $(OBJS) oracle/shim/doctest.h
+	$(CXX) $(CXXFLAGS) $(INC) $< $(OBJS) -o $@
+
+$(OUT)/ref_golden: oracle/ref_golden.cpp $(OBJS)
+	$(CXX) $(CXXFLAGS) $(INC) $< $(OBJS) -o $@
+
+$(OUT)/ref_bench: oracle/ref_bench.cpp $(OBJS)
+	$(CXX) $(CXXFLAGS) $(INC) $< $(OBJS) -o $@
+
+$(OUT):
+	mkdir -p $(OUT)
+
+check: all
+	@for t in $(TESTS); do echo "== $$t"; ./$(OUT)/$$t || exit 1; done
+
+.PHONY: all check

@@ -1,0 +1,268 @@
+// Golden-vector generator: links the UNMODIFIED reference sources compiled
+// into oracle/_ref (see oracle/ref.mk) and dumps, for a fixed set of seeded
+// cases, the full slot content of every hot-path output together with the
+// reference ledger counts and levels. TEST INFRASTRUCTURE ONLY; the emitted
+// JSON is committed under tests/golden/ by tests/golden/make_golden.sh.
+//
+// Call sites exercised (reference file:line):
+//   vmm_interleaved            proj/src/vmm.cpp:179-236
+//   fused_extract (Rope/Mask)  proj/src/vmm.cpp:85-109
+//   k_append / make_v_pieces / v_append   proj/src/kv_attention.cpp:131-182
+//   qk_dot / softmax_times_v   proj/src/kv_attention.cpp:184-241
+//   exact_softmax_maps         proj/src/kv_attention.cpp:395-412
+#include <nlohmann/json.hpp>
+
+#include <cstdio>
+#include <iostream>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "slotforge/engine.hpp"
+#include "slotforge/kv_attention.hpp"
+#include "slotforge/layouts.hpp"
+#include "slotforge/vmm.hpp"
+
+using nlohmann::json;
+using namespace slotforge;
+
+namespace {
+
+json vec_json(const double* p, long n) {
+  json a = json::array();
+  for (long i = 0; i < n; ++i) a.push_back(p[i]);
+  return a;
+}
+json sv_json(const SlotVector& s) { return vec_json(s.data(), s.size()); }
+json v_json(const Vector& s) { return vec_json(s.data(), s.size()); }
+json m_json(const Matrix& m) { return vec_json(m.data(), m.size()); }
+
+json counts_json(const OpCounts& c) {
+  return json{{"rotations", c.rotations},   {"hoisted_rotations", c.hoisted_rotations},
+              {"ct_pt_mults", c.ct_pt_mults}, {"ct_ct_mults", c.ct_ct_mults},
+              {"additions", c.additions},   {"bootstraps", c.bootstraps}};
+}
+json layout_json(const std::optional<Layout>& ly) {
+  if (!ly) return nullptr;
+  return json{{"kind", to_string(ly->kind)}, {"d", ly->d},         {"t", ly->t},
+              {"offset", ly->offset},       {"heads", ly->heads}, {"deferred_mask", ly->deferred_mask}};
+}
+
+Matrix random_matrix(std::mt19937_64& rng, int r, int c) {
+  std::normal_distribution<double> dist(0.0, 1.0);
+  Matrix m(r, c);
+  for (int i = 0; i < r; ++i)
+    for (int j = 0; j < c; ++j) m(i, j) = dist(rng);
+  return m;
+}
+Vector random_vector(std::mt19937_64& rng, int n) {
+  std::normal_distribution<double> dist(0.0, 1.0);
+  Vector v(n);
+  for (int i = 0; i < n; ++i) v[i] = dist(rng);
+  return v;
+}
+
+json vmm_case(int N, int rows, int cols, int tau_in, int tau_out, bool bsgs, bool mask, unsigned seed) {
+  const int L = 8;
+  std::mt19937_64 rng(seed);
+  Matrix w = random_matrix(rng, rows, cols);
+  Vector x = random_vector(rng, rows);
+  SimBackend be({N, L});
+  const int d_in = padded_dim(rows);
+  Layout lin = make_interleaved(d_in, N, tau_in);
+  SlotVector xs = encode(pad_to(x, d_in), lin, N);
+  Ciphertext cx = be.encrypt(xs, L, lin);
+  Ciphertext cy = vmm_interleaved(be, cx, MatrixWeight(w), {.bsgs = bsgs, .out_offset = tau_out, .mask_output = mask});
+  VmmCost pc = predict_interleaved_cost({N, L}, rows, cols, {.bsgs = bsgs, .out_offset = tau_out, .mask_output = mask});
+  return json{{"kind", "vmm"},
+              {"N", N},
+              {"L", L},
+              {"rows", rows},
+              {"cols", cols},
+              {"tau_in", tau_in},
+              {"tau_out", tau_out},
+              {"bsgs", bsgs},
+              {"mask_output", mask},
+              {"W", m_json(w)},
+              {"x", v_json(x)},
+              {"x_slots", sv_json(xs)},
+              {"y_slots", sv_json(cy.slots)},
+              {"y", v_json(decode(cy.slots, *cy.layout))},
+              {"layout", layout_json(cy.layout)},
+              {"level", cy.level},
+              {"counts", counts_json(be.ledger().totals())},
+              {"predicted", json{{"rotations", pc.rotations}, {"ct_pt_mults", pc.ct_pt_mults}, {"depth", pc.depth}}}};
+}
+
+json rope_case(int N, int d, int d_head, int offset, long long pos, unsigned seed) {
+  const int L = 6;
+  std::mt19937_64 rng(seed);
+  Vector x = random_vector(rng, d);
+  SimBackend be({N, L});
+  Layout ly = make_interleaved(d, N, offset);
+  ly.deferred_mask = true;
+  SlotVector raw = encode(x, ly, N);
+  for (int i = 0; i < N; ++i)
+    if (i % ly.t != offset) raw[i] = 99.0 + i;  // garbage a vmm would leave
+  Ciphertext cx = be.encrypt(raw, L, ly);
+  RoPEParams p{10000.0, pos, d_head, ly.t};
+  auto pts = rope_plaintexts(p, ly, N);
+  Ciphertext cy = fused_extract(be, cx, Successor::Rope, &p);
+  return json{{"kind", "rope"},   {"N", N},           {"L", L},
+              {"d", d},           {"d_head", d_head}, {"offset", offset},
+              {"pos", pos},       {"x_slots", sv_json(raw)},
+              {"p0", sv_json(pts[0])}, {"p1", sv_json(pts[1])}, {"p2", sv_json(pts[2])},
+              {"y_slots", sv_json(cy.slots)}, {"level", cy.level},
+              {"layout", layout_json(cy.layout)}, {"counts", counts_json(be.ledger().totals())}};
+}
+
+// Decode-time attention over a cache built by the append protocol: every token
+// goes through make_v_pieces / v_append / k_append (garbage-carrying V input,
+// as in attn-bench, slotforge_cli.cpp:189-198), then one query runs qk_dot,
+// exact softmax and softmax_times_v.
+json attn_case(int N, int d, int H, int np, unsigned seed) {
+  const int L = 12;
+  AttentionConfig cfg{N, d, H, 0, np};
+  SimBackend be({N, L});
+  validate_attention_config(cfg, N);
+  const int t = cfg.t();
+  std::mt19937_64 rng(seed);
+  Matrix K = random_matrix(rng, np, d), V = random_matrix(rng, np, d);
+  Vector q = random_vector(rng, d);
+  KVCache cache;
+  json appends = json::array();
+  for (int u = 0; u < np; ++u) {
+    Layout vly = make_interleaved(d, N, u % t, H);
+    vly.deferred_mask = true;
+    SlotVector open = SlotVector::Constant(N, 7.5);
+    for (int E = 0; E < d; ++E) open[E * t + u % t] = V(u, E);
+    Ciphertext v_open = be.encrypt(open, L - 1, vly);
+    OpCounts c0 = be.ledger().totals();
+    auto parts = make_v_pieces(be, v_open, cfg, u);
+    cache = v_append(be, cache, parts, cfg);
+    Layout kly = make_interleaved(d, N, u % t, H);
+    Vector krow(d);
+    for (int E = 0; E < d; ++E) krow[E] = K(u, E);
+    cache = k_append(be, cache, be.encrypt(encode(krow, kly, N), L - 2, kly), cfg);
+    OpCounts c1 = be.ledger().totals();
+    OpCounts delta;
+    delta.rotations = c1.rotations - c0.rotations;
+    delta.ct_pt_mults = c1.ct_pt_mults - c0.ct_pt_mults;
+    delta.ct_ct_mults = c1.ct_ct_mults - c0.ct_ct_mults;
+    delta.additions = c1.additions - c0.additions;
+    appends.push_back(counts_json(delta));
+  }
+  json k_cts = json::array();
+  for (const auto& c : cache.k_cts) k_cts.push_back(json{{"slots", sv_json(c.slots)}, {"level", c.level}});
+  json v_cts = json::array();
+  for (const auto& grp : cache.v_cts) {
+    json g = json::array();
+    for (const auto& c : grp) g.push_back(json{{"slots", sv_json(c.slots)}, {"level", c.level}});
+    v_cts.push_back(g);
+  }
+  be.ledger().reset();
+  Layout qly = make_interleaved(d, N, 0, H);
+  Ciphertext qc = be.encrypt(encode(q, qly, N), L - 2, qly);
+  std::vector<Ciphertext> maps;
+  {
+    auto ph = be.phase("QK^T");
+    maps = qk_dot(be, qc, cache, cfg);
+  }
+  auto probs = exact_softmax_maps(be, maps, cfg, cache.n_prime);
+  Ciphertext out;
+  {
+    auto ph = be.phase("Score*V");
+    out = softmax_times_v(be, probs, cache, cfg);
+  }
+  json jm = json::array(), jp = json::array();
+  for (auto& m : maps) jm.push_back(sv_json(m.slots));
+  for (auto& p : probs) jp.push_back(sv_json(p.slots));
+  return json{{"kind", "attn"},
+              {"N", N},
+              {"L", L},
+              {"d", d},
+              {"H", H},
+              {"n_prime", np},
+              {"K", m_json(K)},
+              {"V", m_json(V)},
+              {"q", v_json(q)},
+              {"append_counts", appends},
+              {"k_cts", k_cts},
+              {"v_cts", v_cts},
+              {"maps", jm},
+              {"map_level", maps.front().level},
+              {"probs", jp},
+              {"out_slots", sv_json(out.slots)},
+              {"out", v_json(decode(out.slots, *out.layout))},
+              {"out_level", out.level},
+              {"out_layout", layout_json(out.layout)},
+              {"qk_counts", counts_json(be.ledger().phase_totals("QK^T"))},
+              {"sv_counts", counts_json(be.ledger().phase_totals("Score*V"))}};
+}
+
+json engine_case() {
+  SimBackend be({4, 3});
+  SlotVector a(4);
+  a << 1, 2, 3, 4;
+  auto ct = be.encrypt(a, 3);
+  json rots = json::array();
+  for (int r : {1, -1, 0, 4, 5, 3}) rots.push_back(json{{"r", r}, {"slots", sv_json(be.rotate(ct, r).slots)}});
+  return json{{"kind", "engine_rotate"}, {"N", 4}, {"input", sv_json(a)}, {"rotations", rots},
+              {"counted", be.ledger().totals().rotations}};
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  const std::string which = argc > 1 ? argv[1] : "small";
+  json cases = json::array();
+  unsigned seed = 1000;
+  if (which == "small") {
+    cases.push_back(engine_case());
+    for (int N : {8, 64, 256}) {
+      std::vector<std::pair<int, int>> shapes;
+      for (int d : {2, 8, 32})
+        if (d <= N) shapes.emplace_back(d, d);
+      for (int d : {2, 8})
+        for (int a : {2, 4})
+          if (d * a <= N) {
+            shapes.emplace_back(d, d * a);
+            shapes.emplace_back(d * a, d);
+          }
+      if (N <= 64) shapes.emplace_back(N, N);
+      shapes.emplace_back(3, 5);
+      for (auto [r, c] : shapes) {
+        const int t_in = N / padded_dim(r), t_out = N / padded_dim(c);
+        for (bool bsgs : {false, true})
+          for (int ti : {0, t_in - 1})
+            for (int to : {0, t_out - 1}) {
+              if (ti == t_in - 1 && to == t_out - 1 && t_in > 1 && !bsgs) continue;
+              cases.push_back(vmm_case(N, r, c, ti, to, bsgs, (seed % 3) == 0, seed));
+              ++seed;
+            }
+      }
+    }
+    for (int off : {0, 2}) cases.push_back(rope_case(32, 8, 4, off, 7, seed++));
+    cases.push_back(rope_case(64, 16, 8, 3, 123, seed++));
+    for (int d : {4, 16})
+      for (int H : {1, 2, 4})
+        for (int np : {1, 5, 13}) cases.push_back(attn_case(64, d, H, np, seed++));
+    cases.push_back(attn_case(256, 64, 4, 21, seed++));
+    cases.push_back(vmm_case(256, 256, 256, 0, 0, true, false, seed++));  // t = 1 edge
+  } else if (which == "medium") {
+    // N = 2048 slots (ring degree 4096): the GPU parity size
+    cases.push_back(vmm_case(2048, 64, 64, 0, 0, true, false, 7001));
+    cases.push_back(vmm_case(2048, 64, 256, 5, 3, true, false, 7002));
+    cases.push_back(vmm_case(2048, 256, 64, 0, 7, true, true, 7003));
+    cases.push_back(vmm_case(2048, 100, 60, 3, 1, false, false, 7004));
+    cases.push_back(rope_case(2048, 128, 32, 5, 77, 7005));
+    cases.push_back(attn_case(2048, 128, 4, 40, 7006));
+    cases.push_back(attn_case(2048, 64, 1, 70, 7007));
+  }
+  std::cout << json{{"generator", "oracle/ref_golden.cpp over /root/reference/proj/src (unmodified)"},
+                    {"set", which},
+                    {"cases", cases}}
+                   .dump()
+            << "\n";
+  return 0;
+}
