@@ -1,0 +1,351 @@
+"""ctypes wrapper around oracle/ckks_oracle.cpp (the CPU RNS-CKKS oracle) plus a
+slotforge-shaped backend over it. TEST INFRASTRUCTURE ONLY.
+
+The backend enforces the reference's level rules and ledger accounting
+(engine.hpp:102-111, engine.cpp:143-214) exactly like oracle/slot_sim.py, but
+the arithmetic is real CKKS, so (a) its decrypted outputs are compared with the
+reference's golden slot vectors at CKKS precision and (b) its ciphertext words
+are the bit-exact expectation for the GPU product.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from .errors import DomainViolation, Error, InvalidTarget, LevelUnderflow, ShapeMismatch
+from .layout import Layout, is_pow2, validate_layout
+from .slot_sim import CostLedger
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_bin", "libsf_oracle.so")
+
+_lib = None
+U64P = C.POINTER(C.c_uint64)
+DP = C.POINTER(C.c_double)
+
+
+def build():
+    subprocess.run(["make", "-s", "-f", os.path.join("oracle", "oracle.mk")], cwd=os.path.dirname(HERE),
+                   check=True)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            build()
+        L = C.CDLL(LIB_PATH)
+        vp = C.c_void_p
+        sig = {
+            "ock_last_error": (C.c_char_p, []),
+            "ock_context_new": (vp, [C.c_int] * 7 + [C.c_uint64]),
+            "ock_context_free": (None, [vp]),
+            "ock_num_primes": (C.c_int, [vp]),
+            "ock_primes": (None, [vp, U64P]),
+            "ock_secret_key": (None, [vp, U64P]),
+            "ock_key": (None, [vp, C.c_uint64, U64P]),
+            "ock_galois_elt": (C.c_uint64, [vp, C.c_int]),
+            "ock_ntt": (None, [vp, C.c_int, U64P, C.c_int]),
+            "ock_automorph": (None, [vp, U64P, U64P, C.c_uint64]),
+            "ock_encode": (C.c_int, [vp, DP, C.c_double, C.c_int, U64P]),
+            "ock_encode_coeffs": (C.c_int, [vp, DP, C.c_double, C.POINTER(C.c_int64)]),
+            "ock_encrypt": (vp, [vp, DP, C.c_int, C.c_double, C.c_uint64]),
+            "ock_zero": (vp, [vp, C.c_int]),
+            "ock_import": (vp, [vp, U64P, C.c_int, C.c_double, C.c_int]),
+            "ock_ct_free": (None, [vp]),
+            "ock_ct_info": (None, [vp, C.POINTER(C.c_int), DP, C.POINTER(C.c_int)]),
+            "ock_ct_data": (None, [vp, U64P]),
+            "ock_decrypt": (None, [vp, vp, DP]),
+            "ock_add": (vp, [vp, vp, vp]),
+            "ock_sub": (vp, [vp, vp, vp]),
+            "ock_add_plain": (vp, [vp, vp, DP]),
+            "ock_mac_plain": (vp, [vp, C.POINTER(vp), DP, C.c_int]),
+            "ock_mul": (vp, [vp, vp, vp]),
+            "ock_rotate": (vp, [vp, vp, C.c_int]),
+            "ock_rescale": (vp, [vp, vp]),
+            "ock_level_drop": (vp, [vp, vp, C.c_int]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype, f.argtypes = res, args
+        _lib = L
+    return _lib
+
+
+def _u64(a: np.ndarray):
+    return a.ctypes.data_as(U64P)
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(DP)
+
+
+def fmix(z: int) -> int:
+    M = (1 << 64) - 1
+    z ^= z >> 30
+    z = (z * 0xBF58476D1CE4E5B9) & M
+    z ^= z >> 27
+    z = (z * 0x94D049BB133111EB) & M
+    z ^= z >> 31
+    return z
+
+
+def auto_seed(key_seed: int, k: int) -> int:
+    """seed of the k-th encryption a context makes without an
+    explicit seed (client-side re-encryptions inside exact_transform/bootstrap)."""
+    return fmix(key_seed ^ ((0xE1C0000000000000 + k) & ((1 << 64) - 1)))
+
+
+def _raise(msg: str):
+    for cls in (LevelUnderflow, InvalidTarget, ShapeMismatch, DomainViolation):
+        if msg.startswith(cls.__name__):
+            raise cls(msg)
+    raise Error(msg)
+
+
+class OCt:
+    """Oracle ciphertext: C handle + level + layout tag."""
+
+    def __init__(self, ctx, ptr, level: int, layout: Optional[Layout]):
+        if not ptr:
+            _raise(lib().ock_last_error().decode())
+        self.ctx, self.ptr, self.level, self.layout = ctx, ptr, level, layout
+
+    def __del__(self):
+        if self.ptr and lib is not None and _lib is not None:
+            _lib.ock_ct_free(self.ptr)
+            self.ptr = None
+
+    def info(self):
+        limbs, scale, zero = C.c_int(), C.c_double(), C.c_int()
+        lib().ock_ct_info(self.ptr, C.byref(limbs), C.byref(scale), C.byref(zero))
+        return limbs.value, scale.value, bool(zero.value)
+
+    @property
+    def scale(self):
+        return self.info()[1]
+
+    @property
+    def is_zero(self):
+        return self.info()[2]
+
+    def data(self) -> np.ndarray:
+        limbs, _, _ = self.info()
+        out = np.empty(2 * limbs * self.ctx.n, dtype=np.uint64)
+        lib().ock_ct_data(self.ptr, _u64(out))
+        return out.reshape(2, limbs, self.ctx.n)
+
+
+@dataclass
+class CkksParams:
+    """DESIGN.md §3.1. slots = the reference engine's N (power of two <= n/2)."""
+    slots: int
+    L: int
+    log_n: Optional[int] = None
+    alpha: Optional[int] = None
+    q0_bits: int = 60
+    scale_bits: int = 40
+    special_bits: int = 60
+    seed: int = 1
+
+    def resolved(self):
+        log_n = self.log_n if self.log_n is not None else max(2, (2 * self.slots).bit_length() - 1)
+        alpha = self.alpha if self.alpha is not None else min(self.L + 1, 5)
+        return log_n, alpha
+
+
+class CkksOracle:
+    """slotforge-shaped backend over the CPU CKKS oracle."""
+
+    def __init__(self, N: int, L: int, **kw):
+        if not is_pow2(N):
+            raise ShapeMismatch("engine: N must be a power of two")
+        if L < 1:
+            raise InvalidTarget("engine: level budget L must be >= 1")
+        self.params = CkksParams(N, L, **kw)
+        self.log_n, self.alpha = self.params.resolved()
+        self.n = 1 << self.log_n
+        if 2 * N > self.n:
+            raise ShapeMismatch("ckks: slot count exceeds ring degree / 2")
+        self.N, self.L = N, L
+        p = self.params
+        self.ptr = lib().ock_context_new(self.log_n, N, L, p.q0_bits, p.scale_bits, self.alpha, p.special_bits,
+                                         p.seed)
+        if not self.ptr:
+            _raise(lib().ock_last_error().decode())
+        self.delta = float(2 ** p.scale_bits)
+        self.ledger = CostLedger()
+        self.enc_counter = 0
+        np_ = lib().ock_num_primes(self.ptr)
+        self.primes = np.empty(np_, dtype=np.uint64)
+        lib().ock_primes(self.ptr, _u64(self.primes))
+
+    def __del__(self):
+        if getattr(self, "ptr", None) and _lib is not None:
+            _lib.ock_context_free(self.ptr)
+            self.ptr = None
+
+    def phase(self, name):
+        return self.ledger.phase(name)
+
+    # --- helpers
+    def _slots(self, s, what):
+        s = np.ascontiguousarray(np.broadcast_to(np.asarray(s, dtype=np.float64), (self.N,)))
+        return s
+
+    def _check(self, c: OCt, what):
+        if c.level < 0 or c.level > self.L:
+            raise InvalidTarget(f"{what}: ciphertext level {c.level} out of [0, L]")
+
+    def next_seed(self):
+        s = auto_seed(self.params.seed, self.enc_counter)
+        self.enc_counter += 1
+        return s
+
+    def _merge(self, a, b):
+        return a.layout if (a.layout is not None and a.layout == b.layout) else None
+
+    # --- client ops (off-ledger)
+    def encrypt(self, slots, level: int = -1, layout: Optional[Layout] = None, seed: Optional[int] = None,
+                scale: Optional[float] = None) -> OCt:
+        if level < 0:
+            level = self.L
+        slots = np.asarray(slots, dtype=np.float64)
+        if len(slots) != self.N:
+            raise ShapeMismatch(f"encrypt: expected {self.N} slots, got {len(slots)}")
+        if level > self.L:
+            raise InvalidTarget("encrypt: level exceeds budget L")
+        if layout is not None:
+            validate_layout(layout, self.N)
+        seed = self.next_seed() if seed is None else seed
+        s = np.ascontiguousarray(slots)
+        ptr = lib().ock_encrypt(self.ptr, _dp(s), level + 1, scale or self.delta, seed)
+        return OCt(self, ptr, level, layout)
+
+    def zeros(self, level: int = -1) -> OCt:
+        if level < 0:
+            level = self.L
+        return OCt(self, lib().ock_zero(self.ptr, level + 1), level, None)
+
+    def decrypt(self, c: OCt) -> np.ndarray:
+        out = np.empty(self.N)
+        lib().ock_decrypt(self.ptr, c.ptr, _dp(out))
+        return out
+
+    def import_ct(self, data: np.ndarray, level: int, scale: float, layout=None, zero=False) -> OCt:
+        d = np.ascontiguousarray(data, dtype=np.uint64)
+        return OCt(self, lib().ock_import(self.ptr, _u64(d), level + 1, scale, int(zero)), level, layout)
+
+    # --- evaluator ops (ledger-charged)
+    def add(self, a, b):
+        self._check(a, "add"), self._check(b, "add")
+        self.ledger.count_add()
+        return OCt(self, lib().ock_add(self.ptr, a.ptr, b.ptr), min(a.level, b.level), self._merge(a, b))
+
+    def sub(self, a, b):
+        self._check(a, "sub"), self._check(b, "sub")
+        self.ledger.count_add()
+        return OCt(self, lib().ock_sub(self.ptr, a.ptr, b.ptr), min(a.level, b.level), self._merge(a, b))
+
+    def add_plain(self, a, p):
+        self._check(a, "add_plain")
+        p = self._slots(p, "add_plain")
+        self.ledger.count_add()
+        return OCt(self, lib().ock_add_plain(self.ptr, a.ptr, _dp(p)), a.level, a.layout)
+
+    def mul(self, a, b):
+        self._check(a, "mul"), self._check(b, "mul")
+        lvl = min(a.level, b.level)
+        if lvl <= 0:
+            raise LevelUnderflow("mul: no multiplicative level left")
+        self.ledger.count_ct_ct()
+        return OCt(self, lib().ock_mul(self.ptr, a.ptr, b.ptr), lvl - 1, self._merge(a, b))
+
+    def mul_plain(self, a, p):
+        return self.mac_plain([(a, p)], _layout=a.layout)
+
+    def mac_plain(self, terms, _layout="__first__"):
+        """sum_k ct_k * p_k with one rescale (fused MAC); charged as k ct-pt
+        mults and k-1 additions like the reference's mul_plain/add chain."""
+        for c, _ in terms:
+            self._check(c, "mul_plain")
+            if c.level <= 0:
+                raise LevelUnderflow("mul_plain: no multiplicative level left")
+        for i, _ in enumerate(terms):
+            self.ledger.count_ct_pt()
+            if i:
+                self.ledger.count_add()
+        lvl = min(c.level for c, _ in terms)
+        pts = np.ascontiguousarray(np.stack([self._slots(p, "mul_plain") for _, p in terms]))
+        arr = (C.c_void_p * len(terms))(*[c.ptr for c, _ in terms])
+        layout = terms[0][0].layout if _layout == "__first__" else _layout
+        if _layout == "__first__":
+            for c, _ in terms[1:]:
+                if c.layout != layout:
+                    layout = None
+        return OCt(self, lib().ock_mac_plain(self.ptr, arr, _dp(pts), len(terms)), lvl - 1, layout)
+
+    def rotate(self, a, r: int, hoisted: bool = False):
+        self._check(a, "rotate")
+        if r % self.N == 0:
+            return a
+        self.ledger.count_rotation(hoisted)
+        return OCt(self, lib().ock_rotate(self.ptr, a.ptr, int(r)), a.level, None)
+
+    def level_drop(self, a, target: int):
+        self._check(a, "level_drop")
+        if target < 0 or target > a.level:
+            raise InvalidTarget(f"level_drop: target level {target} outside [0, level]")
+        return OCt(self, lib().ock_level_drop(self.ptr, a.ptr, target + 1), target, a.layout)
+
+    def bootstrap(self, a, target: int):
+        """Oracle hook (client round trip): decrypt, re-encrypt at target."""
+        self._check(a, "bootstrap")
+        if target < 1 or target > self.L:
+            raise InvalidTarget(f"bootstrap: target level {target} outside [1, L]")
+        self.ledger.count_bootstrap()
+        return self._reenc(self.decrypt(a), target, a.layout)
+
+    def exact_transform(self, a, f):
+        """Oracle hook: decrypt -> f -> re-encrypt at the same level (free)."""
+        self._check(a, "exact_transform")
+        out = np.asarray(f(self.decrypt(a)), dtype=np.float64)
+        if len(out) != self.N:
+            raise ShapeMismatch("exact_transform result: wrong slot count")
+        return self._reenc(out, a.level, a.layout)
+
+    def _reenc(self, slots, level, layout):
+        ct = self.encrypt(slots, level, None)
+        ct.layout = layout
+        return ct
+
+    def with_layout(self, c, layout):
+        return OCt._alias(c, layout)
+
+
+def _alias(c: OCt, layout):
+    """Same C ciphertext, new layout tag (ciphertexts are immutable values)."""
+    n = OCt.__new__(OCt)
+    n.ctx, n.level, n.layout = c.ctx, c.level, layout
+    n._owner = c  # keep the C handle alive
+    n.ptr = c.ptr
+    n.__dict__["_alias"] = True
+    return n
+
+
+OCt._alias = staticmethod(_alias)
+_orig_del = OCt.__del__
+
+
+def _del(self):
+    if self.__dict__.get("_alias"):
+        return
+    _orig_del(self)
+
+
+OCt.__del__ = _del
