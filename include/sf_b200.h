@@ -1,0 +1,201 @@
+/* sf_b200.h — C ABI of the B200-native encrypted-decode hot path.
+ *
+ * Drop-in boundary for the reference's `slotforge` C++ API
+ * (/root/reference/proj/include/slotforge/*.hpp). Plain pointers, sizes and
+ * opaque handles only; no C++ or torch types. Every entry point returns an
+ * sf_status (0 = OK); on failure sf_last_error() holds the message and the code
+ * maps 1:1 onto the reference exception types (types.hpp:16-46), so a C++ or
+ * Python host layer can rethrow the same types the reference tests expect.
+ *
+ * Ciphertexts are immutable, reference-counted device values (engine.hpp:102-104:
+ * "Operations return fresh ciphertext values"); an op never mutates its inputs.
+ * All work is enqueued on the context's CUDA stream; only decrypt / export /
+ * sf_synchronize block the host.
+ *
+ * Reference interface each entry point replaces is cited per declaration.
+ */
+#ifndef SF_B200_H
+#define SF_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* --- status codes: 1:1 with slotforge exception types (types.hpp:16-46) --- */
+typedef int sf_status;
+#define SF_OK 0
+#define SF_ERR_LEVEL_UNDERFLOW 1 /* slotforge::LevelUnderflow */
+#define SF_ERR_INVALID_TARGET 2  /* slotforge::InvalidTarget  */
+#define SF_ERR_SHAPE_MISMATCH 3  /* slotforge::ShapeMismatch  */
+#define SF_ERR_LAYOUT_MISMATCH 4 /* slotforge::LayoutMismatch */
+#define SF_ERR_CACHE_FULL 5      /* slotforge::CacheFull      */
+#define SF_ERR_CACHE_EMPTY 6     /* slotforge::CacheEmpty     */
+#define SF_ERR_DOMAIN 7          /* slotforge::DomainViolation */
+#define SF_ERR_SCALE_MISMATCH 8  /* CKKS: adding ciphertexts at different scales (slotforge::Error) */
+#define SF_ERR_CUDA 9            /* device failure (slotforge::Error) */
+#define SF_ERR_INTERNAL 10       /* anything else (slotforge::Error) */
+
+typedef struct sf_context sf_context;
+typedef struct sf_ct sf_ct;
+typedef struct sf_vmm_plan sf_vmm_plan;
+typedef struct sf_kvcache sf_kvcache;
+
+/* layouts.hpp:22-33 (Layout). kind: 0 contiguous, 1 replicated, 2 interleaved.
+ * valid = 0 means "no layout tag" (std::optional<Layout> empty). */
+typedef struct {
+  int valid;
+  int kind;
+  int d;
+  int t;
+  int offset;
+  int heads;
+  int deferred_mask;
+} sf_layout;
+
+/* engine.hpp:19-22 (EngineParams{N, L}) extended with the CKKS parameters the
+ * reference leaves "unhoused by design". slots = the reference N.
+ * log_n = ring degree exponent (0: 2*slots). alpha = special primes per digit
+ * (0: min(L+1, 5)). Bits of q0 / scale primes / special primes (0: 60/40/60). */
+typedef struct {
+  int slots;
+  int L;
+  int log_n;
+  int alpha;
+  int q0_bits;
+  int scale_bits;
+  int special_bits;
+  int device;
+  uint64_t seed; /* secret-key / evaluation-key seed */
+} sf_params;
+
+/* engine.hpp:30-49 (OpCounts) */
+typedef struct {
+  long long rotations;
+  long long hoisted_rotations;
+  long long ct_pt_mults;
+  long long ct_ct_mults;
+  long long additions;
+  long long bootstraps;
+} sf_op_counts;
+
+/* --- errors ---------------------------------------------------------------- */
+const char* sf_last_error(void);
+
+/* --- context: Backend::Backend(EngineParams) (engine.cpp:92-95) + keygen ----- */
+sf_status sf_context_create(const sf_params* params, sf_context** out);
+void sf_context_destroy(sf_context* ctx);
+/* ring degree, slots, L, alpha, number of primes (q0..qL, p0..p_{alpha-1});
+ * primes may be NULL, else receives num_primes words. */
+sf_status sf_context_info(const sf_context* ctx, int* n, int* slots, int* L, int* alpha, int* num_primes,
+                          uint64_t* primes);
+sf_status sf_synchronize(sf_context* ctx);
+/* Galois keys are generated lazily on first use; this pre-generates a set. */
+sf_status sf_gen_rotation_keys(sf_context* ctx, const int* rotations, int count);
+/* secret key (NTT domain, all primes: num_primes*n words) and one switching
+ * key (galois element g, 0 = relinearisation; beta*2*num_primes*n words):
+ * exported for bit-exact parity tests only. */
+sf_status sf_secret_key_export(sf_context* ctx, uint64_t* out);
+sf_status sf_switching_key_export(sf_context* ctx, uint64_t galois_elt, uint64_t* out);
+uint64_t sf_galois_elt(const sf_context* ctx, int rotation);
+
+/* --- ciphertext handles ---------------------------------------------------- */
+sf_ct* sf_ct_retain(sf_ct* ct);
+void sf_ct_release(sf_ct* ct);
+/* Ciphertext{slots, level, layout} (engine.hpp:24-28) + CKKS scale. */
+sf_status sf_ct_info(const sf_ct* ct, int* level, double* scale, int* is_zero, sf_layout* layout);
+/* same value, new layout tag (the reference assigns `ct.layout = ...`) */
+sf_status sf_ct_with_layout(sf_context* ctx, const sf_ct* ct, const sf_layout* layout, sf_ct** out);
+/* raw RNS words, limb-major [2][level+1][n] (NTT domain) */
+sf_status sf_ct_export(sf_context* ctx, const sf_ct* ct, uint64_t* out);
+sf_status sf_ct_import(sf_context* ctx, const uint64_t* words, int level, double scale, int is_zero,
+                       const sf_layout* layout, sf_ct** out);
+
+/* --- client side, off-ledger: Backend::encrypt / zeros (engine.cpp:109-123),
+ *     encode/decode (layouts.cpp:66-104 composed with CKKS encoding) -------- */
+/* level < 0: L. use_seed = 0: seed from the context's encryption counter. */
+sf_status sf_encrypt(sf_context* ctx, const double* slots, int level, const sf_layout* layout, uint64_t seed,
+                     int use_seed, sf_ct** out);
+sf_status sf_zeros(sf_context* ctx, int level, sf_ct** out);
+sf_status sf_decrypt(sf_context* ctx, const sf_ct* ct, double* slots_out);
+/* CKKS encode of `slots` at `scale` into `limbs` RNS limbs, NTT domain. */
+sf_status sf_encode(sf_context* ctx, const double* slots, double scale, int limbs, uint64_t* out);
+
+/* --- evaluator: virtual ops of slotforge::Backend (engine.hpp:112-149) ------ */
+sf_status sf_add(sf_context* ctx, const sf_ct* a, const sf_ct* b, sf_ct** out);       /* engine.cpp:143 */
+sf_status sf_sub(sf_context* ctx, const sf_ct* a, const sf_ct* b, sf_ct** out);       /* engine.cpp:150 */
+sf_status sf_add_plain(sf_context* ctx, const sf_ct* a, const double* slots, sf_ct** out); /* :157 */
+sf_status sf_mul(sf_context* ctx, const sf_ct* a, const sf_ct* b, sf_ct** out);       /* engine.cpp:164 */
+sf_status sf_mul_plain(sf_context* ctx, const sf_ct* a, const double* slots, sf_ct** out); /* :173 */
+/* sum_k cts[k] * slots[k*N..] with one rescale; charged as k ct-pt mults and
+ * k-1 additions (the reference's mul_plain/add chain, vmm.cpp:214-219). */
+sf_status sf_mac_plain(sf_context* ctx, const sf_ct* const* cts, const double* slots, int k, sf_ct** out);
+sf_status sf_rotate(sf_context* ctx, const sf_ct* a, int r, int hoisted, sf_ct** out); /* :181 */
+/* k rotations of one ciphertext sharing one ModUp (RotationHint{hoisted}). */
+sf_status sf_rotate_hoisted(sf_context* ctx, const sf_ct* a, const int* r, int k, sf_ct** outs);
+sf_status sf_level_drop(sf_context* ctx, const sf_ct* a, int target, sf_ct** out); /* engine.cpp:201 */
+/* oracle hook (engine.cpp:193): client round trip decrypt -> encrypt at target */
+sf_status sf_bootstrap(sf_context* ctx, const sf_ct* a, int target, sf_ct** out);
+
+/* --- ledger: CostLedger (engine.hpp:54-96) -------------------------------- */
+sf_status sf_ledger_totals(const sf_context* ctx, sf_op_counts* out);
+sf_status sf_ledger_phase_totals(const sf_context* ctx, const char* phase, sf_op_counts* out);
+sf_status sf_ledger_reset(sf_context* ctx);
+sf_status sf_phase_push(sf_context* ctx, const char* phase);
+sf_status sf_phase_pop(sf_context* ctx);
+
+/* --- packed HE-VMM: vmm_interleaved (vmm.hpp:74-75, vmm.cpp:179-236) ------
+ * A plan holds the k interleaved diagonals (vmm.cpp:159-175) pre-encoded on
+ * the device at `level` (offline, not charged). W is row-major
+ * rows x cols with y = x^T W; W == NULL selects the reference bench weight
+ * sin(0.001*(31 r + c) + 0.25) (slotforge_cli.cpp:88-92). */
+sf_status sf_vmm_plan_create(sf_context* ctx, const double* W, int rows, int cols, int level, int in_offset,
+                             int out_offset, int bsgs, sf_vmm_plan** out);
+void sf_vmm_plan_destroy(sf_vmm_plan* plan);
+/* predict_interleaved_cost (vmm.cpp:473-488) */
+sf_status sf_vmm_predict(const sf_context* ctx, int rows, int cols, int bsgs, int mask_output,
+                         long long* rotations, long long* ct_pt_mults, int* depth);
+sf_status sf_vmm_interleaved(sf_context* ctx, const sf_ct* x, const sf_vmm_plan* plan, int mask_output,
+                             sf_ct** out);
+
+/* --- KV-cache attention (kv_attention.hpp:32-109) --------------------------- */
+/* AttentionConfig{N = slots, d, H, n0, n_max}; validate_attention_config */
+sf_status sf_kv_create(sf_context* ctx, int d, int H, int n0, int n_max, sf_kvcache** out);
+sf_kvcache* sf_kv_retain(sf_kvcache* kv);
+void sf_kv_release(sf_kvcache* kv);
+/* n_prime, #k cts, #groups, variants per group */
+sf_status sf_kv_info(const sf_kvcache* kv, int* n_prime, int* n_k, int* n_groups, int* n_variants);
+/* which = 0: K ct idx; which = 1: V handle (group g, variant index idx) */
+sf_status sf_kv_get(const sf_kvcache* kv, int which, int g, int idx, sf_ct** out);
+/* build a cache directly from ciphertexts (the reference tests' direct_cache):
+ * k_cts[n_k], v_cts[n_groups * variants] */
+sf_status sf_kv_from_cts(sf_context* ctx, int d, int H, int n0, int n_max, int n_prime, const sf_ct* const* k_cts,
+                         int n_k, const sf_ct* const* v_cts, int n_groups, sf_kvcache** out);
+/* rope_apply (kv_attention.cpp:111-117 -> fused_extract Rope, vmm.cpp:85-100) */
+sf_status sf_rope_apply(sf_context* ctx, const sf_ct* x, int d, int H, long long position, double base,
+                        sf_ct** out);
+/* fused_extract with a mask successor (vmm.cpp:102-108); coeff may be NULL */
+sf_status sf_fused_extract_mask(sf_context* ctx, const sf_ct* x, const double* coeff, sf_ct** out);
+sf_status sf_k_append(sf_context* ctx, const sf_kvcache* cache, const sf_ct* k_new, sf_kvcache** out);
+/* parts_out receives d/H handles */
+sf_status sf_make_v_pieces(sf_context* ctx, const sf_kvcache* cache, const sf_ct* v_open, int position,
+                           sf_ct** parts_out);
+sf_status sf_v_append(sf_context* ctx, const sf_kvcache* cache, const sf_ct* const* parts, int n_parts,
+                      sf_kvcache** out);
+/* maps_out must hold ceil(n_prime / (N/H)) handles */
+sf_status sf_qk_dot(sf_context* ctx, const sf_ct* q, const sf_kvcache* cache, sf_ct** maps_out, int* n_maps);
+sf_status sf_softmax_times_v(sf_context* ctx, const sf_ct* const* probs, int n_probs, const sf_kvcache* cache,
+                             sf_ct** out);
+
+/* --- device timing of the last enqueued work (CUDA events on the ctx stream) */
+sf_status sf_event_record(sf_context* ctx, int slot);
+sf_status sf_event_elapsed_ms(sf_context* ctx, int slot_begin, int slot_end, float* ms);
+/* number of kernels this context has launched since creation */
+long long sf_kernel_launches(const sf_context* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SF_B200_H */

@@ -1,0 +1,562 @@
+"""B200-native encrypted-decode hot path (arXiv 2602.11470, "Cachemir").
+
+Python mirror of the reference's `slotforge` C++ API
+(/root/reference/proj/include/slotforge/*.hpp) over the C ABI in
+include/sf_b200.h. Names, argument meaning and error types follow the
+reference so code written against slotforge reads the same:
+
+    be = Backend(N=32768, L=13)                 # EngineParams{N, L}  (engine.hpp:19-22)
+    x  = be.encrypt(slots, level, layout)       # Backend::encrypt    (engine.cpp:109-121)
+    y  = vmm_interleaved(be, x, W, bsgs=True)   # vmm.hpp:74-75
+    cache = k_append(be, cache, k_new)          # kv_attention.hpp:79-109 ...
+
+Every operation runs on the GPU through libsf_b200.so (sm_100a kernels); the
+package has no CPU fallback and fails loudly if the library is missing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, replace
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _native
+from ._native import SfLayout, SfOpCounts, SfParams
+
+__all__ = [
+    "Error", "LevelUnderflow", "InvalidTarget", "ShapeMismatch", "LayoutMismatch", "CacheFull", "CacheEmpty",
+    "DomainViolation", "ScaleMismatch", "Layout", "make_interleaved", "OpCounts", "Backend", "Ciphertext",
+    "VmmPlan", "vmm_interleaved", "predict_interleaved_cost", "AttentionConfig", "KVCache", "rope_apply",
+    "fused_extract_mask", "k_append", "make_v_pieces", "v_append", "qk_dot", "softmax_times_v",
+    "exact_softmax_maps", "kv_from_cts",
+]
+
+
+# --------------------------------------------------------------- errors (types.hpp:16-46)
+class Error(RuntimeError):
+    pass
+
+
+class LevelUnderflow(Error):
+    pass
+
+
+class InvalidTarget(Error):
+    pass
+
+
+class ShapeMismatch(Error):
+    pass
+
+
+class LayoutMismatch(Error):
+    pass
+
+
+class CacheFull(Error):
+    pass
+
+
+class CacheEmpty(Error):
+    pass
+
+
+class DomainViolation(Error):
+    pass
+
+
+class ScaleMismatch(Error):
+    pass
+
+
+_CODES = {1: LevelUnderflow, 2: InvalidTarget, 3: ShapeMismatch, 4: LayoutMismatch, 5: CacheFull, 6: CacheEmpty,
+          7: DomainViolation, 8: ScaleMismatch}
+
+
+def _check(status: int):
+    if status != 0:
+        msg = _native.lib().sf_last_error().decode()
+        raise _CODES.get(status, Error)(msg)
+
+
+# ------------------------------------------------------------------- layouts.hpp:22-33
+_KINDS = ["contiguous", "replicated", "interleaved"]
+
+
+@dataclass(frozen=True)
+class Layout:
+    kind: str = "interleaved"
+    d: int = 0
+    t: int = 0
+    offset: int = 0
+    heads: int = 1
+    deferred_mask: bool = False
+
+    def with_(self, **kw) -> "Layout":
+        return replace(self, **kw)
+
+
+def make_interleaved(d: int, N: int, offset: int = 0, heads: int = 1) -> Layout:
+    if d <= 0 or N % d:
+        raise ShapeMismatch("layout: d*t must equal N")
+    return Layout("interleaved", d, N // d, offset, heads, False)
+
+
+def _to_sf(ly) -> Optional[SfLayout]:
+    if ly is None:
+        return None
+    return SfLayout(1, _KINDS.index(ly.kind), ly.d, ly.t, ly.offset, ly.heads, int(bool(ly.deferred_mask)))
+
+
+def _from_sf(s: SfLayout) -> Optional[Layout]:
+    if not s.valid:
+        return None
+    return Layout(_KINDS[s.kind], s.d, s.t, s.offset, s.heads, bool(s.deferred_mask))
+
+
+@dataclass
+class OpCounts:
+    """engine.hpp:30-49."""
+    rotations: int = 0
+    hoisted_rotations: int = 0
+    ct_pt_mults: int = 0
+    ct_ct_mults: int = 0
+    additions: int = 0
+    bootstraps: int = 0
+
+    @staticmethod
+    def _of(s: SfOpCounts) -> "OpCounts":
+        return OpCounts(s.rotations, s.hoisted_rotations, s.ct_pt_mults, s.ct_ct_mults, s.additions, s.bootstraps)
+
+    def __sub__(self, o):
+        return OpCounts(*(getattr(self, f) - getattr(o, f) for f in self.__dataclass_fields__))
+
+    def asdict(self):
+        return {f: getattr(self, f) for f in self.__dataclass_fields__}
+
+
+# ---------------------------------------------------------------------------- handles
+class Ciphertext:
+    """Immutable device ciphertext (engine.hpp:24-28 + CKKS scale)."""
+
+    __slots__ = ("be", "h")
+
+    def __init__(self, be: "Backend", handle: int):
+        self.be, self.h = be, handle
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h and not _shutdown[0]:
+            _native.lib().sf_ct_release(h)
+            self.h = None
+
+    def _info(self):
+        lvl, sc, z, ly = C.c_int(), C.c_double(), C.c_int(), SfLayout()
+        _check(_native.lib().sf_ct_info(self.h, C.byref(lvl), C.byref(sc), C.byref(z), C.byref(ly)))
+        return lvl.value, sc.value, bool(z.value), _from_sf(ly)
+
+    @property
+    def level(self) -> int:
+        return self._info()[0]
+
+    @property
+    def scale(self) -> float:
+        return self._info()[1]
+
+    @property
+    def is_zero(self) -> bool:
+        return self._info()[2]
+
+    @property
+    def layout(self) -> Optional[Layout]:
+        return self._info()[3]
+
+    def data(self) -> np.ndarray:
+        """Raw RNS words [2][level+1][n] (NTT domain)."""
+        out = np.empty((2, self.level + 1, self.be.n), dtype=np.uint64)
+        _check(_native.lib().sf_ct_export(self.be.ctx, self.h, out.ctypes.data_as(_native.u64p)))
+        return out
+
+
+_shutdown = [False]
+
+
+def _atexit():
+    _shutdown[0] = True
+
+
+import atexit  # noqa: E402
+
+atexit.register(_atexit)
+
+
+class _Ledger:
+    """CostLedger view (engine.hpp:54-96)."""
+
+    def __init__(self, be):
+        self.be = be
+
+    def totals(self) -> OpCounts:
+        s = SfOpCounts()
+        _check(_native.lib().sf_ledger_totals(self.be.ctx, C.byref(s)))
+        return OpCounts._of(s)
+
+    def phase_totals(self, name: str) -> OpCounts:
+        s = SfOpCounts()
+        _check(_native.lib().sf_ledger_phase_totals(self.be.ctx, name.encode(), C.byref(s)))
+        return OpCounts._of(s)
+
+    def reset(self):
+        _check(_native.lib().sf_ledger_reset(self.be.ctx))
+
+
+class _Phase:
+    def __init__(self, be, name):
+        self.be, self.name = be, name
+
+    def __enter__(self):
+        _check(_native.lib().sf_phase_push(self.be.ctx, self.name.encode()))
+        return self
+
+    def __exit__(self, *a):
+        _check(_native.lib().sf_phase_pop(self.be.ctx))
+
+
+def _slots(a, N) -> np.ndarray:
+    return np.ascontiguousarray(np.broadcast_to(np.asarray(a, dtype=np.float64), (N,)))
+
+
+class Backend:
+    """slotforge::Backend over real RNS-CKKS on one B200 (engine.hpp:112-149).
+
+    N is the reference's slot count; the ring degree defaults to 2N. Extra
+    keyword arguments select the CKKS parameters (log_n, alpha, q0_bits,
+    scale_bits, special_bits, seed, device); see DESIGN.md §3.1."""
+
+    def __init__(self, N: int, L: int, log_n: int = 0, alpha: int = 0, q0_bits: int = 0, scale_bits: int = 0,
+                 special_bits: int = 0, seed: int = 1, device: int = 0):
+        p = SfParams(N, L, log_n, alpha, q0_bits, scale_bits, special_bits, device, seed)
+        h = C.c_void_p()
+        _check(_native.lib().sf_context_create(C.byref(p), C.byref(h)))
+        self.ctx = h.value
+        n, slots, LL, al, npr = C.c_int(), C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        _check(_native.lib().sf_context_info(self.ctx, C.byref(n), C.byref(slots), C.byref(LL), C.byref(al),
+                                              C.byref(npr), None))
+        self.N, self.L, self.n, self.alpha = slots.value, LL.value, n.value, al.value
+        self.primes = np.empty(npr.value, dtype=np.uint64)
+        _check(_native.lib().sf_context_info(self.ctx, None, None, None, None, None,
+                                              self.primes.ctypes.data_as(_native.u64p)))
+        self.ledger = _Ledger(self)
+        self.seed = seed
+
+    def __del__(self):
+        if getattr(self, "ctx", None) and not _shutdown[0]:
+            _native.lib().sf_context_destroy(self.ctx)
+            self.ctx = None
+
+    def params(self):
+        return (self.N, self.L)
+
+    def phase(self, name: str):
+        return _Phase(self, name)
+
+    def _ct(self, fn, *args) -> Ciphertext:
+        out = C.c_void_p()
+        _check(fn(self.ctx, *args, C.byref(out)))
+        return Ciphertext(self, out.value)
+
+    def synchronize(self):
+        _check(_native.lib().sf_synchronize(self.ctx))
+
+    # --- client side (off-ledger)
+    def encrypt(self, slots, level: int = -1, layout=None, seed: Optional[int] = None) -> Ciphertext:
+        s = np.asarray(slots, dtype=np.float64)
+        if s.shape != (self.N,):
+            raise ShapeMismatch(f"encrypt: expected {self.N} slots, got {s.size}")
+        s = np.ascontiguousarray(s)
+        ly = _to_sf(layout)
+        return self._ct(_native.lib().sf_encrypt, s.ctypes.data_as(_native.dp), level,
+                        C.byref(ly) if ly else None, C.c_uint64(seed or 0), int(seed is not None))
+
+    def zeros(self, level: int = -1) -> Ciphertext:
+        return self._ct(_native.lib().sf_zeros, level)
+
+    def decrypt(self, ct: Ciphertext) -> np.ndarray:
+        out = np.empty(self.N)
+        _check(_native.lib().sf_decrypt(self.ctx, ct.h, out.ctypes.data_as(_native.dp)))
+        return out
+
+    def encode(self, slots, scale: float, limbs: int) -> np.ndarray:
+        s = _slots(slots, self.N)
+        out = np.empty((limbs, self.n), dtype=np.uint64)
+        _check(_native.lib().sf_encode(self.ctx, s.ctypes.data_as(_native.dp), scale, limbs,
+                                        out.ctypes.data_as(_native.u64p)))
+        return out
+
+    def import_ct(self, words, level, scale, layout=None, zero=False) -> Ciphertext:
+        w = np.ascontiguousarray(words, dtype=np.uint64)
+        ly = _to_sf(layout)
+        return self._ct(_native.lib().sf_ct_import, w.ctypes.data_as(_native.u64p), level, scale, int(zero),
+                        C.byref(ly) if ly else None)
+
+    def secret_key(self) -> np.ndarray:
+        out = np.empty((len(self.primes), self.n), dtype=np.uint64)
+        _check(_native.lib().sf_secret_key_export(self.ctx, out.ctypes.data_as(_native.u64p)))
+        return out
+
+    def switching_key(self, galois_elt: int) -> np.ndarray:
+        beta = (self.L + 1 + self.alpha - 1) // self.alpha
+        out = np.empty((beta, 2, len(self.primes), self.n), dtype=np.uint64)
+        _check(_native.lib().sf_switching_key_export(self.ctx, C.c_uint64(galois_elt),
+                                                      out.ctypes.data_as(_native.u64p)))
+        return out
+
+    def galois_elt(self, r: int) -> int:
+        return _native.lib().sf_galois_elt(self.ctx, r)
+
+    def gen_rotation_keys(self, rotations: Sequence[int]):
+        arr = (C.c_int * len(rotations))(*rotations)
+        _check(_native.lib().sf_gen_rotation_keys(self.ctx, arr, len(rotations)))
+
+    # --- evaluator ops (ledger-charged, engine.cpp:143-214)
+    def add(self, a, b):
+        return self._ct(_native.lib().sf_add, a.h, b.h)
+
+    def sub(self, a, b):
+        return self._ct(_native.lib().sf_sub, a.h, b.h)
+
+    def add_plain(self, a, p):
+        s = _slots(p, self.N)
+        return self._ct(_native.lib().sf_add_plain, a.h, s.ctypes.data_as(_native.dp))
+
+    def mul(self, a, b):
+        return self._ct(_native.lib().sf_mul, a.h, b.h)
+
+    def mul_plain(self, a, p):
+        s = _slots(p, self.N)
+        return self._ct(_native.lib().sf_mul_plain, a.h, s.ctypes.data_as(_native.dp))
+
+    def mac_plain(self, terms):
+        cts = (C.c_void_p * len(terms))(*[c.h for c, _ in terms])
+        pts = np.ascontiguousarray(np.stack([_slots(p, self.N) for _, p in terms]))
+        return self._ct(_native.lib().sf_mac_plain, cts, pts.ctypes.data_as(_native.dp), len(terms))
+
+    def rotate(self, a, r: int, hoisted: bool = False):
+        return self._ct(_native.lib().sf_rotate, a.h, int(r), int(hoisted))
+
+    def rotate_hoisted(self, a, rs: Sequence[int]):
+        arr = (C.c_int * len(rs))(*rs)
+        outs = (C.c_void_p * len(rs))()
+        _check(_native.lib().sf_rotate_hoisted(self.ctx, a.h, arr, len(rs), outs))
+        return [Ciphertext(self, o) for o in outs]
+
+    def level_drop(self, a, target: int):
+        return self._ct(_native.lib().sf_level_drop, a.h, target)
+
+    def bootstrap(self, a, target: int):
+        return self._ct(_native.lib().sf_bootstrap, a.h, target)
+
+    def exact_transform(self, a, f):
+        """Oracle hook (engine.cpp:208-214) as a client round trip: decrypt,
+        apply f, re-encrypt at the same level (free, level-neutral)."""
+        out = np.asarray(f(self.decrypt(a)), dtype=np.float64)
+        if out.shape != (self.N,):
+            raise ShapeMismatch("exact_transform result: wrong slot count")
+        return self.encrypt(out, a.level, a.layout)
+
+    def with_layout(self, ct, layout):
+        ly = _to_sf(layout)
+        return self._ct(_native.lib().sf_ct_with_layout, ct.h, C.byref(ly) if ly else None)
+
+    # --- timing / accounting
+    def event_record(self, slot: int):
+        _check(_native.lib().sf_event_record(self.ctx, slot))
+
+    def event_elapsed_ms(self, a: int, b: int) -> float:
+        ms = C.c_float()
+        _check(_native.lib().sf_event_elapsed_ms(self.ctx, a, b, C.byref(ms)))
+        return ms.value
+
+    def kernel_launches(self) -> int:
+        return _native.lib().sf_kernel_launches(self.ctx)
+
+
+# ------------------------------------------------------------------------------ VMM
+class VmmPlan:
+    """Pre-encoded interleaved diagonals (vmm.cpp:159-175) for one weight matrix
+    at one input level; W=None selects the reference bench weight
+    sin(0.001 (31 r + c) + 0.25) (slotforge_cli.cpp:88-92)."""
+
+    def __init__(self, be: Backend, W, rows: int, cols: int, level: int, in_offset: int = 0, out_offset: int = 0,
+                 bsgs: bool = True):
+        self.be, self.rows, self.cols, self.level = be, rows, cols, level
+        self.in_offset, self.out_offset, self.bsgs = in_offset, out_offset, bsgs
+        h = C.c_void_p()
+        if W is not None:
+            W = np.ascontiguousarray(np.asarray(W, dtype=np.float64))
+            if W.shape != (rows, cols):
+                raise ShapeMismatch("vmm plan: W shape")
+        _check(_native.lib().sf_vmm_plan_create(be.ctx, W.ctypes.data_as(_native.dp) if W is not None else None,
+                                                 rows, cols, level, in_offset, out_offset, int(bsgs), C.byref(h)))
+        self.h = h.value
+
+    def __del__(self):
+        if getattr(self, "h", None) and not _shutdown[0]:
+            _native.lib().sf_vmm_plan_destroy(self.h)
+            self.h = None
+
+
+def predict_interleaved_cost(be: Backend, rows: int, cols: int, bsgs: bool = False, mask_output: bool = False):
+    """vmm.cpp:473-488 -> (rotations, ct_pt_mults, depth)."""
+    r, c, d = C.c_longlong(), C.c_longlong(), C.c_int()
+    _check(_native.lib().sf_vmm_predict(be.ctx, rows, cols, int(bsgs), int(mask_output), C.byref(r), C.byref(c),
+                                         C.byref(d)))
+    return r.value, c.value, d.value
+
+
+def vmm_interleaved(be: Backend, x: Ciphertext, W, bsgs: bool = False, out_offset: int = 0,
+                    mask_output: bool = False, plan: Optional[VmmPlan] = None) -> Ciphertext:
+    """vmm_interleaved (vmm.hpp:74-75). Pass `plan` to reuse pre-encoded
+    diagonals; otherwise a plan for W at x's level is built (offline cost)."""
+    if plan is None:
+        ly = x.layout
+        if ly is None or ly.kind != "interleaved":
+            raise LayoutMismatch("vmm_interleaved: input must carry an interleaved layout")
+        W = np.asarray(W, dtype=np.float64)
+        plan = VmmPlan(be, W, W.shape[0], W.shape[1], max(x.level, 1), ly.offset, out_offset, bsgs)
+    return be._ct(_native.lib().sf_vmm_interleaved, x.h, plan.h, int(mask_output))
+
+
+# ------------------------------------------------------------------------ attention
+@dataclass
+class AttentionConfig:
+    """kv_attention.hpp:32-42."""
+    N: int
+    d: int
+    H: int = 1
+    n0: int = 0
+    n_max: int = 0
+
+    @property
+    def d_head(self):
+        return self.d // self.H
+
+    @property
+    def t(self):
+        return self.N // self.d
+
+    @property
+    def group_tokens(self):
+        return self.N // self.H
+
+
+class KVCache:
+    """Copy-on-write KV cache handle (kv_attention.hpp:49-54)."""
+
+    def __init__(self, be: Backend, cfg: AttentionConfig, handle: Optional[int] = None):
+        self.be, self.cfg = be, cfg
+        if handle is None:
+            h = C.c_void_p()
+            _check(_native.lib().sf_kv_create(be.ctx, cfg.d, cfg.H, cfg.n0, cfg.n_max, C.byref(h)))
+            handle = h.value
+        self.h = handle
+
+    def __del__(self):
+        if getattr(self, "h", None) and not _shutdown[0]:
+            _native.lib().sf_kv_release(self.h)
+            self.h = None
+
+    def _info(self):
+        a, b, c, d = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        _check(_native.lib().sf_kv_info(self.h, C.byref(a), C.byref(b), C.byref(c), C.byref(d)))
+        return a.value, b.value, c.value, d.value
+
+    @property
+    def n_prime(self):
+        return self._info()[0]
+
+    @property
+    def k_cts(self):
+        n = self._info()[1]
+        return [self._get(0, 0, i) for i in range(n)]
+
+    @property
+    def v_cts(self):
+        _, _, g, nv = self._info()
+        return [[self._get(1, gi, i) for i in range(nv)] for gi in range(g)]
+
+    def _get(self, which, g, idx):
+        out = C.c_void_p()
+        _check(_native.lib().sf_kv_get(self.h, which, g, idx, C.byref(out)))
+        return Ciphertext(self.be, out.value)
+
+
+def kv_from_cts(be: Backend, cfg: AttentionConfig, n_prime: int, k_cts, v_cts) -> KVCache:
+    ks = (C.c_void_p * max(1, len(k_cts)))(*[c.h for c in k_cts])
+    flat = [c for g in v_cts for c in g]
+    vs = (C.c_void_p * max(1, len(flat)))(*[c.h for c in flat])
+    h = C.c_void_p()
+    _check(_native.lib().sf_kv_from_cts(be.ctx, cfg.d, cfg.H, cfg.n0, cfg.n_max, n_prime, ks, len(k_cts), vs,
+                                         len(v_cts), C.byref(h)))
+    return KVCache(be, cfg, h.value)
+
+
+def rope_apply(be: Backend, x: Ciphertext, cfg: AttentionConfig, position: int, base: float = 10000.0):
+    """kv_attention.cpp:111-117."""
+    return be._ct(_native.lib().sf_rope_apply, x.h, cfg.d, cfg.H, position, base)
+
+
+def fused_extract_mask(be: Backend, x: Ciphertext, coeff=None):
+    """fused_extract with a mask successor (vmm.cpp:102-108)."""
+    c = None if coeff is None else _slots(coeff, be.N)
+    return be._ct(_native.lib().sf_fused_extract_mask, x.h, c.ctypes.data_as(_native.dp) if c is not None else None)
+
+
+def k_append(be: Backend, cache: KVCache, k_new: Ciphertext) -> KVCache:
+    out = C.c_void_p()
+    _check(_native.lib().sf_k_append(be.ctx, cache.h, k_new.h, C.byref(out)))
+    return KVCache(be, cache.cfg, out.value)
+
+
+def make_v_pieces(be: Backend, cache: KVCache, v_open: Ciphertext, position: int):
+    parts = (C.c_void_p * cache.cfg.d_head)()
+    _check(_native.lib().sf_make_v_pieces(be.ctx, cache.h, v_open.h, position, parts))
+    return [Ciphertext(be, p) for p in parts]
+
+
+def v_append(be: Backend, cache: KVCache, parts) -> KVCache:
+    arr = (C.c_void_p * max(1, len(parts)))(*[p.h for p in parts])
+    out = C.c_void_p()
+    _check(_native.lib().sf_v_append(be.ctx, cache.h, arr, len(parts), C.byref(out)))
+    return KVCache(be, cache.cfg, out.value)
+
+
+def qk_dot(be: Backend, q: Ciphertext, cache: KVCache):
+    gt = cache.cfg.group_tokens
+    cap = max(1, (max(cache.n_prime, 1) + gt - 1) // gt)
+    maps = (C.c_void_p * cap)()
+    n = C.c_int()
+    _check(_native.lib().sf_qk_dot(be.ctx, q.h, cache.h, maps, C.byref(n)))
+    return [Ciphertext(be, maps[i]) for i in range(n.value)]
+
+
+def softmax_times_v(be: Backend, probs, cache: KVCache) -> Ciphertext:
+    arr = (C.c_void_p * max(1, len(probs)))(*[p.h for p in probs])
+    return be._ct(_native.lib().sf_softmax_times_v, arr, len(probs), cache.h)
+
+
+def exact_softmax_maps(be: Backend, maps, cfg: AttentionConfig, n_prime: int):
+    """Client-side oracle hook (kv_attention.cpp:395-412): decrypt the score
+    maps, take the exact per-head softmax over the first n_prime scores,
+    re-encrypt at the same level (no ledger cost)."""
+    gt = cfg.group_tokens
+    slots = [be.decrypt(m) for m in maps]
+    out = [np.zeros(cfg.N) for _ in maps]
+    for h in range(cfg.H):
+        sc = np.array([slots[v // gt][h * gt + v % gt] for v in range(n_prime)])
+        p = np.exp(sc - sc.max())
+        p /= p.sum()
+        for v in range(n_prime):
+            out[v // gt][h * gt + v % gt] = p[v]
+    return [be.exact_transform(m, (lambda _s, o=o: o)) for m, o in zip(maps, out)]

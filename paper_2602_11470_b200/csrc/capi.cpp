@@ -1,0 +1,478 @@
+// extern "C" boundary (include/sf_b200.h): opaque refcounted handles over the
+// C++ evaluator and protocols; every exception is mapped 1:1 onto an sf_status
+// code matching the reference's exception types (types.hpp:16-46).
+#include "../../include/sf_b200.h"
+
+#include <cstring>
+#include <string>
+
+#include "context.h"
+#include "protocols.h"
+
+struct sf_context {
+  std::unique_ptr<sf::Context> c;
+};
+struct sf_ct {
+  std::atomic<int> rc{1};
+  sf::Ct v;
+};
+struct sf_vmm_plan {
+  std::unique_ptr<sf::VmmPlan> p;
+};
+struct sf_kvcache {
+  std::atomic<int> rc{1};
+  sf::KV kv;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+sf_status guard(F&& f) {
+  try {
+    f();
+    return SF_OK;
+  } catch (const sf::Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return SF_ERR_INTERNAL;
+  } catch (...) {
+    g_err = "unknown error";
+    return SF_ERR_INTERNAL;
+  }
+}
+
+sf::OptLayout to_layout(const sf_layout* l) {
+  if (!l || !l->valid) return std::nullopt;
+  sf::Layout ly;
+  ly.kind = static_cast<sf::LayoutKind>(l->kind);
+  ly.d = l->d;
+  ly.t = l->t;
+  ly.offset = l->offset;
+  ly.heads = l->heads;
+  ly.deferred_mask = l->deferred_mask != 0;
+  return ly;
+}
+
+void from_layout(const sf::OptLayout& ly, sf_layout* out) {
+  std::memset(out, 0, sizeof(*out));
+  if (!ly) return;
+  out->valid = 1;
+  out->kind = static_cast<int>(ly->kind);
+  out->d = ly->d;
+  out->t = ly->t;
+  out->offset = ly->offset;
+  out->heads = ly->heads;
+  out->deferred_mask = ly->deferred_mask ? 1 : 0;
+}
+
+sf_ct* wrap(sf::Ct v) {
+  auto* h = new sf_ct;
+  h->v = std::move(v);
+  return h;
+}
+sf_kvcache* wrap_kv(sf::KV kv) {
+  auto* h = new sf_kvcache;
+  h->kv = std::move(kv);
+  return h;
+}
+
+void need(const void* p, const char* what) { sf::require(p != nullptr, sf::kInvalidTarget, std::string(what) + ": null"); }
+
+void counts_out(const sf::OpCounts& c, sf_op_counts* o) {
+  o->rotations = c.rotations;
+  o->hoisted_rotations = c.hoisted_rotations;
+  o->ct_pt_mults = c.ct_pt_mults;
+  o->ct_ct_mults = c.ct_ct_mults;
+  o->additions = c.additions;
+  o->bootstraps = c.bootstraps;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sf_last_error(void) { return g_err.c_str(); }
+
+sf_status sf_context_create(const sf_params* p, sf_context** out) {
+  return guard([&] {
+    need(p, "params");
+    auto* h = new sf_context;
+    try {
+      h->c = sf::make_context(p->slots, p->L, p->log_n, p->alpha, p->q0_bits, p->scale_bits, p->special_bits,
+                              p->seed, p->device);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+void sf_context_destroy(sf_context* ctx) { delete ctx; }
+
+sf_status sf_context_info(const sf_context* ctx, int* n, int* slots, int* L, int* alpha, int* num_primes,
+                          uint64_t* primes) {
+  return guard([&] {
+    need(ctx, "ctx");
+    const auto& c = *ctx->c;
+    if (n) *n = c.n;
+    if (slots) *slots = c.slots;
+    if (L) *L = c.L;
+    if (alpha) *alpha = c.alpha;
+    if (num_primes) *num_primes = c.np;
+    if (primes) std::copy(c.primes.begin(), c.primes.end(), primes);
+  });
+}
+
+sf_status sf_synchronize(sf_context* ctx) {
+  return guard([&] { SF_CUDA(cudaStreamSynchronize(ctx->c->stream)); });
+}
+
+sf_status sf_gen_rotation_keys(sf_context* ctx, const int* rotations, int count) {
+  return guard([&] {
+    for (int i = 0; i < count; ++i)
+      if (sf::pos_mod(rotations[i], ctx->c->slots) != 0) sf::get_key(*ctx->c, sf::galois_elt(*ctx->c, rotations[i]));
+  });
+}
+
+sf_status sf_secret_key_export(sf_context* ctx, uint64_t* out) {
+  return guard([&] {
+    auto& c = *ctx->c;
+    SF_CUDA(cudaMemcpyAsync(out, c.sk->p, (size_t)c.np * c.n * 8, cudaMemcpyDeviceToHost, c.stream));
+    SF_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+sf_status sf_switching_key_export(sf_context* ctx, uint64_t g, uint64_t* out) {
+  return guard([&] {
+    auto& c = *ctx->c;
+    const auto& k = sf::get_key(c, g);
+    SF_CUDA(cudaMemcpyAsync(out, k->p, k->words * 8, cudaMemcpyDeviceToHost, c.stream));
+    SF_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+uint64_t sf_galois_elt(const sf_context* ctx, int r) { return sf::galois_elt(*ctx->c, r); }
+
+// --- handles
+sf_ct* sf_ct_retain(sf_ct* ct) {
+  if (ct) ct->rc.fetch_add(1);
+  return ct;
+}
+void sf_ct_release(sf_ct* ct) {
+  if (ct && ct->rc.fetch_sub(1) == 1) delete ct;
+}
+
+sf_status sf_ct_info(const sf_ct* ct, int* level, double* scale, int* is_zero, sf_layout* layout) {
+  return guard([&] {
+    need(ct, "ct");
+    if (level) *level = ct->v.level();
+    if (scale) *scale = ct->v.scale;
+    if (is_zero) *is_zero = ct->v.zero ? 1 : 0;
+    if (layout) from_layout(ct->v.layout, layout);
+  });
+}
+
+sf_status sf_ct_with_layout(sf_context*, const sf_ct* ct, const sf_layout* layout, sf_ct** out) {
+  return guard([&] {
+    need(ct, "ct");
+    sf::Ct v = ct->v;
+    v.layout = to_layout(layout);
+    *out = wrap(std::move(v));
+  });
+}
+
+sf_status sf_ct_export(sf_context* ctx, const sf_ct* ct, uint64_t* out) {
+  return guard([&] {
+    auto& c = *ctx->c;
+    const sf::Ct& v = ct->v;
+    const size_t w = (size_t)v.limbs * c.n;
+    SF_CUDA(cudaMemcpyAsync(out, v.c0(), w * 8, cudaMemcpyDeviceToHost, c.stream));
+    SF_CUDA(cudaMemcpyAsync(out + w, v.c1(c.n), w * 8, cudaMemcpyDeviceToHost, c.stream));
+    SF_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+sf_status sf_ct_import(sf_context* ctx, const uint64_t* words, int level, double scale, int is_zero,
+                       const sf_layout* layout, sf_ct** out) {
+  return guard([&] {
+    auto& c = *ctx->c;
+    sf::require(level >= 0 && level <= c.L, sf::kInvalidTarget, "import: level out of range");
+    sf::Ct v = sf::alloc_ct(c, level + 1, scale);
+    v.zero = is_zero != 0;
+    v.layout = to_layout(layout);
+    SF_CUDA(cudaMemcpyAsync(v.c0(), words, v.buf->words * 8, cudaMemcpyHostToDevice, c.stream));
+    SF_CUDA(cudaStreamSynchronize(c.stream));
+    *out = wrap(std::move(v));
+  });
+}
+
+// --- client side
+sf_status sf_encrypt(sf_context* ctx, const double* slots, int level, const sf_layout* layout, uint64_t seed,
+                     int use_seed, sf_ct** out) {
+  return guard([&] {
+    auto& c = *ctx->c;
+    need(slots, "slots");
+    const uint64_t s = use_seed ? seed : c.next_seed();
+    *out = wrap(sf::encrypt(c, slots, level, s, to_layout(layout)));
+  });
+}
+
+sf_status sf_zeros(sf_context* ctx, int level, sf_ct** out) {
+  return guard([&] { *out = wrap(sf::zeros(*ctx->c, level)); });
+}
+
+sf_status sf_decrypt(sf_context* ctx, const sf_ct* ct, double* slots_out) {
+  return guard([&] {
+    need(ct, "ct");
+    sf::decrypt(*ctx->c, ct->v, slots_out);
+  });
+}
+
+sf_status sf_encode(sf_context* ctx, const double* slots, double scale, int limbs, uint64_t* out) {
+  return guard([&] {
+    auto& c = *ctx->c;
+    sf::Pt p = sf::encode_pt(c, slots, scale, limbs);
+    SF_CUDA(cudaMemcpyAsync(out, p.buf->p, (size_t)limbs * c.n * 8, cudaMemcpyDeviceToHost, c.stream));
+    SF_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+// --- evaluator
+sf_status sf_add(sf_context* ctx, const sf_ct* a, const sf_ct* b, sf_ct** out) {
+  return guard([&] { *out = wrap(sf::add(*ctx->c, a->v, b->v, false)); });
+}
+sf_status sf_sub(sf_context* ctx, const sf_ct* a, const sf_ct* b, sf_ct** out) {
+  return guard([&] { *out = wrap(sf::add(*ctx->c, a->v, b->v, true)); });
+}
+sf_status sf_add_plain(sf_context* ctx, const sf_ct* a, const double* slots, sf_ct** out) {
+  return guard([&] { *out = wrap(sf::add_plain(*ctx->c, a->v, slots)); });
+}
+sf_status sf_mul(sf_context* ctx, const sf_ct* a, const sf_ct* b, sf_ct** out) {
+  return guard([&] { *out = wrap(sf::mul(*ctx->c, a->v, b->v)); });
+}
+sf_status sf_mul_plain(sf_context* ctx, const sf_ct* a, const double* slots, sf_ct** out) {
+  return guard([&] { *out = wrap(sf::mul_plain(*ctx->c, a->v, slots)); });
+}
+sf_status sf_mac_plain(sf_context* ctx, const sf_ct* const* cts, const double* slots, int k, sf_ct** out) {
+  return guard([&] {
+    auto& c = *ctx->c;
+    sf::require(k >= 1, sf::kShapeMismatch, "mac_plain: need at least one term");
+    int limbs = 1 << 30;
+    for (int i = 0; i < k; ++i) {
+      sf::check_ct(c, cts[i]->v, "mul_plain");
+      sf::require(cts[i]->v.level() > 0, sf::kLevelUnderflow, "mul_plain: no multiplicative level left");
+      limbs = std::min(limbs, cts[i]->v.limbs);
+    }
+    std::vector<sf::Pt> pts;
+    pts.reserve(k);
+    for (int i = 0; i < k; ++i)
+      pts.push_back(sf::encode_pt(c, slots + (size_t)i * c.slots, (double)c.primes[limbs - 1], limbs));
+    std::vector<const sf::Ct*> cv;
+    std::vector<const sf::Pt*> pv;
+    for (int i = 0; i < k; ++i) cv.push_back(&cts[i]->v), pv.push_back(&pts[i]);
+    *out = wrap(sf::mac_plain(c, cv, pv));
+  });
+}
+sf_status sf_rotate(sf_context* ctx, const sf_ct* a, int r, int hoisted, sf_ct** out) {
+  return guard([&] { *out = wrap(sf::rotate(*ctx->c, a->v, r, hoisted != 0)); });
+}
+sf_status sf_rotate_hoisted(sf_context* ctx, const sf_ct* a, const int* r, int k, sf_ct** outs) {
+  return guard([&] {
+    auto v = sf::rotate_hoisted(*ctx->c, a->v, std::vector<int>(r, r + k));
+    for (int i = 0; i < k; ++i) outs[i] = wrap(std::move(v[i]));
+  });
+}
+sf_status sf_level_drop(sf_context* ctx, const sf_ct* a, int target, sf_ct** out) {
+  return guard([&] { *out = wrap(sf::level_drop(*ctx->c, a->v, target)); });
+}
+sf_status sf_bootstrap(sf_context* ctx, const sf_ct* a, int target, sf_ct** out) {
+  return guard([&] { *out = wrap(sf::bootstrap(*ctx->c, a->v, target)); });
+}
+
+// --- ledger
+sf_status sf_ledger_totals(const sf_context* ctx, sf_op_counts* out) {
+  return guard([&] {
+    auto& l = ctx->c->ledger;
+    std::lock_guard<std::mutex> lk(l.mu);
+    counts_out(l.total, out);
+  });
+}
+sf_status sf_ledger_phase_totals(const sf_context* ctx, const char* phase, sf_op_counts* out) {
+  return guard([&] {
+    auto& l = ctx->c->ledger;
+    std::lock_guard<std::mutex> lk(l.mu);
+    auto it = l.by_phase.find(phase);
+    counts_out(it == l.by_phase.end() ? sf::OpCounts{} : it->second, out);
+  });
+}
+sf_status sf_ledger_reset(sf_context* ctx) {
+  return guard([&] { ctx->c->ledger.reset(); });
+}
+sf_status sf_phase_push(sf_context* ctx, const char* phase) {
+  return guard([&] {
+    auto& l = ctx->c->ledger;
+    std::lock_guard<std::mutex> lk(l.mu);
+    l.stack.push_back(phase);
+  });
+}
+sf_status sf_phase_pop(sf_context* ctx) {
+  return guard([&] {
+    auto& l = ctx->c->ledger;
+    std::lock_guard<std::mutex> lk(l.mu);
+    if (l.stack.size() > 1) l.stack.pop_back();
+  });
+}
+
+// --- VMM
+sf_status sf_vmm_plan_create(sf_context* ctx, const double* W, int rows, int cols, int level, int in_offset,
+                             int out_offset, int bsgs, sf_vmm_plan** out) {
+  return guard([&] {
+    auto* h = new sf_vmm_plan;
+    try {
+      h->p = sf::make_vmm_plan(*ctx->c, W, rows, cols, level, in_offset, out_offset, bsgs != 0);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+void sf_vmm_plan_destroy(sf_vmm_plan* plan) { delete plan; }
+
+sf_status sf_vmm_predict(const sf_context* ctx, int rows, int cols, int bsgs, int mask_output, long long* rotations,
+                         long long* ct_pt_mults, int* depth) {
+  return guard([&] {
+    sf::predict_interleaved_cost(ctx->c->slots, rows, cols, bsgs != 0, mask_output != 0, rotations, ct_pt_mults,
+                                 depth);
+  });
+}
+
+sf_status sf_vmm_interleaved(sf_context* ctx, const sf_ct* x, const sf_vmm_plan* plan, int mask_output,
+                             sf_ct** out) {
+  return guard([&] { *out = wrap(sf::vmm_interleaved(*ctx->c, x->v, *plan->p, mask_output != 0)); });
+}
+
+// --- KV attention
+sf_status sf_kv_create(sf_context* ctx, int d, int H, int n0, int n_max, sf_kvcache** out) {
+  return guard([&] {
+    sf::KV kv;
+    kv.cfg = sf::AttnCfg{ctx->c->slots, d, H, n0, n_max};
+    sf::validate_attention_config(kv.cfg, ctx->c->slots);
+    *out = wrap_kv(std::move(kv));
+  });
+}
+sf_kvcache* sf_kv_retain(sf_kvcache* kv) {
+  if (kv) kv->rc.fetch_add(1);
+  return kv;
+}
+void sf_kv_release(sf_kvcache* kv) {
+  if (kv && kv->rc.fetch_sub(1) == 1) delete kv;
+}
+sf_status sf_kv_info(const sf_kvcache* kv, int* n_prime, int* n_k, int* n_groups, int* n_variants) {
+  return guard([&] {
+    if (n_prime) *n_prime = kv->kv.n_prime;
+    if (n_k) *n_k = (int)kv->kv.k.size();
+    if (n_groups) *n_groups = (int)kv->kv.v.size();
+    if (n_variants) *n_variants = sf::v_variant_count(kv->kv.cfg);
+  });
+}
+sf_status sf_kv_get(const sf_kvcache* kv, int which, int g, int idx, sf_ct** out) {
+  return guard([&] {
+    const auto& k = kv->kv;
+    if (which == 0) {
+      sf::require(idx >= 0 && idx < (int)k.k.size(), sf::kShapeMismatch, "kv_get: key index");
+      *out = wrap(k.k[idx]);
+    } else {
+      sf::require(g >= 0 && g < (int)k.v.size() && idx >= 0 && idx < (int)k.v[g].size(), sf::kShapeMismatch,
+                  "kv_get: value index");
+      *out = wrap(k.v[g][idx]);
+    }
+  });
+}
+sf_status sf_kv_from_cts(sf_context* ctx, int d, int H, int n0, int n_max, int n_prime, const sf_ct* const* k_cts,
+                         int n_k, const sf_ct* const* v_cts, int n_groups, sf_kvcache** out) {
+  return guard([&] {
+    sf::KV kv;
+    kv.cfg = sf::AttnCfg{ctx->c->slots, d, H, n0, n_max};
+    sf::validate_attention_config(kv.cfg, ctx->c->slots);
+    kv.n_prime = n_prime;
+    for (int i = 0; i < n_k; ++i) kv.k.push_back(k_cts[i]->v);
+    const int nv = sf::v_variant_count(kv.cfg);
+    for (int g = 0; g < n_groups; ++g) {
+      kv.v.emplace_back();
+      for (int i = 0; i < nv; ++i) kv.v.back().push_back(v_cts[(size_t)g * nv + i]->v);
+    }
+    *out = wrap_kv(std::move(kv));
+  });
+}
+sf_status sf_rope_apply(sf_context* ctx, const sf_ct* x, int d, int H, long long position, double base,
+                        sf_ct** out) {
+  return guard([&] {
+    sf::AttnCfg cfg{ctx->c->slots, d, H, 0, 1};
+    *out = wrap(sf::rope_apply(*ctx->c, x->v, cfg, position, base));
+  });
+}
+sf_status sf_fused_extract_mask(sf_context* ctx, const sf_ct* x, const double* coeff, sf_ct** out) {
+  return guard([&] { *out = wrap(sf::fused_extract_mask(*ctx->c, x->v, coeff)); });
+}
+sf_status sf_k_append(sf_context* ctx, const sf_kvcache* cache, const sf_ct* k_new, sf_kvcache** out) {
+  return guard([&] { *out = wrap_kv(sf::k_append(*ctx->c, cache->kv, k_new->v)); });
+}
+sf_status sf_make_v_pieces(sf_context* ctx, const sf_kvcache* cache, const sf_ct* v_open, int position,
+                           sf_ct** parts_out) {
+  return guard([&] {
+    auto parts = sf::make_v_pieces(*ctx->c, cache->kv, v_open->v, position);
+    for (size_t i = 0; i < parts.size(); ++i) parts_out[i] = wrap(std::move(parts[i]));
+  });
+}
+sf_status sf_v_append(sf_context* ctx, const sf_kvcache* cache, const sf_ct* const* parts, int n_parts,
+                      sf_kvcache** out) {
+  return guard([&] {
+    std::vector<sf::Ct> p;
+    for (int i = 0; i < n_parts; ++i) p.push_back(parts[i]->v);
+    *out = wrap_kv(sf::v_append(*ctx->c, cache->kv, p));
+  });
+}
+sf_status sf_qk_dot(sf_context* ctx, const sf_ct* q, const sf_kvcache* cache, sf_ct** maps_out, int* n_maps) {
+  return guard([&] {
+    auto maps = sf::qk_dot(*ctx->c, q->v, cache->kv);
+    *n_maps = (int)maps.size();
+    for (size_t i = 0; i < maps.size(); ++i) maps_out[i] = wrap(std::move(maps[i]));
+  });
+}
+sf_status sf_softmax_times_v(sf_context* ctx, const sf_ct* const* probs, int n_probs, const sf_kvcache* cache,
+                             sf_ct** out) {
+  return guard([&] {
+    std::vector<sf::Ct> p;
+    for (int i = 0; i < n_probs; ++i) p.push_back(probs[i]->v);
+    *out = wrap(sf::softmax_times_v(*ctx->c, p, cache->kv));
+  });
+}
+
+// --- timing
+sf_status sf_event_record(sf_context* ctx, int slot) {
+  return guard([&] {
+    auto& c = *ctx->c;
+    while ((int)c.events.size() <= slot) {
+      cudaEvent_t e;
+      SF_CUDA(cudaEventCreate(&e));
+      c.events.push_back(e);
+    }
+    SF_CUDA(cudaEventRecord(c.events[slot], c.stream));
+  });
+}
+sf_status sf_event_elapsed_ms(sf_context* ctx, int a, int b, float* ms) {
+  return guard([&] {
+    auto& c = *ctx->c;
+    SF_CUDA(cudaEventSynchronize(c.events[b]));
+    SF_CUDA(cudaEventElapsedTime(ms, c.events[a], c.events[b]));
+  });
+}
+long long sf_kernel_launches(const sf_context* ctx) { return ctx->c->launches.load(); }
+
+}  // extern "C"

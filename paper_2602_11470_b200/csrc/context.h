@@ -1,0 +1,205 @@
+// Device-resident CKKS context, ciphertext values and the evaluator.
+// DESIGN.md §3 is the canonical specification these routines implement
+// (shared, as a spec only, with the CPU oracle under oracle/).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <functional>
+#include <map>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "common.h"
+
+namespace sf {
+
+struct Context;
+
+void cuda_check(cudaError_t e, const char* what);
+#define SF_CUDA(x) ::sf::cuda_check((x), #x)
+
+// Stream-ordered device allocation (cudaMallocAsync pool; frees are enqueued on
+// the context stream so in-flight kernels that still read a buffer are safe).
+struct Buf {
+  u64* p = nullptr;
+  size_t words = 0;
+  Context* ctx = nullptr;
+  Buf(Context* c, size_t w);
+  ~Buf();
+  Buf(const Buf&) = delete;
+  Buf& operator=(const Buf&) = delete;
+};
+using BufPtr = std::shared_ptr<Buf>;
+
+// Ciphertext value: c0 at p, c1 at p + stride*n, `limbs` active limbs each
+// (level = limbs - 1); level_drop is an O(1) view.
+struct Ct {
+  BufPtr buf;
+  int limbs = 0;
+  int stride = 0;
+  double scale = 0.0;
+  bool zero = false;  // trivial (0, 0) ciphertext: Backend::zeros (engine.cpp:123)
+  OptLayout layout;
+  int level() const { return limbs - 1; }
+  u64* c0() const { return buf ? buf->p : nullptr; }
+  u64* c1(int n) const { return buf ? buf->p + (size_t)stride * n : nullptr; }
+};
+
+// NTT-domain plaintext (limbs x n words), encoded at `scale`.
+struct Pt {
+  BufPtr buf;
+  int limbs = 0;
+  double scale = 0.0;
+};
+
+// Fast basis conversion tables for src primes -> dst primes.
+struct ConvPlan {
+  int nsrc = 0, ndst = 0;
+  std::vector<int> src, dst;  // prime indices
+  BufPtr tab;                 // [nsrc] qhat_inv, [nsrc] qhat_inv_shoup, [nsrc][ndst] qhat mod dst
+};
+
+struct OpCounts {
+  long long rotations = 0, hoisted_rotations = 0, ct_pt_mults = 0, ct_ct_mults = 0, additions = 0,
+            bootstraps = 0;
+};
+
+// CostLedger (engine.hpp:54-96): totals + first-use-ordered phases.
+struct Ledger {
+  std::mutex mu;
+  OpCounts total;
+  std::vector<std::string> order;
+  std::map<std::string, OpCounts> by_phase;
+  std::vector<std::string> stack{"(unphased)"};
+  template <class F>
+  void bump(F f) {
+    std::lock_guard<std::mutex> lk(mu);
+    f(total);
+    auto it = by_phase.find(stack.back());
+    if (it == by_phase.end()) {
+      order.push_back(stack.back());
+      it = by_phase.emplace(stack.back(), OpCounts{}).first;
+    }
+    f(it->second);
+  }
+  void rot(bool hoisted, long long k = 1) {
+    bump([&](OpCounts& c) {
+      c.rotations += k;
+      if (hoisted) c.hoisted_rotations += k;
+    });
+  }
+  void ctpt(long long k = 1) { bump([&](OpCounts& c) { c.ct_pt_mults += k; }); }
+  void ctct(long long k = 1) { bump([&](OpCounts& c) { c.ct_ct_mults += k; }); }
+  void add(long long k = 1) {
+    if (k) bump([&](OpCounts& c) { c.additions += k; });
+  }
+  void boot() { bump([&](OpCounts& c) { c.bootstraps += 1; }); }
+  void reset() {
+    std::lock_guard<std::mutex> lk(mu);
+    total = {};
+    order.clear();
+    by_phase.clear();
+    stack = {"(unphased)"};
+  }
+};
+
+// Device-side prime / twiddle tables (one array per quantity, indexed by prime).
+struct Tabs {
+  const u64 *q, *mh, *ml;          // prime, Barrett mu = floor(2^128 / q)
+  const u64 *psi, *psi_s;          // [np][n] psi^{br(k)} (+ Shoup)
+  const u64 *ipsi, *ipsi_s;        // [np][n] psi^{-br(k)} (+ Shoup)
+  const u64 *ninv, *ninv_s;        // [np]
+  int n, logn;
+};
+
+// A batch of limbs for one kernel launch: entry b -> (word offset slot[b]*n,
+// prime index prime[b]). Kept small so it travels as a kernel parameter.
+constexpr int kMaxBatch = 96;
+struct LimbBatch {
+  int count = 0;
+  uint16_t slot[kMaxBatch];
+  uint8_t prime[kMaxBatch];
+};
+
+struct Context {
+  // parameters
+  int logn = 0, n = 0, slots = 0, L = 0, alpha = 0, beta = 0, np = 0;
+  double delta = 0.0;
+  u64 seed = 0;
+  int device = 0;
+  std::vector<u64> primes;  // q0..qL, p0..p_{alpha-1}
+  cudaStream_t stream = nullptr;
+  cudaMemPool_t pool = nullptr;
+
+  // device tables
+  BufPtr tab_store;  // owns all table memory below
+  Tabs tabs{};
+  std::vector<u64> mu_hi, mu_lo;
+
+  // host copies needed by the encoder
+  std::vector<double> fft_re, fft_im;  // zeta^{br(k)}
+  std::vector<uint32_t> slot_index;    // transform index of slot j (n/2 entries)
+
+  BufPtr sk;  // [np][n] NTT domain
+  std::map<u64, BufPtr> keys;  // galois element (0 = relin) -> [beta][2][np][n]
+  std::map<std::string, ConvPlan> conv_plans;
+  std::map<std::string, Pt> pt_cache;  // semantic-key plaintext cache (masks)
+  std::map<int, BufPtr> level_consts;  // per-limb-count rescale / moddown constants
+
+  Ledger ledger;
+  u64 enc_counter = 0;
+  std::atomic<long long> launches{0};
+  std::vector<cudaEvent_t> events;
+
+  std::mutex mu;  // guards key / plan caches
+
+  ~Context();
+
+  int P_index(int k) const { return L + 1 + k; }
+  u64 next_seed();  // DESIGN.md §3.4 auto seed
+};
+
+// --- construction ------------------------------------------------------------
+std::unique_ptr<Context> make_context(int slots, int L, int log_n, int alpha, int q0_bits, int scale_bits,
+                                      int special_bits, u64 seed, int device);
+std::vector<u64> generate_primes(int logn, int L, int q0_bits, int scale_bits, int alpha, int special_bits);
+u64 min_primitive_root(u64 q, int n);
+
+// --- encoder (host) ------------------------------------------
+std::vector<i64> encode_coeffs(const Context& c, const double* slots, double scale);
+void decode_coeffs(const Context& c, const std::vector<double>& coeff, double scale, double* slots);
+
+// --- device primitives (kernels.cu) -----------------------------------------
+void launch_ntt(Context& c, u64* base, const LimbBatch& b, bool inverse);
+void ntt_limbs(Context& c, u64* base, int count, int first_prime, bool inverse);  // contiguous limbs
+void ntt_list(Context& c, const std::vector<std::pair<u64*, int>>& limbs, bool inverse);
+
+// --- evaluator (evaluator.cu) -------------------------------------------------
+Ct alloc_ct(Context& c, int limbs, double scale);
+Pt encode_pt(Context& c, const double* slots, double scale, int limbs);
+std::vector<Pt> encode_many(Context& c, const std::function<void(int, double*)>& gen, int count, double scale,
+                            int limbs);
+Pt cached_pt(Context& c, const std::string& key, const double* slots, double scale, int limbs);
+Ct encrypt(Context& c, const double* slots, int level, u64 seed, OptLayout layout);
+Ct zeros(Context& c, int level);
+void decrypt(Context& c, const Ct& a, double* out);
+Ct add(Context& c, const Ct& a, const Ct& b, bool sub = false, bool count = true);
+Ct add_plain(Context& c, const Ct& a, const double* slots);
+Ct rescale(Context& c, const Ct& a);
+Ct mac_plain(Context& c, const std::vector<const Ct*>& cts, const std::vector<const Pt*>& pts, bool count = true);
+Ct mul_plain(Context& c, const Ct& a, const double* slots);
+Ct mul(Context& c, const Ct& a, const Ct& b, bool count = true);
+Ct rotate(Context& c, const Ct& a, int r, bool hoisted, bool count = true);
+std::vector<Ct> rotate_hoisted(Context& c, const Ct& a, const std::vector<int>& rs, bool count = true);
+Ct level_drop(Context& c, const Ct& a, int target);
+Ct bootstrap(Context& c, const Ct& a, int target);
+u64 galois_elt(const Context& c, int r);
+const BufPtr& get_key(Context& c, u64 g);
+void check_ct(const Context& c, const Ct& a, const char* what);
+void check_scales(const Ct& a, const Ct& b, const char* what);
+
+}  // namespace sf

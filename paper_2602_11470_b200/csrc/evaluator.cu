@@ -1,0 +1,678 @@
+// Context construction, key generation and the CKKS evaluator on one B200.
+//
+// Level / ledger semantics are the reference's (engine.hpp:102-111,
+// engine.cpp:143-214); the arithmetic is full-RNS CKKS with hybrid key
+// switching per DESIGN.md §3. Op sequences here are the spec the CPU oracle
+// (oracle/ckks_oracle.cpp) restates, which is what makes every ciphertext word
+// bit-identical between the two.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <thread>
+
+#include "context.h"
+#include "kernels.cuh"
+
+namespace sf {
+
+void build_host_tables(Context& c, std::vector<u64>& psi, std::vector<u64>& psi_s, std::vector<u64>& ipsi,
+                       std::vector<u64>& ipsi_s, std::vector<u64>& ninv, std::vector<u64>& ninv_s);
+
+// ------------------------------------------------------------------ memory
+Buf::Buf(Context* c, size_t w) : words(w), ctx(c) {
+  if (w) SF_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), w * sizeof(u64), c->stream));
+}
+Buf::~Buf() {
+  if (p) cudaFreeAsync(p, ctx->stream);
+}
+
+static BufPtr buf(Context& c, size_t words) { return std::make_shared<Buf>(&c, words); }
+
+Context::~Context() {
+  if (stream) cudaStreamSynchronize(stream);
+  keys.clear();
+  conv_plans.clear();
+  pt_cache.clear();
+  level_consts.clear();
+  sk.reset();
+  tab_store.reset();
+  for (auto e : events) cudaEventDestroy(e);
+  if (stream) {
+    cudaStreamSynchronize(stream);
+    cudaStreamDestroy(stream);
+  }
+}
+
+u64 Context::next_seed() {
+  const u64 k = enc_counter++;
+  return fmix64(seed ^ (0xE1C0000000000000ull + k));
+}
+
+std::unique_ptr<Context> make_context(int slots, int L, int log_n, int alpha, int q0_bits, int scale_bits,
+                                      int special_bits, u64 seed, int device) {
+  require(is_pow2(slots), kShapeMismatch, "engine: N must be a power of two");
+  require(L >= 1, kInvalidTarget, "engine: level budget L must be >= 1");
+  auto c = std::make_unique<Context>();
+  c->slots = slots;
+  c->L = L;
+  c->logn = log_n > 0 ? log_n : std::max(2, log2_exact(2LL * slots));
+  c->n = 1 << c->logn;
+  require(2LL * slots <= c->n, kShapeMismatch, "ckks: slot count exceeds ring degree / 2");
+  require(c->logn <= 17, kShapeMismatch, "ckks: ring degree above 2^17 not supported");
+  c->alpha = alpha > 0 ? alpha : std::min(L + 1, 5);
+  c->beta = (L + 1 + c->alpha - 1) / c->alpha;
+  c->seed = seed;
+  c->device = device;
+  c->delta = std::ldexp(1.0, scale_bits > 0 ? scale_bits : 40);
+  c->primes = generate_primes(c->logn, L, q0_bits > 0 ? q0_bits : 60, scale_bits > 0 ? scale_bits : 40, c->alpha,
+                              special_bits > 0 ? special_bits : 60);
+  c->np = (int)c->primes.size();
+  require(c->np <= 64, kShapeMismatch, "ckks: at most 64 RNS primes");
+
+  SF_CUDA(cudaSetDevice(device));
+  SF_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  SF_CUDA(cudaDeviceGetDefaultMemPool(&c->pool, device));
+  uint64_t thresh = UINT64_MAX;
+  SF_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thresh));
+
+  std::vector<u64> psi, psi_s, ipsi, ipsi_s, ninv, ninv_s;
+  build_host_tables(*c, psi, psi_s, ipsi, ipsi_s, ninv, ninv_s);
+  const size_t np = c->np, n = c->n;
+  const size_t words = 3 * np + 4 * np * n + 2 * np;
+  c->tab_store = buf(*c, words);
+  std::vector<u64> host(words);
+  u64* h = host.data();
+  size_t off = 0;
+  auto put = [&](const std::vector<u64>& v) {
+    std::memcpy(h + off, v.data(), v.size() * sizeof(u64));
+    const size_t o = off;
+    off += v.size();
+    return c->tab_store->p + o;
+  };
+  c->tabs.q = put(c->primes);
+  c->tabs.mh = put(c->mu_hi);
+  c->tabs.ml = put(c->mu_lo);
+  c->tabs.psi = put(psi);
+  c->tabs.psi_s = put(psi_s);
+  c->tabs.ipsi = put(ipsi);
+  c->tabs.ipsi_s = put(ipsi_s);
+  c->tabs.ninv = put(ninv);
+  c->tabs.ninv_s = put(ninv_s);
+  c->tabs.n = c->n;
+  c->tabs.logn = c->logn;
+  SF_CUDA(cudaMemcpyAsync(c->tab_store->p, host.data(), words * sizeof(u64), cudaMemcpyHostToDevice, c->stream));
+
+  // secret key: ternary coefficients, NTT over every prime
+  c->sk = buf(*c, np * n);
+  k_ternary(*c, c->sk->p, stream_key(seed, kStreamSk), (int)np, 0);
+  ntt_limbs(*c, c->sk->p, (int)np, 0, false);
+  SF_CUDA(cudaStreamSynchronize(c->stream));
+  return c;
+}
+
+// ------------------------------------------------------------------ helpers
+u64 galois_elt(const Context& c, int r) {
+  return powmod_h(5, (u64)pos_mod(r, c.slots), 2ull * c.n);
+}
+
+Ct alloc_ct(Context& c, int limbs, double scale) {
+  Ct r;
+  r.buf = buf(c, (size_t)2 * limbs * c.n);
+  r.limbs = limbs;
+  r.stride = limbs;
+  r.scale = scale;
+  return r;
+}
+
+static Ct view(const Ct& a, int limbs) {
+  Ct r = a;
+  r.limbs = limbs;
+  return r;
+}
+
+void check_ct(const Context& c, const Ct& a, const char* what) {
+  require(a.buf != nullptr, kInvalidTarget, std::string(what) + ": null ciphertext");
+  require(a.level() >= 0 && a.level() <= c.L, kInvalidTarget,
+          std::string(what) + ": ciphertext level " + std::to_string(a.level()) + " out of [0, L]");
+}
+
+void check_scales(const Ct& a, const Ct& b, const char* what) {
+  if (a.zero || b.zero) return;
+  if (std::fabs(a.scale / b.scale - 1.0) > 1e-9)
+    fail(kScaleMismatch, std::string("ScaleMismatch: ") + what + ": operand scales differ");
+}
+
+static OptLayout merge_layouts(const Ct& a, const Ct& b) {
+  if (a.layout && b.layout && *a.layout == *b.layout) return a.layout;
+  return std::nullopt;
+}
+
+// device constants for `limbs` active limbs: rescale (drop limb limbs-1) and
+// ModDown (P -> Q_limbs): [inv_ql, inv_ql_s, pinv, pinv_s] each `limbs` words
+static const u64* level_consts(Context& c, int limbs) {
+  std::lock_guard<std::mutex> lk(c.mu);
+  auto it = c.level_consts.find(limbs);
+  if (it != c.level_consts.end()) return it->second->p;
+  std::vector<u64> h(4 * (size_t)limbs, 0);
+  const u64 ql = c.primes[limbs - 1];
+  for (int i = 0; i < limbs; ++i) {
+    const u64 q = c.primes[i];
+    if (i < limbs - 1) {
+      h[i] = invmod_h(ql % q, q);
+      h[limbs + i] = shoup_h(h[i], q);
+    }
+    u64 pm = 1 % q;
+    for (int k = 0; k < c.alpha; ++k) pm = mulmod_h(pm, c.primes[c.P_index(k)] % q, q);
+    h[2 * limbs + i] = invmod_h(pm, q);
+    h[3 * limbs + i] = shoup_h(h[2 * limbs + i], q);
+  }
+  BufPtr b = buf(c, h.size());
+  SF_CUDA(cudaMemcpyAsync(b->p, h.data(), h.size() * sizeof(u64), cudaMemcpyHostToDevice, c.stream));
+  SF_CUDA(cudaStreamSynchronize(c.stream));  // h goes out of scope
+  c.level_consts[limbs] = b;
+  return b->p;
+}
+
+static const ConvPlan& conv_plan(Context& c, const std::vector<int>& src, const std::vector<int>& dst) {
+  std::string key;
+  for (int s : src) key += std::to_string(s) + ",";
+  key += ">";
+  for (int d : dst) key += std::to_string(d) + ",";
+  std::lock_guard<std::mutex> lk(c.mu);
+  auto it = c.conv_plans.find(key);
+  if (it != c.conv_plans.end()) return it->second;
+  ConvPlan p;
+  p.src = src;
+  p.dst = dst;
+  p.nsrc = (int)src.size();
+  p.ndst = (int)dst.size();
+  std::vector<u64> h(2 * (size_t)p.nsrc + (size_t)p.nsrc * p.ndst);
+  for (int i = 0; i < p.nsrc; ++i) {
+    const u64 qi = c.primes[src[i]];
+    u64 hat = 1 % qi;
+    for (int k = 0; k < p.nsrc; ++k)
+      if (k != i) hat = mulmod_h(hat, c.primes[src[k]] % qi, qi);
+    h[i] = invmod_h(hat, qi);
+    h[p.nsrc + i] = shoup_h(h[i], qi);
+    for (int d = 0; d < p.ndst; ++d) {
+      const u64 pd = c.primes[dst[d]];
+      u64 hm = 1 % pd;
+      for (int k = 0; k < p.nsrc; ++k)
+        if (k != i) hm = mulmod_h(hm, c.primes[src[k]] % pd, pd);
+      h[2 * p.nsrc + (size_t)i * p.ndst + d] = hm;
+    }
+  }
+  p.tab = buf(c, h.size());
+  SF_CUDA(cudaMemcpyAsync(p.tab->p, h.data(), h.size() * sizeof(u64), cudaMemcpyHostToDevice, c.stream));
+  SF_CUDA(cudaStreamSynchronize(c.stream));
+  return c.conv_plans.emplace(key, std::move(p)).first->second;
+}
+
+// upload signed coefficients and reduce into `limbs` NTT-domain limbs (+ noise)
+static BufPtr coeffs_to_ntt(Context& c, const std::vector<i64>& co, int limbs, bool noise, u64 ekey) {
+  BufPtr tmp = buf(c, (size_t)c.n);
+  SF_CUDA(cudaMemcpyAsync(tmp->p, co.data(), co.size() * sizeof(i64), cudaMemcpyHostToDevice, c.stream));
+  BufPtr out = buf(c, (size_t)limbs * c.n);
+  std::vector<int> primes(limbs);
+  for (int l = 0; l < limbs; ++l) primes[l] = l;
+  k_small_rns(c, out->p, ekey, noise, reinterpret_cast<const i64*>(tmp->p), primes.data(), limbs);
+  ntt_limbs(c, out->p, limbs, 0, false);
+  // the host vector must outlive the async copy
+  SF_CUDA(cudaStreamSynchronize(c.stream));
+  return out;
+}
+
+Pt encode_pt(Context& c, const double* slots, double scale, int limbs) {
+  Pt p;
+  p.buf = coeffs_to_ntt(c, encode_coeffs(c, slots, scale), limbs, false, 0);
+  p.limbs = limbs;
+  p.scale = scale;
+  return p;
+}
+
+Pt cached_pt(Context& c, const std::string& key, const double* slots, double scale, int limbs) {
+  const std::string k = key + "@" + std::to_string(limbs);
+  {
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto it = c.pt_cache.find(k);
+    if (it != c.pt_cache.end()) return it->second;
+  }
+  Pt p = encode_pt(c, slots, scale, limbs);
+  std::lock_guard<std::mutex> lk(c.mu);
+  c.pt_cache[k] = p;
+  return p;
+}
+
+// ------------------------------------------------------------------ client ops
+Ct encrypt(Context& c, const double* slots, int level, u64 seed, OptLayout layout) {
+  if (level < 0) level = c.L;
+  require(level <= c.L, kInvalidTarget, "encrypt: level exceeds budget L");
+  if (layout) validate_layout(*layout, c.slots);
+  const int limbs = level + 1;
+  Ct r = alloc_ct(c, limbs, c.delta);
+  r.layout = layout;
+  BufPtr em = coeffs_to_ntt(c, encode_coeffs(c, slots, c.delta), limbs, true, stream_key(seed, kStreamEncE));
+  std::vector<u64> keys(limbs);
+  std::vector<int> primes(limbs);
+  for (int l = 0; l < limbs; ++l) keys[l] = stream_key(seed, kStreamEncA | (u64)l), primes[l] = l;
+  k_sample_uniform(c, r.c1(c.n), keys.data(), primes.data(), limbs);
+  k_enc_combine(c, r.c0(), r.c1(c.n), c.sk->p, em->p, limbs);
+  return r;
+}
+
+Ct zeros(Context& c, int level) {
+  if (level < 0) level = c.L;
+  require(level <= c.L, kInvalidTarget, "zeros: level exceeds budget L");
+  Ct r = alloc_ct(c, level + 1, 0.0);
+  SF_CUDA(cudaMemsetAsync(r.buf->p, 0, r.buf->words * sizeof(u64), c.stream));
+  r.zero = true;
+  return r;
+}
+
+void decrypt(Context& c, const Ct& a, double* out) {
+  if (a.zero) {
+    std::fill(out, out + c.slots, 0.0);
+    return;
+  }
+  BufPtr mu = buf(c, c.n);
+  k_dec_combine(c, mu->p, a.c0(), a.c1(c.n), c.sk->p);
+  ntt_limbs(c, mu->p, 1, 0, true);
+  std::vector<u64> h(c.n);
+  SF_CUDA(cudaMemcpyAsync(h.data(), mu->p, c.n * sizeof(u64), cudaMemcpyDeviceToHost, c.stream));
+  SF_CUDA(cudaStreamSynchronize(c.stream));
+  const u64 q = c.primes[0];
+  std::vector<double> co(c.n);
+  for (int k = 0; k < c.n; ++k) co[k] = h[k] > q / 2 ? -(double)(q - h[k]) : (double)h[k];
+  decode_coeffs(c, co, a.scale, out);
+}
+
+// ------------------------------------------------------------------ evaluator
+Ct add(Context& c, const Ct& a, const Ct& b, bool sub, bool count) {
+  check_ct(c, a, sub ? "sub" : "add");
+  check_ct(c, b, sub ? "sub" : "add");
+  const int limbs = std::min(a.limbs, b.limbs);
+  if (count) c.ledger.add();
+  OptLayout ly = merge_layouts(a, b);
+  if (a.zero && b.zero) {
+    Ct r = view(a, limbs);
+    r.layout = ly;
+    return r;
+  }
+  check_scales(a, b, sub ? "sub" : "add");
+  if (b.zero) {  // x + 0 = x - 0 = x (exact on trivial ciphertexts)
+    Ct r = view(a, limbs);
+    r.layout = ly;
+    return r;
+  }
+  Ct r = alloc_ct(c, limbs, a.zero ? b.scale : a.scale);
+  r.layout = ly;
+  k_addsub(c, r.c0(), a.c0(), b.c0(), limbs, sub);
+  k_addsub(c, r.c1(c.n), a.c1(c.n), b.c1(c.n), limbs, sub);
+  return r;
+}
+
+Ct add_plain(Context& c, const Ct& a, const double* slots) {
+  check_ct(c, a, "add_plain");
+  require(!a.zero, kInvalidTarget, "add_plain on a trivial zero ciphertext");
+  c.ledger.add();
+  Pt p = encode_pt(c, slots, a.scale, a.limbs);
+  Ct r = alloc_ct(c, a.limbs, a.scale);
+  r.layout = a.layout;
+  k_addsub(c, r.c0(), a.c0(), p.buf->p, a.limbs, false);
+  k_copy(c, r.c1(c.n), a.c1(c.n), (size_t)a.limbs * c.n);
+  return r;
+}
+
+// divide by the top prime with rounding
+Ct rescale(Context& c, const Ct& a) {
+  const int L1 = a.limbs - 1;
+  require(L1 >= 1, kLevelUnderflow, "rescale: no prime left to drop");
+  Ct r = alloc_ct(c, L1, a.scale / (double)c.primes[L1]);
+  r.zero = a.zero;
+  r.layout = a.layout;
+  const size_t n = c.n;
+  BufPtr last = buf(c, 2 * n);
+  SF_CUDA(cudaMemcpyAsync(last->p, a.c0() + (size_t)L1 * n, n * 8, cudaMemcpyDeviceToDevice, c.stream));
+  SF_CUDA(cudaMemcpyAsync(last->p + n, a.c1(c.n) + (size_t)L1 * n, n * 8, cudaMemcpyDeviceToDevice, c.stream));
+  LimbBatch b;
+  b.count = 2;
+  b.slot[0] = 0, b.slot[1] = 1;
+  b.prime[0] = b.prime[1] = (uint8_t)L1;
+  launch_ntt(c, last->p, b, true);
+  BufPtr lift = buf(c, 2 * (size_t)L1 * n);
+  k_rescale_lift(c, lift->p, last->p, L1, L1);
+  k_rescale_lift(c, lift->p + (size_t)L1 * n, last->p + n, L1, L1);
+  LimbBatch f;
+  f.count = 2 * L1;
+  for (int i = 0; i < 2 * L1; ++i) f.slot[i] = (uint16_t)i, f.prime[i] = (uint8_t)(i % L1);
+  require(2 * L1 <= kMaxBatch, kInternal, "rescale: too many limbs");
+  launch_ntt(c, lift->p, f, false);
+  const u64* k = level_consts(c, a.limbs);
+  k_sub_scale(c, r.c0(), a.c0(), lift->p, k, k + a.limbs, nullptr, 0, L1);
+  k_sub_scale(c, r.c1(c.n), a.c1(c.n), lift->p + (size_t)L1 * n, k, k + a.limbs, nullptr, 0, L1);
+  return r;
+}
+
+Ct mac_plain(Context& c, const std::vector<const Ct*>& cts, const std::vector<const Pt*>& pts, bool count) {
+  require(!cts.empty() && cts.size() == pts.size(), kShapeMismatch, "mac_plain: term count");
+  int limbs = 1 << 30;
+  for (const Ct* x : cts) {
+    check_ct(c, *x, "mul_plain");
+    require(x->level() > 0, kLevelUnderflow, "mul_plain: no multiplicative level left");
+    limbs = std::min(limbs, x->limbs);
+  }
+  double scale = 0.0;
+  for (const Ct* x : cts)
+    if (!x->zero) {
+      if (scale == 0.0)
+        scale = x->scale;
+      else if (std::fabs(x->scale / scale - 1.0) > 1e-9)
+        fail(kScaleMismatch, "ScaleMismatch: mac_plain: operand scales differ");
+    }
+  if (count) {
+    c.ledger.ctpt((long long)cts.size());
+    c.ledger.add((long long)cts.size() - 1);
+  }
+  OptLayout ly = cts[0]->layout;
+  for (const Ct* x : cts)
+    if (!(x->layout == ly)) ly.reset();
+  if (scale == 0.0) {  // every term trivially zero
+    Ct z = zeros(c, limbs - 2);
+    z.layout = ly;
+    return z;
+  }
+  Ct acc = alloc_ct(c, limbs, scale * (double)c.primes[limbs - 1]);
+  for (size_t s = 0; s < cts.size(); s += kMaxTerms) {
+    MacTerms t;
+    t.k = 0;
+    for (size_t i = s; i < cts.size() && t.k < kMaxTerms; ++i) {
+      if (cts[i]->zero) continue;
+      require(pts[i]->limbs >= limbs, kShapeMismatch, "mac_plain: plaintext has too few limbs");
+      t.c0[t.k] = cts[i]->c0();
+      t.c1[t.k] = cts[i]->c1(c.n);
+      t.pt[t.k] = pts[i]->buf->p;
+      ++t.k;
+    }
+    if (t.k == 0) continue;
+    if (s == 0) {
+      k_mac(c, acc.c0(), acc.c1(c.n), t, limbs);
+    } else {  // chunk beyond 64 terms: accumulate into a scratch ct and add
+      Ct part = alloc_ct(c, limbs, acc.scale);
+      k_mac(c, part.c0(), part.c1(c.n), t, limbs);
+      acc = add(c, acc, part, false, false);
+    }
+  }
+  Ct r = rescale(c, acc);
+  r.scale = scale;
+  r.layout = ly;
+  return r;
+}
+
+Ct mul_plain(Context& c, const Ct& a, const double* slots) {
+  check_ct(c, a, "mul_plain");
+  require(a.level() > 0, kLevelUnderflow, "mul_plain: no multiplicative level left");
+  Pt p = encode_pt(c, slots, (double)c.primes[a.limbs - 1], a.limbs);
+  return mac_plain(c, {&a}, {&p});
+}
+
+// ---------------------------------------------------------------- key switching
+const BufPtr& get_key(Context& c, u64 g) {
+  {
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto it = c.keys.find(g);
+    if (it != c.keys.end()) return it->second;
+  }
+  const int np = c.np;
+  const size_t n = c.n;
+  BufPtr key = buf(c, (size_t)c.beta * 2 * np * n);
+  BufPtr sp = buf(c, (size_t)np * n);
+  if (g == 0)
+    k_square(c, sp->p, c.sk->p, np);
+  else
+    k_automorph(c, sp->p, c.sk->p, nullptr, g, np);
+  BufPtr e = buf(c, (size_t)np * n);
+  std::vector<int> primes(np);
+  for (int m = 0; m < np; ++m) primes[m] = m;
+  for (int j = 0; j < c.beta; ++j) {
+    const u64 tag = (g << 16) | ((u64)j << 8);
+    k_small_rns(c, e->p, stream_key(c.seed, kStreamKeyE | tag), true, nullptr, primes.data(), np);
+    ntt_limbs(c, e->p, np, 0, false);
+    u64* b = key->p + ((size_t)j * 2 + 0) * np * n;
+    u64* a = key->p + ((size_t)j * 2 + 1) * np * n;
+    std::vector<u64> keys(np), pm(np, 0);
+    const int lo = j * c.alpha, hi = std::min((j + 1) * c.alpha, c.L + 1);
+    for (int m = 0; m < np; ++m) {
+      keys[m] = stream_key(c.seed, kStreamKeyA | tag | (u64)m);
+      if (m >= lo && m < hi) {
+        const u64 q = c.primes[m];
+        u64 v = 1 % q;
+        for (int k = 0; k < c.alpha; ++k) v = mulmod_h(v, c.primes[c.P_index(k)] % q, q);
+        pm[m] = v;
+      }
+    }
+    k_sample_uniform(c, a, keys.data(), primes.data(), np);
+    k_key_combine(c, b, a, c.sk->p, e->p, sp->p, pm.data(), primes.data(), np);
+  }
+  std::lock_guard<std::mutex> lk(c.mu);
+  return c.keys.emplace(g, key).first->second;
+}
+
+// ModUp: digits of d (NTT, `limbs` limbs) extended to
+// T = Q_limbs ∪ P, NTT domain, layout [ndig][nt][n].
+struct Ext {
+  BufPtr buf;
+  int ndig = 0, nt = 0, limbs = 0;
+  std::vector<int> tprime;
+};
+
+static Ext mod_up(Context& c, const u64* d, int limbs) {
+  Ext x;
+  const size_t n = c.n;
+  x.limbs = limbs;
+  x.ndig = (limbs + c.alpha - 1) / c.alpha;
+  x.nt = limbs + c.alpha;
+  for (int t = 0; t < x.nt; ++t) x.tprime.push_back(t < limbs ? t : c.P_index(t - limbs));
+  BufPtr dcoef = buf(c, (size_t)limbs * n);
+  SF_CUDA(cudaMemcpyAsync(dcoef->p, d, (size_t)limbs * n * 8, cudaMemcpyDeviceToDevice, c.stream));
+  ntt_limbs(c, dcoef->p, limbs, 0, true);
+  x.buf = buf(c, (size_t)x.ndig * x.nt * n);
+  for (int j = 0; j < x.ndig; ++j) {
+    const int lo = j * c.alpha, hi = std::min((j + 1) * c.alpha, limbs);
+    std::vector<int> src, dst, slot;
+    for (int i = lo; i < hi; ++i) src.push_back(i);
+    for (int t = 0; t < x.nt; ++t)
+      if (t < lo || t >= hi) dst.push_back(x.tprime[t]), slot.push_back(t);
+    u64* ext = x.buf->p + (size_t)j * x.nt * n;
+    k_conv(c, conv_plan(c, src, dst), dcoef->p + (size_t)lo * n, ext, slot);
+    SF_CUDA(cudaMemcpyAsync(ext + (size_t)lo * n, d + (size_t)lo * n, (size_t)(hi - lo) * n * 8,
+                            cudaMemcpyDeviceToDevice, c.stream));
+    std::vector<std::pair<u64*, int>> todo;
+    for (size_t i = 0; i < dst.size(); ++i) todo.emplace_back(ext + (size_t)slot[i] * n, dst[i]);
+    ntt_list(c, todo, false);
+  }
+  return x;
+}
+
+// ModDown of acc (nt = limbs + alpha limbs over T, NTT) into out (limbs):
+// out = (acc_Q - conv(iNTT(acc_P))) * P^-1 (+ addend permuted by g).
+static void mod_down(Context& c, u64* acc, int limbs, u64* out, const u64* addend, u64 g) {
+  const size_t n = c.n;
+  std::vector<int> pidx, qidx;
+  for (int k = 0; k < c.alpha; ++k) pidx.push_back(c.P_index(k));
+  for (int l = 0; l < limbs; ++l) qidx.push_back(l);
+  LimbBatch b;
+  b.count = c.alpha;
+  for (int k = 0; k < c.alpha; ++k) b.slot[k] = (uint16_t)(limbs + k), b.prime[k] = (uint8_t)pidx[k];
+  launch_ntt(c, acc, b, true);
+  BufPtr conv = buf(c, (size_t)limbs * n);
+  std::vector<int> slot(qidx);
+  k_conv(c, conv_plan(c, pidx, qidx), acc + (size_t)limbs * n, conv->p, slot);
+  ntt_limbs(c, conv->p, limbs, 0, false);
+  const u64* k = level_consts(c, limbs);
+  k_sub_scale(c, out, acc, conv->p, k + 2 * limbs, k + 3 * limbs, addend, g, limbs);
+}
+
+// key switch of the ModUp'd ext under key g; c0 addend (permuted by g) folded
+// into the b-part. Writes into r.c0 / r.c1.
+static void ks_apply(Context& c, const Ext& x, u64 g, const u64* c0_addend, const u64* c1_addend, Ct& r) {
+  const BufPtr& key = get_key(c, g);
+  const size_t n = c.n;
+  BufPtr acc = buf(c, 2 * (size_t)x.nt * n);
+  k_ks_inner(c, acc->p, acc->p + (size_t)x.nt * n, x.buf->p, x.ndig, x.nt, x.tprime.data(), key->p, g);
+  mod_down(c, acc->p, x.limbs, r.c0(), c0_addend, g);
+  mod_down(c, acc->p + (size_t)x.nt * n, x.limbs, r.c1(c.n), c1_addend, g);
+}
+
+Ct rotate(Context& c, const Ct& a, int r, bool hoisted, bool count) {
+  check_ct(c, a, "rotate");
+  if (pos_mod(r, c.slots) == 0) return a;
+  if (count) c.ledger.rot(hoisted);
+  if (a.zero) {
+    Ct z = a;
+    z.layout.reset();
+    return z;
+  }
+  const u64 g = galois_elt(c, r);
+  Ext x = mod_up(c, a.c1(c.n), a.limbs);
+  Ct out = alloc_ct(c, a.limbs, a.scale);
+  ks_apply(c, x, g, a.c0(), nullptr, out);
+  return out;
+}
+
+std::vector<Ct> rotate_hoisted(Context& c, const Ct& a, const std::vector<int>& rs, bool count) {
+  check_ct(c, a, "rotate");
+  std::vector<Ct> outs(rs.size());
+  Ext x;
+  bool have = false;
+  for (size_t i = 0; i < rs.size(); ++i) {
+    if (pos_mod(rs[i], c.slots) == 0) {
+      outs[i] = a;
+      continue;
+    }
+    if (count) c.ledger.rot(true);
+    if (a.zero) {
+      outs[i] = a;
+      outs[i].layout.reset();
+      continue;
+    }
+    if (!have) x = mod_up(c, a.c1(c.n), a.limbs), have = true;
+    outs[i] = alloc_ct(c, a.limbs, a.scale);
+    ks_apply(c, x, galois_elt(c, rs[i]), a.c0(), nullptr, outs[i]);
+  }
+  return outs;
+}
+
+Ct mul(Context& c, const Ct& a, const Ct& b, bool count) {
+  check_ct(c, a, "mul");
+  check_ct(c, b, "mul");
+  const int limbs = std::min(a.limbs, b.limbs);
+  require(limbs - 1 > 0, kLevelUnderflow, "mul: no multiplicative level left");
+  if (count) c.ledger.ctct();
+  OptLayout ly = merge_layouts(a, b);
+  if (a.zero || b.zero) {
+    Ct z = zeros(c, limbs - 2);
+    z.layout = ly;
+    return z;
+  }
+  const size_t n = c.n;
+  BufPtr d = buf(c, 3 * (size_t)limbs * n);
+  u64 *d0 = d->p, *d1 = d->p + (size_t)limbs * n, *d2 = d->p + 2 * (size_t)limbs * n;
+  k_tensor(c, d0, d1, d2, a.c0(), a.c1(c.n), b.c0(), b.c1(c.n), limbs);
+  Ext x = mod_up(c, d2, limbs);
+  Ct t = alloc_ct(c, limbs, a.scale * b.scale);
+  ks_apply(c, x, 0, d0, d1, t);
+  Ct r = rescale(c, t);
+  r.layout = ly;
+  return r;
+}
+
+Ct level_drop(Context& c, const Ct& a, int target) {
+  check_ct(c, a, "level_drop");
+  require(target >= 0 && target <= a.level(), kInvalidTarget,
+          "level_drop: target level " + std::to_string(target) + " outside [0, level]");
+  return view(a, target + 1);
+}
+
+Ct bootstrap(Context& c, const Ct& a, int target) {
+  check_ct(c, a, "bootstrap");
+  require(target >= 1 && target <= c.L, kInvalidTarget,
+          "bootstrap: target level " + std::to_string(target) + " outside [1, L]");
+  c.ledger.boot();
+  std::vector<double> s(c.slots);
+  decrypt(c, a, s.data());
+  return encrypt(c, s.data(), target, c.next_seed(), a.layout);
+}
+
+}  // namespace sf
+
+namespace sf {
+
+// Batch plaintext encoder for offline plans: slot vectors are
+// synthesised and FFT-encoded on all host cores, uploaded in pinned chunks,
+// reduced into RNS limbs and NTT'd on the device.
+std::vector<Pt> encode_many(Context& c, const std::function<void(int, double*)>& gen, int count, double scale,
+                            int limbs) {
+  std::vector<Pt> out(count);
+  const int chunk = 32;
+  const size_t n = c.n;
+  i64* pinned = nullptr;
+  SF_CUDA(cudaMallocHost(reinterpret_cast<void**>(&pinned), (size_t)chunk * n * sizeof(i64)));
+  std::vector<int> primes(limbs);
+  for (int l = 0; l < limbs; ++l) primes[l] = l;
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  try {
+    for (int s = 0; s < count; s += chunk) {
+      const int m = std::min(chunk, count - s);
+      std::atomic<int> next{0};
+      std::vector<std::thread> th;
+      std::exception_ptr err;
+      std::mutex emu;
+      for (unsigned w = 0; w < std::min<unsigned>(hw, (unsigned)m); ++w)
+        th.emplace_back([&]() {
+          std::vector<double> slots(c.slots);
+          for (int i = next++; i < m; i = next++) {
+            try {
+              gen(s + i, slots.data());
+              auto co = encode_coeffs(c, slots.data(), scale);
+              std::memcpy(pinned + (size_t)i * n, co.data(), n * sizeof(i64));
+            } catch (...) {
+              std::lock_guard<std::mutex> lk(emu);
+              err = std::current_exception();
+            }
+          }
+        });
+      for (auto& t : th) t.join();
+      if (err) std::rethrow_exception(err);
+      BufPtr dev = buf(c, (size_t)m * n);
+      SF_CUDA(cudaMemcpyAsync(dev->p, pinned, (size_t)m * n * sizeof(i64), cudaMemcpyHostToDevice, c.stream));
+      BufPtr all = buf(c, (size_t)m * limbs * n);
+      for (int i = 0; i < m; ++i)
+        k_small_rns(c, all->p + (size_t)i * limbs * n, 0, false, reinterpret_cast<const i64*>(dev->p + (size_t)i * n),
+                    primes.data(), limbs);
+      std::vector<std::pair<u64*, int>> todo;
+      for (int i = 0; i < m; ++i)
+        for (int l = 0; l < limbs; ++l) todo.emplace_back(all->p + ((size_t)i * limbs + l) * n, l);
+      ntt_list(c, todo, false);
+      for (int i = 0; i < m; ++i) {
+        // split the chunk buffer into per-plaintext buffers (copy keeps ownership simple)
+        Pt p;
+        p.buf = buf(c, (size_t)limbs * n);
+        p.limbs = limbs;
+        p.scale = scale;
+        SF_CUDA(cudaMemcpyAsync(p.buf->p, all->p + (size_t)i * limbs * n, (size_t)limbs * n * 8,
+                                cudaMemcpyDeviceToDevice, c.stream));
+        out[s + i] = p;
+      }
+      SF_CUDA(cudaStreamSynchronize(c.stream));  // pinned buffer reused next chunk
+    }
+  } catch (...) {
+    cudaFreeHost(pinned);
+    throw;
+  }
+  cudaFreeHost(pinned);
+  return out;
+}
+
+}  // namespace sf

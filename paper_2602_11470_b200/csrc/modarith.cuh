@@ -1,0 +1,71 @@
+// Device modular arithmetic over 64-bit words, primes q < 2^61 (so 4q < 2^63
+// and 64 lazily accumulated products of two residues fit in 128 bits).
+//
+//  * mul_shoup:   x * w mod q for a constant w with precomputed
+//                 w' = floor(w 2^64 / q) (Shoup): 1 mul.hi + 2 mul.lo.
+//  * reduce128:   (hi:lo) mod q for any 128-bit value via Barrett with
+//                 mu = floor(2^128 / q) stored as (mu_hi, mu_lo); the quotient
+//                 estimate is the exact floor(x mu / 2^128) so the remainder is
+//                 < 3q and two conditional subtractions finish it.
+//  * mac128:      lazy 128-bit multiply-accumulate (no reduction).
+// All results leaving a kernel are canonical ([0, q)), which is what makes
+// ciphertexts bit-identical to the CPU oracle regardless of evaluation order.
+#pragma once
+#include <cstdint>
+
+namespace sf {
+
+struct U128 {
+  uint64_t lo, hi;
+};
+
+__device__ __forceinline__ void mac128(U128& acc, uint64_t a, uint64_t b) {
+  const uint64_t lo = a * b;
+  const uint64_t hi = __umul64hi(a, b);
+  // add with carry (compiles to IADD3 + IADD3.X chains)
+  asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(acc.lo), "+l"(acc.hi) : "l"(lo), "l"(hi));
+}
+
+__device__ __forceinline__ uint64_t reduce128(uint64_t hi, uint64_t lo, uint64_t q, uint64_t mh, uint64_t ml) {
+  const uint64_t t = __umul64hi(lo, ml);
+  const uint64_t a_lo = lo * mh, a_hi = __umul64hi(lo, mh);
+  const uint64_t b_lo = hi * ml, b_hi = __umul64hi(hi, ml);
+  uint64_t s = t + a_lo;
+  uint64_t c = s < a_lo;
+  s += b_lo;
+  c += s < b_lo;
+  const uint64_t qhat = hi * mh + a_hi + b_hi + c;
+  uint64_t r = lo - qhat * q;
+  r = r >= q ? r - q : r;
+  r = r >= q ? r - q : r;
+  return r;
+}
+
+// 64-bit value mod q (hi = 0 specialisation of reduce128)
+__device__ __forceinline__ uint64_t reduce64(uint64_t x, uint64_t q, uint64_t mh) {
+  const uint64_t qhat = __umul64hi(x, mh);
+  uint64_t r = x - qhat * q;
+  r = r >= q ? r - q : r;
+  r = r >= q ? r - q : r;
+  return r;
+}
+
+__device__ __forceinline__ uint64_t mulmod(uint64_t a, uint64_t b, uint64_t q, uint64_t mh, uint64_t ml) {
+  return reduce128(__umul64hi(a, b), a * b, q, mh, ml);
+}
+
+__device__ __forceinline__ uint64_t mul_shoup(uint64_t x, uint64_t w, uint64_t wp, uint64_t q) {
+  const uint64_t qh = __umul64hi(x, wp);
+  const uint64_t r = x * w - qh * q;
+  return r >= q ? r - q : r;
+}
+
+__device__ __forceinline__ uint64_t add_mod(uint64_t a, uint64_t b, uint64_t q) {
+  const uint64_t s = a + b;
+  return s >= q ? s - q : s;
+}
+__device__ __forceinline__ uint64_t sub_mod(uint64_t a, uint64_t b, uint64_t q) {
+  return a >= b ? a - b : a + q - b;
+}
+
+}  // namespace sf

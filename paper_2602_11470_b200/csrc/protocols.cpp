@@ -1,0 +1,384 @@
+// Packed HE-VMM and KV-cache attention over the GPU evaluator.
+//
+// The op sequences restate the reference algorithms (file:line cited per
+// function) and charge the ledger exactly as the reference does; the CKKS
+// arithmetic underneath is bit-identical to the CPU oracle running the same
+// sequence (oracle/protocols.py over oracle/ckks.py).
+#include "protocols.h"
+
+#include <cmath>
+
+namespace sf {
+
+// ============================================================== VMM (vmm.cpp)
+
+BsgsSplit bsgs_split(long long k) {  // vmm.cpp:10-28
+  require(k >= 1, kShapeMismatch, "bsgs_split: k must be >= 1");
+  long long b = (long long)std::sqrt((double)k);
+  while (b * b < k) ++b;
+  while (b > 1 && (b - 1) * (b - 1) >= k) --b;
+  return {(int)b, (int)((k + b - 1) / b)};
+}
+
+VmmShape vmm_shape(int N, int rows, int cols, int tau_in, int tau_out) {  // vmm.cpp:135-153
+  VmmShape s;
+  s.N = N;
+  s.d_in = padded_dim(rows);
+  s.d_out = padded_dim(cols);
+  require(s.d_in <= N && s.d_out <= N, kShapeMismatch, "vmm_interleaved: padded dimension exceeds N");
+  s.t_in = N / s.d_in;
+  s.t_out = N / s.d_out;
+  s.k = std::max<long long>((long long)s.d_in * s.d_out / N, 1);
+  s.alpha_up = std::max(1, s.t_out / s.t_in);
+  s.ladder_T = std::max(s.t_in, s.t_out);
+  require(tau_in >= 0 && tau_in < s.t_in, kShapeMismatch, "vmm_interleaved: input offset out of range");
+  require(tau_out >= 0 && tau_out < s.t_out, kShapeMismatch, "vmm_interleaved: output offset out of range");
+  s.tau_in = tau_in;
+  s.tau_out = tau_out;
+  s.tau_u = tau_in % s.t_out;
+  s.carry = tau_out < s.tau_u ? 1 : 0;
+  s.delta = (int)pos_mod(tau_out - s.tau_u, s.t_out);
+  return s;
+}
+
+void predict_interleaved_cost(int N, int rows, int cols, bool bsgs, bool mask, long long* rot, long long* ctpt,
+                              int* depth) {  // vmm.cpp:473-488
+  const int d_in = padded_dim(rows), d_out = padded_dim(cols);
+  const long long k = std::max<long long>((long long)d_in * d_out / N, 1);
+  long long r = log2_exact(N / d_in) + log2_exact(N / d_out);
+  if (bsgs) {
+    const auto bg = bsgs_split(k);
+    r += (bg.baby - 1) + (bg.giant - 1);
+  } else {
+    r += k - 1;
+  }
+  *rot = r;
+  *ctpt = k + (mask ? 1 : 0);
+  *depth = 1 + (mask ? 1 : 0);
+}
+
+// Generalised interleaved diagonal g at slot j of the pre-giant frame
+// (vmm.cpp:159-168; Appendix B).
+static double diag_value(const VmmShape& s, const std::function<double(int, int)>& w, long long g, long long j) {
+  const long long N = s.N;
+  const long long i0 = pos_mod(j + g * s.t_in * s.t_out - s.tau_in, N);
+  const int row = (int)((i0 / s.t_in + (i0 % s.t_in) * s.alpha_up) % s.d_in);
+  const long long rel = pos_mod(j - s.tau_u, N);
+  const long long u = rel % s.t_out;
+  const long long within = u / s.t_in + (u % s.t_in) * s.alpha_up;
+  if (g * s.t_out + within >= s.d_in) return 0.0;
+  const int col = (int)((rel / s.t_out + s.carry) % s.d_out);
+  return w(row, col);
+}
+
+const std::vector<Pt>& VmmPlan::diagonals(int limbs) {
+  auto it = pts.find(limbs);
+  if (it != pts.end()) return it->second;
+  Context& c = *ctx;
+  const long long unit = (long long)s.t_in * s.t_out;
+  const double scale = (double)c.primes[limbs - 1];  // scale-preserving ct-pt
+  auto gen = [&](int g, double* slots) {
+    // BSGS diagonals are pre-shifted by their giant step (vmm.cpp:170-175, 217)
+    const long long shift = bsgs ? (long long)(g / bg.baby) * bg.baby * unit : 0;
+    for (int i = 0; i < s.N; ++i) slots[i] = diag_value(s, w, g, pos_mod(i - shift, s.N));
+  };
+  return pts.emplace(limbs, encode_many(c, gen, (int)s.k, scale, limbs)).first->second;
+}
+
+std::unique_ptr<VmmPlan> make_vmm_plan(Context& c, const double* W, int rows, int cols, int level, int in_offset,
+                                       int out_offset, bool bsgs) {
+  require(rows > 0 && cols > 0, kShapeMismatch, "vmm plan: empty weight");
+  require(level >= 1 && level <= c.L, kInvalidTarget, "vmm plan: level must be in [1, L]");
+  auto p = std::make_unique<VmmPlan>();
+  p->ctx = &c;
+  p->rows = rows;
+  p->cols = cols;
+  p->level = level;
+  p->bsgs = bsgs;
+  p->s = vmm_shape(c.slots, rows, cols, in_offset, out_offset);
+  p->bg = bsgs ? bsgs_split(p->s.k) : BsgsSplit{1, (int)p->s.k};
+  if (W) {
+    p->w_store.assign(W, W + (size_t)rows * cols);
+    const double* d = p->w_store.data();
+    p->w = [d, rows, cols](int r, int cc) { return (r < rows && cc < cols) ? d[(size_t)r * cols + cc] : 0.0; };
+  } else {  // slotforge_cli.cpp:88-92 bench weight
+    p->w = [rows, cols](int r, int cc) {
+      return (r < rows && cc < cols) ? std::sin(0.001 * ((double)r * 31.0 + cc) + 0.25) : 0.0;
+    };
+  }
+  p->diagonals(level + 1);
+  return p;
+}
+
+// vmm.cpp:179-236 with the giant-step partial sums evaluated as one lazy MAC
+// each (sum of ct (.) pt, a single rescale), the babies sharing one ModUp.
+Ct vmm_interleaved(Context& c, const Ct& x, VmmPlan& plan, bool mask_output) {
+  require(x.layout && x.layout->kind == LayoutKind::Interleaved, kLayoutMismatch,
+          "vmm_interleaved: input must carry an interleaved layout");
+  require(!x.layout->deferred_mask, kLayoutMismatch,
+          "vmm_interleaved: mask (or fuse) deferred garbage before feeding a VMM");
+  require(x.layout->offset == plan.s.tau_in, kLayoutMismatch, "vmm_interleaved: input offset differs from the plan");
+  require(x.layout->d == plan.s.d_in, kShapeMismatch,
+          "vmm_interleaved: layout d=" + std::to_string(x.layout->d) + " but weights want " +
+              std::to_string(plan.s.d_in));
+  check_ct(c, x, "vmm_interleaved");
+  require(x.level() > 0, kLevelUnderflow, "mul_plain: no multiplicative level left");
+  const VmmShape& s = plan.s;
+  const std::vector<Pt>& diag = plan.diagonals(x.limbs);
+  // 1. ladder
+  Ct stair = x;
+  for (int step = 1; step < s.t_in; step <<= 1) stair = add(c, stair, rotate(c, stair, step * (s.ladder_T - 1), false));
+  const long long unit = (long long)s.t_in * s.t_out;
+  Ct acc;
+  if (!plan.bsgs) {
+    std::vector<Ct> xs;
+    xs.reserve(s.k);
+    for (long long g = 0; g < s.k; ++g) xs.push_back(rotate(c, stair, (int)(g * unit), false));
+    std::vector<const Ct*> cts;
+    std::vector<const Pt*> pts;
+    for (long long g = 0; g < s.k; ++g) cts.push_back(&xs[g]), pts.push_back(&diag[g]);
+    acc = mac_plain(c, cts, pts);
+  } else {
+    const int b = plan.bg.baby, giants = plan.bg.giant;
+    std::vector<int> rs;
+    for (int g1 = 1; g1 < b; ++g1) rs.push_back((int)(g1 * unit));
+    std::vector<Ct> baby{stair};
+    for (Ct& r : rotate_hoisted(c, stair, rs)) baby.push_back(std::move(r));
+    for (int g2 = 0; g2 < giants; ++g2) {
+      const long long shift = (long long)g2 * b * unit;
+      std::vector<const Ct*> cts;
+      std::vector<const Pt*> pts;
+      for (int g1 = 0; g1 < b; ++g1) {
+        const long long g = (long long)g2 * b + g1;
+        if (g >= s.k) break;
+        cts.push_back(&baby[g1]);
+        pts.push_back(&diag[g]);
+      }
+      Ct aligned = rotate(c, mac_plain(c, cts, pts), (int)shift, false);
+      acc = g2 == 0 ? aligned : add(c, acc, aligned);
+    }
+  }
+  // 3. reduce
+  for (int m = 0; (1 << m) < s.t_out; ++m) {
+    const int st = 1 << m;
+    acc = add(c, acc, rotate(c, acc, ((s.delta >> m) & 1) ? -st : st, false));
+  }
+  // 4. mask or defer
+  if (mask_output) {
+    std::vector<double> mk(c.slots, 0.0);
+    for (int i = s.tau_out; i < c.slots; i += s.t_out) mk[i] = 1.0;
+    acc = mul_plain(c, acc, mk.data());
+  }
+  acc.layout = Layout{LayoutKind::Interleaved, s.d_out, s.t_out, s.tau_out, 1, !mask_output};
+  return acc;
+}
+
+// ======================================================= attention (kv_attention.cpp)
+
+void validate_attention_config(const AttnCfg& cfg, int N_backend) {  // kv_attention.cpp:80-88
+  require(cfg.N == N_backend, kShapeMismatch,
+          "attention config N " + std::to_string(cfg.N) + " != backend slot count " + std::to_string(N_backend));
+  require(is_pow2(cfg.N) && is_pow2(cfg.d) && is_pow2(cfg.H), kShapeMismatch,
+          "attention config: N, d and H must be powers of two");
+  require(cfg.H <= cfg.d && cfg.d <= cfg.N, kShapeMismatch, "attention config: need H <= d <= N");
+  require(cfg.n0 >= 0 && cfg.n_max >= std::max(cfg.n0, 1), kShapeMismatch,
+          "attention config: need 0 <= n0 <= n_max, n_max >= 1");
+}
+
+int v_variant_count(const AttnCfg& cfg) { return cfg.H == 1 ? cfg.d_head() : 2 * cfg.d_head() - 1; }
+int v_variant_index(const AttnCfg& cfg, int w) {
+  const int dh = cfg.d_head();
+  if (cfg.H == 1) {
+    require(w >= 0 && w < dh, kShapeMismatch, "v_variant_index: merged variant out of range");
+    return w;
+  }
+  require(w > -dh && w < dh, kShapeMismatch, "v_variant_index: variant out of range");
+  return w + dh - 1;
+}
+int v_variant_of(const AttnCfg& cfg, int e, int u_local) {
+  const int raw = e - u_local / cfg.t();
+  return cfg.H == 1 ? (int)pos_mod(raw, cfg.d_head()) : raw;
+}
+
+static void require_clean_interleaved(const Ct& x, const AttnCfg& cfg, int offset, const char* who) {
+  require(x.layout && x.layout->kind == LayoutKind::Interleaved, kLayoutMismatch,
+          std::string(who) + ": input must carry an interleaved layout");
+  require(x.layout->d == cfg.d, kShapeMismatch, std::string(who) + ": layout width mismatch");
+  require(x.layout->offset == offset, kLayoutMismatch,
+          std::string(who) + ": expected slot offset " + std::to_string(offset) + ", got " +
+              std::to_string(x.layout->offset));
+  require(!x.layout->deferred_mask, kLayoutMismatch, std::string(who) + ": input garbage must be cleared first");
+}
+
+static std::vector<double> valid_mask(const Layout& ly, int N) {  // vmm.cpp:45-56
+  std::vector<double> m(N, 0.0);
+  switch (ly.kind) {
+    case LayoutKind::Interleaved:
+      for (int i = ly.offset; i < N; i += ly.t) m[i] = 1.0;
+      break;
+    case LayoutKind::Contiguous:
+      for (int i = 0; i < ly.d; ++i) m[i] = 1.0;
+      break;
+    case LayoutKind::Replicated:
+      std::fill(m.begin(), m.end(), 1.0);
+      break;
+  }
+  return m;
+}
+
+// fused_extract, Rope successor (vmm.cpp:85-100) via rope_apply
+// (kv_attention.cpp:111-117): y = x.p0 + Rot(x.p1, -s) + Rot(x.p2, s), s = t.
+Ct rope_apply(Context& c, const Ct& x, const AttnCfg& cfg, long long position, double base) {
+  require(x.layout && x.layout->kind == LayoutKind::Interleaved && x.layout->d == cfg.d, kLayoutMismatch,
+          "rope_apply: input must be interleaved at the configured width");
+  const Layout ly = *x.layout;
+  const int dh = cfg.d_head(), N = c.slots;
+  require(dh > 0 && dh % 2 == 0, kShapeMismatch, "rope_plaintexts: d_head must be positive and even");
+  std::vector<double> p0(N, 0.0), p1(N, 0.0), p2(N, 0.0);
+  for (int e = 0; e < ly.d; ++e) {  // vmm.cpp:66-83
+    const int pair = (e % dh) / 2;
+    const double angle = (double)position * std::pow(base, -2.0 * pair / (double)dh);
+    const int i = e * ly.t + ly.offset;
+    p0[i] = std::cos(angle);
+    if (e % 2 == 0)
+      p1[i] = std::sin(angle);
+    else
+      p2[i] = -std::sin(angle);
+  }
+  const int s = cfg.t();
+  Ct y = mul_plain(c, x, p0.data());
+  y = add(c, y, rotate(c, mul_plain(c, x, p1.data()), -s, false));
+  y = add(c, y, rotate(c, mul_plain(c, x, p2.data()), s, false));
+  Layout out = ly;
+  out.deferred_mask = false;
+  y.layout = out;
+  return y;
+}
+
+Ct fused_extract_mask(Context& c, const Ct& x, const double* coeff) {  // vmm.cpp:102-108
+  require(x.layout.has_value(), kLayoutMismatch, "fused_extract: input must carry a layout");
+  std::vector<double> m = valid_mask(*x.layout, c.slots);
+  if (coeff)
+    for (int i = 0; i < c.slots; ++i) m[i] *= coeff[i];
+  Ct y = mul_plain(c, x, m.data());
+  Layout out = *x.layout;
+  out.deferred_mask = false;
+  y.layout = out;
+  return y;
+}
+
+KV k_append(Context& c, const KV& cache, const Ct& k_new) {  // kv_attention.cpp:131-143
+  require(cache.n_prime < cache.cfg.n_max, kCacheFull, "k_append: cache at capacity");
+  const int t = cache.cfg.t();
+  require_clean_interleaved(k_new, cache.cfg, cache.n_prime % t, "k_append");
+  KV out = cache;
+  if (cache.n_prime % t == 0)
+    out.k.push_back(k_new);
+  else
+    out.k.back() = add(c, out.k.back(), k_new);
+  out.n_prime = cache.n_prime + 1;
+  return out;
+}
+
+std::vector<Ct> make_v_pieces(Context& c, const KV& cache, const Ct& v_open, int position) {  // :145-163
+  const AttnCfg& cfg = cache.cfg;
+  require(position >= 0 && position < cfg.n_max, kShapeMismatch, "make_v_pieces: position outside cache capacity");
+  require(v_open.layout && v_open.layout->kind == LayoutKind::Interleaved && v_open.layout->d == cfg.d,
+          kLayoutMismatch, "make_v_pieces: input must be interleaved at the configured width");
+  const int t = cfg.t(), dh = cfg.d_head(), j0 = position % t;
+  require(v_open.layout->offset == j0, kLayoutMismatch,
+          "make_v_pieces: value ct offset does not match the token position");
+  std::vector<Ct> parts;
+  parts.reserve(dh);
+  std::vector<double> m(c.slots);
+  for (int e = 0; e < dh; ++e) {
+    std::fill(m.begin(), m.end(), 0.0);
+    for (int h = 0; h < cfg.H; ++h) m[(h * dh + e) * t + j0] = 1.0;
+    parts.push_back(fused_extract_mask(c, v_open, m.data()));
+  }
+  return parts;
+}
+
+KV v_append(Context& c, const KV& cache, const std::vector<Ct>& parts) {  // kv_attention.cpp:165-182
+  const AttnCfg& cfg = cache.cfg;
+  require(cache.n_prime < cfg.n_max, kCacheFull, "v_append: cache at capacity");
+  const int dh = cfg.d_head();
+  require((int)parts.size() == dh, kShapeMismatch,
+          "v_append: expected d/H pieces, got " + std::to_string(parts.size()));
+  const int gt = cfg.group_tokens();
+  const int g = cache.n_prime / gt;
+  const int u_local = cache.n_prime - g * gt;
+  KV out = cache;
+  if (g == (int)out.v.size()) out.v.emplace_back(v_variant_count(cfg), zeros(c, -1));
+  for (int e = 0; e < dh; ++e) {
+    const int idx = v_variant_index(cfg, v_variant_of(cfg, e, u_local));
+    out.v[g][idx] = add(c, out.v[g][idx], parts[e]);
+  }
+  return out;
+}
+
+static int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+std::vector<Ct> qk_dot(Context& c, const Ct& q, const KV& cache) {  // kv_attention.cpp:184-214
+  const AttnCfg& cfg = cache.cfg;
+  require(cache.n_prime != 0, kCacheEmpty, "qk_dot: no cached keys");
+  require_clean_interleaved(q, cfg, 0, "qk_dot");
+  const int t = cfg.t(), dh = cfg.d_head(), gt = cfg.group_tokens(), N = cfg.N;
+  require((int)cache.k.size() == ceil_div(cache.n_prime, t), kShapeMismatch,
+          "qk_dot: key ct count does not match n_prime");
+  // replicate_lanes (30-34)
+  Ct q_rep = q;
+  for (int step = 1; step < t; step <<= 1) q_rep = add(c, q_rep, rotate(c, q_rep, -step, false));
+  // ReplicateExtract head mask (layouts.cpp:134-138)
+  std::vector<double> head_mask(N, 0.0);
+  const int hb = N / cfg.H;
+  for (int h = 0; h < cfg.H; ++h)
+    for (int i = 0; i < t; ++i) head_mask[h * hb + i] = 1.0;
+  std::vector<std::optional<Ct>> maps(ceil_div(cache.n_prime, gt));
+  for (int j = 0; j < (int)cache.k.size(); ++j) {
+    Ct prod = mul(c, q_rep, cache.k[j]);
+    for (int l = 0; (1 << l) < dh; ++l) prod = add(c, prod, rotate(c, prod, (1 << l) * t, false));  // 38-41
+    Ct masked = mul_plain(c, prod, head_mask.data());
+    const int local = (j * t) % gt;
+    Ct packed = local ? rotate(c, masked, -local, false) : masked;
+    auto& slot = maps[(j * t) / gt];
+    slot = slot ? add(c, *slot, packed) : packed;
+  }
+  std::vector<Ct> out;
+  for (auto& m : maps) {
+    m->layout.reset();
+    out.push_back(*m);
+  }
+  return out;
+}
+
+Ct softmax_times_v(Context& c, const std::vector<Ct>& probs, const KV& cache) {  // kv_attention.cpp:216-241
+  const AttnCfg& cfg = cache.cfg;
+  require(cache.n_prime != 0, kCacheEmpty, "softmax_times_v: no cached values");
+  const int t = cfg.t(), gt = cfg.group_tokens();
+  const int n_maps = ceil_div(cache.n_prime, gt);
+  require((int)probs.size() == n_maps, kShapeMismatch,
+          "softmax_times_v: expected " + std::to_string(n_maps) + " probability maps, got " +
+              std::to_string(probs.size()));
+  require((int)cache.v.size() >= n_maps, kShapeMismatch, "softmax_times_v: value cache is missing groups");
+  std::optional<Ct> acc;
+  for (int g = 0; g < n_maps; ++g) {
+    const int tokens = std::min(gt, cache.n_prime - g * gt);
+    const int u_max = (tokens - 1) / t;  // touched_variants (53-57)
+    const int w_lo = cfg.H == 1 ? 0 : -u_max, w_hi = cfg.d_head();
+    for (int w = w_lo; w < w_hi; ++w) {
+      Ct scores = w ? rotate(c, probs[g], -w * t, false) : probs[g];
+      Ct prod = mul(c, scores, cache.v[g][v_variant_index(cfg, w)]);
+      acc = acc ? add(c, *acc, prod) : prod;
+    }
+  }
+  Ct folded = *acc;
+  for (int step = 1; step < t; step <<= 1) folded = add(c, folded, rotate(c, folded, step, false));  // 44-47
+  std::vector<double> sm(cfg.N, 0.0);
+  for (int i = 0; i < cfg.N; i += t) sm[i] = 1.0;
+  Ct out = mul_plain(c, folded, sm.data());
+  out.layout = make_interleaved(cfg.d, cfg.N, 0, cfg.H);
+  return out;
+}
+
+}  // namespace sf

@@ -1,0 +1,68 @@
+// Hot-path protocols over the GPU evaluator: the packed HE-VMM
+// (vmm.hpp:74-75 / vmm.cpp:179-236) and the KV-cache attention decode step
+// (kv_attention.hpp:32-109 / kv_attention.cpp:80-241).
+#pragma once
+#include <functional>
+
+#include "context.h"
+
+namespace sf {
+
+// vmm.cpp:124-153 (InterleavedShape)
+struct VmmShape {
+  int N = 0, d_in = 0, d_out = 0, t_in = 0, t_out = 0;
+  long long k = 0;
+  int alpha_up = 0, ladder_T = 0, tau_in = 0, tau_out = 0, tau_u = 0, carry = 0, delta = 0;
+};
+VmmShape vmm_shape(int N, int rows, int cols, int tau_in, int tau_out);
+struct BsgsSplit {
+  int baby, giant;
+};
+BsgsSplit bsgs_split(long long k);
+void predict_interleaved_cost(int N, int rows, int cols, bool bsgs, bool mask, long long* rot, long long* ctpt,
+                              int* depth);
+
+struct VmmPlan {
+  Context* ctx = nullptr;
+  int rows = 0, cols = 0, level = 0;
+  bool bsgs = false;
+  VmmShape s;
+  BsgsSplit bg{1, 1};
+  std::function<double(int, int)> w;  // weight_at (vmm.cpp:17-19 semantics: 0 outside)
+  std::vector<double> w_store;
+  std::map<int, std::vector<Pt>> pts;  // limbs -> k diagonals (NTT, scale q_top)
+  const std::vector<Pt>& diagonals(int limbs);
+};
+
+std::unique_ptr<VmmPlan> make_vmm_plan(Context& c, const double* W, int rows, int cols, int level, int in_offset,
+                                       int out_offset, bool bsgs);
+Ct vmm_interleaved(Context& c, const Ct& x, VmmPlan& plan, bool mask_output);
+
+// --- attention ---------------------------------------------------------------
+struct AttnCfg {
+  int N = 0, d = 0, H = 1, n0 = 0, n_max = 0;
+  int d_head() const { return d / H; }
+  int t() const { return N / d; }
+  int group_tokens() const { return N / H; }
+};
+void validate_attention_config(const AttnCfg& cfg, int N_backend);
+
+struct KV {
+  AttnCfg cfg;
+  int n_prime = 0;
+  std::vector<Ct> k;
+  std::vector<std::vector<Ct>> v;  // [group][variant]
+};
+int v_variant_count(const AttnCfg& cfg);
+int v_variant_index(const AttnCfg& cfg, int w);
+int v_variant_of(const AttnCfg& cfg, int e, int u_local);
+
+Ct rope_apply(Context& c, const Ct& x, const AttnCfg& cfg, long long position, double base);
+Ct fused_extract_mask(Context& c, const Ct& x, const double* coeff);
+KV k_append(Context& c, const KV& cache, const Ct& k_new);
+std::vector<Ct> make_v_pieces(Context& c, const KV& cache, const Ct& v_open, int position);
+KV v_append(Context& c, const KV& cache, const std::vector<Ct>& parts);
+std::vector<Ct> qk_dot(Context& c, const Ct& q, const KV& cache);
+Ct softmax_times_v(Context& c, const std::vector<Ct>& probs, const KV& cache);
+
+}  // namespace sf
