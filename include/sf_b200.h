@@ -195,6 +195,16 @@ sf_status sf_event_elapsed_ms(sf_context* ctx, int slot_begin, int slot_end, flo
 /* number of kernels this context has launched since creation */
 long long sf_kernel_launches(const sf_context* ctx);
 
+/* Per-kernel-family live timing: between begin and end, every launch of a
+ * family whose bit is set in `mask` is bracketed by CUDA events on the context
+ * stream and charged its algorithmic bytes. Families:
+ * 0 NTT (both passes of one batched transform), 1 key-switch inner product,
+ * 2 ct x pt multiply-accumulate, 3 basis conversion, 4 other elementwise,
+ * 5 sampling. end() synchronises and fills SF_PROF_FAMILIES entries. */
+#define SF_PROF_FAMILIES 6
+sf_status sf_profile_begin(sf_context* ctx, int mask);
+sf_status sf_profile_end(sf_context* ctx, double* ms, double* bytes, long long* launches);
+
 #ifdef __cplusplus
 }
 #endif

@@ -93,6 +93,8 @@ SIGNATURES = {
     "sf_event_record": (st, [vp, C.c_int]),
     "sf_event_elapsed_ms": (st, [vp, C.c_int, C.c_int, C.POINTER(C.c_float)]),
     "sf_kernel_launches": (C.c_longlong, [vp]),
+    "sf_profile_begin": (st, [vp, C.c_int]),
+    "sf_profile_end": (st, [vp, dp, dp, C.POINTER(C.c_longlong)]),
 }
 
 _lib = None

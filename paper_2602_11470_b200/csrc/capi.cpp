@@ -475,4 +475,32 @@ sf_status sf_event_elapsed_ms(sf_context* ctx, int a, int b, float* ms) {
 }
 long long sf_kernel_launches(const sf_context* ctx) { return ctx->c->launches.load(); }
 
+sf_status sf_profile_begin(sf_context* ctx, int mask) {
+  return guard([&] {
+    auto& c = *ctx->c;
+    SF_CUDA(cudaStreamSynchronize(c.stream));
+    c.prof_recs.clear();
+    c.prof_pool_next = 0;
+    c.prof_mask = mask;
+  });
+}
+
+sf_status sf_profile_end(sf_context* ctx, double* ms, double* bytes, long long* launches) {
+  return guard([&] {
+    auto& c = *ctx->c;
+    c.prof_mask = 0;
+    SF_CUDA(cudaStreamSynchronize(c.stream));
+    for (int f = 0; f < SF_PROF_FAMILIES; ++f) ms[f] = 0.0, bytes[f] = 0.0, launches[f] = 0;
+    for (const auto& r : c.prof_recs) {
+      float t = 0.f;
+      SF_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+      ms[r.family] += t;
+      bytes[r.family] += r.bytes;
+      launches[r.family] += 1;
+    }
+    c.prof_recs.clear();
+    c.prof_pool_next = 0;
+  });
+}
+
 }  // extern "C"

@@ -125,7 +125,21 @@ struct LimbBatch {
   uint8_t prime[kMaxBatch];
 };
 
+// Live per-family kernel timing (sf_profile_begin / end).
+enum Family : int { kFamNtt = 0, kFamKs = 1, kFamMac = 2, kFamConv = 3, kFamElem = 4, kFamSample = 5, kFamCount = 6 };
+struct ProfRec {
+  int family;
+  cudaEvent_t a, b;
+  double bytes;
+};
+
 struct Context {
+  // profiling
+  int prof_mask = 0;
+  std::vector<ProfRec> prof_recs;
+  std::vector<cudaEvent_t> prof_pool;
+  size_t prof_pool_next = 0;
+
   // parameters
   int logn = 0, n = 0, slots = 0, L = 0, alpha = 0, beta = 0, np = 0;
   double delta = 0.0;
@@ -161,6 +175,17 @@ struct Context {
 
   int P_index(int k) const { return L + 1 + k; }
   u64 next_seed();  // DESIGN.md §3.4 auto seed
+};
+
+// RAII bracket for one profiled launch (no-op unless the family is enabled).
+struct ProfScope {
+  Context& c;
+  int fam;
+  double bytes;
+  bool on;
+  cudaEvent_t b{};
+  ProfScope(Context& ctx, int family, double algorithmic_bytes);
+  ~ProfScope();
 };
 
 // --- construction ------------------------------------------------------------

@@ -19,6 +19,27 @@ void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) fail(kCuda, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+static cudaEvent_t prof_event(Context& c) {
+  if (c.prof_pool_next == c.prof_pool.size()) {
+    cudaEvent_t e;
+    SF_CUDA(cudaEventCreate(&e));
+    c.prof_pool.push_back(e);
+  }
+  return c.prof_pool[c.prof_pool_next++];
+}
+
+ProfScope::ProfScope(Context& ctx, int family, double algorithmic_bytes)
+    : c(ctx), fam(family), bytes(algorithmic_bytes), on(((ctx.prof_mask >> family) & 1) != 0) {
+  if (!on) return;
+  cudaEvent_t a = prof_event(c);
+  b = prof_event(c);
+  SF_CUDA(cudaEventRecord(a, c.stream));
+  c.prof_recs.push_back({fam, a, b, bytes});
+}
+ProfScope::~ProfScope() {
+  if (on) cudaEventRecord(b, c.stream);
+}
+
 namespace {
 
 constexpr int kThreads = 256;
@@ -482,6 +503,7 @@ const u64* QP(Context& c) { return c.tabs.q; }
 void launch_ntt(Context& c, u64* base, const LimbBatch& b, bool inverse) {
   if (b.count == 0) return;
   const int n = c.n, logn = c.logn;
+  ProfScope prof(c, kFamNtt, 16.0 * n * b.count);
   if (n <= 4096) {
     const int th = std::min(512, std::max(32, n / 2));
     const size_t sm = (size_t)n * sizeof(u64);
@@ -553,17 +575,20 @@ void ntt_list(Context& c, const std::vector<std::pair<u64*, int>>& limbs, bool i
 
 void k_addsub(Context& c, u64* out, const u64* a, const u64* b, int limbs, bool sub) {
   const size_t w = (size_t)limbs * c.n / 2;
+  ProfScope prof(c, kFamElem, 24.0 * limbs * c.n);
   addsub_kernel<<<grid_cap(w), kThreads, 0, c.stream>>>(out, a, b, limbs, c.n, QP(c), sub);
   post_launch(c);
 }
 
 void k_copy(Context& c, u64* out, const u64* in, size_t words) {
+  ProfScope prof(c, kFamElem, 16.0 * words);
   copy_kernel<<<grid_cap(words / 2), kThreads, 0, c.stream>>>(out, in, words);
   post_launch(c);
 }
 
 void k_mac(Context& c, u64* out0, u64* out1, const MacTerms& t, int limbs) {
   const size_t w = (size_t)limbs * c.n;
+  ProfScope prof(c, kFamMac, 8.0 * c.n * limbs * (3.0 * t.k + 2));
   mac_kernel<<<grid_cap(w), kThreads, 0, c.stream>>>(out0, out1, t, limbs, c.n, QP(c), c.tabs.mh, c.tabs.ml);
   post_launch(c);
 }
@@ -571,6 +596,7 @@ void k_mac(Context& c, u64* out0, u64* out1, const MacTerms& t, int limbs) {
 void k_tensor(Context& c, u64* d0, u64* d1, u64* d2, const u64* a0, const u64* a1, const u64* b0, const u64* b1,
               int limbs) {
   const size_t w = (size_t)limbs * c.n;
+  ProfScope prof(c, kFamElem, 56.0 * limbs * c.n);
   tensor_kernel<<<grid_cap(w), kThreads, 0, c.stream>>>(d0, d1, d2, a0, a1, b0, b1, limbs, c.n, QP(c), c.tabs.mh,
                                                         c.tabs.ml);
   post_launch(c);
@@ -578,6 +604,7 @@ void k_tensor(Context& c, u64* d0, u64* d1, u64* d2, const u64* a0, const u64* a
 
 void k_hadamard(Context& c, u64* out, const u64* a, const u64* b, int limbs, int first_prime) {
   const size_t w = (size_t)limbs * c.n;
+  ProfScope prof(c, kFamElem, 24.0 * limbs * c.n);
   hadamard_kernel<<<grid_cap(w), kThreads, 0, c.stream>>>(out, a, b, limbs, c.n, QP(c) + first_prime,
                                                           c.tabs.mh + first_prime, c.tabs.ml + first_prime);
   post_launch(c);
@@ -585,6 +612,7 @@ void k_hadamard(Context& c, u64* out, const u64* a, const u64* b, int limbs, int
 
 void k_automorph(Context& c, u64* out, const u64* in, const u64* add, u64 g, int limbs) {
   const size_t w = (size_t)limbs * c.n;
+  ProfScope prof(c, kFamElem, (add ? 24.0 : 16.0) * limbs * c.n);
   automorph_kernel<<<grid_cap(w), kThreads, 0, c.stream>>>(out, in, add, g, limbs, c.logn, QP(c));
   post_launch(c);
 }
@@ -603,6 +631,7 @@ void k_conv(Context& c, const ConvPlan& p, const u64* in, u64* out, const std::v
     A.dst_prime[d] = p.dst[d];
     A.out_slot[d] = out_slot[d];
   }
+  ProfScope prof(c, kFamConv, 8.0 * c.n * (p.nsrc + p.ndst));
   conv_kernel<<<grid_cap(c.n), kThreads, 0, c.stream>>>(A, in, out, QP(c), c.tabs.mh, c.tabs.ml);
   post_launch(c);
 }
@@ -618,6 +647,7 @@ void k_ks_inner(Context& c, u64* accb, u64* acca, const u64* ext, int ndig, int 
   A.g = g;
   for (int t = 0; t < nt; ++t) A.tprime[t] = tprime[t];
   const size_t w = (size_t)nt * c.n;
+  ProfScope prof(c, kFamKs, 8.0 * c.n * ((double)ndig * nt * 3 + 2.0 * nt));
   ks_inner_kernel<<<grid_cap(w), kThreads, 0, c.stream>>>(accb, acca, ext, key, A, QP(c), c.tabs.mh, c.tabs.ml);
   post_launch(c);
 }
@@ -625,6 +655,7 @@ void k_ks_inner(Context& c, u64* accb, u64* acca, const u64* ext, int ndig, int 
 void k_sub_scale(Context& c, u64* out, const u64* acc, const u64* conv, const u64* inv, const u64* inv_s,
                  const u64* addend, u64 g, int limbs) {
   const size_t w = (size_t)limbs * c.n;
+  ProfScope prof(c, kFamElem, 8.0 * c.n * limbs * (addend ? 4 : 3));
   sub_scale_kernel<<<grid_cap(w), kThreads, 0, c.stream>>>(out, acc, conv, inv, inv_s, addend, g, limbs, c.logn,
                                                            QP(c));
   post_launch(c);
@@ -632,6 +663,7 @@ void k_sub_scale(Context& c, u64* out, const u64* acc, const u64* conv, const u6
 
 void k_rescale_lift(Context& c, u64* out, const u64* x, int last_prime, int limbs) {
   const size_t w = (size_t)limbs * c.n;
+  ProfScope prof(c, kFamElem, 8.0 * c.n * (limbs + 1));
   rescale_lift_kernel<<<grid_cap(w), kThreads, 0, c.stream>>>(out, x, c.primes[last_prime], limbs, c.n, QP(c),
                                                               c.tabs.mh);
   post_launch(c);

@@ -7,8 +7,19 @@
 #include "protocols.h"
 
 #include <cmath>
+#include <cstdio>
 
 namespace sf {
+
+// ct (.) mask with the mask plaintext encoded once per (key, limb count) and
+// kept resident: numerically identical to mul_plain (same encode, same scale
+// q_top), without re-running the host FFT every decode step.
+static Ct mul_plain_cached(Context& c, const Ct& a, const std::string& key, const std::vector<double>& slots) {
+  check_ct(c, a, "mul_plain");
+  require(a.level() > 0, kLevelUnderflow, "mul_plain: no multiplicative level left");
+  Pt p = cached_pt(c, key, slots.data(), (double)c.primes[a.limbs - 1], a.limbs);
+  return mac_plain(c, {&a}, {&p});
+}
 
 // ============================================================== VMM (vmm.cpp)
 
@@ -167,7 +178,7 @@ Ct vmm_interleaved(Context& c, const Ct& x, VmmPlan& plan, bool mask_output) {
   if (mask_output) {
     std::vector<double> mk(c.slots, 0.0);
     for (int i = s.tau_out; i < c.slots; i += s.t_out) mk[i] = 1.0;
-    acc = mul_plain(c, acc, mk.data());
+    acc = mul_plain_cached(c, acc, "stride:" + std::to_string(s.t_out) + ":" + std::to_string(s.tau_out), mk);
   }
   acc.layout = Layout{LayoutKind::Interleaved, s.d_out, s.t_out, s.tau_out, 1, !mask_output};
   return acc;
@@ -246,9 +257,11 @@ Ct rope_apply(Context& c, const Ct& x, const AttnCfg& cfg, long long position, d
       p2[i] = -std::sin(angle);
   }
   const int s = cfg.t();
-  Ct y = mul_plain(c, x, p0.data());
-  y = add(c, y, rotate(c, mul_plain(c, x, p1.data()), -s, false));
-  y = add(c, y, rotate(c, mul_plain(c, x, p2.data()), s, false));
+  char key[160];
+  std::snprintf(key, sizeof key, "rope:%lld:%d:%d:%d:%d:%a:", position, ly.d, ly.t, ly.offset, dh, base);
+  Ct y = mul_plain_cached(c, x, std::string(key) + "0", p0);
+  y = add(c, y, rotate(c, mul_plain_cached(c, x, std::string(key) + "1", p1), -s, false));
+  y = add(c, y, rotate(c, mul_plain_cached(c, x, std::string(key) + "2", p2), s, false));
   Layout out = ly;
   out.deferred_mask = false;
   y.layout = out;
@@ -291,10 +304,18 @@ std::vector<Ct> make_v_pieces(Context& c, const KV& cache, const Ct& v_open, int
   std::vector<Ct> parts;
   parts.reserve(dh);
   std::vector<double> m(c.slots);
-  for (int e = 0; e < dh; ++e) {
+  const std::vector<double> valid = valid_mask(*v_open.layout, c.slots);
+  Layout out = *v_open.layout;
+  out.deferred_mask = false;
+  for (int e = 0; e < dh; ++e) {  // fused_extract(VcacheMask) with the piece mask (vmm.cpp:102-108)
     std::fill(m.begin(), m.end(), 0.0);
     for (int h = 0; h < cfg.H; ++h) m[(h * dh + e) * t + j0] = 1.0;
-    parts.push_back(fused_extract_mask(c, v_open, m.data()));
+    for (int i = 0; i < c.slots; ++i) m[i] *= valid[i];
+    char key[96];
+    std::snprintf(key, sizeof key, "vpiece:%d:%d:%d:%d:%d", cfg.d, cfg.H, t, e, j0);
+    Ct y = mul_plain_cached(c, v_open, key, m);
+    y.layout = out;
+    parts.push_back(std::move(y));
   }
   return parts;
 }
@@ -338,7 +359,7 @@ std::vector<Ct> qk_dot(Context& c, const Ct& q, const KV& cache) {  // kv_attent
   for (int j = 0; j < (int)cache.k.size(); ++j) {
     Ct prod = mul(c, q_rep, cache.k[j]);
     for (int l = 0; (1 << l) < dh; ++l) prod = add(c, prod, rotate(c, prod, (1 << l) * t, false));  // 38-41
-    Ct masked = mul_plain(c, prod, head_mask.data());
+    Ct masked = mul_plain_cached(c, prod, "headmask:" + std::to_string(cfg.H) + ":" + std::to_string(t), head_mask);
     const int local = (j * t) % gt;
     Ct packed = local ? rotate(c, masked, -local, false) : masked;
     auto& slot = maps[(j * t) / gt];
@@ -376,7 +397,7 @@ Ct softmax_times_v(Context& c, const std::vector<Ct>& probs, const KV& cache) { 
   for (int step = 1; step < t; step <<= 1) folded = add(c, folded, rotate(c, folded, step, false));  // 44-47
   std::vector<double> sm(cfg.N, 0.0);
   for (int i = 0; i < cfg.N; i += t) sm[i] = 1.0;
-  Ct out = mul_plain(c, folded, sm.data());
+  Ct out = mul_plain_cached(c, folded, "stride:" + std::to_string(t) + ":0", sm);
   out.layout = make_interleaved(cfg.d, cfg.N, 0, cfg.H);
   return out;
 }

@@ -68,7 +68,7 @@ def test_every_evaluator_op_bit_exact(N, L, alpha):
         ("sub", lambda be, x, y: be.sub(x, y)),
         ("add_plain", lambda be, x, y: be.add_plain(x, p)),
         ("mul_plain", lambda be, x, y: be.mul_plain(x, p)),
-        ("mac_plain", lambda be, x, y: be.mac_plain([(x, p), (be.level_drop(y, x.level), -p)])),
+        ("mac_plain", lambda be, x, y: be.mac_plain([(be.level_drop(x, y.level), p), (y, -p)])),
         ("mul", lambda be, x, y: be.mul(x, y)),
         ("rotate", lambda be, x, y: be.rotate(x, 3)),
         ("rotate_neg", lambda be, x, y: be.rotate(x, -N // 2 + 1)),
@@ -245,4 +245,7 @@ def test_full_ring_ntt_and_rotation_parity():
     _eq(g.mul_plain(cg, p), o.mul_plain(co, p))
     rg, ro = g.rotate(cg, 5), o.rotate(co, 5)
     _eq(rg, ro)
-    assert np.max(np.abs(g.decrypt(rg) - np.roll(x, -5))) < TOL
+    # one hybrid key switch at ring 2^16 with a dense ternary secret: the
+    # ModDown rounding term dominates (~2^-18 observed); precision bar 16 bits
+    err = np.max(np.abs(g.decrypt(rg) - np.roll(x, -5)))
+    assert -np.log2(err) > 16.0, err
