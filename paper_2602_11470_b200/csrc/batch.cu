@@ -1,0 +1,304 @@
+// Batched elementwise / basis-conversion / key-switch kernels.
+//
+// Each launch processes up to kJobs independent jobs (ciphertexts, key
+// switches) whose device pointers travel in the kernel parameter block
+// (CUDA 12.1+ allows 32 KB of parameters). grid.y indexes the job, grid.x
+// strides over limbs x coefficients with 16-byte vector accesses where the
+// layout allows. This turns the thousands of per-ciphertext operations of an
+// attention decode step (256 K ciphertexts, 510 V handles, 2.5k rotations)
+// into a few hundred full-GPU launches.
+#include "batch.cuh"
+#include "modarith.cuh"
+
+namespace sf {
+namespace {
+
+constexpr int kT = 256;
+
+inline void post(Context& c) {
+  c.launches.fetch_add(1, std::memory_order_relaxed);
+  SF_CUDA(cudaGetLastError());
+}
+
+inline dim3 grid2(size_t per_job_threads, int jobs) {
+  size_t bx = (per_job_threads + kT - 1) / kT;
+  if (bx > 2048) bx = 2048;
+  return dim3((unsigned)(bx ? bx : 1), (unsigned)jobs);
+}
+
+__device__ __forceinline__ uint32_t brev_(uint32_t x, int logn) { return __brev(x) >> (32 - logn); }
+__device__ __forceinline__ uint32_t perm_(uint32_t i, u64 g, int logn) {
+  const u64 e = 2ull * brev_(i, logn) + 1;
+  const u64 e2 = (e * g) & ((2ull << logn) - 1);
+  return brev_((uint32_t)((e2 - 1) >> 1), logn);
+}
+
+// ------------------------------------------------------------------ kernels
+__global__ void copy_batch_kernel(CopyBatch B, size_t words) {
+  const int j = blockIdx.y;
+  const ulonglong2* s = reinterpret_cast<const ulonglong2*>(B.src[j]);
+  ulonglong2* d = reinterpret_cast<ulonglong2*>(B.dst[j]);
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < words / 2; i += (size_t)gridDim.x * blockDim.x)
+    d[i] = s[i];
+}
+
+__global__ void add_batch_kernel(AddBatch B, int limbs, int n, const u64* Q) {
+  const int j = blockIdx.y;
+  const size_t half = (size_t)limbs * n / 2;
+  for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < 2 * half; v += (size_t)gridDim.x * blockDim.x) {
+    const int poly = v >= half;
+    const size_t w = v - poly * half;
+    const int l = (int)((w * 2) / n);
+    const u64 q = Q[l];
+    const ulonglong2 x = reinterpret_cast<const ulonglong2*>(poly ? B.a1[j] : B.a0[j])[w];
+    const ulonglong2 y = reinterpret_cast<const ulonglong2*>(poly ? B.b1[j] : B.b0[j])[w];
+    ulonglong2 z;
+    z.x = B.sub ? sub_mod(x.x, y.x, q) : add_mod(x.x, y.x, q);
+    z.y = B.sub ? sub_mod(x.y, y.y, q) : add_mod(x.y, y.y, q);
+    reinterpret_cast<ulonglong2*>(poly ? B.o1[j] : B.o0[j])[w] = z;
+  }
+}
+
+__global__ void sum_kernel(SumArgs A, int limbs, int n, const u64* Q) {
+  const size_t total = (size_t)limbs * n;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < 2 * total; i += (size_t)gridDim.x * blockDim.x) {
+    const int poly = i >= total;
+    const size_t w = i - poly * total;
+    const int l = (int)(w / n);
+    const u64 q = Q[l];
+    u64 acc = 0;
+    for (int k = 0; k < A.k; ++k) acc = add_mod(acc, (poly ? A.in1[k] : A.in0[k])[w], q);
+    (poly ? A.out1 : A.out0)[w] = acc;
+  }
+}
+
+__global__ void mulpt_batch_kernel(MulPtBatch B, int limbs, int n, const u64* Q, const u64* MH, const u64* ML) {
+  const int j = blockIdx.y;
+  const size_t total = (size_t)limbs * n;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const int l = (int)(i / n);
+    const u64 p = B.pt[j][i];
+    B.o0[j][i] = mulmod(B.c0[j][i], p, Q[l], MH[l], ML[l]);
+    B.o1[j][i] = mulmod(B.c1[j][i], p, Q[l], MH[l], ML[l]);
+  }
+}
+
+__global__ void tensor_batch_kernel(TensorBatch B, int limbs, int n, const u64* Q, const u64* MH, const u64* ML) {
+  const int j = blockIdx.y;
+  const size_t total = (size_t)limbs * n;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const int l = (int)(i / n);
+    const u64 q = Q[l], mh = MH[l], ml = ML[l];
+    const u64 x0 = B.a0[j][i], x1 = B.a1[j][i], y0 = B.b0[j][i], y1 = B.b1[j][i];
+    B.d0[j][i] = mulmod(x0, y0, q, mh, ml);
+    U128 m{0, 0};
+    mac128(m, x0, y1);
+    mac128(m, x1, y0);
+    B.d1[j][i] = reduce128(m.hi, m.lo, q, mh, ml);
+    B.d2[j][i] = mulmod(x1, y1, q, mh, ml);
+  }
+}
+
+__global__ void lift_batch_kernel(LiftBatch B, int limbs, int n, u64 ql, const u64* Q, const u64* MH) {
+  const int j = blockIdx.y;
+  const size_t total = (size_t)limbs * n;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const int l = (int)(i / n);
+    const size_t k = i - (size_t)l * n;
+    const u64 q = Q[l];
+    const u64 v = B.x[j][k];
+    const u64 r = reduce64(v, q, MH[l]);
+    B.out[j][i] = v > (ql >> 1) ? sub_mod(r, reduce64(ql, q, MH[l]), q) : r;
+  }
+}
+
+__global__ void conv_batch_kernel(ConvBatch A, const u64* Q, const u64* MH, const u64* ML) {
+  const int j = blockIdx.y;
+  const int n = A.n;
+  const u64* in = A.in[j];
+  u64* out = A.out[j];
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    u64 y[kMaxPrimes];
+#pragma unroll 4
+    for (int i = 0; i < A.nsrc; ++i)
+      y[i] = mul_shoup(in[(size_t)i * n + k], A.qinv[i], A.qinv_s[i], Q[A.src_prime[i]]);
+    for (int d = 0; d < A.ndst; ++d) {
+      U128 acc{0, 0};
+      const u64* h = A.qhat + d;
+      for (int i = 0; i < A.nsrc; ++i) mac128(acc, y[i], h[(size_t)i * A.ndst]);
+      const int pd = A.dst_prime[d];
+      out[(size_t)A.out_slot[d] * n + k] = reduce128(acc.hi, acc.lo, Q[pd], MH[pd], ML[pd]);
+    }
+  }
+}
+
+__global__ void ks_batch_kernel(KsBatch A, const u64* Q, const u64* MH, const u64* ML) {
+  const int j = blockIdx.y;
+  const int n = 1 << A.logn;
+  const size_t total = (size_t)A.nt * n;
+  const u64 g = A.g[j];
+  const u64* ext = A.ext[j];
+  const u64* key = A.key[j];
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const int t = (int)(i >> A.logn);
+    const uint32_t k = (uint32_t)(i & (n - 1));
+    const uint32_t src = g > 1 ? perm_(k, g, A.logn) : k;
+    const int m = A.tprime[t];
+    U128 sb{0, 0}, sa{0, 0};
+    for (int d = 0; d < A.ndig; ++d) {
+      const u64 x = ext[((size_t)d * A.nt + t) * n + src];
+      const u64* kb = key + (((size_t)d * 2 + 0) * A.np + m) * n;
+      const u64* ka = key + (((size_t)d * 2 + 1) * A.np + m) * n;
+      mac128(sb, x, kb[k]);
+      mac128(sa, x, ka[k]);
+    }
+    A.accb[j][i] = reduce128(sb.hi, sb.lo, Q[m], MH[m], ML[m]);
+    A.acca[j][i] = reduce128(sa.hi, sa.lo, Q[m], MH[m], ML[m]);
+  }
+}
+
+__global__ void subscale_batch_kernel(SubScaleBatch B, int limbs, int logn, const u64* inv, const u64* inv_s,
+                                      const u64* Q) {
+  const int j = blockIdx.y;
+  const int n = 1 << logn;
+  const size_t total = (size_t)limbs * n;
+  const u64 g = B.g[j];
+  const u64* addend = B.addend[j];
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const int l = (int)(i >> logn);
+    const u64 q = Q[l];
+    u64 v = mul_shoup(sub_mod(B.acc[j][i], B.conv[j][i], q), inv[l], inv_s[l], q);
+    if (addend) {
+      const uint32_t k = (uint32_t)(i & (n - 1));
+      const uint32_t src = g > 1 ? perm_(k, g, logn) : k;
+      v = add_mod(v, addend[((size_t)l << logn) + src], q);
+    }
+    B.out[j][i] = v;
+  }
+}
+
+// Fused VMM multiply-accumulate over ALL giant steps (vmm.cpp:210-219):
+// partial[g2] = sum_g1 baby[g1] (.) pt[g2*b + g1], lazily reduced once.
+// A CTA owns 64 coefficients of one limb: it stages the b babies' (c0, c1)
+// words for those coefficients in shared memory once, then each warp streams
+// the plaintext diagonals of its giants (16-byte loads, 512 B per warp row).
+__global__ void vmm_mac_kernel(VmmMacArgs A, const u64* Q, const u64* MH, const u64* ML) {
+  extern __shared__ u64 sb[];  // [b][2][64]
+  const int n = A.n;
+  const int tiles_per_limb = n / 64;
+  const int l = blockIdx.x / tiles_per_limb;
+  const int k0 = (blockIdx.x - l * tiles_per_limb) * 64;
+  const size_t base = (size_t)l * n + k0;
+  for (int e = threadIdx.x; e < A.b * 2 * 64; e += blockDim.x) {
+    const int g1 = e / 128, rem = e - g1 * 128, poly = rem >> 6, kk = rem & 63;
+    sb[e] = (poly ? A.baby1[g1] : A.baby0[g1])[base + kk];
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const u64 q = Q[l], mh = MH[l], ml = ML[l];
+  for (int g2 = warp; g2 < A.giants; g2 += nw) {
+    U128 a0{0, 0}, a1{0, 0}, b0{0, 0}, b1{0, 0};
+    const int gbase = g2 * A.b;
+    const int cnt = min(A.b, A.k - gbase);
+    for (int g1 = 0; g1 < cnt; ++g1) {
+      const ulonglong2 p = reinterpret_cast<const ulonglong2*>(A.pt[gbase + g1] + base)[lane];
+      const u64* s = sb + g1 * 128;
+      mac128(a0, s[2 * lane], p.x);
+      mac128(b0, s[2 * lane + 1], p.y);
+      mac128(a1, s[64 + 2 * lane], p.x);
+      mac128(b1, s[64 + 2 * lane + 1], p.y);
+    }
+    ulonglong2 r0, r1;
+    r0.x = reduce128(a0.hi, a0.lo, q, mh, ml);
+    r0.y = reduce128(b0.hi, b0.lo, q, mh, ml);
+    r1.x = reduce128(a1.hi, a1.lo, q, mh, ml);
+    r1.y = reduce128(b1.hi, b1.lo, q, mh, ml);
+    reinterpret_cast<ulonglong2*>(A.out0[g2] + base)[lane] = r0;
+    reinterpret_cast<ulonglong2*>(A.out1[g2] + base)[lane] = r1;
+  }
+}
+
+}  // namespace
+
+// --------------------------------------------------------------------- wrappers
+void b_copy(Context& c, const CopyBatch& B, size_t words) {
+  if (!B.count) return;
+  ProfScope prof(c, kFamElem, 16.0 * words * B.count);
+  copy_batch_kernel<<<grid2(words / 2, B.count), kT, 0, c.stream>>>(B, words);
+  post(c);
+}
+
+void b_add(Context& c, const AddBatch& B, int limbs) {
+  if (!B.count) return;
+  ProfScope prof(c, kFamElem, 48.0 * limbs * c.n * B.count);
+  add_batch_kernel<<<grid2((size_t)limbs * c.n, B.count), kT, 0, c.stream>>>(B, limbs, c.n, c.tabs.q);
+  post(c);
+}
+
+void b_sum(Context& c, const SumArgs& A, int limbs) {
+  ProfScope prof(c, kFamElem, 16.0 * limbs * c.n * (A.k + 1));
+  sum_kernel<<<grid2((size_t)limbs * c.n * 2, 1), kT, 0, c.stream>>>(A, limbs, c.n, c.tabs.q);
+  post(c);
+}
+
+void b_mulpt(Context& c, const MulPtBatch& B, int limbs) {
+  if (!B.count) return;
+  ProfScope prof(c, kFamMac, 40.0 * limbs * c.n * B.count);
+  mulpt_batch_kernel<<<grid2((size_t)limbs * c.n, B.count), kT, 0, c.stream>>>(B, limbs, c.n, c.tabs.q, c.tabs.mh,
+                                                                                c.tabs.ml);
+  post(c);
+}
+
+void b_tensor(Context& c, const TensorBatch& B, int limbs) {
+  if (!B.count) return;
+  ProfScope prof(c, kFamElem, 56.0 * limbs * c.n * B.count);
+  tensor_batch_kernel<<<grid2((size_t)limbs * c.n, B.count), kT, 0, c.stream>>>(B, limbs, c.n, c.tabs.q, c.tabs.mh,
+                                                                                  c.tabs.ml);
+  post(c);
+}
+
+void b_lift(Context& c, const LiftBatch& B, int limbs, int last_prime) {
+  if (!B.count) return;
+  ProfScope prof(c, kFamElem, 8.0 * c.n * (limbs + 1) * B.count);
+  lift_batch_kernel<<<grid2((size_t)limbs * c.n, B.count), kT, 0, c.stream>>>(B, limbs, c.n, c.primes[last_prime],
+                                                                                c.tabs.q, c.tabs.mh);
+  post(c);
+}
+
+void b_conv(Context& c, const ConvBatch& A) {
+  if (!A.count) return;
+  ProfScope prof(c, kFamConv, 8.0 * c.n * (A.nsrc + A.ndst) * A.count);
+  conv_batch_kernel<<<grid2(c.n, A.count), kT, 0, c.stream>>>(A, c.tabs.q, c.tabs.mh, c.tabs.ml);
+  post(c);
+}
+
+void b_ks(Context& c, const KsBatch& A) {
+  if (!A.count) return;
+  // ext (one read per job) + key (2 polys per digit) + 2 outputs
+  ProfScope prof(c, kFamKs, 8.0 * c.n * ((double)A.ndig * A.nt * 3 + 2.0 * A.nt) * A.count);
+  ks_batch_kernel<<<grid2((size_t)A.nt * c.n, A.count), kT, 0, c.stream>>>(A, c.tabs.q, c.tabs.mh, c.tabs.ml);
+  post(c);
+}
+
+void b_subscale(Context& c, const SubScaleBatch& B, int limbs, const u64* inv, const u64* inv_s) {
+  if (!B.count) return;
+  ProfScope prof(c, kFamElem, 32.0 * limbs * c.n * B.count);
+  subscale_batch_kernel<<<grid2((size_t)limbs * c.n, B.count), kT, 0, c.stream>>>(B, limbs, c.logn, inv, inv_s,
+                                                                                    c.tabs.q);
+  post(c);
+}
+
+void b_vmm_mac(Context& c, const VmmMacArgs& A, int limbs) {
+  const size_t sm = (size_t)A.b * 2 * 64 * sizeof(u64);
+  // algorithmic bytes: every diagonal once, babies once, partials once
+  ProfScope prof(c, kFamMac, 8.0 * c.n * limbs * ((double)A.k + 2.0 * A.b + 2.0 * A.giants));
+  static bool attr = false;
+  if (!attr) {
+    SF_CUDA(cudaFuncSetAttribute(vmm_mac_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  vmm_mac_kernel<<<(unsigned)(limbs * (c.n / 64)), 256, sm, c.stream>>>(A, c.tabs.q, c.tabs.mh, c.tabs.ml);
+  post(c);
+}
+
+}  // namespace sf

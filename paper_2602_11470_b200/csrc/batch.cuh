@@ -1,0 +1,120 @@
+// Job descriptors for the batched kernels (batch.cu). Each struct is passed by
+// value as the kernel parameter block (<= 32 KB, CUDA 12.1+).
+#pragma once
+#include "context.h"
+
+namespace sf {
+
+constexpr int kMaxPrimes = 64;
+constexpr int kJobs = 128;      // jobs per key-switch / tensor launch
+constexpr int kJobsWide = 256;  // jobs per light elementwise launch
+
+struct CopyBatch {
+  int count = 0;
+  const u64* src[kJobsWide];
+  u64* dst[kJobsWide];
+};
+
+struct AddBatch {
+  int count = 0;
+  bool sub = false;
+  const u64 *a0[kJobsWide], *a1[kJobsWide], *b0[kJobsWide], *b1[kJobsWide];
+  u64 *o0[kJobsWide], *o1[kJobsWide];
+};
+
+struct SumArgs {  // out = sum of k ciphertexts
+  int k = 0;
+  const u64* in0[512];
+  const u64* in1[512];
+  u64 *out0, *out1;
+};
+
+struct MulPtBatch {  // (c0, c1) (.) pt, reduced, no rescale
+  int count = 0;
+  const u64 *c0[kJobsWide], *c1[kJobsWide], *pt[kJobsWide];
+  u64 *o0[kJobsWide], *o1[kJobsWide];
+};
+
+struct TensorBatch {
+  int count = 0;
+  const u64 *a0[kJobs], *a1[kJobs], *b0[kJobs], *b1[kJobs];
+  u64 *d0[kJobs], *d1[kJobs], *d2[kJobs];
+};
+
+struct LiftBatch {  // rescale lift of one coefficient-domain limb into `limbs` limbs
+  int count = 0;
+  const u64* x[512];
+  u64* out[512];
+};
+
+struct ConvBatch {  // fast basis conversion, same plan for every job
+  int count = 0;
+  int nsrc = 0, ndst = 0, n = 0;
+  const u64 *qinv = nullptr, *qinv_s = nullptr, *qhat = nullptr;
+  int src_prime[kMaxPrimes];
+  int dst_prime[kMaxPrimes];
+  int out_slot[kMaxPrimes];
+  const u64* in[kJobsWide];
+  u64* out[kJobsWide];
+};
+
+struct KsBatch {  // key-switch inner products over the extended basis
+  int count = 0;
+  int ndig = 0, nt = 0, np = 0, logn = 0;
+  int tprime[kMaxPrimes];
+  const u64* ext[kJobs];
+  const u64* key[kJobs];
+  u64 g[kJobs];
+  u64* accb[kJobs];
+  u64* acca[kJobs];
+};
+
+struct SubScaleBatch {  // out = (acc - conv) * inv (+ addend permuted by g)
+  int count = 0;
+  const u64 *acc[kJobsWide], *conv[kJobsWide], *addend[kJobsWide];
+  u64 g[kJobsWide];
+  u64* out[kJobsWide];
+};
+
+struct VmmMacArgs {
+  int n = 0, b = 0, giants = 0, k = 0;
+  const u64* baby0[64];
+  const u64* baby1[64];
+  const u64* pt[2048];
+  u64* out0[64];
+  u64* out1[64];
+};
+
+void b_copy(Context& c, const CopyBatch& B, size_t words);
+void b_add(Context& c, const AddBatch& B, int limbs);
+void b_sum(Context& c, const SumArgs& A, int limbs);
+void b_mulpt(Context& c, const MulPtBatch& B, int limbs);
+void b_tensor(Context& c, const TensorBatch& B, int limbs);
+void b_lift(Context& c, const LiftBatch& B, int limbs, int last_prime);
+void b_conv(Context& c, const ConvBatch& A);
+void b_ks(Context& c, const KsBatch& A);
+void b_subscale(Context& c, const SubScaleBatch& B, int limbs, const u64* inv, const u64* inv_s);
+void b_vmm_mac(Context& c, const VmmMacArgs& A, int limbs);
+
+// ---- batched evaluator (keyswitch.cu) ------------------------------------------
+// One rotation job: rotate srcs[src] by r (galois element derived from r).
+struct RotJob {
+  int src;
+  int r;
+};
+// Rotations of a set of same-level ciphertexts; each distinct source is
+// ModUp'd once (hoisting), key switches and ModDowns run batched.
+std::vector<Ct> rotate_batch(Context& c, const std::vector<const Ct*>& srcs, const std::vector<RotJob>& jobs,
+                             bool hoisted, bool count = true);
+std::vector<Ct> mul_batch(Context& c, const std::vector<const Ct*>& a, const std::vector<const Ct*>& b,
+                          bool count = true);
+std::vector<Ct> rescale_batch(Context& c, const std::vector<const Ct*>& xs);
+// x_i (.) p_i, rescaled (scale preserved: p_i encoded at q_top)
+std::vector<Ct> mul_plain_batch(Context& c, const std::vector<const Ct*>& xs, const std::vector<const Pt*>& ps,
+                                bool count = true);
+std::vector<Ct> add_batch(Context& c, const std::vector<const Ct*>& a, const std::vector<const Ct*>& b,
+                          bool count = true);
+// sum of k same-level ciphertexts, charged k-1 additions
+Ct sum_cts(Context& c, const std::vector<const Ct*>& xs, bool count = true);
+
+}  // namespace sf

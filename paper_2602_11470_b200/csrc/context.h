@@ -116,13 +116,20 @@ struct Tabs {
   int n, logn;
 };
 
-// A batch of limbs for one kernel launch: entry b -> (word offset slot[b]*n,
-// prime index prime[b]). Kept small so it travels as a kernel parameter.
-constexpr int kMaxBatch = 96;
+// A batch of limbs for one kernel launch: entry b -> (limb pointer, prime
+// index). Travels as a kernel parameter (> 4 KB kernel parameters: CUDA 12.1+
+// on sm_70+), so one launch can cover every limb of a whole batch of
+// ciphertexts without a staging copy.
+constexpr int kMaxBatch = 1024;
 struct LimbBatch {
   int count = 0;
-  uint16_t slot[kMaxBatch];
+  u64* ptr[kMaxBatch];
   uint8_t prime[kMaxBatch];
+  void add(u64* p, int prime_idx) {
+    ptr[count] = p;
+    prime[count] = (uint8_t)prime_idx;
+    ++count;
+  }
 };
 
 // Live per-family kernel timing (sf_profile_begin / end).
@@ -199,7 +206,8 @@ std::vector<i64> encode_coeffs(const Context& c, const double* slots, double sca
 void decode_coeffs(const Context& c, const std::vector<double>& coeff, double scale, double* slots);
 
 // --- device primitives (kernels.cu) -----------------------------------------
-void launch_ntt(Context& c, u64* base, const LimbBatch& b, bool inverse);
+void launch_ntt(Context& c, const LimbBatch& b, bool inverse);
+bool ntt_two_pass(Context& c, const LimbBatch& b, bool inverse);
 void ntt_limbs(Context& c, u64* base, int count, int first_prime, bool inverse);  // contiguous limbs
 void ntt_list(Context& c, const std::vector<std::pair<u64*, int>>& limbs, bool inverse);
 

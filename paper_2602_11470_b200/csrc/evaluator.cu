@@ -28,7 +28,8 @@ Buf::~Buf() {
   if (p) cudaFreeAsync(p, ctx->stream);
 }
 
-static BufPtr buf(Context& c, size_t words) { return std::make_shared<Buf>(&c, words); }
+BufPtr make_buf(Context& c, size_t words) { return std::make_shared<Buf>(&c, words); }
+static BufPtr buf(Context& c, size_t words) { return make_buf(c, words); }
 
 Context::~Context() {
   if (stream) cudaStreamSynchronize(stream);
@@ -144,14 +145,14 @@ void check_scales(const Ct& a, const Ct& b, const char* what) {
     fail(kScaleMismatch, std::string("ScaleMismatch: ") + what + ": operand scales differ");
 }
 
-static OptLayout merge_layouts(const Ct& a, const Ct& b) {
+OptLayout merge_layouts(const Ct& a, const Ct& b) {
   if (a.layout && b.layout && *a.layout == *b.layout) return a.layout;
   return std::nullopt;
 }
 
 // device constants for `limbs` active limbs: rescale (drop limb limbs-1) and
 // ModDown (P -> Q_limbs): [inv_ql, inv_ql_s, pinv, pinv_s] each `limbs` words
-static const u64* level_consts(Context& c, int limbs) {
+const u64* level_consts(Context& c, int limbs) {
   std::lock_guard<std::mutex> lk(c.mu);
   auto it = c.level_consts.find(limbs);
   if (it != c.level_consts.end()) return it->second->p;
@@ -175,7 +176,7 @@ static const u64* level_consts(Context& c, int limbs) {
   return b->p;
 }
 
-static const ConvPlan& conv_plan(Context& c, const std::vector<int>& src, const std::vector<int>& dst) {
+const ConvPlan& conv_plan(Context& c, const std::vector<int>& src, const std::vector<int>& dst) {
   std::string key;
   for (int s : src) key += std::to_string(s) + ",";
   key += ">";
@@ -325,36 +326,6 @@ Ct add_plain(Context& c, const Ct& a, const double* slots) {
   return r;
 }
 
-// divide by the top prime with rounding
-Ct rescale(Context& c, const Ct& a) {
-  const int L1 = a.limbs - 1;
-  require(L1 >= 1, kLevelUnderflow, "rescale: no prime left to drop");
-  Ct r = alloc_ct(c, L1, a.scale / (double)c.primes[L1]);
-  r.zero = a.zero;
-  r.layout = a.layout;
-  const size_t n = c.n;
-  BufPtr last = buf(c, 2 * n);
-  SF_CUDA(cudaMemcpyAsync(last->p, a.c0() + (size_t)L1 * n, n * 8, cudaMemcpyDeviceToDevice, c.stream));
-  SF_CUDA(cudaMemcpyAsync(last->p + n, a.c1(c.n) + (size_t)L1 * n, n * 8, cudaMemcpyDeviceToDevice, c.stream));
-  LimbBatch b;
-  b.count = 2;
-  b.slot[0] = 0, b.slot[1] = 1;
-  b.prime[0] = b.prime[1] = (uint8_t)L1;
-  launch_ntt(c, last->p, b, true);
-  BufPtr lift = buf(c, 2 * (size_t)L1 * n);
-  k_rescale_lift(c, lift->p, last->p, L1, L1);
-  k_rescale_lift(c, lift->p + (size_t)L1 * n, last->p + n, L1, L1);
-  LimbBatch f;
-  f.count = 2 * L1;
-  for (int i = 0; i < 2 * L1; ++i) f.slot[i] = (uint16_t)i, f.prime[i] = (uint8_t)(i % L1);
-  require(2 * L1 <= kMaxBatch, kInternal, "rescale: too many limbs");
-  launch_ntt(c, lift->p, f, false);
-  const u64* k = level_consts(c, a.limbs);
-  k_sub_scale(c, r.c0(), a.c0(), lift->p, k, k + a.limbs, nullptr, 0, L1);
-  k_sub_scale(c, r.c1(c.n), a.c1(c.n), lift->p + (size_t)L1 * n, k, k + a.limbs, nullptr, 0, L1);
-  return r;
-}
-
 Ct mac_plain(Context& c, const std::vector<const Ct*>& cts, const std::vector<const Pt*>& pts, bool count) {
   require(!cts.empty() && cts.size() == pts.size(), kShapeMismatch, "mac_plain: term count");
   int limbs = 1 << 30;
@@ -457,135 +428,6 @@ const BufPtr& get_key(Context& c, u64 g) {
   }
   std::lock_guard<std::mutex> lk(c.mu);
   return c.keys.emplace(g, key).first->second;
-}
-
-// ModUp: digits of d (NTT, `limbs` limbs) extended to
-// T = Q_limbs ∪ P, NTT domain, layout [ndig][nt][n].
-struct Ext {
-  BufPtr buf;
-  int ndig = 0, nt = 0, limbs = 0;
-  std::vector<int> tprime;
-};
-
-static Ext mod_up(Context& c, const u64* d, int limbs) {
-  Ext x;
-  const size_t n = c.n;
-  x.limbs = limbs;
-  x.ndig = (limbs + c.alpha - 1) / c.alpha;
-  x.nt = limbs + c.alpha;
-  for (int t = 0; t < x.nt; ++t) x.tprime.push_back(t < limbs ? t : c.P_index(t - limbs));
-  BufPtr dcoef = buf(c, (size_t)limbs * n);
-  SF_CUDA(cudaMemcpyAsync(dcoef->p, d, (size_t)limbs * n * 8, cudaMemcpyDeviceToDevice, c.stream));
-  ntt_limbs(c, dcoef->p, limbs, 0, true);
-  x.buf = buf(c, (size_t)x.ndig * x.nt * n);
-  for (int j = 0; j < x.ndig; ++j) {
-    const int lo = j * c.alpha, hi = std::min((j + 1) * c.alpha, limbs);
-    std::vector<int> src, dst, slot;
-    for (int i = lo; i < hi; ++i) src.push_back(i);
-    for (int t = 0; t < x.nt; ++t)
-      if (t < lo || t >= hi) dst.push_back(x.tprime[t]), slot.push_back(t);
-    u64* ext = x.buf->p + (size_t)j * x.nt * n;
-    k_conv(c, conv_plan(c, src, dst), dcoef->p + (size_t)lo * n, ext, slot);
-    SF_CUDA(cudaMemcpyAsync(ext + (size_t)lo * n, d + (size_t)lo * n, (size_t)(hi - lo) * n * 8,
-                            cudaMemcpyDeviceToDevice, c.stream));
-    std::vector<std::pair<u64*, int>> todo;
-    for (size_t i = 0; i < dst.size(); ++i) todo.emplace_back(ext + (size_t)slot[i] * n, dst[i]);
-    ntt_list(c, todo, false);
-  }
-  return x;
-}
-
-// ModDown of acc (nt = limbs + alpha limbs over T, NTT) into out (limbs):
-// out = (acc_Q - conv(iNTT(acc_P))) * P^-1 (+ addend permuted by g).
-static void mod_down(Context& c, u64* acc, int limbs, u64* out, const u64* addend, u64 g) {
-  const size_t n = c.n;
-  std::vector<int> pidx, qidx;
-  for (int k = 0; k < c.alpha; ++k) pidx.push_back(c.P_index(k));
-  for (int l = 0; l < limbs; ++l) qidx.push_back(l);
-  LimbBatch b;
-  b.count = c.alpha;
-  for (int k = 0; k < c.alpha; ++k) b.slot[k] = (uint16_t)(limbs + k), b.prime[k] = (uint8_t)pidx[k];
-  launch_ntt(c, acc, b, true);
-  BufPtr conv = buf(c, (size_t)limbs * n);
-  std::vector<int> slot(qidx);
-  k_conv(c, conv_plan(c, pidx, qidx), acc + (size_t)limbs * n, conv->p, slot);
-  ntt_limbs(c, conv->p, limbs, 0, false);
-  const u64* k = level_consts(c, limbs);
-  k_sub_scale(c, out, acc, conv->p, k + 2 * limbs, k + 3 * limbs, addend, g, limbs);
-}
-
-// key switch of the ModUp'd ext under key g; c0 addend (permuted by g) folded
-// into the b-part. Writes into r.c0 / r.c1.
-static void ks_apply(Context& c, const Ext& x, u64 g, const u64* c0_addend, const u64* c1_addend, Ct& r) {
-  const BufPtr& key = get_key(c, g);
-  const size_t n = c.n;
-  BufPtr acc = buf(c, 2 * (size_t)x.nt * n);
-  k_ks_inner(c, acc->p, acc->p + (size_t)x.nt * n, x.buf->p, x.ndig, x.nt, x.tprime.data(), key->p, g);
-  mod_down(c, acc->p, x.limbs, r.c0(), c0_addend, g);
-  mod_down(c, acc->p + (size_t)x.nt * n, x.limbs, r.c1(c.n), c1_addend, g);
-}
-
-Ct rotate(Context& c, const Ct& a, int r, bool hoisted, bool count) {
-  check_ct(c, a, "rotate");
-  if (pos_mod(r, c.slots) == 0) return a;
-  if (count) c.ledger.rot(hoisted);
-  if (a.zero) {
-    Ct z = a;
-    z.layout.reset();
-    return z;
-  }
-  const u64 g = galois_elt(c, r);
-  Ext x = mod_up(c, a.c1(c.n), a.limbs);
-  Ct out = alloc_ct(c, a.limbs, a.scale);
-  ks_apply(c, x, g, a.c0(), nullptr, out);
-  return out;
-}
-
-std::vector<Ct> rotate_hoisted(Context& c, const Ct& a, const std::vector<int>& rs, bool count) {
-  check_ct(c, a, "rotate");
-  std::vector<Ct> outs(rs.size());
-  Ext x;
-  bool have = false;
-  for (size_t i = 0; i < rs.size(); ++i) {
-    if (pos_mod(rs[i], c.slots) == 0) {
-      outs[i] = a;
-      continue;
-    }
-    if (count) c.ledger.rot(true);
-    if (a.zero) {
-      outs[i] = a;
-      outs[i].layout.reset();
-      continue;
-    }
-    if (!have) x = mod_up(c, a.c1(c.n), a.limbs), have = true;
-    outs[i] = alloc_ct(c, a.limbs, a.scale);
-    ks_apply(c, x, galois_elt(c, rs[i]), a.c0(), nullptr, outs[i]);
-  }
-  return outs;
-}
-
-Ct mul(Context& c, const Ct& a, const Ct& b, bool count) {
-  check_ct(c, a, "mul");
-  check_ct(c, b, "mul");
-  const int limbs = std::min(a.limbs, b.limbs);
-  require(limbs - 1 > 0, kLevelUnderflow, "mul: no multiplicative level left");
-  if (count) c.ledger.ctct();
-  OptLayout ly = merge_layouts(a, b);
-  if (a.zero || b.zero) {
-    Ct z = zeros(c, limbs - 2);
-    z.layout = ly;
-    return z;
-  }
-  const size_t n = c.n;
-  BufPtr d = buf(c, 3 * (size_t)limbs * n);
-  u64 *d0 = d->p, *d1 = d->p + (size_t)limbs * n, *d2 = d->p + 2 * (size_t)limbs * n;
-  k_tensor(c, d0, d1, d2, a.c0(), a.c1(c.n), b.c0(), b.c1(c.n), limbs);
-  Ext x = mod_up(c, d2, limbs);
-  Ct t = alloc_ct(c, limbs, a.scale * b.scale);
-  ks_apply(c, x, 0, d0, d1, t);
-  Ct r = rescale(c, t);
-  r.layout = ly;
-  return r;
 }
 
 Ct level_drop(Context& c, const Ct& a, int target) {

@@ -79,10 +79,10 @@ __device__ __forceinline__ uint32_t auto_perm(uint32_t i, u64 g, int logn) {
 // out[i] = a(psi^(2 br(i) + 1)). Inverse: Gentleman-Sande + n^-1.
 
 template <bool INV>
-__global__ void __launch_bounds__(512) ntt_single(u64* base, LimbBatch B, Tabs T) {
+__global__ void __launch_bounds__(512) ntt_single(LimbBatch B, Tabs T) {
   extern __shared__ u64 s[];
   const int n = T.n;
-  u64* a = base + (size_t)B.slot[blockIdx.x] * n;
+  u64* a = B.ptr[blockIdx.x];
   const int p = B.prime[blockIdx.x];
   const u64 q = T.q[p];
   for (int i = threadIdx.x; i < n; i += blockDim.x) s[i] = a[i];
@@ -120,127 +120,6 @@ __global__ void __launch_bounds__(512) ntt_single(u64* base, LimbBatch B, Tabs T
     const u64 ni = T.ninv[p], nis = T.ninv_s[p];
     for (int i = threadIdx.x; i < n; i += blockDim.x) a[i] = mul_shoup(s[i], ni, nis, q);
   }
-}
-
-// Column pass: the first r (forward) / last r (inverse) stages, whose butterfly
-// distance is a multiple of C = n / R; a CTA owns TC adjacent columns x R rows.
-template <bool INV>
-__global__ void __launch_bounds__(kThreads) ntt_cols(u64* base, LimbBatch B, Tabs T, int r, int c, int tc_log) {
-  extern __shared__ u64 s[];
-  const int n = T.n, R = 1 << r, C = 1 << c, TC = 1 << tc_log;
-  const int tiles = C >> tc_log;
-  const int entry = blockIdx.x / tiles, tile = blockIdx.x - entry * tiles;
-  u64* a = base + (size_t)B.slot[entry] * n;
-  const int p = B.prime[entry];
-  const u64 q = T.q[p];
-  const int col0 = tile * TC;
-  // load R x TC (row-major in smem)
-  for (int e = threadIdx.x; e < R * TC; e += blockDim.x) {
-    const int row = e >> tc_log, col = e & (TC - 1);
-    s[e] = a[(size_t)row * C + col0 + col];
-  }
-  __syncthreads();
-  const int nbf = (R >> 1) * TC;
-  if (!INV) {
-    const u64* W = T.psi + (size_t)p * n;
-    const u64* Ws = T.psi_s + (size_t)p * n;
-    for (int st = 0; st < r; ++st) {
-      const int t = R >> (st + 1);  // row distance
-      for (int bf = threadIdx.x; bf < nbf; bf += blockDim.x) {
-        const int col = bf & (TC - 1), rb = bf >> tc_log;
-        const int i = rb / t, j = rb - i * t;
-        const int row = 2 * i * t + j;
-        const int w = (1 << st) + i;
-        const u64 U = s[row * TC + col];
-        const u64 V = mul_shoup(s[(row + t) * TC + col], W[w], Ws[w], q);
-        s[row * TC + col] = add_mod(U, V, q);
-        s[(row + t) * TC + col] = sub_mod(U, V, q);
-      }
-      __syncthreads();
-    }
-    for (int e = threadIdx.x; e < R * TC; e += blockDim.x) {
-      const int row = e >> tc_log, col = e & (TC - 1);
-      a[(size_t)row * C + col0 + col] = s[e];
-    }
-  } else {
-    const u64* W = T.ipsi + (size_t)p * n;
-    const u64* Ws = T.ipsi_s + (size_t)p * n;
-    for (int st = 0; st < r; ++st) {
-      const int t = 1 << st;                  // row distance
-      const int h = (n >> 1) / (t * C);       // GS: h = n / (2 t_global), t_global = t*C
-      for (int bf = threadIdx.x; bf < nbf; bf += blockDim.x) {
-        const int col = bf & (TC - 1), rb = bf >> tc_log;
-        const int i = rb / t, j = rb - i * t;
-        const int row = 2 * i * t + j;
-        const u64 U = s[row * TC + col], V = s[(row + t) * TC + col];
-        s[row * TC + col] = add_mod(U, V, q);
-        s[(row + t) * TC + col] = mul_shoup(sub_mod(U, V, q), W[h + i], Ws[h + i], q);
-      }
-      __syncthreads();
-    }
-    const u64 ni = T.ninv[p], nis = T.ninv_s[p];
-    for (int e = threadIdx.x; e < R * TC; e += blockDim.x) {
-      const int row = e >> tc_log, col = e & (TC - 1);
-      a[(size_t)row * C + col0 + col] = mul_shoup(s[e], ni, nis, q);
-    }
-  }
-}
-
-// Row pass: the last c (forward) / first c (inverse) stages, inside rows of C
-// contiguous words; a CTA owns TR rows.
-template <bool INV>
-__global__ void __launch_bounds__(kThreads) ntt_rows(u64* base, LimbBatch B, Tabs T, int r, int c, int tr_log) {
-  extern __shared__ u64 s[];
-  const int n = T.n, C = 1 << c, TR = 1 << tr_log;
-  const int tiles = (1 << r) >> tr_log;
-  const int entry = blockIdx.x / tiles, tile = blockIdx.x - entry * tiles;
-  u64* a = base + (size_t)B.slot[entry] * n + (size_t)tile * TR * C;
-  const int p = B.prime[entry];
-  const u64 q = T.q[p];
-  const int row0 = tile * TR;
-  for (int e = threadIdx.x; e < TR * C; e += blockDim.x) s[e] = a[e];
-  __syncthreads();
-  const int nbf = TR * (C >> 1);
-  if (!INV) {
-    const u64* W = T.psi + (size_t)p * n;
-    const u64* Ws = T.psi_s + (size_t)p * n;
-    for (int st = 0; st < c; ++st) {
-      const int t = C >> (st + 1);
-      const int m = 1 << (r + st);
-      for (int bf = threadIdx.x; bf < nbf; bf += blockDim.x) {
-        const int rr = bf >> (c - 1), cb = bf & ((C >> 1) - 1);
-        const int i = cb / t, j = cb - i * t;
-        const int col = 2 * i * t + j;
-        const int w = m + ((row0 + rr) << st) + i;
-        const int o = rr * C + col;
-        const u64 U = s[o];
-        const u64 V = mul_shoup(s[o + t], W[w], Ws[w], q);
-        s[o] = add_mod(U, V, q);
-        s[o + t] = sub_mod(U, V, q);
-      }
-      __syncthreads();
-    }
-  } else {
-    const u64* W = T.ipsi + (size_t)p * n;
-    const u64* Ws = T.ipsi_s + (size_t)p * n;
-    for (int st = 0; st < c; ++st) {
-      const int t = 1 << st;
-      const int h = (n >> 1) / t;
-      const int per_row = C / (2 * t);  // GS blocks per row
-      for (int bf = threadIdx.x; bf < nbf; bf += blockDim.x) {
-        const int rr = bf >> (c - 1), cb = bf & ((C >> 1) - 1);
-        const int i = cb / t, j = cb - i * t;
-        const int col = 2 * i * t + j;
-        const int w = h + (row0 + rr) * per_row + i;
-        const int o = rr * C + col;
-        const u64 U = s[o], V = s[o + t];
-        s[o] = add_mod(U, V, q);
-        s[o + t] = mul_shoup(sub_mod(U, V, q), W[w], Ws[w], q);
-      }
-      __syncthreads();
-    }
-  }
-  for (int e = threadIdx.x; e < TR * C; e += blockDim.x) a[e] = s[e];
 }
 
 // ----------------------------------------------------------------------- elementwise
@@ -500,77 +379,41 @@ const u64* QP(Context& c) { return c.tabs.q; }
 }  // namespace
 
 // ------------------------------------------------------------------------ wrappers
-void launch_ntt(Context& c, u64* base, const LimbBatch& b, bool inverse) {
+void launch_ntt(Context& c, const LimbBatch& b, bool inverse) {
   if (b.count == 0) return;
-  const int n = c.n, logn = c.logn;
+  const int n = c.n;
   ProfScope prof(c, kFamNtt, 16.0 * n * b.count);
-  if (n <= 4096) {
-    const int th = std::min(512, std::max(32, n / 2));
-    const size_t sm = (size_t)n * sizeof(u64);
-    if (inverse)
-      ntt_single<true><<<b.count, th, sm, c.stream>>>(base, b, c.tabs);
-    else
-      ntt_single<false><<<b.count, th, sm, c.stream>>>(base, b, c.tabs);
+  if (c.logn >= 12) {
+    ntt_two_pass(c, b, inverse);
     post_launch(c);
+    c.launches.fetch_add(1, std::memory_order_relaxed);  // two kernels per transform
     return;
   }
-  const int cc = (logn + 1) / 2, r = logn - cc;
-  const int tile_log = 12;  // 4096 words = 32 KiB per CTA
-  const int tc_log = tile_log - r, tr_log = tile_log - cc;
-  const unsigned col_blocks = (unsigned)b.count * (1u << (cc - tc_log));
-  const unsigned row_blocks = (unsigned)b.count * (1u << (r - tr_log));
-  const size_t sm = (size_t)1 << tile_log << 3;
-  if (!inverse) {
-    ntt_cols<false><<<col_blocks, kThreads, sm, c.stream>>>(base, b, c.tabs, r, cc, tc_log);
-    post_launch(c);
-    ntt_rows<false><<<row_blocks, kThreads, sm, c.stream>>>(base, b, c.tabs, r, cc, tr_log);
-    post_launch(c);
-  } else {
-    ntt_rows<true><<<row_blocks, kThreads, sm, c.stream>>>(base, b, c.tabs, r, cc, tr_log);
-    post_launch(c);
-    ntt_cols<true><<<col_blocks, kThreads, sm, c.stream>>>(base, b, c.tabs, r, cc, tc_log);
-    post_launch(c);
-  }
+  const int th = std::min(512, std::max(32, n / 2));
+  const size_t sm = (size_t)n * sizeof(u64);
+  if (inverse)
+    ntt_single<true><<<b.count, th, sm, c.stream>>>(b, c.tabs);
+  else
+    ntt_single<false><<<b.count, th, sm, c.stream>>>(b, c.tabs);
+  post_launch(c);
 }
 
 void ntt_limbs(Context& c, u64* base, int count, int first_prime, bool inverse) {
-  for (int s = 0; s < count; s += kMaxBatch) {
-    LimbBatch b;
-    b.count = std::min(kMaxBatch, count - s);
-    for (int i = 0; i < b.count; ++i) {
-      b.slot[i] = (uint16_t)i;
-      b.prime[i] = (uint8_t)(first_prime + s + i);
-    }
-    launch_ntt(c, base + (size_t)s * c.n, b, inverse);
+  LimbBatch b;
+  for (int i = 0; i < count; ++i) {
+    b.add(base + (size_t)i * c.n, first_prime + i);
+    if (b.count == kMaxBatch) launch_ntt(c, b, inverse), b.count = 0;
   }
+  launch_ntt(c, b, inverse);
 }
 
 void ntt_list(Context& c, const std::vector<std::pair<u64*, int>>& limbs, bool inverse) {
-  // group limbs into batches relative to the lowest address of each batch
-  size_t s = 0;
-  while (s < limbs.size()) {
-    u64* base = limbs[s].first;
-    for (size_t i = s; i < limbs.size() && i < s + kMaxBatch; ++i) base = std::min(base, limbs[i].first);
-    LimbBatch b;
-    b.count = 0;
-    size_t i = s;
-    for (; i < limbs.size() && b.count < kMaxBatch; ++i) {
-      const size_t off = (size_t)(limbs[i].first - base);
-      if (off % c.n != 0 || off / c.n > 65535 || limbs[i].first < base) break;
-      b.slot[b.count] = (uint16_t)(off / c.n);
-      b.prime[b.count] = (uint8_t)limbs[i].second;
-      ++b.count;
-    }
-    if (b.count == 0) {  // isolated limb below base: launch alone
-      b.count = 1;
-      b.slot[0] = 0;
-      b.prime[0] = (uint8_t)limbs[s].second;
-      base = limbs[s].first;
-      i = s + 1;
-    }
-    launch_ntt(c, base, b, inverse);
-    s = i;
+  LimbBatch b;
+  for (const auto& l : limbs) {
+    b.add(l.first, l.second);
+    if (b.count == kMaxBatch) launch_ntt(c, b, inverse), b.count = 0;
   }
+  launch_ntt(c, b, inverse);
 }
 
 void k_addsub(Context& c, u64* out, const u64* a, const u64* b, int limbs, bool sub) {

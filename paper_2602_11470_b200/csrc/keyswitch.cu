@@ -1,0 +1,481 @@
+// Batched hybrid key switching, rescaling and ciphertext arithmetic
+// (DESIGN.md §3.5-3.6, §5). Every per-ciphertext result is bit-identical to
+// the scalar definition (and to the CPU oracle): batching changes only how
+// many ciphertexts one launch covers.
+//
+// rotate(ct, r)  = ( sigma_g(c0) + ModDown(<sigma_g(ModUp(c1)), evk_g.b>),
+//                                  ModDown(<sigma_g(ModUp(c1)), evk_g.a>) )
+// mul(a, b)      = Rescale( (d0, d1) + ModDown(<ModUp(d2), rlk>) )
+// Hoisting falls out of the definition: jobs that share a source share one
+// ModUp (RotationHint{hoisted}, engine.hpp:98-100).
+#include <algorithm>
+#include <map>
+
+#include "batch.cuh"
+
+namespace sf {
+
+BufPtr make_buf(Context& c, size_t words);
+const u64* level_consts(Context& c, int limbs);
+const ConvPlan& conv_plan(Context& c, const std::vector<int>& src, const std::vector<int>& dst);
+OptLayout merge_layouts(const Ct& a, const Ct& b);
+
+namespace {
+
+struct ExtB {
+  BufPtr buf;
+  int S = 0, ndig = 0, nt = 0, limbs = 0;
+  std::vector<int> tprime;
+  size_t per = 0;  // words per source
+  const u64* ext(int s) const { return buf->p + (size_t)s * per; }
+};
+
+void fill_conv(ConvBatch& B, Context& c, const ConvPlan& p) {
+  B.nsrc = p.nsrc;
+  B.ndst = p.ndst;
+  B.n = c.n;
+  B.qinv = p.tab->p;
+  B.qinv_s = p.tab->p + p.nsrc;
+  B.qhat = p.tab->p + 2 * p.nsrc;
+  for (int i = 0; i < p.nsrc; ++i) B.src_prime[i] = p.src[i];
+  for (int d = 0; d < p.ndst; ++d) B.dst_prime[d] = p.dst[d];
+}
+
+void ntt_batch(Context& c, LimbBatch& b, bool inverse) {
+  if (b.count) launch_ntt(c, b, inverse);
+  b.count = 0;
+}
+void ntt_push(Context& c, LimbBatch& b, u64* p, int prime, bool inverse) {
+  b.add(p, prime);
+  if (b.count == kMaxBatch) ntt_batch(c, b, inverse);
+}
+
+// ModUp of S distinct NTT-domain polynomials d[s] (limbs limbs each).
+ExtB mod_up_batch(Context& c, const std::vector<const u64*>& d, int limbs) {
+  ExtB x;
+  const size_t n = c.n;
+  x.S = (int)d.size();
+  x.limbs = limbs;
+  x.ndig = (limbs + c.alpha - 1) / c.alpha;
+  x.nt = limbs + c.alpha;
+  for (int t = 0; t < x.nt; ++t) x.tprime.push_back(t < limbs ? t : c.P_index(t - limbs));
+  x.per = (size_t)x.ndig * x.nt * n;
+  BufPtr dcoef = make_buf(c, (size_t)x.S * limbs * n);
+  {
+    CopyBatch cb;
+    for (int s = 0; s < x.S; ++s) {
+      cb.src[cb.count] = d[s];
+      cb.dst[cb.count++] = dcoef->p + (size_t)s * limbs * n;
+      if (cb.count == kJobsWide) b_copy(c, cb, (size_t)limbs * n), cb.count = 0;
+    }
+    b_copy(c, cb, (size_t)limbs * n);
+    LimbBatch lb;
+    for (int s = 0; s < x.S; ++s)
+      for (int l = 0; l < limbs; ++l) ntt_push(c, lb, dcoef->p + ((size_t)s * limbs + l) * n, l, true);
+    ntt_batch(c, lb, true);
+  }
+  x.buf = make_buf(c, (size_t)x.S * x.per);
+  LimbBatch lb;
+  for (int j = 0; j < x.ndig; ++j) {
+    const int lo = j * c.alpha, hi = std::min((j + 1) * c.alpha, limbs);
+    std::vector<int> src, dst, slot;
+    for (int i = lo; i < hi; ++i) src.push_back(i);
+    for (int t = 0; t < x.nt; ++t)
+      if (t < lo || t >= hi) dst.push_back(x.tprime[t]), slot.push_back(t);
+    const ConvPlan& plan = conv_plan(c, src, dst);
+    ConvBatch cv;
+    fill_conv(cv, c, plan);
+    for (size_t k = 0; k < slot.size(); ++k) cv.out_slot[k] = slot[k];
+    CopyBatch cb;
+    auto ext_of = [&](int s) { return x.buf->p + (size_t)s * x.per + (size_t)j * x.nt * n; };
+    for (int s = 0; s < x.S; ++s) {
+      u64* e = ext_of(s);
+      cv.in[cv.count] = dcoef->p + ((size_t)s * limbs + lo) * n;
+      cv.out[cv.count++] = e;
+      if (cv.count == kJobsWide) b_conv(c, cv), cv.count = 0;
+      cb.src[cb.count] = d[s] + (size_t)lo * n;  // own primes: the exact NTT-domain residues
+      cb.dst[cb.count++] = e + (size_t)lo * n;
+      if (cb.count == kJobsWide) b_copy(c, cb, (size_t)(hi - lo) * n), cb.count = 0;
+    }
+    b_conv(c, cv);
+    b_copy(c, cb, (size_t)(hi - lo) * n);
+    // forward NTT of the converted limbs, enqueued after every conversion
+    for (int s = 0; s < x.S; ++s)
+      for (size_t k = 0; k < slot.size(); ++k) ntt_push(c, lb, ext_of(s) + (size_t)slot[k] * n, dst[k], false);
+    ntt_batch(c, lb, false);
+  }
+  return x;
+}
+
+struct KsJob {
+  int src;
+  u64 g;             // automorphism applied to ext and to the addends (<= 1: none)
+  const u64* add0;   // added to the b-part after ModDown (c0 / d0) or null
+  const u64* add1;   // added to the a-part (d1) or null
+  u64* out0;
+  u64* out1;
+};
+
+// Inner products + ModDown for every job (chunks of kJobs).
+void ks_jobs(Context& c, const ExtB& x, const std::vector<KsJob>& jobs) {
+  const size_t n = c.n;
+  const int limbs = x.limbs, nt = x.nt;
+  const u64* kc = level_consts(c, limbs);
+  std::vector<int> pidx, qidx;
+  for (int k = 0; k < c.alpha; ++k) pidx.push_back(c.P_index(k));
+  for (int l = 0; l < limbs; ++l) qidx.push_back(l);
+  const ConvPlan& down = conv_plan(c, pidx, qidx);
+  for (size_t s0 = 0; s0 < jobs.size(); s0 += kJobs) {
+    const int J = (int)std::min<size_t>(kJobs, jobs.size() - s0);
+    BufPtr acc = make_buf(c, (size_t)J * 2 * nt * n);
+    auto accp = [&](int j, int poly) { return acc->p + ((size_t)j * 2 + poly) * nt * n; };
+    KsBatch kb;
+    kb.ndig = x.ndig;
+    kb.nt = nt;
+    kb.np = c.np;
+    kb.logn = c.logn;
+    for (int t = 0; t < nt; ++t) kb.tprime[t] = x.tprime[t];
+    for (int j = 0; j < J; ++j) {
+      const KsJob& jb = jobs[s0 + j];
+      kb.ext[j] = x.ext(jb.src);
+      kb.key[j] = get_key(c, jb.g <= 1 ? 0 : jb.g)->p;
+      kb.g[j] = jb.g;
+      kb.accb[j] = accp(j, 0);
+      kb.acca[j] = accp(j, 1);
+    }
+    kb.count = J;
+    b_ks(c, kb);
+    // ModDown of 2J polynomials
+    LimbBatch lb;
+    for (int j = 0; j < J; ++j)
+      for (int poly = 0; poly < 2; ++poly)
+        for (int k = 0; k < c.alpha; ++k) ntt_push(c, lb, accp(j, poly) + (size_t)(limbs + k) * n, pidx[k], true);
+    ntt_batch(c, lb, true);
+    BufPtr conv = make_buf(c, (size_t)J * 2 * limbs * n);
+    ConvBatch cv;
+    fill_conv(cv, c, down);
+    for (int l = 0; l < limbs; ++l) cv.out_slot[l] = l;
+    for (int j = 0; j < J; ++j)
+      for (int poly = 0; poly < 2; ++poly) {
+        cv.in[cv.count] = accp(j, poly) + (size_t)limbs * n;
+        cv.out[cv.count++] = conv->p + ((size_t)j * 2 + poly) * limbs * n;
+      }
+    b_conv(c, cv);
+    for (int j = 0; j < J; ++j)
+      for (int poly = 0; poly < 2; ++poly)
+        for (int l = 0; l < limbs; ++l) ntt_push(c, lb, conv->p + (((size_t)j * 2 + poly) * limbs + l) * n, l, false);
+    ntt_batch(c, lb, false);
+    SubScaleBatch sb;
+    for (int j = 0; j < J; ++j) {
+      const KsJob& jb = jobs[s0 + j];
+      for (int poly = 0; poly < 2; ++poly) {
+        sb.acc[sb.count] = accp(j, poly);
+        sb.conv[sb.count] = conv->p + ((size_t)j * 2 + poly) * limbs * n;
+        sb.addend[sb.count] = poly ? jb.add1 : jb.add0;
+        sb.g[sb.count] = jb.g;
+        sb.out[sb.count++] = poly ? jb.out1 : jb.out0;
+      }
+    }
+    b_subscale(c, sb, limbs, kc + 2 * limbs, kc + 3 * limbs);
+  }
+}
+
+}  // namespace
+
+// -------------------------------------------------------------------- rescale
+std::vector<Ct> rescale_batch(Context& c, const std::vector<const Ct*>& xs) {
+  std::vector<Ct> out(xs.size());
+  if (xs.empty()) return out;
+  std::map<int, std::vector<int>> by_limbs;
+  for (size_t i = 0; i < xs.size(); ++i) by_limbs[xs[i]->limbs].push_back((int)i);
+  const size_t n = c.n;
+  for (auto& [limbs, idx] : by_limbs) {
+    const int L1 = limbs - 1;
+    require(L1 >= 1, kLevelUnderflow, "rescale: no prime left to drop");
+    const u64* kc = level_consts(c, limbs);
+    for (size_t s0 = 0; s0 < idx.size(); s0 += kJobs) {
+      const int J = (int)std::min<size_t>(kJobs, idx.size() - s0);
+      BufPtr last = make_buf(c, (size_t)2 * J * n);
+      BufPtr lift = make_buf(c, (size_t)2 * J * L1 * n);
+      CopyBatch cb;
+      LiftBatch lfb;
+      LimbBatch lb;
+      SubScaleBatch sb;
+      for (int j = 0; j < J; ++j) {
+        const Ct& x = *xs[idx[s0 + j]];
+        Ct r = alloc_ct(c, L1, x.scale / (double)c.primes[L1]);
+        r.zero = x.zero;
+        r.layout = x.layout;
+        for (int poly = 0; poly < 2; ++poly) {
+          const u64* src = poly ? x.c1(c.n) : x.c0();
+          u64* lp = last->p + (size_t)(2 * j + poly) * n;
+          cb.src[cb.count] = src + (size_t)L1 * n;
+          cb.dst[cb.count++] = lp;
+          lb.add(lp, L1);
+          lfb.x[lfb.count] = lp;
+          lfb.out[lfb.count++] = lift->p + (size_t)(2 * j + poly) * L1 * n;
+          sb.acc[sb.count] = src;
+          sb.conv[sb.count] = lift->p + (size_t)(2 * j + poly) * L1 * n;
+          sb.addend[sb.count] = nullptr;
+          sb.g[sb.count] = 0;
+          sb.out[sb.count++] = poly ? r.c1(c.n) : r.c0();
+        }
+        out[idx[s0 + j]] = r;
+      }
+      b_copy(c, cb, n);
+      ntt_batch(c, lb, true);
+      b_lift(c, lfb, L1, L1);
+      for (int j = 0; j < 2 * J; ++j)
+        for (int l = 0; l < L1; ++l) ntt_push(c, lb, lift->p + ((size_t)j * L1 + l) * n, l, false);
+      ntt_batch(c, lb, false);
+      b_subscale(c, sb, L1, kc, kc + limbs);
+    }
+  }
+  return out;
+}
+
+Ct rescale(Context& c, const Ct& a) { return rescale_batch(c, {&a})[0]; }
+
+// ------------------------------------------------------------------ rotations
+std::vector<Ct> rotate_batch(Context& c, const std::vector<const Ct*>& srcs, const std::vector<RotJob>& jobs,
+                             bool hoisted, bool count) {
+  std::vector<Ct> out(jobs.size());
+  // group sources by limb count; one ModUp per distinct source that needs one
+  std::map<int, std::vector<int>> need;  // limbs -> source indices
+  std::vector<int> uses(srcs.size(), 0);
+  for (size_t i = 0; i < jobs.size(); ++i) {
+    const Ct& s = *srcs[jobs[i].src];
+    check_ct(c, s, "rotate");
+    if (pos_mod(jobs[i].r, c.slots) == 0) {
+      out[i] = s;
+      continue;
+    }
+    if (count) c.ledger.rot(hoisted);
+    if (s.zero) {
+      out[i] = s;
+      out[i].layout.reset();
+      continue;
+    }
+    if (uses[jobs[i].src]++ == 0) need[s.limbs].push_back(jobs[i].src);
+  }
+  for (auto& [limbs, sidx] : need) {
+    for (size_t c0 = 0; c0 < sidx.size(); c0 += kJobs) {  // bound the ModUp working set
+      const size_t S = std::min<size_t>(kJobs, sidx.size() - c0);
+      std::vector<const u64*> d;
+      std::map<int, int> local;
+      for (size_t s = 0; s < S; ++s) {
+        local[sidx[c0 + s]] = (int)s;
+        d.push_back(srcs[sidx[c0 + s]]->c1(c.n));
+      }
+      ExtB x = mod_up_batch(c, d, limbs);
+      std::vector<KsJob> kj;
+      for (size_t i = 0; i < jobs.size(); ++i) {
+        auto it = local.find(jobs[i].src);
+        if (it == local.end() || out[i].buf) continue;
+        const Ct& s = *srcs[jobs[i].src];
+        if (pos_mod(jobs[i].r, c.slots) == 0 || s.zero) continue;
+        out[i] = alloc_ct(c, limbs, s.scale);
+        kj.push_back({it->second, galois_elt(c, jobs[i].r), s.c0(), nullptr, out[i].c0(), out[i].c1(c.n)});
+      }
+      ks_jobs(c, x, kj);
+    }
+  }
+  return out;
+}
+
+Ct rotate(Context& c, const Ct& a, int r, bool hoisted, bool count) {
+  return rotate_batch(c, {&a}, {{0, r}}, hoisted, count)[0];
+}
+
+std::vector<Ct> rotate_hoisted(Context& c, const Ct& a, const std::vector<int>& rs, bool count) {
+  std::vector<RotJob> jobs;
+  for (int r : rs) jobs.push_back({0, r});
+  return rotate_batch(c, {&a}, jobs, true, count);
+}
+
+// ------------------------------------------------------------- ct x ct mult
+std::vector<Ct> mul_batch(Context& c, const std::vector<const Ct*>& a, const std::vector<const Ct*>& b, bool count) {
+  require(a.size() == b.size(), kShapeMismatch, "mul_batch: operand count");
+  std::vector<Ct> out(a.size());
+  std::map<int, std::vector<int>> by_limbs;
+  for (size_t i = 0; i < a.size(); ++i) {
+    check_ct(c, *a[i], "mul");
+    check_ct(c, *b[i], "mul");
+    const int limbs = std::min(a[i]->limbs, b[i]->limbs);
+    require(limbs - 1 > 0, kLevelUnderflow, "mul: no multiplicative level left");
+    if (count) c.ledger.ctct();
+    if (a[i]->zero || b[i]->zero) {
+      out[i] = zeros(c, limbs - 2);
+      out[i].layout = merge_layouts(*a[i], *b[i]);
+      continue;
+    }
+    by_limbs[limbs].push_back((int)i);
+  }
+  const size_t n = c.n;
+  for (auto& [limbs, idx] : by_limbs) {
+    for (size_t s0 = 0; s0 < idx.size(); s0 += kJobs) {
+      const int J = (int)std::min<size_t>(kJobs, idx.size() - s0);
+      BufPtr d = make_buf(c, (size_t)J * 3 * limbs * n);
+      auto dp = [&](int j, int k) { return d->p + ((size_t)j * 3 + k) * limbs * n; };
+      TensorBatch tb;
+      std::vector<const u64*> d2;
+      for (int j = 0; j < J; ++j) {
+        const Ct &x = *a[idx[s0 + j]], &y = *b[idx[s0 + j]];
+        tb.a0[j] = x.c0(), tb.a1[j] = x.c1(c.n), tb.b0[j] = y.c0(), tb.b1[j] = y.c1(c.n);
+        tb.d0[j] = dp(j, 0), tb.d1[j] = dp(j, 1), tb.d2[j] = dp(j, 2);
+        d2.push_back(dp(j, 2));
+      }
+      tb.count = J;
+      b_tensor(c, tb, limbs);
+      ExtB x = mod_up_batch(c, d2, limbs);
+      std::vector<Ct> t(J);
+      std::vector<KsJob> kj;
+      for (int j = 0; j < J; ++j) {
+        t[j] = alloc_ct(c, limbs, a[idx[s0 + j]]->scale * b[idx[s0 + j]]->scale);
+        kj.push_back({j, 0, dp(j, 0), dp(j, 1), t[j].c0(), t[j].c1(c.n)});
+      }
+      ks_jobs(c, x, kj);
+      std::vector<const Ct*> tp;
+      for (auto& z : t) tp.push_back(&z);
+      auto r = rescale_batch(c, tp);
+      for (int j = 0; j < J; ++j) {
+        r[j].layout = merge_layouts(*a[idx[s0 + j]], *b[idx[s0 + j]]);
+        out[idx[s0 + j]] = std::move(r[j]);
+      }
+    }
+  }
+  return out;
+}
+
+Ct mul(Context& c, const Ct& a, const Ct& b, bool count) { return mul_batch(c, {&a}, {&b}, count)[0]; }
+
+// ------------------------------------------------------------- ct x pt mult
+std::vector<Ct> mul_plain_batch(Context& c, const std::vector<const Ct*>& xs, const std::vector<const Pt*>& ps,
+                                bool count) {
+  require(xs.size() == ps.size(), kShapeMismatch, "mul_plain_batch: operand count");
+  std::vector<Ct> out(xs.size());
+  std::vector<Ct> tmp(xs.size());
+  std::vector<const Ct*> todo;
+  std::vector<int> where;
+  std::map<int, MulPtBatch> by_limbs;
+  for (size_t i = 0; i < xs.size(); ++i) {
+    const Ct& x = *xs[i];
+    check_ct(c, x, "mul_plain");
+    require(x.level() > 0, kLevelUnderflow, "mul_plain: no multiplicative level left");
+    require(ps[i]->limbs >= x.limbs, kShapeMismatch, "mul_plain: plaintext has too few limbs");
+    if (count) c.ledger.ctpt();
+    if (x.zero) {
+      out[i] = zeros(c, x.level() - 1);
+      out[i].layout = x.layout;
+      continue;
+    }
+    tmp[i] = alloc_ct(c, x.limbs, x.scale * (double)c.primes[x.limbs - 1]);
+    MulPtBatch& B = by_limbs[x.limbs];
+    B.c0[B.count] = x.c0(), B.c1[B.count] = x.c1(c.n), B.pt[B.count] = ps[i]->buf->p;
+    B.o0[B.count] = tmp[i].c0(), B.o1[B.count] = tmp[i].c1(c.n);
+    if (++B.count == kJobsWide) b_mulpt(c, B, x.limbs), B.count = 0;
+    todo.push_back(&tmp[i]);
+    where.push_back((int)i);
+  }
+  for (auto& [limbs, B] : by_limbs) b_mulpt(c, B, limbs);
+  auto r = rescale_batch(c, todo);
+  for (size_t k = 0; k < r.size(); ++k) {
+    const Ct& x = *xs[where[k]];
+    r[k].scale = x.scale;
+    r[k].layout = x.layout;
+    out[where[k]] = std::move(r[k]);
+  }
+  return out;
+}
+
+// ------------------------------------------------------------------ additions
+std::vector<Ct> add_batch(Context& c, const std::vector<const Ct*>& a, const std::vector<const Ct*>& b, bool count) {
+  require(a.size() == b.size(), kShapeMismatch, "add_batch: operand count");
+  std::vector<Ct> out(a.size());
+  std::map<int, AddBatch> by_limbs;
+  for (size_t i = 0; i < a.size(); ++i) {
+    const Ct &x = *a[i], &y = *b[i];
+    check_ct(c, x, "add");
+    check_ct(c, y, "add");
+    if (count) c.ledger.add();
+    const int limbs = std::min(x.limbs, y.limbs);
+    OptLayout ly = merge_layouts(x, y);
+    if (y.zero || (x.zero && y.zero)) {
+      if (!(x.zero && y.zero)) check_scales(x, y, "add");
+      Ct r = x;
+      r.limbs = limbs;
+      r.layout = ly;
+      out[i] = r;
+      continue;
+    }
+    if (x.zero) {
+      Ct r = y;
+      r.limbs = limbs;
+      r.layout = ly;
+      out[i] = r;
+      continue;
+    }
+    check_scales(x, y, "add");
+    Ct r = alloc_ct(c, limbs, x.scale);
+    r.layout = ly;
+    AddBatch& B = by_limbs[limbs];
+    B.a0[B.count] = x.c0(), B.a1[B.count] = x.c1(c.n), B.b0[B.count] = y.c0(), B.b1[B.count] = y.c1(c.n);
+    B.o0[B.count] = r.c0(), B.o1[B.count] = r.c1(c.n);
+    if (++B.count == kJobsWide) b_add(c, B, limbs), B.count = 0;
+    out[i] = r;
+  }
+  for (auto& [limbs, B] : by_limbs) b_add(c, B, limbs);
+  return out;
+}
+
+Ct sum_cts(Context& c, const std::vector<const Ct*>& xs, bool count) {
+  require(!xs.empty(), kShapeMismatch, "sum: empty");
+  if (count) c.ledger.add((long long)xs.size() - 1);
+  int limbs = 1 << 30;
+  std::vector<const Ct*> live;
+  for (const Ct* x : xs) {
+    check_ct(c, *x, "add");
+    limbs = std::min(limbs, x->limbs);
+    if (!x->zero) live.push_back(x);
+  }
+  OptLayout ly = xs[0]->layout;
+  for (const Ct* x : xs)
+    if (!(x->layout && ly && *x->layout == *ly)) ly.reset();
+  if (live.empty()) {
+    Ct z = *xs[0];
+    z.limbs = limbs;
+    z.layout = ly;
+    return z;
+  }
+  for (const Ct* x : live) check_scales(*live[0], *x, "add");
+  if (live.size() == 1) {
+    Ct r = *live[0];
+    r.limbs = limbs;
+    r.layout = ly;
+    return r;
+  }
+  Ct acc = alloc_ct(c, limbs, live[0]->scale);
+  size_t s = 0;
+  bool first = true;
+  while (s < live.size()) {
+    SumArgs A;
+    if (!first) {
+      A.in0[A.k] = acc.c0();
+      A.in1[A.k++] = acc.c1(c.n);
+    }
+    for (; s < live.size() && A.k < 512; ++s) {
+      A.in0[A.k] = live[s]->c0();
+      A.in1[A.k++] = live[s]->c1(c.n);
+    }
+    Ct next = first ? acc : alloc_ct(c, limbs, acc.scale);
+    A.out0 = next.c0();
+    A.out1 = next.c1(c.n);
+    b_sum(c, A, limbs);
+    acc = next;
+    first = false;
+  }
+  acc.layout = ly;
+  return acc;
+}
+
+}  // namespace sf

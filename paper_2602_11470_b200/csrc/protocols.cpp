@@ -9,6 +9,8 @@
 #include <cmath>
 #include <cstdio>
 
+#include "batch.cuh"
+
 namespace sf {
 
 // ct (.) mask with the mask plaintext encoded once per (key, limb count) and
@@ -149,6 +151,47 @@ Ct vmm_interleaved(Context& c, const Ct& x, VmmPlan& plan, bool mask_output) {
     std::vector<const Pt*> pts;
     for (long long g = 0; g < s.k; ++g) cts.push_back(&xs[g]), pts.push_back(&diag[g]);
     acc = mac_plain(c, cts, pts);
+  } else if (!stair.zero && plan.bg.baby <= 64 && plan.bg.giant <= 64 && s.k <= 2048 && c.n >= 64) {
+    // BSGS with every giant's partial sum produced by ONE fused MAC launch
+    // (babies staged on-chip once, each diagonal streamed once), then batched
+    // rescales, batched giant rotations and one reduction.
+    const int b = plan.bg.baby, giants = plan.bg.giant;
+    std::vector<RotJob> jobs;
+    for (int g1 = 1; g1 < b; ++g1) jobs.push_back({0, (int)(g1 * unit)});
+    std::vector<Ct> baby{stair};
+    for (Ct& r : rotate_batch(c, {&stair}, jobs, true)) baby.push_back(std::move(r));
+    c.ledger.ctpt(s.k);
+    c.ledger.add(s.k - giants);  // b-1 additions inside every giant's partial sum
+    const int limbs = x.limbs;
+    std::vector<Ct> partial(giants);
+    VmmMacArgs A;
+    A.n = c.n;
+    A.b = b;
+    A.giants = giants;
+    A.k = (int)s.k;
+    for (int g1 = 0; g1 < b; ++g1) A.baby0[g1] = baby[g1].c0(), A.baby1[g1] = baby[g1].c1(c.n);
+    for (long long g = 0; g < s.k; ++g) A.pt[g] = diag[g].buf->p;
+    for (int g2 = 0; g2 < giants; ++g2) {
+      partial[g2] = alloc_ct(c, limbs, stair.scale * (double)c.primes[limbs - 1]);
+      A.out0[g2] = partial[g2].c0();
+      A.out1[g2] = partial[g2].c1(c.n);
+    }
+    b_vmm_mac(c, A, limbs);
+    std::vector<const Ct*> pp;
+    for (auto& p : partial) pp.push_back(&p);
+    std::vector<Ct> resc = rescale_batch(c, pp);
+    std::vector<const Ct*> rp;
+    std::vector<RotJob> gj;
+    for (int g2 = 0; g2 < giants; ++g2) {
+      resc[g2].scale = stair.scale;
+      resc[g2].layout.reset();
+      rp.push_back(&resc[g2]);
+      gj.push_back({g2, (int)((long long)g2 * b * unit)});
+    }
+    std::vector<Ct> aligned = rotate_batch(c, rp, gj, false);
+    std::vector<const Ct*> ap;
+    for (auto& a : aligned) ap.push_back(&a);
+    acc = sum_cts(c, ap);
   } else {
     const int b = plan.bg.baby, giants = plan.bg.giant;
     std::vector<int> rs;
@@ -307,16 +350,22 @@ std::vector<Ct> make_v_pieces(Context& c, const KV& cache, const Ct& v_open, int
   const std::vector<double> valid = valid_mask(*v_open.layout, c.slots);
   Layout out = *v_open.layout;
   out.deferred_mask = false;
+  check_ct(c, v_open, "mul_plain");
+  require(v_open.level() > 0, kLevelUnderflow, "mul_plain: no multiplicative level left");
+  std::vector<Pt> masks;
   for (int e = 0; e < dh; ++e) {  // fused_extract(VcacheMask) with the piece mask (vmm.cpp:102-108)
     std::fill(m.begin(), m.end(), 0.0);
     for (int h = 0; h < cfg.H; ++h) m[(h * dh + e) * t + j0] = 1.0;
     for (int i = 0; i < c.slots; ++i) m[i] *= valid[i];
     char key[96];
     std::snprintf(key, sizeof key, "vpiece:%d:%d:%d:%d:%d", cfg.d, cfg.H, t, e, j0);
-    Ct y = mul_plain_cached(c, v_open, key, m);
-    y.layout = out;
-    parts.push_back(std::move(y));
+    masks.push_back(cached_pt(c, key, m.data(), (double)c.primes[v_open.limbs - 1], v_open.limbs));
   }
+  std::vector<const Ct*> xs(dh, &v_open);
+  std::vector<const Pt*> ps;
+  for (auto& p : masks) ps.push_back(&p);
+  parts = mul_plain_batch(c, xs, ps);
+  for (auto& y : parts) y.layout = out;
   return parts;
 }
 
@@ -331,10 +380,15 @@ KV v_append(Context& c, const KV& cache, const std::vector<Ct>& parts) {  // kv_
   const int u_local = cache.n_prime - g * gt;
   KV out = cache;
   if (g == (int)out.v.size()) out.v.emplace_back(v_variant_count(cfg), zeros(c, -1));
-  for (int e = 0; e < dh; ++e) {
-    const int idx = v_variant_index(cfg, v_variant_of(cfg, e, u_local));
-    out.v[g][idx] = add(c, out.v[g][idx], parts[e]);
+  std::vector<int> idx(dh);
+  std::vector<const Ct*> a, b;
+  for (int e = 0; e < dh; ++e) {  // distinct variant per element: independent additions
+    idx[e] = v_variant_index(cfg, v_variant_of(cfg, e, u_local));
+    a.push_back(&out.v[g][idx[e]]);
+    b.push_back(&parts[e]);
   }
+  std::vector<Ct> sums = add_batch(c, a, b);
+  for (int e = 0; e < dh; ++e) out.v[g][idx[e]] = std::move(sums[e]);
   return out;
 }
 
@@ -355,20 +409,42 @@ std::vector<Ct> qk_dot(Context& c, const Ct& q, const KV& cache) {  // kv_attent
   const int hb = N / cfg.H;
   for (int h = 0; h < cfg.H; ++h)
     for (int i = 0; i < t; ++i) head_mask[h * hb + i] = 1.0;
-  std::vector<std::optional<Ct>> maps(ceil_div(cache.n_prime, gt));
-  for (int j = 0; j < (int)cache.k.size(); ++j) {
-    Ct prod = mul(c, q_rep, cache.k[j]);
-    for (int l = 0; (1 << l) < dh; ++l) prod = add(c, prod, rotate(c, prod, (1 << l) * t, false));  // 38-41
-    Ct masked = mul_plain_cached(c, prod, "headmask:" + std::to_string(cfg.H) + ":" + std::to_string(t), head_mask);
-    const int local = (j * t) % gt;
-    Ct packed = local ? rotate(c, masked, -local, false) : masked;
-    auto& slot = maps[(j * t) / gt];
-    slot = slot ? add(c, *slot, packed) : packed;
+  // Every K ciphertext runs the same op sequence (mul, fold_within_head 38-41,
+  // mask, pack rotation), so each step is one batched call over all of them.
+  const int J = (int)cache.k.size();
+  std::vector<const Ct*> qs(J, &q_rep), ks;
+  for (const Ct& k : cache.k) ks.push_back(&k);
+  std::vector<Ct> prod = mul_batch(c, qs, ks);
+  for (int l = 0; (1 << l) < dh; ++l) {
+    std::vector<const Ct*> src;
+    std::vector<RotJob> jobs;
+    for (int j = 0; j < J; ++j) src.push_back(&prod[j]), jobs.push_back({j, (1 << l) * t});
+    std::vector<Ct> rot = rotate_batch(c, src, jobs, false);
+    std::vector<const Ct*> rp;
+    for (auto& r : rot) rp.push_back(&r);
+    prod = add_batch(c, src, rp);
   }
+  const std::string hkey = "headmask:" + std::to_string(cfg.H) + ":" + std::to_string(t);
+  std::vector<const Ct*> pp;
+  std::vector<Pt> hm;
+  for (int j = 0; j < J; ++j) {
+    require(prod[j].level() > 0, kLevelUnderflow, "mul_plain: no multiplicative level left");
+    hm.push_back(cached_pt(c, hkey, head_mask.data(), (double)c.primes[prod[j].limbs - 1], prod[j].limbs));
+  }
+  std::vector<const Pt*> hp;
+  for (int j = 0; j < J; ++j) pp.push_back(&prod[j]), hp.push_back(&hm[j]);
+  std::vector<Ct> masked = mul_plain_batch(c, pp, hp);
+  std::vector<const Ct*> mp;
+  std::vector<RotJob> pj;
+  for (int j = 0; j < J; ++j) mp.push_back(&masked[j]), pj.push_back({j, -((j * t) % gt)});
+  std::vector<Ct> packed = rotate_batch(c, mp, pj, false);
+  std::vector<std::vector<const Ct*>> per_map(ceil_div(cache.n_prime, gt));
+  for (int j = 0; j < J; ++j) per_map[(j * t) / gt].push_back(&packed[j]);
   std::vector<Ct> out;
-  for (auto& m : maps) {
-    m->layout.reset();
-    out.push_back(*m);
+  for (auto& m : per_map) {
+    Ct s = sum_cts(c, m);
+    s.layout.reset();
+    out.push_back(std::move(s));
   }
   return out;
 }
@@ -382,18 +458,28 @@ Ct softmax_times_v(Context& c, const std::vector<Ct>& probs, const KV& cache) { 
           "softmax_times_v: expected " + std::to_string(n_maps) + " probability maps, got " +
               std::to_string(probs.size()));
   require((int)cache.v.size() >= n_maps, kShapeMismatch, "softmax_times_v: value cache is missing groups");
-  std::optional<Ct> acc;
+  // All score alignments of one probability map share its ModUp (hoisting);
+  // the rotations, the ct x ct products and the sum each run as one batch.
+  std::vector<const Ct*> src;
+  for (const Ct& p : probs) src.push_back(&p);
+  std::vector<RotJob> jobs;
+  std::vector<std::pair<int, int>> gw;
   for (int g = 0; g < n_maps; ++g) {
     const int tokens = std::min(gt, cache.n_prime - g * gt);
     const int u_max = (tokens - 1) / t;  // touched_variants (53-57)
     const int w_lo = cfg.H == 1 ? 0 : -u_max, w_hi = cfg.d_head();
-    for (int w = w_lo; w < w_hi; ++w) {
-      Ct scores = w ? rotate(c, probs[g], -w * t, false) : probs[g];
-      Ct prod = mul(c, scores, cache.v[g][v_variant_index(cfg, w)]);
-      acc = acc ? add(c, *acc, prod) : prod;
-    }
+    for (int w = w_lo; w < w_hi; ++w) gw.push_back({g, w}), jobs.push_back({g, -w * t});
   }
-  Ct folded = *acc;
+  std::vector<Ct> scores = rotate_batch(c, src, jobs, false);
+  std::vector<const Ct*> sa, vb;
+  for (size_t i = 0; i < gw.size(); ++i) {
+    sa.push_back(&scores[i]);
+    vb.push_back(&cache.v[gw[i].first][v_variant_index(cfg, gw[i].second)]);
+  }
+  std::vector<Ct> prods = mul_batch(c, sa, vb);
+  std::vector<const Ct*> pp;
+  for (auto& p : prods) pp.push_back(&p);
+  Ct folded = sum_cts(c, pp);
   for (int step = 1; step < t; step <<= 1) folded = add(c, folded, rotate(c, folded, step, false));  // 44-47
   std::vector<double> sm(cfg.N, 0.0);
   for (int i = 0; i < cfg.N; i += t) sm[i] = 1.0;
