@@ -149,29 +149,51 @@ class LlamaLayer:
         self.probs = [be.encrypt(probs, LEVELS["probs"]), be.encrypt(probs, LEVELS["probs"])]
         self.inputs = [self.x, self.h7, self.h3, self.h1] + self.probs
 
-    def step(self, inputs=None):
+    PHASES = ["Q, K, V", "RoPE & Cache", "QK^T", "Score*V", "Output projection", "Up & Gate projection",
+              "Down projection"]
+
+    def phase_ms(self, steps):
+        """Device time per phase (CUDA events between phases on the library stream)."""
+        be = self.be
+        tot = [0.0] * len(self.PHASES)
+        for _ in range(steps):
+            self.step(marks=True)
+            for i in range(len(self.PHASES)):
+                tot[i] += be.event_elapsed_ms(10 + i, 11 + i)
+        return {p: round(t / steps, 3) for p, t in zip(self.PHASES, tot)}
+
+    def step(self, inputs=None, marks=False):
         be, sf = self.be, self.sf
         x, h7, h3, h1, p0, p1 = inputs or self.inputs
+        mark = (lambda i: be.event_record(10 + i)) if marks else (lambda i: None)
+        mark(0)
         with be.phase("Q, K, V"):
             q = sf.vmm_interleaved(be, x, None, plan=self.wq)
             k = sf.vmm_interleaved(be, x, None, plan=self.wk)
             v = sf.vmm_interleaved(be, x, None, plan=self.wv)
+        mark(1)
         with be.phase("RoPE & Cache"):
             qr = sf.rope_apply(be, q, self.cfg, self.pos)
             kr = sf.rope_apply(be, k, self.cfg, self.pos)
             cache = sf.v_append(be, self.cache, sf.make_v_pieces(be, self.cache, v, self.pos))
             cache = sf.k_append(be, cache, kr)
+        mark(2)
         with be.phase("QK^T"):
             maps = sf.qk_dot(be, qr, cache)
+        mark(3)
         with be.phase("Score*V"):
             att = sf.softmax_times_v(be, [p0, p1], cache)
+        mark(4)
         with be.phase("Output projection"):
             o = sf.vmm_interleaved(be, h7, None, plan=self.wo)
+        mark(5)
         with be.phase("Up & Gate projection"):
             g = sf.vmm_interleaved(be, h3, None, plan=self.wg)
             u = sf.vmm_interleaved(be, h3, None, plan=self.wu)
+        mark(6)
         with be.phase("Down projection"):
             dn = sf.vmm_interleaved(be, h1, None, plan=self.wd)
+        mark(7)
         return [q, k, v, maps[0], att, o, g, u, dn]
 
 
@@ -226,6 +248,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--alpha", type=int, default=2, help="special primes per key-switching digit")
     ap.add_argument("--quiet", action="store_true")
     args = ap.parse_args()
 
@@ -248,7 +271,7 @@ def main():
     log = (lambda *a: None) if (args.quiet or rank != 0) else (lambda *a: print(*a, file=sys.stderr, flush=True))
     import paper_2602_11470_b200 as sf
     t0 = time.time()
-    be = sf.Backend(SLOTS, 7, alpha=5, seed=1, device=local)
+    be = sf.Backend(SLOTS, 7, alpha=args.alpha, seed=1, device=local)
     layer = LlamaLayer(be, sf, log)
     log(f"[bench] setup {time.time() - t0:.1f}s")
 
@@ -284,6 +307,8 @@ def main():
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
     value = ms_step / world  # whole-job: `world` independent tokens per step time
+
+    phases = layer.phase_ms(args.steps)
 
     # ---- roofline: live per-family kernel timing over the same steps
     import ctypes as C
@@ -338,7 +363,7 @@ def main():
         "vs_baseline": None, "dtype": "u64",
         "data": "synthetic: reference bench weights sin(0.001(31r+c)+0.25), N(0,1) activations/cache, seeded",
         "config": {"workload": "llama3-8b-layer-decode@n'=2048", "ring_degree": 2 * SLOTS, "slots": SLOTS,
-                   "d": D, "heads": H, "ffn": FF, "context": NP, "levels": LEVELS, "L": 7, "alpha": 5,
+                   "d": D, "heads": H, "ffn": FF, "context": NP, "levels": LEVELS, "L": 7, "alpha": args.alpha,
                    "parallelism": f"replicas{world}" if world > 1 else "single",
                    "l2": "working set (plaintext diagonals + keys ~30 GB) >> 126 MB L2; no flush needed"},
         "hevmm_ct_per_s": round(vmm_per_step * world / (ms_step * 1e-3), 2),
@@ -350,6 +375,7 @@ def main():
         "clocks": clk.summary(),
         "ledger_per_step": {k: v // args.steps for k, v in counts.asdict().items()},
         "kernel_families": prof,
+        "phase_ms": phases,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

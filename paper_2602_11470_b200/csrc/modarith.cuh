@@ -60,6 +60,11 @@ __device__ __forceinline__ uint64_t mul_shoup(uint64_t x, uint64_t w, uint64_t w
   return r >= q ? r - q : r;
 }
 
+// Shoup product without the final correction: result in [0, 2q) for any x < 2^64
+__device__ __forceinline__ uint64_t mul_shoup_lazy(uint64_t x, uint64_t w, uint64_t wp, uint64_t q) {
+  return x * w - __umul64hi(x, wp) * q;
+}
+
 __device__ __forceinline__ uint64_t add_mod(uint64_t a, uint64_t b, uint64_t q) {
   const uint64_t s = a + b;
   return s >= q ? s - q : s;

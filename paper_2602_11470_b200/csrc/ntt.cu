@@ -49,6 +49,7 @@ template <int LOGM, class TW>
 __device__ __forceinline__ void warp_fwd(u64 (&x)[1 << (LOGM - 5)], u64* sm, int lane, u64 q, const TW& tw) {
   constexpr int LOGE = LOGM - 5;
   constexpr int E = 1 << LOGE;
+  const u64 q2 = 2 * q;
   int s0 = LOGM - LOGE;
 #pragma unroll
   for (int hi = LOGM; hi > 0; hi -= LOGE) {
@@ -64,10 +65,12 @@ __device__ __forceinline__ void warp_fwd(u64 (&x)[1 << (LOGM - 5)], u64* sm, int
         const int idx = lay<LOGE>(lane, k, s0);
         u64 w, ws;
         tw(b, idx >> (b + 1), w, ws);
-        const u64 U = x[k];
-        const u64 V = mul_shoup(x[k | (1 << rb)], w, ws, q);
-        x[k] = add_mod(U, V, q);
-        x[k | (1 << rb)] = sub_mod(U, V, q);
+        // Harvey lazy CT butterfly: operands in [0, 4q), T in [0, 2q)
+        u64 U = x[k];
+        U = U >= q2 ? U - q2 : U;
+        const u64 T = mul_shoup_lazy(x[k | (1 << rb)], w, ws, q);
+        x[k] = U + T;
+        x[k | (1 << rb)] = U - T + q2;
       }
     }
   }
@@ -79,6 +82,7 @@ template <int LOGM, class TW>
 __device__ __forceinline__ void warp_inv(u64 (&x)[1 << (LOGM - 5)], u64* sm, int lane, u64 q, const TW& tw) {
   constexpr int LOGE = LOGM - 5;
   constexpr int E = 1 << LOGE;
+  const u64 q2 = 2 * q;
   int s0 = LOGM - LOGE;
 #pragma unroll
   for (int lo = 0; lo < LOGM; lo += LOGE) {
@@ -95,9 +99,11 @@ __device__ __forceinline__ void warp_inv(u64 (&x)[1 << (LOGM - 5)], u64* sm, int
         const int idx = lay<LOGE>(lane, k, s0);
         u64 w, ws;
         tw(b, idx >> (b + 1), w, ws);
+        // Harvey lazy GS butterfly: operands in [0, 2q)
         const u64 U = x[k], V = x[k | (1 << rb)];
-        x[k] = add_mod(U, V, q);
-        x[k | (1 << rb)] = mul_shoup(sub_mod(U, V, q), w, ws, q);
+        const u64 S = U + V;
+        x[k] = S >= q2 ? S - q2 : S;
+        x[k | (1 << rb)] = mul_shoup_lazy(U - V + q2, w, ws, q);
       }
     }
   }
@@ -133,6 +139,12 @@ __global__ void __launch_bounds__(kWarps * 32) ntt_row_pass(LimbBatch B, Tabs T)
       ws = Ws[i];
     };
     warp_fwd<LOGC>(x, sm, lane, q, tw);
+#pragma unroll
+    for (int k = 0; k < E; ++k) {  // [0, 4q) -> canonical
+      u64 v = x[k];
+      v = v >= 2 * q ? v - 2 * q : v;
+      x[k] = v >= q ? v - q : v;
+    }
   } else {
     const u64* W = T.ipsi + ((size_t)p << LOGN);
     const u64* Ws = T.ipsi_s + ((size_t)p << LOGN);
