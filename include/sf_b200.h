@@ -189,6 +189,28 @@ sf_status sf_qk_dot(sf_context* ctx, const sf_ct* q, const sf_kvcache* cache, sf
 sf_status sf_softmax_times_v(sf_context* ctx, const sf_ct* const* probs, int n_probs, const sf_kvcache* cache,
                              sf_ct** out);
 
+/* --- sharded hot path (one process per GPU) ------------------
+ * Each rank computes its share (VMM giant steps g2 = rank mod world; QK^T key
+ * ciphertexts j = rank mod world; Score*V (group, variant) pairs by index mod
+ * world), the partial ciphertexts are exchanged (all-gather over NVLink) and
+ * summed mod q with sf_sum_partials, then the replicated tail runs.
+ * Modular sums are exact: the result is bit-identical to world = 1. */
+sf_status sf_vmm_partial(sf_context* ctx, const sf_ct* x, const sf_vmm_plan* plan, int rank, int world,
+                         sf_ct** out);
+sf_status sf_vmm_finish(sf_context* ctx, const sf_ct* acc, const sf_vmm_plan* plan, int mask_output, sf_ct** out);
+sf_status sf_qk_dot_partial(sf_context* ctx, const sf_ct* q, const sf_kvcache* cache, int rank, int world,
+                            sf_ct** maps_out, int* n_maps);
+sf_status sf_softmax_times_v_partial(sf_context* ctx, const sf_ct* const* probs, int n_probs,
+                                     const sf_kvcache* cache, int rank, int world, sf_ct** out);
+sf_status sf_softmax_times_v_finish(sf_context* ctx, const sf_ct* acc, const sf_kvcache* cache, sf_ct** out);
+sf_status sf_sum_partials(sf_context* ctx, const sf_ct* const* parts, int n, sf_ct** out);
+/* device words of a ciphertext for peer/NCCL exchange: c0 and c1 each
+ * (level+1)*n words; the view stays valid while the handle is alive */
+sf_status sf_ct_device_view(const sf_ct* ct, uint64_t** c0, uint64_t** c1, size_t* words_per_poly);
+/* new ciphertext from device words (copied on the context stream) */
+sf_status sf_ct_from_device(sf_context* ctx, const uint64_t* c0, const uint64_t* c1, int level, double scale,
+                            int is_zero, const sf_layout* layout, sf_ct** out);
+
 /* --- device timing of the last enqueued work (CUDA events on the ctx stream) */
 sf_status sf_event_record(sf_context* ctx, int slot);
 sf_status sf_event_elapsed_ms(sf_context* ctx, int slot_begin, int slot_end, float* ms);

@@ -1,0 +1,107 @@
+"""Oracle restatement of the sharded hot path (TEST INFRASTRUCTURE ONLY).
+
+Mirrors paper_2602_11470_b200/csrc/protocols.cpp (vmm_partial / vmm_finish,
+qk_dot_partial, softmax_times_v_partial / _finish) over any slotforge-shaped
+backend, so the multi-process tests can check on CPU (gloo, world_size 2) that
+partial results exchanged between ranks and summed mod q reproduce the
+single-device ciphertexts bit for bit. Ownership rules: VMM giant steps
+g2 = rank mod world; K ciphertexts j = rank mod world; Score*V (group, variant)
+pairs by running index mod world.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import protocols as P
+from .layout import Layout, make_interleaved, make_mask, stride_mask
+
+
+def vmm_partial(be, x, W, bsgs, out_offset, rank, world):
+    N = be.N
+    W = np.asarray(W, dtype=np.float64)
+    s = P.interleaved_shape(N, W.shape[0], W.shape[1], x.layout.offset, out_offset)
+    stair = x
+    step = 1
+    while step < s.t_in:
+        stair = be.add(stair, be.rotate(stair, step * (s.ladder_T - 1)))
+        step <<= 1
+    unit = s.t_in * s.t_out
+    if not bsgs:
+        own = list(range(rank, s.k, world))
+        if not own:
+            return be.zeros(x.level - 1)
+        return be.mac_plain([(be.rotate(stair, g * unit), P.interleaved_plain(s, W, g, 0)) for g in own])
+    b, giants = P.bsgs_split(s.k)
+    mine = list(range(rank, giants, world))
+    if not mine:
+        return be.zeros(x.level - 1)
+    baby = [stair] + [be.rotate(stair, g1 * unit, hoisted=True) for g1 in range(1, b)]
+    acc = None
+    for g2 in mine:
+        shift = g2 * b * unit
+        terms = [(baby[g1], P.interleaved_plain(s, W, g2 * b + g1, shift)) for g1 in range(b) if g2 * b + g1 < s.k]
+        aligned = be.rotate(be.mac_plain(terms), shift)
+        acc = aligned if acc is None else be.add(acc, aligned)
+    return acc
+
+
+def vmm_finish(be, acc, W, in_offset, out_offset, mask_output=False):
+    W = np.asarray(W)
+    s = P.interleaved_shape(be.N, W.shape[0], W.shape[1], in_offset, out_offset)
+    m = 0
+    while (1 << m) < s.t_out:
+        st = 1 << m
+        acc = be.add(acc, be.rotate(acc, -st if (s.delta >> m) & 1 else st))
+        m += 1
+    if mask_output:
+        acc = be.mul_plain(acc, stride_mask(be.N, s.t_out, s.tau_out))
+    return be.with_layout(acc, Layout("interleaved", s.d_out, s.t_out, s.tau_out, 1, not mask_output))
+
+
+def qk_dot_partial(be, q, cache, cfg, rank, world):
+    t, dh, gt = cfg.t, cfg.d_head, cfg.group_tokens
+    q_rep = P.replicate_lanes(be, q, t)
+    head_mask = make_mask(make_interleaved(cfg.d, cfg.N, 0, cfg.H), cfg.N, "replicate_extract")
+    n_maps = (cache.n_prime + gt - 1) // gt
+    maps = [None] * n_maps
+    for j in range(rank, len(cache.k_cts), world):
+        prod = P.fold_within_head(be, be.mul(q_rep, cache.k_cts[j]), dh, t)
+        masked = be.mul_plain(prod, head_mask)
+        local = (j * t) % gt
+        packed = be.rotate(masked, -local) if local else masked
+        m = (j * t) // gt
+        maps[m] = packed if maps[m] is None else be.add(maps[m], packed)
+    return [be.with_layout(m, None) if m is not None else be.zeros(q.level - 2) for m in maps]
+
+
+def softmax_times_v_partial(be, probs, cache, cfg, rank, world):
+    t, gt = cfg.t, cfg.group_tokens
+    acc, idx = None, 0
+    for g in range(len(probs)):
+        tokens = min(gt, cache.n_prime - g * gt)
+        lo, hi = P.touched_variants(cfg, tokens)
+        for w in range(lo, hi):
+            if idx % world == rank:
+                scores = be.rotate(probs[g], -w * t) if w else probs[g]
+                prod = be.mul(scores, cache.v_cts[g][P.v_variant_index(cfg, w)])
+                acc = prod if acc is None else be.add(acc, prod)
+            idx += 1
+    if acc is None:
+        return be.zeros(min(probs[0].level, cache.v_cts[0][0].level) - 1)
+    return acc
+
+
+def softmax_times_v_finish(be, acc, cfg):
+    folded = P.fold_lanes(be, acc, cfg.t)
+    out = be.mul_plain(folded, stride_mask(cfg.N, cfg.t, 0))
+    return be.with_layout(out, make_interleaved(cfg.d, cfg.N, 0, cfg.H))
+
+
+def sum_partials(be, parts):
+    live = [p for p in parts if not getattr(p, "is_zero", False)]
+    if not live:
+        return parts[0]
+    acc = live[0]
+    for p in live[1:]:
+        acc = be.add(acc, p)
+    return acc

@@ -198,7 +198,7 @@ __global__ void vmm_mac_kernel(VmmMacArgs A, const u64* Q, const u64* MH, const 
   const u64 q = Q[l], mh = MH[l], ml = ML[l];
   for (int g2 = warp; g2 < A.giants; g2 += nw) {
     U128 a0{0, 0}, a1{0, 0}, b0{0, 0}, b1{0, 0};
-    const int gbase = g2 * A.b;
+    const int gbase = A.gidx[g2] * A.b;
     const int cnt = min(A.b, A.k - gbase);
     for (int g1 = 0; g1 < cnt; ++g1) {
       const ulonglong2 p = reinterpret_cast<const ulonglong2*>(A.pt[gbase + g1] + base)[lane];

@@ -77,7 +77,8 @@ struct SubScaleBatch {  // out = (acc - conv) * inv (+ addend permuted by g)
 };
 
 struct VmmMacArgs {
-  int n = 0, b = 0, giants = 0, k = 0;
+  int n = 0, b = 0, giants = 0, k = 0;  // giants = number of outputs
+  int gidx[64];                          // global giant-step index of output i
   const u64* baby0[64];
   const u64* baby1[64];
   const u64* pt[2048];

@@ -454,6 +454,66 @@ sf_status sf_softmax_times_v(sf_context* ctx, const sf_ct* const* probs, int n_p
   });
 }
 
+// --- sharded hot path
+sf_status sf_vmm_partial(sf_context* ctx, const sf_ct* x, const sf_vmm_plan* plan, int rank, int world,
+                         sf_ct** out) {
+  return guard([&] { *out = wrap(sf::vmm_partial(*ctx->c, x->v, *plan->p, rank, world)); });
+}
+sf_status sf_vmm_finish(sf_context* ctx, const sf_ct* acc, const sf_vmm_plan* plan, int mask_output, sf_ct** out) {
+  return guard([&] { *out = wrap(sf::vmm_finish(*ctx->c, acc->v, *plan->p, mask_output != 0)); });
+}
+sf_status sf_qk_dot_partial(sf_context* ctx, const sf_ct* q, const sf_kvcache* cache, int rank, int world,
+                            sf_ct** maps_out, int* n_maps) {
+  return guard([&] {
+    auto maps = sf::qk_dot_partial(*ctx->c, q->v, cache->kv, rank, world);
+    *n_maps = (int)maps.size();
+    for (size_t i = 0; i < maps.size(); ++i) maps_out[i] = wrap(std::move(maps[i]));
+  });
+}
+sf_status sf_softmax_times_v_partial(sf_context* ctx, const sf_ct* const* probs, int n_probs,
+                                     const sf_kvcache* cache, int rank, int world, sf_ct** out) {
+  return guard([&] {
+    std::vector<sf::Ct> p;
+    for (int i = 0; i < n_probs; ++i) p.push_back(probs[i]->v);
+    *out = wrap(sf::softmax_times_v_partial(*ctx->c, p, cache->kv, rank, world));
+  });
+}
+sf_status sf_softmax_times_v_finish(sf_context* ctx, const sf_ct* acc, const sf_kvcache* cache, sf_ct** out) {
+  return guard([&] { *out = wrap(sf::softmax_times_v_finish(*ctx->c, acc->v, cache->kv)); });
+}
+sf_status sf_sum_partials(sf_context* ctx, const sf_ct* const* parts, int n, sf_ct** out) {
+  return guard([&] {
+    sf::require(n >= 1, sf::kShapeMismatch, "sum_partials: need at least one part");
+    std::vector<const sf::Ct*> p;
+    for (int i = 0; i < n; ++i) p.push_back(&parts[i]->v);
+    *out = wrap(sf::sum_partials(*ctx->c, p));
+  });
+}
+sf_status sf_ct_device_view(const sf_ct* ct, uint64_t** c0, uint64_t** c1, size_t* words_per_poly) {
+  return guard([&] {
+    need(ct, "ct");
+    const auto& v = ct->v;
+    const int n = (int)(v.buf->words / (2 * (size_t)v.stride));
+    *c0 = v.c0();
+    *c1 = v.c1(n);
+    *words_per_poly = (size_t)v.limbs * n;
+  });
+}
+sf_status sf_ct_from_device(sf_context* ctx, const uint64_t* c0, const uint64_t* c1, int level, double scale,
+                            int is_zero, const sf_layout* layout, sf_ct** out) {
+  return guard([&] {
+    auto& c = *ctx->c;
+    sf::require(level >= 0 && level <= c.L, sf::kInvalidTarget, "from_device: level out of range");
+    sf::Ct v = sf::alloc_ct(c, level + 1, scale);
+    v.zero = is_zero != 0;
+    v.layout = to_layout(layout);
+    const size_t w = (size_t)v.limbs * c.n;
+    SF_CUDA(cudaMemcpyAsync(v.c0(), c0, w * 8, cudaMemcpyDeviceToDevice, c.stream));
+    SF_CUDA(cudaMemcpyAsync(v.c1(c.n), c1, w * 8, cudaMemcpyDeviceToDevice, c.stream));
+    *out = wrap(std::move(v));
+  });
+}
+
 // --- timing
 sf_status sf_event_record(sf_context* ctx, int slot) {
   return guard([&] {

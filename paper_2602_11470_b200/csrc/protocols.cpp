@@ -123,9 +123,7 @@ std::unique_ptr<VmmPlan> make_vmm_plan(Context& c, const double* W, int rows, in
   return p;
 }
 
-// vmm.cpp:179-236 with the giant-step partial sums evaluated as one lazy MAC
-// each (sum of ct (.) pt, a single rescale), the babies sharing one ModUp.
-Ct vmm_interleaved(Context& c, const Ct& x, VmmPlan& plan, bool mask_output) {
+static void vmm_check_input(Context& c, const Ct& x, const VmmPlan& plan) {
   require(x.layout && x.layout->kind == LayoutKind::Interleaved, kLayoutMismatch,
           "vmm_interleaved: input must carry an interleaved layout");
   require(!x.layout->deferred_mask, kLayoutMismatch,
@@ -136,88 +134,95 @@ Ct vmm_interleaved(Context& c, const Ct& x, VmmPlan& plan, bool mask_output) {
               std::to_string(plan.s.d_in));
   check_ct(c, x, "vmm_interleaved");
   require(x.level() > 0, kLevelUnderflow, "mul_plain: no multiplicative level left");
+}
+
+// Steps 1-2 of vmm.cpp:179-236 for the giant steps this rank owns
+// (g2 = rank mod world; world = 1 is the whole VMM): preprocess ladder,
+// hoisted babies, the giants' lazy MACs (one rescale each), giant rotations and
+// their sum. Work every rank repeats (ladder, babies) is charged on rank 0 only,
+// so the ledgers of all ranks sum to the reference's counts.
+Ct vmm_partial(Context& c, const Ct& x, VmmPlan& plan, int rank, int world) {
+  vmm_check_input(c, x, plan);
+  require(world >= 1 && rank >= 0 && rank < world, kInvalidTarget, "vmm: bad rank/world");
+  const bool lead = rank == 0;
   const VmmShape& s = plan.s;
   const std::vector<Pt>& diag = plan.diagonals(x.limbs);
-  // 1. ladder
   Ct stair = x;
-  for (int step = 1; step < s.t_in; step <<= 1) stair = add(c, stair, rotate(c, stair, step * (s.ladder_T - 1), false));
+  for (int step = 1; step < s.t_in; step <<= 1)
+    stair = add(c, stair, rotate(c, stair, step * (s.ladder_T - 1), false, lead), false, lead);
   const long long unit = (long long)s.t_in * s.t_out;
-  Ct acc;
+  const int limbs = x.limbs;
   if (!plan.bsgs) {
     std::vector<Ct> xs;
-    xs.reserve(s.k);
-    for (long long g = 0; g < s.k; ++g) xs.push_back(rotate(c, stair, (int)(g * unit), false));
+    std::vector<long long> own;
+    for (long long g = rank; g < s.k; g += world) own.push_back(g), xs.push_back(rotate(c, stair, (int)(g * unit), false));
+    if (own.empty()) return zeros(c, x.level() - 1);
     std::vector<const Ct*> cts;
     std::vector<const Pt*> pts;
-    for (long long g = 0; g < s.k; ++g) cts.push_back(&xs[g]), pts.push_back(&diag[g]);
-    acc = mac_plain(c, cts, pts);
-  } else if (!stair.zero && plan.bg.baby <= 64 && plan.bg.giant <= 64 && s.k <= 2048 && c.n >= 64) {
-    // BSGS with every giant's partial sum produced by ONE fused MAC launch
-    // (babies staged on-chip once, each diagonal streamed once), then batched
-    // rescales, batched giant rotations and one reduction.
-    const int b = plan.bg.baby, giants = plan.bg.giant;
-    std::vector<RotJob> jobs;
-    for (int g1 = 1; g1 < b; ++g1) jobs.push_back({0, (int)(g1 * unit)});
-    std::vector<Ct> baby{stair};
-    for (Ct& r : rotate_batch(c, {&stair}, jobs, true)) baby.push_back(std::move(r));
-    c.ledger.ctpt(s.k);
-    c.ledger.add(s.k - giants);  // b-1 additions inside every giant's partial sum
-    const int limbs = x.limbs;
-    std::vector<Ct> partial(giants);
+    for (size_t i = 0; i < own.size(); ++i) cts.push_back(&xs[i]), pts.push_back(&diag[own[i]]);
+    return mac_plain(c, cts, pts);
+  }
+  const int b = plan.bg.baby, giants = plan.bg.giant;
+  std::vector<int> mine;
+  for (int g2 = rank; g2 < giants; g2 += world) mine.push_back(g2);
+  if (mine.empty()) return zeros(c, x.level() - 1);
+  std::vector<RotJob> jobs;
+  for (int g1 = 1; g1 < b; ++g1) jobs.push_back({0, (int)(g1 * unit)});
+  std::vector<Ct> baby{stair};
+  for (Ct& r : rotate_batch(c, {&stair}, jobs, true, lead)) baby.push_back(std::move(r));
+  std::vector<Ct> resc;
+  if (!stair.zero && b <= 64 && giants <= 64 && s.k <= 2048 && c.n >= 64) {
+    // every owned giant's partial sum in ONE fused MAC launch (babies staged
+    // on-chip once, each diagonal streamed once), then one batched rescale
     VmmMacArgs A;
     A.n = c.n;
     A.b = b;
-    A.giants = giants;
+    A.giants = (int)mine.size();
     A.k = (int)s.k;
     for (int g1 = 0; g1 < b; ++g1) A.baby0[g1] = baby[g1].c0(), A.baby1[g1] = baby[g1].c1(c.n);
     for (long long g = 0; g < s.k; ++g) A.pt[g] = diag[g].buf->p;
-    for (int g2 = 0; g2 < giants; ++g2) {
-      partial[g2] = alloc_ct(c, limbs, stair.scale * (double)c.primes[limbs - 1]);
-      A.out0[g2] = partial[g2].c0();
-      A.out1[g2] = partial[g2].c1(c.n);
+    std::vector<Ct> partial(mine.size());
+    for (size_t i = 0; i < mine.size(); ++i) {
+      const int cnt = (int)std::min<long long>(b, s.k - (long long)mine[i] * b);
+      c.ledger.ctpt(cnt);
+      c.ledger.add(cnt - 1);  // the reference's partial-sum additions (vmm.cpp:214-219)
+      partial[i] = alloc_ct(c, limbs, stair.scale * (double)c.primes[limbs - 1]);
+      A.gidx[i] = mine[i];
+      A.out0[i] = partial[i].c0();
+      A.out1[i] = partial[i].c1(c.n);
     }
     b_vmm_mac(c, A, limbs);
     std::vector<const Ct*> pp;
     for (auto& p : partial) pp.push_back(&p);
-    std::vector<Ct> resc = rescale_batch(c, pp);
-    std::vector<const Ct*> rp;
-    std::vector<RotJob> gj;
-    for (int g2 = 0; g2 < giants; ++g2) {
-      resc[g2].scale = stair.scale;
-      resc[g2].layout.reset();
-      rp.push_back(&resc[g2]);
-      gj.push_back({g2, (int)((long long)g2 * b * unit)});
-    }
-    std::vector<Ct> aligned = rotate_batch(c, rp, gj, false);
-    std::vector<const Ct*> ap;
-    for (auto& a : aligned) ap.push_back(&a);
-    acc = sum_cts(c, ap);
+    resc = rescale_batch(c, pp);
+    for (auto& r : resc) r.scale = stair.scale, r.layout.reset();
   } else {
-    const int b = plan.bg.baby, giants = plan.bg.giant;
-    std::vector<int> rs;
-    for (int g1 = 1; g1 < b; ++g1) rs.push_back((int)(g1 * unit));
-    std::vector<Ct> baby{stair};
-    for (Ct& r : rotate_hoisted(c, stair, rs)) baby.push_back(std::move(r));
-    for (int g2 = 0; g2 < giants; ++g2) {
-      const long long shift = (long long)g2 * b * unit;
+    for (int g2 : mine) {
       std::vector<const Ct*> cts;
       std::vector<const Pt*> pts;
-      for (int g1 = 0; g1 < b; ++g1) {
-        const long long g = (long long)g2 * b + g1;
-        if (g >= s.k) break;
-        cts.push_back(&baby[g1]);
-        pts.push_back(&diag[g]);
-      }
-      Ct aligned = rotate(c, mac_plain(c, cts, pts), (int)shift, false);
-      acc = g2 == 0 ? aligned : add(c, acc, aligned);
+      for (int g1 = 0; g1 < b && (long long)g2 * b + g1 < s.k; ++g1)
+        cts.push_back(&baby[g1]), pts.push_back(&diag[(long long)g2 * b + g1]);
+      resc.push_back(mac_plain(c, cts, pts));
     }
   }
-  // 3. reduce
+  std::vector<const Ct*> rp;
+  std::vector<RotJob> gj;
+  for (size_t i = 0; i < mine.size(); ++i) rp.push_back(&resc[i]), gj.push_back({(int)i, (int)((long long)mine[i] * b * unit)});
+  std::vector<Ct> aligned = rotate_batch(c, rp, gj, false);
+  std::vector<const Ct*> ap;
+  for (auto& a : aligned) ap.push_back(&a);
+  return sum_cts(c, ap);
+}
+
+// Steps 3-4 of vmm.cpp:179-236 on the summed partials: the reduce ladder
+// folding each t_out window onto its output offset, then mask or defer.
+Ct vmm_finish(Context& c, const Ct& acc_in, VmmPlan& plan, bool mask_output) {
+  const VmmShape& s = plan.s;
+  Ct acc = acc_in;
   for (int m = 0; (1 << m) < s.t_out; ++m) {
     const int st = 1 << m;
     acc = add(c, acc, rotate(c, acc, ((s.delta >> m) & 1) ? -st : st, false));
   }
-  // 4. mask or defer
   if (mask_output) {
     std::vector<double> mk(c.slots, 0.0);
     for (int i = s.tau_out; i < c.slots; i += s.t_out) mk[i] = 1.0;
@@ -225,6 +230,21 @@ Ct vmm_interleaved(Context& c, const Ct& x, VmmPlan& plan, bool mask_output) {
   }
   acc.layout = Layout{LayoutKind::Interleaved, s.d_out, s.t_out, s.tau_out, 1, !mask_output};
   return acc;
+}
+
+// vmm.cpp:179-236: the whole VMM on one GPU.
+Ct vmm_interleaved(Context& c, const Ct& x, VmmPlan& plan, bool mask_output) {
+  return vmm_finish(c, vmm_partial(c, x, plan, 0, 1), plan, mask_output);
+}
+
+// Sum of per-rank partial results (the exchange's modular reduction; NCCL has
+// no mod-q sum). Charges one addition per non-trivial operand beyond the first.
+Ct sum_partials(Context& c, const std::vector<const Ct*>& parts) {
+  std::vector<const Ct*> live;
+  for (const Ct* p : parts)
+    if (!p->zero) live.push_back(p);
+  if (live.empty()) return *parts[0];
+  return sum_cts(c, live);
 }
 
 // ======================================================= attention (kv_attention.cpp)
@@ -394,31 +414,43 @@ KV v_append(Context& c, const KV& cache, const std::vector<Ct>& parts) {  // kv_
 
 static int ceil_div(int a, int b) { return (a + b - 1) / b; }
 
-std::vector<Ct> qk_dot(Context& c, const Ct& q, const KV& cache) {  // kv_attention.cpp:184-214
+// kv_attention.cpp:184-214 for the K ciphertexts this rank owns (j = rank
+// mod world; world = 1 is the whole QK^T). Every K ciphertext runs the same op
+// sequence (mul, fold_within_head 38-41, mask, pack rotation), so each step is
+// one batched call over all owned ciphertexts. Returns per-map partial sums
+// (trivial zeros for maps this rank has no keys for); the lane replication of
+// q (30-34), repeated on every rank, is charged on rank 0 only.
+std::vector<Ct> qk_dot_partial(Context& c, const Ct& q, const KV& cache, int rank, int world) {
   const AttnCfg& cfg = cache.cfg;
   require(cache.n_prime != 0, kCacheEmpty, "qk_dot: no cached keys");
   require_clean_interleaved(q, cfg, 0, "qk_dot");
+  require(world >= 1 && rank >= 0 && rank < world, kInvalidTarget, "qk_dot: bad rank/world");
   const int t = cfg.t(), dh = cfg.d_head(), gt = cfg.group_tokens(), N = cfg.N;
   require((int)cache.k.size() == ceil_div(cache.n_prime, t), kShapeMismatch,
           "qk_dot: key ct count does not match n_prime");
-  // replicate_lanes (30-34)
+  const bool lead = rank == 0;
   Ct q_rep = q;
-  for (int step = 1; step < t; step <<= 1) q_rep = add(c, q_rep, rotate(c, q_rep, -step, false));
-  // ReplicateExtract head mask (layouts.cpp:134-138)
-  std::vector<double> head_mask(N, 0.0);
+  for (int step = 1; step < t; step <<= 1) q_rep = add(c, q_rep, rotate(c, q_rep, -step, false, lead), false, lead);
+  std::vector<double> head_mask(N, 0.0);  // ReplicateExtract (layouts.cpp:134-138)
   const int hb = N / cfg.H;
   for (int h = 0; h < cfg.H; ++h)
     for (int i = 0; i < t; ++i) head_mask[h * hb + i] = 1.0;
-  // Every K ciphertext runs the same op sequence (mul, fold_within_head 38-41,
-  // mask, pack rotation), so each step is one batched call over all of them.
-  const int J = (int)cache.k.size();
+  std::vector<int> own;
+  for (int j = rank; j < (int)cache.k.size(); j += world) own.push_back(j);
+  const int J = (int)own.size();
+  const int n_maps = ceil_div(cache.n_prime, gt);
+  std::vector<Ct> out;
+  if (J == 0) {
+    for (int m = 0; m < n_maps; ++m) out.push_back(zeros(c, q.level() - 2));
+    return out;
+  }
   std::vector<const Ct*> qs(J, &q_rep), ks;
-  for (const Ct& k : cache.k) ks.push_back(&k);
+  for (int j : own) ks.push_back(&cache.k[j]);
   std::vector<Ct> prod = mul_batch(c, qs, ks);
   for (int l = 0; (1 << l) < dh; ++l) {
     std::vector<const Ct*> src;
     std::vector<RotJob> jobs;
-    for (int j = 0; j < J; ++j) src.push_back(&prod[j]), jobs.push_back({j, (1 << l) * t});
+    for (int i = 0; i < J; ++i) src.push_back(&prod[i]), jobs.push_back({i, (1 << l) * t});
     std::vector<Ct> rot = rotate_batch(c, src, jobs, false);
     std::vector<const Ct*> rp;
     for (auto& r : rot) rp.push_back(&r);
@@ -427,21 +459,24 @@ std::vector<Ct> qk_dot(Context& c, const Ct& q, const KV& cache) {  // kv_attent
   const std::string hkey = "headmask:" + std::to_string(cfg.H) + ":" + std::to_string(t);
   std::vector<const Ct*> pp;
   std::vector<Pt> hm;
-  for (int j = 0; j < J; ++j) {
-    require(prod[j].level() > 0, kLevelUnderflow, "mul_plain: no multiplicative level left");
-    hm.push_back(cached_pt(c, hkey, head_mask.data(), (double)c.primes[prod[j].limbs - 1], prod[j].limbs));
+  for (int i = 0; i < J; ++i) {
+    require(prod[i].level() > 0, kLevelUnderflow, "mul_plain: no multiplicative level left");
+    hm.push_back(cached_pt(c, hkey, head_mask.data(), (double)c.primes[prod[i].limbs - 1], prod[i].limbs));
   }
   std::vector<const Pt*> hp;
-  for (int j = 0; j < J; ++j) pp.push_back(&prod[j]), hp.push_back(&hm[j]);
+  for (int i = 0; i < J; ++i) pp.push_back(&prod[i]), hp.push_back(&hm[i]);
   std::vector<Ct> masked = mul_plain_batch(c, pp, hp);
   std::vector<const Ct*> mp;
   std::vector<RotJob> pj;
-  for (int j = 0; j < J; ++j) mp.push_back(&masked[j]), pj.push_back({j, -((j * t) % gt)});
+  for (int i = 0; i < J; ++i) mp.push_back(&masked[i]), pj.push_back({i, -((own[i] * t) % gt)});
   std::vector<Ct> packed = rotate_batch(c, mp, pj, false);
-  std::vector<std::vector<const Ct*>> per_map(ceil_div(cache.n_prime, gt));
-  for (int j = 0; j < J; ++j) per_map[(j * t) / gt].push_back(&packed[j]);
-  std::vector<Ct> out;
+  std::vector<std::vector<const Ct*>> per_map(n_maps);
+  for (int i = 0; i < J; ++i) per_map[(own[i] * t) / gt].push_back(&packed[i]);
   for (auto& m : per_map) {
+    if (m.empty()) {
+      out.push_back(zeros(c, q.level() - 2));
+      continue;
+    }
     Ct s = sum_cts(c, m);
     s.layout.reset();
     out.push_back(std::move(s));
@@ -449,27 +484,35 @@ std::vector<Ct> qk_dot(Context& c, const Ct& q, const KV& cache) {  // kv_attent
   return out;
 }
 
-Ct softmax_times_v(Context& c, const std::vector<Ct>& probs, const KV& cache) {  // kv_attention.cpp:216-241
+std::vector<Ct> qk_dot(Context& c, const Ct& q, const KV& cache) { return qk_dot_partial(c, q, cache, 0, 1); }
+
+// kv_attention.cpp:216-241 (before the lane fold) for the (group, variant)
+// pairs this rank owns: all score alignments of one probability map share its
+// ModUp (hoisting); the rotations, the ct x ct products and the sum each run as
+// one batch.
+Ct softmax_times_v_partial(Context& c, const std::vector<Ct>& probs, const KV& cache, int rank, int world) {
   const AttnCfg& cfg = cache.cfg;
   require(cache.n_prime != 0, kCacheEmpty, "softmax_times_v: no cached values");
+  require(world >= 1 && rank >= 0 && rank < world, kInvalidTarget, "softmax_times_v: bad rank/world");
   const int t = cfg.t(), gt = cfg.group_tokens();
   const int n_maps = ceil_div(cache.n_prime, gt);
   require((int)probs.size() == n_maps, kShapeMismatch,
           "softmax_times_v: expected " + std::to_string(n_maps) + " probability maps, got " +
               std::to_string(probs.size()));
   require((int)cache.v.size() >= n_maps, kShapeMismatch, "softmax_times_v: value cache is missing groups");
-  // All score alignments of one probability map share its ModUp (hoisting);
-  // the rotations, the ct x ct products and the sum each run as one batch.
   std::vector<const Ct*> src;
   for (const Ct& p : probs) src.push_back(&p);
   std::vector<RotJob> jobs;
   std::vector<std::pair<int, int>> gw;
+  int idx = 0;
   for (int g = 0; g < n_maps; ++g) {
     const int tokens = std::min(gt, cache.n_prime - g * gt);
     const int u_max = (tokens - 1) / t;  // touched_variants (53-57)
     const int w_lo = cfg.H == 1 ? 0 : -u_max, w_hi = cfg.d_head();
-    for (int w = w_lo; w < w_hi; ++w) gw.push_back({g, w}), jobs.push_back({g, -w * t});
+    for (int w = w_lo; w < w_hi; ++w, ++idx)
+      if (idx % world == rank) gw.push_back({g, w}), jobs.push_back({g, -w * t});
   }
+  if (gw.empty()) return zeros(c, std::min(probs[0].level(), cache.v[0][0].level()) - 1);
   std::vector<Ct> scores = rotate_batch(c, src, jobs, false);
   std::vector<const Ct*> sa, vb;
   for (size_t i = 0; i < gw.size(); ++i) {
@@ -479,13 +522,24 @@ Ct softmax_times_v(Context& c, const std::vector<Ct>& probs, const KV& cache) { 
   std::vector<Ct> prods = mul_batch(c, sa, vb);
   std::vector<const Ct*> pp;
   for (auto& p : prods) pp.push_back(&p);
-  Ct folded = sum_cts(c, pp);
-  for (int step = 1; step < t; step <<= 1) folded = add(c, folded, rotate(c, folded, step, false));  // 44-47
+  return sum_cts(c, pp);
+}
+
+// fold_lanes (44-47) + final stride mask (238) on the summed partials.
+Ct softmax_times_v_finish(Context& c, const Ct& acc, const KV& cache) {
+  const AttnCfg& cfg = cache.cfg;
+  const int t = cfg.t();
+  Ct folded = acc;
+  for (int step = 1; step < t; step <<= 1) folded = add(c, folded, rotate(c, folded, step, false));
   std::vector<double> sm(cfg.N, 0.0);
   for (int i = 0; i < cfg.N; i += t) sm[i] = 1.0;
   Ct out = mul_plain_cached(c, folded, "stride:" + std::to_string(t) + ":0", sm);
   out.layout = make_interleaved(cfg.d, cfg.N, 0, cfg.H);
   return out;
+}
+
+Ct softmax_times_v(Context& c, const std::vector<Ct>& probs, const KV& cache) {
+  return softmax_times_v_finish(c, softmax_times_v_partial(c, probs, cache, 0, 1), cache);
 }
 
 }  // namespace sf

@@ -37,6 +37,11 @@ struct VmmPlan {
 std::unique_ptr<VmmPlan> make_vmm_plan(Context& c, const double* W, int rows, int cols, int level, int in_offset,
                                        int out_offset, bool bsgs);
 Ct vmm_interleaved(Context& c, const Ct& x, VmmPlan& plan, bool mask_output);
+// sharded form: partial over the giant steps g2 = rank mod world, then (after
+// the exchange's modular sum) the reduce ladder + mask
+Ct vmm_partial(Context& c, const Ct& x, VmmPlan& plan, int rank, int world);
+Ct vmm_finish(Context& c, const Ct& acc, VmmPlan& plan, bool mask_output);
+Ct sum_partials(Context& c, const std::vector<const Ct*>& parts);
 
 // --- attention ---------------------------------------------------------------
 struct AttnCfg {
@@ -63,6 +68,9 @@ KV k_append(Context& c, const KV& cache, const Ct& k_new);
 std::vector<Ct> make_v_pieces(Context& c, const KV& cache, const Ct& v_open, int position);
 KV v_append(Context& c, const KV& cache, const std::vector<Ct>& parts);
 std::vector<Ct> qk_dot(Context& c, const Ct& q, const KV& cache);
+std::vector<Ct> qk_dot_partial(Context& c, const Ct& q, const KV& cache, int rank, int world);
+Ct softmax_times_v_partial(Context& c, const std::vector<Ct>& probs, const KV& cache, int rank, int world);
+Ct softmax_times_v_finish(Context& c, const Ct& acc, const KV& cache);
 Ct softmax_times_v(Context& c, const std::vector<Ct>& probs, const KV& cache);
 
 }  // namespace sf
