@@ -248,6 +248,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--nvtx-step", action="store_true", help="run one NVTX-ranged step after warm-up and exit")
     ap.add_argument("--alpha", type=int, default=2, help="special primes per key-switching digit")
     ap.add_argument("--quiet", action="store_true")
     args = ap.parse_args()
@@ -278,6 +279,15 @@ def main():
     for _ in range(args.warmup):
         layer.step()
     be.synchronize()
+    if args.nvtx_step:
+        # profiling hook: one decode step inside an NVTX range, e.g.
+        #   ncu --nvtx --nvtx-include "sf_step/" ... python bench.py --nvtx-step
+        import torch
+        torch.cuda.nvtx.range_push("sf_step")
+        layer.step()
+        be.synchronize()
+        torch.cuda.nvtx.range_pop()
+        return
 
     def barrier():
         if dist:

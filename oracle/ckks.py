@@ -68,6 +68,11 @@ def lib():
             "ock_mul": (vp, [vp, vp, vp]),
             "ock_rotate": (vp, [vp, vp, C.c_int]),
             "ock_rescale": (vp, [vp, vp]),
+            "ock_tensor_sum": (vp, [vp, C.POINTER(vp), C.POINTER(vp), C.c_int]),
+            "ock_relin_rescale": (vp, [vp, vp]),
+            "ock_ct_is_three": (C.c_int, [vp]),
+            "ock_ct_d2": (None, [vp, U64P]),
+            "ock_ct_set_d2": (None, [vp, U64P]),
             "ock_level_drop": (vp, [vp, vp, C.c_int]),
         }
         for name, (res, args) in sig.items():
@@ -135,10 +140,17 @@ class OCt:
         return self.info()[2]
 
     def data(self) -> np.ndarray:
+        """[2][limbs][n] words, or [3][limbs][n] for a degree-2 (lazily
+        relinearised) ciphertext."""
         limbs, _, _ = self.info()
         out = np.empty(2 * limbs * self.ctx.n, dtype=np.uint64)
         lib().ock_ct_data(self.ptr, _u64(out))
-        return out.reshape(2, limbs, self.ctx.n)
+        out = out.reshape(2, limbs, self.ctx.n)
+        if lib().ock_ct_is_three(self.ptr):
+            d2 = np.empty(limbs * self.ctx.n, dtype=np.uint64)
+            lib().ock_ct_d2(self.ptr, _u64(d2))
+            out = np.concatenate([out, d2.reshape(1, limbs, self.ctx.n)])
+        return out
 
 
 @dataclass
@@ -238,8 +250,37 @@ class CkksOracle:
         return out
 
     def import_ct(self, data: np.ndarray, level: int, scale: float, layout=None, zero=False) -> OCt:
-        d = np.ascontiguousarray(data, dtype=np.uint64)
-        return OCt(self, lib().ock_import(self.ptr, _u64(d), level + 1, scale, int(zero)), level, layout)
+        """Words [2|3][level+1][n] (3 = degree-2 ciphertext)."""
+        d = np.ascontiguousarray(data, dtype=np.uint64).reshape(-1)
+        w = (level + 1) * self.n
+        ct = OCt(self, lib().ock_import(self.ptr, _u64(d[:2 * w].copy()), level + 1, scale, int(zero)), level,
+                 layout)
+        if d.size == 3 * w:
+            lib().ock_ct_set_d2(ct.ptr, _u64(d[2 * w:].copy()))
+        return ct
+
+    # --- lazily relinearised products (DESIGN.md §3.6; Score*V)
+    def tensor_sum(self, pairs) -> OCt:
+        """sum of ct x ct products kept as a degree-2 ciphertext (no relin);
+        charged k ct-ct mults and k-1 additions like the reference chain."""
+        for a, b in pairs:
+            self._check(a, "mul"), self._check(b, "mul")
+            if min(a.level, b.level) <= 0:
+                raise LevelUnderflow("mul: no multiplicative level left")
+        for i, _ in enumerate(pairs):
+            self.ledger.count_ct_ct()
+            if i:
+                self.ledger.count_add()
+        aa = (C.c_void_p * len(pairs))(*[a.ptr for a, _ in pairs])
+        bb = (C.c_void_p * len(pairs))(*[b.ptr for _, b in pairs])
+        lvl = min(min(a.level, b.level) for a, b in pairs)
+        return OCt(self, lib().ock_tensor_sum(self.ptr, aa, bb, len(pairs)), lvl, None)
+
+    def relin_rescale(self, x) -> OCt:
+        return OCt(self, lib().ock_relin_rescale(self.ptr, x.ptr), x.level - 1, None)
+
+    def mul_sum(self, pairs) -> OCt:
+        return self.relin_rescale(self.tensor_sum(pairs))
 
     # --- evaluator ops (ledger-charged)
     def add(self, a, b):

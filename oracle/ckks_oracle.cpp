@@ -106,7 +106,8 @@ u64 to_mod(i64 v, u64 q) {
 }
 
 struct Ct {
-  std::vector<u64> d;  // [2][limbs][n]
+  std::vector<u64> d;   // [2][limbs][n]
+  std::vector<u64> d2;  // degree-2 part [limbs][n] of a lazily relinearised sum (empty otherwise)
   int limbs = 0;
   double scale = 0.0;
   bool zero = false;
@@ -461,14 +462,20 @@ Ct* addsub(const Ctx& c, const Ct* a, const Ct* b, bool sub) {
   }
   check_scales(a, b);
   Ct* r = new_ct(c, limbs, a->zero ? b->scale : a->scale);
+  const bool three = !a->d2.empty() || !b->d2.empty();
+  if (three) r->d2.assign((size_t)limbs * c.n, 0);
 #pragma omp parallel for
   for (int l = 0; l < limbs; ++l) {
     const u64 q = c.primes[l];
-    for (int p = 0; p < 2; ++p) {
-      const u64* x = poly(c, a, p, l);
-      const u64* y = poly(c, b, p, l);
-      u64* o = poly(c, r, p, l);
-      for (int k = 0; k < c.n; ++k) o[k] = sub ? submod(x[k], y[k], q) : addmod(x[k], y[k], q);
+    for (int p = 0; p < 3; ++p) {
+      if (p == 2 && !three) break;
+      const u64* x = p < 2 ? poly(c, a, p, l) : (a->d2.empty() ? nullptr : a->d2.data() + (size_t)l * c.n);
+      const u64* y = p < 2 ? poly(c, b, p, l) : (b->d2.empty() ? nullptr : b->d2.data() + (size_t)l * c.n);
+      u64* o = p < 2 ? poly(c, r, p, l) : r->d2.data() + (size_t)l * c.n;
+      for (int k = 0; k < c.n; ++k) {
+        const u64 xv = x ? x[k] : 0, yv = y ? y[k] : 0;
+        o[k] = sub ? submod(xv, yv, q) : addmod(xv, yv, q);
+      }
     }
   }
   return r;
@@ -654,6 +661,68 @@ Ct* mul(Ctx& c, const Ct* a, const Ct* b) {
     for (int k = 0; k < n; ++k) {
       o0[k] = addmod(o0[k], kb[(size_t)l * n + k], q);
       o1[k] = addmod(o1[k], ka[(size_t)l * n + k], q);
+    }
+  }
+  Ct* r = rescale(c, t);
+  delete t;
+  return r;
+}
+
+// Lazily relinearised sum of ct x ct products: (d0, d1, d2) =
+// sum_i tensor(a_i, b_i), kept as a degree-2 ciphertext until relin_rescale.
+Ct* tensor_sum(Ctx& c, const Ct* const* a, const Ct* const* b, int k) {
+  int limbs = 1 << 30;
+  double scale = 0.0;
+  for (int i = 0; i < k; ++i) {
+    limbs = std::min(limbs, std::min(a[i]->limbs, b[i]->limbs));
+    if (a[i]->zero || b[i]->zero) continue;
+    const double s = a[i]->scale * b[i]->scale;
+    if (scale == 0.0)
+      scale = s;
+    else if (std::fabs(s / scale - 1.0) > 1e-9)
+      throw std::runtime_error("ScaleMismatch: add: operand scales differ");
+  }
+  Ct* r = new_ct(c, limbs, scale);
+  r->d2.assign((size_t)limbs * c.n, 0);
+  r->zero = scale == 0.0;
+  const int n = c.n;
+#pragma omp parallel for
+  for (int l = 0; l < limbs; ++l) {
+    const u64 q = c.primes[l];
+    u64* o0 = poly(c, r, 0, l);
+    u64* o1 = poly(c, r, 1, l);
+    u64* o2 = r->d2.data() + (size_t)l * n;
+    for (int i = 0; i < k; ++i) {
+      if (a[i]->zero || b[i]->zero) continue;
+      const u64 *a0 = poly(c, a[i], 0, l), *a1 = poly(c, a[i], 1, l), *b0 = poly(c, b[i], 0, l),
+                *b1 = poly(c, b[i], 1, l);
+      for (int j = 0; j < n; ++j) {
+        o0[j] = addmod(o0[j], mulmod(a0[j], b0[j], q), q);
+        o1[j] = addmod(o1[j], addmod(mulmod(a0[j], b1[j], q), mulmod(a1[j], b0[j], q), q), q);
+        o2[j] = addmod(o2[j], mulmod(a1[j], b1[j], q), q);
+      }
+    }
+  }
+  return r;
+}
+
+Ct* relin_rescale(Ctx& c, const Ct* x) {
+  const int limbs = x->limbs, n = c.n;
+  if (x->zero) {
+    Ct* z = new_ct(c, limbs - 1, 0.0);
+    z->zero = true;
+    return z;
+  }
+  if (x->d2.empty()) throw std::runtime_error("relin_rescale: not a degree-2 ciphertext");
+  std::vector<u64> kb((size_t)limbs * n), ka((size_t)limbs * n);
+  key_switch(c, x->d2.data(), limbs, 0, kb.data(), ka.data());
+  Ct* t = new_ct(c, limbs, x->scale);
+#pragma omp parallel for
+  for (int l = 0; l < limbs; ++l) {
+    const u64 q = c.primes[l];
+    for (int k = 0; k < n; ++k) {
+      poly(c, t, 0, l)[k] = addmod(poly(c, x, 0, l)[k], kb[(size_t)l * n + k], q);
+      poly(c, t, 1, l)[k] = addmod(poly(c, x, 1, l)[k], ka[(size_t)l * n + k], q);
     }
   }
   Ct* r = rescale(c, t);
@@ -856,6 +925,21 @@ void* ock_mul(void* c, void* a, void* b) {
 }
 void* ock_rotate(void* c, void* a, int r) {
   return guard([&]() -> void* { return rotate(*static_cast<Ctx*>(c), (Ct*)a, r); });
+}
+void* ock_tensor_sum(void* c, void** a, void** b, int k) {
+  return guard([&]() -> void* { return tensor_sum(*static_cast<Ctx*>(c), (Ct* const*)a, (Ct* const*)b, k); });
+}
+void* ock_relin_rescale(void* c, void* a) {
+  return guard([&]() -> void* { return relin_rescale(*static_cast<Ctx*>(c), (Ct*)a); });
+}
+int ock_ct_is_three(void* ct) { return static_cast<Ct*>(ct)->d2.empty() ? 0 : 1; }
+void ock_ct_d2(void* ct, uint64_t* out) {
+  auto* x = static_cast<Ct*>(ct);
+  std::copy(x->d2.begin(), x->d2.end(), out);
+}
+void ock_ct_set_d2(void* ct, const uint64_t* in) {
+  auto* x = static_cast<Ct*>(ct);
+  x->d2.assign(in, in + (size_t)x->limbs * (x->d.size() / (2 * (size_t)x->limbs)));
 }
 void* ock_rescale(void* c, void* a) {
   return guard([&]() -> void* { return rescale(*static_cast<Ctx*>(c), (Ct*)a); });

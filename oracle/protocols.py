@@ -427,14 +427,16 @@ def softmax_times_v(be, probs, cache: KVCache, cfg):
         raise ShapeMismatch(f"softmax_times_v: expected {n_maps} probability maps, got {len(probs)}")
     if len(cache.v_cts) < n_maps:
         raise ShapeMismatch("softmax_times_v: value cache is missing groups")
-    acc = None
+    pairs = []
     for g in range(n_maps):
         tokens = min(gt, cache.n_prime - g * gt)
         lo, hi = touched_variants(cfg, tokens)
         for w in range(lo, hi):
             scores = be.rotate(probs[g], -w * t) if w else probs[g]
-            prod = be.mul(scores, cache.v_cts[g][v_variant_index(cfg, w)])
-            acc = prod if acc is None else be.add(acc, prod)
+            pairs.append((scores, cache.v_cts[g][v_variant_index(cfg, w)]))
+    # sum of the products (kv_attention.cpp:230-235); CKKS backends evaluate it
+    # with one lazy relinearisation, same ledger charge
+    acc = be.mul_sum(pairs)
     folded = fold_lanes(be, acc, t)
     out = be.mul_plain(folded, stride_mask(cfg.N, t, 0))
     return be.with_layout(out, make_interleaved(cfg.d, cfg.N, 0, cfg.H))

@@ -75,24 +75,25 @@ def qk_dot_partial(be, q, cache, cfg, rank, world):
 
 
 def softmax_times_v_partial(be, probs, cache, cfg, rank, world):
+    """The rank's degree-2 (lazily relinearised) product sum."""
     t, gt = cfg.t, cfg.group_tokens
-    acc, idx = None, 0
+    pairs, idx = [], 0
     for g in range(len(probs)):
         tokens = min(gt, cache.n_prime - g * gt)
         lo, hi = P.touched_variants(cfg, tokens)
         for w in range(lo, hi):
             if idx % world == rank:
                 scores = be.rotate(probs[g], -w * t) if w else probs[g]
-                prod = be.mul(scores, cache.v_cts[g][P.v_variant_index(cfg, w)])
-                acc = prod if acc is None else be.add(acc, prod)
+                pairs.append((scores, cache.v_cts[g][P.v_variant_index(cfg, w)]))
             idx += 1
-    if acc is None:
-        return be.zeros(min(probs[0].level, cache.v_cts[0][0].level) - 1)
-    return acc
+    if not pairs:
+        return be.zeros(min(probs[0].level, cache.v_cts[0][0].level))
+    return be.tensor_sum(pairs)
 
 
-def softmax_times_v_finish(be, acc, cfg):
-    folded = P.fold_lanes(be, acc, cfg.t)
+def softmax_times_v_finish(be, parts, cfg):
+    """Sum the degree-2 partials, relinearise + rescale once, fold, mask."""
+    folded = P.fold_lanes(be, be.relin_rescale(sum_partials(be, parts)), cfg.t)
     out = be.mul_plain(folded, stride_mask(cfg.N, cfg.t, 0))
     return be.with_layout(out, make_interleaved(cfg.d, cfg.N, 0, cfg.H))
 

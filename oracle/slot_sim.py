@@ -201,6 +201,15 @@ class SimBackend:
             acc = t if acc is None else self.add(acc, t)
         return acc
 
+    def mul_sum(self, pairs):
+        """sum_i a_i * b_i charged as the reference's mul/add chain
+        (kv_attention.cpp:230-235)."""
+        acc = None
+        for a, b in pairs:
+            t = self.mul(a, b)
+            acc = t if acc is None else self.add(acc, t)
+        return acc
+
     def rotate(self, a, r: int, hoisted: bool = False):
         self._check(a, "rotate")
         s = r % self.N

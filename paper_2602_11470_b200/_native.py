@@ -94,7 +94,7 @@ SIGNATURES = {
     "sf_vmm_finish": (st, [vp, vp, vp, C.c_int, vpp]),
     "sf_qk_dot_partial": (st, [vp, vp, vp, C.c_int, C.c_int, vpp, ip]),
     "sf_softmax_times_v_partial": (st, [vp, vpp, C.c_int, vp, C.c_int, C.c_int, vpp]),
-    "sf_softmax_times_v_finish": (st, [vp, vp, vp, vpp]),
+    "sf_softmax_times_v_finish": (st, [vp, vpp, vpp, C.c_int, vp, vpp]),
     "sf_sum_partials": (st, [vp, vpp, C.c_int, vpp]),
     "sf_ct_device_view": (st, [vp, C.POINTER(u64p), C.POINTER(u64p), C.POINTER(C.c_size_t)]),
     "sf_ct_from_device": (st, [vp, C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_int, C.POINTER(SfLayout), vpp]),

@@ -99,6 +99,32 @@ __global__ void tensor_batch_kernel(TensorBatch B, int limbs, int n, const u64* 
   }
 }
 
+// Lazily relinearised sum of ct x ct products (Score*V): 128-bit accumulation,
+// folded back to a residue every 16 terms (16 * 2 * q^2 < 2^127 for q < 2^61).
+__global__ void tensor_sum_kernel(TensorSumArgs A, int limbs, int n, const u64* Q, const u64* MH, const u64* ML) {
+  const size_t total = (size_t)limbs * n;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const int l = (int)(i / n);
+    const u64 q = Q[l], mh = MH[l], ml = ML[l];
+    U128 s0{A.accumulate ? A.d0[i] : 0, 0}, s1{A.accumulate ? A.d1[i] : 0, 0}, s2{A.accumulate ? A.d2[i] : 0, 0};
+    for (int k = 0; k < A.k; ++k) {
+      const u64 x0 = A.a0[k][i], x1 = A.a1[k][i], y0 = A.b0[k][i], y1 = A.b1[k][i];
+      mac128(s0, x0, y0);
+      mac128(s1, x0, y1);
+      mac128(s1, x1, y0);
+      mac128(s2, x1, y1);
+      if ((k & 15) == 15) {
+        s0 = {reduce128(s0.hi, s0.lo, q, mh, ml), 0};
+        s1 = {reduce128(s1.hi, s1.lo, q, mh, ml), 0};
+        s2 = {reduce128(s2.hi, s2.lo, q, mh, ml), 0};
+      }
+    }
+    A.d0[i] = reduce128(s0.hi, s0.lo, q, mh, ml);
+    A.d1[i] = reduce128(s1.hi, s1.lo, q, mh, ml);
+    A.d2[i] = reduce128(s2.hi, s2.lo, q, mh, ml);
+  }
+}
+
 __global__ void lift_batch_kernel(LiftBatch B, int limbs, int n, u64 ql, const u64* Q, const u64* MH) {
   const int j = blockIdx.y;
   const size_t total = (size_t)limbs * n;
@@ -254,6 +280,39 @@ void b_tensor(Context& c, const TensorBatch& B, int limbs) {
   ProfScope prof(c, kFamElem, 56.0 * limbs * c.n * B.count);
   tensor_batch_kernel<<<grid2((size_t)limbs * c.n, B.count), kT, 0, c.stream>>>(B, limbs, c.n, c.tabs.q, c.tabs.mh,
                                                                                   c.tabs.ml);
+  post(c);
+}
+
+// One NTT row pass moves 8n bytes in and 8n out per limb; the fused column
+// stage reads ns and writes nd limbs (its transforms stay in shared memory).
+void b_row(Context& c, const LimbBatch& b, bool inverse) {
+  if (!b.count) return;
+  ProfScope prof(c, kFamNtt, 16.0 * c.n * b.count);
+  ntt_row_only(c, b, inverse);
+  post(c);
+}
+
+void b_fused_col(Context& c, const FusedColArgs& A) {
+  if (!A.count) return;
+  ProfScope prof(c, kFamNtt, 8.0 * c.n * (A.ns + A.nd) * A.count);
+  ntt_fused_col(c, A);
+  post(c);
+}
+
+void b_row_epi(Context& c, const EpiBatch& E) {
+  if (!E.count) return;
+  // row pass in + acc + addend + out
+  double bytes = 0;
+  for (int i = 0; i < E.count; ++i) bytes += 8.0 * c.n * (E.addend[i] ? 4 : 3);
+  ProfScope prof(c, kFamNtt, bytes);
+  ntt_row_epi(c, E);
+  post(c);
+}
+
+void b_tensor_sum(Context& c, const TensorSumArgs& A, int limbs) {
+  ProfScope prof(c, kFamMac, 8.0 * limbs * c.n * (4.0 * A.k + 3));
+  tensor_sum_kernel<<<grid2((size_t)limbs * c.n, 1), kT, 0, c.stream>>>(A, limbs, c.n, c.tabs.q, c.tabs.mh,
+                                                                        c.tabs.ml);
   post(c);
 }
 

@@ -86,7 +86,53 @@ struct VmmMacArgs {
   u64* out1[64];
 };
 
+struct TensorSumArgs {  // (D0, D1, D2) = sum_i tensor(a_i, b_i), no relinearisation
+  int k = 0;
+  const u64 *a0[512], *a1[512], *b0[512], *b1[512];
+  u64 *d0, *d1, *d2;
+  bool accumulate = false;  // add into existing (D0, D1, D2)
+};
+
+// Fused column stage of ModUp / ModDown / rescale (fused.cu): per job, the
+// inverse column NTT of ns source limbs (already inverse-row-passed), the
+// basis conversion (mode 0) or rescale lift (mode 1) into nd destination limbs
+// in shared memory, and their forward column NTT; the destination limbs then
+// need only the forward row pass. Source limbs of job j: src[j] + s*n;
+// destination limb d: dst[j] + out_slot[d]*n.
+struct FusedColArgs {
+  int count = 0, ns = 0, nd = 0, mode = 0;
+  int src_prime[kMaxPrimes], dst_prime[kMaxPrimes], out_slot[kMaxPrimes];
+  const u64 *qinv = nullptr, *qinv_s = nullptr, *qhat = nullptr;  // mode 0 (ConvPlan tables)
+  u64 q_last = 0;                                                  // mode 1
+  const u64* src[kJobsWide];
+  u64* dst[kJobsWide];
+};
+
+// Forward row pass with the ModDown / rescale combine as epilogue:
+// out = (acc - NTT(buf)) * inv (+ addend[perm_g]) on limb `prime`.
+struct EpiBatch {
+  int count = 0;
+  u64* buf[kJobsWide];
+  const u64* acc[kJobsWide];
+  const u64* addend[kJobsWide];
+  u64* out[kJobsWide];
+  u64 g[kJobsWide];
+  u64 inv[kJobsWide], inv_s[kJobsWide];
+  uint8_t prime[kJobsWide];
+};
+
+// ntt.cu dispatchers (false when the ring degree has no two-pass kernels)
+bool ntt_row_only(Context& c, const LimbBatch& b, bool inverse);
+bool ntt_row_epi(Context& c, const EpiBatch& e);
+bool ntt_fused_col(Context& c, const FusedColArgs& a);
+inline bool fused_path(const Context& c) { return c.logn >= 12 && c.logn <= 17 && c.alpha <= 8; }
+// profiled launch wrappers (batch.cu)
+void b_row(Context& c, const LimbBatch& b, bool inverse);
+void b_fused_col(Context& c, const FusedColArgs& A);
+void b_row_epi(Context& c, const EpiBatch& E);
+
 void b_copy(Context& c, const CopyBatch& B, size_t words);
+void b_tensor_sum(Context& c, const TensorSumArgs& A, int limbs);
 void b_add(Context& c, const AddBatch& B, int limbs);
 void b_sum(Context& c, const SumArgs& A, int limbs);
 void b_mulpt(Context& c, const MulPtBatch& B, int limbs);
@@ -117,5 +163,19 @@ std::vector<Ct> add_batch(Context& c, const std::vector<const Ct*>& a, const std
                           bool count = true);
 // sum of k same-level ciphertexts, charged k-1 additions
 Ct sum_cts(Context& c, const std::vector<const Ct*>& xs, bool count = true);
+
+// Degree-2 ciphertext (d0, d1, d2) decrypting under (1, s, s^2): the lazily
+// relinearised sum of ct x ct products. d01 holds (d0, d1); d2 lives in the
+// c0 polynomial of its own Ct (c1 unused, zero).
+struct Ct3 {
+  Ct d01, d2;
+  bool zero = true;
+};
+// sum_i a_i (x) b_i without relinearisation; charged k ct-ct mults and k-1 additions
+Ct3 tensor_sum(Context& c, const std::vector<const Ct*>& a, const std::vector<const Ct*>& b, bool count = true);
+// component-wise sum of degree-2 partials (no ledger charge)
+Ct3 add_ct3(Context& c, const std::vector<const Ct3*>& xs);
+// relinearise (key switch d2 under s^2) and rescale
+Ct relin_rescale(Context& c, const Ct3& x);
 
 }  // namespace sf

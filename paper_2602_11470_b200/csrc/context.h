@@ -124,9 +124,11 @@ constexpr int kMaxBatch = 1024;
 struct LimbBatch {
   int count = 0;
   u64* ptr[kMaxBatch];
+  u64* optr[kMaxBatch];  // out-of-place destination (nullptr: in place); row passes only
   uint8_t prime[kMaxBatch];
-  void add(u64* p, int prime_idx) {
+  void add(u64* p, int prime_idx, u64* out = nullptr) {
     ptr[count] = p;
+    optr[count] = out;
     prime[count] = (uint8_t)prime_idx;
     ++count;
   }
@@ -170,6 +172,7 @@ struct Context {
   std::map<std::string, ConvPlan> conv_plans;
   std::map<std::string, Pt> pt_cache;  // semantic-key plaintext cache (masks)
   std::map<int, BufPtr> level_consts;  // per-limb-count rescale / moddown constants
+  std::map<int, std::vector<u64>> level_consts_h;  // host copies (row-pass epilogue parameters)
 
   Ledger ledger;
   u64 enc_counter = 0;

@@ -173,6 +173,7 @@ const u64* level_consts(Context& c, int limbs) {
   SF_CUDA(cudaMemcpyAsync(b->p, h.data(), h.size() * sizeof(u64), cudaMemcpyHostToDevice, c.stream));
   SF_CUDA(cudaStreamSynchronize(c.stream));  // h goes out of scope
   c.level_consts[limbs] = b;
+  c.level_consts_h[limbs] = h;
   return b->p;
 }
 

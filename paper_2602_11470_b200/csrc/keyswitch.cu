@@ -9,6 +9,7 @@
 // Hoisting falls out of the definition: jobs that share a source share one
 // ModUp (RotationHint{hoisted}, engine.hpp:98-100).
 #include <algorithm>
+#include <cmath>
 #include <map>
 
 #include "batch.cuh"
@@ -61,6 +62,54 @@ ExtB mod_up_batch(Context& c, const std::vector<const u64*>& d, int limbs) {
   for (int t = 0; t < x.nt; ++t) x.tprime.push_back(t < limbs ? t : c.P_index(t - limbs));
   x.per = (size_t)x.ndig * x.nt * n;
   BufPtr dcoef = make_buf(c, (size_t)x.S * limbs * n);
+  if (fused_path(c)) {
+    // inverse row pass (out of place) -> per digit: fused [inverse column pass,
+    // conversion, forward column pass] straight into ext -> forward row pass
+    LimbBatch lb;
+    for (int s = 0; s < x.S; ++s)
+      for (int l = 0; l < limbs; ++l) {
+        lb.add(const_cast<u64*>(d[s]) + (size_t)l * n, l, dcoef->p + ((size_t)s * limbs + l) * n);
+        if (lb.count == kMaxBatch) b_row(c, lb, true), lb.count = 0;
+      }
+    if (lb.count) b_row(c, lb, true), lb.count = 0;
+    x.buf = make_buf(c, (size_t)x.S * x.per);
+    for (int j = 0; j < x.ndig; ++j) {
+      const int lo = j * c.alpha, hi = std::min((j + 1) * c.alpha, limbs);
+      std::vector<int> src, dst, slot;
+      for (int i = lo; i < hi; ++i) src.push_back(i);
+      for (int t = 0; t < x.nt; ++t)
+        if (t < lo || t >= hi) dst.push_back(x.tprime[t]), slot.push_back(t);
+      const ConvPlan& plan = conv_plan(c, src, dst);
+      FusedColArgs A;
+      A.ns = hi - lo;
+      A.nd = (int)dst.size();
+      A.mode = 0;
+      A.qinv = plan.tab->p;
+      A.qinv_s = plan.tab->p + plan.nsrc;
+      A.qhat = plan.tab->p + 2 * plan.nsrc;
+      for (int i = 0; i < A.ns; ++i) A.src_prime[i] = src[i];
+      for (int k = 0; k < A.nd; ++k) A.dst_prime[k] = dst[k], A.out_slot[k] = slot[k];
+      CopyBatch cb;
+      auto ext_of = [&](int s) { return x.buf->p + (size_t)s * x.per + (size_t)j * x.nt * n; };
+      for (int s = 0; s < x.S; ++s) {
+        A.src[A.count] = dcoef->p + ((size_t)s * limbs + lo) * n;
+        A.dst[A.count++] = ext_of(s);
+        if (A.count == kJobsWide) b_fused_col(c, A), A.count = 0;
+        cb.src[cb.count] = d[s] + (size_t)lo * n;  // own primes: the exact NTT-domain residues
+        cb.dst[cb.count++] = ext_of(s) + (size_t)lo * n;
+        if (cb.count == kJobsWide) b_copy(c, cb, (size_t)(hi - lo) * n), cb.count = 0;
+      }
+      if (A.count) b_fused_col(c, A);
+      b_copy(c, cb, (size_t)(hi - lo) * n);
+      for (int s = 0; s < x.S; ++s)
+        for (size_t k = 0; k < slot.size(); ++k) {
+          lb.add(ext_of(s) + (size_t)slot[k] * n, dst[k]);
+          if (lb.count == kMaxBatch) b_row(c, lb, false), lb.count = 0;
+        }
+      if (lb.count) b_row(c, lb, false), lb.count = 0;
+    }
+    return x;
+  }
   {
     CopyBatch cb;
     for (int s = 0; s < x.S; ++s) {
@@ -145,6 +194,56 @@ void ks_jobs(Context& c, const ExtB& x, const std::vector<KsJob>& jobs) {
     }
     kb.count = J;
     b_ks(c, kb);
+    if (fused_path(c)) {
+      // ModDown of 2J polynomials: inverse row pass of the P limbs (in place),
+      // fused [inverse column, P -> Q conversion, forward column], then the
+      // forward row pass with the (acc - conv) * P^-1 (+ addend) epilogue
+      const std::vector<u64>& kh = c.level_consts_h[limbs];
+      LimbBatch lb;
+      for (int j = 0; j < J; ++j)
+        for (int poly = 0; poly < 2; ++poly)
+          for (int k = 0; k < c.alpha; ++k) {
+            lb.add(accp(j, poly) + (size_t)(limbs + k) * n, pidx[k]);
+            if (lb.count == kMaxBatch) b_row(c, lb, true), lb.count = 0;
+          }
+      b_row(c, lb, true);
+      BufPtr conv = make_buf(c, (size_t)J * 2 * limbs * n);
+      FusedColArgs A;
+      A.ns = c.alpha;
+      A.nd = limbs;
+      A.qinv = down.tab->p;
+      A.qinv_s = down.tab->p + down.nsrc;
+      A.qhat = down.tab->p + 2 * down.nsrc;
+      for (int k = 0; k < c.alpha; ++k) A.src_prime[k] = pidx[k];
+      for (int l = 0; l < limbs; ++l) A.dst_prime[l] = l, A.out_slot[l] = l;
+      for (int j = 0; j < J; ++j)
+        for (int poly = 0; poly < 2; ++poly) {
+          A.src[A.count] = accp(j, poly) + (size_t)limbs * n;
+          A.dst[A.count++] = conv->p + ((size_t)j * 2 + poly) * limbs * n;
+        }
+      b_fused_col(c, A);
+      EpiBatch E;
+      for (int j = 0; j < J; ++j) {
+        const KsJob& jb = jobs[s0 + j];
+        for (int poly = 0; poly < 2; ++poly) {
+          const u64* add = poly ? jb.add1 : jb.add0;
+          u64* out = poly ? jb.out1 : jb.out0;
+          for (int l = 0; l < limbs; ++l) {
+            E.buf[E.count] = conv->p + (((size_t)j * 2 + poly) * limbs + l) * n;
+            E.acc[E.count] = accp(j, poly) + (size_t)l * n;
+            E.addend[E.count] = add ? add + (size_t)l * n : nullptr;
+            E.out[E.count] = out + (size_t)l * n;
+            E.g[E.count] = jb.g;
+            E.inv[E.count] = kh[2 * limbs + l];
+            E.inv_s[E.count] = kh[3 * limbs + l];
+            E.prime[E.count++] = (uint8_t)l;
+            if (E.count == kJobsWide) b_row_epi(c, E), E.count = 0;
+          }
+        }
+      }
+      b_row_epi(c, E);
+      continue;
+    }
     // ModDown of 2J polynomials
     LimbBatch lb;
     for (int j = 0; j < J; ++j)
@@ -193,6 +292,65 @@ std::vector<Ct> rescale_batch(Context& c, const std::vector<const Ct*>& xs) {
     const int L1 = limbs - 1;
     require(L1 >= 1, kLevelUnderflow, "rescale: no prime left to drop");
     const u64* kc = level_consts(c, limbs);
+    if (fused_path(c)) {
+      // inverse row pass of the top limb (out of place), fused [inverse column,
+      // centred lift to the remaining primes, forward column], then the forward
+      // row pass with the (c_i - lift_i) * q_top^-1 epilogue
+      const std::vector<u64>& kh = c.level_consts_h[limbs];
+      for (size_t s0 = 0; s0 < idx.size(); s0 += kJobs) {
+        const int J = (int)std::min<size_t>(kJobs, idx.size() - s0);
+        BufPtr last = make_buf(c, (size_t)2 * J * n);
+        BufPtr lift = make_buf(c, (size_t)2 * J * L1 * n);
+        LimbBatch lb;
+        FusedColArgs A;
+        A.ns = 1;
+        A.nd = L1;
+        A.mode = 1;
+        A.q_last = c.primes[L1];
+        A.src_prime[0] = L1;
+        for (int l = 0; l < L1; ++l) A.dst_prime[l] = l, A.out_slot[l] = l;
+        EpiBatch E;
+        auto flush_epi = [&]() {
+          b_row_epi(c, E);
+          E.count = 0;
+        };
+        std::vector<std::array<const u64*, 2>> srcs(J);
+        for (int j = 0; j < J; ++j) {
+          const Ct& x = *xs[idx[s0 + j]];
+          Ct r = alloc_ct(c, L1, x.scale / (double)c.primes[L1]);
+          r.zero = x.zero;
+          r.layout = x.layout;
+          for (int poly = 0; poly < 2; ++poly) {
+            const u64* src = poly ? x.c1(c.n) : x.c0();
+            u64* lp = last->p + (size_t)(2 * j + poly) * n;
+            lb.add(const_cast<u64*>(src) + (size_t)L1 * n, L1, lp);
+            A.src[A.count] = lp;
+            A.dst[A.count++] = lift->p + (size_t)(2 * j + poly) * L1 * n;
+          }
+          out[idx[s0 + j]] = r;
+        }
+        b_row(c, lb, true);
+        b_fused_col(c, A);
+        for (int j = 0; j < J; ++j) {
+          const Ct& x = *xs[idx[s0 + j]];
+          const Ct& r = out[idx[s0 + j]];
+          for (int poly = 0; poly < 2; ++poly)
+            for (int l = 0; l < L1; ++l) {
+              E.buf[E.count] = lift->p + ((size_t)(2 * j + poly) * L1 + l) * n;
+              E.acc[E.count] = (poly ? x.c1(c.n) : x.c0()) + (size_t)l * n;
+              E.addend[E.count] = nullptr;
+              E.out[E.count] = (poly ? r.c1(c.n) : r.c0()) + (size_t)l * n;
+              E.g[E.count] = 0;
+              E.inv[E.count] = kh[l];
+              E.inv_s[E.count] = kh[limbs + l];
+              E.prime[E.count++] = (uint8_t)l;
+              if (E.count == kJobsWide) flush_epi();
+            }
+        }
+        flush_epi();
+      }
+      continue;
+    }
     for (size_t s0 = 0; s0 < idx.size(); s0 += kJobs) {
       const int J = (int)std::min<size_t>(kJobs, idx.size() - s0);
       BufPtr last = make_buf(c, (size_t)2 * J * n);
@@ -348,6 +506,78 @@ std::vector<Ct> mul_batch(Context& c, const std::vector<const Ct*>& a, const std
 }
 
 Ct mul(Context& c, const Ct& a, const Ct& b, bool count) { return mul_batch(c, {&a}, {&b}, count)[0]; }
+
+// ------------------------------------------------- lazily relinearised sums
+Ct3 tensor_sum(Context& c, const std::vector<const Ct*>& a, const std::vector<const Ct*>& b, bool count) {
+  require(a.size() == b.size() && !a.empty(), kShapeMismatch, "tensor_sum: operand count");
+  int limbs = 1 << 30;
+  double scale = 0.0;
+  std::vector<int> live;
+  for (size_t i = 0; i < a.size(); ++i) {
+    check_ct(c, *a[i], "mul");
+    check_ct(c, *b[i], "mul");
+    const int l = std::min(a[i]->limbs, b[i]->limbs);
+    require(l - 1 > 0, kLevelUnderflow, "mul: no multiplicative level left");
+    limbs = std::min(limbs, l);
+    if (a[i]->zero || b[i]->zero) continue;
+    const double s = a[i]->scale * b[i]->scale;
+    if (scale == 0.0)
+      scale = s;
+    else if (std::fabs(s / scale - 1.0) > 1e-9)
+      fail(kScaleMismatch, "ScaleMismatch: add: operand scales differ");
+    live.push_back((int)i);
+  }
+  if (count) {
+    c.ledger.ctct((long long)a.size());
+    c.ledger.add((long long)a.size() - 1);
+  }
+  Ct3 r;
+  if (live.empty()) {
+    r.d01 = zeros(c, limbs - 1);
+    r.d2 = zeros(c, limbs - 1);
+    return r;
+  }
+  r.zero = false;
+  r.d01 = alloc_ct(c, limbs, scale);
+  r.d2 = alloc_ct(c, limbs, scale);
+  SF_CUDA(cudaMemsetAsync(r.d2.c1(c.n), 0, (size_t)limbs * c.n * 8, c.stream));
+  TensorSumArgs A;
+  A.d0 = r.d01.c0();
+  A.d1 = r.d01.c1(c.n);
+  A.d2 = r.d2.c0();
+  for (size_t s = 0; s < live.size();) {
+    A.k = 0;
+    for (; s < live.size() && A.k < 512; ++s) {
+      const Ct &x = *a[live[s]], &y = *b[live[s]];
+      A.a0[A.k] = x.c0(), A.a1[A.k] = x.c1(c.n), A.b0[A.k] = y.c0(), A.b1[A.k] = y.c1(c.n);
+      ++A.k;
+    }
+    b_tensor_sum(c, A, limbs);
+    A.accumulate = true;
+  }
+  return r;
+}
+
+Ct3 add_ct3(Context& c, const std::vector<const Ct3*>& xs) {
+  std::vector<const Ct*> a, b;
+  for (const Ct3* x : xs)
+    if (!x->zero) a.push_back(&x->d01), b.push_back(&x->d2);
+  if (a.empty()) return *xs[0];
+  Ct3 r;
+  r.zero = false;
+  r.d01 = sum_cts(c, a, false);
+  r.d2 = sum_cts(c, b, false);
+  return r;
+}
+
+Ct relin_rescale(Context& c, const Ct3& x) {
+  if (x.zero) return zeros(c, x.d01.level() - 1);
+  const int limbs = std::min(x.d01.limbs, x.d2.limbs);
+  ExtB e = mod_up_batch(c, {x.d2.c0()}, limbs);
+  Ct t = alloc_ct(c, limbs, x.d01.scale);
+  ks_jobs(c, e, {KsJob{0, 0, x.d01.c0(), x.d01.c1(c.n), t.c0(), t.c1(c.n)}});
+  return rescale(c, t);
+}
 
 // ------------------------------------------------------------- ct x pt mult
 std::vector<Ct> mul_plain_batch(Context& c, const std::vector<const Ct*>& xs, const std::vector<const Pt*>& ps,

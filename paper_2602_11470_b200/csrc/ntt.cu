@@ -1,114 +1,28 @@
-// Batched negacyclic NTT / inverse NTT over 64-bit RNS limbs, sm_100a.
+// Batched negacyclic NTT / inverse NTT over 64-bit RNS limbs, sm_100a, and the
+// fused column kernel of ModUp / ModDown / rescale.
 //
 // n = R x C (R = 2^r rows, C = 2^c columns, element (row, col) at row*C+col).
 // Forward (Cooley-Tukey, natural -> bit-reversed): the first r stages have
 // butterfly distance >= C and act within columns (column pass), the last c
 // stages act within rows (row pass). Inverse (Gentleman-Sande) runs the row
-// pass first, then the column pass, folding n^-1 into the last stage.
+// pass first, then the column pass, folding n^-1 into the last stage. Every
+// sub-transform is owned by one warp (warp_ntt.cuh). A launch covers any number
+// of limbs (LimbBatch), so one launch touches every limb of a whole batch of
+// ciphertexts.
 //
-// Each sub-NTT of m = 32 * E points is owned by ONE warp: every lane holds E
-// residues in registers, all butterflies of a group of log2(E) stages are
-// register-local, and the warp re-distributes residues between groups through a
-// private swizzled shared-memory region (no __syncthreads inside a transform).
-// Global loads/stores are 256-byte coalesced rows (row pass) or 64-byte row
-// segments staged through shared memory (column pass). A launch covers any
-// number of limbs (the LimbBatch), so one launch of a ModUp / ModDown / rescale
-// touches every limb of every ciphertext in the batch.
-#include "context.h"
-#include "kernels.cuh"
-#include "modarith.cuh"
+// Fusion: basis conversion / rescale lifting is elementwise over
+// coefficients, so it runs in shared memory between the inverse column pass of
+// its source limbs and the forward column pass of its destination limbs, and
+// the ModDown / rescale combine runs as the epilogue of the forward row pass:
+// ModUp, ModDown and rescale each cost three passes over HBM instead of six.
+#include "batch.cuh"
+#include "warp_ntt.cuh"
 
 namespace sf {
 namespace {
 
+using namespace wntt;
 constexpr int kWarps = 8;  // sub-NTTs per CTA
-
-// 64-bit-bank swizzle inside a warp region (16 x 8-byte banks per half warp)
-__device__ __forceinline__ int swz(int i) { return i ^ ((i >> 4) & 15); }
-
-// index of register k of `lane` when register bits are [s0, s0 + LOGE)
-template <int LOGE>
-__device__ __forceinline__ int lay(int lane, int k, int s0) {
-  return (lane & ((1 << s0) - 1)) | (k << s0) | ((lane >> s0) << (s0 + LOGE));
-}
-
-template <int LOGE>
-__device__ __forceinline__ void relayout(u64 (&x)[1 << LOGE], u64* sm, int lane, int from, int to) {
-  if (from == to) return;
-#pragma unroll
-  for (int k = 0; k < (1 << LOGE); ++k) sm[swz(lay<LOGE>(lane, k, from))] = x[k];
-  __syncwarp();
-#pragma unroll
-  for (int k = 0; k < (1 << LOGE); ++k) x[k] = sm[swz(lay<LOGE>(lane, k, to))];
-  __syncwarp();
-}
-
-// Forward sub-NTT (CT). Entry/exit layout: s0 = LOGM - LOGE (lane = low 5 bits).
-// tw(b, blk) -> (w, w_shoup) for the stage of butterfly distance 2^b.
-template <int LOGM, class TW>
-__device__ __forceinline__ void warp_fwd(u64 (&x)[1 << (LOGM - 5)], u64* sm, int lane, u64 q, const TW& tw) {
-  constexpr int LOGE = LOGM - 5;
-  constexpr int E = 1 << LOGE;
-  const u64 q2 = 2 * q;
-  int s0 = LOGM - LOGE;
-#pragma unroll
-  for (int hi = LOGM; hi > 0; hi -= LOGE) {
-    const int lo = hi - LOGE > 0 ? hi - LOGE : 0;
-    relayout<LOGE>(x, sm, lane, s0, lo);
-    s0 = lo;
-#pragma unroll
-    for (int b = hi - 1; b >= lo; --b) {
-      const int rb = b - s0;
-#pragma unroll
-      for (int k = 0; k < E; ++k) {
-        if (k & (1 << rb)) continue;
-        const int idx = lay<LOGE>(lane, k, s0);
-        u64 w, ws;
-        tw(b, idx >> (b + 1), w, ws);
-        // Harvey lazy CT butterfly: operands in [0, 4q), T in [0, 2q)
-        u64 U = x[k];
-        U = U >= q2 ? U - q2 : U;
-        const u64 T = mul_shoup_lazy(x[k | (1 << rb)], w, ws, q);
-        x[k] = U + T;
-        x[k | (1 << rb)] = U - T + q2;
-      }
-    }
-  }
-  relayout<LOGE>(x, sm, lane, s0, LOGM - LOGE);
-}
-
-// Inverse sub-NTT (GS), same entry/exit layout.
-template <int LOGM, class TW>
-__device__ __forceinline__ void warp_inv(u64 (&x)[1 << (LOGM - 5)], u64* sm, int lane, u64 q, const TW& tw) {
-  constexpr int LOGE = LOGM - 5;
-  constexpr int E = 1 << LOGE;
-  const u64 q2 = 2 * q;
-  int s0 = LOGM - LOGE;
-#pragma unroll
-  for (int lo = 0; lo < LOGM; lo += LOGE) {
-    const int hi = lo + LOGE < LOGM ? lo + LOGE : LOGM;
-    const int ns0 = hi - LOGE > 0 ? hi - LOGE : 0;
-    relayout<LOGE>(x, sm, lane, s0, ns0);
-    s0 = ns0;
-#pragma unroll
-    for (int b = lo; b < hi; ++b) {
-      const int rb = b - s0;
-#pragma unroll
-      for (int k = 0; k < E; ++k) {
-        if (k & (1 << rb)) continue;
-        const int idx = lay<LOGE>(lane, k, s0);
-        u64 w, ws;
-        tw(b, idx >> (b + 1), w, ws);
-        // Harvey lazy GS butterfly: operands in [0, 2q)
-        const u64 U = x[k], V = x[k | (1 << rb)];
-        const u64 S = U + V;
-        x[k] = S >= q2 ? S - q2 : S;
-        x[k | (1 << rb)] = mul_shoup_lazy(U - V + q2, w, ws, q);
-      }
-    }
-  }
-  relayout<LOGE>(x, sm, lane, s0, LOGM - LOGE);
-}
 
 // ---------------------------------------------------------------- row pass
 // Warp w of a CTA transforms row (tile*kWarps + w) of its limb (C = 2^LOGC).
@@ -122,7 +36,8 @@ __global__ void __launch_bounds__(kWarps * 32) ntt_row_pass(LimbBatch B, Tabs T)
   const int row = tile * kWarps + warp;
   const int p = B.prime[entry];
   const u64 q = T.q[p];
-  u64* a = B.ptr[entry] + (size_t)row * C;
+  const u64* a = B.ptr[entry] + (size_t)row * C;
+  u64* o = (B.optr[entry] ? B.optr[entry] : B.ptr[entry]) + (size_t)row * C;
   u64* sm = sm_all + warp * C;
   u64 x[E];
 #pragma unroll
@@ -140,11 +55,7 @@ __global__ void __launch_bounds__(kWarps * 32) ntt_row_pass(LimbBatch B, Tabs T)
     };
     warp_fwd<LOGC>(x, sm, lane, q, tw);
 #pragma unroll
-    for (int k = 0; k < E; ++k) {  // [0, 4q) -> canonical
-      u64 v = x[k];
-      v = v >= 2 * q ? v - 2 * q : v;
-      x[k] = v >= q ? v - q : v;
-    }
+    for (int k = 0; k < E; ++k) x[k] = canon4(x[k], q);
   } else {
     const u64* W = T.ipsi + ((size_t)p << LOGN);
     const u64* Ws = T.ipsi_s + ((size_t)p << LOGN);
@@ -157,7 +68,45 @@ __global__ void __launch_bounds__(kWarps * 32) ntt_row_pass(LimbBatch B, Tabs T)
     warp_inv<LOGC>(x, sm, lane, q, tw);
   }
 #pragma unroll
-  for (int k = 0; k < E; ++k) a[lane + 32 * k] = x[k];
+  for (int k = 0; k < E; ++k) o[lane + 32 * k] = x[k];
+}
+
+// Forward row pass + combine epilogue (EpiBatch): out = (acc - v) * inv (+ addend).
+template <int LOGR, int LOGC>
+__global__ void __launch_bounds__(kWarps * 32) ntt_row_epi(EpiBatch B, Tabs T) {
+  constexpr int C = 1 << LOGC, E = C / 32, LOGN = LOGR + LOGC;
+  constexpr int tiles = (1 << LOGR) / kWarps;
+  __shared__ u64 sm_all[kWarps * C];
+  const int entry = blockIdx.x / tiles, tile = blockIdx.x - entry * tiles;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = tile * kWarps + warp;
+  const int p = B.prime[entry];
+  const u64 q = T.q[p];
+  const u64* a = B.buf[entry] + (size_t)row * C;
+  u64* sm = sm_all + warp * C;
+  u64 x[E];
+#pragma unroll
+  for (int k = 0; k < E; ++k) x[k] = a[lane + 32 * k];
+  const u64* W = T.psi + ((size_t)p << LOGN);
+  const u64* Ws = T.psi_s + ((size_t)p << LOGN);
+  auto tw = [&](int b, int blk, u64& w, u64& ws) {
+    const int sp = LOGC - 1 - b;
+    const int i = (1 << (LOGR + sp)) + (row << sp) + blk;
+    w = W[i];
+    ws = Ws[i];
+  };
+  warp_fwd<LOGC>(x, sm, lane, q, tw);
+  const u64* acc = B.acc[entry];
+  const u64* addend = B.addend[entry];
+  const u64 g = B.g[entry], inv = B.inv[entry], inv_s = B.inv_s[entry];
+  u64* out = B.out[entry];
+#pragma unroll
+  for (int k = 0; k < E; ++k) {
+    const int i = row * C + lane + 32 * k;
+    u64 v = mul_shoup(sub_mod(acc[i], canon4(x[k], q), q), inv, inv_s, q);
+    if (addend) v = add_mod(v, addend[g > 1 ? auto_perm((uint32_t)i, g, LOGN) : i], q);
+    out[i] = v;
+  }
 }
 
 // ------------------------------------------------------------- column pass
@@ -184,7 +133,6 @@ __global__ void __launch_bounds__(kWarps * 32) ntt_col_pass(LimbBatch B, Tabs T)
       tw_s[R + i] = Ws[i];
     }
   }
-  // stage the R x kWarps tile: element (row, col) -> column region col
   for (int e = threadIdx.x; e < R * kWarps; e += blockDim.x) {
     const int row = e / kWarps, col = e % kWarps;
     sm_all[col * PAD + swz(row)] = a[(size_t)row * C + col];
@@ -195,21 +143,16 @@ __global__ void __launch_bounds__(kWarps * 32) ntt_col_pass(LimbBatch B, Tabs T)
 #pragma unroll
   for (int k = 0; k < E; ++k) x[k] = sm[swz(lane + 32 * k)];
   __syncwarp();
+  // column stage with distance 2^b rows: forward global stage r-1-b uses
+  // psi[2^(r-1-b) + blk]; GS: h = n / (2 * 2^b * C) = 2^(r-1-b)
+  auto tw = [&](int b, int blk, u64& w, u64& ws) {
+    const int i = (1 << (LOGR - 1 - b)) + blk;
+    w = tw_s[i];
+    ws = tw_s[R + i];
+  };
   if (!INV) {
-    // column stage with distance 2^b (rows) is global stage r-1-b: psi[2^(r-1-b) + blk]
-    auto tw = [&](int b, int blk, u64& w, u64& ws) {
-      const int i = (1 << (LOGR - 1 - b)) + blk;
-      w = tw_s[i];
-      ws = tw_s[R + i];
-    };
-    warp_fwd<LOGR>(x, sm, lane, q, tw);
+    warp_fwd<LOGR>(x, sm, lane, q, tw);  // lazy output in [0, 4q): the row pass accepts it
   } else {
-    // GS distance 2^b rows = 2^b * C words: h = n / (2 t) = 2^(r-1-b)
-    auto tw = [&](int b, int blk, u64& w, u64& ws) {
-      const int i = (1 << (LOGR - 1 - b)) + blk;
-      w = tw_s[i];
-      ws = tw_s[R + i];
-    };
     warp_inv<LOGR>(x, sm, lane, q, tw);
     const u64 ni = T.ninv[p], nis = T.ninv_s[p];
 #pragma unroll
@@ -221,6 +164,111 @@ __global__ void __launch_bounds__(kWarps * 32) ntt_col_pass(LimbBatch B, Tabs T)
   for (int e = threadIdx.x; e < R * kWarps; e += blockDim.x) {
     const int row = e / kWarps, col = e % kWarps;
     a[(size_t)row * C + col] = sm_all[col * PAD + swz(row)];
+  }
+}
+
+// ------------------------------------------------------------ fused column
+// One CTA = one job x TCF columns. Shared memory holds ns + nd column tiles.
+constexpr int TCF = 4;
+
+template <int LOGR, int LOGC>
+__global__ void __launch_bounds__(kWarps * 32) fused_col_kernel(FusedColArgs A, Tabs T) {
+  constexpr int R = 1 << LOGR, C = 1 << LOGC, E = R / 32, LOGN = LOGR + LOGC;
+  constexpr int PAD = R + 1;
+  constexpr int tiles = C / TCF;
+  extern __shared__ u64 sm_all[];  // [(ns + nd) * TCF][PAD]
+  const int job = blockIdx.x / tiles, tile = blockIdx.x - job * tiles;
+  const int col0 = tile * TCF;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = T.n;
+  const u64* src = A.src[job];
+  u64* dst = A.dst[job];
+  auto region = [&](int limb, int col) { return sm_all + (size_t)(limb * TCF + col) * PAD; };
+  // 1. stage the source tiles (32-byte row segments)
+  for (int e = threadIdx.x; e < A.ns * R * TCF; e += blockDim.x) {
+    const int s = e / (R * TCF), rem = e - s * R * TCF, row = rem / TCF, col = rem - row * TCF;
+    region(s, col)[swz(row)] = src[(size_t)s * n + (size_t)row * C + col0 + col];
+  }
+  __syncthreads();
+  // 2. inverse column NTT of every (source limb, column)
+  for (int task = warp; task < A.ns * TCF; task += kWarps) {
+    const int s = task / TCF, col = task - s * TCF;
+    const int p = A.src_prime[s];
+    const u64 q = T.q[p];
+    const u64* W = T.ipsi + ((size_t)p << LOGN);
+    const u64* Ws = T.ipsi_s + ((size_t)p << LOGN);
+    auto tw = [&](int b, int blk, u64& w, u64& ws) {
+      const int i = (1 << (LOGR - 1 - b)) + blk;
+      w = W[i];
+      ws = Ws[i];
+    };
+    u64* sm = region(s, col);
+    u64 x[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k) x[k] = sm[swz(lane + 32 * k)];
+    __syncwarp();
+    warp_inv<LOGR>(x, sm, lane, q, tw);
+    const u64 ni = T.ninv[p], nis = T.ninv_s[p];
+#pragma unroll
+    for (int k = 0; k < E; ++k) sm[swz(lane + 32 * k)] = mul_shoup(x[k], ni, nis, q);
+    __syncwarp();
+  }
+  __syncthreads();
+  // 3. conversion into the destination tiles (coefficient domain)
+  for (int e = threadIdx.x; e < R * TCF; e += blockDim.x) {
+    const int row = e / TCF, col = e - row * TCF;
+    const int r = swz(row);
+    if (A.mode == 0) {
+      u64 y[8];  // ns <= alpha <= 8 (fused_path); compile-time indexing keeps y in registers
+#pragma unroll
+      for (int s = 0; s < 8; ++s)
+        if (s < A.ns) y[s] = mul_shoup(region(s, col)[r], A.qinv[s], A.qinv_s[s], T.q[A.src_prime[s]]);
+      for (int d = 0; d < A.nd; ++d) {
+        U128 acc{0, 0};
+#pragma unroll
+        for (int s = 0; s < 8; ++s)
+          if (s < A.ns) mac128(acc, y[s], A.qhat[(size_t)s * A.nd + d]);
+        const int pd = A.dst_prime[d];
+        region(A.ns + d, col)[r] = reduce128(acc.hi, acc.lo, T.q[pd], T.mh[pd], T.ml[pd]);
+      }
+    } else {  // rescale lift: centred x mod q_last reduced mod each destination prime
+      const u64 v = region(0, col)[r];
+      for (int d = 0; d < A.nd; ++d) {
+        const int pd = A.dst_prime[d];
+        const u64 q = T.q[pd];
+        const u64 rr = reduce64(v, q, T.mh[pd]);
+        region(A.ns + d, col)[r] = v > (A.q_last >> 1) ? sub_mod(rr, reduce64(A.q_last, q, T.mh[pd]), q) : rr;
+      }
+    }
+  }
+  __syncthreads();
+  // 4. forward column NTT of every (destination limb, column)
+  for (int task = warp; task < A.nd * TCF; task += kWarps) {
+    const int d = task / TCF, col = task - d * TCF;
+    const int p = A.dst_prime[d];
+    const u64 q = T.q[p];
+    const u64* W = T.psi + ((size_t)p << LOGN);
+    const u64* Ws = T.psi_s + ((size_t)p << LOGN);
+    auto tw = [&](int b, int blk, u64& w, u64& ws) {
+      const int i = (1 << (LOGR - 1 - b)) + blk;
+      w = W[i];
+      ws = Ws[i];
+    };
+    u64* sm = region(A.ns + d, col);
+    u64 x[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k) x[k] = sm[swz(lane + 32 * k)];
+    __syncwarp();
+    warp_fwd<LOGR>(x, sm, lane, q, tw);
+#pragma unroll
+    for (int k = 0; k < E; ++k) sm[swz(lane + 32 * k)] = x[k];
+    __syncwarp();
+  }
+  __syncthreads();
+  // 5. store the destination tiles (lazy [0, 4q) values; the row pass accepts them)
+  for (int e = threadIdx.x; e < A.nd * R * TCF; e += blockDim.x) {
+    const int d = e / (R * TCF), rem = e - d * R * TCF, row = rem / TCF, col = rem - row * TCF;
+    dst[(size_t)A.out_slot[d] * n + (size_t)row * C + col0 + col] = region(A.ns + d, col)[swz(row)];
   }
 }
 
@@ -237,18 +285,52 @@ void run_two_pass(Context& c, const LimbBatch& b, bool inverse) {
   }
 }
 
+template <int LOGR, int LOGC>
+void run_row(Context& c, const LimbBatch& b, bool inverse) {
+  const unsigned grid = (unsigned)b.count * ((1u << LOGR) / kWarps);
+  if (inverse)
+    ntt_row_pass<LOGR, LOGC, true><<<grid, kWarps * 32, 0, c.stream>>>(b, c.tabs);
+  else
+    ntt_row_pass<LOGR, LOGC, false><<<grid, kWarps * 32, 0, c.stream>>>(b, c.tabs);
+}
+
+template <int LOGR, int LOGC>
+void run_epi(Context& c, const EpiBatch& e) {
+  const unsigned grid = (unsigned)e.count * ((1u << LOGR) / kWarps);
+  ntt_row_epi<LOGR, LOGC><<<grid, kWarps * 32, 0, c.stream>>>(e, c.tabs);
+}
+
+template <int LOGR, int LOGC>
+void run_fused(Context& c, const FusedColArgs& a) {
+  constexpr int R = 1 << LOGR;
+  const size_t sm = (size_t)(a.ns + a.nd) * TCF * (R + 1) * sizeof(u64);
+  static int configured = 0;
+  if (!configured) {
+    SF_CUDA(cudaFuncSetAttribute(fused_col_kernel<LOGR, LOGC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 200 * 1024));
+    configured = 1;
+  }
+  require(sm <= 200 * 1024, kInternal, "fused column stage: too many limbs for shared memory");
+  const unsigned grid = (unsigned)a.count * ((1u << LOGC) / TCF);
+  fused_col_kernel<LOGR, LOGC><<<grid, kWarps * 32, sm, c.stream>>>(a, c.tabs);
+}
+
+#define SF_NTT_DISPATCH(FN, ...)                        \
+  switch (c.logn) {                                     \
+    case 12: FN<6, 6>(c, __VA_ARGS__); return true;     \
+    case 13: FN<6, 7>(c, __VA_ARGS__); return true;     \
+    case 14: FN<7, 7>(c, __VA_ARGS__); return true;     \
+    case 15: FN<7, 8>(c, __VA_ARGS__); return true;     \
+    case 16: FN<8, 8>(c, __VA_ARGS__); return true;     \
+    case 17: FN<8, 9>(c, __VA_ARGS__); return true;     \
+    default: return false;                              \
+  }
+
 }  // namespace
 
-bool ntt_two_pass(Context& c, const LimbBatch& b, bool inverse) {
-  switch (c.logn) {
-    case 12: run_two_pass<6, 6>(c, b, inverse); return true;
-    case 13: run_two_pass<6, 7>(c, b, inverse); return true;
-    case 14: run_two_pass<7, 7>(c, b, inverse); return true;
-    case 15: run_two_pass<7, 8>(c, b, inverse); return true;
-    case 16: run_two_pass<8, 8>(c, b, inverse); return true;
-    case 17: run_two_pass<8, 9>(c, b, inverse); return true;
-    default: return false;
-  }
-}
+bool ntt_two_pass(Context& c, const LimbBatch& b, bool inverse) { SF_NTT_DISPATCH(run_two_pass, b, inverse) }
+bool ntt_row_only(Context& c, const LimbBatch& b, bool inverse) { SF_NTT_DISPATCH(run_row, b, inverse) }
+bool ntt_row_epi(Context& c, const EpiBatch& e) { SF_NTT_DISPATCH(run_epi, e) }
+bool ntt_fused_col(Context& c, const FusedColArgs& a) { SF_NTT_DISPATCH(run_fused, a) }
 
 }  // namespace sf

@@ -488,9 +488,11 @@ std::vector<Ct> qk_dot(Context& c, const Ct& q, const KV& cache) { return qk_dot
 
 // kv_attention.cpp:216-241 (before the lane fold) for the (group, variant)
 // pairs this rank owns: all score alignments of one probability map share its
-// ModUp (hoisting); the rotations, the ct x ct products and the sum each run as
-// one batch.
-Ct softmax_times_v_partial(Context& c, const std::vector<Ct>& probs, const KV& cache, int rank, int world) {
+// ModUp (hoisting), the rotations run as one batch, and the products are
+// accumulated as degree-2 tensors without relinearisation (lazy relin): the
+// reference's 510 ct-ct mults + 509 additions (kv_attention.cpp:230-235) cost
+// one key switch and one rescale in softmax_times_v_finish instead of 510.
+Ct3 softmax_times_v_partial(Context& c, const std::vector<Ct>& probs, const KV& cache, int rank, int world) {
   const AttnCfg& cfg = cache.cfg;
   require(cache.n_prime != 0, kCacheEmpty, "softmax_times_v: no cached values");
   require(world >= 1 && rank >= 0 && rank < world, kInvalidTarget, "softmax_times_v: bad rank/world");
@@ -512,24 +514,29 @@ Ct softmax_times_v_partial(Context& c, const std::vector<Ct>& probs, const KV& c
     for (int w = w_lo; w < w_hi; ++w, ++idx)
       if (idx % world == rank) gw.push_back({g, w}), jobs.push_back({g, -w * t});
   }
-  if (gw.empty()) return zeros(c, std::min(probs[0].level(), cache.v[0][0].level()) - 1);
+  if (gw.empty()) {
+    Ct3 z;
+    z.d01 = z.d2 = zeros(c, std::min(probs[0].level(), cache.v[0][0].level()));
+    return z;
+  }
   std::vector<Ct> scores = rotate_batch(c, src, jobs, false);
   std::vector<const Ct*> sa, vb;
   for (size_t i = 0; i < gw.size(); ++i) {
     sa.push_back(&scores[i]);
     vb.push_back(&cache.v[gw[i].first][v_variant_index(cfg, gw[i].second)]);
   }
-  std::vector<Ct> prods = mul_batch(c, sa, vb);
-  std::vector<const Ct*> pp;
-  for (auto& p : prods) pp.push_back(&p);
-  return sum_cts(c, pp);
+  return tensor_sum(c, sa, vb);
 }
 
-// fold_lanes (44-47) + final stride mask (238) on the summed partials.
-Ct softmax_times_v_finish(Context& c, const Ct& acc, const KV& cache) {
+// Sum of the ranks' degree-2 partials, one relinearisation + rescale, then
+// fold_lanes (44-47) and the final stride mask (238).
+Ct softmax_times_v_finish(Context& c, const std::vector<const Ct3*>& parts, const KV& cache) {
   const AttnCfg& cfg = cache.cfg;
   const int t = cfg.t();
-  Ct folded = acc;
+  long long live = 0;
+  for (const Ct3* p : parts) live += p->zero ? 0 : 1;
+  if (live > 1) c.ledger.add(live - 1);
+  Ct folded = relin_rescale(c, add_ct3(c, parts));
   for (int step = 1; step < t; step <<= 1) folded = add(c, folded, rotate(c, folded, step, false));
   std::vector<double> sm(cfg.N, 0.0);
   for (int i = 0; i < cfg.N; i += t) sm[i] = 1.0;
@@ -539,7 +546,8 @@ Ct softmax_times_v_finish(Context& c, const Ct& acc, const KV& cache) {
 }
 
 Ct softmax_times_v(Context& c, const std::vector<Ct>& probs, const KV& cache) {
-  return softmax_times_v_finish(c, softmax_times_v_partial(c, probs, cache, 0, 1), cache);
+  Ct3 p = softmax_times_v_partial(c, probs, cache, 0, 1);
+  return softmax_times_v_finish(c, {&p}, cache);
 }
 
 }  // namespace sf

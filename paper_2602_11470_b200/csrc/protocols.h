@@ -4,6 +4,7 @@
 #pragma once
 #include <functional>
 
+#include "batch.cuh"
 #include "context.h"
 
 namespace sf {
@@ -69,8 +70,8 @@ std::vector<Ct> make_v_pieces(Context& c, const KV& cache, const Ct& v_open, int
 KV v_append(Context& c, const KV& cache, const std::vector<Ct>& parts);
 std::vector<Ct> qk_dot(Context& c, const Ct& q, const KV& cache);
 std::vector<Ct> qk_dot_partial(Context& c, const Ct& q, const KV& cache, int rank, int world);
-Ct softmax_times_v_partial(Context& c, const std::vector<Ct>& probs, const KV& cache, int rank, int world);
-Ct softmax_times_v_finish(Context& c, const Ct& acc, const KV& cache);
+Ct3 softmax_times_v_partial(Context& c, const std::vector<Ct>& probs, const KV& cache, int rank, int world);
+Ct softmax_times_v_finish(Context& c, const std::vector<const Ct3*>& parts, const KV& cache);
 Ct softmax_times_v(Context& c, const std::vector<Ct>& probs, const KV& cache);
 
 }  // namespace sf

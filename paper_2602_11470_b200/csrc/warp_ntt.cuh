@@ -1,0 +1,115 @@
+// Warp-level negacyclic sub-NTT building blocks (used by ntt.cu and fused.cu).
+//
+// A sub-transform of m = 32 * E points is owned by ONE warp: every lane holds E
+// residues in registers, all butterflies of a group of log2(E) stages are
+// register-local, and the warp re-distributes residues between groups through
+// a private swizzled shared-memory region (__syncwarp only). Butterflies are
+// Harvey-lazy: forward operands live in [0, 4q), inverse operands in [0, 2q);
+// callers normalise at the end of a full transform.
+#pragma once
+#include "context.h"
+#include "modarith.cuh"
+
+namespace sf {
+namespace wntt {
+
+// 64-bit-bank swizzle inside a warp region (16 x 8-byte banks per half warp)
+__device__ __forceinline__ int swz(int i) { return i ^ ((i >> 4) & 15); }
+
+// index of register k of `lane` when register bits are [s0, s0 + LOGE)
+template <int LOGE>
+__device__ __forceinline__ int lay(int lane, int k, int s0) {
+  return (lane & ((1 << s0) - 1)) | (k << s0) | ((lane >> s0) << (s0 + LOGE));
+}
+
+template <int LOGE>
+__device__ __forceinline__ void relayout(u64 (&x)[1 << LOGE], u64* sm, int lane, int from, int to) {
+  if (from == to) return;
+#pragma unroll
+  for (int k = 0; k < (1 << LOGE); ++k) sm[swz(lay<LOGE>(lane, k, from))] = x[k];
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < (1 << LOGE); ++k) x[k] = sm[swz(lay<LOGE>(lane, k, to))];
+  __syncwarp();
+}
+
+// Forward sub-NTT (Cooley-Tukey). Entry/exit layout: lane = low 5 index bits.
+// tw(b, blk, w, ws) gives the twiddle (and Shoup companion) of the stage with
+// butterfly distance 2^b for block blk.
+template <int LOGM, class TW>
+__device__ __forceinline__ void warp_fwd(u64 (&x)[1 << (LOGM - 5)], u64* sm, int lane, u64 q, const TW& tw) {
+  constexpr int LOGE = LOGM - 5;
+  constexpr int E = 1 << LOGE;
+  const u64 q2 = 2 * q;
+  int s0 = LOGM - LOGE;
+#pragma unroll
+  for (int hi = LOGM; hi > 0; hi -= LOGE) {
+    const int lo = hi - LOGE > 0 ? hi - LOGE : 0;
+    relayout<LOGE>(x, sm, lane, s0, lo);
+    s0 = lo;
+#pragma unroll
+    for (int b = hi - 1; b >= lo; --b) {
+      const int rb = b - s0;
+#pragma unroll
+      for (int k = 0; k < E; ++k) {
+        if (k & (1 << rb)) continue;
+        const int idx = lay<LOGE>(lane, k, s0);
+        u64 w, ws;
+        tw(b, idx >> (b + 1), w, ws);
+        u64 U = x[k];
+        U = U >= q2 ? U - q2 : U;
+        const u64 T = mul_shoup_lazy(x[k | (1 << rb)], w, ws, q);
+        x[k] = U + T;
+        x[k | (1 << rb)] = U - T + q2;
+      }
+    }
+  }
+  relayout<LOGE>(x, sm, lane, s0, LOGM - LOGE);
+}
+
+// Inverse sub-NTT (Gentleman-Sande), same entry/exit layout.
+template <int LOGM, class TW>
+__device__ __forceinline__ void warp_inv(u64 (&x)[1 << (LOGM - 5)], u64* sm, int lane, u64 q, const TW& tw) {
+  constexpr int LOGE = LOGM - 5;
+  constexpr int E = 1 << LOGE;
+  const u64 q2 = 2 * q;
+  int s0 = LOGM - LOGE;
+#pragma unroll
+  for (int lo = 0; lo < LOGM; lo += LOGE) {
+    const int hi = lo + LOGE < LOGM ? lo + LOGE : LOGM;
+    const int ns0 = hi - LOGE > 0 ? hi - LOGE : 0;
+    relayout<LOGE>(x, sm, lane, s0, ns0);
+    s0 = ns0;
+#pragma unroll
+    for (int b = lo; b < hi; ++b) {
+      const int rb = b - s0;
+#pragma unroll
+      for (int k = 0; k < E; ++k) {
+        if (k & (1 << rb)) continue;
+        const int idx = lay<LOGE>(lane, k, s0);
+        u64 w, ws;
+        tw(b, idx >> (b + 1), w, ws);
+        const u64 U = x[k], V = x[k | (1 << rb)];
+        const u64 S = U + V;
+        x[k] = S >= q2 ? S - q2 : S;
+        x[k | (1 << rb)] = mul_shoup_lazy(U - V + q2, w, ws, q);
+      }
+    }
+  }
+  relayout<LOGE>(x, sm, lane, s0, LOGM - LOGE);
+}
+
+__device__ __forceinline__ u64 canon4(u64 v, u64 q) {  // [0, 4q) -> [0, q)
+  v = v >= 2 * q ? v - 2 * q : v;
+  return v >= q ? v - q : v;
+}
+
+__device__ __forceinline__ uint32_t brev(uint32_t x, int logn) { return __brev(x) >> (32 - logn); }
+__device__ __forceinline__ uint32_t auto_perm(uint32_t i, u64 g, int logn) {
+  const u64 e = 2ull * brev(i, logn) + 1;
+  const u64 e2 = (e * g) & ((2ull << logn) - 1);
+  return brev((uint32_t)((e2 - 1) >> 1), logn);
+}
+
+}  // namespace wntt
+}  // namespace sf

@@ -129,13 +129,19 @@ def qk_dot_partial(be: Backend, q: Ciphertext, cache: KVCache, rank: int, world:
     return [Ciphertext(be, maps[i]) for i in range(n.value)]
 
 
-def softmax_times_v_partial(be: Backend, probs, cache: KVCache, rank: int, world: int) -> Ciphertext:
+def softmax_times_v_partial(be: Backend, probs, cache: KVCache, rank: int, world: int) -> List[Ciphertext]:
+    """The rank's lazily relinearised Score*V product sum: [(d0, d1), (d2, 0)]."""
     arr = (C.c_void_p * len(probs))(*[p.h for p in probs])
-    return _ct(be, _native.lib().sf_softmax_times_v_partial, arr, len(probs), cache.h, rank, world)
+    out = (C.c_void_p * 2)()
+    _check(_native.lib().sf_softmax_times_v_partial(be.ctx, arr, len(probs), cache.h, rank, world, out))
+    return [Ciphertext(be, out[0]), Ciphertext(be, out[1])]
 
 
-def softmax_times_v_finish(be: Backend, acc: Ciphertext, cache: KVCache) -> Ciphertext:
-    return _ct(be, _native.lib().sf_softmax_times_v_finish, acc.h, cache.h)
+def softmax_times_v_finish(be: Backend, parts: List[List[Ciphertext]], cache: KVCache) -> Ciphertext:
+    """Sum the ranks' degree-2 partials, relinearise + rescale once, fold, mask."""
+    a = (C.c_void_p * len(parts))(*[p[0].h for p in parts])
+    b = (C.c_void_p * len(parts))(*[p[1].h for p in parts])
+    return _ct(be, _native.lib().sf_softmax_times_v_finish, a, b, len(parts), cache.h)
 
 
 class Sharded:
@@ -158,5 +164,4 @@ class Sharded:
 
     def softmax_times_v(self, probs, cache: KVCache) -> Ciphertext:
         part = softmax_times_v_partial(self.be, probs, cache, self.rank, self.world)
-        parts = [p[0] for p in allgather_cts(self.be, [part], self.group)]
-        return softmax_times_v_finish(self.be, sum_partials(self.be, parts), cache)
+        return softmax_times_v_finish(self.be, allgather_cts(self.be, part, self.group), cache)

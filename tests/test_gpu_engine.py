@@ -1,0 +1,130 @@
+"""The reference's engine contract (tests/test_engine.cpp) on the GPU backend:
+level rules, ledger counting and phases, rotation semantics, layout
+propagation, error types. Values are compared at CKKS precision instead of
+exactly (the reference backend is a cleartext simulator)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-6
+
+
+def test_add_sub_add_plain_values_levels_counts():  # test_engine.cpp:19-38
+    import paper_2602_11470_b200 as sf
+    be = sf.Backend(8, 5)
+    a = be.encrypt(np.full(8, 1.5), 2)
+    b = be.encrypt(np.full(8, 2.0), 4)
+    s = be.add(a, b)
+    assert s.level == 2 and np.allclose(be.decrypt(s), 3.5, atol=TOL)
+    d = be.sub(b, a)
+    assert d.level == 2 and np.allclose(be.decrypt(d), 0.5, atol=TOL)
+    p = be.add_plain(b, 1.0)
+    assert p.level == 4 and np.allclose(be.decrypt(p), 3.0, atol=TOL)
+    t = be.ledger.totals()
+    assert t.additions == 3 and t.ct_ct_mults == 0
+
+
+def test_rotate_semantics_group_law_and_counts():  # test_engine.cpp:64-94
+    import paper_2602_11470_b200 as sf
+    be = sf.Backend(4, 3)
+    a = be.encrypt(np.array([1.0, 2, 3, 4]), 3)
+    assert np.allclose(be.decrypt(be.rotate(a, 1)), [2, 3, 4, 1], atol=TOL)
+    assert np.allclose(be.decrypt(be.rotate(a, -1)), [4, 1, 2, 3], atol=TOL)
+    assert np.allclose(be.decrypt(be.rotate(a, 0)), [1, 2, 3, 4], atol=TOL)
+    assert np.allclose(be.decrypt(be.rotate(a, 4)), [1, 2, 3, 4], atol=TOL)
+    assert be.ledger.totals().rotations == 2
+    lhs = be.rotate(be.rotate(a, 3), 2)
+    assert np.allclose(be.decrypt(lhs), be.decrypt(be.rotate(a, 5)), atol=TOL) and lhs.level == 3
+    be2 = sf.Backend(8, 2)
+    z = be2.zeros()
+    be2.rotate(z, 1, hoisted=True)
+    be2.rotate(z, 2, hoisted=True)
+    be2.rotate(z, 3)
+    t = be2.ledger.totals()
+    assert (t.rotations, t.hoisted_rotations) == (3, 2)
+
+
+def test_bootstrap_and_level_drop():  # test_engine.cpp:96-112
+    import paper_2602_11470_b200 as sf
+    be = sf.Backend(8, 6)
+    a = be.encrypt(np.full(8, 7.0), 1)
+    up = be.bootstrap(a, 5)
+    assert up.level == 5 and np.allclose(be.decrypt(up), 7.0, atol=TOL)
+    assert be.ledger.totals().bootstraps == 1
+    with pytest.raises(sf.InvalidTarget):
+        be.bootstrap(a, 0)
+    with pytest.raises(sf.InvalidTarget):
+        be.bootstrap(a, 7)
+    down = be.level_drop(up, 2)
+    assert down.level == 2
+    with pytest.raises(sf.InvalidTarget):
+        be.level_drop(down, 3)
+    with pytest.raises(sf.InvalidTarget):
+        be.level_drop(down, -1)
+    assert be.ledger.totals().bootstraps == 1
+
+
+def test_exact_transform_is_free_and_level_neutral():  # test_engine.cpp:114-121
+    import paper_2602_11470_b200 as sf
+    be = sf.Backend(8, 3)
+    x = np.linspace(-2.0, 5.0, 8)
+    a = be.encrypt(x, 1)
+    y = be.exact_transform(a, np.exp)
+    assert y.level == 1 and np.allclose(be.decrypt(y), np.exp(x), rtol=1e-6, atol=1e-6)
+    assert be.ledger.totals() == sf.OpCounts()
+
+
+def test_ledger_phases_nesting_conservation():  # test_engine.cpp:131-166
+    import paper_2602_11470_b200 as sf
+    be = sf.Backend(8, 9)
+    a = be.encrypt(np.ones(8))
+    be.add(a, a)
+    with be.phase("alpha"):
+        be.mul(a, a)
+        be.rotate(a, 1)
+        with be.phase("beta"):
+            be.rotate(a, 2, hoisted=True)
+        be.mul_plain(a, 2.0)
+    be.add(a, a)
+    L = be.ledger
+    al, bt, dflt = L.phase_totals("alpha"), L.phase_totals("beta"), L.phase_totals("(unphased)")
+    assert (al.ct_ct_mults, al.ct_pt_mults, al.rotations) == (1, 1, 1)
+    assert (bt.rotations, bt.hoisted_rotations) == (1, 1)
+    assert dflt.additions == 2
+    tot = L.totals()
+    for f in ("rotations", "hoisted_rotations", "ct_pt_mults", "ct_ct_mults", "additions"):
+        assert getattr(tot, f) == getattr(al, f) + getattr(bt, f) + getattr(dflt, f)
+    L.reset()
+    assert L.totals() == sf.OpCounts()
+
+
+def test_layout_propagation():  # test_engine.cpp:168-181
+    import paper_2602_11470_b200 as sf
+    be = sf.Backend(8, 4)
+    ly = sf.make_interleaved(4, 8, 1)
+    a = be.encrypt(np.ones(8), 4, ly)
+    b = be.encrypt(np.full(8, 2.0), 4, ly)
+    assert be.add(a, b).layout == ly
+    assert be.mul(a, b).layout == ly
+    assert be.mul_plain(a, 2.0).layout == ly
+    assert be.bootstrap(be.level_drop(a, 1), 3).layout == ly
+    assert be.rotate(a, 1).layout is None
+    c = be.encrypt(np.full(8, 3.0), 4, sf.Layout("replicated", 4, 2, 0, 1, False))
+    assert be.add(a, c).layout is None
+
+
+def test_full_ring_fused_and_chained_ops_track_oracle():
+    # ring 2^16 exercises the fused ModUp / ModDown / rescale kernels on every
+    # op class; the chain must stay word-identical to the CPU oracle
+    import paper_2602_11470_b200 as sf
+    from oracle.ckks import CkksOracle
+    g, o = sf.Backend(32768, 5, alpha=2), CkksOracle(32768, 5, alpha=2)
+    rng = np.random.default_rng(1)
+    x, y, p = rng.normal(size=32768), rng.normal(size=32768), rng.normal(size=32768)
+    cg, co = g.encrypt(x, 5, seed=1), o.encrypt(x, 5, seed=1)
+    dg, do = g.encrypt(y, 4, seed=2), o.encrypt(y, 4, seed=2)
+    rg = g.rotate(g.mul(g.mul_plain(cg, p), dg), 7)
+    ro = o.rotate(o.mul(o.mul_plain(co, p), do), 7)
+    assert np.array_equal(rg.data(), ro.data())
+    want = np.roll(x * p * y, -7)
+    assert np.max(np.abs(g.decrypt(rg) - want)) < 1e-4

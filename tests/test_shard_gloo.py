@@ -83,7 +83,7 @@ def _worker(rank, world, port, out):
         sv_full = P.softmax_times_v(be, probs, cache, cfg)
         sp = S.softmax_times_v_partial(be, probs, cache, cfg, rank, world)
         parts = [r[0] for r in _exchange(be, [sp])]
-        sv = S.softmax_times_v_finish(be, S.sum_partials(be, parts), cfg)
+        sv = S.softmax_times_v_finish(be, parts, cfg)
         res["sv"] = bool(np.array_equal(sv.data(), sv_full.data()))
         # --- ownership rules of the product partition the work exactly
         from paper_2602_11470_b200 import shard
