@@ -40,9 +40,10 @@ __global__ void __launch_bounds__(kWarps * 32) ntt_row_pass(LimbBatch B, Tabs T)
   u64* o = (B.optr[entry] ? B.optr[entry] : B.ptr[entry]) + (size_t)row * C;
   u64* sm = sm_all + warp * C;
   u64 x[E];
-#pragma unroll
-  for (int k = 0; k < E; ++k) x[k] = a[lane + 32 * k];
   if (!INV) {
+    // strided 256-byte coalesced loads in, blocked 16-byte vector stores out
+#pragma unroll
+    for (int k = 0; k < E; ++k) x[k] = a[lane + 32 * k];
     const u64* W = T.psi + ((size_t)p << LOGN);
     const u64* Ws = T.psi_s + ((size_t)p << LOGN);
     // row stage with in-row distance 2^b is global stage s = r + (c-1-b):
@@ -53,10 +54,18 @@ __global__ void __launch_bounds__(kWarps * 32) ntt_row_pass(LimbBatch B, Tabs T)
       w = W[i];
       ws = Ws[i];
     };
-    warp_fwd<LOGC>(x, sm, lane, q, tw);
+    warp_fwd<LOGC, kBlocked>(x, sm, lane, q, tw);
 #pragma unroll
-    for (int k = 0; k < E; ++k) x[k] = canon4(x[k], q);
+    for (int k = 0; k < E; k += 2)
+      reinterpret_cast<ulonglong2*>(o + lane * E)[k / 2] = make_ulonglong2(canon4(x[k], q), canon4(x[k + 1], q));
   } else {
+    // blocked 16-byte vector loads in, strided coalesced stores out
+#pragma unroll
+    for (int k = 0; k < E; k += 2) {
+      const ulonglong2 v = reinterpret_cast<const ulonglong2*>(a + lane * E)[k / 2];
+      x[k] = v.x;
+      x[k + 1] = v.y;
+    }
     const u64* W = T.ipsi + ((size_t)p << LOGN);
     const u64* Ws = T.ipsi_s + ((size_t)p << LOGN);
     // GS stage with distance t = 2^b: h = n/(2t); blocks per row C/(2t)
@@ -65,10 +74,10 @@ __global__ void __launch_bounds__(kWarps * 32) ntt_row_pass(LimbBatch B, Tabs T)
       w = W[i];
       ws = Ws[i];
     };
-    warp_inv<LOGC>(x, sm, lane, q, tw);
-  }
+    warp_inv<LOGC, kBlocked>(x, sm, lane, q, tw);
 #pragma unroll
-  for (int k = 0; k < E; ++k) o[lane + 32 * k] = x[k];
+    for (int k = 0; k < E; ++k) o[lane + 32 * k] = x[k];
+  }
 }
 
 // Forward row pass + combine epilogue (EpiBatch): out = (acc - v) * inv (+ addend).
@@ -95,17 +104,28 @@ __global__ void __launch_bounds__(kWarps * 32) ntt_row_epi(EpiBatch B, Tabs T) {
     w = W[i];
     ws = Ws[i];
   };
-  warp_fwd<LOGC>(x, sm, lane, q, tw);
+  warp_fwd<LOGC, kBlocked>(x, sm, lane, q, tw);
   const u64* acc = B.acc[entry];
   const u64* addend = B.addend[entry];
   const u64 g = B.g[entry], inv = B.inv[entry], inv_s = B.inv_s[entry];
   u64* out = B.out[entry];
+  const int base = row * C + lane * E;  // blocked: this lane owns E consecutive outputs
 #pragma unroll
-  for (int k = 0; k < E; ++k) {
-    const int i = row * C + lane + 32 * k;
-    u64 v = mul_shoup(sub_mod(acc[i], canon4(x[k], q), q), inv, inv_s, q);
-    if (addend) v = add_mod(v, addend[g > 1 ? auto_perm((uint32_t)i, g, LOGN) : i], q);
-    out[i] = v;
+  for (int k = 0; k < E; k += 2) {
+    const ulonglong2 av = *reinterpret_cast<const ulonglong2*>(acc + base + k);
+    u64 v0 = mul_shoup(sub_mod(av.x, canon4(x[k], q), q), inv, inv_s, q);
+    u64 v1 = mul_shoup(sub_mod(av.y, canon4(x[k + 1], q), q), inv, inv_s, q);
+    if (addend) {
+      if (g > 1) {
+        v0 = add_mod(v0, addend[auto_perm((uint32_t)(base + k), g, LOGN)], q);
+        v1 = add_mod(v1, addend[auto_perm((uint32_t)(base + k + 1), g, LOGN)], q);
+      } else {
+        const ulonglong2 dv = *reinterpret_cast<const ulonglong2*>(addend + base + k);
+        v0 = add_mod(v0, dv.x, q);
+        v1 = add_mod(v1, dv.y, q);
+      }
+    }
+    *reinterpret_cast<ulonglong2*>(out + base + k) = make_ulonglong2(v0, v1);
   }
 }
 

@@ -33,10 +33,15 @@ __device__ __forceinline__ void relayout(u64 (&x)[1 << LOGE], u64* sm, int lane,
   __syncwarp();
 }
 
-// Forward sub-NTT (Cooley-Tukey). Entry/exit layout: lane = low 5 index bits.
+// Register layouts: STRIDED (register bits = the top LOGE index bits, lane =
+// the low 5 bits: element lane + 32k) or BLOCKED (register bits = the low LOGE
+// bits: lane owns E consecutive elements, 16-byte vector loads/stores).
+enum : int { kStrided = 0, kBlocked = 1 };
+
+// Forward sub-NTT (Cooley-Tukey). Entry layout: strided. Exit layout: EXIT.
 // tw(b, blk, w, ws) gives the twiddle (and Shoup companion) of the stage with
 // butterfly distance 2^b for block blk.
-template <int LOGM, class TW>
+template <int LOGM, int EXIT = kStrided, class TW>
 __device__ __forceinline__ void warp_fwd(u64 (&x)[1 << (LOGM - 5)], u64* sm, int lane, u64 q, const TW& tw) {
   constexpr int LOGE = LOGM - 5;
   constexpr int E = 1 << LOGE;
@@ -64,16 +69,16 @@ __device__ __forceinline__ void warp_fwd(u64 (&x)[1 << (LOGM - 5)], u64* sm, int
       }
     }
   }
-  relayout<LOGE>(x, sm, lane, s0, LOGM - LOGE);
+  relayout<LOGE>(x, sm, lane, s0, EXIT == kBlocked ? 0 : LOGM - LOGE);
 }
 
-// Inverse sub-NTT (Gentleman-Sande), same entry/exit layout.
-template <int LOGM, class TW>
+// Inverse sub-NTT (Gentleman-Sande). Entry layout: ENTRY. Exit layout: strided.
+template <int LOGM, int ENTRY = kStrided, class TW>
 __device__ __forceinline__ void warp_inv(u64 (&x)[1 << (LOGM - 5)], u64* sm, int lane, u64 q, const TW& tw) {
   constexpr int LOGE = LOGM - 5;
   constexpr int E = 1 << LOGE;
   const u64 q2 = 2 * q;
-  int s0 = LOGM - LOGE;
+  int s0 = ENTRY == kBlocked ? 0 : LOGM - LOGE;
 #pragma unroll
   for (int lo = 0; lo < LOGM; lo += LOGE) {
     const int hi = lo + LOGE < LOGM ? lo + LOGE : LOGM;
