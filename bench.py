@@ -302,8 +302,10 @@ def main():
     l0 = be.kernel_launches()
     with Clocks(local) as clk:
         be.event_record(0)
+        t_host = time.perf_counter()
         for _ in range(args.steps):
             outs = layer.step()
+        t_host = (time.perf_counter() - t_host) * 1e3 / args.steps
         be.event_record(1)
         ms_total = be.event_elapsed_ms(0, 1)
     be.synchronize()
@@ -343,22 +345,42 @@ def main():
                 "algorithmic_bytes_per_launch": by[dom] / max(nl[dom], 1),
                 "avg_launch_us": ms[dom] * 1e3 / max(nl[dom], 1)}
 
-    # ---- e2e: public API with host buffers (import inputs, read outputs back)
+    # ---- e2e: public API with host buffers (import inputs from pinned host
+    # memory, read the results back), host wall clock around whole steps
     host_in = [(c.data(), c.level, c.scale, c.layout) for c in layer.inputs]
-    pinned_in = host_in
+    pinned_in = []
+    try:
+        import torch
+        for w, lvl, sc, ly in host_in:
+            t = torch.empty(w.shape, dtype=torch.uint64 if hasattr(torch, "uint64") else torch.int64, pin_memory=True)
+            a = t.numpy().view(np.uint64)
+            a[...] = w
+            pinned_in.append((a, lvl, sc, ly, t))
+        pinned = True
+    except Exception:
+        pinned_in = [(w, lvl, sc, ly, None) for w, lvl, sc, ly in host_in]
+        pinned = False
     h2d = sum(w.nbytes for w, *_ in host_in)
     d2h = 0
     be.synchronize()
     barrier()
+    t_imp = t_iss = t_rd = 0.0
     t_e = time.perf_counter()
     for _ in range(args.steps):
-        ins = [be.import_ct(w, lvl, sc, ly) for w, lvl, sc, ly in pinned_in]
+        t1 = time.perf_counter()
+        ins = [be.import_ct(w, lvl, sc, ly) for w, lvl, sc, ly, _ in pinned_in]
+        t2 = time.perf_counter()
         outs = layer.step(ins)
+        t3 = time.perf_counter()
         res = [outs[4].data(), outs[8].data()]  # attention output and the layer's down-projection output
+        t4 = time.perf_counter()
+        t_imp, t_iss, t_rd = t_imp + t2 - t1, t_iss + t3 - t2, t_rd + t4 - t3
         d2h = sum(r.nbytes for r in res)
     be.synchronize()
     barrier()
     e2e_ms = (time.perf_counter() - t_e) * 1e3 / args.steps
+    e2e_parts = {"import_ms": round(t_imp * 1e3 / args.steps, 3), "host_issue_ms": round(t_iss * 1e3 / args.steps, 3),
+                 "readback_wait_ms": round(t_rd * 1e3 / args.steps, 3), "pinned": pinned}
     if dist:
         import torch
         t = torch.tensor([e2e_ms], device="cuda")
@@ -380,8 +402,9 @@ def main():
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": {"value": round(e2e_ms / world, 3), "unit": "ms/token", "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h)},
+                "d2h_bytes_per_step": int(d2h), "breakdown": e2e_parts},
         "gpu_launches": int(launches),
+        "host_issue_ms_per_step": round(t_host, 3),
         "clocks": clk.summary(),
         "ledger_per_step": {k: v // args.steps for k, v in counts.asdict().items()},
         "kernel_families": prof,

@@ -28,6 +28,9 @@ METRICS = {
     "regs": "launch__registers_per_thread",
     "occ": "sm__warps_active.avg.pct_of_peak_sustained_active",
     "bank_conf": "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+    "issue_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "fmaheavy_pct": "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed",
+    "warp_inst_M": "smsp__inst_executed.sum",
 }
 UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1, "msecond": 1e3,
               "ns": 1e-3, "us": 1, "ms": 1e3}
@@ -60,15 +63,18 @@ def main():
     ap.add_argument("--launches")
     a = ap.parse_args()
     if a.rep:
-        print("| kernel | grid | us | DRAM MB (rd+wr) | DRAM GB/s | DRAM % | SM % | ALU % | FMA % | LSU % | regs | warps % | smem bank conflicts |")
-        print("|---|---|---|---|---|---|---|---|---|---|---|---|---|")
-        for r in rep_rows(a.rep):
+        print("| kernel | grid | us | DRAM MB (rd+wr) | DRAM GB/s | DRAM % | SM % | ALU % | FMA % | LSU % | regs | warps % | smem bank conflicts | issue % | fmaheavy % | warp-inst M |")
+        print("|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|")
+        for rep in a.rep.split(","):
+          for r in rep_rows(rep):
             tb = (r.get("dram_rd") or 0) + (r.get("dram_wr") or 0)
             gbs = tb / (r["dur_us"] * 1e-6) / 1e9 if r.get("dur_us") else None
+            wi = r.get("warp_inst_M")
             print(f"| {r['kernel']} | {r['grid']} | {fmt(r.get('dur_us'))} | {tb / 1e6:.1f} | {fmt(gbs, 0)} | "
                   f"{fmt(r.get('dram_pct'))} | {fmt(r.get('sm_pct'))} | {fmt(r.get('alu_pct'))} | "
                   f"{fmt(r.get('fma_pct'))} | {fmt(r.get('lsu_pct'))} | {fmt(r.get('regs'), 0)} | "
-                  f"{fmt(r.get('occ'))} | {fmt(r.get('bank_conf'), 0)} |")
+                  f"{fmt(r.get('occ'))} | {fmt(r.get('bank_conf'), 0)} | {fmt(r.get('issue_pct'))} | "
+                  f"{fmt(r.get('fmaheavy_pct'))} | {fmt(wi / 1e6 if wi else None)} |")
     if a.launches:
         text = open(a.launches).read()
         lines = [l for l in text.splitlines() if l.startswith('"')]
