@@ -339,6 +339,15 @@ void b_ks(Context& c, const KsBatch& A) {
   post(c);
 }
 
+void b_ks_row(Context& c, const KsRowArgs& A) {
+  if (!A.nsrc) return;
+  // sources: ndig rows per target; jobs: 2 key rows per digit + 2 outputs per target
+  const double jobs = A.job_begin[A.nsrc];
+  ProfScope prof(c, kFamKs, 8.0 * c.n * A.nt * ((double)A.nsrc * A.ndig + jobs * (2.0 * A.ndig + 2.0)));
+  ntt_ks_row(c, A);
+  post(c);
+}
+
 void b_subscale(Context& c, const SubScaleBatch& B, int limbs, const u64* inv, const u64* inv_s) {
   if (!B.count) return;
   ProfScope prof(c, kFamElem, 32.0 * limbs * c.n * B.count);

@@ -121,15 +121,34 @@ struct EpiBatch {
   uint8_t prime[kJobsWide];
 };
 
+// Fused key-switch row stage (ntt.cu ks_row_kernel): per (source, target prime
+// t, row), the forward row pass of the ModUp output of every digit (own limbs
+// read straight from the NTT-domain source), then per job of that source the
+// automorphism + inner product with the switching key, reduced, written in
+// the NTT domain for t < limbs and inverse-row-passed (ModDown's first pass)
+// for the special primes. Jobs are grouped by source (CSR in job_begin).
+struct KsRowArgs {
+  int nsrc = 0, limbs = 0, nt = 0, ndig = 0, alpha = 0, np = 0;
+  int tprime[kMaxPrimes];
+  const u64* c1[kJobs];   // NTT-domain source polynomial (limbs x n)
+  const u64* ext[kJobs];  // column-pass ModUp output [ndig][nt][n] (own slots unused)
+  int job_begin[kJobs + 1];
+  u64 g[kJobs], ginv[kJobs];
+  const u64* key[kJobs];  // [beta][2][np][n]
+  u64* acc[kJobs];        // [2][nt][n]
+};
+
 // ntt.cu dispatchers (false when the ring degree has no two-pass kernels)
 bool ntt_row_only(Context& c, const LimbBatch& b, bool inverse);
 bool ntt_row_epi(Context& c, const EpiBatch& e);
 bool ntt_fused_col(Context& c, const FusedColArgs& a);
+bool ntt_ks_row(Context& c, const KsRowArgs& a);
 inline bool fused_path(const Context& c) { return c.logn >= 12 && c.logn <= 17 && c.alpha <= 8; }
 // profiled launch wrappers (batch.cu)
 void b_row(Context& c, const LimbBatch& b, bool inverse);
 void b_fused_col(Context& c, const FusedColArgs& A);
 void b_row_epi(Context& c, const EpiBatch& E);
+void b_ks_row(Context& c, const KsRowArgs& A);
 
 void b_copy(Context& c, const CopyBatch& B, size_t words);
 void b_tensor_sum(Context& c, const TensorSumArgs& A, int limbs);

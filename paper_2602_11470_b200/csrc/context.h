@@ -154,6 +154,7 @@ struct Context {
   double delta = 0.0;
   u64 seed = 0;
   int device = 0;
+  bool ks_row = true;  // fused key-switch row stage (SF_KS_ROW=0: separate passes, for A/B timing)
   std::vector<u64> primes;  // q0..qL, p0..p_{alpha-1}
   cudaStream_t stream = nullptr;
   cudaMemPool_t pool = nullptr;

@@ -26,6 +26,8 @@ namespace {
 struct ExtB {
   BufPtr buf;
   int S = 0, ndig = 0, nt = 0, limbs = 0;
+  bool col_only = false;        // ext holds column-pass output; ks_row_kernel finishes it
+  std::vector<const u64*> src;  // the NTT-domain sources (own-prime rows)
   std::vector<int> tprime;
   size_t per = 0;  // words per source
   const u64* ext(int s) const { return buf->p + (size_t)s * per; }
@@ -61,8 +63,10 @@ ExtB mod_up_batch(Context& c, const std::vector<const u64*>& d, int limbs) {
   x.nt = limbs + c.alpha;
   for (int t = 0; t < x.nt; ++t) x.tprime.push_back(t < limbs ? t : c.P_index(t - limbs));
   x.per = (size_t)x.ndig * x.nt * n;
+  x.src = d;
   BufPtr dcoef = make_buf(c, (size_t)x.S * limbs * n);
   if (fused_path(c)) {
+    x.col_only = c.ks_row;
     // inverse row pass (out of place) -> per digit: fused [inverse column pass,
     // conversion, forward column pass] straight into ext -> forward row pass
     LimbBatch lb;
@@ -95,11 +99,13 @@ ExtB mod_up_batch(Context& c, const std::vector<const u64*>& d, int limbs) {
         A.src[A.count] = dcoef->p + ((size_t)s * limbs + lo) * n;
         A.dst[A.count++] = ext_of(s);
         if (A.count == kJobsWide) b_fused_col(c, A), A.count = 0;
+        if (x.col_only) continue;
         cb.src[cb.count] = d[s] + (size_t)lo * n;  // own primes: the exact NTT-domain residues
         cb.dst[cb.count++] = ext_of(s) + (size_t)lo * n;
         if (cb.count == kJobsWide) b_copy(c, cb, (size_t)(hi - lo) * n), cb.count = 0;
       }
       if (A.count) b_fused_col(c, A);
+      if (x.col_only) continue;
       b_copy(c, cb, (size_t)(hi - lo) * n);
       for (int s = 0; s < x.S; ++s)
         for (size_t k = 0; k < slot.size(); ++k) {
@@ -178,6 +184,42 @@ void ks_jobs(Context& c, const ExtB& x, const std::vector<KsJob>& jobs) {
     const int J = (int)std::min<size_t>(kJobs, jobs.size() - s0);
     BufPtr acc = make_buf(c, (size_t)J * 2 * nt * n);
     auto accp = [&](int j, int poly) { return acc->p + ((size_t)j * 2 + poly) * nt * n; };
+    if (x.col_only) {
+      // fused: forward row pass of ext + automorphism + inner product + ModDown's
+      // inverse row pass of the special primes, one launch (jobs grouped by source)
+      KsRowArgs ka;
+      ka.limbs = limbs;
+      ka.nt = nt;
+      ka.ndig = x.ndig;
+      ka.alpha = c.alpha;
+      ka.np = c.np;
+      for (int t = 0; t < nt; ++t) ka.tprime[t] = x.tprime[t];
+      std::vector<int> order(J);
+      for (int j = 0; j < J; ++j) order[j] = j;
+      std::stable_sort(order.begin(), order.end(),
+                       [&](int a, int b) { return jobs[s0 + a].src < jobs[s0 + b].src; });
+      int prev = -1;
+      for (int k = 0; k < J; ++k) {
+        const int j = order[k];
+        const KsJob& jb = jobs[s0 + j];
+        if (jb.src != prev) {
+          ka.c1[ka.nsrc] = x.src[jb.src];
+          ka.ext[ka.nsrc] = x.ext(jb.src);
+          ka.job_begin[ka.nsrc++] = k;
+          prev = jb.src;
+        }
+        ka.g[k] = jb.g;
+        u64 gi = 1;  // g^-1 mod 2n = g^(n-1) (the unit group mod 2n has order n)
+        if (jb.g > 1)
+          for (u64 e = (u64)n - 1, b = jb.g, m2 = 2ull * n - 1; e; e >>= 1, b = (b * b) & m2)
+            if (e & 1) gi = (gi * b) & m2;
+        ka.ginv[k] = gi;
+        ka.key[k] = get_key(c, jb.g <= 1 ? 0 : jb.g)->p;
+        ka.acc[k] = accp(j, 0);
+      }
+      ka.job_begin[ka.nsrc] = J;
+      b_ks_row(c, ka);
+    }
     KsBatch kb;
     kb.ndig = x.ndig;
     kb.nt = nt;
@@ -193,20 +235,22 @@ void ks_jobs(Context& c, const ExtB& x, const std::vector<KsJob>& jobs) {
       kb.acca[j] = accp(j, 1);
     }
     kb.count = J;
-    b_ks(c, kb);
+    if (!x.col_only) b_ks(c, kb);
     if (fused_path(c)) {
       // ModDown of 2J polynomials: inverse row pass of the P limbs (in place),
       // fused [inverse column, P -> Q conversion, forward column], then the
       // forward row pass with the (acc - conv) * P^-1 (+ addend) epilogue
       const std::vector<u64>& kh = c.level_consts_h[limbs];
       LimbBatch lb;
-      for (int j = 0; j < J; ++j)
-        for (int poly = 0; poly < 2; ++poly)
-          for (int k = 0; k < c.alpha; ++k) {
-            lb.add(accp(j, poly) + (size_t)(limbs + k) * n, pidx[k]);
-            if (lb.count == kMaxBatch) b_row(c, lb, true), lb.count = 0;
-          }
-      b_row(c, lb, true);
+      if (!x.col_only) {
+        for (int j = 0; j < J; ++j)
+          for (int poly = 0; poly < 2; ++poly)
+            for (int k = 0; k < c.alpha; ++k) {
+              lb.add(accp(j, poly) + (size_t)(limbs + k) * n, pidx[k]);
+              if (lb.count == kMaxBatch) b_row(c, lb, true), lb.count = 0;
+            }
+        b_row(c, lb, true);
+      }
       BufPtr conv = make_buf(c, (size_t)J * 2 * limbs * n);
       FusedColArgs A;
       A.ns = c.alpha;

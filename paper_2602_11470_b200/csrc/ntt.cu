@@ -292,6 +292,117 @@ __global__ void __launch_bounds__(kWarps * 32) fused_col_kernel(FusedColArgs A, 
   }
 }
 
+// ------------------------------------------------------ fused key-switch row
+// One CTA = (source s, target slot t, kWarps source rows); warp w owns source
+// row rs. Automorphisms map whole rows to whole rows in the bit-reversed
+// evaluation order (the row index is the top LOGR bits of the position, which
+// fix e = 2 br(i) + 1 mod 2C and hence e*g mod 2C), so every output row of a
+// job reads exactly one source row: rd = perm_{g^-1}(rs), and within it the
+// column perm_g(rd*C + c) mod C.
+template <int LOGR, int LOGC>
+__global__ void __launch_bounds__(kWarps * 32) ks_row_kernel(KsRowArgs A, Tabs T) {
+  constexpr int C = 1 << LOGC, E = C / 32, LOGN = LOGR + LOGC;
+  constexpr int tiles = (1 << LOGR) / kWarps;
+  constexpr int n = 1 << LOGN;
+  extern __shared__ u64 ks_sm[];  // [kWarps][ndig + 1][C]
+  const int tile = blockIdx.x % tiles, rest = blockIdx.x / tiles;
+  const int t = rest % A.nt, s = rest / A.nt;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rs = tile * kWarps + warp;
+  const int m = A.tprime[t];
+  const u64 q = T.q[m];
+  u64* wsm = ks_sm + (size_t)warp * (A.ndig + 1) * C;
+  // 1. row rs of every digit's extended polynomial, NTT domain, natural order
+  for (int j = 0; j < A.ndig; ++j) {
+    u64* X = wsm + j * C;
+    const int lo = j * A.alpha, hi = min(lo + A.alpha, A.limbs);
+    if (t >= lo && t < hi) {  // own prime: the exact NTT-domain source residues
+      const u64* a = A.c1[s] + (size_t)t * n + (size_t)rs * C + lane * E;
+#pragma unroll
+      for (int k = 0; k < E; k += 2)
+        reinterpret_cast<ulonglong2*>(X + lane * E)[k / 2] = reinterpret_cast<const ulonglong2*>(a)[k / 2];
+    } else {
+      const u64* a = A.ext[s] + ((size_t)j * A.nt + t) * n + (size_t)rs * C;
+      u64 x[E];
+#pragma unroll
+      for (int k = 0; k < E; ++k) x[k] = a[lane + 32 * k];
+      const u64* W = T.psi + ((size_t)m << LOGN);
+      const u64* Ws = T.psi_s + ((size_t)m << LOGN);
+      auto tw = [&](int b, int blk, u64& w, u64& ws) {
+        const int sp = LOGC - 1 - b;
+        const int i = (1 << (LOGR + sp)) + (rs << sp) + blk;
+        w = W[i];
+        ws = Ws[i];
+      };
+      warp_fwd<LOGC, kBlocked>(x, X, lane, q, tw);
+#pragma unroll
+      for (int k = 0; k < E; k += 2)
+        reinterpret_cast<ulonglong2*>(X + lane * E)[k / 2] = make_ulonglong2(canon4(x[k], q), canon4(x[k + 1], q));
+    }
+  }
+  __syncwarp();
+  const u64 mh = T.mh[m], ml = T.ml[m];
+  u64* scratch = wsm + A.ndig * C;
+  // 2. every job of this source: permuted inner product with its key
+  for (int jb = A.job_begin[s]; jb < A.job_begin[s + 1]; ++jb) {
+    const u64 g = A.g[jb];
+    const int rd = g > 1 ? (int)(auto_perm((uint32_t)rs << LOGC, A.ginv[jb], LOGN) >> LOGC) : rs;
+    const size_t rowoff = (size_t)rd * C + lane * E;
+    U128 sb[E], sa[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k) sb[k] = U128{0, 0}, sa[k] = U128{0, 0};
+    uint32_t sc[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k)
+      sc[k] = g > 1 ? (auto_perm((uint32_t)(rd * C + lane * E + k), g, LOGN) & (C - 1)) : (uint32_t)(lane * E + k);
+    for (int j = 0; j < A.ndig; ++j) {
+      const u64* X = wsm + j * C;
+      const u64* kb = A.key[jb] + ((size_t)(j * 2 + 0) * A.np + m) * n + rowoff;
+      const u64* ka = A.key[jb] + ((size_t)(j * 2 + 1) * A.np + m) * n + rowoff;
+#pragma unroll
+      for (int k = 0; k < E; k += 2) {
+        const ulonglong2 vb = reinterpret_cast<const ulonglong2*>(kb)[k / 2];
+        const ulonglong2 va = reinterpret_cast<const ulonglong2*>(ka)[k / 2];
+        const u64 x0 = X[sc[k]], x1 = X[sc[k + 1]];
+        mac128(sb[k], x0, vb.x);
+        mac128(sa[k], x0, va.x);
+        mac128(sb[k + 1], x1, vb.y);
+        mac128(sa[k + 1], x1, va.y);
+      }
+    }
+    u64 vb[E], va[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      vb[k] = reduce128(sb[k].hi, sb[k].lo, q, mh, ml);
+      va[k] = reduce128(sa[k].hi, sa[k].lo, q, mh, ml);
+    }
+    u64* accb = A.acc[jb] + (size_t)t * n;
+    u64* acca = A.acc[jb] + (size_t)(A.nt + t) * n;
+    if (t < A.limbs) {
+#pragma unroll
+      for (int k = 0; k < E; k += 2) {
+        reinterpret_cast<ulonglong2*>(accb + rowoff)[k / 2] = make_ulonglong2(vb[k], vb[k + 1]);
+        reinterpret_cast<ulonglong2*>(acca + rowoff)[k / 2] = make_ulonglong2(va[k], va[k + 1]);
+      }
+    } else {  // special prime: ModDown's inverse row pass, strided stores
+      const u64* W = T.ipsi + ((size_t)m << LOGN);
+      const u64* Ws = T.ipsi_s + ((size_t)m << LOGN);
+      auto tw = [&](int b, int blk, u64& w, u64& ws) {
+        const int i = (1 << (LOGN - 1 - b)) + (rd << (LOGC - 1 - b)) + blk;
+        w = W[i];
+        ws = Ws[i];
+      };
+      warp_inv<LOGC, kBlocked>(vb, scratch, lane, q, tw);
+      warp_inv<LOGC, kBlocked>(va, scratch, lane, q, tw);
+#pragma unroll
+      for (int k = 0; k < E; ++k) {
+        accb[(size_t)rd * C + lane + 32 * k] = vb[k];
+        acca[(size_t)rd * C + lane + 32 * k] = va[k];
+      }
+    }
+  }
+}
+
 template <int LOGR, int LOGC>
 void run_two_pass(Context& c, const LimbBatch& b, bool inverse) {
   const unsigned rows_grid = (unsigned)b.count * ((1u << LOGR) / kWarps);
@@ -335,6 +446,21 @@ void run_fused(Context& c, const FusedColArgs& a) {
   fused_col_kernel<LOGR, LOGC><<<grid, kWarps * 32, sm, c.stream>>>(a, c.tabs);
 }
 
+template <int LOGR, int LOGC>
+void run_ks_row(Context& c, const KsRowArgs& a) {
+  constexpr int C = 1 << LOGC;
+  const size_t sm = (size_t)kWarps * (a.ndig + 1) * C * sizeof(u64);
+  static int configured = 0;
+  if (!configured) {
+    SF_CUDA(cudaFuncSetAttribute(ks_row_kernel<LOGR, LOGC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 200 * 1024));
+    configured = 1;
+  }
+  require(sm <= 200 * 1024, kInternal, "key-switch row stage: too many digits for shared memory");
+  const unsigned grid = (unsigned)(a.nsrc * a.nt * ((1 << LOGR) / kWarps));
+  ks_row_kernel<LOGR, LOGC><<<grid, kWarps * 32, sm, c.stream>>>(a, c.tabs);
+}
+
 #define SF_NTT_DISPATCH(FN, ...)                        \
   switch (c.logn) {                                     \
     case 12: FN<6, 6>(c, __VA_ARGS__); return true;     \
@@ -352,5 +478,6 @@ bool ntt_two_pass(Context& c, const LimbBatch& b, bool inverse) { SF_NTT_DISPATC
 bool ntt_row_only(Context& c, const LimbBatch& b, bool inverse) { SF_NTT_DISPATCH(run_row, b, inverse) }
 bool ntt_row_epi(Context& c, const EpiBatch& e) { SF_NTT_DISPATCH(run_epi, e) }
 bool ntt_fused_col(Context& c, const FusedColArgs& a) { SF_NTT_DISPATCH(run_fused, a) }
+bool ntt_ks_row(Context& c, const KsRowArgs& a) { SF_NTT_DISPATCH(run_ks_row, a) }
 
 }  // namespace sf
