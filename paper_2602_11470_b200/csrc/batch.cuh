@@ -100,10 +100,18 @@ struct TensorSumArgs {  // (D0, D1, D2) = sum_i tensor(a_i, b_i), no relinearisa
 // need only the forward row pass. Source limbs of job j: src[j] + s*n;
 // destination limb d: dst[j] + out_slot[d]*n.
 struct FusedColArgs {
+  void set_plan(const u64* tab, int nsrc, int ndst) {
+    const size_t base2 = 2 * (size_t)nsrc + (size_t)nsrc * ndst;
+    qhat = tab + 2 * nsrc;
+    ymul = tab + base2;
+    ymul_s = tab + base2 + nsrc;
+    qhat_s = tab + base2 + 2 * nsrc;
+  }
   int count = 0, ns = 0, nd = 0, mode = 0;
   int src_prime[kMaxPrimes], dst_prime[kMaxPrimes], out_slot[kMaxPrimes];
-  const u64 *qinv = nullptr, *qinv_s = nullptr, *qhat = nullptr;  // mode 0 (ConvPlan tables)
-  u64 q_last = 0;                                                  // mode 1
+  // mode 0 (ConvPlan tables): y_s = x_s * (n^-1 qhat_s^-1) (Shoup), out_d = sum_s y_s * qhat[s][d] (Shoup)
+  const u64 *ymul = nullptr, *ymul_s = nullptr, *qhat = nullptr, *qhat_s = nullptr;
+  u64 q_last = 0;  // mode 1
   const u64* src[kJobsWide];
   u64* dst[kJobsWide];
 };
@@ -129,7 +137,9 @@ struct EpiBatch {
 // for the special primes. Jobs are grouped by source (CSR in job_begin).
 struct KsRowArgs {
   int nsrc = 0, limbs = 0, nt = 0, ndig = 0, alpha = 0, np = 0;
+  int run_len = 0;  // host-side scratch (jobs of the current source while splitting)
   int tprime[kMaxPrimes];
+  // per work unit (a source, or a chunk of one source's jobs):
   const u64* c1[kJobs];   // NTT-domain source polynomial (limbs x n)
   const u64* ext[kJobs];  // column-pass ModUp output [ndig][nt][n] (own slots unused)
   int job_begin[kJobs + 1];

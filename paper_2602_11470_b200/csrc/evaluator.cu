@@ -193,7 +193,10 @@ const ConvPlan& conv_plan(Context& c, const std::vector<int>& src, const std::ve
   p.dst = dst;
   p.nsrc = (int)src.size();
   p.ndst = (int)dst.size();
-  std::vector<u64> h(2 * (size_t)p.nsrc + (size_t)p.nsrc * p.ndst);
+  // [nsrc] qhat^-1, [nsrc] Shoup, [nsrc][ndst] qhat mod dst,
+  // then for the fused column stage: [nsrc] n^-1 qhat^-1, [nsrc] Shoup, [nsrc][ndst] Shoup of qhat mod dst
+  const size_t base2 = 2 * (size_t)p.nsrc + (size_t)p.nsrc * p.ndst;
+  std::vector<u64> h(2 * base2);
   for (int i = 0; i < p.nsrc; ++i) {
     const u64 qi = c.primes[src[i]];
     u64 hat = 1 % qi;
@@ -207,7 +210,11 @@ const ConvPlan& conv_plan(Context& c, const std::vector<int>& src, const std::ve
       for (int k = 0; k < p.nsrc; ++k)
         if (k != i) hm = mulmod_h(hm, c.primes[src[k]] % pd, pd);
       h[2 * p.nsrc + (size_t)i * p.ndst + d] = hm;
+      h[base2 + 2 * p.nsrc + (size_t)i * p.ndst + d] = shoup_h(hm, pd);
     }
+    const u64 ni = invmod_h((u64)c.n % qi, qi);
+    h[base2 + i] = mulmod_h(ni, h[i], qi);
+    h[base2 + p.nsrc + i] = shoup_h(h[base2 + i], qi);
   }
   p.tab = buf(c, h.size());
   SF_CUDA(cudaMemcpyAsync(p.tab->p, h.data(), h.size() * sizeof(u64), cudaMemcpyHostToDevice, c.stream));

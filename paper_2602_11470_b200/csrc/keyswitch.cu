@@ -88,9 +88,7 @@ ExtB mod_up_batch(Context& c, const std::vector<const u64*>& d, int limbs) {
       A.ns = hi - lo;
       A.nd = (int)dst.size();
       A.mode = 0;
-      A.qinv = plan.tab->p;
-      A.qinv_s = plan.tab->p + plan.nsrc;
-      A.qhat = plan.tab->p + 2 * plan.nsrc;
+      A.set_plan(plan.tab->p, plan.nsrc, plan.ndst);
       for (int i = 0; i < A.ns; ++i) A.src_prime[i] = src[i];
       for (int k = 0; k < A.nd; ++k) A.dst_prime[k] = dst[k], A.out_slot[k] = slot[k];
       CopyBatch cb;
@@ -198,15 +196,33 @@ void ks_jobs(Context& c, const ExtB& x, const std::vector<KsJob>& jobs) {
       for (int j = 0; j < J; ++j) order[j] = j;
       std::stable_sort(order.begin(), order.end(),
                        [&](int a, int b) { return jobs[s0 + a].src < jobs[s0 + b].src; });
-      int prev = -1;
+      // work units = (source, chunk of its jobs); a source with many hoisted
+      // jobs is split so the grid still covers the GPU (each unit recomputes
+      // the source rows' forward row pass, a small cost next to its jobs)
+      int nsrc_present = 0;
+      for (int k = 0; k < J; ++k)
+        if (k == 0 || jobs[s0 + order[k]].src != jobs[s0 + order[k - 1]].src) ++nsrc_present;
+      const int tiles = (1 << (c.logn / 2)) / 8;
+      const int want_units = (1184 + nt * tiles - 1) / (nt * tiles);
+      const int chunks = nsrc_present >= want_units ? 1 : (want_units + nsrc_present - 1) / nsrc_present;
+      int prev = -1, run_begin = 0;
       for (int k = 0; k < J; ++k) {
         const int j = order[k];
         const KsJob& jb = jobs[s0 + j];
         if (jb.src != prev) {
+          int run = 1;
+          while (k + run < J && jobs[s0 + order[k + run]].src == jb.src) ++run;
+          run_begin = k;
+          prev = jb.src;
+          (void)run;
           ka.c1[ka.nsrc] = x.src[jb.src];
           ka.ext[ka.nsrc] = x.ext(jb.src);
           ka.job_begin[ka.nsrc++] = k;
-          prev = jb.src;
+          ka.run_len = run;
+        } else if (chunks > 1 && (k - run_begin) % ((ka.run_len + chunks - 1) / chunks) == 0) {
+          ka.c1[ka.nsrc] = x.src[jb.src];
+          ka.ext[ka.nsrc] = x.ext(jb.src);
+          ka.job_begin[ka.nsrc++] = k;
         }
         ka.g[k] = jb.g;
         u64 gi = 1;  // g^-1 mod 2n = g^(n-1) (the unit group mod 2n has order n)
@@ -255,9 +271,7 @@ void ks_jobs(Context& c, const ExtB& x, const std::vector<KsJob>& jobs) {
       FusedColArgs A;
       A.ns = c.alpha;
       A.nd = limbs;
-      A.qinv = down.tab->p;
-      A.qinv_s = down.tab->p + down.nsrc;
-      A.qhat = down.tab->p + 2 * down.nsrc;
+      A.set_plan(down.tab->p, down.nsrc, down.ndst);
       for (int k = 0; k < c.alpha; ++k) A.src_prime[k] = pidx[k];
       for (int l = 0; l < limbs; ++l) A.dst_prime[l] = l, A.out_slot[l] = l;
       for (int j = 0; j < J; ++j)

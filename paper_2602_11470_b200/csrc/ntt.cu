@@ -210,7 +210,8 @@ __global__ void __launch_bounds__(kWarps * 32) fused_col_kernel(FusedColArgs A, 
     region(s, col)[swz(row)] = src[(size_t)s * n + (size_t)row * C + col0 + col];
   }
   __syncthreads();
-  // 2. inverse column NTT of every (source limb, column)
+  // 2. inverse column NTT of every (source limb, column); the epilogue applies
+  //    n^-1 (mode 1) or n^-1 qhat_s^-1 (mode 0: the conversion's first factor)
   for (int task = warp; task < A.ns * TCF; task += kWarps) {
     const int s = task / TCF, col = task - s * TCF;
     const int p = A.src_prime[s];
@@ -228,36 +229,45 @@ __global__ void __launch_bounds__(kWarps * 32) fused_col_kernel(FusedColArgs A, 
     for (int k = 0; k < E; ++k) x[k] = sm[swz(lane + 32 * k)];
     __syncwarp();
     warp_inv<LOGR>(x, sm, lane, q, tw);
-    const u64 ni = T.ninv[p], nis = T.ninv_s[p];
+    const u64 ym = A.mode == 0 ? A.ymul[s] : T.ninv[p], yms = A.mode == 0 ? A.ymul_s[s] : T.ninv_s[p];
 #pragma unroll
-    for (int k = 0; k < E; ++k) sm[swz(lane + 32 * k)] = mul_shoup(x[k], ni, nis, q);
+    for (int k = 0; k < E; ++k) sm[swz(lane + 32 * k)] = mul_shoup(x[k], ym, yms, q);
     __syncwarp();
   }
   __syncthreads();
-  // 3. conversion into the destination tiles (coefficient domain)
-  for (int e = threadIdx.x; e < R * TCF; e += blockDim.x) {
-    const int row = e / TCF, col = e - row * TCF;
-    const int r = swz(row);
+  // 3. conversion into the destination tiles (coefficient domain), one
+  //    destination prime at a time so its constants stay in registers
+  for (int d = 0; d < A.nd; ++d) {
+    const int pd = A.dst_prime[d];
+    const u64 q = T.q[pd];
+    u64* out = region(A.ns + d, 0);
     if (A.mode == 0) {
-      u64 y[8];  // ns <= alpha <= 8 (fused_path); compile-time indexing keeps y in registers
+      u64 h[8], hs[8];
 #pragma unroll
       for (int s = 0; s < 8; ++s)
-        if (s < A.ns) y[s] = mul_shoup(region(s, col)[r], A.qinv[s], A.qinv_s[s], T.q[A.src_prime[s]]);
-      for (int d = 0; d < A.nd; ++d) {
-        U128 acc{0, 0};
+        if (s < A.ns) h[s] = A.qhat[(size_t)s * A.nd + d], hs[s] = A.qhat_s[(size_t)s * A.nd + d];
+      const u64 q2 = 2 * q;
+      for (int e = threadIdx.x; e < R * TCF; e += blockDim.x) {
+        const int row = e / TCF, col = e - row * TCF;
+        const int r = swz(row);
+        u64 acc = 0;  // sum of lazy Shoup products, kept in [0, 2q)
 #pragma unroll
         for (int s = 0; s < 8; ++s)
-          if (s < A.ns) mac128(acc, y[s], A.qhat[(size_t)s * A.nd + d]);
-        const int pd = A.dst_prime[d];
-        region(A.ns + d, col)[r] = reduce128(acc.hi, acc.lo, T.q[pd], T.mh[pd], T.ml[pd]);
+          if (s < A.ns) {
+            acc += mul_shoup_lazy(region(s, col)[r], h[s], hs[s], q);
+            acc = acc >= q2 ? acc - q2 : acc;
+          }
+        out[(size_t)col * PAD + r] = acc >= q ? acc - q : acc;
       }
     } else {  // rescale lift: centred x mod q_last reduced mod each destination prime
-      const u64 v = region(0, col)[r];
-      for (int d = 0; d < A.nd; ++d) {
-        const int pd = A.dst_prime[d];
-        const u64 q = T.q[pd];
-        const u64 rr = reduce64(v, q, T.mh[pd]);
-        region(A.ns + d, col)[r] = v > (A.q_last >> 1) ? sub_mod(rr, reduce64(A.q_last, q, T.mh[pd]), q) : rr;
+      const u64 mh = T.mh[pd];
+      const u64 ql = reduce64(A.q_last, q, mh), half = A.q_last >> 1;
+      for (int e = threadIdx.x; e < R * TCF; e += blockDim.x) {
+        const int row = e / TCF, col = e - row * TCF;
+        const int r = swz(row);
+        const u64 v = region(0, col)[r];
+        const u64 rr = reduce64(v, q, mh);
+        out[(size_t)col * PAD + r] = v > half ? sub_mod(rr, ql, q) : rr;
       }
     }
   }
@@ -286,9 +296,12 @@ __global__ void __launch_bounds__(kWarps * 32) fused_col_kernel(FusedColArgs A, 
   }
   __syncthreads();
   // 5. store the destination tiles (lazy [0, 4q) values; the row pass accepts them)
-  for (int e = threadIdx.x; e < A.nd * R * TCF; e += blockDim.x) {
-    const int d = e / (R * TCF), rem = e - d * R * TCF, row = rem / TCF, col = rem - row * TCF;
-    dst[(size_t)A.out_slot[d] * n + (size_t)row * C + col0 + col] = region(A.ns + d, col)[swz(row)];
+  for (int d = 0; d < A.nd; ++d) {
+    u64* o = dst + (size_t)A.out_slot[d] * n + col0;
+    for (int e = threadIdx.x; e < R * TCF; e += blockDim.x) {
+      const int row = e / TCF, col = e - row * TCF;
+      o[(size_t)row * C + col] = region(A.ns + d, col)[swz(row)];
+    }
   }
 }
 
