@@ -69,6 +69,15 @@ class Clocks:
         for line in self.proc.stdout:
             self.rows.append([x.strip() for x in line.split(",")])
 
+    def wait_first(self, timeout=5.0):
+        """nvidia-smi's start-up is not allowed to overlap the timed region."""
+        t = time.time()
+        while self.proc and not self.rows and time.time() - t < timeout:
+            time.sleep(0.05)
+
+    def mark(self):
+        self.start = len(self.rows)
+
     def __exit__(self, *a):
         if self.proc:
             self.proc.terminate()
@@ -78,14 +87,15 @@ class Clocks:
                 self.proc.kill()
 
     def summary(self):
-        if not self.rows:
+        rows = self.rows[getattr(self, "start", 0):] or self.rows[-1:]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > i + 2 and r[i + 2] == "Active"})
+        reasons = sorted({names[i] for r in rows for i in range(4) if len(r) > i + 2 and r[i + 2] == "Active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(rows)}
 
 
 # ------------------------------------------------------------------------ workload
@@ -276,6 +286,8 @@ def main():
     layer = LlamaLayer(be, sf, log)
     log(f"[bench] setup {time.time() - t0:.1f}s")
 
+    clk = Clocks(local).__enter__()  # sampling starts before the warm-up
+    clk.wait_first()
     for _ in range(args.warmup):
         layer.step()
     be.synchronize()
@@ -287,6 +299,7 @@ def main():
         layer.step()
         be.synchronize()
         torch.cuda.nvtx.range_pop()
+        clk.__exit__()
         return
 
     def barrier():
@@ -300,14 +313,15 @@ def main():
     barrier()
     be.synchronize()
     l0 = be.kernel_launches()
-    with Clocks(local) as clk:
-        be.event_record(0)
-        t_host = time.perf_counter()
-        for _ in range(args.steps):
-            outs = layer.step()
-        t_host = (time.perf_counter() - t_host) * 1e3 / args.steps
-        be.event_record(1)
-        ms_total = be.event_elapsed_ms(0, 1)
+    clk.mark()
+    be.event_record(0)
+    t_host = time.perf_counter()
+    for _ in range(args.steps):
+        outs = layer.step()
+    t_host = (time.perf_counter() - t_host) * 1e3 / args.steps
+    be.event_record(1)
+    ms_total = be.event_elapsed_ms(0, 1)
+    clk.__exit__()
     be.synchronize()
     barrier()
     launches = be.kernel_launches() - l0

@@ -188,32 +188,35 @@ __global__ void __launch_bounds__(kWarps * 32) ntt_col_pass(LimbBatch B, Tabs T)
 }
 
 // ------------------------------------------------------------ fused column
-// One CTA = one job x TCF columns. Shared memory holds ns + nd column tiles.
-constexpr int TCF = 4;
-
-template <int LOGR, int LOGC>
-__global__ void __launch_bounds__(kWarps * 32) fused_col_kernel(FusedColArgs A, Tabs T) {
+// One CTA = one job x TCF adjacent columns, one warp per column (TCF warps).
+// Shared memory holds the ns source tiles and two destination tiles; the
+// destinations are produced one prime at a time (conversion -> forward column
+// NTT -> store), so shared memory does not grow with nd and every phase keeps
+// all warps busy. TCF = 8 gives 64-byte row segments for big batches; TCF = 2
+// gives 4x more CTAs for single-ciphertext launches.
+template <int LOGR, int LOGC, int TCF>
+__global__ void __launch_bounds__(TCF * 32, TCF == 8 ? 3 : 8) fused_col_kernel(FusedColArgs A, Tabs T) {
   constexpr int R = 1 << LOGR, C = 1 << LOGC, E = R / 32, LOGN = LOGR + LOGC;
   constexpr int PAD = R + 1;
   constexpr int tiles = C / TCF;
-  extern __shared__ u64 sm_all[];  // [(ns + nd) * TCF][PAD]
+  constexpr int NT = TCF * 32;
+  extern __shared__ u64 sm_all[];  // [ns][TCF][PAD] sources, [2][TCF][PAD] destinations
   const int job = blockIdx.x / tiles, tile = blockIdx.x - job * tiles;
   const int col0 = tile * TCF;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n = T.n;
+  constexpr int n = 1 << LOGN;
   const u64* src = A.src[job];
   u64* dst = A.dst[job];
   auto region = [&](int limb, int col) { return sm_all + (size_t)(limb * TCF + col) * PAD; };
-  // 1. stage the source tiles (32-byte row segments)
-  for (int e = threadIdx.x; e < A.ns * R * TCF; e += blockDim.x) {
+  // 1. stage the source tiles (TCF*8-byte row segments)
+  for (int e = threadIdx.x; e < A.ns * R * TCF; e += NT) {
     const int s = e / (R * TCF), rem = e - s * R * TCF, row = rem / TCF, col = rem - row * TCF;
     region(s, col)[swz(row)] = src[(size_t)s * n + (size_t)row * C + col0 + col];
   }
   __syncthreads();
   // 2. inverse column NTT of every (source limb, column); the epilogue applies
   //    n^-1 (mode 1) or n^-1 qhat_s^-1 (mode 0: the conversion's first factor)
-  for (int task = warp; task < A.ns * TCF; task += kWarps) {
-    const int s = task / TCF, col = task - s * TCF;
+  for (int s = 0; s < A.ns; ++s) {
     const int p = A.src_prime[s];
     const u64 q = T.q[p];
     const u64* W = T.ipsi + ((size_t)p << LOGN);
@@ -223,7 +226,7 @@ __global__ void __launch_bounds__(kWarps * 32) fused_col_kernel(FusedColArgs A, 
       w = W[i];
       ws = Ws[i];
     };
-    u64* sm = region(s, col);
+    u64* sm = region(s, warp);
     u64 x[E];
 #pragma unroll
     for (int k = 0; k < E; ++k) x[k] = sm[swz(lane + 32 * k)];
@@ -235,19 +238,18 @@ __global__ void __launch_bounds__(kWarps * 32) fused_col_kernel(FusedColArgs A, 
     __syncwarp();
   }
   __syncthreads();
-  // 3. conversion into the destination tiles (coefficient domain), one
-  //    destination prime at a time so its constants stay in registers
   for (int d = 0; d < A.nd; ++d) {
     const int pd = A.dst_prime[d];
     const u64 q = T.q[pd];
-    u64* out = region(A.ns + d, 0);
+    u64* out = region(A.ns + (d & 1), 0);
+    // 3. conversion (coefficient domain) into destination tile d & 1
     if (A.mode == 0) {
       u64 h[8], hs[8];
 #pragma unroll
       for (int s = 0; s < 8; ++s)
         if (s < A.ns) h[s] = A.qhat[(size_t)s * A.nd + d], hs[s] = A.qhat_s[(size_t)s * A.nd + d];
       const u64 q2 = 2 * q;
-      for (int e = threadIdx.x; e < R * TCF; e += blockDim.x) {
+      for (int e = threadIdx.x; e < R * TCF; e += NT) {
         const int row = e / TCF, col = e - row * TCF;
         const int r = swz(row);
         u64 acc = 0;  // sum of lazy Shoup products, kept in [0, 2q)
@@ -262,7 +264,7 @@ __global__ void __launch_bounds__(kWarps * 32) fused_col_kernel(FusedColArgs A, 
     } else {  // rescale lift: centred x mod q_last reduced mod each destination prime
       const u64 mh = T.mh[pd];
       const u64 ql = reduce64(A.q_last, q, mh), half = A.q_last >> 1;
-      for (int e = threadIdx.x; e < R * TCF; e += blockDim.x) {
+      for (int e = threadIdx.x; e < R * TCF; e += NT) {
         const int row = e / TCF, col = e - row * TCF;
         const int r = swz(row);
         const u64 v = region(0, col)[r];
@@ -270,37 +272,32 @@ __global__ void __launch_bounds__(kWarps * 32) fused_col_kernel(FusedColArgs A, 
         out[(size_t)col * PAD + r] = v > half ? sub_mod(rr, ql, q) : rr;
       }
     }
-  }
-  __syncthreads();
-  // 4. forward column NTT of every (destination limb, column)
-  for (int task = warp; task < A.nd * TCF; task += kWarps) {
-    const int d = task / TCF, col = task - d * TCF;
-    const int p = A.dst_prime[d];
-    const u64 q = T.q[p];
-    const u64* W = T.psi + ((size_t)p << LOGN);
-    const u64* Ws = T.psi_s + ((size_t)p << LOGN);
-    auto tw = [&](int b, int blk, u64& w, u64& ws) {
-      const int i = (1 << (LOGR - 1 - b)) + blk;
-      w = W[i];
-      ws = Ws[i];
-    };
-    u64* sm = region(A.ns + d, col);
-    u64 x[E];
+    __syncthreads();
+    // 4. forward column NTT, one column per warp
+    {
+      const u64* W = T.psi + ((size_t)pd << LOGN);
+      const u64* Ws = T.psi_s + ((size_t)pd << LOGN);
+      auto tw = [&](int b, int blk, u64& w, u64& ws) {
+        const int i = (1 << (LOGR - 1 - b)) + blk;
+        w = W[i];
+        ws = Ws[i];
+      };
+      u64* sm = out + (size_t)warp * PAD;
+      u64 x[E];
 #pragma unroll
-    for (int k = 0; k < E; ++k) x[k] = sm[swz(lane + 32 * k)];
-    __syncwarp();
-    warp_fwd<LOGR>(x, sm, lane, q, tw);
+      for (int k = 0; k < E; ++k) x[k] = sm[swz(lane + 32 * k)];
+      __syncwarp();
+      warp_fwd<LOGR>(x, sm, lane, q, tw);
 #pragma unroll
-    for (int k = 0; k < E; ++k) sm[swz(lane + 32 * k)] = x[k];
-    __syncwarp();
-  }
-  __syncthreads();
-  // 5. store the destination tiles (lazy [0, 4q) values; the row pass accepts them)
-  for (int d = 0; d < A.nd; ++d) {
+      for (int k = 0; k < E; ++k) sm[swz(lane + 32 * k)] = x[k];
+    }
+    __syncthreads();
+    // 5. store (lazy [0, 4q) values; the row pass accepts them). The next
+    //    destination converts into the other tile, so no barrier is needed here.
     u64* o = dst + (size_t)A.out_slot[d] * n + col0;
-    for (int e = threadIdx.x; e < R * TCF; e += blockDim.x) {
+    for (int e = threadIdx.x; e < R * TCF; e += NT) {
       const int row = e / TCF, col = e - row * TCF;
-      o[(size_t)row * C + col] = region(A.ns + d, col)[swz(row)];
+      o[(size_t)row * C + col] = out[(size_t)col * PAD + swz(row)];
     }
   }
 }
@@ -444,19 +441,27 @@ void run_epi(Context& c, const EpiBatch& e) {
   ntt_row_epi<LOGR, LOGC><<<grid, kWarps * 32, 0, c.stream>>>(e, c.tabs);
 }
 
-template <int LOGR, int LOGC>
-void run_fused(Context& c, const FusedColArgs& a) {
+template <int LOGR, int LOGC, int TCF>
+void run_fused_t(Context& c, const FusedColArgs& a) {
   constexpr int R = 1 << LOGR;
-  const size_t sm = (size_t)(a.ns + a.nd) * TCF * (R + 1) * sizeof(u64);
+  const size_t sm = (size_t)(a.ns + 2) * TCF * (R + 1) * sizeof(u64);
   static int configured = 0;
   if (!configured) {
-    SF_CUDA(cudaFuncSetAttribute(fused_col_kernel<LOGR, LOGC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SF_CUDA(cudaFuncSetAttribute(fused_col_kernel<LOGR, LOGC, TCF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  200 * 1024));
     configured = 1;
   }
-  require(sm <= 200 * 1024, kInternal, "fused column stage: too many limbs for shared memory");
+  require(sm <= 200 * 1024, kInternal, "fused column stage: too many source limbs for shared memory");
   const unsigned grid = (unsigned)a.count * ((1u << LOGC) / TCF);
-  fused_col_kernel<LOGR, LOGC><<<grid, kWarps * 32, sm, c.stream>>>(a, c.tabs);
+  fused_col_kernel<LOGR, LOGC, TCF><<<grid, TCF * 32, sm, c.stream>>>(a, c.tabs);
+}
+
+template <int LOGR, int LOGC>
+void run_fused(Context& c, const FusedColArgs& a) {
+  if ((size_t)a.count * ((1u << LOGC) / 8) >= 444)
+    run_fused_t<LOGR, LOGC, 8>(c, a);
+  else
+    run_fused_t<LOGR, LOGC, 2>(c, a);
 }
 
 template <int LOGR, int LOGC>

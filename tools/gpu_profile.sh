@@ -1,0 +1,10 @@
+#!/usr/bin/env bash
+# launch list of one decode step + ncu --set full of the largest launch of the top kernels
+#   gpurun -- bash tools/gpu_profile.sh TAG [K]
+TAG=$1; K=${2:-5}
+OUT=gpurun_out/$TAG; mkdir -p $OUT
+timeout 900 ncu --nvtx --nvtx-include "sf_step/" --metrics gpu__time_duration.sum --clock-control none \
+    --csv --log-file $OUT/launches.csv python bench.py --nvtx-step --warmup 3 --no-cpu-baseline > $OUT/ncu_launch.log 2>&1
+echo "launch list rc=$?"
+SPECS=$(python tools/pick_launches.py $OUT/launches.csv $K); echo "picked: $SPECS"
+bash tools/ncu_big.sh $TAG "$SPECS"

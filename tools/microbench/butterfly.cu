@@ -1,0 +1,70 @@
+// Butterfly throughput microbenchmark (B200): exact vs approximate-hi Shoup.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o butterfly butterfly.cu
+#include <cstdint>
+#include <cstdio>
+typedef uint64_t u64;
+typedef uint32_t u32;
+
+__device__ __forceinline__ u64 shoup_exact(u64 x, u64 w, u64 wp, u64 q) { return x * w - __umul64hi(x, wp) * q; }
+__device__ __forceinline__ u64 hi_approx(u64 x, u64 wp) {
+  const u32 xl = (u32)x, xh = (u32)(x >> 32), wl = (u32)wp, wh = (u32)(wp >> 32);
+  return (u64)xh * wh + __umulhi(xh, wl) + __umulhi(xl, wh);
+}
+__device__ __forceinline__ u64 shoup_approx(u64 x, u64 w, u64 wp, u64 q) { return x * w - hi_approx(x, wp) * q; }
+
+template <int V>
+__global__ void bench(u64* out, const u64* in, u64 q, u64 w0, u64 wp0, int iters) {
+  u64 x[8];
+  for (int k = 0; k < 8; ++k) x[k] = in[(threadIdx.x + blockIdx.x * blockDim.x) * 8 + k] % q;
+  const u64 q2 = 2 * q;
+  u64 w = w0, wp = wp0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (k & (1 << b)) continue;
+        u64 U = x[k];
+        U = U >= q2 ? U - q2 : U;
+        u64 T;
+        if (V == 0) T = shoup_exact(x[k | (1 << b)], w, wp, q);
+        else { T = shoup_approx(x[k | (1 << b)], w, wp, q); T = T >= q2 ? T - q2 : T; }
+        x[k] = U + T;
+        x[k | (1 << b)] = U - T + q2;
+      }
+    }
+    w ^= (u64)it & 1;  // keep twiddles loop-variant
+  }
+  u64 s = 0;
+  for (int k = 0; k < 8; ++k) s ^= x[k];
+  out[threadIdx.x + blockIdx.x * blockDim.x] = s;
+}
+
+int main() {
+  const int blocks = 148 * 8, threads = 256, iters = 2000;
+  const size_t nth = (size_t)blocks * threads;
+  u64 *in, *out;
+  cudaMalloc(&in, nth * 8 * 8);
+  cudaMalloc(&out, nth * 8);
+  cudaMemset(in, 0x5a, nth * 64);
+  const u64 q = 1152921504606584833ull;  // < 2^60
+  const u64 w = 123456789123456789ull % q;
+  const u64 wp = (u64)(((unsigned __int128)w << 64) / q);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  for (int v = 0; v < 2; ++v) {
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaEventRecord(a);
+      if (v == 0) bench<0><<<blocks, threads>>>(out, in, q, w, wp, iters);
+      else bench<1><<<blocks, threads>>>(out, in, q, w, wp, iters);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms;
+      cudaEventElapsedTime(&ms, a, b);
+      const double bf = (double)nth * iters * 12;
+      if (rep) printf("variant %d: %.3f ms, %.1f G butterflies/s\n", v, ms, bf / ms / 1e6);
+    }
+  }
+  return 0;
+}
