@@ -346,6 +346,8 @@ def main():
     by = (C.c_double * 6)()
     nl = (C.c_longlong * 6)()
     lib.sf_profile_end(be.ctx, ms, by, nl)
+    bf = (C.c_double * 6)()
+    lib.sf_profile_butterflies(be.ctx, bf)
     fams = ["ntt", "keyswitch_inner", "ctpt_mac", "basis_conv", "elementwise", "sampling"]
     prof = {f: {"ms_per_step": ms[i] / args.steps, "launches_per_step": nl[i] / args.steps,
                 "GBps": (by[i] / (ms[i] * 1e-3) / 1e9) if ms[i] > 0 else None} for i, f in enumerate(fams)}
@@ -358,6 +360,22 @@ def main():
                 "traffic": None, "peak_source": "measured" if not P.get("_fallback") else "fallback",
                 "algorithmic_bytes_per_launch": by[dom] / max(nl[dom], 1),
                 "avg_launch_us": ms[dom] * 1e3 / max(nl[dom], 1)}
+
+    # INT roofline: the NTT-bearing kernels (row / column / key-switch row passes)
+    # against the measured register-resident butterfly peak
+    try:
+        bpk = json.load(open(os.path.join(ROOT, "profiles", "r1_butterfly_peak.json")))["exact_shoup_G_butterflies_per_s"]
+    except Exception:
+        bpk = None
+    nt_ms = ms[0] + ms[1]
+    bf_tot = bf[0] + bf[1]
+    int_roofline = {"bound": "int (FMA-heavy pipe: 64-bit IMAD of the Shoup butterflies)",
+                    "kernels": "ntt + keyswitch_inner families",
+                    "butterflies_per_step": bf_tot / args.steps,
+                    "achieved": round(bf_tot / (nt_ms * 1e-3) / 1e9, 1) if nt_ms > 0 else None,
+                    "peak": bpk, "unit": "G butterfly/s",
+                    "frac": round(bf_tot / (nt_ms * 1e-3) / 1e9 / bpk, 4) if (nt_ms > 0 and bpk) else None,
+                    "peak_source": "profiles/r1_butterfly_peak.json (tools/microbench/butterfly.cu on B200)"}
 
     # ---- e2e: public API with host buffers (import inputs from pinned host
     # memory, read the results back), host wall clock around whole steps
@@ -414,6 +432,7 @@ def main():
                    "l2": "working set (plaintext diagonals + keys ~30 GB) >> 126 MB L2; no flush needed"},
         "hevmm_ct_per_s": round(vmm_per_step * world / (ms_step * 1e-3), 2),
         "roofline": roofline,
+        "int_roofline": int_roofline,
         "cpu_baseline": cpu,
         "e2e": {"value": round(e2e_ms / world, 3), "unit": "ms/token", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "breakdown": e2e_parts},

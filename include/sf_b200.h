@@ -231,6 +231,9 @@ long long sf_kernel_launches(const sf_context* ctx);
 #define SF_PROF_FAMILIES 6
 sf_status sf_profile_begin(sf_context* ctx, int mask);
 sf_status sf_profile_end(sf_context* ctx, double* ms, double* bytes, long long* launches);
+/* Radix-2 NTT butterflies each family executed in the last profile window
+   (the INT-pipe work measure behind bench.py's int_roofline). */
+sf_status sf_profile_butterflies(sf_context* ctx, double* butterflies);
 
 #ifdef __cplusplus
 }

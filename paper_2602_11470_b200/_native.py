@@ -39,6 +39,7 @@ st = C.c_int
 
 SIGNATURES = {
     "sf_last_error": (C.c_char_p, []),
+    "sf_profile_butterflies": (st, [vp, dp]),
     "sf_context_create": (st, [C.POINTER(SfParams), vpp]),
     "sf_context_destroy": (None, [vp]),
     "sf_context_info": (st, [vp, ip, ip, ip, ip, ip, u64p]),

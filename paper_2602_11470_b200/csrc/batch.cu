@@ -7,6 +7,8 @@
 // layout allows. This turns the thousands of per-ciphertext operations of an
 // attention decode step (256 K ciphertexts, 510 V handles, 2.5k rotations)
 // into a few hundred full-GPU launches.
+#include <algorithm>
+
 #include "batch.cuh"
 #include "modarith.cuh"
 
@@ -18,6 +20,12 @@ constexpr int kT = 256;
 inline void post(Context& c) {
   c.launches.fetch_add(1, std::memory_order_relaxed);
   SF_CUDA(cudaGetLastError());
+}
+
+// butterflies of one half (row or column pass) of a limb NTT: n/2 per stage
+inline double half_bfly(const Context& c, bool column) {
+  const int logr = c.logn / 2, logc = c.logn - logr;
+  return 0.5 * c.n * (column ? logr : logc);
 }
 
 inline dim3 grid2(size_t per_job_threads, int jobs) {
@@ -287,14 +295,14 @@ void b_tensor(Context& c, const TensorBatch& B, int limbs) {
 // stage reads ns and writes nd limbs (its transforms stay in shared memory).
 void b_row(Context& c, const LimbBatch& b, bool inverse) {
   if (!b.count) return;
-  ProfScope prof(c, kFamNtt, 16.0 * c.n * b.count);
+  ProfScope prof(c, kFamNtt, 16.0 * c.n * b.count, half_bfly(c, false) * b.count);
   ntt_row_only(c, b, inverse);
   post(c);
 }
 
 void b_fused_col(Context& c, const FusedColArgs& A) {
   if (!A.count) return;
-  ProfScope prof(c, kFamNtt, 8.0 * c.n * (A.ns + A.nd) * A.count);
+  ProfScope prof(c, kFamNtt, 8.0 * c.n * (A.ns + A.nd) * A.count, half_bfly(c, true) * (A.ns + A.nd) * A.count);
   ntt_fused_col(c, A);
   post(c);
 }
@@ -304,7 +312,7 @@ void b_row_epi(Context& c, const EpiBatch& E) {
   // row pass in + acc + addend + out
   double bytes = 0;
   for (int i = 0; i < E.count; ++i) bytes += 8.0 * c.n * (E.addend[i] ? 4 : 3);
-  ProfScope prof(c, kFamNtt, bytes);
+  ProfScope prof(c, kFamNtt, bytes, half_bfly(c, false) * E.count);
   ntt_row_epi(c, E);
   post(c);
 }
@@ -343,7 +351,16 @@ void b_ks_row(Context& c, const KsRowArgs& A) {
   if (!A.nsrc) return;
   // sources: ndig rows per target; jobs: 2 key rows per digit + 2 outputs per target
   const double jobs = A.job_begin[A.nsrc];
-  ProfScope prof(c, kFamKs, 8.0 * c.n * A.nt * ((double)A.nsrc * A.ndig + jobs * (2.0 * A.ndig + 2.0)));
+  // row NTTs: every non-own digit row of every unit and target; two inverse rows per job and special prime
+  double rows = 0;
+  for (int t = 0; t < A.nt; ++t)
+    for (int j = 0; j < A.ndig; ++j) {
+      const int lo = j * A.alpha, hi = std::min(lo + A.alpha, A.limbs);
+      if (!(t >= lo && t < hi)) rows += A.nsrc;
+    }
+  rows += jobs * 2.0 * (A.nt - A.limbs);
+  ProfScope prof(c, kFamKs, 8.0 * c.n * A.nt * ((double)A.nsrc * A.ndig + jobs * (2.0 * A.ndig + 2.0)),
+                 half_bfly(c, false) * rows);
   ntt_ks_row(c, A);
   post(c);
 }

@@ -565,8 +565,9 @@ sf_status sf_profile_end(sf_context* ctx, double* ms, double* bytes, long long* 
     auto& c = *ctx->c;
     c.prof_mask = 0;
     SF_CUDA(cudaStreamSynchronize(c.stream));
-    for (int f = 0; f < SF_PROF_FAMILIES; ++f) ms[f] = 0.0, bytes[f] = 0.0, launches[f] = 0;
+    for (int f = 0; f < SF_PROF_FAMILIES; ++f) ms[f] = 0.0, bytes[f] = 0.0, launches[f] = 0, c.prof_bfly[f] = 0.0;
     for (const auto& r : c.prof_recs) {
+      c.prof_bfly[r.family] += r.bfly;
       float t = 0.f;
       SF_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
       ms[r.family] += t;
@@ -575,6 +576,12 @@ sf_status sf_profile_end(sf_context* ctx, double* ms, double* bytes, long long* 
     }
     c.prof_recs.clear();
     c.prof_pool_next = 0;
+  });
+}
+
+sf_status sf_profile_butterflies(sf_context* ctx, double* out) {
+  return guard([&] {
+    for (int f = 0; f < SF_PROF_FAMILIES; ++f) out[f] = ctx->c->prof_bfly[f];
   });
 }
 

@@ -140,6 +140,7 @@ struct ProfRec {
   int family;
   cudaEvent_t a, b;
   double bytes;
+  double bfly;  // radix-2 NTT butterflies the launch executes (0 for non-NTT kernels)
 };
 
 struct Context {
@@ -148,6 +149,7 @@ struct Context {
   std::vector<ProfRec> prof_recs;
   std::vector<cudaEvent_t> prof_pool;
   size_t prof_pool_next = 0;
+  double prof_bfly[kFamCount] = {};  // butterflies per family of the last profile window
 
   // parameters
   int logn = 0, n = 0, slots = 0, L = 0, alpha = 0, beta = 0, np = 0;
@@ -195,7 +197,7 @@ struct ProfScope {
   double bytes;
   bool on;
   cudaEvent_t b{};
-  ProfScope(Context& ctx, int family, double algorithmic_bytes);
+  ProfScope(Context& ctx, int family, double algorithmic_bytes, double butterflies = 0.0);
   ~ProfScope();
 };
 

@@ -28,13 +28,13 @@ static cudaEvent_t prof_event(Context& c) {
   return c.prof_pool[c.prof_pool_next++];
 }
 
-ProfScope::ProfScope(Context& ctx, int family, double algorithmic_bytes)
+ProfScope::ProfScope(Context& ctx, int family, double algorithmic_bytes, double butterflies)
     : c(ctx), fam(family), bytes(algorithmic_bytes), on(((ctx.prof_mask >> family) & 1) != 0) {
   if (!on) return;
   cudaEvent_t a = prof_event(c);
   b = prof_event(c);
   SF_CUDA(cudaEventRecord(a, c.stream));
-  c.prof_recs.push_back({fam, a, b, bytes});
+  c.prof_recs.push_back({fam, a, b, bytes, butterflies});
 }
 ProfScope::~ProfScope() {
   if (on) cudaEventRecord(b, c.stream);
@@ -382,7 +382,7 @@ const u64* QP(Context& c) { return c.tabs.q; }
 void launch_ntt(Context& c, const LimbBatch& b, bool inverse) {
   if (b.count == 0) return;
   const int n = c.n;
-  ProfScope prof(c, kFamNtt, 16.0 * n * b.count);
+  ProfScope prof(c, kFamNtt, 16.0 * n * b.count, 0.5 * n * c.logn * b.count);
   if (c.logn >= 12) {
     ntt_two_pass(c, b, inverse);
     post_launch(c);
