@@ -234,6 +234,9 @@ sf_status sf_profile_end(sf_context* ctx, double* ms, double* bytes, long long* 
 /* Radix-2 NTT butterflies each family executed in the last profile window
    (the INT-pipe work measure behind bench.py's int_roofline). */
 sf_status sf_profile_butterflies(sf_context* ctx, double* butterflies);
+/* Host-side wall time per internal scope ("name total_us calls" lines), collected
+   when SF_HOST_PROF=1 is set in the environment; diagnostics only. */
+sf_status sf_host_profile(char* buf, int len, int reset);
 
 #ifdef __cplusplus
 }

@@ -69,6 +69,7 @@ def lib():
             "ock_rotate": (vp, [vp, vp, C.c_int]),
             "ock_rescale": (vp, [vp, vp]),
             "ock_tensor_sum": (vp, [vp, C.POINTER(vp), C.POINTER(vp), C.c_int]),
+            "ock_rot_sum": (vp, [vp, C.POINTER(vp), C.POINTER(C.c_int), C.c_int]),
             "ock_relin_rescale": (vp, [vp, vp]),
             "ock_ct_is_three": (C.c_int, [vp]),
             "ock_ct_d2": (None, [vp, U64P]),
@@ -88,6 +89,15 @@ def _u64(a: np.ndarray):
 
 def _dp(a: np.ndarray):
     return a.ctypes.data_as(DP)
+
+
+def fold_radix(d_head: int):
+    """Radix split of the head fold: log2(d_head) = D bits as
+    one rotation sum when D <= 3, else two sums of ceil(D/2) and floor(D/2) bits."""
+    D = d_head.bit_length() - 1
+    if D <= 0:
+        return []
+    return [D] if D <= 3 else [(D + 1) // 2, D // 2]
 
 
 def fmix(z: int) -> int:
@@ -337,6 +347,46 @@ class CkksOracle:
             return a
         self.ledger.count_rotation(hoisted)
         return OCt(self, lib().ock_rotate(self.ptr, a.ptr, int(r)), a.level, None)
+
+    def rot_sum(self, terms, hoisted: bool = False):
+        """sum_i Rot(a_i, r_i) (one ModDown for the whole sum),
+        charged as the reference's rotate/add chain: one rotation per r_i != 0
+        (mod N) and len(terms) - 1 additions; layouts merge as that chain's."""
+        for a, _ in terms:
+            self._check(a, "rotate")
+        ly = None
+        for i, (a, r) in enumerate(terms):
+            if r % self.N:
+                self.ledger.count_rotation(hoisted)
+            t_ly = a.layout if r % self.N == 0 else None
+            ly = t_ly if i == 0 else (ly if (ly is not None and ly == t_ly) else None)
+        for _ in range(len(terms) - 1):
+            self.ledger.count_add()
+        arr = (C.c_void_p * len(terms))(*[a.ptr for a, _ in terms])
+        rr = (C.c_int * len(terms))(*[int(r) for _, r in terms])
+        lvl = min(a.level for a, _ in terms)
+        return OCt(self, lib().ock_rot_sum(self.ptr, arr, rr, len(terms)), lvl, ly)
+
+    def fold(self, c, d_head: int, t: int):
+        """fold_within_head (kv_attention.cpp:38-41): sum_{k < d_head} Rot(c, k t),
+        evaluated as radix rotation sums (fold_radix) and charged
+        as the reference's log2(d_head) rotate + add steps."""
+        self._check(c, "rotate")
+        steps = fold_radix(d_head)
+        nrot = sum(1 for l in range(d_head.bit_length() - 1) if ((1 << l) * t) % self.N)
+        for _ in range(nrot):
+            self.ledger.count_rotation(False)
+        for _ in range(d_head.bit_length() - 1):
+            self.ledger.count_add()
+        led, self.ledger = self.ledger, CostLedger()
+        try:
+            stride = t
+            for bits in steps:
+                c = self.rot_sum([(c, k * stride) for k in range(1 << bits)])
+                stride <<= bits
+        finally:
+            self.ledger = led
+        return OCt._alias(c, None)
 
     def level_drop(self, a, target: int):
         self._check(a, "level_drop")

@@ -535,9 +535,11 @@ void conv_basis(const Ctx& c, const std::vector<int>& src, const std::vector<con
   }
 }
 
-// hybrid key switch of d (NTT, `limbs` limbs) under key `g` with the NTT-domain
-// automorphism applied after ModUp. Returns (kb, ka) in out.
-void key_switch(Ctx& c, const u64* d, int limbs, u64 g, u64* kb, u64* ka) {
+// Key-switch inner product in the extended basis: ModUp of d
+// (NTT, `limbs` limbs), the NTT-domain automorphism g applied to the ModUp
+// output, and the inner product with key g, ADDED into (accb, acca) = nt limbs
+// each over Q_l u P, NTT domain.
+void key_switch_ext(Ctx& c, const u64* d, int limbs, u64 g, std::vector<u64>& accb, std::vector<u64>& acca) {
   const int n = c.n, np = c.np();
   const auto& key = get_key(c, g);
   std::vector<int> T;  // extended basis, key limb indices
@@ -547,7 +549,6 @@ void key_switch(Ctx& c, const u64* d, int limbs, u64 g, u64* kb, u64* ka) {
   std::vector<u64> dcoef(d, d + (size_t)limbs * n);
 #pragma omp parallel for
   for (int l = 0; l < limbs; ++l) ntt_inv(c, l, dcoef.data() + (size_t)l * n);
-  std::vector<u64> accb((size_t)nt * n, 0), acca((size_t)nt * n, 0);
   const int ndig = (limbs + c.alpha - 1) / c.alpha;
   for (int j = 0; j < ndig; ++j) {
     const int lo = j * c.alpha, hi = std::min((j + 1) * c.alpha, limbs);
@@ -586,28 +587,90 @@ void key_switch(Ctx& c, const u64* d, int limbs, u64 g, u64* kb, u64* ka) {
       }
     }
   }
-  // ModDown
+}
+
+// ModDown of an extended-basis polynomial (nt = limbs + alpha limbs, NTT
+// domain; the P limbs are consumed): out = (acc_Q - conv_{P->Q}(acc_P)) * P^-1.
+void mod_down(Ctx& c, std::vector<u64>& acc, int limbs, u64* out) {
+  const int n = c.n;
   std::vector<int> Pidx;
   for (int k = 0; k < c.alpha; ++k) Pidx.push_back((int)c.P_index(k));
-  for (int which = 0; which < 2; ++which) {
-    std::vector<u64>& acc = which == 0 ? accb : acca;
-    u64* out = which == 0 ? kb : ka;
 #pragma omp parallel for
-    for (int k = 0; k < c.alpha; ++k) ntt_inv(c, Pidx[k], acc.data() + (size_t)(limbs + k) * n);
-    std::vector<const u64*> in;
-    for (int k = 0; k < c.alpha; ++k) in.push_back(acc.data() + (size_t)(limbs + k) * n);
+  for (int k = 0; k < c.alpha; ++k) ntt_inv(c, Pidx[k], acc.data() + (size_t)(limbs + k) * n);
+  std::vector<const u64*> in;
+  for (int k = 0; k < c.alpha; ++k) in.push_back(acc.data() + (size_t)(limbs + k) * n);
+#pragma omp parallel for
+  for (int l = 0; l < limbs; ++l) {
+    const u64 q = c.primes[l];
+    std::vector<u64> t(n);
+    conv_basis(c, Pidx, in, l, t.data());
+    ntt_fwd(c, l, t.data());
+    const u64 pinv = invmod(P_mod(c, q), q);
+    const u64* x = acc.data() + (size_t)l * n;
+    u64* o = out + (size_t)l * n;
+    for (int k = 0; k < n; ++k) o[k] = mulmod(submod(x[k], t[k], q), pinv, q);
+  }
+}
+
+// hybrid key switch of d under key `g` (ModUp, automorphism, inner product,
+// ModDown of both parts). Returns (kb, ka), `limbs` limbs each.
+void key_switch(Ctx& c, const u64* d, int limbs, u64 g, u64* kb, u64* ka) {
+  const size_t nt = (size_t)limbs + c.alpha;
+  std::vector<u64> accb(nt * c.n, 0), acca(nt * c.n, 0);
+  key_switch_ext(c, d, limbs, g, accb, acca);
+  mod_down(c, accb, limbs, kb);
+  mod_down(c, acca, limbs, ka);
+}
+
+// Sum of rotations sum_i Rot(a_i, r_i) with ONE ModDown per part (DESIGN.md
+// §3.8): every term is accumulated in the extended basis Q_l u P -- a
+// rotation contributes its key-switch inner products plus P * sigma_g(c0) on
+// the Q limbs, a zero rotation contributes P * (c0, c1) -- and the sum is
+// brought back to Q_l once. Same value as the op-by-op sum up to the ModDown
+// rounding of one instead of k terms.
+Ct* rot_sum(Ctx& c, const Ct* const* a, const int* rots, int k) {
+  int limbs = 1 << 30;
+  double scale = 0.0;
+  bool any = false;
+  for (int i = 0; i < k; ++i) {
+    limbs = std::min(limbs, a[i]->limbs);
+    if (a[i]->zero) continue;
+    if (!any)
+      scale = a[i]->scale, any = true;
+    else if (std::fabs(a[i]->scale / scale - 1.0) > 1e-9)
+      throw std::runtime_error("ScaleMismatch: add: operand scales differ");
+  }
+  if (!any) return drop_to(c, a[0], limbs);
+  const int n = c.n;
+  const size_t nt = (size_t)limbs + c.alpha;
+  std::vector<u64> accb(nt * n, 0), acca(nt * n, 0);
+  for (int i = 0; i < k; ++i) {
+    if (a[i]->zero) continue;
+    const int r = (int)(((long long)rots[i] % c.slots + c.slots) % c.slots);
+    const u64 g = r == 0 ? 1 : galois_elt(c, r);
+    if (r != 0) key_switch_ext(c, poly(c, a[i], 1, 0), limbs, g, accb, acca);
 #pragma omp parallel for
     for (int l = 0; l < limbs; ++l) {
       const u64 q = c.primes[l];
-      std::vector<u64> t(n);
-      conv_basis(c, Pidx, in, l, t.data());
-      ntt_fwd(c, l, t.data());
-      const u64 pinv = invmod(P_mod(c, q), q);
-      const u64* x = acc.data() + (size_t)l * n;
-      u64* o = out + (size_t)l * n;
-      for (int k = 0; k < n; ++k) o[k] = mulmod(submod(x[k], t[k], q), pinv, q);
+      const u64 pm = P_mod(c, q);
+      std::vector<u64> s0(n);
+      if (r != 0)
+        automorph(c, poly(c, a[i], 0, l), s0.data(), g);
+      else
+        std::memcpy(s0.data(), poly(c, a[i], 0, l), sizeof(u64) * n);
+      u64* ob = accb.data() + (size_t)l * n;
+      for (int j = 0; j < n; ++j) ob[j] = addmod(ob[j], mulmod(s0[j], pm, q), q);
+      if (r == 0) {
+        const u64* s1 = poly(c, a[i], 1, l);
+        u64* oa = acca.data() + (size_t)l * n;
+        for (int j = 0; j < n; ++j) oa[j] = addmod(oa[j], mulmod(s1[j], pm, q), q);
+      }
     }
   }
+  Ct* out = new_ct(c, limbs, scale);
+  mod_down(c, accb, limbs, poly(c, out, 0, 0));
+  mod_down(c, acca, limbs, poly(c, out, 1, 0));
+  return out;
 }
 
 Ct* rotate(Ctx& c, const Ct* a, int r) {
@@ -925,6 +988,9 @@ void* ock_mul(void* c, void* a, void* b) {
 }
 void* ock_rotate(void* c, void* a, int r) {
   return guard([&]() -> void* { return rotate(*static_cast<Ctx*>(c), (Ct*)a, r); });
+}
+void* ock_rot_sum(void* c, void** a, const int* rots, int k) {
+  return guard([&]() -> void* { return rot_sum(*static_cast<Ctx*>(c), (Ct* const*)a, rots, k); });
 }
 void* ock_tensor_sum(void* c, void** a, void** b, int k) {
   return guard([&]() -> void* { return tensor_sum(*static_cast<Ctx*>(c), (Ct* const*)a, (Ct* const*)b, k); });

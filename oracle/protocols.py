@@ -96,6 +96,9 @@ def interleaved_plain(s: Shape, W: np.ndarray, g: int, giant_shift: int) -> np.n
     return interleaved_diag(s, W, g, (i - giant_shift) % s.N)
 
 
+GIANT_GROUPS = 8  # giant-step groups of the BSGS rotation sums
+
+
 def vmm_interleaved(be, x, W: np.ndarray, bsgs: bool = False, out_offset: int = 0,
                     mask_output: bool = False):
     """vmm.cpp:179-236 (the scheme of record)."""
@@ -122,14 +125,19 @@ def vmm_interleaved(be, x, W: np.ndarray, bsgs: bool = False, out_offset: int = 
     else:
         b, giants = bsgs_split(s.k)
         baby = [stair] + [be.rotate(stair, g1 * unit, hoisted=True) for g1 in range(1, b)]
-        acc = None
+        partials = []
         for g2 in range(giants):
             shift = g2 * b * unit
             terms = [(baby[g1], interleaved_plain(s, W, g2 * b + g1, shift))
                      for g1 in range(b) if g2 * b + g1 < s.k]
-            partial = be.mac_plain(terms)
-            aligned = be.rotate(partial, shift)
-            acc = aligned if g2 == 0 else be.add(acc, aligned)
+            partials.append((be.mac_plain(terms), shift))
+        # giant alignment + sum (vmm.cpp:221-222) as GIANT_GROUPS rotation sums
+        # (DESIGN.md §3.8): giants g2 = r mod GIANT_GROUPS share one ModDown,
+        # so shards owning whole groups reproduce this sum exactly
+        acc = None
+        for r in range(min(GIANT_GROUPS, giants)):
+            grp = be.rot_sum(partials[r::GIANT_GROUPS])
+            acc = grp if acc is None else be.add(acc, grp)
     # 3. reduce (vmm.cpp:226-230)
     m = 0
     while (1 << m) < s.t_out:
@@ -303,7 +311,10 @@ def replicate_lanes(be, q, t):
 
 
 def fold_within_head(be, c, d_head, t):
-    """kv_attention.cpp:38-41."""
+    """kv_attention.cpp:38-41 (CKKS backends evaluate it as radix rotation
+    sums, with the reference's ledger charge)."""
+    if hasattr(be, "fold"):
+        return be.fold(c, d_head, t)
     l = 0
     while (1 << l) < d_head:
         c = be.add(c, be.rotate(c, (1 << l) * t))

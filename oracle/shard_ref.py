@@ -32,16 +32,21 @@ def vmm_partial(be, x, W, bsgs, out_offset, rank, world):
             return be.zeros(x.level - 1)
         return be.mac_plain([(be.rotate(stair, g * unit), P.interleaved_plain(s, W, g, 0)) for g in own])
     b, giants = P.bsgs_split(s.k)
-    mine = list(range(rank, giants, world))
-    if not mine:
+    G = P.GIANT_GROUPS
+    groups = [r for r in range(min(G, giants)) if r % world == rank]
+    if not groups:
         return be.zeros(x.level - 1)
     baby = [stair] + [be.rotate(stair, g1 * unit, hoisted=True) for g1 in range(1, b)]
     acc = None
-    for g2 in mine:
-        shift = g2 * b * unit
-        terms = [(baby[g1], P.interleaved_plain(s, W, g2 * b + g1, shift)) for g1 in range(b) if g2 * b + g1 < s.k]
-        aligned = be.rotate(be.mac_plain(terms), shift)
-        acc = aligned if acc is None else be.add(acc, aligned)
+    for r in groups:
+        terms_r = []
+        for g2 in range(r, giants, G):
+            shift = g2 * b * unit
+            terms = [(baby[g1], P.interleaved_plain(s, W, g2 * b + g1, shift))
+                     for g1 in range(b) if g2 * b + g1 < s.k]
+            terms_r.append((be.mac_plain(terms), shift))
+        grp = be.rot_sum(terms_r)
+        acc = grp if acc is None else be.add(acc, grp)
     return acc
 
 

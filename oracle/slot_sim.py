@@ -210,6 +210,22 @@ class SimBackend:
             acc = t if acc is None else self.add(acc, t)
         return acc
 
+    def rot_sum(self, terms, hoisted: bool = False):
+        """sum_i Rot(a_i, r_i) as the reference's rotate/add chain."""
+        acc = None
+        for a, r in terms:
+            x = self.rotate(a, r, hoisted)
+            acc = x if acc is None else self.add(acc, x)
+        return acc
+
+    def fold(self, c, d_head: int, t: int):
+        """fold_within_head, kv_attention.cpp:38-41."""
+        l = 0
+        while (1 << l) < d_head:
+            c = self.add(c, self.rotate(c, (1 << l) * t))
+            l += 1
+        return c
+
     def rotate(self, a, r: int, hoisted: bool = False):
         self._check(a, "rotate")
         s = r % self.N

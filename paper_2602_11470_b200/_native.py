@@ -40,6 +40,7 @@ st = C.c_int
 SIGNATURES = {
     "sf_last_error": (C.c_char_p, []),
     "sf_profile_butterflies": (st, [vp, dp]),
+    "sf_host_profile": (st, [C.c_char_p, C.c_int, C.c_int]),
     "sf_context_create": (st, [C.POINTER(SfParams), vpp]),
     "sf_context_destroy": (None, [vp]),
     "sf_context_info": (st, [vp, ip, ip, ip, ip, ip, u64p]),

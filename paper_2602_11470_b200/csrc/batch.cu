@@ -252,10 +252,57 @@ __global__ void vmm_mac_kernel(VmmMacArgs A, const u64* Q, const u64* MH, const 
   }
 }
 
+// Rotation-sum inner products for ring degrees without the two-pass kernels:
+// one thread per (output, extended limb, coefficient), every limb written in
+// the NTT domain (the generic ModDown follows).
+__global__ void ks_sum_generic_kernel(KsSumArgs A, const u64* Q, const u64* MH, const u64* ML, int logn) {
+  const int o = blockIdx.y;
+  const int n = 1 << logn;
+  const size_t total = (size_t)A.nt * n;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const int t = (int)(i >> logn);
+    const uint32_t k = (uint32_t)(i & (n - 1));
+    const int m = A.tprime[t];
+    const u64 q = Q[m], mh = MH[m], ml = ML[m];
+    const bool qt = t < A.limbs;
+    U128 sb{0, 0}, sa{0, 0};
+    int terms = 0;
+    for (int jb = A.out_begin[o]; jb < A.out_begin[o + 1]; ++jb) {
+      if (terms > 200) {
+        sb = U128{reduce128(sb.hi, sb.lo, q, mh, ml), 0};
+        sa = U128{reduce128(sa.hi, sa.lo, q, mh, ml), 0};
+        terms = 0;
+      }
+      const int s = A.jsrc[jb];
+      const u64 g = A.g[jb];
+      if (g <= 1) {
+        if (qt) {
+          mac128(sb, A.c0[s][(size_t)t * n + k], A.pm[t]);
+          mac128(sa, A.c1[s][(size_t)t * n + k], A.pm[t]);
+          ++terms;
+        }
+        continue;
+      }
+      const uint32_t src = perm_(k, g, logn);
+      for (int j = 0; j < A.ndig; ++j) {
+        const int lo = j * A.alpha, hi = min(lo + A.alpha, A.limbs);
+        const u64 x = (t >= lo && t < hi) ? A.c1[s][(size_t)t * n + src] : A.ext[s][((size_t)j * A.nt + t) * n + src];
+        mac128(sb, x, A.key[jb][((size_t)(j * 2 + 0) * A.np + m) * n + k]);
+        mac128(sa, x, A.key[jb][((size_t)(j * 2 + 1) * A.np + m) * n + k]);
+      }
+      if (qt) mac128(sb, A.c0[s][(size_t)t * n + src], A.pm[t]);
+      terms += A.ndig + 1;
+    }
+    A.acc[o][i] = reduce128(sb.hi, sb.lo, q, mh, ml);
+    A.acc[o][total + i] = reduce128(sa.hi, sa.lo, q, mh, ml);
+  }
+}
+
 }  // namespace
 
 // --------------------------------------------------------------------- wrappers
 void b_copy(Context& c, const CopyBatch& B, size_t words) {
+  SF_HPROF("b_copy");
   if (!B.count) return;
   ProfScope prof(c, kFamElem, 16.0 * words * B.count);
   copy_batch_kernel<<<grid2(words / 2, B.count), kT, 0, c.stream>>>(B, words);
@@ -263,6 +310,7 @@ void b_copy(Context& c, const CopyBatch& B, size_t words) {
 }
 
 void b_add(Context& c, const AddBatch& B, int limbs) {
+  SF_HPROF("b_add");
   if (!B.count) return;
   ProfScope prof(c, kFamElem, 48.0 * limbs * c.n * B.count);
   add_batch_kernel<<<grid2((size_t)limbs * c.n, B.count), kT, 0, c.stream>>>(B, limbs, c.n, c.tabs.q);
@@ -270,12 +318,14 @@ void b_add(Context& c, const AddBatch& B, int limbs) {
 }
 
 void b_sum(Context& c, const SumArgs& A, int limbs) {
+  SF_HPROF("b_sum");
   ProfScope prof(c, kFamElem, 16.0 * limbs * c.n * (A.k + 1));
   sum_kernel<<<grid2((size_t)limbs * c.n * 2, 1), kT, 0, c.stream>>>(A, limbs, c.n, c.tabs.q);
   post(c);
 }
 
 void b_mulpt(Context& c, const MulPtBatch& B, int limbs) {
+  SF_HPROF("b_mulpt");
   if (!B.count) return;
   ProfScope prof(c, kFamMac, 40.0 * limbs * c.n * B.count);
   mulpt_batch_kernel<<<grid2((size_t)limbs * c.n, B.count), kT, 0, c.stream>>>(B, limbs, c.n, c.tabs.q, c.tabs.mh,
@@ -284,6 +334,7 @@ void b_mulpt(Context& c, const MulPtBatch& B, int limbs) {
 }
 
 void b_tensor(Context& c, const TensorBatch& B, int limbs) {
+  SF_HPROF("b_tensor");
   if (!B.count) return;
   ProfScope prof(c, kFamElem, 56.0 * limbs * c.n * B.count);
   tensor_batch_kernel<<<grid2((size_t)limbs * c.n, B.count), kT, 0, c.stream>>>(B, limbs, c.n, c.tabs.q, c.tabs.mh,
@@ -294,6 +345,7 @@ void b_tensor(Context& c, const TensorBatch& B, int limbs) {
 // One NTT row pass moves 8n bytes in and 8n out per limb; the fused column
 // stage reads ns and writes nd limbs (its transforms stay in shared memory).
 void b_row(Context& c, const LimbBatch& b, bool inverse) {
+  SF_HPROF("b_row");
   if (!b.count) return;
   ProfScope prof(c, kFamNtt, 16.0 * c.n * b.count, half_bfly(c, false) * b.count);
   ntt_row_only(c, b, inverse);
@@ -301,6 +353,7 @@ void b_row(Context& c, const LimbBatch& b, bool inverse) {
 }
 
 void b_fused_col(Context& c, const FusedColArgs& A) {
+  SF_HPROF("b_fused_col");
   if (!A.count) return;
   ProfScope prof(c, kFamNtt, 8.0 * c.n * (A.ns + A.nd) * A.count, half_bfly(c, true) * (A.ns + A.nd) * A.count);
   ntt_fused_col(c, A);
@@ -308,6 +361,7 @@ void b_fused_col(Context& c, const FusedColArgs& A) {
 }
 
 void b_row_epi(Context& c, const EpiBatch& E) {
+  SF_HPROF("b_row_epi");
   if (!E.count) return;
   // row pass in + acc + addend + out
   double bytes = 0;
@@ -318,6 +372,7 @@ void b_row_epi(Context& c, const EpiBatch& E) {
 }
 
 void b_tensor_sum(Context& c, const TensorSumArgs& A, int limbs) {
+  SF_HPROF("b_tensor_sum");
   ProfScope prof(c, kFamMac, 8.0 * limbs * c.n * (4.0 * A.k + 3));
   tensor_sum_kernel<<<grid2((size_t)limbs * c.n, 1), kT, 0, c.stream>>>(A, limbs, c.n, c.tabs.q, c.tabs.mh,
                                                                         c.tabs.ml);
@@ -325,6 +380,7 @@ void b_tensor_sum(Context& c, const TensorSumArgs& A, int limbs) {
 }
 
 void b_lift(Context& c, const LiftBatch& B, int limbs, int last_prime) {
+  SF_HPROF("b_lift");
   if (!B.count) return;
   ProfScope prof(c, kFamElem, 8.0 * c.n * (limbs + 1) * B.count);
   lift_batch_kernel<<<grid2((size_t)limbs * c.n, B.count), kT, 0, c.stream>>>(B, limbs, c.n, c.primes[last_prime],
@@ -333,6 +389,7 @@ void b_lift(Context& c, const LiftBatch& B, int limbs, int last_prime) {
 }
 
 void b_conv(Context& c, const ConvBatch& A) {
+  SF_HPROF("b_conv");
   if (!A.count) return;
   ProfScope prof(c, kFamConv, 8.0 * c.n * (A.nsrc + A.ndst) * A.count);
   conv_batch_kernel<<<grid2(c.n, A.count), kT, 0, c.stream>>>(A, c.tabs.q, c.tabs.mh, c.tabs.ml);
@@ -340,6 +397,7 @@ void b_conv(Context& c, const ConvBatch& A) {
 }
 
 void b_ks(Context& c, const KsBatch& A) {
+  SF_HPROF("b_ks");
   if (!A.count) return;
   // ext (one read per job) + key (2 polys per digit) + 2 outputs
   ProfScope prof(c, kFamKs, 8.0 * c.n * ((double)A.ndig * A.nt * 3 + 2.0 * A.nt) * A.count);
@@ -348,6 +406,7 @@ void b_ks(Context& c, const KsBatch& A) {
 }
 
 void b_ks_row(Context& c, const KsRowArgs& A) {
+  SF_HPROF("b_ks_row");
   if (!A.nsrc) return;
   // sources: ndig rows per target; jobs: 2 key rows per digit + 2 outputs per target
   const double jobs = A.job_begin[A.nsrc];
@@ -365,7 +424,20 @@ void b_ks_row(Context& c, const KsRowArgs& A) {
   post(c);
 }
 
+void b_ks_sum(Context& c, const KsSumArgs& A) {
+  SF_HPROF("b_ks_sum");
+  if (!A.nout) return;
+  const double jobs = A.out_begin[A.nout];
+  ProfScope prof(c, kFamKs, 8.0 * c.n * A.nt * (jobs * (3.0 * A.ndig + 2.0) + 2.0 * A.nout),
+                 half_bfly(c, false) * 2.0 * A.nout * (A.nt - A.limbs));
+  if (!ntt_ks_sum(c, A))
+    ks_sum_generic_kernel<<<grid2((size_t)A.nt * c.n, A.nout), kT, 0, c.stream>>>(A, c.tabs.q, c.tabs.mh, c.tabs.ml,
+                                                                                   c.logn);
+  post(c);
+}
+
 void b_subscale(Context& c, const SubScaleBatch& B, int limbs, const u64* inv, const u64* inv_s) {
+  SF_HPROF("b_subscale");
   if (!B.count) return;
   ProfScope prof(c, kFamElem, 32.0 * limbs * c.n * B.count);
   subscale_batch_kernel<<<grid2((size_t)limbs * c.n, B.count), kT, 0, c.stream>>>(B, limbs, c.logn, inv, inv_s,
@@ -374,6 +446,7 @@ void b_subscale(Context& c, const SubScaleBatch& B, int limbs, const u64* inv, c
 }
 
 void b_vmm_mac(Context& c, const VmmMacArgs& A, int limbs) {
+  SF_HPROF("b_vmm_mac");
   const size_t sm = (size_t)A.b * 2 * 64 * sizeof(u64);
   // algorithmic bytes: every diagonal once, babies once, partials once
   ProfScope prof(c, kFamMac, 8.0 * c.n * limbs * ((double)A.k + 2.0 * A.b + 2.0 * A.giants));

@@ -148,17 +148,40 @@ struct KsRowArgs {
   u64* acc[kJobs];        // [2][nt][n]
 };
 
+// Rotation-sum row stage (ntt.cu ks_sum_kernel): per output o,
+// target slot t and destination row, the extended-basis accumulation
+//   acc_o = sum_{jobs of o} [ <sigma_g(ModUp(c1_s)), key_g> + P * sigma_g(c0_s) ]
+// (identity jobs, g <= 1: P * (c0_s, c1_s)), reduced once, written NTT-domain
+// for t < limbs and inverse-row-passed for the special primes (ModDown input).
+// ext holds the FULLY NTT'd ModUp output of every non-own target.
+constexpr int kSumOuts = 128, kSumJobs = 1024, kSumSrcs = 128;
+struct KsSumArgs {
+  int nout = 0, limbs = 0, nt = 0, ndig = 0, alpha = 0, np = 0;
+  int tprime[kMaxPrimes];
+  u64 pm[kMaxPrimes];  // P mod q_t, t < limbs
+  int out_begin[kSumOuts + 1];
+  u64* acc[kSumOuts];  // [2][nt][n]
+  int jsrc[kSumJobs];
+  u64 g[kSumJobs];
+  const u64* key[kSumJobs];
+  const u64* c0[kSumSrcs];
+  const u64* c1[kSumSrcs];
+  const u64* ext[kSumSrcs];  // [ndig][nt][n]
+};
+
 // ntt.cu dispatchers (false when the ring degree has no two-pass kernels)
 bool ntt_row_only(Context& c, const LimbBatch& b, bool inverse);
 bool ntt_row_epi(Context& c, const EpiBatch& e);
 bool ntt_fused_col(Context& c, const FusedColArgs& a);
 bool ntt_ks_row(Context& c, const KsRowArgs& a);
+bool ntt_ks_sum(Context& c, const KsSumArgs& a);
 inline bool fused_path(const Context& c) { return c.logn >= 12 && c.logn <= 17 && c.alpha <= 8; }
 // profiled launch wrappers (batch.cu)
 void b_row(Context& c, const LimbBatch& b, bool inverse);
 void b_fused_col(Context& c, const FusedColArgs& A);
 void b_row_epi(Context& c, const EpiBatch& E);
 void b_ks_row(Context& c, const KsRowArgs& A);
+void b_ks_sum(Context& c, const KsSumArgs& A);
 
 void b_copy(Context& c, const CopyBatch& B, size_t words);
 void b_tensor_sum(Context& c, const TensorSumArgs& A, int limbs);
@@ -190,6 +213,15 @@ std::vector<Ct> mul_plain_batch(Context& c, const std::vector<const Ct*>& xs, co
                                 bool count = true);
 std::vector<Ct> add_batch(Context& c, const std::vector<const Ct*>& a, const std::vector<const Ct*>& b,
                           bool count = true);
+// sum_i Rot(a_i, r_i) per group with one ModDown per part
+struct SumTerm {
+  const Ct* ct;
+  int r;
+};
+std::vector<Ct> rot_sum_batch(Context& c, const std::vector<std::vector<SumTerm>>& groups, bool hoisted,
+                              bool count = true);
+// fold_within_head of every x (radix rotation sums), reference ledger charge
+std::vector<Ct> fold_batch(Context& c, const std::vector<const Ct*>& xs, int d_head, int t, bool count = true);
 // sum of k same-level ciphertexts, charged k-1 additions
 Ct sum_cts(Context& c, const std::vector<const Ct*>& xs, bool count = true);
 

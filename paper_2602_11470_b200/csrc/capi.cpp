@@ -579,6 +579,17 @@ sf_status sf_profile_end(sf_context* ctx, double* ms, double* bytes, long long* 
   });
 }
 
+sf_status sf_host_profile(char* buf, int len, int reset) {
+  return guard([&] {
+    const std::string s = sf::host_prof_dump(reset != 0);
+    if (buf && len > 0) {
+      const size_t k = std::min<size_t>(s.size(), (size_t)len - 1);
+      std::memcpy(buf, s.data(), k);
+      buf[k] = 0;
+    }
+  });
+}
+
 sf_status sf_profile_butterflies(sf_context* ctx, double* out) {
   return guard([&] {
     for (int f = 0; f < SF_PROF_FAMILIES; ++f) out[f] = ctx->c->prof_bfly[f];

@@ -2,6 +2,7 @@
 // Product code: nothing here (or anywhere under csrc/) touches oracle/.
 #pragma once
 
+#include <chrono>
 #include <cstdint>
 #include <memory>
 #include <optional>
@@ -10,6 +11,25 @@
 #include <vector>
 
 namespace sf {
+
+// Host-side cost accounting (SF_HOST_PROF=1; sf_host_profile): wall time per
+// named scope, for finding what the host spends issuing a decode step.
+bool host_prof_on();
+void host_prof_add(const char* name, double us);
+struct HostProfScope {
+  const char* name;
+  std::chrono::steady_clock::time_point t0;
+  bool on;
+  explicit HostProfScope(const char* n) : name(n), on(host_prof_on()) {
+    if (on) t0 = std::chrono::steady_clock::now();
+  }
+  ~HostProfScope() {
+    if (on) host_prof_add(name, std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
+  }
+};
+#define SF_HPROF_CAT2(a, b) a##b
+#define SF_HPROF_CAT(a, b) SF_HPROF_CAT2(a, b)
+#define SF_HPROF(name) ::sf::HostProfScope SF_HPROF_CAT(_hprof_, __LINE__)(name)
 
 using u64 = uint64_t;
 using i64 = int64_t;

@@ -201,6 +201,8 @@ struct ProfScope {
   ~ProfScope();
 };
 
+std::string host_prof_dump(bool reset);
+
 // --- construction ------------------------------------------------------------
 std::unique_ptr<Context> make_context(int slots, int L, int log_n, int alpha, int q0_bits, int scale_bits,
                                       int special_bits, u64 seed, int device);

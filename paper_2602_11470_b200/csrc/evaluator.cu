@@ -24,9 +24,11 @@ void build_host_tables(Context& c, std::vector<u64>& psi, std::vector<u64>& psi_
 
 // ------------------------------------------------------------------ memory
 Buf::Buf(Context* c, size_t w) : words(w), ctx(c) {
+  SF_HPROF("cudaMallocAsync");
   if (w) SF_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), w * sizeof(u64), c->stream));
 }
 Buf::~Buf() {
+  SF_HPROF("cudaFreeAsync");
   if (p) cudaFreeAsync(p, ctx->stream);
 }
 
@@ -118,10 +120,12 @@ std::unique_ptr<Context> make_context(int slots, int L, int log_n, int alpha, in
 
 // ------------------------------------------------------------------ helpers
 u64 galois_elt(const Context& c, int r) {
+  SF_HPROF("galois_elt");
   return powmod_h(5, (u64)pos_mod(r, c.slots), 2ull * c.n);
 }
 
 Ct alloc_ct(Context& c, int limbs, double scale) {
+  SF_HPROF("alloc_ct");
   Ct r;
   r.buf = buf(c, (size_t)2 * limbs * c.n);
   r.limbs = limbs;
@@ -131,18 +135,21 @@ Ct alloc_ct(Context& c, int limbs, double scale) {
 }
 
 static Ct view(const Ct& a, int limbs) {
+  SF_HPROF("view");
   Ct r = a;
   r.limbs = limbs;
   return r;
 }
 
 void check_ct(const Context& c, const Ct& a, const char* what) {
+  SF_HPROF("check_ct");
   require(a.buf != nullptr, kInvalidTarget, std::string(what) + ": null ciphertext");
   require(a.level() >= 0 && a.level() <= c.L, kInvalidTarget,
           std::string(what) + ": ciphertext level " + std::to_string(a.level()) + " out of [0, L]");
 }
 
 void check_scales(const Ct& a, const Ct& b, const char* what) {
+  SF_HPROF("check_scales");
   if (a.zero || b.zero) return;
   if (std::fabs(a.scale / b.scale - 1.0) > 1e-9)
     fail(kScaleMismatch, std::string("ScaleMismatch: ") + what + ": operand scales differ");
@@ -156,6 +163,7 @@ OptLayout merge_layouts(const Ct& a, const Ct& b) {
 // device constants for `limbs` active limbs: rescale (drop limb limbs-1) and
 // ModDown (P -> Q_limbs): [inv_ql, inv_ql_s, pinv, pinv_s] each `limbs` words
 const u64* level_consts(Context& c, int limbs) {
+  SF_HPROF("level_consts");
   std::lock_guard<std::mutex> lk(c.mu);
   auto it = c.level_consts.find(limbs);
   if (it != c.level_consts.end()) return it->second->p;
@@ -181,6 +189,7 @@ const u64* level_consts(Context& c, int limbs) {
 }
 
 const ConvPlan& conv_plan(Context& c, const std::vector<int>& src, const std::vector<int>& dst) {
+  SF_HPROF("conv_plan");
   std::string key;
   for (int s : src) key += std::to_string(s) + ",";
   key += ">";
@@ -224,6 +233,7 @@ const ConvPlan& conv_plan(Context& c, const std::vector<int>& src, const std::ve
 
 // upload signed coefficients and reduce into `limbs` NTT-domain limbs (+ noise)
 static BufPtr coeffs_to_ntt(Context& c, const std::vector<i64>& co, int limbs, bool noise, u64 ekey) {
+  SF_HPROF("coeffs_to_ntt");
   BufPtr tmp = buf(c, (size_t)c.n);
   SF_CUDA(cudaMemcpyAsync(tmp->p, co.data(), co.size() * sizeof(i64), cudaMemcpyHostToDevice, c.stream));
   BufPtr out = buf(c, (size_t)limbs * c.n);
@@ -237,6 +247,7 @@ static BufPtr coeffs_to_ntt(Context& c, const std::vector<i64>& co, int limbs, b
 }
 
 Pt encode_pt(Context& c, const double* slots, double scale, int limbs) {
+  SF_HPROF("encode_pt");
   Pt p;
   p.buf = coeffs_to_ntt(c, encode_coeffs(c, slots, scale), limbs, false, 0);
   p.limbs = limbs;
@@ -245,6 +256,7 @@ Pt encode_pt(Context& c, const double* slots, double scale, int limbs) {
 }
 
 Pt cached_pt(Context& c, const std::string& key, const double* slots, double scale, int limbs) {
+  SF_HPROF("cached_pt");
   const std::string k = key + "@" + std::to_string(limbs);
   {
     std::lock_guard<std::mutex> lk(c.mu);
@@ -259,6 +271,7 @@ Pt cached_pt(Context& c, const std::string& key, const double* slots, double sca
 
 // ------------------------------------------------------------------ client ops
 Ct encrypt(Context& c, const double* slots, int level, u64 seed, OptLayout layout) {
+  SF_HPROF("encrypt");
   if (level < 0) level = c.L;
   require(level <= c.L, kInvalidTarget, "encrypt: level exceeds budget L");
   if (layout) validate_layout(*layout, c.slots);
@@ -275,6 +288,7 @@ Ct encrypt(Context& c, const double* slots, int level, u64 seed, OptLayout layou
 }
 
 Ct zeros(Context& c, int level) {
+  SF_HPROF("zeros");
   if (level < 0) level = c.L;
   require(level <= c.L, kInvalidTarget, "zeros: level exceeds budget L");
   Ct r = alloc_ct(c, level + 1, 0.0);
@@ -284,6 +298,7 @@ Ct zeros(Context& c, int level) {
 }
 
 void decrypt(Context& c, const Ct& a, double* out) {
+  SF_HPROF("decrypt");
   if (a.zero) {
     std::fill(out, out + c.slots, 0.0);
     return;
@@ -302,6 +317,7 @@ void decrypt(Context& c, const Ct& a, double* out) {
 
 // ------------------------------------------------------------------ evaluator
 Ct add(Context& c, const Ct& a, const Ct& b, bool sub, bool count) {
+  SF_HPROF("add");
   check_ct(c, a, sub ? "sub" : "add");
   check_ct(c, b, sub ? "sub" : "add");
   const int limbs = std::min(a.limbs, b.limbs);
@@ -326,6 +342,7 @@ Ct add(Context& c, const Ct& a, const Ct& b, bool sub, bool count) {
 }
 
 Ct add_plain(Context& c, const Ct& a, const double* slots) {
+  SF_HPROF("add_plain");
   check_ct(c, a, "add_plain");
   require(!a.zero, kInvalidTarget, "add_plain on a trivial zero ciphertext");
   c.ledger.add();
@@ -338,6 +355,7 @@ Ct add_plain(Context& c, const Ct& a, const double* slots) {
 }
 
 Ct mac_plain(Context& c, const std::vector<const Ct*>& cts, const std::vector<const Pt*>& pts, bool count) {
+  SF_HPROF("mac_plain");
   require(!cts.empty() && cts.size() == pts.size(), kShapeMismatch, "mac_plain: term count");
   int limbs = 1 << 30;
   for (const Ct* x : cts) {
@@ -393,6 +411,7 @@ Ct mac_plain(Context& c, const std::vector<const Ct*>& cts, const std::vector<co
 }
 
 Ct mul_plain(Context& c, const Ct& a, const double* slots) {
+  SF_HPROF("mul_plain");
   check_ct(c, a, "mul_plain");
   require(a.level() > 0, kLevelUnderflow, "mul_plain: no multiplicative level left");
   Pt p = encode_pt(c, slots, (double)c.primes[a.limbs - 1], a.limbs);
@@ -401,6 +420,7 @@ Ct mul_plain(Context& c, const Ct& a, const double* slots) {
 
 // ---------------------------------------------------------------- key switching
 const BufPtr& get_key(Context& c, u64 g) {
+  SF_HPROF("get_key");
   {
     std::lock_guard<std::mutex> lk(c.mu);
     auto it = c.keys.find(g);
@@ -442,6 +462,7 @@ const BufPtr& get_key(Context& c, u64 g) {
 }
 
 Ct level_drop(Context& c, const Ct& a, int target) {
+  SF_HPROF("level_drop");
   check_ct(c, a, "level_drop");
   require(target >= 0 && target <= a.level(), kInvalidTarget,
           "level_drop: target level " + std::to_string(target) + " outside [0, level]");
@@ -449,6 +470,7 @@ Ct level_drop(Context& c, const Ct& a, int target) {
 }
 
 Ct bootstrap(Context& c, const Ct& a, int target) {
+  SF_HPROF("bootstrap");
   check_ct(c, a, "bootstrap");
   require(target >= 1 && target <= c.L, kInvalidTarget,
           "bootstrap: target level " + std::to_string(target) + " outside [1, L]");

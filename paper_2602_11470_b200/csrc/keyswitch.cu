@@ -34,6 +34,7 @@ struct ExtB {
 };
 
 void fill_conv(ConvBatch& B, Context& c, const ConvPlan& p) {
+  SF_HPROF("fill_conv");
   B.nsrc = p.nsrc;
   B.ndst = p.ndst;
   B.n = c.n;
@@ -45,16 +46,22 @@ void fill_conv(ConvBatch& B, Context& c, const ConvPlan& p) {
 }
 
 void ntt_batch(Context& c, LimbBatch& b, bool inverse) {
+  SF_HPROF("ntt_batch");
   if (b.count) launch_ntt(c, b, inverse);
   b.count = 0;
 }
 void ntt_push(Context& c, LimbBatch& b, u64* p, int prime, bool inverse) {
+  SF_HPROF("ntt_push");
   b.add(p, prime);
   if (b.count == kMaxBatch) ntt_batch(c, b, inverse);
 }
 
 // ModUp of S distinct NTT-domain polynomials d[s] (limbs limbs each).
-ExtB mod_up_batch(Context& c, const std::vector<const u64*>& d, int limbs) {
+// full_ext: the ext limbs are fully NTT'd (forward row pass run here) and the
+// digit's own limbs are not copied (the consumer reads the source) -- the
+// layout ks_sum_kernel expects; otherwise ks_row_kernel's column-only layout.
+ExtB mod_up_batch(Context& c, const std::vector<const u64*>& d, int limbs, bool full_ext = false) {
+  SF_HPROF("mod_up_batch");
   ExtB x;
   const size_t n = c.n;
   x.S = (int)d.size();
@@ -66,7 +73,7 @@ ExtB mod_up_batch(Context& c, const std::vector<const u64*>& d, int limbs) {
   x.src = d;
   BufPtr dcoef = make_buf(c, (size_t)x.S * limbs * n);
   if (fused_path(c)) {
-    x.col_only = c.ks_row;
+    x.col_only = c.ks_row && !full_ext;
     // inverse row pass (out of place) -> per digit: fused [inverse column pass,
     // conversion, forward column pass] straight into ext -> forward row pass
     LimbBatch lb;
@@ -97,14 +104,14 @@ ExtB mod_up_batch(Context& c, const std::vector<const u64*>& d, int limbs) {
         A.src[A.count] = dcoef->p + ((size_t)s * limbs + lo) * n;
         A.dst[A.count++] = ext_of(s);
         if (A.count == kJobsWide) b_fused_col(c, A), A.count = 0;
-        if (x.col_only) continue;
+        if (x.col_only || full_ext) continue;
         cb.src[cb.count] = d[s] + (size_t)lo * n;  // own primes: the exact NTT-domain residues
         cb.dst[cb.count++] = ext_of(s) + (size_t)lo * n;
         if (cb.count == kJobsWide) b_copy(c, cb, (size_t)(hi - lo) * n), cb.count = 0;
       }
       if (A.count) b_fused_col(c, A);
       if (x.col_only) continue;
-      b_copy(c, cb, (size_t)(hi - lo) * n);
+      if (!full_ext) b_copy(c, cb, (size_t)(hi - lo) * n);
       for (int s = 0; s < x.S; ++s)
         for (size_t k = 0; k < slot.size(); ++k) {
           lb.add(ext_of(s) + (size_t)slot[k] * n, dst[k]);
@@ -171,6 +178,7 @@ struct KsJob {
 
 // Inner products + ModDown for every job (chunks of kJobs).
 void ks_jobs(Context& c, const ExtB& x, const std::vector<KsJob>& jobs) {
+  SF_HPROF("ks_jobs");
   const size_t n = c.n;
   const int limbs = x.limbs, nt = x.nt;
   const u64* kc = level_consts(c, limbs);
@@ -339,8 +347,252 @@ void ks_jobs(Context& c, const ExtB& x, const std::vector<KsJob>& jobs) {
 
 }  // namespace
 
+// ---------------------------------------------------------- ModDown of polys
+// out = (acc_Q - conv_{P->Q}(acc_P)) * P^-1 (+ addend permuted by g) for
+// extended-basis polynomials acc = [nt][n]. p_rowpassed: the P limbs already
+// had ModDown's inverse row pass (fused path); otherwise they are NTT domain.
+struct MdPoly {
+  const u64* acc;
+  const u64* addend;
+  u64 g;
+  u64* out;
+};
+
+void mod_down_polys(Context& c, int limbs, const std::vector<MdPoly>& P, bool p_rowpassed) {
+  SF_HPROF("mod_down_polys");
+  const size_t n = c.n;
+  std::vector<int> pidx, qidx;
+  for (int k = 0; k < c.alpha; ++k) pidx.push_back(c.P_index(k));
+  for (int l = 0; l < limbs; ++l) qidx.push_back(l);
+  const ConvPlan& down = conv_plan(c, pidx, qidx);
+  const u64* kc = level_consts(c, limbs);
+  for (size_t s0 = 0; s0 < P.size(); s0 += kJobsWide) {
+    const int J = (int)std::min<size_t>(kJobsWide, P.size() - s0);
+    BufPtr conv = make_buf(c, (size_t)J * limbs * n);
+    if (fused_path(c)) {
+      LimbBatch lb;
+      if (!p_rowpassed) {
+        for (int j = 0; j < J; ++j)
+          for (int k = 0; k < c.alpha; ++k) {
+            lb.add(const_cast<u64*>(P[s0 + j].acc) + (size_t)(limbs + k) * n, pidx[k]);
+            if (lb.count == kMaxBatch) b_row(c, lb, true), lb.count = 0;
+          }
+        b_row(c, lb, true);
+      }
+      const std::vector<u64>& kh = c.level_consts_h[limbs];
+      FusedColArgs A;
+      A.ns = c.alpha;
+      A.nd = limbs;
+      A.set_plan(down.tab->p, down.nsrc, down.ndst);
+      for (int k = 0; k < c.alpha; ++k) A.src_prime[k] = pidx[k];
+      for (int l = 0; l < limbs; ++l) A.dst_prime[l] = l, A.out_slot[l] = l;
+      for (int j = 0; j < J; ++j) {
+        A.src[A.count] = P[s0 + j].acc + (size_t)limbs * n;
+        A.dst[A.count++] = conv->p + (size_t)j * limbs * n;
+      }
+      b_fused_col(c, A);
+      EpiBatch E;
+      for (int j = 0; j < J; ++j) {
+        const MdPoly& m = P[s0 + j];
+        for (int l = 0; l < limbs; ++l) {
+          E.buf[E.count] = conv->p + ((size_t)j * limbs + l) * n;
+          E.acc[E.count] = m.acc + (size_t)l * n;
+          E.addend[E.count] = m.addend ? m.addend + (size_t)l * n : nullptr;
+          E.out[E.count] = m.out + (size_t)l * n;
+          E.g[E.count] = m.g;
+          E.inv[E.count] = kh[2 * limbs + l];
+          E.inv_s[E.count] = kh[3 * limbs + l];
+          E.prime[E.count++] = (uint8_t)l;
+          if (E.count == kJobsWide) b_row_epi(c, E), E.count = 0;
+        }
+      }
+      b_row_epi(c, E);
+      continue;
+    }
+    require(!p_rowpassed, kInternal, "mod_down_polys: row-passed input on the generic path");
+    LimbBatch lb;
+    for (int j = 0; j < J; ++j)
+      for (int k = 0; k < c.alpha; ++k)
+        ntt_push(c, lb, const_cast<u64*>(P[s0 + j].acc) + (size_t)(limbs + k) * n, pidx[k], true);
+    ntt_batch(c, lb, true);
+    ConvBatch cv;
+    fill_conv(cv, c, down);
+    for (int l = 0; l < limbs; ++l) cv.out_slot[l] = l;
+    for (int j = 0; j < J; ++j) {
+      cv.in[cv.count] = P[s0 + j].acc + (size_t)limbs * n;
+      cv.out[cv.count++] = conv->p + (size_t)j * limbs * n;
+    }
+    b_conv(c, cv);
+    for (int j = 0; j < J; ++j)
+      for (int l = 0; l < limbs; ++l) ntt_push(c, lb, conv->p + ((size_t)j * limbs + l) * n, l, false);
+    ntt_batch(c, lb, false);
+    SubScaleBatch sb;
+    for (int j = 0; j < J; ++j) {
+      sb.acc[sb.count] = P[s0 + j].acc;
+      sb.conv[sb.count] = conv->p + (size_t)j * limbs * n;
+      sb.addend[sb.count] = P[s0 + j].addend;
+      sb.g[sb.count] = P[s0 + j].g;
+      sb.out[sb.count++] = P[s0 + j].out;
+    }
+    b_subscale(c, sb, limbs, kc + 2 * limbs, kc + 3 * limbs);
+  }
+}
+
+// ------------------------------------------------------------ rotation sums
+// sum_i Rot(a_i, r_i) accumulated in the extended basis and
+// brought back with one ModDown per part; the same function as the CPU
+// oracle's rot_sum, charged as the reference's rotate/add chain.
+std::vector<Ct> rot_sum_batch(Context& c, const std::vector<std::vector<SumTerm>>& groups, bool hoisted, bool count) {
+  SF_HPROF("rot_sum_batch");
+  std::vector<Ct> out(groups.size());
+  std::map<int, std::vector<int>> by_limbs;
+  for (size_t gi = 0; gi < groups.size(); ++gi) {
+    const auto& G = groups[gi];
+    require(!G.empty(), kShapeMismatch, "rot_sum: empty term list");
+    int limbs = 1 << 30;
+    const Ct* first = nullptr;
+    OptLayout ly;
+    for (size_t i = 0; i < G.size(); ++i) {
+      const Ct& a = *G[i].ct;
+      check_ct(c, a, "rotate");
+      const bool rot = pos_mod(G[i].r, c.slots) != 0;
+      if (count && rot) c.ledger.rot(hoisted);
+      limbs = std::min(limbs, a.limbs);
+      OptLayout t_ly = rot ? OptLayout() : a.layout;
+      if (i == 0)
+        ly = t_ly;
+      else if (!(ly && t_ly && *ly == *t_ly))
+        ly.reset();
+      if (a.zero) continue;
+      if (!first)
+        first = &a;
+      else
+        check_scales(*first, a, "add");
+    }
+    if (count) c.ledger.add((long long)G.size() - 1);
+    if (!first) {
+      Ct z = *G[0].ct;
+      z.limbs = limbs;
+      z.layout = ly;
+      out[gi] = z;
+      continue;
+    }
+    out[gi] = alloc_ct(c, limbs, first->scale);
+    out[gi].layout = ly;
+    by_limbs[limbs].push_back((int)gi);
+  }
+  const size_t n = c.n;
+  for (auto& [limbs, gidx] : by_limbs) {
+    std::vector<u64> pm(limbs);
+    for (int l = 0; l < limbs; ++l) {
+      u64 r = 1 % c.primes[l];
+      for (int k = 0; k < c.alpha; ++k) r = mulmod_h(r, c.primes[c.P_index(k)] % c.primes[l], c.primes[l]);
+      pm[l] = r;
+    }
+    size_t gpos = 0;
+    while (gpos < gidx.size()) {
+      // chunk: <= kSumOuts outputs, <= kSumJobs jobs, <= kSumSrcs sources
+      std::map<const Ct*, int> src;
+      std::vector<const Ct*> srcv;
+      std::vector<int> chunk;
+      int njobs = 0;
+      while (gpos < gidx.size()) {
+        const auto& G = groups[gidx[gpos]];
+        int newsrc = 0;
+        for (const auto& tm : G)
+          if (!tm.ct->zero && !src.count(tm.ct)) ++newsrc;
+        if (!chunk.empty() && ((int)chunk.size() == kSumOuts || njobs + (int)G.size() > kSumJobs ||
+                               (int)srcv.size() + newsrc > kSumSrcs))
+          break;
+        require((int)G.size() <= kSumJobs && newsrc <= kSumSrcs, kShapeMismatch, "rot_sum: too many terms");
+        for (const auto& tm : G)
+          if (!tm.ct->zero && !src.count(tm.ct)) src[tm.ct] = (int)srcv.size(), srcv.push_back(tm.ct);
+        njobs += (int)G.size();
+        chunk.push_back(gidx[gpos++]);
+      }
+      std::vector<const u64*> d;
+      for (const Ct* a : srcv) d.push_back(a->c1(c.n));
+      ExtB x = mod_up_batch(c, d, limbs, true);
+      const int nt = x.nt;
+      BufPtr acc = make_buf(c, chunk.size() * 2 * nt * n);
+      KsSumArgs A;
+      A.limbs = limbs;
+      A.nt = nt;
+      A.ndig = x.ndig;
+      A.alpha = c.alpha;
+      A.np = c.np;
+      for (int t = 0; t < nt; ++t) A.tprime[t] = x.tprime[t];
+      for (int l = 0; l < limbs; ++l) A.pm[l] = pm[l];
+      for (size_t s = 0; s < srcv.size(); ++s) {
+        A.c0[s] = srcv[s]->c0();
+        A.c1[s] = srcv[s]->c1(c.n);
+        A.ext[s] = x.ext((int)s);
+      }
+      int jb = 0;
+      std::vector<MdPoly> md;
+      for (size_t o = 0; o < chunk.size(); ++o) {
+        A.out_begin[o] = jb;
+        A.acc[o] = acc->p + o * 2 * nt * n;
+        for (const auto& tm : groups[chunk[o]]) {
+          if (tm.ct->zero) continue;
+          const int r = pos_mod(tm.r, c.slots);
+          A.jsrc[jb] = src[tm.ct];
+          A.g[jb] = r == 0 ? 1 : galois_elt(c, r);
+          A.key[jb] = r == 0 ? nullptr : get_key(c, A.g[jb])->p;
+          ++jb;
+        }
+        const Ct& y = out[chunk[o]];
+        md.push_back({A.acc[o], nullptr, 0, y.c0()});
+        md.push_back({A.acc[o] + (size_t)nt * n, nullptr, 0, y.c1(c.n)});
+      }
+      A.out_begin[chunk.size()] = jb;
+      A.nout = (int)chunk.size();
+      b_ks_sum(c, A);
+      mod_down_polys(c, limbs, md, fused_path(c));
+    }
+  }
+  return out;
+}
+
+// fold_within_head (kv_attention.cpp:38-41) of many ciphertexts: the radix
+// rotation sums of DESIGN.md §3.8, charged as the reference's log2(d_head)
+// rotate + add steps per ciphertext.
+std::vector<Ct> fold_batch(Context& c, const std::vector<const Ct*>& xs, int d_head, int t, bool count) {
+  SF_HPROF("fold_batch");
+  int D = 0;
+  while ((1 << D) < d_head) ++D;
+  if (count)
+    for (size_t i = 0; i < xs.size(); ++i) {
+      check_ct(c, *xs[i], "rotate");
+      for (int l = 0; l < D; ++l)
+        if (pos_mod((1 << l) * t, c.slots) != 0) c.ledger.rot(false);
+      c.ledger.add(D);
+    }
+  std::vector<int> steps;
+  if (D > 0) {
+    if (D <= 3)
+      steps.push_back(D);
+    else
+      steps.push_back((D + 1) / 2), steps.push_back(D / 2);
+  }
+  std::vector<Ct> cur;
+  for (const Ct* x : xs) cur.push_back(*x);
+  long long stride = t;
+  for (int bits : steps) {
+    std::vector<std::vector<SumTerm>> groups(cur.size());
+    for (size_t i = 0; i < cur.size(); ++i)
+      for (int k = 0; k < (1 << bits); ++k) groups[i].push_back({&cur[i], (int)(k * stride % c.slots)});
+    std::vector<Ct> nxt = rot_sum_batch(c, groups, false, false);
+    cur.swap(nxt);
+    stride <<= bits;
+  }
+  for (Ct& y : cur) y.layout.reset();
+  return cur;
+}
+
 // -------------------------------------------------------------------- rescale
 std::vector<Ct> rescale_batch(Context& c, const std::vector<const Ct*>& xs) {
+  SF_HPROF("rescale_batch");
   std::vector<Ct> out(xs.size());
   if (xs.empty()) return out;
   std::map<int, std::vector<int>> by_limbs;
@@ -455,6 +707,7 @@ Ct rescale(Context& c, const Ct& a) { return rescale_batch(c, {&a})[0]; }
 // ------------------------------------------------------------------ rotations
 std::vector<Ct> rotate_batch(Context& c, const std::vector<const Ct*>& srcs, const std::vector<RotJob>& jobs,
                              bool hoisted, bool count) {
+  SF_HPROF("rotate_batch");
   std::vector<Ct> out(jobs.size());
   // group sources by limb count; one ModUp per distinct source that needs one
   std::map<int, std::vector<int>> need;  // limbs -> source indices
@@ -500,10 +753,12 @@ std::vector<Ct> rotate_batch(Context& c, const std::vector<const Ct*>& srcs, con
 }
 
 Ct rotate(Context& c, const Ct& a, int r, bool hoisted, bool count) {
+  SF_HPROF("rotate");
   return rotate_batch(c, {&a}, {{0, r}}, hoisted, count)[0];
 }
 
 std::vector<Ct> rotate_hoisted(Context& c, const Ct& a, const std::vector<int>& rs, bool count) {
+  SF_HPROF("rotate_hoisted");
   std::vector<RotJob> jobs;
   for (int r : rs) jobs.push_back({0, r});
   return rotate_batch(c, {&a}, jobs, true, count);
@@ -511,6 +766,7 @@ std::vector<Ct> rotate_hoisted(Context& c, const Ct& a, const std::vector<int>& 
 
 // ------------------------------------------------------------- ct x ct mult
 std::vector<Ct> mul_batch(Context& c, const std::vector<const Ct*>& a, const std::vector<const Ct*>& b, bool count) {
+  SF_HPROF("mul_batch");
   require(a.size() == b.size(), kShapeMismatch, "mul_batch: operand count");
   std::vector<Ct> out(a.size());
   std::map<int, std::vector<int>> by_limbs;
@@ -567,6 +823,7 @@ Ct mul(Context& c, const Ct& a, const Ct& b, bool count) { return mul_batch(c, {
 
 // ------------------------------------------------- lazily relinearised sums
 Ct3 tensor_sum(Context& c, const std::vector<const Ct*>& a, const std::vector<const Ct*>& b, bool count) {
+  SF_HPROF("tensor_sum");
   require(a.size() == b.size() && !a.empty(), kShapeMismatch, "tensor_sum: operand count");
   int limbs = 1 << 30;
   double scale = 0.0;
@@ -617,6 +874,7 @@ Ct3 tensor_sum(Context& c, const std::vector<const Ct*>& a, const std::vector<co
 }
 
 Ct3 add_ct3(Context& c, const std::vector<const Ct3*>& xs) {
+  SF_HPROF("add_ct3");
   std::vector<const Ct*> a, b;
   for (const Ct3* x : xs)
     if (!x->zero) a.push_back(&x->d01), b.push_back(&x->d2);
@@ -629,6 +887,7 @@ Ct3 add_ct3(Context& c, const std::vector<const Ct3*>& xs) {
 }
 
 Ct relin_rescale(Context& c, const Ct3& x) {
+  SF_HPROF("relin_rescale");
   if (x.zero) return zeros(c, x.d01.level() - 1);
   const int limbs = std::min(x.d01.limbs, x.d2.limbs);
   ExtB e = mod_up_batch(c, {x.d2.c0()}, limbs);
@@ -678,6 +937,7 @@ std::vector<Ct> mul_plain_batch(Context& c, const std::vector<const Ct*>& xs, co
 
 // ------------------------------------------------------------------ additions
 std::vector<Ct> add_batch(Context& c, const std::vector<const Ct*>& a, const std::vector<const Ct*>& b, bool count) {
+  SF_HPROF("add_batch");
   require(a.size() == b.size(), kShapeMismatch, "add_batch: operand count");
   std::vector<Ct> out(a.size());
   std::map<int, AddBatch> by_limbs;
@@ -717,6 +977,7 @@ std::vector<Ct> add_batch(Context& c, const std::vector<const Ct*>& a, const std
 }
 
 Ct sum_cts(Context& c, const std::vector<const Ct*>& xs, bool count) {
+  SF_HPROF("sum_cts");
   require(!xs.empty(), kShapeMismatch, "sum: empty");
   if (count) c.ledger.add((long long)xs.size() - 1);
   int limbs = 1 << 30;

@@ -413,6 +413,129 @@ __global__ void __launch_bounds__(kWarps * 32) ks_row_kernel(KsRowArgs A, Tabs T
   }
 }
 
+// ------------------------------------------------------- rotation-sum row
+// One CTA = (output o, target slot t, kWarps destination rows); warp w owns
+// destination row rd and walks the jobs of o: each non-identity job reads its
+// source rows rs = perm_g(rd) (digit ext rows / own c1 row and the c0 row),
+// staged through the warp's shared row buffer for the in-row permutation.
+template <int LOGR, int LOGC>
+__global__ void __launch_bounds__(kWarps * 32) ks_sum_kernel(KsSumArgs A, Tabs T) {
+  constexpr int C = 1 << LOGC, E = C / 32, LOGN = LOGR + LOGC;
+  constexpr int tiles = (1 << LOGR) / kWarps;
+  constexpr int n = 1 << LOGN;
+  __shared__ u64 rowbuf[kWarps][C];
+  const int tile = blockIdx.x % tiles, rest = blockIdx.x / tiles;
+  const int t = rest % A.nt, o = rest / A.nt;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rd = tile * kWarps + warp;
+  const int m = A.tprime[t];
+  const u64 q = T.q[m], mh = T.mh[m], ml = T.ml[m];
+  const bool qt = t < A.limbs;
+  const u64 pm = qt ? A.pm[t] : 0;
+  u64* buf = rowbuf[warp];
+  const size_t rowoff = (size_t)rd * C + lane * E;
+  U128 sb[E], sa[E];
+#pragma unroll
+  for (int k = 0; k < E; ++k) sb[k] = U128{0, 0}, sa[k] = U128{0, 0};
+  int terms = 0;  // products accumulated since the last partial reduction (< 2^120 each)
+  auto fold = [&]() {
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      sb[k] = U128{reduce128(sb[k].hi, sb[k].lo, q, mh, ml), 0};
+      sa[k] = U128{reduce128(sa[k].hi, sa[k].lo, q, mh, ml), 0};
+    }
+    terms = 0;
+  };
+  for (int jb = A.out_begin[o]; jb < A.out_begin[o + 1]; ++jb) {
+    const int s = A.jsrc[jb];
+    const u64 g = A.g[jb];
+    if (terms > 200) fold();
+    if (g <= 1) {  // identity term: P * (c0, c1) on the Q primes
+      if (!qt) continue;
+      const u64* a0 = A.c0[s] + (size_t)t * n + rowoff;
+      const u64* a1 = A.c1[s] + (size_t)t * n + rowoff;
+#pragma unroll
+      for (int k = 0; k < E; k += 2) {
+        const ulonglong2 v0 = reinterpret_cast<const ulonglong2*>(a0)[k / 2];
+        const ulonglong2 v1 = reinterpret_cast<const ulonglong2*>(a1)[k / 2];
+        mac128(sb[k], v0.x, pm);
+        mac128(sb[k + 1], v0.y, pm);
+        mac128(sa[k], v1.x, pm);
+        mac128(sa[k + 1], v1.y, pm);
+      }
+      ++terms;
+      continue;
+    }
+    const int rs = (int)(auto_perm((uint32_t)rd << LOGC, g, LOGN) >> LOGC);
+    uint32_t sc[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k) sc[k] = auto_perm((uint32_t)(rd * C + lane * E + k), g, LOGN) & (C - 1);
+    for (int j = 0; j < A.ndig; ++j) {
+      const int lo = j * A.alpha, hi = min(lo + A.alpha, A.limbs);
+      const u64* src = (t >= lo && t < hi) ? A.c1[s] + (size_t)t * n + (size_t)rs * C
+                                           : A.ext[s] + ((size_t)j * A.nt + t) * n + (size_t)rs * C;
+#pragma unroll
+      for (int k = 0; k < E; k += 2)
+        reinterpret_cast<ulonglong2*>(buf + lane * E)[k / 2] = reinterpret_cast<const ulonglong2*>(src + lane * E)[k / 2];
+      __syncwarp();
+      const u64* kb = A.key[jb] + ((size_t)(j * 2 + 0) * A.np + m) * n + rowoff;
+      const u64* ka = A.key[jb] + ((size_t)(j * 2 + 1) * A.np + m) * n + rowoff;
+#pragma unroll
+      for (int k = 0; k < E; k += 2) {
+        const ulonglong2 vb = reinterpret_cast<const ulonglong2*>(kb)[k / 2];
+        const ulonglong2 va = reinterpret_cast<const ulonglong2*>(ka)[k / 2];
+        const u64 x0 = buf[sc[k]], x1 = buf[sc[k + 1]];
+        mac128(sb[k], x0, vb.x);
+        mac128(sa[k], x0, va.x);
+        mac128(sb[k + 1], x1, vb.y);
+        mac128(sa[k + 1], x1, va.y);
+      }
+      __syncwarp();
+    }
+    if (qt) {  // P * sigma_g(c0)
+      const u64* src = A.c0[s] + (size_t)t * n + (size_t)rs * C;
+#pragma unroll
+      for (int k = 0; k < E; k += 2)
+        reinterpret_cast<ulonglong2*>(buf + lane * E)[k / 2] = reinterpret_cast<const ulonglong2*>(src + lane * E)[k / 2];
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < E; ++k) mac128(sb[k], buf[sc[k]], pm);
+      __syncwarp();
+    }
+    terms += A.ndig + 1;
+  }
+  u64 vb[E], va[E];
+#pragma unroll
+  for (int k = 0; k < E; ++k) {
+    vb[k] = reduce128(sb[k].hi, sb[k].lo, q, mh, ml);
+    va[k] = reduce128(sa[k].hi, sa[k].lo, q, mh, ml);
+  }
+  u64* accb = A.acc[o] + (size_t)t * n;
+  u64* acca = A.acc[o] + (size_t)(A.nt + t) * n;
+  if (qt) {
+#pragma unroll
+    for (int k = 0; k < E; k += 2) {
+      reinterpret_cast<ulonglong2*>(accb + rowoff)[k / 2] = make_ulonglong2(vb[k], vb[k + 1]);
+      reinterpret_cast<ulonglong2*>(acca + rowoff)[k / 2] = make_ulonglong2(va[k], va[k + 1]);
+    }
+  } else {  // special prime: ModDown's inverse row pass, strided stores
+    const u64* W = T.ipsi + ((size_t)m << LOGN);
+    const u64* Ws = T.ipsi_s + ((size_t)m << LOGN);
+    auto tw = [&](int b, int blk, u64& w, u64& ws) {
+      const int i = (1 << (LOGN - 1 - b)) + (rd << (LOGC - 1 - b)) + blk;
+      w = W[i];
+      ws = Ws[i];
+    };
+    warp_inv<LOGC, kBlocked>(vb, buf, lane, q, tw);
+    warp_inv<LOGC, kBlocked>(va, buf, lane, q, tw);
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      accb[(size_t)rd * C + lane + 32 * k] = vb[k];
+      acca[(size_t)rd * C + lane + 32 * k] = va[k];
+    }
+  }
+}
+
 template <int LOGR, int LOGC>
 void run_two_pass(Context& c, const LimbBatch& b, bool inverse) {
   const unsigned rows_grid = (unsigned)b.count * ((1u << LOGR) / kWarps);
@@ -479,6 +602,12 @@ void run_ks_row(Context& c, const KsRowArgs& a) {
   ks_row_kernel<LOGR, LOGC><<<grid, kWarps * 32, sm, c.stream>>>(a, c.tabs);
 }
 
+template <int LOGR, int LOGC>
+void run_ks_sum(Context& c, const KsSumArgs& a) {
+  const unsigned grid = (unsigned)(a.nout * a.nt * ((1 << LOGR) / kWarps));
+  ks_sum_kernel<LOGR, LOGC><<<grid, kWarps * 32, 0, c.stream>>>(a, c.tabs);
+}
+
 #define SF_NTT_DISPATCH(FN, ...)                        \
   switch (c.logn) {                                     \
     case 12: FN<6, 6>(c, __VA_ARGS__); return true;     \
@@ -497,5 +626,6 @@ bool ntt_row_only(Context& c, const LimbBatch& b, bool inverse) { SF_NTT_DISPATC
 bool ntt_row_epi(Context& c, const EpiBatch& e) { SF_NTT_DISPATCH(run_epi, e) }
 bool ntt_fused_col(Context& c, const FusedColArgs& a) { SF_NTT_DISPATCH(run_fused, a) }
 bool ntt_ks_row(Context& c, const KsRowArgs& a) { SF_NTT_DISPATCH(run_ks_row, a) }
+bool ntt_ks_sum(Context& c, const KsSumArgs& a) { SF_NTT_DISPATCH(run_ks_sum, a) }
 
 }  // namespace sf

@@ -4,9 +4,43 @@
 #include <cmath>
 #include <cstring>
 
+#include <cstdio>
+#include <cstdlib>
+#include <map>
+#include <mutex>
+
 #include "context.h"
 
 namespace sf {
+
+namespace {
+std::mutex g_hp_mu;
+std::map<std::string, std::pair<double, long long>> g_hp;
+}  // namespace
+bool host_prof_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("SF_HOST_PROF");
+    return e && std::atoi(e) != 0;
+  }();
+  return on;
+}
+void host_prof_add(const char* name, double us) {
+  std::lock_guard<std::mutex> lk(g_hp_mu);
+  auto& v = g_hp[name];
+  v.first += us;
+  v.second += 1;
+}
+std::string host_prof_dump(bool reset) {
+  std::lock_guard<std::mutex> lk(g_hp_mu);
+  std::string out;
+  char line[160];
+  for (auto& [k, v] : g_hp) {
+    std::snprintf(line, sizeof line, "%s %.1f %lld\n", k.c_str(), v.first, v.second);
+    out += line;
+  }
+  if (reset) g_hp.clear();
+  return out;
+}
 
 namespace {
 

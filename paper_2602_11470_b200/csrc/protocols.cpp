@@ -17,6 +17,7 @@ namespace sf {
 // kept resident: numerically identical to mul_plain (same encode, same scale
 // q_top), without re-running the host FFT every decode step.
 static Ct mul_plain_cached(Context& c, const Ct& a, const std::string& key, const std::vector<double>& slots) {
+  SF_HPROF("mul_plain_cached");
   check_ct(c, a, "mul_plain");
   require(a.level() > 0, kLevelUnderflow, "mul_plain: no multiplicative level left");
   Pt p = cached_pt(c, key, slots.data(), (double)c.primes[a.limbs - 1], a.limbs);
@@ -124,6 +125,7 @@ std::unique_ptr<VmmPlan> make_vmm_plan(Context& c, const double* W, int rows, in
 }
 
 static void vmm_check_input(Context& c, const Ct& x, const VmmPlan& plan) {
+  SF_HPROF("vmm_check_input");
   require(x.layout && x.layout->kind == LayoutKind::Interleaved, kLayoutMismatch,
           "vmm_interleaved: input must carry an interleaved layout");
   require(!x.layout->deferred_mask, kLayoutMismatch,
@@ -136,12 +138,15 @@ static void vmm_check_input(Context& c, const Ct& x, const VmmPlan& plan) {
   require(x.level() > 0, kLevelUnderflow, "mul_plain: no multiplicative level left");
 }
 
+constexpr int kGiantGroups = 8;  // giant-step groups of the BSGS rotation sums
+
 // Steps 1-2 of vmm.cpp:179-236 for the giant steps this rank owns
 // (g2 = rank mod world; world = 1 is the whole VMM): preprocess ladder,
 // hoisted babies, the giants' lazy MACs (one rescale each), giant rotations and
 // their sum. Work every rank repeats (ladder, babies) is charged on rank 0 only,
 // so the ledgers of all ranks sum to the reference's counts.
 Ct vmm_partial(Context& c, const Ct& x, VmmPlan& plan, int rank, int world) {
+  SF_HPROF("vmm_partial");
   vmm_check_input(c, x, plan);
   require(world >= 1 && rank >= 0 && rank < world, kInvalidTarget, "vmm: bad rank/world");
   const bool lead = rank == 0;
@@ -163,8 +168,9 @@ Ct vmm_partial(Context& c, const Ct& x, VmmPlan& plan, int rank, int world) {
     return mac_plain(c, cts, pts);
   }
   const int b = plan.bg.baby, giants = plan.bg.giant;
-  std::vector<int> mine;
-  for (int g2 = rank; g2 < giants; g2 += world) mine.push_back(g2);
+  std::vector<int> mine;  // whole giant groups r = g2 mod kGiantGroups with r mod world == rank
+  for (int g2 = 0; g2 < giants; ++g2)
+    if ((g2 % kGiantGroups) % world == rank) mine.push_back(g2);
   if (mine.empty()) return zeros(c, x.level() - 1);
   std::vector<RotJob> jobs;
   for (int g1 = 1; g1 < b; ++g1) jobs.push_back({0, (int)(g1 * unit)});
@@ -205,18 +211,25 @@ Ct vmm_partial(Context& c, const Ct& x, VmmPlan& plan, int rank, int world) {
       resc.push_back(mac_plain(c, cts, pts));
     }
   }
-  std::vector<const Ct*> rp;
-  std::vector<RotJob> gj;
-  for (size_t i = 0; i < mine.size(); ++i) rp.push_back(&resc[i]), gj.push_back({(int)i, (int)((long long)mine[i] * b * unit)});
-  std::vector<Ct> aligned = rotate_batch(c, rp, gj, false);
+  // giant alignment + sum (vmm.cpp:221-222): one rotation sum per giant group
+  // (ModDown once per group instead of once per giant)
+  std::vector<std::vector<SumTerm>> groups;
+  std::map<int, int> gpos;
+  for (size_t i = 0; i < mine.size(); ++i) {
+    const int r = mine[i] % kGiantGroups;
+    if (!gpos.count(r)) gpos[r] = (int)groups.size(), groups.emplace_back();
+    groups[gpos[r]].push_back({&resc[i], (int)(((long long)mine[i] * b * unit) % c.slots)});
+  }
+  std::vector<Ct> gs = rot_sum_batch(c, groups, false);
   std::vector<const Ct*> ap;
-  for (auto& a : aligned) ap.push_back(&a);
+  for (auto& a : gs) ap.push_back(&a);
   return sum_cts(c, ap);
 }
 
 // Steps 3-4 of vmm.cpp:179-236 on the summed partials: the reduce ladder
 // folding each t_out window onto its output offset, then mask or defer.
 Ct vmm_finish(Context& c, const Ct& acc_in, VmmPlan& plan, bool mask_output) {
+  SF_HPROF("vmm_finish");
   const VmmShape& s = plan.s;
   Ct acc = acc_in;
   for (int m = 0; (1 << m) < s.t_out; ++m) {
@@ -234,12 +247,14 @@ Ct vmm_finish(Context& c, const Ct& acc_in, VmmPlan& plan, bool mask_output) {
 
 // vmm.cpp:179-236: the whole VMM on one GPU.
 Ct vmm_interleaved(Context& c, const Ct& x, VmmPlan& plan, bool mask_output) {
+  SF_HPROF("vmm_interleaved");
   return vmm_finish(c, vmm_partial(c, x, plan, 0, 1), plan, mask_output);
 }
 
 // Sum of per-rank partial results (the exchange's modular reduction; NCCL has
 // no mod-q sum). Charges one addition per non-trivial operand beyond the first.
 Ct sum_partials(Context& c, const std::vector<const Ct*>& parts) {
+  SF_HPROF("sum_partials");
   std::vector<const Ct*> live;
   for (const Ct* p : parts)
     if (!p->zero) live.push_back(p);
@@ -275,6 +290,7 @@ int v_variant_of(const AttnCfg& cfg, int e, int u_local) {
 }
 
 static void require_clean_interleaved(const Ct& x, const AttnCfg& cfg, int offset, const char* who) {
+  SF_HPROF("require_clean_interleaved");
   require(x.layout && x.layout->kind == LayoutKind::Interleaved, kLayoutMismatch,
           std::string(who) + ": input must carry an interleaved layout");
   require(x.layout->d == cfg.d, kShapeMismatch, std::string(who) + ": layout width mismatch");
@@ -303,6 +319,7 @@ static std::vector<double> valid_mask(const Layout& ly, int N) {  // vmm.cpp:45-
 // fused_extract, Rope successor (vmm.cpp:85-100) via rope_apply
 // (kv_attention.cpp:111-117): y = x.p0 + Rot(x.p1, -s) + Rot(x.p2, s), s = t.
 Ct rope_apply(Context& c, const Ct& x, const AttnCfg& cfg, long long position, double base) {
+  SF_HPROF("rope_apply");
   require(x.layout && x.layout->kind == LayoutKind::Interleaved && x.layout->d == cfg.d, kLayoutMismatch,
           "rope_apply: input must be interleaved at the configured width");
   const Layout ly = *x.layout;
@@ -421,6 +438,7 @@ static int ceil_div(int a, int b) { return (a + b - 1) / b; }
 // (trivial zeros for maps this rank has no keys for); the lane replication of
 // q (30-34), repeated on every rank, is charged on rank 0 only.
 std::vector<Ct> qk_dot_partial(Context& c, const Ct& q, const KV& cache, int rank, int world) {
+  SF_HPROF("qk_dot_partial");
   const AttnCfg& cfg = cache.cfg;
   require(cache.n_prime != 0, kCacheEmpty, "qk_dot: no cached keys");
   require_clean_interleaved(q, cfg, 0, "qk_dot");
@@ -446,16 +464,10 @@ std::vector<Ct> qk_dot_partial(Context& c, const Ct& q, const KV& cache, int ran
   }
   std::vector<const Ct*> qs(J, &q_rep), ks;
   for (int j : own) ks.push_back(&cache.k[j]);
-  std::vector<Ct> prod = mul_batch(c, qs, ks);
-  for (int l = 0; (1 << l) < dh; ++l) {
-    std::vector<const Ct*> src;
-    std::vector<RotJob> jobs;
-    for (int i = 0; i < J; ++i) src.push_back(&prod[i]), jobs.push_back({i, (1 << l) * t});
-    std::vector<Ct> rot = rotate_batch(c, src, jobs, false);
-    std::vector<const Ct*> rp;
-    for (auto& r : rot) rp.push_back(&r);
-    prod = add_batch(c, src, rp);
-  }
+  std::vector<Ct> prod0 = mul_batch(c, qs, ks);
+  std::vector<const Ct*> pp0;
+  for (auto& p : prod0) pp0.push_back(&p);
+  std::vector<Ct> prod = fold_batch(c, pp0, dh, t);  // fold_within_head (38-41), DESIGN.md §3.8
   const std::string hkey = "headmask:" + std::to_string(cfg.H) + ":" + std::to_string(t);
   std::vector<const Ct*> pp;
   std::vector<Pt> hm;
@@ -493,6 +505,7 @@ std::vector<Ct> qk_dot(Context& c, const Ct& q, const KV& cache) { return qk_dot
 // reference's 510 ct-ct mults + 509 additions (kv_attention.cpp:230-235) cost
 // one key switch and one rescale in softmax_times_v_finish instead of 510.
 Ct3 softmax_times_v_partial(Context& c, const std::vector<Ct>& probs, const KV& cache, int rank, int world) {
+  SF_HPROF("softmax_times_v_partial");
   const AttnCfg& cfg = cache.cfg;
   require(cache.n_prime != 0, kCacheEmpty, "softmax_times_v: no cached values");
   require(world >= 1 && rank >= 0 && rank < world, kInvalidTarget, "softmax_times_v: bad rank/world");
@@ -531,6 +544,7 @@ Ct3 softmax_times_v_partial(Context& c, const std::vector<Ct>& probs, const KV& 
 // Sum of the ranks' degree-2 partials, one relinearisation + rescale, then
 // fold_lanes (44-47) and the final stride mask (238).
 Ct softmax_times_v_finish(Context& c, const std::vector<const Ct3*>& parts, const KV& cache) {
+  SF_HPROF("softmax_times_v_finish");
   const AttnCfg& cfg = cache.cfg;
   const int t = cfg.t();
   long long live = 0;
@@ -546,6 +560,7 @@ Ct softmax_times_v_finish(Context& c, const std::vector<const Ct3*>& parts, cons
 }
 
 Ct softmax_times_v(Context& c, const std::vector<Ct>& probs, const KV& cache) {
+  SF_HPROF("softmax_times_v");
   Ct3 p = softmax_times_v_partial(c, probs, cache, 0, 1);
   return softmax_times_v_finish(c, {&p}, cache);
 }

@@ -21,9 +21,14 @@ from ._native import SfLayout
 
 
 # ------------------------------------------------------------------ ownership rules
+GIANT_GROUPS = 8  # giants g2 = r mod 8 share one rotation sum
+
+
 def own_giants(giants: int, rank: int, world: int) -> List[int]:
-    """VMM giant steps a rank computes (csrc/protocols.cpp:vmm_partial)."""
-    return list(range(rank, giants, world))
+    """VMM giant steps a rank computes (csrc/protocols.cpp:vmm_partial): whole
+    giant groups r = g2 mod GIANT_GROUPS with r mod world == rank (for world
+    dividing 8 this is g2 mod world == rank)."""
+    return [g for g in range(giants) if (g % GIANT_GROUPS) % world == rank]
 
 
 def own_keys(n_k: int, rank: int, world: int) -> List[int]:
