@@ -310,24 +310,40 @@ def main():
             torch.cuda.synchronize()
             dist.barrier()
 
-    # ---- value: device-resident inputs, CUDA events on the library stream
+    # ---- eager reference timing (host-issued step, for the record)
     be.ledger.reset()
     barrier()
     be.synchronize()
-    l0 = be.kernel_launches()
-    clk.mark()
     be.event_record(0)
     t_host = time.perf_counter()
     for _ in range(args.steps):
         outs = layer.step()
     t_host = (time.perf_counter() - t_host) * 1e3 / args.steps
     be.event_record(1)
+    ms_eager = be.event_elapsed_ms(0, 1) / args.steps
+    counts = be.ledger.totals()
+    be.synchronize()
+
+    # ---- capture the decode step once into a CUDA graph (nothing runs during
+    # the capture); every replay re-executes all of the step's kernels
+    graph, gouts = be.capture(layer.step)
+    graph.launch()
+    be.synchronize()
+
+    # ---- value: graph replays, device-resident inputs, CUDA events on the library stream
+    barrier()
+    be.synchronize()
+    l0 = be.kernel_launches()
+    clk.mark()
+    be.event_record(0)
+    for _ in range(args.steps):
+        graph.launch()
+    be.event_record(1)
     ms_total = be.event_elapsed_ms(0, 1)
     clk.__exit__()
     be.synchronize()
     barrier()
     launches = be.kernel_launches() - l0
-    counts = be.ledger.totals()
     if dist:
         import torch
         t = torch.tensor([ms_total], device="cuda")
@@ -402,18 +418,19 @@ def main():
     t_e = time.perf_counter()
     for _ in range(args.steps):
         t1 = time.perf_counter()
-        ins = [be.import_ct(w, lvl, sc, ly) for w, lvl, sc, ly, _ in pinned_in]
+        for slot, (w, *_r) in zip(layer.inputs, pinned_in):  # H2D into the step's input ciphertexts
+            be.refill(slot, w)
         t2 = time.perf_counter()
-        outs = layer.step(ins)
+        graph.launch()
         t3 = time.perf_counter()
-        res = [outs[4].data(), outs[8].data()]  # attention output and the layer's down-projection output
+        res = [gouts[4].data(), gouts[8].data()]  # attention output and the layer's down-projection output
         t4 = time.perf_counter()
         t_imp, t_iss, t_rd = t_imp + t2 - t1, t_iss + t3 - t2, t_rd + t4 - t3
         d2h = sum(r.nbytes for r in res)
     be.synchronize()
     barrier()
     e2e_ms = (time.perf_counter() - t_e) * 1e3 / args.steps
-    e2e_parts = {"import_ms": round(t_imp * 1e3 / args.steps, 3), "host_issue_ms": round(t_iss * 1e3 / args.steps, 3),
+    e2e_parts = {"h2d_enqueue_ms": round(t_imp * 1e3 / args.steps, 3), "graph_launch_ms": round(t_iss * 1e3 / args.steps, 3),
                  "readback_wait_ms": round(t_rd * 1e3 / args.steps, 3), "pinned": pinned}
     if dist:
         import torch
@@ -440,6 +457,8 @@ def main():
                 "d2h_bytes_per_step": int(d2h), "breakdown": e2e_parts},
         "gpu_launches": int(launches),
         "host_issue_ms_per_step": round(t_host, 3),
+        "eager_ms_per_step": round(ms_eager, 3),
+        "execution": f"CUDA graph of the whole decode step ({graph.kernel_launches} kernels), replayed per token",
         "clocks": clk.summary(),
         "ledger_per_step": {k: v // args.steps for k, v in counts.asdict().items()},
         "kernel_families": prof,

@@ -234,6 +234,22 @@ sf_status sf_profile_end(sf_context* ctx, double* ms, double* bytes, long long* 
 /* Radix-2 NTT butterflies each family executed in the last profile window
    (the INT-pipe work measure behind bench.py's int_roofline). */
 sf_status sf_profile_butterflies(sf_context* ctx, double* butterflies);
+/* ---- CUDA graphs of whole decode steps ----------------------------------------
+   Everything the library enqueues between begin and end (on this thread) is
+   captured into one graph instead of running; replaying it re-executes every
+   kernel of the step on the same device buffers. Handles created during the
+   capture stay valid and hold the latest replay's results; inputs are fed by
+   sf_ct_refill on handles created before the capture. */
+typedef struct sf_graph sf_graph;
+sf_status sf_graph_capture_begin(sf_context* ctx);
+sf_status sf_graph_capture_end(sf_context* ctx, sf_graph** out);
+sf_status sf_graph_launch(sf_context* ctx, sf_graph* g);
+long long sf_graph_kernel_launches(const sf_graph* g);
+void sf_graph_destroy(sf_graph* g);
+/* Overwrite a ciphertext's words from host memory (stream-ordered; pinned host
+   memory makes it asynchronous): the input slots of a captured graph. */
+sf_status sf_ct_refill(sf_context* ctx, sf_ct* ct, const uint64_t* words);
+
 /* Host-side wall time per internal scope ("name total_us calls" lines), collected
    when SF_HOST_PROF=1 is set in the environment; diagnostics only. */
 sf_status sf_host_profile(char* buf, int len, int reset);

@@ -137,6 +137,26 @@ class OpCounts:
 
 
 # ---------------------------------------------------------------------------- handles
+class StepGraph:
+    """A captured decode step (Backend.capture): launch() replays every kernel."""
+
+    def __init__(self, be: "Backend", handle: int):
+        self.be, self.h = be, handle
+
+    def launch(self):
+        _check(_native.lib().sf_graph_launch(self.be.ctx, self.h))
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(_native.lib().sf_graph_kernel_launches(self.h))
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h and not _shutdown[0]:
+            _native.lib().sf_graph_destroy(h)
+            self.h = None
+
+
 class Ciphertext:
     """Immutable device ciphertext (engine.hpp:24-28 + CKKS scale)."""
 
@@ -268,6 +288,27 @@ class Backend:
 
     def synchronize(self):
         _check(_native.lib().sf_synchronize(self.ctx))
+
+    # --- CUDA graphs of whole steps (include/sf_b200.h sf_graph_*)
+    def capture(self, fn, *args, **kw):
+        """Capture everything fn(*args, **kw) enqueues into one CUDA graph
+        (nothing runs during the capture). Returns (graph, fn's result): the
+        result's ciphertexts hold the latest replay's values; inputs created
+        before the capture are fed with refill() between replays."""
+        lib = _native.lib()
+        _check(lib.sf_graph_capture_begin(self.ctx))
+        try:
+            res = fn(*args, **kw)
+        finally:
+            g = C.c_void_p()
+            st = lib.sf_graph_capture_end(self.ctx, C.byref(g))
+        _check(st)
+        return StepGraph(self, g.value), res
+
+    def refill(self, ct: "Ciphertext", words: np.ndarray):
+        """Overwrite ct's device words from (pinned) host memory, stream-ordered."""
+        w = np.ascontiguousarray(words, dtype=np.uint64)
+        _check(_native.lib().sf_ct_refill(self.ctx, ct.h, w.ctypes.data_as(_native.u64p)))
 
     # --- client side (off-ledger)
     def encrypt(self, slots, level: int = -1, layout=None, seed: Optional[int] = None) -> Ciphertext:

@@ -41,6 +41,12 @@ SIGNATURES = {
     "sf_last_error": (C.c_char_p, []),
     "sf_profile_butterflies": (st, [vp, dp]),
     "sf_host_profile": (st, [C.c_char_p, C.c_int, C.c_int]),
+    "sf_graph_capture_begin": (st, [vp]),
+    "sf_graph_capture_end": (st, [vp, vpp]),
+    "sf_graph_launch": (st, [vp, vp]),
+    "sf_graph_kernel_launches": (C.c_longlong, [vp]),
+    "sf_graph_destroy": (None, [vp]),
+    "sf_ct_refill": (st, [vp, vp, u64p]),
     "sf_context_create": (st, [C.POINTER(SfParams), vpp]),
     "sf_context_destroy": (None, [vp]),
     "sf_context_info": (st, [vp, ip, ip, ip, ip, ip, u64p]),

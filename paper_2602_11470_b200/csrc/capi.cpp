@@ -19,6 +19,13 @@ struct sf_ct {
 struct sf_vmm_plan {
   std::unique_ptr<sf::VmmPlan> p;
 };
+struct sf_graph {
+  sf_context* ctx = nullptr;
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t x = nullptr;
+  long long launches = 0;  // library kernels per replay
+  std::vector<std::pair<sf::u64*, size_t>> deferred;
+};
 struct sf_kvcache {
   std::atomic<int> rc{1};
   sf::KV kv;
@@ -576,6 +583,70 @@ sf_status sf_profile_end(sf_context* ctx, double* ms, double* bytes, long long* 
     }
     c.prof_recs.clear();
     c.prof_pool_next = 0;
+  });
+}
+
+sf_status sf_graph_capture_begin(sf_context* ctx) {
+  return guard([&] {
+    auto& c = *ctx->c;
+    sf::require(!c.capturing, sf::kInvalidTarget, "graph capture already in progress");
+    SF_CUDA(cudaStreamSynchronize(c.stream));
+    c.capture_deferred.clear();
+    c.capturing = true;
+    c.graph_launch_base = c.launches.load();
+    const cudaError_t e = cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) c.capturing = false;
+    SF_CUDA(e);
+  });
+}
+
+sf_status sf_graph_capture_end(sf_context* ctx, sf_graph** out) {
+  return guard([&] {
+    auto& c = *ctx->c;
+    sf::require(c.capturing, sf::kInvalidTarget, "no graph capture in progress");
+    auto g = std::make_unique<sf_graph>();
+    g->ctx = ctx;
+    const cudaError_t e = cudaStreamEndCapture(c.stream, &g->g);
+    c.capturing = false;
+    g->deferred.swap(c.capture_deferred);
+    g->launches = c.launches.load() - c.graph_launch_base;
+    SF_CUDA(e);
+    SF_CUDA(cudaGraphInstantiateWithFlags(&g->x, g->g, cudaGraphInstantiateFlagAutoFreeOnLaunch));
+    *out = g.release();
+  });
+}
+
+sf_status sf_graph_launch(sf_context* ctx, sf_graph* g) {
+  return guard([&] {
+    auto& c = *ctx->c;
+    sf::require(g && g->ctx == ctx, sf::kInvalidTarget, "graph belongs to another context");
+    SF_CUDA(cudaGraphLaunch(g->x, c.stream));
+    c.launches.fetch_add(g->launches);
+  });
+}
+
+long long sf_graph_kernel_launches(const sf_graph* g) { return g ? g->launches : 0; }
+
+void sf_graph_destroy(sf_graph* g) {
+  if (!g) return;
+  auto& c = *g->ctx->c;
+  cudaStreamSynchronize(c.stream);
+  if (g->x) cudaGraphExecDestroy(g->x);
+  if (g->g) cudaGraphDestroy(g->g);
+  for (auto& d : g->deferred) cudaFreeAsync(d.first, c.stream);
+  cudaStreamSynchronize(c.stream);
+  cudaDeviceGraphMemTrim(c.device);
+  delete g;
+}
+
+sf_status sf_ct_refill(sf_context* ctx, sf_ct* ct, const uint64_t* words) {
+  return guard([&] {
+    auto& c = *ctx->c;
+    const sf::Ct& v = ct->v;
+    sf::require(v.buf && !v.zero, sf::kInvalidTarget, "refill: ciphertext has no device words");
+    const size_t w = (size_t)v.limbs * c.n;
+    SF_CUDA(cudaMemcpyAsync(v.c0(), words, w * 8, cudaMemcpyHostToDevice, c.stream));
+    SF_CUDA(cudaMemcpyAsync(v.c1(c.n), words + w, w * 8, cudaMemcpyHostToDevice, c.stream));
   });
 }
 

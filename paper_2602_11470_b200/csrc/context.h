@@ -28,6 +28,7 @@ struct Buf {
   u64* p = nullptr;
   size_t words = 0;
   Context* ctx = nullptr;
+  bool graph_owned = false;  // allocated while capturing a CUDA graph (a graph memory node)
   Buf(Context* c, size_t w);
   ~Buf();
   Buf(const Buf&) = delete;
@@ -156,6 +157,12 @@ struct Context {
   double delta = 0.0;
   u64 seed = 0;
   int device = 0;
+  // CUDA-graph capture of whole decode steps (sf_graph_*): allocations made while
+  // capturing become graph memory nodes; frees of older buffers are deferred
+  // to graph destruction (a replay still reads them).
+  bool capturing = false;
+  std::vector<std::pair<u64*, size_t>> capture_deferred;
+  long long graph_launch_base = 0;
   bool ks_row = true;  // fused key-switch row stage (SF_KS_ROW=0: separate passes, for A/B timing)
   std::vector<u64> primes;  // q0..qL, p0..p_{alpha-1}
   cudaStream_t stream = nullptr;

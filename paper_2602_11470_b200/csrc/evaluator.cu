@@ -26,10 +26,20 @@ void build_host_tables(Context& c, std::vector<u64>& psi, std::vector<u64>& psi_
 Buf::Buf(Context* c, size_t w) : words(w), ctx(c) {
   SF_HPROF("cudaMallocAsync");
   if (w) SF_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), w * sizeof(u64), c->stream));
+  graph_owned = c->capturing;
 }
 Buf::~Buf() {
   SF_HPROF("cudaFreeAsync");
-  if (p) cudaFreeAsync(p, ctx->stream);
+  if (!p) return;
+  if (ctx->capturing) {
+    if (graph_owned)
+      cudaFreeAsync(p, ctx->stream);  // captured free node
+    else
+      ctx->capture_deferred.push_back({p, words});  // a replay still reads it
+    return;
+  }
+  if (graph_owned) return;  // lives in the graph's memory (freed with the graph)
+  cudaFreeAsync(p, ctx->stream);
 }
 
 BufPtr make_buf(Context& c, size_t words) { return std::make_shared<Buf>(&c, words); }
