@@ -310,8 +310,9 @@ __global__ void __launch_bounds__(TCF * 32, TCF == 8 ? 3 : 8) fused_col_kernel(F
 // job reads exactly one source row: rd = perm_{g^-1}(rs), and within it the
 // column perm_g(rd*C + c) mod C.
 template <int LOGR, int LOGC>
-__global__ void __launch_bounds__(kWarps * 32) ks_row_kernel(KsRowArgs A, Tabs T) {
+__global__ void __launch_bounds__(kWarps * 32, 2) ks_row_kernel(KsRowArgs A, Tabs T) {
   constexpr int C = 1 << LOGC, E = C / 32, LOGN = LOGR + LOGC;
+  auto rbr = [](uint32_t col) { return __brev(col) >> (32 - LOGC); };
   constexpr int tiles = (1 << LOGR) / kWarps;
   constexpr int n = 1 << LOGN;
   extern __shared__ u64 ks_sm[];  // [kWarps][ndig + 1][C]
@@ -329,8 +330,11 @@ __global__ void __launch_bounds__(kWarps * 32) ks_row_kernel(KsRowArgs A, Tabs T
     if (t >= lo && t < hi) {  // own prime: the exact NTT-domain source residues
       const u64* a = A.c1[s] + (size_t)t * n + (size_t)rs * C + lane * E;
 #pragma unroll
-      for (int k = 0; k < E; k += 2)
-        reinterpret_cast<ulonglong2*>(X + lane * E)[k / 2] = reinterpret_cast<const ulonglong2*>(a)[k / 2];
+      for (int k = 0; k < E; k += 2) {
+        const ulonglong2 v = reinterpret_cast<const ulonglong2*>(a)[k / 2];
+        X[rbr(lane * E + k)] = v.x;
+        X[rbr(lane * E + k + 1)] = v.y;
+      }
     } else {
       const u64* a = A.ext[s] + ((size_t)j * A.nt + t) * n + (size_t)rs * C;
       u64 x[E];
@@ -346,8 +350,7 @@ __global__ void __launch_bounds__(kWarps * 32) ks_row_kernel(KsRowArgs A, Tabs T
       };
       warp_fwd<LOGC, kBlocked>(x, X, lane, q, tw);
 #pragma unroll
-      for (int k = 0; k < E; k += 2)
-        reinterpret_cast<ulonglong2*>(X + lane * E)[k / 2] = make_ulonglong2(canon4(x[k], q), canon4(x[k + 1], q));
+      for (int k = 0; k < E; ++k) X[rbr(lane * E + k)] = canon4(x[k], q);
     }
   }
   __syncwarp();
@@ -361,10 +364,10 @@ __global__ void __launch_bounds__(kWarps * 32) ks_row_kernel(KsRowArgs A, Tabs T
     U128 sb[E], sa[E];
 #pragma unroll
     for (int k = 0; k < E; ++k) sb[k] = U128{0, 0}, sa[k] = U128{0, 0};
-    uint32_t sc[E];
+    uint32_t sc[E];  // positions in the bit-reversed row buffers (bank-conflict free gathers)
 #pragma unroll
     for (int k = 0; k < E; ++k)
-      sc[k] = g > 1 ? (auto_perm((uint32_t)(rd * C + lane * E + k), g, LOGN) & (C - 1)) : (uint32_t)(lane * E + k);
+      sc[k] = rbr(g > 1 ? (auto_perm((uint32_t)(rd * C + lane * E + k), g, LOGN) & (C - 1)) : (uint32_t)(lane * E + k));
     for (int j = 0; j < A.ndig; ++j) {
       const u64* X = wsm + j * C;
       const u64* kb = A.key[jb] + ((size_t)(j * 2 + 0) * A.np + m) * n + rowoff;
@@ -419,8 +422,9 @@ __global__ void __launch_bounds__(kWarps * 32) ks_row_kernel(KsRowArgs A, Tabs T
 // source rows rs = perm_g(rd) (digit ext rows / own c1 row and the c0 row),
 // staged through the warp's shared row buffer for the in-row permutation.
 template <int LOGR, int LOGC>
-__global__ void __launch_bounds__(kWarps * 32) ks_sum_kernel(KsSumArgs A, Tabs T) {
+__global__ void __launch_bounds__(kWarps * 32, 2) ks_sum_kernel(KsSumArgs A, Tabs T) {
   constexpr int C = 1 << LOGC, E = C / 32, LOGN = LOGR + LOGC;
+  auto rbr = [](uint32_t col) { return __brev(col) >> (32 - LOGC); };
   constexpr int tiles = (1 << LOGR) / kWarps;
   constexpr int n = 1 << LOGN;
   __shared__ u64 rowbuf[kWarps][C];
@@ -467,16 +471,21 @@ __global__ void __launch_bounds__(kWarps * 32) ks_sum_kernel(KsSumArgs A, Tabs T
       continue;
     }
     const int rs = (int)(auto_perm((uint32_t)rd << LOGC, g, LOGN) >> LOGC);
+    // source positions in the bit-reversed row buffer: an affine map of
+    // br(column) with odd slope g, so every 16 lanes hit 16 distinct banks
     uint32_t sc[E];
 #pragma unroll
-    for (int k = 0; k < E; ++k) sc[k] = auto_perm((uint32_t)(rd * C + lane * E + k), g, LOGN) & (C - 1);
+    for (int k = 0; k < E; ++k) sc[k] = rbr(auto_perm((uint32_t)(rd * C + lane * E + k), g, LOGN) & (C - 1));
     for (int j = 0; j < A.ndig; ++j) {
       const int lo = j * A.alpha, hi = min(lo + A.alpha, A.limbs);
       const u64* src = (t >= lo && t < hi) ? A.c1[s] + (size_t)t * n + (size_t)rs * C
                                            : A.ext[s] + ((size_t)j * A.nt + t) * n + (size_t)rs * C;
 #pragma unroll
-      for (int k = 0; k < E; k += 2)
-        reinterpret_cast<ulonglong2*>(buf + lane * E)[k / 2] = reinterpret_cast<const ulonglong2*>(src + lane * E)[k / 2];
+      for (int k = 0; k < E; k += 2) {
+        const ulonglong2 v = reinterpret_cast<const ulonglong2*>(src + lane * E)[k / 2];
+        buf[rbr(lane * E + k)] = v.x;
+        buf[rbr(lane * E + k + 1)] = v.y;
+      }
       __syncwarp();
       const u64* kb = A.key[jb] + ((size_t)(j * 2 + 0) * A.np + m) * n + rowoff;
       const u64* ka = A.key[jb] + ((size_t)(j * 2 + 1) * A.np + m) * n + rowoff;
@@ -495,8 +504,11 @@ __global__ void __launch_bounds__(kWarps * 32) ks_sum_kernel(KsSumArgs A, Tabs T
     if (qt) {  // P * sigma_g(c0)
       const u64* src = A.c0[s] + (size_t)t * n + (size_t)rs * C;
 #pragma unroll
-      for (int k = 0; k < E; k += 2)
-        reinterpret_cast<ulonglong2*>(buf + lane * E)[k / 2] = reinterpret_cast<const ulonglong2*>(src + lane * E)[k / 2];
+      for (int k = 0; k < E; k += 2) {
+        const ulonglong2 v = reinterpret_cast<const ulonglong2*>(src + lane * E)[k / 2];
+        buf[rbr(lane * E + k)] = v.x;
+        buf[rbr(lane * E + k + 1)] = v.y;
+      }
       __syncwarp();
 #pragma unroll
       for (int k = 0; k < E; ++k) mac128(sb[k], buf[sc[k]], pm);
