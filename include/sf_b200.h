@@ -135,6 +135,13 @@ sf_status sf_mac_plain(sf_context* ctx, const sf_ct* const* cts, const double* s
 sf_status sf_rotate(sf_context* ctx, const sf_ct* a, int r, int hoisted, sf_ct** out); /* :181 */
 /* k rotations of one ciphertext sharing one ModUp (RotationHint{hoisted}). */
 sf_status sf_rotate_hoisted(sf_context* ctx, const sf_ct* a, const int* r, int k, sf_ct** outs);
+/* k independent rotations Rot(a[i], r) (same Galois key), batched into one
+   key-switching pass; charged k rotations. Extension (no reference twin):
+   the throughput form of Backend::rotate used by the C5 sweep. */
+sf_status sf_rotate_many(sf_context* ctx, const sf_ct* const* a, int k, int r, sf_ct** outs);
+/* Microbenchmark: batched two-pass NTT of count x limbs scratch limbs (forward
+   and inverse alternating), device time per limb transform. Diagnostics. */
+sf_status sf_bench_ntt(sf_context* ctx, int limbs, int count, int reps, double* ms_per_limb_ntt);
 sf_status sf_level_drop(sf_context* ctx, const sf_ct* a, int target, sf_ct** out); /* engine.cpp:201 */
 /* oracle hook (engine.cpp:193): client round trip decrypt -> encrypt at target */
 sf_status sf_bootstrap(sf_context* ctx, const sf_ct* a, int target, sf_ct** out);

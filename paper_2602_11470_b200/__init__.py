@@ -305,6 +305,20 @@ class Backend:
         _check(st)
         return StepGraph(self, g.value), res
 
+    def rotate_many(self, cts, r: int):
+        """Rot(c, r) for every c, one batched key-switching pass (sf_rotate_many)."""
+        k = len(cts)
+        arr = (C.c_void_p * k)(*[c.h for c in cts])
+        outs = (C.c_void_p * k)()
+        _check(_native.lib().sf_rotate_many(self.ctx, arr, k, int(r), outs))
+        return [Ciphertext(self, outs[i]) for i in range(k)]
+
+    def bench_ntt(self, limbs: int, count: int, reps: int = 10) -> float:
+        """Device ms per limb NTT of a batch of count x limbs limbs (sf_bench_ntt)."""
+        ms = C.c_double()
+        _check(_native.lib().sf_bench_ntt(self.ctx, limbs, count, reps, C.byref(ms)))
+        return ms.value
+
     def refill(self, ct: "Ciphertext", words: np.ndarray):
         """Overwrite ct's device words from (pinned) host memory, stream-ordered."""
         w = np.ascontiguousarray(words, dtype=np.uint64)

@@ -41,6 +41,8 @@ SIGNATURES = {
     "sf_last_error": (C.c_char_p, []),
     "sf_profile_butterflies": (st, [vp, dp]),
     "sf_host_profile": (st, [C.c_char_p, C.c_int, C.c_int]),
+    "sf_rotate_many": (st, [vp, vpp, C.c_int, C.c_int, vpp]),
+    "sf_bench_ntt": (st, [vp, C.c_int, C.c_int, C.c_int, dp]),
     "sf_graph_capture_begin": (st, [vp]),
     "sf_graph_capture_end": (st, [vp, vpp]),
     "sf_graph_launch": (st, [vp, vp]),

@@ -8,6 +8,7 @@
 
 #include "context.h"
 #include "protocols.h"
+#include "batch.cuh"
 
 struct sf_context {
   std::unique_ptr<sf::Context> c;
@@ -292,6 +293,40 @@ sf_status sf_rotate_hoisted(sf_context* ctx, const sf_ct* a, const int* r, int k
   return guard([&] {
     auto v = sf::rotate_hoisted(*ctx->c, a->v, std::vector<int>(r, r + k));
     for (int i = 0; i < k; ++i) outs[i] = wrap(std::move(v[i]));
+  });
+}
+sf_status sf_rotate_many(sf_context* ctx, const sf_ct* const* a, int k, int r, sf_ct** outs) {
+  return guard([&] {
+    std::vector<const sf::Ct*> src(k);
+    std::vector<sf::RotJob> jobs(k);
+    for (int i = 0; i < k; ++i) src[i] = &a[i]->v, jobs[i] = {i, r};
+    auto v = sf::rotate_batch(*ctx->c, src, jobs, false);
+    for (int i = 0; i < k; ++i) outs[i] = wrap(std::move(v[i]));
+  });
+}
+sf_status sf_bench_ntt(sf_context* ctx, int limbs, int count, int reps, double* ms_per_limb_ntt) {
+  return guard([&] {
+    auto& c = *ctx->c;
+    sf::require(limbs >= 1 && limbs <= c.L + 1 && count >= 1 && reps >= 1, sf::kInvalidTarget, "bench_ntt: bad sizes");
+    sf::BufPtr b = sf::make_buf(c, (size_t)count * limbs * c.n);
+    SF_CUDA(cudaMemsetAsync(b->p, 0x11, (size_t)count * limbs * c.n * 8, c.stream));
+    std::vector<std::pair<sf::u64*, int>> lst;
+    for (int j = 0; j < count; ++j)
+      for (int l = 0; l < limbs; ++l) lst.push_back({b->p + ((size_t)j * limbs + l) * c.n, l});
+    sf::ntt_list(c, lst, false);  // warm-up (both directions: lazy module loading)
+    sf::ntt_list(c, lst, true);
+    cudaEvent_t e0, e1;
+    SF_CUDA(cudaEventCreate(&e0));
+    SF_CUDA(cudaEventCreate(&e1));
+    SF_CUDA(cudaEventRecord(e0, c.stream));
+    for (int i = 0; i < reps; ++i) sf::ntt_list(c, lst, (i & 1) != 0);
+    SF_CUDA(cudaEventRecord(e1, c.stream));
+    SF_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    SF_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *ms_per_limb_ntt = ms / ((double)reps * count * limbs);
   });
 }
 sf_status sf_level_drop(sf_context* ctx, const sf_ct* a, int target, sf_ct** out) {

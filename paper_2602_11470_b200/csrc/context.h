@@ -227,6 +227,7 @@ void ntt_limbs(Context& c, u64* base, int count, int first_prime, bool inverse);
 void ntt_list(Context& c, const std::vector<std::pair<u64*, int>>& limbs, bool inverse);
 
 // --- evaluator (evaluator.cu) -------------------------------------------------
+BufPtr make_buf(Context& c, size_t words);
 Ct alloc_ct(Context& c, int limbs, double scale);
 Pt encode_pt(Context& c, const double* slots, double scale, int limbs);
 std::vector<Pt> encode_many(Context& c, const std::function<void(int, double*)>& gen, int count, double scale,

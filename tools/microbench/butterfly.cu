@@ -27,8 +27,19 @@ __global__ void bench(u64* out, const u64* in, u64 q, u64 w0, u64 wp0, int iters
         u64 U = x[k];
         U = U >= q2 ? U - q2 : U;
         u64 T;
-        if (V == 0) T = shoup_exact(x[k | (1 << b)], w, wp, q);
-        else { T = shoup_approx(x[k | (1 << b)], w, wp, q); T = T >= q2 ? T - q2 : T; }
+        if (V == 0) {
+          T = shoup_exact(x[k | (1 << b)], w, wp, q);
+        } else if (V == 1) {
+          T = shoup_approx(x[k | (1 << b)], w, wp, q);
+          T = T >= q2 ? T - q2 : T;
+        } else {  // V2: [0, 8q) invariant, approximate high product, one correction
+          U = x[k];
+          U = U >= 2 * q2 ? U - 2 * q2 : U;
+          T = shoup_approx(x[k | (1 << b)], w, wp, q);
+          x[k] = U + T;
+          x[k | (1 << b)] = U - T + 2 * q2;
+          continue;
+        }
         x[k] = U + T;
         x[k | (1 << b)] = U - T + q2;
       }
@@ -53,11 +64,12 @@ int main() {
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  for (int v = 0; v < 2; ++v) {
+  for (int v = 0; v < 3; ++v) {
     for (int rep = 0; rep < 2; ++rep) {
       cudaEventRecord(a);
       if (v == 0) bench<0><<<blocks, threads>>>(out, in, q, w, wp, iters);
-      else bench<1><<<blocks, threads>>>(out, in, q, w, wp, iters);
+      else if (v == 1) bench<1><<<blocks, threads>>>(out, in, q, w, wp, iters);
+      else bench<2><<<blocks, threads>>>(out, in, q, w, wp, iters);
       cudaEventRecord(b);
       cudaEventSynchronize(b);
       float ms;
