@@ -416,16 +416,30 @@ def qk_dot(be, q, cache: KVCache, cfg):
         raise ShapeMismatch("qk_dot: key ct count does not match n_prime")
     q_rep = replicate_lanes(be, q, t)
     head_mask = make_mask(make_interleaved(cfg.d, cfg.N, 0, cfg.H), cfg.N, "replicate_extract")
-    maps = [None] * _ceil_div(cache.n_prime, gt)
+    n_maps = _ceil_div(cache.n_prime, gt)
+    terms = [[[] for _ in range(PACK_GROUPS)] for _ in range(n_maps)]
     for j, kc in enumerate(cache.k_cts):
         prod = be.mul(q_rep, kc)
         prod = fold_within_head(be, prod, dh, t)
         masked = be.mul_plain(prod, head_mask)
-        local = (j * t) % gt
-        packed = be.rotate(masked, -local) if local else masked
-        m = (j * t) // gt
-        maps[m] = packed if maps[m] is None else be.add(maps[m], packed)
-    return [be.with_layout(m, None) for m in maps]
+        terms[(j * t) // gt][j % PACK_GROUPS].append((masked, -((j * t) % gt)))
+    # pack + accumulate (kv_attention.cpp:202-206) as rotation sums, one per
+    # (map, key-ct group j mod PACK_GROUPS)
+    return [be.with_layout(pack_sum(be, grp), None) for grp in terms]
+
+
+PACK_GROUPS = 8  # key-ct groups of the QK^T pack sums
+
+
+def pack_sum(be, groups):
+    """sum over non-empty groups of rot_sum(group), accumulated in group order."""
+    acc = None
+    for grp in groups:
+        if not grp:
+            continue
+        s = be.rot_sum(grp)
+        acc = s if acc is None else be.add(acc, s)
+    return acc
 
 
 def softmax_times_v(be, probs, cache: KVCache, cfg):

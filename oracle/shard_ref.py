@@ -68,14 +68,15 @@ def qk_dot_partial(be, q, cache, cfg, rank, world):
     q_rep = P.replicate_lanes(be, q, t)
     head_mask = make_mask(make_interleaved(cfg.d, cfg.N, 0, cfg.H), cfg.N, "replicate_extract")
     n_maps = (cache.n_prime + gt - 1) // gt
-    maps = [None] * n_maps
-    for j in range(rank, len(cache.k_cts), world):
+    G = P.PACK_GROUPS
+    terms = [[[] for _ in range(G)] for _ in range(n_maps)]
+    for j in range(len(cache.k_cts)):
+        if (j % G) % world != rank:  # whole pack groups per rank
+            continue
         prod = P.fold_within_head(be, be.mul(q_rep, cache.k_cts[j]), dh, t)
         masked = be.mul_plain(prod, head_mask)
-        local = (j * t) % gt
-        packed = be.rotate(masked, -local) if local else masked
-        m = (j * t) // gt
-        maps[m] = packed if maps[m] is None else be.add(maps[m], packed)
+        terms[(j * t) // gt][j % G].append((masked, -((j * t) % gt)))
+    maps = [P.pack_sum(be, grp) for grp in terms]
     return [be.with_layout(m, None) if m is not None else be.zeros(q.level - 2) for m in maps]
 
 

@@ -139,6 +139,7 @@ static void vmm_check_input(Context& c, const Ct& x, const VmmPlan& plan) {
 }
 
 constexpr int kGiantGroups = 8;  // giant-step groups of the BSGS rotation sums
+constexpr int kPackGroups = 8;   // key-ct groups of the QK^T pack rotation sums
 
 // Steps 1-2 of vmm.cpp:179-236 for the giant steps this rank owns
 // (g2 = rank mod world; world = 1 is the whole VMM): preprocess ladder,
@@ -453,8 +454,9 @@ std::vector<Ct> qk_dot_partial(Context& c, const Ct& q, const KV& cache, int ran
   const int hb = N / cfg.H;
   for (int h = 0; h < cfg.H; ++h)
     for (int i = 0; i < t; ++i) head_mask[h * hb + i] = 1.0;
-  std::vector<int> own;
-  for (int j = rank; j < (int)cache.k.size(); j += world) own.push_back(j);
+  std::vector<int> own;  // whole pack groups r = j mod kPackGroups with r mod world == rank
+  for (int j = 0; j < (int)cache.k.size(); ++j)
+    if ((j % kPackGroups) % world == rank) own.push_back(j);
   const int J = (int)own.size();
   const int n_maps = ceil_div(cache.n_prime, gt);
   std::vector<Ct> out;
@@ -478,12 +480,23 @@ std::vector<Ct> qk_dot_partial(Context& c, const Ct& q, const KV& cache, int ran
   std::vector<const Pt*> hp;
   for (int i = 0; i < J; ++i) pp.push_back(&prod[i]), hp.push_back(&hm[i]);
   std::vector<Ct> masked = mul_plain_batch(c, pp, hp);
-  std::vector<const Ct*> mp;
-  std::vector<RotJob> pj;
-  for (int i = 0; i < J; ++i) mp.push_back(&masked[i]), pj.push_back({i, -((own[i] * t) % gt)});
-  std::vector<Ct> packed = rotate_batch(c, mp, pj, false);
+  // pack + accumulate (kv_attention.cpp:202-206): one rotation sum per (map,
+  // key-ct group j mod kPackGroups), then the groups' sum
+  std::vector<std::vector<SumTerm>> groups;
+  std::vector<std::pair<int, int>> gid;  // (map, group) of each rotation sum
+  std::map<std::pair<int, int>, int> where;
+  for (int i = 0; i < J; ++i) {
+    const std::pair<int, int> key{(own[i] * t) / gt, own[i] % kPackGroups};
+    if (!where.count(key)) where[key] = (int)groups.size(), groups.emplace_back(), gid.push_back(key);
+    groups[where[key]].push_back({&masked[i], -((own[i] * t) % gt)});
+  }
+  std::vector<Ct> gs = rot_sum_batch(c, groups, false);
   std::vector<std::vector<const Ct*>> per_map(n_maps);
-  for (int i = 0; i < J; ++i) per_map[(own[i] * t) / gt].push_back(&packed[i]);
+  for (int m = 0; m < n_maps; ++m)
+    for (int r = 0; r < kPackGroups; ++r) {
+      auto it = where.find({m, r});
+      if (it != where.end()) per_map[m].push_back(&gs[it->second]);
+    }
   for (auto& m : per_map) {
     if (m.empty()) {
       out.push_back(zeros(c, q.level() - 2));

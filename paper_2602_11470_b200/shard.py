@@ -31,9 +31,13 @@ def own_giants(giants: int, rank: int, world: int) -> List[int]:
     return [g for g in range(giants) if (g % GIANT_GROUPS) % world == rank]
 
 
+PACK_GROUPS = 8  # key ciphertexts j = r mod 8 share one pack rotation sum
+
+
 def own_keys(n_k: int, rank: int, world: int) -> List[int]:
-    """K-cache ciphertexts a rank scores (csrc/protocols.cpp:qk_dot_partial)."""
-    return list(range(rank, n_k, world))
+    """K-cache ciphertexts a rank scores (csrc/protocols.cpp:qk_dot_partial):
+    whole pack groups r = j mod PACK_GROUPS with r mod world == rank."""
+    return [j for j in range(n_k) if (j % PACK_GROUPS) % world == rank]
 
 
 def own_pairs(n_pairs: int, rank: int, world: int) -> List[int]:
