@@ -179,10 +179,8 @@ class LlamaLayer:
         x, h7, h3, h1, p0, p1 = inputs or self.inputs
         mark = (lambda i: be.event_record(10 + i)) if marks else (lambda i: None)
         mark(0)
-        with be.phase("Q, K, V"):
-            q = sf.vmm_interleaved(be, x, None, plan=self.wq)
-            k = sf.vmm_interleaved(be, x, None, plan=self.wk)
-            v = sf.vmm_interleaved(be, x, None, plan=self.wv)
+        with be.phase("Q, K, V"):  # three VMMs of one input: shared ladder + babies
+            q, k, v = sf.vmm_interleaved_multi(be, x, [self.wq, self.wk, self.wv])
         mark(1)
         with be.phase("RoPE & Cache"):
             qr = sf.rope_apply(be, q, self.cfg, self.pos)
@@ -200,8 +198,7 @@ class LlamaLayer:
             o = sf.vmm_interleaved(be, h7, None, plan=self.wo)
         mark(5)
         with be.phase("Up & Gate projection"):
-            g = sf.vmm_interleaved(be, h3, None, plan=self.wg)
-            u = sf.vmm_interleaved(be, h3, None, plan=self.wu)
+            g, u = sf.vmm_interleaved_multi(be, h3, [self.wg, self.wu])
         mark(6)
         with be.phase("Down projection"):
             dn = sf.vmm_interleaved(be, h1, None, plan=self.wd)

@@ -166,6 +166,11 @@ sf_status sf_vmm_predict(const sf_context* ctx, int rows, int cols, int bsgs, in
                          long long* rotations, long long* ct_pt_mults, int* depth);
 sf_status sf_vmm_interleaved(sf_context* ctx, const sf_ct* x, const sf_vmm_plan* plan, int mask_output,
                              sf_ct** out);
+/* k VMMs of the same input (e.g. Q/K/V): outs[i] is word-for-word the result of
+   sf_vmm_interleaved(x, plans[i]) and the ledger is charged as k such calls;
+   the input-only ladder and baby steps run once, the rest as batched launches. */
+sf_status sf_vmm_interleaved_multi(sf_context* ctx, const sf_ct* x, sf_vmm_plan* const* plans, int k,
+                                   int mask_output, sf_ct** outs);
 
 /* --- KV-cache attention (kv_attention.hpp:32-109) --------------------------- */
 /* AttentionConfig{N = slots, d, H, n0, n_max}; validate_attention_config */

@@ -470,6 +470,17 @@ def predict_interleaved_cost(be: Backend, rows: int, cols: int, bsgs: bool = Fal
     return r.value, c.value, d.value
 
 
+def vmm_interleaved_multi(be: Backend, x: Ciphertext, plans, mask_output: bool = False):
+    """[vmm_interleaved(be, x, None, plan=p, mask_output=mask_output) for p in plans],
+    word for word and in the ledger, with the input-only ladder and baby steps
+    evaluated once (sf_vmm_interleaved_multi)."""
+    k = len(plans)
+    arr = (C.c_void_p * k)(*[p.h for p in plans])
+    outs = (C.c_void_p * k)()
+    _check(_native.lib().sf_vmm_interleaved_multi(be.ctx, x.h, arr, k, int(mask_output), outs))
+    return [Ciphertext(be, outs[i]) for i in range(k)]
+
+
 def vmm_interleaved(be: Backend, x: Ciphertext, W, bsgs: bool = False, out_offset: int = 0,
                     mask_output: bool = False, plan: Optional[VmmPlan] = None) -> Ciphertext:
     """vmm_interleaved (vmm.hpp:74-75). Pass `plan` to reuse pre-encoded

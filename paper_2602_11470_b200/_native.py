@@ -42,6 +42,7 @@ SIGNATURES = {
     "sf_profile_butterflies": (st, [vp, dp]),
     "sf_host_profile": (st, [C.c_char_p, C.c_int, C.c_int]),
     "sf_rotate_many": (st, [vp, vpp, C.c_int, C.c_int, vpp]),
+    "sf_vmm_interleaved_multi": (st, [vp, vp, vpp, C.c_int, C.c_int, vpp]),
     "sf_bench_ntt": (st, [vp, C.c_int, C.c_int, C.c_int, dp]),
     "sf_graph_capture_begin": (st, [vp]),
     "sf_graph_capture_end": (st, [vp, vpp]),

@@ -399,6 +399,16 @@ sf_status sf_vmm_interleaved(sf_context* ctx, const sf_ct* x, const sf_vmm_plan*
   return guard([&] { *out = wrap(sf::vmm_interleaved(*ctx->c, x->v, *plan->p, mask_output != 0)); });
 }
 
+sf_status sf_vmm_interleaved_multi(sf_context* ctx, const sf_ct* x, sf_vmm_plan* const* plans, int k,
+                                   int mask_output, sf_ct** outs) {
+  return guard([&] {
+    std::vector<sf::VmmPlan*> ps(k);
+    for (int i = 0; i < k; ++i) ps[i] = plans[i]->p.get();
+    auto v = sf::vmm_interleaved_multi(*ctx->c, x->v, ps, mask_output != 0);
+    for (int i = 0; i < k; ++i) outs[i] = wrap(std::move(v[i]));
+  });
+}
+
 // --- KV attention
 sf_status sf_kv_create(sf_context* ctx, int d, int H, int n0, int n_max, sf_kvcache** out) {
   return guard([&] {

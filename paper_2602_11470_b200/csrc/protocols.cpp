@@ -246,6 +246,127 @@ Ct vmm_finish(Context& c, const Ct& acc_in, VmmPlan& plan, bool mask_output) {
   return acc;
 }
 
+// Several VMMs of the SAME input x (the decode step's Q/K/V and gate/up
+// projections): identical to separate vmm_interleaved calls word for word and
+// in the ledger (each call's charges are applied), but the input-only work --
+// the preprocess ladder and the hoisted baby steps, which depend on x, t_in,
+// t_out and b alone -- runs once, and the per-call work (MACs, rescales, giant
+// rotation sums, reduce ladders, masks) runs as batched launches.
+std::vector<Ct> vmm_interleaved_multi(Context& c, const Ct& x, const std::vector<VmmPlan*>& plans, bool mask_output) {
+  SF_HPROF("vmm_interleaved_multi");
+  const int P = (int)plans.size();
+  std::vector<Ct> out;
+  require(P >= 1, kShapeMismatch, "vmm_multi: no plans");
+  bool share = !x.zero;
+  for (VmmPlan* p : plans) {
+    vmm_check_input(c, x, *p);
+    const VmmShape &a = p->s, &b0 = plans[0]->s;
+    share = share && p->bsgs && a.t_in == b0.t_in && a.t_out == b0.t_out && a.ladder_T == b0.ladder_T &&
+            a.k == b0.k && p->bg.baby == plans[0]->bg.baby && p->bg.giant == plans[0]->bg.giant &&
+            !(p->bg.baby > 64 || p->bg.giant > 64 || a.k > 2048 || c.n < 64);
+  }
+  if (!share) {
+    for (VmmPlan* p : plans) out.push_back(vmm_interleaved(c, x, *p, mask_output));
+    return out;
+  }
+  const VmmShape& s0 = plans[0]->s;
+  const long long unit = (long long)s0.t_in * s0.t_out;
+  const int limbs = x.limbs, b = plans[0]->bg.baby, giants = plans[0]->bg.giant;
+  // 1. ladder (vmm.cpp:190-193), charged once per call
+  Ct stair = x;
+  for (int step = 1; step < s0.t_in; step <<= 1) {
+    const int r = step * (s0.ladder_T - 1);
+    if (pos_mod(r, c.slots) != 0) c.ledger.rot(false, P);
+    c.ledger.add(P);
+    stair = add(c, stair, rotate(c, stair, r, false, false), false, false);
+  }
+  // 2. hoisted babies (vmm.cpp:208-209), charged once per call
+  std::vector<RotJob> jobs;
+  for (int g1 = 1; g1 < b; ++g1) {
+    jobs.push_back({0, (int)(g1 * unit)});
+    if (pos_mod(g1 * unit, c.slots) != 0) c.ledger.rot(true, P);
+  }
+  std::vector<Ct> baby{stair};
+  for (Ct& r : rotate_batch(c, {&stair}, jobs, true, false)) baby.push_back(std::move(r));
+  // 3. every call's fused MAC over all giants, then one batched rescale
+  std::vector<Ct> partial((size_t)P * giants);
+  for (int pi = 0; pi < P; ++pi) {
+    const std::vector<Pt>& diag = plans[pi]->diagonals(limbs);
+    VmmMacArgs A;
+    A.n = c.n;
+    A.b = b;
+    A.giants = giants;
+    A.k = (int)s0.k;
+    for (int g1 = 0; g1 < b; ++g1) A.baby0[g1] = baby[g1].c0(), A.baby1[g1] = baby[g1].c1(c.n);
+    for (long long g = 0; g < s0.k; ++g) A.pt[g] = diag[g].buf->p;
+    for (int g2 = 0; g2 < giants; ++g2) {
+      const int cnt = (int)std::min<long long>(b, s0.k - (long long)g2 * b);
+      c.ledger.ctpt(cnt);
+      c.ledger.add(cnt - 1);
+      Ct& pt = partial[(size_t)pi * giants + g2];
+      pt = alloc_ct(c, limbs, stair.scale * (double)c.primes[limbs - 1]);
+      A.gidx[g2] = g2;
+      A.out0[g2] = pt.c0();
+      A.out1[g2] = pt.c1(c.n);
+    }
+    b_vmm_mac(c, A, limbs);
+  }
+  std::vector<const Ct*> pp;
+  for (auto& p : partial) pp.push_back(&p);
+  std::vector<Ct> resc = rescale_batch(c, pp);
+  for (auto& r : resc) r.scale = stair.scale, r.layout.reset();
+  // 4. giant alignment + sum: the groups of every call in one batch
+  std::vector<std::vector<SumTerm>> groups;
+  std::vector<int> gowner;
+  for (int pi = 0; pi < P; ++pi)
+    for (int r = 0; r < std::min(kGiantGroups, giants); ++r) {
+      groups.emplace_back();
+      gowner.push_back(pi);
+      for (int g2 = r; g2 < giants; g2 += kGiantGroups)
+        groups.back().push_back({&resc[(size_t)pi * giants + g2], (int)(((long long)g2 * b * unit) % c.slots)});
+    }
+  std::vector<Ct> gs = rot_sum_batch(c, groups, false);
+  std::vector<Ct> acc(P);
+  for (int pi = 0; pi < P; ++pi) {
+    std::vector<const Ct*> ap;
+    for (size_t i = 0; i < gs.size(); ++i)
+      if (gowner[i] == pi) ap.push_back(&gs[i]);
+    acc[pi] = sum_cts(c, ap);
+  }
+  // 5. reduce ladders (vmm.cpp:226-230), one batched rotation + addition per step
+  for (int m = 0; (1 << m) < s0.t_out; ++m) {
+    const int st = 1 << m;
+    std::vector<const Ct*> src;
+    std::vector<RotJob> rj;
+    for (int pi = 0; pi < P; ++pi) src.push_back(&acc[pi]), rj.push_back({pi, ((plans[pi]->s.delta >> m) & 1) ? -st : st});
+    std::vector<Ct> rot = rotate_batch(c, src, rj, false);
+    std::vector<const Ct*> rp;
+    for (auto& r : rot) rp.push_back(&r);
+    acc = add_batch(c, src, rp);
+  }
+  // 6. masks (vmm.cpp:233) and layouts
+  if (mask_output) {
+    std::vector<Pt> mk;
+    std::vector<const Ct*> xs;
+    for (int pi = 0; pi < P; ++pi) {
+      const VmmShape& sp = plans[pi]->s;
+      std::vector<double> m(c.slots, 0.0);
+      for (int i = sp.tau_out; i < c.slots; i += sp.t_out) m[i] = 1.0;
+      mk.push_back(cached_pt(c, "stride:" + std::to_string(sp.t_out) + ":" + std::to_string(sp.tau_out), m.data(),
+                             (double)c.primes[acc[pi].limbs - 1], acc[pi].limbs));
+      xs.push_back(&acc[pi]);
+    }
+    std::vector<const Pt*> ps;
+    for (auto& m : mk) ps.push_back(&m);
+    acc = mul_plain_batch(c, xs, ps);
+  }
+  for (int pi = 0; pi < P; ++pi) {
+    const VmmShape& sp = plans[pi]->s;
+    acc[pi].layout = Layout{LayoutKind::Interleaved, sp.d_out, sp.t_out, sp.tau_out, 1, !mask_output};
+  }
+  return acc;
+}
+
 // vmm.cpp:179-236: the whole VMM on one GPU.
 Ct vmm_interleaved(Context& c, const Ct& x, VmmPlan& plan, bool mask_output) {
   SF_HPROF("vmm_interleaved");

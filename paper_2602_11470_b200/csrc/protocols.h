@@ -38,6 +38,8 @@ struct VmmPlan {
 std::unique_ptr<VmmPlan> make_vmm_plan(Context& c, const double* W, int rows, int cols, int level, int in_offset,
                                        int out_offset, bool bsgs);
 Ct vmm_interleaved(Context& c, const Ct& x, VmmPlan& plan, bool mask_output);
+// several VMMs of the same input (shared ladder + babies, batched tails)
+std::vector<Ct> vmm_interleaved_multi(Context& c, const Ct& x, const std::vector<VmmPlan*>& plans, bool mask_output);
 // sharded form: partial over the giant steps g2 = rank mod world, then (after
 // the exchange's modular sum) the reduce ladder + mask
 Ct vmm_partial(Context& c, const Ct& x, VmmPlan& plan, int rank, int world);

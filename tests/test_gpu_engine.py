@@ -167,3 +167,30 @@ def test_graph_capture_replays_the_step_bit_exactly():
         graph.launch()
         got = [c.data() for c in outs]
         assert all(np.array_equal(g_, w_) for g_, w_ in zip(got, want))
+
+
+def test_vmm_multi_equals_separate_calls_and_ledger():
+    # Q/K/V-style: three plans on one input (different output offsets) must give
+    # the separate calls' ciphertexts word for word and the same ledger totals
+    import paper_2602_11470_b200 as sf
+    from oracle.layout import make_interleaved
+    N, L = 4096, 4
+    rng = np.random.default_rng(11)
+    Ws = [rng.normal(size=(128, 128)) / 12 for _ in range(3)]
+    s = np.zeros(N)
+    ly = make_interleaved(128, N, 0)
+    s[np.arange(128) * ly.t] = rng.normal(size=128)
+    res = []
+    for multi in (False, True):
+        be = sf.Backend(N, L, alpha=2, seed=3)
+        x = be.encrypt(s, L, ly, seed=8)
+        plans = [sf.VmmPlan(be, W, 128, 128, L, 0, off, True) for W, off in zip(Ws, (0, 3, 5))]
+        be.ledger.reset()
+        if multi:
+            ys = sf.vmm_interleaved_multi(be, x, plans, mask_output=True)
+        else:
+            ys = [sf.vmm_interleaved(be, x, None, mask_output=True, plan=p) for p in plans]
+        res.append(([y.data() for y in ys], be.ledger.totals().asdict(), [y.layout for y in ys]))
+    (d0, l0, y0), (d1, l1, y1) = res
+    assert all(np.array_equal(a, b) for a, b in zip(d0, d1))
+    assert l0 == l1 and y0 == y1
