@@ -100,6 +100,7 @@ struct TensorSumArgs {  // (D0, D1, D2) = sum_i tensor(a_i, b_i), no relinearisa
 // need only the forward row pass. Source limbs of job j: src[j] + s*n;
 // destination limb d: dst[j] + out_slot[d]*n.
 struct FusedColArgs {
+  int d_per_cta = 0;  // destinations per CTA (0: all); the launcher sets it for small launches
   void set_plan(const u64* tab, int nsrc, int ndst) {
     const size_t base2 = 2 * (size_t)nsrc + (size_t)nsrc * ndst;
     qhat = tab + 2 * nsrc;

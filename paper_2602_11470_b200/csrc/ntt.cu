@@ -201,7 +201,13 @@ __global__ void __launch_bounds__(TCF * 32, TCF == 8 ? 3 : 8) fused_col_kernel(F
   constexpr int tiles = C / TCF;
   constexpr int NT = TCF * 32;
   extern __shared__ u64 sm_all[];  // [ns][TCF][PAD] sources, [2][TCF][PAD] destinations
-  const int job = blockIdx.x / tiles, tile = blockIdx.x - job * tiles;
+  // blockIdx.x = (job * dgroups + dgroup) * tiles + tile; a CTA converts the
+  // destinations [dgroup * dpc, +dpc) (dpc = nd: all of them)
+  const int dpc = A.d_per_cta > 0 ? A.d_per_cta : A.nd;
+  const int dgroups = (A.nd + dpc - 1) / dpc;
+  const int tile = blockIdx.x % tiles, jd = blockIdx.x / tiles;
+  const int job = jd / dgroups, dgroup = jd - job * dgroups;
+  const int d_lo = dgroup * dpc, d_hi = min(A.nd, d_lo + dpc);
   const int col0 = tile * TCF;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int n = 1 << LOGN;
@@ -238,7 +244,7 @@ __global__ void __launch_bounds__(TCF * 32, TCF == 8 ? 3 : 8) fused_col_kernel(F
     __syncwarp();
   }
   __syncthreads();
-  for (int d = 0; d < A.nd; ++d) {
+  for (int d = d_lo; d < d_hi; ++d) {
     const int pd = A.dst_prime[d];
     const u64 q = T.q[pd];
     u64* out = region(A.ns + (d & 1), 0);
@@ -587,16 +593,23 @@ void run_fused_t(Context& c, const FusedColArgs& a) {
     configured = 1;
   }
   require(sm <= 200 * 1024, kInternal, "fused column stage: too many source limbs for shared memory");
-  const unsigned grid = (unsigned)a.count * ((1u << LOGC) / TCF);
+  const int dpc = a.d_per_cta > 0 ? a.d_per_cta : a.nd;
+  const unsigned grid = (unsigned)a.count * ((a.nd + dpc - 1) / dpc) * ((1u << LOGC) / TCF);
   fused_col_kernel<LOGR, LOGC, TCF><<<grid, TCF * 32, sm, c.stream>>>(a, c.tabs);
 }
 
 template <int LOGR, int LOGC>
 void run_fused(Context& c, const FusedColArgs& a) {
-  if ((size_t)a.count * ((1u << LOGC) / 8) >= 444)
+  if ((size_t)a.count * ((1u << LOGC) / 8) >= 444) {
     run_fused_t<LOGR, LOGC, 8>(c, a);
-  else
-    run_fused_t<LOGR, LOGC, 2>(c, a);
+    return;
+  }
+  // small launch (single ciphertexts): 2-column CTAs, and the destinations
+  // spread over CTAs (each recomputes the few source inverse transforms) so the
+  // chain of per-destination transforms does not serialise inside one warp
+  FusedColArgs b = a;
+  b.d_per_cta = 1;
+  run_fused_t<LOGR, LOGC, 2>(c, b);
 }
 
 template <int LOGR, int LOGC>
