@@ -367,26 +367,39 @@ class CkksOracle:
         lvl = min(a.level for a, _ in terms)
         return OCt(self, lib().ock_rot_sum(self.ptr, arr, rr, len(terms)), lvl, ly)
 
-    def fold(self, c, d_head: int, t: int):
-        """fold_within_head (kv_attention.cpp:38-41): sum_{k < d_head} Rot(c, k t),
+    def fold_steps(self, c, rots):
+        """The doubling chain c <- c + Rot(c, r_i), i = 0..m-1 (fold_within_head,
+        replicate_lanes, fold_lanes, the VMM ladders: kv_attention.cpp:30-47,
+        vmm.cpp:190-193, 226-230), i.e. sum_{k < 2^m} Rot(c, sum_i bit_i(k) r_i),
         evaluated as radix rotation sums (fold_radix) and charged
-        as the reference's log2(d_head) rotate + add steps."""
+        as the reference's m rotate + add steps."""
         self._check(c, "rotate")
-        steps = fold_radix(d_head)
-        nrot = sum(1 for l in range(d_head.bit_length() - 1) if ((1 << l) * t) % self.N)
-        for _ in range(nrot):
-            self.ledger.count_rotation(False)
-        for _ in range(d_head.bit_length() - 1):
+        m = len(rots)
+        if m == 0:
+            return c
+        for r in rots:
+            if r % self.N:
+                self.ledger.count_rotation(False)
+        for _ in range(m):
             self.ledger.count_add()
+        ly = c.layout if all(r % self.N == 0 for r in rots) else None
         led, self.ledger = self.ledger, CostLedger()
         try:
-            stride = t
-            for bits in steps:
-                c = self.rot_sum([(c, k * stride) for k in range(1 << bits)])
-                stride <<= bits
+            lo = 0
+            for bits in fold_radix(1 << m):
+                rs = rots[lo:lo + bits]
+                terms = []
+                for k in range(1 << bits):
+                    terms.append((c, sum(rs[i] for i in range(bits) if (k >> i) & 1)))
+                c = self.rot_sum(terms)
+                lo += bits
         finally:
             self.ledger = led
-        return OCt._alias(c, None)
+        return OCt._alias(c, ly)
+
+    def fold(self, c, d_head: int, t: int):
+        """fold_within_head (kv_attention.cpp:38-41)."""
+        return self.fold_steps(c, [(1 << l) * t for l in range(d_head.bit_length() - 1)])
 
     def level_drop(self, a, target: int):
         self._check(a, "level_drop")

@@ -99,6 +99,16 @@ def interleaved_plain(s: Shape, W: np.ndarray, g: int, giant_shift: int) -> np.n
 GIANT_GROUPS = 8  # giant-step groups of the BSGS rotation sums
 
 
+def ladder_rots(s):
+    """Preprocess ladder rotation amounts (vmm.cpp:190-193)."""
+    return [step * (s.ladder_T - 1) for step in (1 << i for i in range(s.t_in.bit_length() - 1))]
+
+
+def reduce_rots(s):
+    """Reduce ladder rotation amounts (vmm.cpp:226-230): -2^m if bit m of delta is set, else +2^m."""
+    return [-(1 << m) if (s.delta >> m) & 1 else (1 << m) for m in range(s.t_out.bit_length() - 1)]
+
+
 def vmm_interleaved(be, x, W: np.ndarray, bsgs: bool = False, out_offset: int = 0,
                     mask_output: bool = False):
     """vmm.cpp:179-236 (the scheme of record)."""
@@ -112,11 +122,7 @@ def vmm_interleaved(be, x, W: np.ndarray, bsgs: bool = False, out_offset: int = 
     if x.layout.d != s.d_in:
         raise ShapeMismatch(f"vmm_interleaved: layout d={x.layout.d} but weights want {s.d_in}")
     # 1. ladder (vmm.cpp:190-193)
-    stair = x
-    step = 1
-    while step < s.t_in:
-        stair = be.add(stair, be.rotate(stair, step * (s.ladder_T - 1)))
-        step <<= 1
+    stair = _fold_steps(be, x, ladder_rots(s))
     unit = s.t_in * s.t_out
     # 2. multiply-accumulate (vmm.cpp:196-224)
     if not bsgs:
@@ -139,11 +145,7 @@ def vmm_interleaved(be, x, W: np.ndarray, bsgs: bool = False, out_offset: int = 
             grp = be.rot_sum(partials[r::GIANT_GROUPS])
             acc = grp if acc is None else be.add(acc, grp)
     # 3. reduce (vmm.cpp:226-230)
-    m = 0
-    while (1 << m) < s.t_out:
-        st = 1 << m
-        acc = be.add(acc, be.rotate(acc, -st if (s.delta >> m) & 1 else st))
-        m += 1
+    acc = _fold_steps(be, acc, reduce_rots(s))
     # 4. mask or defer (vmm.cpp:233-234)
     if mask_output:
         acc = be.mul_plain(acc, stride_mask(N, s.t_out, s.tau_out))
@@ -300,8 +302,20 @@ def _require_clean_interleaved(x, cfg, offset, who):
         raise LayoutMismatch(f"{who}: input garbage must be cleared first")
 
 
+def _fold_steps(be, c, rots):
+    """c <- c + Rot(c, r) for r in rots; CKKS backends evaluate the chain as
+    radix rotation sums with the same ledger charge."""
+    if hasattr(be, "fold_steps"):
+        return be.fold_steps(c, rots)
+    for r in rots:
+        c = be.add(c, be.rotate(c, r))
+    return c
+
+
 def replicate_lanes(be, q, t):
     """kv_attention.cpp:30-34."""
+    if hasattr(be, "fold_steps"):
+        return be.fold_steps(q, [-(1 << s) for s in range(t.bit_length() - 1)])
     r = q
     step = 1
     while step < t:
@@ -324,6 +338,8 @@ def fold_within_head(be, c, d_head, t):
 
 def fold_lanes(be, c, t):
     """kv_attention.cpp:44-47."""
+    if hasattr(be, "fold_steps"):
+        return be.fold_steps(c, [1 << s for s in range(t.bit_length() - 1)])
     step = 1
     while step < t:
         c = be.add(c, be.rotate(c, step))

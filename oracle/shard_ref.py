@@ -20,11 +20,7 @@ def vmm_partial(be, x, W, bsgs, out_offset, rank, world):
     N = be.N
     W = np.asarray(W, dtype=np.float64)
     s = P.interleaved_shape(N, W.shape[0], W.shape[1], x.layout.offset, out_offset)
-    stair = x
-    step = 1
-    while step < s.t_in:
-        stair = be.add(stair, be.rotate(stair, step * (s.ladder_T - 1)))
-        step <<= 1
+    stair = P._fold_steps(be, x, P.ladder_rots(s))
     unit = s.t_in * s.t_out
     if not bsgs:
         own = list(range(rank, s.k, world))
@@ -53,11 +49,7 @@ def vmm_partial(be, x, W, bsgs, out_offset, rank, world):
 def vmm_finish(be, acc, W, in_offset, out_offset, mask_output=False):
     W = np.asarray(W)
     s = P.interleaved_shape(be.N, W.shape[0], W.shape[1], in_offset, out_offset)
-    m = 0
-    while (1 << m) < s.t_out:
-        st = 1 << m
-        acc = be.add(acc, be.rotate(acc, -st if (s.delta >> m) & 1 else st))
-        m += 1
+    acc = P._fold_steps(be, acc, P.reduce_rots(s))
     if mask_output:
         acc = be.mul_plain(acc, stride_mask(be.N, s.t_out, s.tau_out))
     return be.with_layout(acc, Layout("interleaved", s.d_out, s.t_out, s.tau_out, 1, not mask_output))

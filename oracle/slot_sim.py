@@ -218,13 +218,15 @@ class SimBackend:
             acc = x if acc is None else self.add(acc, x)
         return acc
 
+    def fold_steps(self, c, rots):
+        """c <- c + Rot(c, r) for r in rots (the reference's doubling loops)."""
+        for r in rots:
+            c = self.add(c, self.rotate(c, r))
+        return c
+
     def fold(self, c, d_head: int, t: int):
         """fold_within_head, kv_attention.cpp:38-41."""
-        l = 0
-        while (1 << l) < d_head:
-            c = self.add(c, self.rotate(c, (1 << l) * t))
-            l += 1
-        return c
+        return self.fold_steps(c, [(1 << l) * t for l in range(d_head.bit_length() - 1)])
 
     def rotate(self, a, r: int, hoisted: bool = False):
         self._check(a, "rotate")

@@ -221,6 +221,10 @@ struct SumTerm {
 };
 std::vector<Ct> rot_sum_batch(Context& c, const std::vector<std::vector<SumTerm>>& groups, bool hoisted,
                               bool count = true);
+// doubling chains x <- x + Rot(x, r) over rots[i] (radix rotation sums); charged
+// as the reference's rotate + add steps when count && lead
+std::vector<Ct> fold_steps_batch(Context& c, const std::vector<const Ct*>& xs, const std::vector<std::vector<int>>& rots,
+                                 bool count = true, bool lead = true);
 // fold_within_head of every x (radix rotation sums), reference ledger charge
 std::vector<Ct> fold_batch(Context& c, const std::vector<const Ct*>& xs, int d_head, int t, bool count = true);
 // sum of k same-level ciphertexts, charged k-1 additions

@@ -554,40 +554,67 @@ std::vector<Ct> rot_sum_batch(Context& c, const std::vector<std::vector<SumTerm>
   return out;
 }
 
-// fold_within_head (kv_attention.cpp:38-41) of many ciphertexts: the radix
-// rotation sums of DESIGN.md §3.8, charged as the reference's log2(d_head)
-// rotate + add steps per ciphertext.
-std::vector<Ct> fold_batch(Context& c, const std::vector<const Ct*>& xs, int d_head, int t, bool count) {
-  SF_HPROF("fold_batch");
-  int D = 0;
-  while ((1 << D) < d_head) ++D;
-  if (count)
-    for (size_t i = 0; i < xs.size(); ++i) {
-      check_ct(c, *xs[i], "rotate");
-      for (int l = 0; l < D; ++l)
-        if (pos_mod((1 << l) * t, c.slots) != 0) c.ledger.rot(false);
-      c.ledger.add(D);
-    }
-  std::vector<int> steps;
-  if (D > 0) {
-    if (D <= 3)
-      steps.push_back(D);
-    else
-      steps.push_back((D + 1) / 2), steps.push_back(D / 2);
-  }
+// Doubling chains x <- x + Rot(x, r_i), i < m, of many ciphertexts (each with
+// its own amounts): fold_within_head, replicate_lanes, fold_lanes and the VMM
+// ladders (kv_attention.cpp:30-47, vmm.cpp:190-193, 226-230). The value is
+// sum_{k < 2^m} Rot(x, sum_i bit_i(k) r_i), evaluated as the radix rotation sums
+// of DESIGN.md §3.8 (m <= 3 bits in one sum, else ceil(m/2) then floor(m/2));
+// charged as the reference's m rotate + add steps per ciphertext.
+std::vector<Ct> fold_steps_batch(Context& c, const std::vector<const Ct*>& xs, const std::vector<std::vector<int>>& rots,
+                                 bool count, bool lead) {
+  SF_HPROF("fold_steps_batch");
+  require(xs.size() == rots.size(), kShapeMismatch, "fold_steps: operand count");
   std::vector<Ct> cur;
-  for (const Ct* x : xs) cur.push_back(*x);
-  long long stride = t;
-  for (int bits : steps) {
-    std::vector<std::vector<SumTerm>> groups(cur.size());
-    for (size_t i = 0; i < cur.size(); ++i)
-      for (int k = 0; k < (1 << bits); ++k) groups[i].push_back({&cur[i], (int)(k * stride % c.slots)});
-    std::vector<Ct> nxt = rot_sum_batch(c, groups, false, false);
-    cur.swap(nxt);
-    stride <<= bits;
+  size_t mmax = 0;
+  for (size_t i = 0; i < xs.size(); ++i) {
+    check_ct(c, *xs[i], "rotate");
+    if (count && lead) {
+      for (int r : rots[i])
+        if (pos_mod(r, c.slots) != 0) c.ledger.rot(false);
+      c.ledger.add((long long)rots[i].size());
+    }
+    cur.push_back(*xs[i]);
+    mmax = std::max(mmax, rots[i].size());
   }
-  for (Ct& y : cur) y.layout.reset();
+  // all chains share the radix schedule of their own length; group by length
+  std::map<int, std::vector<int>> by_len;
+  for (size_t i = 0; i < xs.size(); ++i) by_len[(int)rots[i].size()].push_back((int)i);
+  for (auto& [m, idx] : by_len) {
+    if (m == 0) continue;
+    std::vector<int> steps;
+    if (m <= 3)
+      steps.push_back(m);
+    else
+      steps.push_back((m + 1) / 2), steps.push_back(m / 2);
+    int lo = 0;
+    for (int bits : steps) {
+      std::vector<std::vector<SumTerm>> groups(idx.size());
+      for (size_t g = 0; g < idx.size(); ++g) {
+        const std::vector<int>& rs = rots[idx[g]];
+        for (int k = 0; k < (1 << bits); ++k) {
+          long long r = 0;
+          for (int i = 0; i < bits; ++i)
+            if ((k >> i) & 1) r += rs[lo + i];
+          groups[g].push_back({&cur[idx[g]], (int)pos_mod(r, c.slots)});
+        }
+      }
+      std::vector<Ct> nxt = rot_sum_batch(c, groups, false, false);
+      for (size_t g = 0; g < idx.size(); ++g) cur[idx[g]] = std::move(nxt[g]);
+      lo += bits;
+    }
+  }
+  for (size_t i = 0; i < xs.size(); ++i) {
+    bool all0 = true;
+    for (int r : rots[i]) all0 = all0 && pos_mod(r, c.slots) == 0;
+    cur[i].layout = all0 ? xs[i]->layout : OptLayout();
+  }
   return cur;
+}
+
+std::vector<Ct> fold_batch(Context& c, const std::vector<const Ct*>& xs, int d_head, int t, bool count) {
+  std::vector<int> rs;
+  for (int l = 0; (1 << l) < d_head; ++l) rs.push_back((1 << l) * t);
+  return fold_steps_batch(c, xs, std::vector<std::vector<int>>(xs.size(), rs), count, true);
 }
 
 // -------------------------------------------------------------------- rescale

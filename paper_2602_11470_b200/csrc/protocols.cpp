@@ -138,6 +138,17 @@ static void vmm_check_input(Context& c, const Ct& x, const VmmPlan& plan) {
   require(x.level() > 0, kLevelUnderflow, "mul_plain: no multiplicative level left");
 }
 
+static std::vector<int> ladder_rots(const VmmShape& s) {  // vmm.cpp:190-193
+  std::vector<int> r;
+  for (int step = 1; step < s.t_in; step <<= 1) r.push_back(step * (s.ladder_T - 1));
+  return r;
+}
+static std::vector<int> reduce_rots(const VmmShape& s) {  // vmm.cpp:226-230
+  std::vector<int> r;
+  for (int m = 0; (1 << m) < s.t_out; ++m) r.push_back(((s.delta >> m) & 1) ? -(1 << m) : (1 << m));
+  return r;
+}
+
 constexpr int kGiantGroups = 8;  // giant-step groups of the BSGS rotation sums
 constexpr int kPackGroups = 8;   // key-ct groups of the QK^T pack rotation sums
 
@@ -153,9 +164,7 @@ Ct vmm_partial(Context& c, const Ct& x, VmmPlan& plan, int rank, int world) {
   const bool lead = rank == 0;
   const VmmShape& s = plan.s;
   const std::vector<Pt>& diag = plan.diagonals(x.limbs);
-  Ct stair = x;
-  for (int step = 1; step < s.t_in; step <<= 1)
-    stair = add(c, stair, rotate(c, stair, step * (s.ladder_T - 1), false, lead), false, lead);
+  Ct stair = fold_steps_batch(c, {&x}, {ladder_rots(s)}, true, lead)[0];  // ladder (vmm.cpp:190-193)
   const long long unit = (long long)s.t_in * s.t_out;
   const int limbs = x.limbs;
   if (!plan.bsgs) {
@@ -232,11 +241,7 @@ Ct vmm_partial(Context& c, const Ct& x, VmmPlan& plan, int rank, int world) {
 Ct vmm_finish(Context& c, const Ct& acc_in, VmmPlan& plan, bool mask_output) {
   SF_HPROF("vmm_finish");
   const VmmShape& s = plan.s;
-  Ct acc = acc_in;
-  for (int m = 0; (1 << m) < s.t_out; ++m) {
-    const int st = 1 << m;
-    acc = add(c, acc, rotate(c, acc, ((s.delta >> m) & 1) ? -st : st, false));
-  }
+  Ct acc = fold_steps_batch(c, {&acc_in}, {reduce_rots(s)})[0];  // reduce (vmm.cpp:226-230)
   if (mask_output) {
     std::vector<double> mk(c.slots, 0.0);
     for (int i = s.tau_out; i < c.slots; i += s.t_out) mk[i] = 1.0;
@@ -273,13 +278,11 @@ std::vector<Ct> vmm_interleaved_multi(Context& c, const Ct& x, const std::vector
   const long long unit = (long long)s0.t_in * s0.t_out;
   const int limbs = x.limbs, b = plans[0]->bg.baby, giants = plans[0]->bg.giant;
   // 1. ladder (vmm.cpp:190-193), charged once per call
-  Ct stair = x;
-  for (int step = 1; step < s0.t_in; step <<= 1) {
-    const int r = step * (s0.ladder_T - 1);
+  const std::vector<int> lr = ladder_rots(s0);
+  for (int r : lr)
     if (pos_mod(r, c.slots) != 0) c.ledger.rot(false, P);
-    c.ledger.add(P);
-    stair = add(c, stair, rotate(c, stair, r, false, false), false, false);
-  }
+  c.ledger.add((long long)P * lr.size());
+  Ct stair = fold_steps_batch(c, {&x}, {lr}, false)[0];
   // 2. hoisted babies (vmm.cpp:208-209), charged once per call
   std::vector<RotJob> jobs;
   for (int g1 = 1; g1 < b; ++g1) {
@@ -334,15 +337,11 @@ std::vector<Ct> vmm_interleaved_multi(Context& c, const Ct& x, const std::vector
     acc[pi] = sum_cts(c, ap);
   }
   // 5. reduce ladders (vmm.cpp:226-230), one batched rotation + addition per step
-  for (int m = 0; (1 << m) < s0.t_out; ++m) {
-    const int st = 1 << m;
+  {
     std::vector<const Ct*> src;
-    std::vector<RotJob> rj;
-    for (int pi = 0; pi < P; ++pi) src.push_back(&acc[pi]), rj.push_back({pi, ((plans[pi]->s.delta >> m) & 1) ? -st : st});
-    std::vector<Ct> rot = rotate_batch(c, src, rj, false);
-    std::vector<const Ct*> rp;
-    for (auto& r : rot) rp.push_back(&r);
-    acc = add_batch(c, src, rp);
+    std::vector<std::vector<int>> rr;
+    for (int pi = 0; pi < P; ++pi) src.push_back(&acc[pi]), rr.push_back(reduce_rots(plans[pi]->s));
+    acc = fold_steps_batch(c, src, rr);
   }
   // 6. masks (vmm.cpp:233) and layouts
   if (mask_output) {
@@ -569,8 +568,9 @@ std::vector<Ct> qk_dot_partial(Context& c, const Ct& q, const KV& cache, int ran
   require((int)cache.k.size() == ceil_div(cache.n_prime, t), kShapeMismatch,
           "qk_dot: key ct count does not match n_prime");
   const bool lead = rank == 0;
-  Ct q_rep = q;
-  for (int step = 1; step < t; step <<= 1) q_rep = add(c, q_rep, rotate(c, q_rep, -step, false, lead), false, lead);
+  std::vector<int> rep;  // replicate_lanes (30-34)
+  for (int step = 1; step < t; step <<= 1) rep.push_back(-step);
+  Ct q_rep = fold_steps_batch(c, {&q}, {rep}, true, lead)[0];
   std::vector<double> head_mask(N, 0.0);  // ReplicateExtract (layouts.cpp:134-138)
   const int hb = N / cfg.H;
   for (int h = 0; h < cfg.H; ++h)
@@ -685,7 +685,11 @@ Ct softmax_times_v_finish(Context& c, const std::vector<const Ct3*>& parts, cons
   for (const Ct3* p : parts) live += p->zero ? 0 : 1;
   if (live > 1) c.ledger.add(live - 1);
   Ct folded = relin_rescale(c, add_ct3(c, parts));
-  for (int step = 1; step < t; step <<= 1) folded = add(c, folded, rotate(c, folded, step, false));
+  {
+    std::vector<int> fl;  // fold_lanes (44-47)
+    for (int step = 1; step < t; step <<= 1) fl.push_back(step);
+    folded = fold_steps_batch(c, {&folded}, {fl})[0];
+  }
   std::vector<double> sm(cfg.N, 0.0);
   for (int i = 0; i < cfg.N; i += t) sm[i] = 1.0;
   Ct out = mul_plain_cached(c, folded, "stride:" + std::to_string(t) + ":0", sm);
