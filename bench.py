@@ -165,13 +165,19 @@ class LlamaLayer:
               "Down projection"]
 
     def phase_ms(self, steps):
-        """Device time per phase (CUDA events between phases on the library stream)."""
+        """Device time per phase: CUDA events between phases, recorded inside a
+        captured graph of the marked step (host issue time cannot leak in)."""
         be = self.be
+        graph, _ = be.capture(self.step, marks=True)
+        graph.launch()
+        be.synchronize()
         tot = [0.0] * len(self.PHASES)
         for _ in range(steps):
-            self.step(marks=True)
+            graph.launch()
+            be.synchronize()
             for i in range(len(self.PHASES)):
                 tot[i] += be.event_elapsed_ms(10 + i, 11 + i)
+        del graph
         return {p: round(t / steps, 3) for p, t in zip(self.PHASES, tot)}
 
     def step(self, inputs=None, marks=False):

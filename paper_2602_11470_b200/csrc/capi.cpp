@@ -590,7 +590,12 @@ sf_status sf_event_record(sf_context* ctx, int slot) {
       SF_CUDA(cudaEventCreate(&e));
       c.events.push_back(e);
     }
-    SF_CUDA(cudaEventRecord(c.events[slot], c.stream));
+    // inside a graph capture the record must be an external event node, so
+    // the event is really recorded (and timed) on every replay
+    if (c.capturing)
+      SF_CUDA(cudaEventRecordWithFlags(c.events[slot], c.stream, cudaEventRecordExternal));
+    else
+      SF_CUDA(cudaEventRecord(c.events[slot], c.stream));
   });
 }
 sf_status sf_event_elapsed_ms(sf_context* ctx, int a, int b, float* ms) {
@@ -680,7 +685,6 @@ void sf_graph_destroy(sf_graph* g) {
   if (g->g) cudaGraphDestroy(g->g);
   for (auto& d : g->deferred) cudaFreeAsync(d.first, c.stream);
   cudaStreamSynchronize(c.stream);
-  cudaDeviceGraphMemTrim(c.device);
   delete g;
 }
 
