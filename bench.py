@@ -355,7 +355,6 @@ def main():
     ms_step = ms_total / args.steps
     value = ms_step / world  # whole-job: `world` independent tokens per step time
 
-    phases = layer.phase_ms(args.steps)
 
     # ---- roofline: live per-family kernel timing over the same steps
     import ctypes as C
@@ -441,6 +440,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
 
+    phases = layer.phase_ms(args.steps)  # last: its graph's memory must not disturb the timed graph
     cpu = None if (args.no_cpu_baseline or rank != 0) else cpu_baseline_sample()
     vmm_per_step = 7
     line = {

@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) ks_row_kernel(KsRowArgs A, Tab
   // 2. every job of this source: permuted inner product with its key
   for (int jb = A.job_begin[s]; jb < A.job_begin[s + 1]; ++jb) {
     const u64 g = A.g[jb];
-    const int rd = g > 1 ? (int)(auto_perm((uint32_t)rs << LOGC, A.ginv[jb], LOGN) >> LOGC) : rs;
+    const int rd = g > 1 ? (int)RowPerm<LOGR, LOGC>(rs, A.ginv[jb]).src_row : rs;
     const size_t rowoff = (size_t)rd * C + lane * E;
     U128 sb[E], sa[E];
 #pragma unroll
@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) ks_row_kernel(KsRowArgs A, Tab
     uint32_t sc[E];  // positions in the bit-reversed row buffers (bank-conflict free gathers)
 #pragma unroll
     for (int k = 0; k < E; ++k)
-      sc[k] = rbr(g > 1 ? (auto_perm((uint32_t)(rd * C + lane * E + k), g, LOGN) & (C - 1)) : (uint32_t)(lane * E + k));
+      sc[k] = g > 1 ? RowPerm<LOGR, LOGC>(rd, g).pos(rbr(lane * E + k)) : rbr(lane * E + k);
     for (int j = 0; j < A.ndig; ++j) {
       const u64* X = wsm + j * C;
       const u64* kb = A.key[jb] + ((size_t)(j * 2 + 0) * A.np + m) * n + rowoff;
@@ -476,12 +476,13 @@ __global__ void __launch_bounds__(kWarps * 32, 2) ks_sum_kernel(KsSumArgs A, Tab
       ++terms;
       continue;
     }
-    const int rs = (int)(auto_perm((uint32_t)rd << LOGC, g, LOGN) >> LOGC);
+    const RowPerm<LOGR, LOGC> rp(rd, g);
+    const int rs = (int)rp.src_row;
     // source positions in the bit-reversed row buffer: an affine map of
     // br(column) with odd slope g, so every 16 lanes hit 16 distinct banks
     uint32_t sc[E];
 #pragma unroll
-    for (int k = 0; k < E; ++k) sc[k] = rbr(auto_perm((uint32_t)(rd * C + lane * E + k), g, LOGN) & (C - 1));
+    for (int k = 0; k < E; ++k) sc[k] = rp.pos(rbr(lane * E + k));
     for (int j = 0; j < A.ndig; ++j) {
       const int lo = j * A.alpha, hi = min(lo + A.alpha, A.limbs);
       const u64* src = (t >= lo && t < hi) ? A.c1[s] + (size_t)t * n + (size_t)rs * C

@@ -116,5 +116,26 @@ __device__ __forceinline__ uint32_t auto_perm(uint32_t i, u64 g, int logn) {
   return brev((uint32_t)((e2 - 1) >> 1), logn);
 }
 
+// Row-granular automorphism X -> X^g in the bit-reversed evaluation order with
+// n = R x C: position i = rd*C + c maps to perm_g(i), whose row
+// and bit-reversed column are
+//   row(perm_g(i))        = br_R(B mod R)
+//   br_C(col(perm_g(i)))  = (floor(B / R) + g * br_C(c)) mod C
+// with B = ((2 br_R(rd) + 1) g - 1) / 2: the source row depends on rd only and
+// the in-row position is affine in br_C(c) (odd slope g).
+template <int LOGR, int LOGC>
+struct RowPerm {
+  uint32_t src_row, base, slope;  // position(bc) = (base + slope * bc) mod C
+  __device__ __forceinline__ RowPerm(int rd, u64 g) {
+    constexpr uint32_t R = 1u << LOGR, C = 1u << LOGC;
+    const u64 B = ((2ull * (__brev((uint32_t)rd) >> (32 - LOGR)) + 1) * g - 1) >> 1;
+    src_row = __brev((uint32_t)(B & (R - 1))) >> (32 - LOGR);
+    base = (uint32_t)(B >> LOGR) & (C - 1);
+    slope = (uint32_t)g & (C - 1);
+  }
+  // bit-reversed source column of the element whose own column has br_C = bc
+  __device__ __forceinline__ uint32_t pos(uint32_t bc) const { return (base + slope * bc) & ((1u << LOGC) - 1); }
+};
+
 }  // namespace wntt
 }  // namespace sf
