@@ -612,6 +612,54 @@ void mod_down(Ctx& c, std::vector<u64>& acc, int limbs, u64* out) {
   }
 }
 
+// Relinearise-and-rescale in one basis conversion: for the
+// degree-2 ciphertext (d0, d1, d2) at `limbs` limbs, (kb, ka) = the key-switch
+// inner products of d2 under the relinearisation key (extended basis), and
+// X = (kb + P d0, ka + P d1) on the Q limbs; the result, at limbs - 1 limbs, is
+// (X_i - conv_{M -> q_i}(X_M)) * M^-1 mod q_i with M = q_{limbs-1} * P, i.e.
+// ModDown and the rescale by the top prime as ONE fast basis conversion.
+Ct* relin_rescale_merged(Ctx& c, const u64* d0, const u64* d1, const u64* d2, int limbs, double scale) {
+  const int n = c.n;
+  const size_t nt = (size_t)limbs + c.alpha;
+  std::vector<u64> acc[2] = {std::vector<u64>(nt * n, 0), std::vector<u64>(nt * n, 0)};
+  key_switch_ext(c, d2, limbs, 0, acc[0], acc[1]);
+  const u64* dd[2] = {d0, d1};
+  std::vector<int> M{limbs - 1};
+  for (int k = 0; k < c.alpha; ++k) M.push_back((int)c.P_index(k));
+  Ct* out = new_ct(c, limbs - 1, scale);
+  for (int part = 0; part < 2; ++part) {
+    std::vector<u64>& X = acc[part];
+#pragma omp parallel for
+    for (int l = 0; l < limbs; ++l) {  // X_Q = acc_Q + P d
+      const u64 q = c.primes[l], pm = P_mod(c, q);
+      u64* x = X.data() + (size_t)l * n;
+      const u64* d = dd[part] + (size_t)l * n;
+      for (int k = 0; k < n; ++k) x[k] = addmod(x[k], mulmod(d[k], pm, q), q);
+    }
+    // coefficient forms of the M limbs: slot limbs-1 (q_top), then the P slots
+    std::vector<u64> coef((size_t)M.size() * n);
+#pragma omp parallel for
+    for (int j = 0; j < (int)M.size(); ++j) {
+      std::memcpy(coef.data() + (size_t)j * n, X.data() + (size_t)(limbs - 1 + j) * n, sizeof(u64) * n);
+      ntt_inv(c, M[j], coef.data() + (size_t)j * n);
+    }
+    std::vector<const u64*> in;
+    for (size_t j = 0; j < M.size(); ++j) in.push_back(coef.data() + j * n);
+#pragma omp parallel for
+    for (int l = 0; l < limbs - 1; ++l) {
+      const u64 q = c.primes[l];
+      std::vector<u64> t(n);
+      conv_basis(c, M, in, l, t.data());
+      ntt_fwd(c, l, t.data());
+      const u64 minv = invmod(mulmod(P_mod(c, q), c.primes[limbs - 1] % q, q), q);
+      const u64* x = X.data() + (size_t)l * n;
+      u64* o = poly(c, out, part, l);
+      for (int k = 0; k < n; ++k) o[k] = mulmod(submod(x[k], t[k], q), minv, q);
+    }
+  }
+  return out;
+}
+
 // hybrid key switch of d under key `g` (ModUp, automorphism, inner product,
 // ModDown of both parts). Returns (kb, ka), `limbs` limbs each.
 void key_switch(Ctx& c, const u64* d, int limbs, u64 g, u64* kb, u64* ka) {
@@ -702,33 +750,22 @@ Ct* mul(Ctx& c, const Ct* a, const Ct* b) {
     r->zero = true;
     return r;
   }
-  Ct* t = new_ct(c, limbs, a->scale * b->scale);
-  std::vector<u64> d2((size_t)limbs * n);
+  std::vector<u64> d((size_t)3 * limbs * n);
 #pragma omp parallel for
   for (int l = 0; l < limbs; ++l) {
     const u64 q = c.primes[l];
     const u64 *a0 = poly(c, a, 0, l), *a1 = poly(c, a, 1, l), *b0 = poly(c, b, 0, l), *b1 = poly(c, b, 1, l);
-    u64 *o0 = poly(c, t, 0, l), *o1 = poly(c, t, 1, l);
+    u64* o0 = d.data() + (size_t)l * n;
+    u64* o1 = d.data() + ((size_t)limbs + l) * n;
+    u64* o2 = d.data() + ((size_t)2 * limbs + l) * n;
     for (int k = 0; k < n; ++k) {
       o0[k] = mulmod(a0[k], b0[k], q);
       o1[k] = addmod(mulmod(a0[k], b1[k], q), mulmod(a1[k], b0[k], q), q);
-      d2[(size_t)l * n + k] = mulmod(a1[k], b1[k], q);
+      o2[k] = mulmod(a1[k], b1[k], q);
     }
   }
-  std::vector<u64> kb((size_t)limbs * n), ka((size_t)limbs * n);
-  key_switch(c, d2.data(), limbs, 0, kb.data(), ka.data());
-#pragma omp parallel for
-  for (int l = 0; l < limbs; ++l) {
-    const u64 q = c.primes[l];
-    u64 *o0 = poly(c, t, 0, l), *o1 = poly(c, t, 1, l);
-    for (int k = 0; k < n; ++k) {
-      o0[k] = addmod(o0[k], kb[(size_t)l * n + k], q);
-      o1[k] = addmod(o1[k], ka[(size_t)l * n + k], q);
-    }
-  }
-  Ct* r = rescale(c, t);
-  delete t;
-  return r;
+  return relin_rescale_merged(c, d.data(), d.data() + (size_t)limbs * n, d.data() + (size_t)2 * limbs * n, limbs,
+                              a->scale * b->scale / (double)c.primes[limbs - 1]);
 }
 
 // Lazily relinearised sum of ct x ct products: (d0, d1, d2) =
@@ -777,20 +814,9 @@ Ct* relin_rescale(Ctx& c, const Ct* x) {
     return z;
   }
   if (x->d2.empty()) throw std::runtime_error("relin_rescale: not a degree-2 ciphertext");
-  std::vector<u64> kb((size_t)limbs * n), ka((size_t)limbs * n);
-  key_switch(c, x->d2.data(), limbs, 0, kb.data(), ka.data());
-  Ct* t = new_ct(c, limbs, x->scale);
-#pragma omp parallel for
-  for (int l = 0; l < limbs; ++l) {
-    const u64 q = c.primes[l];
-    for (int k = 0; k < n; ++k) {
-      poly(c, t, 0, l)[k] = addmod(poly(c, x, 0, l)[k], kb[(size_t)l * n + k], q);
-      poly(c, t, 1, l)[k] = addmod(poly(c, x, 1, l)[k], ka[(size_t)l * n + k], q);
-    }
-  }
-  Ct* r = rescale(c, t);
-  delete t;
-  return r;
+  (void)n;
+  return relin_rescale_merged(c, poly(c, x, 0, 0), poly(c, x, 1, 0), x->d2.data(), limbs,
+                              x->scale / (double)c.primes[limbs - 1]);
 }
 
 // sum_k ct_k (*) pt_k with plaintexts encoded at scale q_top (so the scale is

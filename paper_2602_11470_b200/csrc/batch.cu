@@ -252,6 +252,17 @@ __global__ void vmm_mac_kernel(VmmMacArgs A, const u64* Q, const u64* MH, const 
   }
 }
 
+__global__ void axpy_pm_kernel(AxpyBatch B, int limbs, int logn, const u64* pm, const u64* Q, const u64* MH,
+                               const u64* ML) {
+  const int j = blockIdx.y;
+  const size_t total = (size_t)limbs << logn;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const int l = (int)(i >> logn);
+    const u64 q = Q[l];
+    B.acc[j][i] = add_mod(B.acc[j][i], mulmod(B.d[j][i], pm[l], q, MH[l], ML[l]), q);
+  }
+}
+
 // Rotation-sum inner products for ring degrees without the two-pass kernels:
 // one thread per (output, extended limb, coefficient), every limb written in
 // the NTT domain (the generic ModDown follows).
@@ -433,6 +444,14 @@ void b_ks_sum(Context& c, const KsSumArgs& A) {
   if (!ntt_ks_sum(c, A))
     ks_sum_generic_kernel<<<grid2((size_t)A.nt * c.n, A.nout), kT, 0, c.stream>>>(A, c.tabs.q, c.tabs.mh, c.tabs.ml,
                                                                                    c.logn);
+  post(c);
+}
+
+void b_axpy_pm(Context& c, const AxpyBatch& B, int limbs, const u64* pm_dev) {
+  if (!B.count) return;
+  ProfScope prof(c, kFamElem, 24.0 * limbs * c.n * B.count);
+  axpy_pm_kernel<<<grid2((size_t)limbs * c.n, B.count), kT, 0, c.stream>>>(B, limbs, c.logn, pm_dev, c.tabs.q,
+                                                                            c.tabs.mh, c.tabs.ml);
   post(c);
 }
 

@@ -69,6 +69,12 @@ struct KsBatch {  // key-switch inner products over the extended basis
   u64* acca[kJobs];
 };
 
+struct AxpyBatch {  // acc[l] += pm[l] * d[l] (mod q_l), l < limbs
+  int count = 0;
+  u64* acc[kJobsWide];
+  const u64* d[kJobsWide];
+};
+
 struct SubScaleBatch {  // out = (acc - conv) * inv (+ addend permuted by g)
   int count = 0;
   const u64 *acc[kJobsWide], *conv[kJobsWide], *addend[kJobsWide];
@@ -139,6 +145,12 @@ struct EpiBatch {
 struct KsRowArgs {
   int nsrc = 0, limbs = 0, nt = 0, ndig = 0, alpha = 0, np = 0;
   int run_len = 0;  // host-side scratch (jobs of the current source while splitting)
+  // merged relinearise + rescale: Q targets accumulate
+  // P * (add0, add1) and the top Q prime is inverse-row-passed like the P primes
+  int merged = 0;
+  u64 pm[kMaxPrimes];
+  const u64* add0[kJobs];
+  const u64* add1[kJobs];
   int tprime[kMaxPrimes];
   // per work unit (a source, or a chunk of one source's jobs):
   const u64* c1[kJobs];   // NTT-domain source polynomial (limbs x n)
@@ -194,6 +206,7 @@ void b_lift(Context& c, const LiftBatch& B, int limbs, int last_prime);
 void b_conv(Context& c, const ConvBatch& A);
 void b_ks(Context& c, const KsBatch& A);
 void b_subscale(Context& c, const SubScaleBatch& B, int limbs, const u64* inv, const u64* inv_s);
+void b_axpy_pm(Context& c, const AxpyBatch& B, int limbs, const u64* pm_dev);
 void b_vmm_mac(Context& c, const VmmMacArgs& A, int limbs);
 
 // ---- batched evaluator (keyswitch.cu) ------------------------------------------

@@ -182,7 +182,9 @@ struct Context {
   std::map<std::string, ConvPlan> conv_plans;
   std::map<std::string, Pt> pt_cache;  // semantic-key plaintext cache (masks)
   std::map<int, BufPtr> level_consts;  // per-limb-count rescale / moddown constants
-  std::map<int, std::vector<u64>> level_consts_h;  // host copies (row-pass epilogue parameters)
+  std::map<int, std::vector<u64>> level_consts_h;
+  std::map<int, BufPtr> merged_consts;               // (q_top P)^-1 per limb count (merged relin + rescale)
+  std::map<int, std::vector<u64>> merged_consts_h;  // host copies (row-pass epilogue parameters)
 
   Ledger ledger;
   u64 enc_counter = 0;

@@ -51,6 +51,7 @@ Context::~Context() {
   conv_plans.clear();
   pt_cache.clear();
   level_consts.clear();
+  merged_consts.clear();
   sk.reset();
   tab_store.reset();
   for (auto e : events) cudaEventDestroy(e);

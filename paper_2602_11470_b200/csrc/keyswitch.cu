@@ -33,6 +33,14 @@ struct ExtB {
   const u64* ext(int s) const { return buf->p + (size_t)s * per; }
 };
 
+// one polynomial for ModDown (mod_down_polys / mod_down_rescale_polys)
+struct MdPoly {
+  const u64* acc;
+  const u64* addend;
+  u64 g;
+  u64* out;
+};
+
 void fill_conv(ConvBatch& B, Context& c, const ConvPlan& p) {
   SF_HPROF("fill_conv");
   B.nsrc = p.nsrc;
@@ -177,7 +185,105 @@ struct KsJob {
 };
 
 // Inner products + ModDown for every job (chunks of kJobs).
-void ks_jobs(Context& c, const ExtB& x, const std::vector<KsJob>& jobs) {
+// (q_top * P)^-1 mod q_l (+ Shoup), l < limbs - 1: the merged relinearise + rescale constants
+const std::vector<u64>& merged_consts(Context& c, int limbs, const u64** dev) {
+  std::lock_guard<std::mutex> lk(c.mu);
+  auto it = c.merged_consts_h.find(limbs);
+  if (it == c.merged_consts_h.end()) {
+    std::vector<u64> h(2 * (size_t)(limbs - 1));
+    const u64 qt = c.primes[limbs - 1];
+    for (int l = 0; l < limbs - 1; ++l) {
+      const u64 q = c.primes[l];
+      u64 m = qt % q;
+      for (int k = 0; k < c.alpha; ++k) m = mulmod_h(m, c.primes[c.P_index(k)] % q, q);
+      h[l] = invmod_h(m, q);
+      h[limbs - 1 + l] = shoup_h(h[l], q);
+    }
+    BufPtr b = make_buf(c, h.size());
+    SF_CUDA(cudaMemcpyAsync(b->p, h.data(), h.size() * sizeof(u64), cudaMemcpyHostToDevice, c.stream));
+    SF_CUDA(cudaStreamSynchronize(c.stream));
+    c.merged_consts[limbs] = b;
+    it = c.merged_consts_h.emplace(limbs, std::move(h)).first;
+  }
+  *dev = c.merged_consts[limbs]->p;
+  return it->second;
+}
+
+// ModDown and rescale by the top prime as one conversion:
+// out = (X_Q' - conv_{M -> Q'}(X_M)) * M^-1, M = {q_top} u P, Q' = q_0..q_{limbs-2};
+// X = [limbs + alpha][n] with the q_top and P limbs inverse-row-passed (fused
+// path) or NTT domain (generic path).
+void mod_down_rescale_polys(Context& c, int limbs, const std::vector<MdPoly>& P, bool rowpassed) {
+  SF_HPROF("mod_down_rescale_polys");
+  const size_t n = c.n;
+  const int L1 = limbs - 1;
+  std::vector<int> mp{L1}, qidx;
+  for (int k = 0; k < c.alpha; ++k) mp.push_back(c.P_index(k));
+  for (int l = 0; l < L1; ++l) qidx.push_back(l);
+  const ConvPlan& plan = conv_plan(c, mp, qidx);
+  const u64* kd = nullptr;
+  const std::vector<u64>& kh = merged_consts(c, limbs, &kd);
+  for (size_t s0 = 0; s0 < P.size(); s0 += kJobsWide) {
+    const int J = (int)std::min<size_t>(kJobsWide, P.size() - s0);
+    BufPtr conv = make_buf(c, (size_t)J * L1 * n);
+    if (fused_path(c)) {
+      require(rowpassed, kInternal, "mod_down_rescale: fused path expects row-passed inputs");
+      FusedColArgs A;
+      A.ns = (int)mp.size();
+      A.nd = L1;
+      A.set_plan(plan.tab->p, plan.nsrc, plan.ndst);
+      for (int k = 0; k < A.ns; ++k) A.src_prime[k] = mp[k];
+      for (int l = 0; l < L1; ++l) A.dst_prime[l] = l, A.out_slot[l] = l;
+      for (int j = 0; j < J; ++j) {
+        A.src[A.count] = P[s0 + j].acc + (size_t)L1 * n;
+        A.dst[A.count++] = conv->p + (size_t)j * L1 * n;
+      }
+      b_fused_col(c, A);
+      EpiBatch E;
+      for (int j = 0; j < J; ++j)
+        for (int l = 0; l < L1; ++l) {
+          E.buf[E.count] = conv->p + ((size_t)j * L1 + l) * n;
+          E.acc[E.count] = P[s0 + j].acc + (size_t)l * n;
+          E.addend[E.count] = nullptr;
+          E.out[E.count] = P[s0 + j].out + (size_t)l * n;
+          E.g[E.count] = 0;
+          E.inv[E.count] = kh[l];
+          E.inv_s[E.count] = kh[L1 + l];
+          E.prime[E.count++] = (uint8_t)l;
+          if (E.count == kJobsWide) b_row_epi(c, E), E.count = 0;
+        }
+      b_row_epi(c, E);
+      continue;
+    }
+    LimbBatch lb;
+    for (int j = 0; j < J; ++j)
+      for (size_t k = 0; k < mp.size(); ++k)
+        ntt_push(c, lb, const_cast<u64*>(P[s0 + j].acc) + (size_t)(L1 + k) * n, mp[k], true);
+    ntt_batch(c, lb, true);
+    ConvBatch cv;
+    fill_conv(cv, c, plan);
+    for (int l = 0; l < L1; ++l) cv.out_slot[l] = l;
+    for (int j = 0; j < J; ++j) {
+      cv.in[cv.count] = P[s0 + j].acc + (size_t)L1 * n;
+      cv.out[cv.count++] = conv->p + (size_t)j * L1 * n;
+    }
+    b_conv(c, cv);
+    for (int j = 0; j < J; ++j)
+      for (int l = 0; l < L1; ++l) ntt_push(c, lb, conv->p + ((size_t)j * L1 + l) * n, l, false);
+    ntt_batch(c, lb, false);
+    SubScaleBatch sb;
+    for (int j = 0; j < J; ++j) {
+      sb.acc[sb.count] = P[s0 + j].acc;
+      sb.conv[sb.count] = conv->p + (size_t)j * L1 * n;
+      sb.addend[sb.count] = nullptr;
+      sb.g[sb.count] = 0;
+      sb.out[sb.count++] = P[s0 + j].out;
+    }
+    b_subscale(c, sb, L1, kd, kd + L1);
+  }
+}
+
+void ks_jobs(Context& c, const ExtB& x, const std::vector<KsJob>& jobs, bool merged = false) {
   SF_HPROF("ks_jobs");
   const size_t n = c.n;
   const int limbs = x.limbs, nt = x.nt;
@@ -240,8 +346,18 @@ void ks_jobs(Context& c, const ExtB& x, const std::vector<KsJob>& jobs) {
         ka.ginv[k] = gi;
         ka.key[k] = get_key(c, jb.g <= 1 ? 0 : jb.g)->p;
         ka.acc[k] = accp(j, 0);
+        ka.add0[k] = jb.add0;
+        ka.add1[k] = jb.add1;
       }
       ka.job_begin[ka.nsrc] = J;
+      if (merged) {
+        ka.merged = 1;
+        for (int l = 0; l < limbs; ++l) {
+          u64 r = 1 % c.primes[l];
+          for (int k = 0; k < c.alpha; ++k) r = mulmod_h(r, c.primes[c.P_index(k)] % c.primes[l], c.primes[l]);
+          ka.pm[l] = r;
+        }
+      }
       b_ks_row(c, ka);
     }
     KsBatch kb;
@@ -260,6 +376,34 @@ void ks_jobs(Context& c, const ExtB& x, const std::vector<KsJob>& jobs) {
     }
     kb.count = J;
     if (!x.col_only) b_ks(c, kb);
+    if (merged) {
+      // X = acc + P (d0, d1) on the Q limbs, then one ModDown-and-rescale
+      std::vector<MdPoly> md;
+      if (!x.col_only) {
+        const u64* kd = nullptr;
+        (void)kd;
+        std::vector<u64> pmh(limbs);
+        for (int l = 0; l < limbs; ++l) {
+          u64 r = 1 % c.primes[l];
+          for (int k = 0; k < c.alpha; ++k) r = mulmod_h(r, c.primes[c.P_index(k)] % c.primes[l], c.primes[l]);
+          pmh[l] = r;
+        }
+        BufPtr pmd = make_buf(c, limbs);
+        SF_CUDA(cudaMemcpyAsync(pmd->p, pmh.data(), limbs * sizeof(u64), cudaMemcpyHostToDevice, c.stream));
+        AxpyBatch ab;
+        for (int j = 0; j < J; ++j)
+          for (int poly = 0; poly < 2; ++poly) {
+            ab.acc[ab.count] = accp(j, poly);
+            ab.d[ab.count++] = poly ? jobs[s0 + j].add1 : jobs[s0 + j].add0;
+          }
+        b_axpy_pm(c, ab, limbs, pmd->p);
+        SF_CUDA(cudaStreamSynchronize(c.stream));  // pmh outlives the copy (generic small-ring path only)
+      }
+      for (int j = 0; j < J; ++j)
+        for (int poly = 0; poly < 2; ++poly) md.push_back({accp(j, poly), nullptr, 0, poly ? jobs[s0 + j].out1 : jobs[s0 + j].out0});
+      mod_down_rescale_polys(c, limbs, md, x.col_only);
+      continue;
+    }
     if (fused_path(c)) {
       // ModDown of 2J polynomials: inverse row pass of the P limbs (in place),
       // fused [inverse column, P -> Q conversion, forward column], then the
@@ -351,12 +495,6 @@ void ks_jobs(Context& c, const ExtB& x, const std::vector<KsJob>& jobs) {
 // out = (acc_Q - conv_{P->Q}(acc_P)) * P^-1 (+ addend permuted by g) for
 // extended-basis polynomials acc = [nt][n]. p_rowpassed: the P limbs already
 // had ModDown's inverse row pass (fused path); otherwise they are NTT domain.
-struct MdPoly {
-  const u64* acc;
-  const u64* addend;
-  u64 g;
-  u64* out;
-};
 
 void mod_down_polys(Context& c, int limbs, const std::vector<MdPoly>& P, bool p_rowpassed) {
   SF_HPROF("mod_down_polys");
@@ -829,17 +967,15 @@ std::vector<Ct> mul_batch(Context& c, const std::vector<const Ct*>& a, const std
       ExtB x = mod_up_batch(c, d2, limbs);
       std::vector<Ct> t(J);
       std::vector<KsJob> kj;
-      for (int j = 0; j < J; ++j) {
-        t[j] = alloc_ct(c, limbs, a[idx[s0 + j]]->scale * b[idx[s0 + j]]->scale);
+      for (int j = 0; j < J; ++j) {  // relinearise + rescale in one conversion
+        t[j] = alloc_ct(c, limbs - 1,
+                        a[idx[s0 + j]]->scale * b[idx[s0 + j]]->scale / (double)c.primes[limbs - 1]);
         kj.push_back({j, 0, dp(j, 0), dp(j, 1), t[j].c0(), t[j].c1(c.n)});
       }
-      ks_jobs(c, x, kj);
-      std::vector<const Ct*> tp;
-      for (auto& z : t) tp.push_back(&z);
-      auto r = rescale_batch(c, tp);
+      ks_jobs(c, x, kj, true);
       for (int j = 0; j < J; ++j) {
-        r[j].layout = merge_layouts(*a[idx[s0 + j]], *b[idx[s0 + j]]);
-        out[idx[s0 + j]] = std::move(r[j]);
+        t[j].layout = merge_layouts(*a[idx[s0 + j]], *b[idx[s0 + j]]);
+        out[idx[s0 + j]] = std::move(t[j]);
       }
     }
   }
@@ -918,9 +1054,9 @@ Ct relin_rescale(Context& c, const Ct3& x) {
   if (x.zero) return zeros(c, x.d01.level() - 1);
   const int limbs = std::min(x.d01.limbs, x.d2.limbs);
   ExtB e = mod_up_batch(c, {x.d2.c0()}, limbs);
-  Ct t = alloc_ct(c, limbs, x.d01.scale);
-  ks_jobs(c, e, {KsJob{0, 0, x.d01.c0(), x.d01.c1(c.n), t.c0(), t.c1(c.n)}});
-  return rescale(c, t);
+  Ct t = alloc_ct(c, limbs - 1, x.d01.scale / (double)c.primes[limbs - 1]);
+  ks_jobs(c, e, {KsJob{0, 0, x.d01.c0(), x.d01.c1(c.n), t.c0(), t.c1(c.n)}}, true);
+  return t;
 }
 
 // ------------------------------------------------------------- ct x pt mult

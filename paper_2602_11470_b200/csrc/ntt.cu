@@ -389,6 +389,20 @@ __global__ void __launch_bounds__(kWarps * 32, 2) ks_row_kernel(KsRowArgs A, Tab
         mac128(sa[k + 1], x1, va.y);
       }
     }
+    if (A.merged && t < A.limbs) {  // + P * (d0, d1): the relinearised pair in the extended basis
+      const u64 pmt = A.pm[t];
+      const u64* a0 = A.add0[jb] + (size_t)t * n + rowoff;
+      const u64* a1 = A.add1[jb] + (size_t)t * n + rowoff;
+#pragma unroll
+      for (int k = 0; k < E; k += 2) {
+        const ulonglong2 v0 = reinterpret_cast<const ulonglong2*>(a0)[k / 2];
+        const ulonglong2 v1 = reinterpret_cast<const ulonglong2*>(a1)[k / 2];
+        mac128(sb[k], v0.x, pmt);
+        mac128(sb[k + 1], v0.y, pmt);
+        mac128(sa[k], v1.x, pmt);
+        mac128(sa[k + 1], v1.y, pmt);
+      }
+    }
     u64 vb[E], va[E];
 #pragma unroll
     for (int k = 0; k < E; ++k) {
@@ -397,7 +411,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) ks_row_kernel(KsRowArgs A, Tab
     }
     u64* accb = A.acc[jb] + (size_t)t * n;
     u64* acca = A.acc[jb] + (size_t)(A.nt + t) * n;
-    if (t < A.limbs) {
+    if (t < A.limbs && !(A.merged && t == A.limbs - 1)) {
 #pragma unroll
       for (int k = 0; k < E; k += 2) {
         reinterpret_cast<ulonglong2*>(accb + rowoff)[k / 2] = make_ulonglong2(vb[k], vb[k + 1]);
