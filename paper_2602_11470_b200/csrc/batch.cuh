@@ -188,7 +188,7 @@ bool ntt_row_epi(Context& c, const EpiBatch& e);
 bool ntt_fused_col(Context& c, const FusedColArgs& a);
 bool ntt_ks_row(Context& c, const KsRowArgs& a);
 bool ntt_ks_sum(Context& c, const KsSumArgs& a);
-inline bool fused_path(const Context& c) { return c.logn >= 12 && c.logn <= 17 && c.alpha <= 8; }
+inline bool fused_path(const Context& c) { return c.logn >= 12 && c.logn <= 17 && c.alpha <= 7; }
 // profiled launch wrappers (batch.cu)
 void b_row(Context& c, const LimbBatch& b, bool inverse);
 void b_fused_col(Context& c, const FusedColArgs& A);

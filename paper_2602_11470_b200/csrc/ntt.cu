@@ -238,6 +238,7 @@ __global__ void __launch_bounds__(TCF * 32, TCF == 8 ? 3 : 8) fused_col_kernel(F
     for (int k = 0; k < E; ++k) x[k] = sm[swz(lane + 32 * k)];
     __syncwarp();
     warp_inv<LOGR>(x, sm, lane, q, tw);
+    // canonical y_s: the basis conversion's [x q^_s^-1]_{q_s} (and the centred lift) need it
     const u64 ym = A.mode == 0 ? A.ymul[s] : T.ninv[p], yms = A.mode == 0 ? A.ymul_s[s] : T.ninv_s[p];
 #pragma unroll
     for (int k = 0; k < E; ++k) sm[swz(lane + 32 * k)] = mul_shoup(x[k], ym, yms, q);
@@ -254,18 +255,19 @@ __global__ void __launch_bounds__(TCF * 32, TCF == 8 ? 3 : 8) fused_col_kernel(F
 #pragma unroll
       for (int s = 0; s < 8; ++s)
         if (s < A.ns) h[s] = A.qhat[(size_t)s * A.nd + d], hs[s] = A.qhat_s[(size_t)s * A.nd + d];
-      const u64 q2 = 2 * q;
+      // the forward column NTT accepts [0, 4q): the ns lazy Shoup products (each
+      // in [0, 2q), q < 2^60) are summed and brought below 4q only as needed
+      const u64 q4 = 4 * q, q8 = 8 * q;
       for (int e = threadIdx.x; e < R * TCF; e += NT) {
         const int row = e / TCF, col = e - row * TCF;
         const int r = swz(row);
-        u64 acc = 0;  // sum of lazy Shoup products, kept in [0, 2q)
+        u64 acc = 0;
 #pragma unroll
         for (int s = 0; s < 8; ++s)
-          if (s < A.ns) {
-            acc += mul_shoup_lazy(region(s, col)[r], h[s], hs[s], q);
-            acc = acc >= q2 ? acc - q2 : acc;
-          }
-        out[(size_t)col * PAD + r] = acc >= q ? acc - q : acc;
+          if (s < A.ns) acc += mul_shoup_lazy(region(s, col)[r], h[s], hs[s], q);
+        if (A.ns > 4) acc = acc >= q8 ? acc - q8 : acc;
+        if (A.ns > 2) acc = acc >= q4 ? acc - q4 : acc;
+        out[(size_t)col * PAD + r] = acc;
       }
     } else {  // rescale lift: centred x mod q_last reduced mod each destination prime
       const u64 mh = T.mh[pd];
