@@ -368,16 +368,25 @@ def main():
     lib.sf_profile_end(be.ctx, ms, by, nl)
     bf = (C.c_double * 6)()
     lib.sf_profile_butterflies(be.ctx, bf)
-    fams = ["ntt", "keyswitch_inner", "ctpt_mac", "basis_conv", "elementwise", "sampling"]
+    # families: 0 row passes (plain / epilogue), 1 key-switch row stages (ks_row, ks_sum),
+    # 2 MACs, 3 fused column stages (ModUp / ModDown / rescale conversions), 4 elementwise, 5 sampling
+    fams = ["ntt_rows", "keyswitch_rows", "ctpt_mac", "fused_col", "elementwise", "sampling"]
     prof = {f: {"ms_per_step": ms[i] / args.steps, "launches_per_step": nl[i] / args.steps,
                 "GBps": (by[i] / (ms[i] * 1e-3) / 1e9) if ms[i] > 0 else None} for i, f in enumerate(fams)}
     dom = max(range(6), key=lambda i: ms[i])
     P = peaks()
     peak = P.get("hbm_gbs", 6650.0)
     achieved = by[dom] / (ms[dom] * 1e-3) / 1e9 if ms[dom] > 0 else 0.0
+    traffic = None
+    try:  # ncu DRAM bytes per launch of the same family (profiles/r1_traffic.json, tools/traffic.py)
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "r1_traffic.json")))["families"][fams[dom]][
+            "dram_bytes_per_launch"]
+    except Exception:
+        pass
     roofline = {"bound": "hbm", "kernel": fams[dom], "achieved": round(achieved, 1), "peak": peak,
                 "unit": "GB/s", "frac": round(achieved / peak, 4),
-                "traffic": None, "peak_source": "measured" if not P.get("_fallback") else "fallback",
+                "traffic": traffic, "traffic_source": "profiles/r1_traffic.json (ncu launch list, same family)",
+                "peak_source": "measured" if not P.get("_fallback") else "fallback",
                 "algorithmic_bytes_per_launch": by[dom] / max(nl[dom], 1),
                 "avg_launch_us": ms[dom] * 1e3 / max(nl[dom], 1)}
 
@@ -387,10 +396,10 @@ def main():
         bpk = json.load(open(os.path.join(ROOT, "profiles", "r1_butterfly_peak.json")))["exact_shoup_G_butterflies_per_s"]
     except Exception:
         bpk = None
-    nt_ms = ms[0] + ms[1]
-    bf_tot = bf[0] + bf[1]
+    nt_ms = ms[0] + ms[1] + ms[3]
+    bf_tot = bf[0] + bf[1] + bf[3]
     int_roofline = {"bound": "int (FMA-heavy pipe: 64-bit IMAD of the Shoup butterflies)",
-                    "kernels": "ntt + keyswitch_inner families",
+                    "kernels": "ntt_rows + keyswitch_rows + fused_col families",
                     "butterflies_per_step": bf_tot / args.steps,
                     "achieved": round(bf_tot / (nt_ms * 1e-3) / 1e9, 1) if nt_ms > 0 else None,
                     "peak": bpk, "unit": "G butterfly/s",

@@ -366,7 +366,7 @@ void b_row(Context& c, const LimbBatch& b, bool inverse) {
 void b_fused_col(Context& c, const FusedColArgs& A) {
   SF_HPROF("b_fused_col");
   if (!A.count) return;
-  ProfScope prof(c, kFamNtt, 8.0 * c.n * (A.ns + A.nd) * A.count, half_bfly(c, true) * (A.ns + A.nd) * A.count);
+  ProfScope prof(c, kFamConv, 8.0 * c.n * (A.ns + A.nd) * A.count, half_bfly(c, true) * (A.ns + A.nd) * A.count);
   ntt_fused_col(c, A);
   post(c);
 }

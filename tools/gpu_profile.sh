@@ -3,7 +3,7 @@
 #   gpurun -- bash tools/gpu_profile.sh TAG [K]
 TAG=$1; K=${2:-5}
 OUT=gpurun_out/$TAG; mkdir -p $OUT
-timeout 900 ncu --nvtx --nvtx-include "sf_step/" --metrics gpu__time_duration.sum --clock-control none \
+timeout 900 ncu --nvtx --nvtx-include "sf_step/" --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     --csv --log-file $OUT/launches.csv python bench.py --nvtx-step --warmup 3 --no-cpu-baseline > $OUT/ncu_launch.log 2>&1
 echo "launch list rc=$?"
 SPECS=$(python tools/pick_launches.py $OUT/launches.csv $K); echo "picked: $SPECS"
