@@ -8,3 +8,4 @@ timeout 900 ncu --nvtx --nvtx-include "sf_step/" --metrics gpu__time_duration.su
 echo "launch list rc=$?"
 SPECS=$(python tools/pick_launches.py $OUT/launches.csv $K); echo "picked: $SPECS"
 bash tools/ncu_big.sh $TAG "$SPECS"
+python tools/traffic.py $OUT/launches.csv > $OUT/traffic.json

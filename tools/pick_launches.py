@@ -7,6 +7,8 @@ path, k = sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 5
 rows = [r for r in csv.reader(open(path)) if len(r) > 10]
 h = rows[0]
 ki, gi, vi = h.index("Kernel Name"), h.index("Grid Size"), h.index("Metric Value")
+mi = h.index("Metric Name")
+rows = [rows[0]] + [r for r in rows[1:] if r[mi] == "gpu__time_duration.sum"]
 tot, idx, best = collections.Counter(), collections.Counter(), {}
 for r in rows[1:]:
     name = r[ki].split("(")[0].split("::")[-1].split("<")[0]
