@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(TCF * 32, TCF == 8 ? 3 : 8) fused_col_kernel(F
   constexpr int PAD = R + 1;
   constexpr int tiles = C / TCF;
   constexpr int NT = TCF * 32;
-  extern __shared__ u64 sm_all[];  // [ns][TCF][PAD] sources, [2][TCF][PAD] destinations
+  extern __shared__ u64 sm_all[];  // [ns][TCF][PAD] sources, [TCF][PAD] destination
   // blockIdx.x = (job * dgroups + dgroup) * tiles + tile; a CTA converts the
   // destinations [dgroup * dpc, +dpc) (dpc = nd: all of them)
   const int dpc = A.d_per_cta > 0 ? A.d_per_cta : A.nd;
@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(TCF * 32, TCF == 8 ? 3 : 8) fused_col_kernel(F
   for (int d = d_lo; d < d_hi; ++d) {
     const int pd = A.dst_prime[d];
     const u64 q = T.q[pd];
-    u64* out = region(A.ns + (d & 1), 0);
+    u64* out = region(A.ns, 0);
     // 3. conversion (coefficient domain) into destination tile d & 1
     if (A.mode == 0) {
       u64 h[8], hs[8];
@@ -300,13 +300,14 @@ __global__ void __launch_bounds__(TCF * 32, TCF == 8 ? 3 : 8) fused_col_kernel(F
       for (int k = 0; k < E; ++k) sm[swz(lane + 32 * k)] = x[k];
     }
     __syncthreads();
-    // 5. store (lazy [0, 4q) values; the row pass accepts them). The next
-    //    destination converts into the other tile, so no barrier is needed here.
+    // 5. store (lazy [0, 4q) values; the row pass accepts them); one
+    //    destination tile, so the next conversion waits for the stores
     u64* o = dst + (size_t)A.out_slot[d] * n + col0;
     for (int e = threadIdx.x; e < R * TCF; e += NT) {
       const int row = e / TCF, col = e - row * TCF;
       o[(size_t)row * C + col] = out[(size_t)col * PAD + swz(row)];
     }
+    if (d + 1 < d_hi) __syncthreads();
   }
 }
 
@@ -602,7 +603,7 @@ void run_epi(Context& c, const EpiBatch& e) {
 template <int LOGR, int LOGC, int TCF>
 void run_fused_t(Context& c, const FusedColArgs& a) {
   constexpr int R = 1 << LOGR;
-  const size_t sm = (size_t)(a.ns + 2) * TCF * (R + 1) * sizeof(u64);
+  const size_t sm = (size_t)(a.ns + 1) * TCF * (R + 1) * sizeof(u64);
   static int configured = 0;
   if (!configured) {
     SF_CUDA(cudaFuncSetAttribute(fused_col_kernel<LOGR, LOGC, TCF>, cudaFuncAttributeMaxDynamicSharedMemorySize,

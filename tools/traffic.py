@@ -10,7 +10,8 @@ import sys
 FAMILY = {"ntt_row_pass": "ntt_rows", "ntt_row_epi": "ntt_rows", "ks_row_kernel": "keyswitch_rows",
           "ks_sum_kernel": "keyswitch_rows", "fused_col_kernel": "fused_col", "vmm_mac_kernel": "ctpt_mac",
           "tensor_sum_kernel": "ctpt_mac", "mulpt_batch_kernel": "ctpt_mac", "mac_kernel": "ctpt_mac"}
-UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3}
+UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3,
+        "ns": 1e-9, "us": 1e-6, "ms": 1e-3}
 rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 10]
 h = rows[0]
 ki, ii, mi, vi, ui = (h.index(x) for x in ("Kernel Name", "ID", "Metric Name", "Metric Value", "Metric Unit"))
