@@ -505,3 +505,205 @@ def exact_softmax_maps(be, maps, cfg, n_prime):
         for i in v:
             out[i // gt][h * gt + i % gt] = p[i]
     return [be.exact_transform(m, (lambda _s, o=o: o)) for m, o in zip(maps, out)]
+
+
+# --------------------------------------------------------------------- prefill
+# kv_attention.cpp:119-129, 245-376, 414-454 and vmm.cpp:30-43, 417-467: the
+# step before decode, which builds the KV cache a decode step consumes.
+
+def inner_rotate(be, x, r, block, hoisted=False):
+    """vmm.cpp:30-43: cyclic rotation by r inside every block of `block` slots."""
+    N = be.N
+    if block <= 0 or N % block:
+        raise ShapeMismatch("inner_rotate: block must divide N")
+    s = r % block
+    if s == 0:
+        return x
+    i = np.arange(N)
+    keep = (i % block < block - s).astype(np.float64)
+    lo = be.mul_plain(be.rotate(x, s, hoisted), keep)
+    hi = be.mul_plain(be.rotate(x, s - block, hoisted), 1.0 - keep)
+    return be.add(lo, hi)
+
+
+def batch_plain(W: np.ndarray, d: int, N: int, j: int, pre: int) -> np.ndarray:
+    """vmm.cpp:426-433: slot i of the j-th token-batched diagonal, pre-shifted by pre."""
+    t = N // d
+    e = ((np.arange(N) - pre) % N) // t
+    r = (e + j) % d
+    rows, cols = W.shape
+    out = np.zeros(N)
+    ok = (r < rows) & (e < cols)
+    out[ok] = W[r[ok], e[ok]]
+    return out
+
+
+def vmm_batch(be, x, W: np.ndarray, bsgs: bool = True):
+    """vmm.cpp:417-467: square VMM over a token batch (lane tau = token tau)."""
+    N = be.N
+    if x.layout is None or x.layout.kind != "interleaved":
+        raise LayoutMismatch("vmm_batch: input must carry an interleaved layout")
+    if x.layout.deferred_mask:
+        raise LayoutMismatch("vmm_batch: input garbage must be cleared first")
+    W = np.asarray(W, dtype=np.float64)
+    d = padded_dim(W.shape[0])
+    if padded_dim(W.shape[1]) != d:
+        raise ShapeMismatch("vmm_batch: square weights only")
+    if x.layout.d != d:
+        raise ShapeMismatch("vmm_batch: layout/weight dimension mismatch")
+    t = N // d
+    if not bsgs:
+        acc = be.mac_plain([(be.rotate(x, j * t), batch_plain(W, d, N, j, 0)) for j in range(d)])
+    else:
+        b, giants = bsgs_split(d)
+        baby = [x] + [be.rotate(x, g1 * t, hoisted=True) for g1 in range(1, b)]
+        partials = []
+        for g2 in range(giants):
+            shift = g2 * b * t
+            terms = [(baby[g1], batch_plain(W, d, N, g2 * b + g1, shift)) for g1 in range(b) if g2 * b + g1 < d]
+            partials.append((be.mac_plain(terms), shift))
+        acc = None  # giant alignment + sum, grouped as in vmm_interleaved (DESIGN.md §3.8)
+        for r in range(min(GIANT_GROUPS, giants)):
+            grp = be.rot_sum(partials[r::GIANT_GROUPS])
+            acc = grp if acc is None else be.add(acc, grp)
+    return be.with_layout(acc, Layout("interleaved", d, t, 0, 1, False))
+
+
+def rope_batch_plain(which: int, cfg, first_pos: int, base: float = 10000.0) -> np.ndarray:
+    """kv_attention.cpp:59-76: lane tau carries position first_pos + tau."""
+    N, t, dh = cfg.N, cfg.t, cfg.d_head
+    i = np.arange(N)
+    e = (i // t) % dh
+    pair = e // 2
+    angle = (first_pos + i % t).astype(np.float64) * np.power(base, -2.0 * pair / dh)
+    if which == 0:
+        return np.cos(angle)
+    p = np.zeros(N)
+    m = (e % 2 == 0) if which == 1 else (e % 2 == 1)
+    p[m] = np.sin(angle[m]) if which == 1 else -np.sin(angle[m])
+    return p
+
+
+def rope_apply_batch(be, x, cfg, first_pos, base=10000.0):
+    """kv_attention.cpp:119-129."""
+    _require_clean_interleaved(x, cfg, 0, "rope_apply_batch")
+    if cfg.d_head % 2:
+        raise ShapeMismatch("rope_apply_batch: d_head must be even")
+    s = cfg.t
+    y = be.mul_plain(x, rope_batch_plain(0, cfg, first_pos, base))
+    y = be.add(y, be.rotate(be.mul_plain(x, rope_batch_plain(1, cfg, first_pos, base)), -s))
+    y = be.add(y, be.rotate(be.mul_plain(x, rope_batch_plain(2, cfg, first_pos, base)), s))
+    return be.with_layout(y, x.layout)
+
+
+def prefill(be, x_prompt, Wq, Wk, Wv, cfg, softmax_fn, rope_base=10000.0):
+    """kv_attention.cpp:245-376. Returns (attention cts, KVCache)."""
+    t, dh, gt, N, n0 = cfg.t, cfg.d_head, cfg.group_tokens, cfg.N, cfg.n0
+    if n0 < 1:
+        raise ShapeMismatch("prefill: need a nonempty prompt")
+    if n0 > cfg.n_max:
+        raise CacheFull("prefill: prompt exceeds cache capacity")
+    P = _ceil_div(n0, t)
+    if len(x_prompt) != P:
+        raise ShapeMismatch(f"prefill: expected {P} prompt cts, got {len(x_prompt)}")
+    cache = KVCache()
+    q_cts = []
+    for p in range(P):
+        q_cts.append(rope_apply_batch(be, vmm_batch(be, x_prompt[p], Wq), cfg, p * t, rope_base))
+        cache.k_cts.append(rope_apply_batch(be, vmm_batch(be, x_prompt[p], Wk), cfg, p * t, rope_base))
+    for p in range(P):
+        v_raw = vmm_batch(be, x_prompt[p], Wv)
+        g = (p * t) // gt
+        u_cap = p - g * dh
+        if g == len(cache.v_cts):
+            z = be.zeros()
+            cache.v_cts.append([z] * v_variant_count(cfg))
+        for e in range(dh):
+            m = np.zeros(N)
+            for h in range(cfg.H):
+                m[(h * dh + e) * t:(h * dh + e + 1) * t] = 1.0
+            piece = be.mul_plain(v_raw, m)
+            idx = v_variant_index(cfg, v_variant_of(cfg, e, u_cap * t))
+            cache.v_cts[g][idx] = be.add(cache.v_cts[g][idx], piece)
+    cache.n_prime = n0
+    k_rot = [[cache.k_cts[j]] + [inner_rotate(be, cache.k_cts[j], rho, t) for rho in range(1, t)] for j in range(P)]
+    acc = [[[None] * t for _ in range((p * t) // gt + 1)] for p in range(P)]
+    for p in range(P):
+        for j in range(p + 1):
+            g_key, local = (j * t) // gt, (j * t) % gt
+            for rho in range(t):
+                m = np.zeros(N)
+                any_ = False
+                for tau in range(t):
+                    key, query = j * t + (tau + rho) % t, p * t + tau
+                    if key <= query and key < n0 and query < n0:
+                        for h in range(cfg.H):
+                            m[h * gt + tau] = 1.0
+                        any_ = True
+                if not any_:
+                    continue
+                prod = be.mul(q_cts[p], k_rot[j][rho])
+                prod = fold_within_head(be, prod, dh, t)
+                masked = be.mul_plain(prod, m)
+                packed = be.rotate(masked, -local) if local else masked
+                cell = acc[p][g_key][rho]
+                acc[p][g_key][rho] = packed if cell is None else be.add(cell, packed)
+    maps = []
+    for p in range(P):
+        rows = []
+        for g in range(len(acc[p])):
+            ref_level = acc[p][g][0].level
+            rows.append([be.with_layout(c if c is not None else be.zeros(ref_level), None) for c in acc[p][g]])
+        maps.append(rows)
+    probs = softmax_fn(be, maps, cfg, n0)
+    if len(probs) != len(maps):
+        raise ShapeMismatch("prefill: softmax changed the map shape")
+    groups = len(cache.v_cts)
+    v_rot = []
+    for g in range(groups):
+        tokens = min(gt, n0 - g * gt)
+        lo, hi = touched_variants(cfg, tokens)
+        rows = []
+        for w in range(lo, hi):
+            base_ct = cache.v_cts[g][v_variant_index(cfg, w)]
+            rows.append([base_ct] + [inner_rotate(be, base_ct, rho, t) for rho in range(1, t)])
+        v_rot.append((lo, rows))
+    att = []
+    for p in range(P):
+        pairs = []
+        for g in range(len(probs[p])):
+            tokens = min(gt, n0 - g * gt)
+            lo, hi = touched_variants(cfg, tokens)
+            for rho in range(t):
+                pm = probs[p][g][rho]
+                for w in range(lo, hi):
+                    scores = be.rotate(pm, -w * t) if w else pm
+                    pairs.append((scores, v_rot[g][1][w - lo][rho]))
+        # sum of the products (kv_attention.cpp:358-368); CKKS backends relinearise
+        # once (DESIGN.md §3.6), charged as the reference's mul/add chain
+        a = be.mul_sum(pairs)
+        att.append(be.with_layout(a, make_interleaved(cfg.d, N, 0, cfg.H)))
+    return att, cache
+
+
+def exact_softmax_prefill_maps(be, maps, cfg, n0):
+    """kv_attention.cpp:414-454: oracle softmax over the packed prefill maps."""
+    t, gt = cfg.t, cfg.group_tokens
+    slots = [[[be.decrypt(c) for c in row] for row in mp] for mp in maps]
+    out = [[[np.zeros(cfg.N) for _ in range(t)] for _ in mp] for mp in maps]
+    for p in range(len(maps)):
+        for tau in range(t):
+            query = p * t + tau
+            if query >= n0:
+                continue
+            for h in range(cfg.H):
+                ks = np.arange(query + 1)
+                g = ks // gt
+                rho = (ks % t - tau) % t
+                pos = h * gt + (ks - g * gt) // t * t + tau
+                sc = np.array([slots[p][g[i]][rho[i]][pos[i]] for i in range(len(ks))])
+                pr = plain_softmax(sc)
+                for i in range(len(ks)):
+                    out[p][g[i]][rho[i]][pos[i]] = pr[i]
+    return [[[be.exact_transform(c, (lambda _s, o=out[p][g][r]: o)) for r, c in enumerate(row)]
+             for g, row in enumerate(mp)] for p, mp in enumerate(maps)]

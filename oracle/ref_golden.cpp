@@ -10,6 +10,8 @@
 //   k_append / make_v_pieces / v_append   proj/src/kv_attention.cpp:131-182
 //   qk_dot / softmax_times_v   proj/src/kv_attention.cpp:184-241
 //   exact_softmax_maps         proj/src/kv_attention.cpp:395-412
+//   prefill (vmm_batch, rope_apply_batch, inner_rotate, exact_softmax_prefill_maps)
+//                              proj/src/kv_attention.cpp:119-129, 245-376, 414-454; vmm.cpp:30-43, 417-467
 #include <nlohmann/json.hpp>
 
 #include <cstdio>
@@ -200,6 +202,49 @@ json attn_case(int N, int d, int H, int np, unsigned seed) {
               {"sv_counts", counts_json(be.ledger().phase_totals("Score*V"))}};
 }
 
+// Prefill of an n0-token prompt (kv_attention.cpp:245-376) with the exact
+// softmax hook, as in test_kv.cpp:360-428.
+json prefill_case(int N, int d, int H, int n0, unsigned seed) {
+  const int L = 10;
+  const int t = N / d;
+  AttentionConfig cfg{N, d, H, n0, std::max(n0, 16)};
+  SimBackend be({N, L});
+  validate_attention_config(cfg, N);
+  std::mt19937_64 rng(seed);
+  Matrix Wq = random_matrix(rng, d, d), Wk = random_matrix(rng, d, d), Wv = random_matrix(rng, d, d);
+  MatrixWeight wq(Wq), wk(Wk), wv(Wv);
+  Matrix X = random_matrix(rng, n0, d);
+  const int P = (n0 + t - 1) / t;
+  std::vector<Ciphertext> xs;
+  json xj = json::array();
+  for (int p = 0; p < P; ++p) {
+    SlotVector sl = SlotVector::Zero(N);
+    for (int tau = 0; tau < t && p * t + tau < n0; ++tau)
+      for (int E = 0; E < d; ++E) sl[E * t + tau] = X(p * t + tau, E);
+    xj.push_back(sv_json(sl));
+    xs.push_back(be.encrypt(std::move(sl), -1, make_interleaved(d, N, 0, H)));
+  }
+  PrefillResult pre = prefill(be, xs, {wq, wk, wv, 10000.0}, cfg,
+                              [](Backend& b, const PrefillMaps& m, const AttentionConfig& c, int n) {
+                                return exact_softmax_prefill_maps(b, m, c, n);
+                              });
+  json k_cts = json::array();
+  for (const auto& c : pre.cache.k_cts) k_cts.push_back(json{{"slots", sv_json(c.slots)}, {"level", c.level}});
+  json v_cts = json::array();
+  for (const auto& grp : pre.cache.v_cts) {
+    json g = json::array();
+    for (const auto& c : grp) g.push_back(json{{"slots", sv_json(c.slots)}, {"level", c.level}});
+    v_cts.push_back(g);
+  }
+  json att = json::array();
+  for (const auto& a : pre.attention)
+    att.push_back(json{{"slots", sv_json(a.slots)}, {"level", a.level}, {"layout", layout_json(a.layout)}});
+  return json{{"kind", "prefill"}, {"N", N}, {"L", L}, {"d", d}, {"H", H}, {"n0", n0},
+              {"Wq", m_json(Wq)}, {"Wk", m_json(Wk)}, {"Wv", m_json(Wv)}, {"X", m_json(X)},
+              {"x_prompt", xj}, {"k_cts", k_cts}, {"v_cts", v_cts}, {"attention", att},
+              {"n_prime", pre.cache.n_prime}, {"counts", counts_json(be.ledger().totals())}};
+}
+
 json engine_case() {
   SimBackend be({4, 3});
   SlotVector a(4);
@@ -249,6 +294,11 @@ int main(int argc, char** argv) {
         for (int np : {1, 5, 13}) cases.push_back(attn_case(64, d, H, np, seed++));
     cases.push_back(attn_case(256, 64, 4, 21, seed++));
     cases.push_back(vmm_case(256, 256, 256, 0, 0, true, false, seed++));  // t = 1 edge
+    // prefill shapes of test_kv.cpp:360-428 and a 1-token prompt (430-459)
+    cases.push_back(prefill_case(16, 4, 2, 6, seed++));
+    cases.push_back(prefill_case(16, 8, 2, 11, seed++));
+    cases.push_back(prefill_case(16, 4, 1, 1, seed++));
+    cases.push_back(prefill_case(64, 16, 4, 13, seed++));
   } else if (which == "medium") {
     // N = 2048 slots (ring degree 4096): the GPU parity size
     cases.push_back(vmm_case(2048, 64, 64, 0, 0, true, false, 7001));
@@ -258,6 +308,7 @@ int main(int argc, char** argv) {
     cases.push_back(rope_case(2048, 128, 32, 5, 77, 7005));
     cases.push_back(attn_case(2048, 128, 4, 40, 7006));
     cases.push_back(attn_case(2048, 64, 1, 70, 7007));
+    cases.push_back(prefill_case(2048, 256, 4, 19, 7008));
   }
   std::cout << json{{"generator", "oracle/ref_golden.cpp over /root/reference/proj/src (unmodified)"},
                     {"set", which},

@@ -144,3 +144,21 @@ def test_rope_protocol_decrypts_to_reference():
         y = P.fused_extract(be, x, "rope", dict(n=c["pos"], d_head=c["d_head"], s=ly.t))
         assert np.max(np.abs(be.decrypt(y) - np.array(c["y_slots"]))) < 1e-5
         assert counts_dict(be.ledger.totals()) == c["counts"]
+
+
+def test_prefill_replays_decrypt_to_reference_goldens():
+    # kv_attention.cpp:245-376 on real CKKS: cache entries and attention outputs
+    # decrypt to the reference's slot vectors, counts and levels exact
+    from test_oracle_golden import replay_prefill
+    for c in cases("small", "prefill"):
+        be = CkksOracle(c["N"], c["L"], alpha=3)
+        att, cache = replay_prefill(be, c)
+        for got, want in zip(cache.k_cts, c["k_cts"]):
+            assert np.max(np.abs(be.decrypt(got) - np.array(want["slots"]))) < TOL and got.level == want["level"]
+        for gg, gw in zip(cache.v_cts, c["v_cts"]):
+            for got, want in zip(gg, gw):
+                assert np.max(np.abs(be.decrypt(got) - np.array(want["slots"]))) < TOL
+        for got, want in zip(att, c["attention"]):
+            assert np.max(np.abs(be.decrypt(got) - np.array(want["slots"]))) < 1e-5
+            assert got.level == want["level"] and got.layout == layout_from(want["layout"])
+        assert counts_dict(be.ledger.totals()) == c["counts"]

@@ -131,3 +131,38 @@ def test_paper_scale_counts():
     for k, bg in {1: (1, 1), 2: (2, 1), 4: (2, 2), 5: (3, 2), 128: (12, 11), 512: (23, 23),
                   4096: (64, 64)}.items():
         assert P.bsgs_split(k) == bg
+
+
+def replay_prefill(be, c):
+    """oracle/ref_golden.cpp:prefill_case through the restated prefill."""
+    N, L, d, H, n0 = c["N"], c["L"], c["d"], c["H"], c["n0"]
+    cfg = P.AttentionConfig(N, d, H, n0, max(n0, 16))
+    P.validate_attention_config(cfg, N)
+    W = [np.array(c[k]).reshape(d, d) for k in ("Wq", "Wk", "Wv")]
+    xs = [be.encrypt(np.array(s), L, make_interleaved(d, N, 0, H)) for s in c["x_prompt"]]
+    att, cache = P.prefill(be, xs, W[0], W[1], W[2], cfg, P.exact_softmax_prefill_maps)
+    return att, cache
+
+
+@pytest.mark.parametrize("which", ["small", "medium"])
+def test_prefill_cases_match_reference(which):
+    cs = cases(which, "prefill")
+    assert len(cs) >= (4 if which == "small" else 1)
+    for c in cs:
+        be = SimBackend(c["N"], c["L"])
+        att, cache = replay_prefill(be, c)
+        assert cache.n_prime == c["n_prime"]
+        assert len(cache.k_cts) == len(c["k_cts"])
+        for got, want in zip(cache.k_cts, c["k_cts"]):
+            assert np.max(np.abs(got.slots - np.array(want["slots"]))) < 1e-9 and got.level == want["level"]
+        assert [len(g) for g in cache.v_cts] == [len(g) for g in c["v_cts"]]
+        for gg, gw in zip(cache.v_cts, c["v_cts"]):
+            for got, want in zip(gg, gw):
+                assert np.max(np.abs(got.slots - np.array(want["slots"]))) < 1e-9
+        assert len(att) == len(c["attention"])
+        for got, want in zip(att, c["attention"]):
+            w = np.array(want["slots"])
+            assert np.max(np.abs(got.slots - w)) < 1e-9
+            assert np.all(got.slots[w == 0.0] == 0.0)
+            assert got.level == want["level"] and got.layout == layout_from(want["layout"])
+        assert counts_dict(be.ledger.totals()) == c["counts"]
