@@ -172,6 +172,26 @@ sf_status sf_vmm_interleaved(sf_context* ctx, const sf_ct* x, const sf_vmm_plan*
 sf_status sf_vmm_interleaved_multi(sf_context* ctx, const sf_ct* x, sf_vmm_plan* const* plans, int k,
                                    int mask_output, sf_ct** outs);
 
+/* ---- prefill (kv_attention.hpp:111-150; kv_attention.cpp:245-376) -------------
+   vmm_batch (vmm.cpp:417-467) with its own plan type (token-batched square
+   diagonals), inner_rotate (vmm.cpp:30-43), rope_apply_batch (kv_attention.cpp:
+   119-129). The reference's prefill takes a softmax callback; across the ABI it
+   is split at that callback: sf_prefill_scores returns the cache (slot-identical
+   to sequential appends) and the score maps flattened in [p][g][rho] order
+   (g < p*t/(N/H) + 1, rho < t); the caller applies its softmax and hands the
+   probability maps, same order and count, to sf_prefill_attend. */
+sf_status sf_vmm_batch_plan_create(sf_context* ctx, const double* W, int rows, int cols, int level, int bsgs,
+                                   sf_vmm_plan** out);
+sf_status sf_vmm_batch(sf_context* ctx, const sf_ct* x, sf_vmm_plan* plan, sf_ct** out);
+sf_status sf_inner_rotate(sf_context* ctx, const sf_ct* x, int r, int block, int hoisted, sf_ct** out);
+sf_status sf_rope_apply_batch(sf_context* ctx, const sf_ct* x, int d, int H, long long first_pos, double base,
+                              sf_ct** out);
+sf_status sf_prefill_scores(sf_context* ctx, const sf_ct* const* xs, int P, sf_vmm_plan* wq, sf_vmm_plan* wk,
+                            sf_vmm_plan* wv, int d, int H, int n0, int n_max, double base, sf_kvcache** cache_out,
+                            sf_ct** maps_out, int maps_cap, int* n_maps);
+sf_status sf_prefill_attend(sf_context* ctx, const sf_ct* const* probs, int n_probs, const sf_kvcache* cache,
+                            sf_ct** att_out, int att_cap, int* n_att);
+
 /* --- KV-cache attention (kv_attention.hpp:32-109) --------------------------- */
 /* AttentionConfig{N = slots, d, H, n0, n_max}; validate_attention_config */
 sf_status sf_kv_create(sf_context* ctx, int d, int H, int n0, int n_max, sf_kvcache** out);

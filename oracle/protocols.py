@@ -572,15 +572,16 @@ def vmm_batch(be, x, W: np.ndarray, bsgs: bool = True):
 def rope_batch_plain(which: int, cfg, first_pos: int, base: float = 10000.0) -> np.ndarray:
     """kv_attention.cpp:59-76: lane tau carries position first_pos + tau."""
     N, t, dh = cfg.N, cfg.t, cfg.d_head
-    i = np.arange(N)
-    e = (i // t) % dh
-    pair = e // 2
-    angle = (first_pos + i % t).astype(np.float64) * np.power(base, -2.0 * pair / dh)
-    if which == 0:
-        return np.cos(angle)
     p = np.zeros(N)
-    m = (e % 2 == 0) if which == 1 else (e % 2 == 1)
-    p[m] = np.sin(angle[m]) if which == 1 else -np.sin(angle[m])
+    for i in range(N):  # libm cos / sin / pow, as the C++ product computes them
+        e = (i // t) % dh
+        angle = float(first_pos + i % t) * math.pow(base, -2.0 * (e // 2) / float(dh))
+        if which == 0:
+            p[i] = math.cos(angle)
+        elif which == 1 and e % 2 == 0:
+            p[i] = math.sin(angle)
+        elif which == 2 and e % 2 == 1:
+            p[i] = -math.sin(angle)
     return p
 
 

@@ -462,6 +462,19 @@ class VmmPlan:
             self.h = None
 
 
+class VmmBatchPlan(VmmPlan):
+    """Pre-encoded token-batched square diagonals (vmm.cpp:426-433) for vmm_batch."""
+
+    def __init__(self, be: Backend, W, level: int, bsgs: bool = True):
+        W = np.ascontiguousarray(np.asarray(W, dtype=np.float64))
+        self.be, self.rows, self.cols, self.level, self.bsgs = be, W.shape[0], W.shape[1], level, bsgs
+        self.in_offset = self.out_offset = 0
+        h = C.c_void_p()
+        _check(_native.lib().sf_vmm_batch_plan_create(be.ctx, W.ctypes.data_as(_native.dp), W.shape[0], W.shape[1],
+                                                       level, int(bsgs), C.byref(h)))
+        self.h = h.value
+
+
 def predict_interleaved_cost(be: Backend, rows: int, cols: int, bsgs: bool = False, mask_output: bool = False):
     """vmm.cpp:473-488 -> (rotations, ct_pt_mults, depth)."""
     r, c, d = C.c_longlong(), C.c_longlong(), C.c_int()
@@ -626,3 +639,81 @@ def exact_softmax_maps(be: Backend, maps, cfg: AttentionConfig, n_prime: int):
         for v in range(n_prime):
             out[v // gt][h * gt + v % gt] = p[v]
     return [be.exact_transform(m, (lambda _s, o=o: o)) for m, o in zip(maps, out)]
+
+
+# --------------------------------------------------------------------- prefill
+def inner_rotate(be: Backend, x: Ciphertext, r: int, block: int, hoisted: bool = False) -> Ciphertext:
+    """vmm.cpp:30-43."""
+    return be._ct(_native.lib().sf_inner_rotate, x.h, int(r), int(block), int(hoisted))
+
+
+def vmm_batch(be: Backend, x: Ciphertext, W=None, bsgs: bool = True, plan: Optional[VmmBatchPlan] = None):
+    """vmm.cpp:417-467 (pass `plan` to reuse the encoded diagonals)."""
+    if plan is None:
+        plan = VmmBatchPlan(be, W, x.level, bsgs)
+    return be._ct(_native.lib().sf_vmm_batch, x.h, plan.h)
+
+
+def rope_apply_batch(be: Backend, x: Ciphertext, cfg: AttentionConfig, first_pos: int, base: float = 10000.0):
+    """kv_attention.cpp:119-129."""
+    return be._ct(_native.lib().sf_rope_apply_batch, x.h, cfg.d, cfg.H, int(first_pos), base)
+
+
+def prefill(be: Backend, x_prompt, Wq, Wk, Wv, cfg: AttentionConfig, softmax_fn, rope_base: float = 10000.0):
+    """kv_attention.cpp:245-376 -> (attention cts, KVCache). The score maps are
+    handed to softmax_fn(be, maps[p][g][rho], cfg, n0) between the two halves."""
+    lib = _native.lib()
+    t, gt, n0 = cfg.t, cfg.group_tokens, cfg.n0
+    P = len(x_prompt)
+    lvl = x_prompt[0].level if P else 0
+    plans = [p if isinstance(p, VmmBatchPlan) else VmmBatchPlan(be, p, lvl) for p in (Wq, Wk, Wv)]
+    xs = (C.c_void_p * max(1, P))(*[x.h for x in x_prompt])
+    shape = [(p * t) // gt + 1 for p in range(P)]
+    cap = max(1, sum(shape) * t)
+    maps_out = (C.c_void_p * cap)()
+    n = C.c_int()
+    kv = C.c_void_p()
+    _check(lib.sf_prefill_scores(be.ctx, xs, P, plans[0].h, plans[1].h, plans[2].h, cfg.d, cfg.H, n0, cfg.n_max,
+                                 rope_base, C.byref(kv), maps_out, cap, C.byref(n)))
+    cache = KVCache(be, cfg, kv.value)
+    flat = [Ciphertext(be, maps_out[i]) for i in range(n.value)]
+    maps, k = [], 0
+    for p in range(P):
+        rows = []
+        for _ in range(shape[p]):
+            rows.append(flat[k:k + t])
+            k += t
+        maps.append(rows)
+    probs = softmax_fn(be, maps, cfg, n0)
+    pf = [c for mp in probs for row in mp for c in row]
+    arr = (C.c_void_p * max(1, len(pf)))(*[c.h for c in pf])
+    att_out = (C.c_void_p * max(1, P))()
+    na = C.c_int()
+    _check(lib.sf_prefill_attend(be.ctx, arr, len(pf), cache.h, att_out, P, C.byref(na)))
+    return [Ciphertext(be, att_out[i]) for i in range(na.value)], cache
+
+
+def exact_softmax_prefill_maps(be: Backend, maps, cfg: AttentionConfig, n0: int):
+    """Client-side oracle hook (kv_attention.cpp:414-454): decrypt the packed
+    prefill maps, exact causal softmax per query and head, re-encrypt each map
+    at its level (no ledger cost)."""
+    t, gt = cfg.t, cfg.group_tokens
+    slots = [[[be.decrypt(c) for c in row] for row in mp] for mp in maps]
+    out = [[[np.zeros(cfg.N) for _ in range(t)] for _ in mp] for mp in maps]
+    for p in range(len(maps)):
+        for tau in range(t):
+            query = p * t + tau
+            if query >= n0:
+                continue
+            for h in range(cfg.H):
+                idx = []
+                for k in range(query + 1):
+                    g, rho = k // gt, (k % t - tau) % t
+                    idx.append((g, rho, h * gt + (k - g * gt) // t * t + tau))
+                sc = np.array([slots[p][g][r][i] for g, r, i in idx])
+                e = np.exp(sc - sc.max())
+                pr = e / e.sum()
+                for (g, r, i), v in zip(idx, pr):
+                    out[p][g][r][i] = v
+    return [[[be.exact_transform(c, (lambda _s, o=out[p][g][r]: o)) for r, c in enumerate(row)]
+             for g, row in enumerate(mp)] for p, mp in enumerate(maps)]

@@ -43,6 +43,13 @@ SIGNATURES = {
     "sf_host_profile": (st, [C.c_char_p, C.c_int, C.c_int]),
     "sf_rotate_many": (st, [vp, vpp, C.c_int, C.c_int, vpp]),
     "sf_vmm_interleaved_multi": (st, [vp, vp, vpp, C.c_int, C.c_int, vpp]),
+    "sf_vmm_batch_plan_create": (st, [vp, dp, C.c_int, C.c_int, C.c_int, C.c_int, vpp]),
+    "sf_vmm_batch": (st, [vp, vp, vp, vpp]),
+    "sf_inner_rotate": (st, [vp, vp, C.c_int, C.c_int, C.c_int, vpp]),
+    "sf_rope_apply_batch": (st, [vp, vp, C.c_int, C.c_int, C.c_longlong, C.c_double, vpp]),
+    "sf_prefill_scores": (st, [vp, vpp, C.c_int, vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, vpp,
+                               vpp, C.c_int, ip]),
+    "sf_prefill_attend": (st, [vp, vpp, C.c_int, vp, vpp, C.c_int, ip]),
     "sf_bench_ntt": (st, [vp, C.c_int, C.c_int, C.c_int, dp]),
     "sf_graph_capture_begin": (st, [vp]),
     "sf_graph_capture_end": (st, [vp, vpp]),

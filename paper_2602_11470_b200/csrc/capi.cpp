@@ -409,6 +409,79 @@ sf_status sf_vmm_interleaved_multi(sf_context* ctx, const sf_ct* x, sf_vmm_plan*
   });
 }
 
+// --- prefill (kv_attention.cpp:119-129, 245-376; vmm.cpp:30-43, 417-467)
+sf_status sf_vmm_batch_plan_create(sf_context* ctx, const double* W, int rows, int cols, int level, int bsgs,
+                                   sf_vmm_plan** out) {
+  return guard([&] {
+    auto* h = new sf_vmm_plan;
+    try {
+      h->p = sf::make_vmm_batch_plan(*ctx->c, W, rows, cols, level, bsgs != 0);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+sf_status sf_vmm_batch(sf_context* ctx, const sf_ct* x, sf_vmm_plan* plan, sf_ct** out) {
+  return guard([&] { *out = wrap(sf::vmm_batch(*ctx->c, x->v, *plan->p)); });
+}
+sf_status sf_inner_rotate(sf_context* ctx, const sf_ct* x, int r, int block, int hoisted, sf_ct** out) {
+  return guard([&] { *out = wrap(sf::inner_rotate(*ctx->c, x->v, r, block, hoisted != 0)); });
+}
+sf_status sf_rope_apply_batch(sf_context* ctx, const sf_ct* x, int d, int H, long long first_pos, double base,
+                              sf_ct** out) {
+  return guard([&] {
+    sf::AttnCfg cfg{ctx->c->slots, d, H, 0, 1};
+    sf::validate_attention_config(cfg, ctx->c->slots);
+    *out = wrap(sf::rope_apply_batch(*ctx->c, x->v, cfg, first_pos, base));
+  });
+}
+sf_status sf_prefill_scores(sf_context* ctx, const sf_ct* const* xs, int P, sf_vmm_plan* wq, sf_vmm_plan* wk,
+                            sf_vmm_plan* wv, int d, int H, int n0, int n_max, double base, sf_kvcache** cache_out,
+                            sf_ct** maps_out, int maps_cap, int* n_maps) {
+  return guard([&] {
+    sf::AttnCfg cfg{ctx->c->slots, d, H, n0, n_max};
+    sf::validate_attention_config(cfg, ctx->c->slots);
+    std::vector<sf::Ct> x;
+    for (int p = 0; p < P; ++p) x.push_back(xs[p]->v);
+    sf::PrefillScores r = sf::prefill_scores(*ctx->c, x, *wq->p, *wk->p, *wv->p, cfg, base);
+    int k = 0;
+    for (auto& mp : r.maps)
+      for (auto& row : mp) k += (int)row.size();
+    sf::require(k <= maps_cap, sf::kShapeMismatch, "prefill: map buffer too small");
+    k = 0;
+    for (auto& mp : r.maps)
+      for (auto& row : mp)
+        for (auto& m : row) maps_out[k++] = wrap(std::move(m));
+    *n_maps = k;
+    *cache_out = wrap_kv(std::move(r.cache));
+  });
+}
+sf_status sf_prefill_attend(sf_context* ctx, const sf_ct* const* probs, int n_probs, const sf_kvcache* cache,
+                            sf_ct** att_out, int att_cap, int* n_att) {
+  return guard([&] {
+    const sf::KV& kv = cache->kv;
+    const int t = kv.cfg.t(), gt = kv.cfg.group_tokens();
+    const int P = (kv.n_prime + t - 1) / t;
+    std::vector<std::vector<std::vector<sf::Ct>>> pm(P);
+    int k = 0;
+    for (int p = 0; p < P; ++p) {
+      pm[p].resize((p * t) / gt + 1);
+      for (auto& row : pm[p])
+        for (int rho = 0; rho < t; ++rho) {
+          sf::require(k < n_probs, sf::kShapeMismatch, "prefill: softmax changed the map shape");
+          row.push_back(probs[k++]->v);
+        }
+    }
+    sf::require(k == n_probs, sf::kShapeMismatch, "prefill: softmax changed the map shape");
+    sf::require(P <= att_cap, sf::kShapeMismatch, "prefill: attention buffer too small");
+    auto att = sf::prefill_attend(*ctx->c, pm, kv);
+    for (int p = 0; p < P; ++p) att_out[p] = wrap(std::move(att[p]));
+    *n_att = P;
+  });
+}
+
 // --- KV attention
 sf_status sf_kv_create(sf_context* ctx, int d, int H, int n0, int n_max, sf_kvcache** out) {
   return guard([&] {

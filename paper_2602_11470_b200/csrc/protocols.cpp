@@ -94,6 +94,14 @@ const std::vector<Pt>& VmmPlan::diagonals(int limbs) {
   auto gen = [&](int g, double* slots) {
     // BSGS diagonals are pre-shifted by their giant step (vmm.cpp:170-175, 217)
     const long long shift = bsgs ? (long long)(g / bg.baby) * bg.baby * unit : 0;
+    if (batch) {  // vmm.cpp:426-433: p[i] = W[(e + j) mod d][e], e = ((i - pre) mod N) / t
+      const int d = s.d_in, t = s.t_in;
+      for (int i = 0; i < s.N; ++i) {
+        const int e = (int)(pos_mod(i - shift, s.N) / t);
+        slots[i] = w((e + g) % d, e);
+      }
+      return;
+    }
     for (int i = 0; i < s.N; ++i) slots[i] = diag_value(s, w, g, pos_mod(i - shift, s.N));
   };
   return pts.emplace(limbs, encode_many(c, gen, (int)s.k, scale, limbs)).first->second;
@@ -701,6 +709,267 @@ Ct softmax_times_v(Context& c, const std::vector<Ct>& probs, const KV& cache) {
   SF_HPROF("softmax_times_v");
   Ct3 p = softmax_times_v_partial(c, probs, cache, 0, 1);
   return softmax_times_v_finish(c, {&p}, cache);
+}
+
+// ============================================================== prefill
+// kv_attention.cpp:245-376 and the helpers it uses. Every op is the reference's
+// op on the batched evaluator; the plaintexts (masks, batched RoPE, batched
+// diagonals) are encoded once and cached like the decode step's.
+
+Ct inner_rotate(Context& c, const Ct& x, int r, int block, bool hoisted) {  // vmm.cpp:30-43
+  SF_HPROF("inner_rotate");
+  const int N = c.slots;
+  require(block > 0 && N % block == 0, kShapeMismatch, "inner_rotate: block must divide N");
+  const int s = (int)pos_mod(r, block);
+  if (s == 0) return x;
+  std::vector<double> keep(N), wrap(N);
+  for (int i = 0; i < N; ++i) keep[i] = (i % block < block - s) ? 1.0 : 0.0, wrap[i] = 1.0 - keep[i];
+  // the two rotations of x share one ModUp (same ciphertexts as two calls)
+  std::vector<Ct> rot = rotate_batch(c, {&x}, {{0, s}, {0, s - block}}, hoisted);
+  const std::string k = "irot:" + std::to_string(block) + ":" + std::to_string(s) + ":";
+  Ct lo = mul_plain_cached(c, rot[0], k + "keep", keep);
+  Ct hi = mul_plain_cached(c, rot[1], k + "wrap", wrap);
+  return add(c, lo, hi);
+}
+
+std::unique_ptr<VmmPlan> make_vmm_batch_plan(Context& c, const double* W, int rows, int cols, int level, bool bsgs) {
+  require(rows > 0 && cols > 0 && W, kShapeMismatch, "vmm_batch plan: empty weight");
+  require(level >= 1 && level <= c.L, kInvalidTarget, "vmm plan: level must be in [1, L]");
+  const int d = padded_dim(rows);
+  require(padded_dim(cols) == d, kShapeMismatch, "vmm_batch: square weights only");
+  require(d <= c.slots, kShapeMismatch, "vmm_batch: dimension exceeds N");
+  auto p = std::make_unique<VmmPlan>();
+  p->ctx = &c;
+  p->rows = rows;
+  p->cols = cols;
+  p->level = level;
+  p->bsgs = bsgs;
+  p->batch = true;
+  VmmShape& s = p->s;
+  s.N = c.slots;
+  s.d_in = s.d_out = d;
+  s.t_in = c.slots / d;
+  s.t_out = 1;  // giant unit = t_in * t_out = t (vmm.cpp:450)
+  s.k = d;
+  p->bg = bsgs ? bsgs_split(d) : BsgsSplit{1, d};
+  p->w_store.assign(W, W + (size_t)rows * cols);
+  const double* wd = p->w_store.data();
+  p->w = [wd, rows, cols](int r, int cc) { return (r < rows && cc < cols) ? wd[(size_t)r * cols + cc] : 0.0; };
+  p->diagonals(level + 1);
+  return p;
+}
+
+Ct vmm_batch(Context& c, const Ct& x, VmmPlan& plan) {  // vmm.cpp:417-467
+  SF_HPROF("vmm_batch");
+  require(plan.batch, kInvalidTarget, "vmm_batch: plan is not a token-batched plan");
+  require(x.layout && x.layout->kind == LayoutKind::Interleaved, kLayoutMismatch,
+          "vmm_batch: input must carry an interleaved layout");
+  require(!x.layout->deferred_mask, kLayoutMismatch, "vmm_batch: input garbage must be cleared first");
+  const int d = plan.s.d_in, t = plan.s.t_in;
+  require(x.layout->d == d, kShapeMismatch, "vmm_batch: layout/weight dimension mismatch");
+  check_ct(c, x, "vmm_batch");
+  require(x.level() > 0, kLevelUnderflow, "mul_plain: no multiplicative level left");
+  const std::vector<Pt>& diag = plan.diagonals(x.limbs);
+  Ct acc;
+  if (!plan.bsgs) {
+    std::vector<RotJob> jobs;
+    for (int j = 0; j < d; ++j) jobs.push_back({0, j * t});
+    std::vector<Ct> rx = rotate_batch(c, {&x}, jobs, false);
+    std::vector<const Ct*> cts;
+    std::vector<const Pt*> pts;
+    for (int j = 0; j < d; ++j) cts.push_back(&rx[j]), pts.push_back(&diag[j]);
+    acc = mac_plain(c, cts, pts);
+  } else {
+    const int b = plan.bg.baby, giants = plan.bg.giant;
+    std::vector<RotJob> jobs;
+    for (int g1 = 1; g1 < b; ++g1) jobs.push_back({0, g1 * t});
+    std::vector<Ct> baby{x};
+    for (Ct& r : rotate_batch(c, {&x}, jobs, true)) baby.push_back(std::move(r));
+    std::vector<Ct> partial(giants);
+    for (int g2 = 0; g2 < giants; ++g2) {
+      std::vector<const Ct*> cts;
+      std::vector<const Pt*> pts;
+      for (int g1 = 0; g1 < b && g2 * b + g1 < d; ++g1) cts.push_back(&baby[g1]), pts.push_back(&diag[g2 * b + g1]);
+      partial[g2] = mac_plain(c, cts, pts);
+    }
+    std::vector<std::vector<SumTerm>> groups;
+    for (int r = 0; r < std::min(kGiantGroups, giants); ++r) {
+      groups.emplace_back();
+      for (int g2 = r; g2 < giants; g2 += kGiantGroups)
+        groups.back().push_back({&partial[g2], (int)(((long long)g2 * b * t) % c.slots)});
+    }
+    std::vector<Ct> gs = rot_sum_batch(c, groups, false);
+    std::vector<const Ct*> ap;
+    for (auto& a : gs) ap.push_back(&a);
+    acc = sum_cts(c, ap);
+  }
+  acc.layout = Layout{LayoutKind::Interleaved, d, t, 0, 1, false};
+  return acc;
+}
+
+Ct rope_apply_batch(Context& c, const Ct& x, const AttnCfg& cfg, long long first_pos, double base) {
+  SF_HPROF("rope_apply_batch");  // kv_attention.cpp:119-129 (plaintexts: 59-76)
+  require_clean_interleaved(x, cfg, 0, "rope_apply_batch");
+  const int N = cfg.N, t = cfg.t(), dh = cfg.d_head();
+  require(dh % 2 == 0, kShapeMismatch, "rope_apply_batch: d_head must be even");
+  std::vector<double> p[3] = {std::vector<double>(N, 0.0), std::vector<double>(N, 0.0), std::vector<double>(N, 0.0)};
+  for (int i = 0; i < N; ++i) {
+    const int e = (i / t) % dh;
+    const double angle = (double)(first_pos + i % t) * std::pow(base, -2.0 * (e / 2) / (double)dh);
+    p[0][i] = std::cos(angle);
+    if (e % 2 == 0)
+      p[1][i] = std::sin(angle);
+    else
+      p[2][i] = -std::sin(angle);
+  }
+  char key[160];
+  std::snprintf(key, sizeof key, "ropeb:%lld:%d:%d:%d:%a:", first_pos, N, t, dh, base);
+  const int s = t;
+  Ct y = mul_plain_cached(c, x, std::string(key) + "0", p[0]);
+  y = add(c, y, rotate(c, mul_plain_cached(c, x, std::string(key) + "1", p[1]), -s, false));
+  y = add(c, y, rotate(c, mul_plain_cached(c, x, std::string(key) + "2", p[2]), s, false));
+  y.layout = x.layout;
+  return y;
+}
+
+PrefillScores prefill_scores(Context& c, const std::vector<Ct>& xs, VmmPlan& wq, VmmPlan& wk, VmmPlan& wv,
+                             const AttnCfg& cfg, double base) {
+  SF_HPROF("prefill_scores");  // kv_attention.cpp:245-333
+  const int t = cfg.t(), dh = cfg.d_head(), gt = cfg.group_tokens(), N = cfg.N, n0 = cfg.n0;
+  require(n0 >= 1, kShapeMismatch, "prefill: need a nonempty prompt");
+  require(n0 <= cfg.n_max, kCacheFull, "prefill: prompt exceeds cache capacity");
+  const int P = ceil_div(n0, t);
+  require((int)xs.size() == P, kShapeMismatch,
+          "prefill: expected " + std::to_string(P) + " prompt cts, got " + std::to_string(xs.size()));
+  PrefillScores out;
+  KV& cache = out.cache;
+  cache.cfg = cfg;
+  std::vector<Ct> q_cts;
+  for (int p = 0; p < P; ++p) {
+    q_cts.push_back(rope_apply_batch(c, vmm_batch(c, xs[p], wq), cfg, (long long)p * t, base));
+    cache.k.push_back(rope_apply_batch(c, vmm_batch(c, xs[p], wk), cfg, (long long)p * t, base));
+  }
+  for (int p = 0; p < P; ++p) {
+    const Ct v_raw = vmm_batch(c, xs[p], wv);
+    const int g = (p * t) / gt;
+    const int u_cap = p - g * dh;
+    if (g == (int)cache.v.size()) cache.v.emplace_back(v_variant_count(cfg), zeros(c, -1));
+    std::vector<Pt> masks;
+    for (int e = 0; e < dh; ++e) {
+      std::vector<double> m(N, 0.0);
+      for (int h = 0; h < cfg.H; ++h)
+        for (int j = 0; j < t; ++j) m[(h * dh + e) * t + j] = 1.0;
+      masks.push_back(cached_pt(c, "vblk:" + std::to_string(cfg.H) + ":" + std::to_string(dh) + ":" +
+                                       std::to_string(t) + ":" + std::to_string(e),
+                                m.data(), (double)c.primes[v_raw.limbs - 1], v_raw.limbs));
+    }
+    std::vector<const Ct*> vx(dh, &v_raw);
+    std::vector<const Pt*> ps;
+    for (auto& m : masks) ps.push_back(&m);
+    std::vector<Ct> pieces = mul_plain_batch(c, vx, ps);
+    for (int e = 0; e < dh; ++e) {
+      const int idx = v_variant_index(cfg, v_variant_of(cfg, e, u_cap * t));
+      cache.v[g][idx] = add(c, cache.v[g][idx], pieces[e]);
+    }
+  }
+  cache.n_prime = n0;
+  std::vector<std::vector<Ct>> k_rot(P);
+  for (int j = 0; j < P; ++j) {
+    k_rot[j].push_back(cache.k[j]);
+    for (int rho = 1; rho < t; ++rho) k_rot[j].push_back(inner_rotate(c, cache.k[j], rho, t, false));
+  }
+  std::vector<std::vector<std::vector<std::optional<Ct>>>> acc(P);
+  for (int p = 0; p < P; ++p) acc[p].assign((p * t) / gt + 1, std::vector<std::optional<Ct>>(t));
+  for (int p = 0; p < P; ++p)
+    for (int j = 0; j <= p; ++j) {
+      const int g_key = (j * t) / gt, local = (j * t) % gt;
+      for (int rho = 0; rho < t; ++rho) {
+        std::vector<double> m(N, 0.0);
+        bool any = false;
+        std::string mk = "causal:" + std::to_string(cfg.H) + ":" + std::to_string(gt) + ":";
+        for (int tau = 0; tau < t; ++tau) {
+          const int key = j * t + (tau + rho) % t, query = p * t + tau;
+          if (key <= query && key < n0 && query < n0) {
+            for (int h = 0; h < cfg.H; ++h) m[h * gt + tau] = 1.0;
+            any = true;
+            mk += std::to_string(tau) + ",";
+          }
+        }
+        if (!any) continue;
+        Ct prod = mul(c, q_cts[p], k_rot[j][rho]);
+        prod = fold_batch(c, {&prod}, dh, t)[0];  // fold_within_head (38-41)
+        Ct masked = mul_plain_cached(c, prod, mk, m);
+        Ct packed = local ? rotate(c, masked, -local, false) : masked;
+        auto& cell = acc[p][g_key][rho];
+        cell = cell ? add(c, *cell, packed) : packed;
+      }
+    }
+  out.maps.resize(P);
+  for (int p = 0; p < P; ++p) {
+    for (size_t g = 0; g < acc[p].size(); ++g) {
+      const int ref_level = acc[p][g][0]->level();
+      std::vector<Ct> row;
+      for (int rho = 0; rho < t; ++rho) {
+        Ct cell = acc[p][g][rho] ? *acc[p][g][rho] : zeros(c, ref_level);
+        cell.layout.reset();
+        row.push_back(cell);
+      }
+      out.maps[p].push_back(std::move(row));
+    }
+  }
+  return out;
+}
+
+std::vector<Ct> prefill_attend(Context& c, const std::vector<std::vector<std::vector<Ct>>>& probs, const KV& cache) {
+  SF_HPROF("prefill_attend");  // kv_attention.cpp:340-376
+  const AttnCfg& cfg = cache.cfg;
+  const int t = cfg.t(), gt = cfg.group_tokens(), n0 = cache.n_prime;
+  const int groups = (int)cache.v.size();
+  std::vector<int> w_lo(groups);
+  std::vector<std::vector<std::vector<Ct>>> v_rot(groups);
+  for (int g = 0; g < groups; ++g) {
+    const int tokens = std::min(gt, n0 - g * gt);
+    const int u_max = (tokens - 1) / t;  // touched_variants (53-57)
+    const int lo = cfg.H == 1 ? 0 : -u_max, hi = cfg.d_head();
+    w_lo[g] = lo;
+    for (int w = lo; w < hi; ++w) {
+      const Ct& base = cache.v[g][v_variant_index(cfg, w)];
+      std::vector<Ct> row{base};
+      for (int rho = 1; rho < t; ++rho) row.push_back(inner_rotate(c, base, rho, t, false));
+      v_rot[g].push_back(std::move(row));
+    }
+  }
+  std::vector<Ct> att;
+  for (size_t p = 0; p < probs.size(); ++p) {
+    std::vector<Ct> scores;
+    std::vector<std::pair<int, int>> who;  // (g, w index, rho) flattened below
+    std::vector<const Ct*> vv;
+    scores.reserve(probs[p].size() * t * (2 * cfg.d_head()));
+    for (size_t g = 0; g < probs[p].size(); ++g) {
+      const int tokens = std::min(gt, n0 - (int)g * gt);
+      const int u_max = (tokens - 1) / t;
+      const int lo = cfg.H == 1 ? 0 : -u_max, hi = cfg.d_head();
+      for (int rho = 0; rho < t; ++rho) {
+        const Ct& pm = probs[p][g][rho];
+        // the map's alignment rotations share one ModUp (same words as separate calls)
+        std::vector<RotJob> jobs;
+        for (int w = lo; w < hi; ++w) jobs.push_back({0, -w * t});
+        std::vector<Ct> rs = rotate_batch(c, {&pm}, jobs, false);
+        for (int w = lo; w < hi; ++w) {
+          scores.push_back(std::move(rs[w - lo]));
+          vv.push_back(&v_rot[g][w - w_lo[g]][rho]);
+        }
+      }
+    }
+    std::vector<const Ct*> sp;
+    for (auto& x : scores) sp.push_back(&x);
+    // sum of the products (kv_attention.cpp:358-368) relinearised once
+    Ct3 s3 = tensor_sum(c, sp, vv);
+    Ct a = relin_rescale(c, s3);
+    a.layout = make_interleaved(cfg.d, cfg.N, 0, cfg.H);
+    att.push_back(std::move(a));
+  }
+  return att;
 }
 
 }  // namespace sf

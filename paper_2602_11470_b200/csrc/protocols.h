@@ -32,6 +32,7 @@ struct VmmPlan {
   std::function<double(int, int)> w;  // weight_at (vmm.cpp:17-19 semantics: 0 outside)
   std::vector<double> w_store;
   std::map<int, std::vector<Pt>> pts;  // limbs -> k diagonals (NTT, scale q_top)
+  bool batch = false;                   // token-batched square diagonals (vmm.cpp:426-433, vmm_batch)
   const std::vector<Pt>& diagonals(int limbs);
 };
 
@@ -75,5 +76,20 @@ std::vector<Ct> qk_dot_partial(Context& c, const Ct& q, const KV& cache, int ran
 Ct3 softmax_times_v_partial(Context& c, const std::vector<Ct>& probs, const KV& cache, int rank, int world);
 Ct softmax_times_v_finish(Context& c, const std::vector<const Ct3*>& parts, const KV& cache);
 Ct softmax_times_v(Context& c, const std::vector<Ct>& probs, const KV& cache);
+
+// --- prefill (kv_attention.cpp:119-129, 245-376; vmm.cpp:30-43, 417-467) ------
+Ct inner_rotate(Context& c, const Ct& x, int r, int block, bool hoisted);
+std::unique_ptr<VmmPlan> make_vmm_batch_plan(Context& c, const double* W, int rows, int cols, int level, bool bsgs);
+Ct vmm_batch(Context& c, const Ct& x, VmmPlan& plan);
+Ct rope_apply_batch(Context& c, const Ct& x, const AttnCfg& cfg, long long first_pos, double base);
+// prefill up to the caller's softmax: the cache and the score maps [p][g][rho]
+struct PrefillScores {
+  KV cache;
+  std::vector<std::vector<std::vector<Ct>>> maps;
+};
+PrefillScores prefill_scores(Context& c, const std::vector<Ct>& xs, VmmPlan& wq, VmmPlan& wk, VmmPlan& wv,
+                             const AttnCfg& cfg, double base);
+// the probability-weighted values per prompt ct (after the caller's softmax)
+std::vector<Ct> prefill_attend(Context& c, const std::vector<std::vector<std::vector<Ct>>>& probs, const KV& cache);
 
 }  // namespace sf

@@ -249,3 +249,37 @@ def test_full_ring_ntt_and_rotation_parity():
     # ModDown rounding term dominates (~2^-18 observed); precision bar 16 bits
     err = np.max(np.abs(g.decrypt(rg) - np.roll(x, -5)))
     assert -np.log2(err) > 16.0, err
+
+
+@pytest.mark.parametrize("which", ["small", "medium"])
+def test_prefill_bit_exact_and_matches_reference(which):
+    # kv_attention.cpp:245-376 through the C ABI (sf_prefill_scores / _attend
+    # around the exact softmax hook) vs the oracle restatement on CKKS
+    import paper_2602_11470_b200 as sf
+    from oracle import protocols as P
+    from oracle.layout import make_interleaved
+    for c in cases(which, "prefill"):
+        N, L, d, H, n0 = c["N"], c["L"], c["d"], c["H"], c["n0"]
+        g, o = _pair(N, L, alpha=3)
+        W = [np.array(c[k]).reshape(d, d) for k in ("Wq", "Wk", "Wv")]
+        ocfg = P.AttentionConfig(N, d, H, n0, max(n0, 16))
+        gcfg = sf.AttentionConfig(N, d, H, n0, max(n0, 16))
+        xo = [o.encrypt(np.array(s), L, make_interleaved(d, N, 0, H), seed=50 + i) for i, s in enumerate(c["x_prompt"])]
+        xg = [g.encrypt(np.array(s), L, make_interleaved(d, N, 0, H), seed=50 + i) for i, s in enumerate(c["x_prompt"])]
+        att_o, cache_o = P.prefill(o, xo, W[0], W[1], W[2], ocfg, P.exact_softmax_prefill_maps)
+        att_g, cache_g = sf.prefill(g, xg, W[0], W[1], W[2], gcfg, sf.exact_softmax_prefill_maps)
+        assert cache_g.n_prime == n0
+        for a, b in zip(cache_g.k_cts, cache_o.k_cts):
+            _eq(a, b)
+        for ga, gb in zip(cache_g.v_cts, cache_o.v_cts):
+            for a, b in zip(ga, gb):
+                _eq(a, b)
+        assert len(att_g) == len(c["attention"])
+        for a, b, want in zip(att_g, att_o, c["attention"]):
+            _eq(a, b)
+            assert np.max(np.abs(g.decrypt(a) - np.array(want["slots"]))) < 1e-5
+            lw = layout_from(want["layout"])
+            assert a.level == want["level"] and (a.layout.kind, a.layout.d, a.layout.t, a.layout.offset,
+                                                  a.layout.heads, a.layout.deferred_mask) == (
+                lw.kind, lw.d, lw.t, lw.offset, lw.heads, lw.deferred_mask)
+        assert counts_dict(g.ledger.totals()) == c["counts"] == counts_dict(o.ledger.totals())
