@@ -172,6 +172,21 @@ sf_status sf_vmm_interleaved(sf_context* ctx, const sf_ct* x, const sf_vmm_plan*
 sf_status sf_vmm_interleaved_multi(sf_context* ctx, const sf_ct* x, sf_vmm_plan* const* plans, int k,
                                    int mask_output, sf_ct** outs);
 
+/* ---- wire and on-disk formats ---------------------------------
+   Weights in the reference's files (layouts.cpp:158-184: <dir>/<name>.bin =
+   rows x cols row-major float64, <name>.json = {"name","rows","cols"}); an
+   encoded-plan cache (the plan's NTT-domain diagonals + weights, so a restart
+   skips the offline encode); and the client <-> server ciphertext format
+   (header with magic, version, ring fingerprint, level, scale, layout; then the
+   2 x limbs x n RNS words). Loading checks the ring fingerprint. */
+sf_status sf_vmm_plan_create_from_file(sf_context* ctx, const char* dir, const char* name, int level, int in_offset,
+                                       int out_offset, int bsgs, sf_vmm_plan** out);
+sf_status sf_vmm_plan_save(sf_context* ctx, sf_vmm_plan* plan, const char* path);
+sf_status sf_vmm_plan_load(sf_context* ctx, const char* path, sf_vmm_plan** out);
+sf_status sf_ct_wire_size(sf_context* ctx, const sf_ct* ct, size_t* bytes);
+sf_status sf_ct_serialize(sf_context* ctx, const sf_ct* ct, uint8_t* buf, size_t cap, size_t* len);
+sf_status sf_ct_deserialize(sf_context* ctx, const uint8_t* buf, size_t len, sf_ct** out);
+
 /* ---- prefill (kv_attention.hpp:111-150; kv_attention.cpp:245-376) -------------
    vmm_batch (vmm.cpp:417-467) with its own plan type (token-batched square
    diagonals), inner_rotate (vmm.cpp:30-43), rope_apply_batch (kv_attention.cpp:

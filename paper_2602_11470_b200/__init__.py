@@ -319,6 +319,18 @@ class Backend:
         _check(_native.lib().sf_bench_ntt(self.ctx, limbs, count, reps, C.byref(ms)))
         return ms.value
 
+    # --- wire format (include/sf_b200.h sf_ct_serialize / sf_ct_deserialize)
+    def serialize(self, ct: "Ciphertext") -> bytes:
+        n = C.c_size_t()
+        _check(_native.lib().sf_ct_wire_size(self.ctx, ct.h, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        ln = C.c_size_t()
+        _check(_native.lib().sf_ct_serialize(self.ctx, ct.h, buf, n.value, C.byref(ln)))
+        return buf.raw[:ln.value]
+
+    def deserialize(self, data: bytes) -> "Ciphertext":
+        return self._ct(_native.lib().sf_ct_deserialize, data, len(data))
+
     def refill(self, ct: "Ciphertext", words: np.ndarray):
         """Overwrite ct's device words from (pinned) host memory, stream-ordered."""
         w = np.ascontiguousarray(words, dtype=np.uint64)
@@ -456,10 +468,49 @@ class VmmPlan:
                                                  rows, cols, level, in_offset, out_offset, int(bsgs), C.byref(h)))
         self.h = h.value
 
+    @classmethod
+    def _wrap(cls, be, handle, level, in_offset, out_offset, bsgs):
+        p = cls.__new__(cls)
+        p.be, p.rows, p.cols, p.level = be, None, None, level
+        p.in_offset, p.out_offset, p.bsgs, p.h = in_offset, out_offset, bsgs, handle
+        return p
+
+    def save(self, path: str) -> None:
+        """Encoded-plan cache: diagonals (NTT words) + weights, reloadable with vmm_plan_load."""
+        _check(_native.lib().sf_vmm_plan_save(self.be.ctx, self.h, path.encode()))
+
     def __del__(self):
         if getattr(self, "h", None) and not _shutdown[0]:
             _native.lib().sf_vmm_plan_destroy(self.h)
             self.h = None
+
+
+def save_weight(dir: str, name: str, W) -> None:
+    """The reference's weight files (layouts.cpp:158-170): <name>.bin row-major
+    float64 + <name>.json {"name", "rows", "cols"}."""
+    import json
+    import os
+    W = np.ascontiguousarray(np.asarray(W, dtype=np.float64))
+    os.makedirs(dir, exist_ok=True)
+    W.tofile(os.path.join(dir, name + ".bin"))
+    with open(os.path.join(dir, name + ".json"), "w") as f:
+        f.write(json.dumps({"name": name, "rows": int(W.shape[0]), "cols": int(W.shape[1])}, indent=2) + "\n")
+
+
+def vmm_plan_from_file(be: Backend, dir: str, name: str, level: int, in_offset: int = 0, out_offset: int = 0,
+                       bsgs: bool = True) -> "VmmPlan":
+    """A VMM plan straight from the reference's weight files (load_weight, layouts.cpp:172-184)."""
+    h = C.c_void_p()
+    _check(_native.lib().sf_vmm_plan_create_from_file(be.ctx, dir.encode(), name.encode(), level, in_offset,
+                                                       out_offset, int(bsgs), C.byref(h)))
+    return VmmPlan._wrap(be, h.value, level, in_offset, out_offset, bsgs)
+
+
+def vmm_plan_load(be: Backend, path: str) -> "VmmPlan":
+    """Reload an encoded-plan cache written by VmmPlan.save (no re-encoding)."""
+    h = C.c_void_p()
+    _check(_native.lib().sf_vmm_plan_load(be.ctx, path.encode(), C.byref(h)))
+    return VmmPlan._wrap(be, h.value, -1, 0, 0, True)
 
 
 class VmmBatchPlan(VmmPlan):

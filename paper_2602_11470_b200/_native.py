@@ -44,6 +44,12 @@ SIGNATURES = {
     "sf_rotate_many": (st, [vp, vpp, C.c_int, C.c_int, vpp]),
     "sf_vmm_interleaved_multi": (st, [vp, vp, vpp, C.c_int, C.c_int, vpp]),
     "sf_vmm_batch_plan_create": (st, [vp, dp, C.c_int, C.c_int, C.c_int, C.c_int, vpp]),
+    "sf_vmm_plan_create_from_file": (st, [vp, C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, vpp]),
+    "sf_vmm_plan_save": (st, [vp, vp, C.c_char_p]),
+    "sf_vmm_plan_load": (st, [vp, C.c_char_p, vpp]),
+    "sf_ct_wire_size": (st, [vp, vp, C.POINTER(C.c_size_t)]),
+    "sf_ct_serialize": (st, [vp, vp, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "sf_ct_deserialize": (st, [vp, C.c_char_p, C.c_size_t, vpp]),
     "sf_vmm_batch": (st, [vp, vp, vp, vpp]),
     "sf_inner_rotate": (st, [vp, vp, C.c_int, C.c_int, C.c_int, vpp]),
     "sf_rope_apply_batch": (st, [vp, vp, C.c_int, C.c_int, C.c_longlong, C.c_double, vpp]),

@@ -409,6 +409,52 @@ sf_status sf_vmm_interleaved_multi(sf_context* ctx, const sf_ct* x, sf_vmm_plan*
   });
 }
 
+// --- wire / on-disk formats (wire.cpp)
+sf_status sf_vmm_plan_create_from_file(sf_context* ctx, const char* dir, const char* name, int level, int in_offset,
+                                       int out_offset, int bsgs, sf_vmm_plan** out) {
+  return guard([&] {
+    int rows = 0, cols = 0;
+    const std::vector<double> w = sf::load_weight(dir, name, &rows, &cols);
+    auto* h = new sf_vmm_plan;
+    try {
+      h->p = sf::make_vmm_plan(*ctx->c, w.data(), rows, cols, level, in_offset, out_offset, bsgs != 0);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+sf_status sf_vmm_plan_save(sf_context* ctx, sf_vmm_plan* plan, const char* path) {
+  return guard([&] { sf::vmm_plan_save(*ctx->c, *plan->p, path); });
+}
+sf_status sf_vmm_plan_load(sf_context* ctx, const char* path, sf_vmm_plan** out) {
+  return guard([&] {
+    auto* h = new sf_vmm_plan;
+    try {
+      h->p = sf::vmm_plan_load(*ctx->c, path);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+sf_status sf_ct_wire_size(sf_context* ctx, const sf_ct* ct, size_t* bytes) {
+  return guard([&] { *bytes = sf::ct_wire_size(*ctx->c, ct->v); });
+}
+sf_status sf_ct_serialize(sf_context* ctx, const sf_ct* ct, uint8_t* buf, size_t cap, size_t* len) {
+  return guard([&] {
+    const size_t need = sf::ct_wire_size(*ctx->c, ct->v);
+    sf::require(cap >= need, sf::kShapeMismatch, "ct_serialize: buffer too small");
+    sf::ct_serialize(*ctx->c, ct->v, buf);
+    *len = need;
+  });
+}
+sf_status sf_ct_deserialize(sf_context* ctx, const uint8_t* buf, size_t len, sf_ct** out) {
+  return guard([&] { *out = wrap(sf::ct_deserialize(*ctx->c, buf, len)); });
+}
+
 // --- prefill (kv_attention.cpp:119-129, 245-376; vmm.cpp:30-43, 417-467)
 sf_status sf_vmm_batch_plan_create(sf_context* ctx, const double* W, int rows, int cols, int level, int bsgs,
                                    sf_vmm_plan** out) {

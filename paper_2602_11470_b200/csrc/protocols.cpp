@@ -108,7 +108,7 @@ const std::vector<Pt>& VmmPlan::diagonals(int limbs) {
 }
 
 std::unique_ptr<VmmPlan> make_vmm_plan(Context& c, const double* W, int rows, int cols, int level, int in_offset,
-                                       int out_offset, bool bsgs) {
+                                       int out_offset, bool bsgs, bool encode) {
   require(rows > 0 && cols > 0, kShapeMismatch, "vmm plan: empty weight");
   require(level >= 1 && level <= c.L, kInvalidTarget, "vmm plan: level must be in [1, L]");
   auto p = std::make_unique<VmmPlan>();
@@ -128,7 +128,7 @@ std::unique_ptr<VmmPlan> make_vmm_plan(Context& c, const double* W, int rows, in
       return (r < rows && cc < cols) ? std::sin(0.001 * ((double)r * 31.0 + cc) + 0.25) : 0.0;
     };
   }
-  p->diagonals(level + 1);
+  if (encode) p->diagonals(level + 1);
   return p;
 }
 
@@ -732,7 +732,8 @@ Ct inner_rotate(Context& c, const Ct& x, int r, int block, bool hoisted) {  // v
   return add(c, lo, hi);
 }
 
-std::unique_ptr<VmmPlan> make_vmm_batch_plan(Context& c, const double* W, int rows, int cols, int level, bool bsgs) {
+std::unique_ptr<VmmPlan> make_vmm_batch_plan(Context& c, const double* W, int rows, int cols, int level, bool bsgs,
+                                             bool encode) {
   require(rows > 0 && cols > 0 && W, kShapeMismatch, "vmm_batch plan: empty weight");
   require(level >= 1 && level <= c.L, kInvalidTarget, "vmm plan: level must be in [1, L]");
   const int d = padded_dim(rows);
@@ -755,7 +756,7 @@ std::unique_ptr<VmmPlan> make_vmm_batch_plan(Context& c, const double* W, int ro
   p->w_store.assign(W, W + (size_t)rows * cols);
   const double* wd = p->w_store.data();
   p->w = [wd, rows, cols](int r, int cc) { return (r < rows && cc < cols) ? wd[(size_t)r * cols + cc] : 0.0; };
-  p->diagonals(level + 1);
+  if (encode) p->diagonals(level + 1);
   return p;
 }
 

@@ -37,7 +37,7 @@ struct VmmPlan {
 };
 
 std::unique_ptr<VmmPlan> make_vmm_plan(Context& c, const double* W, int rows, int cols, int level, int in_offset,
-                                       int out_offset, bool bsgs);
+                                       int out_offset, bool bsgs, bool encode = true);
 Ct vmm_interleaved(Context& c, const Ct& x, VmmPlan& plan, bool mask_output);
 // several VMMs of the same input (shared ladder + babies, batched tails)
 std::vector<Ct> vmm_interleaved_multi(Context& c, const Ct& x, const std::vector<VmmPlan*>& plans, bool mask_output);
@@ -79,7 +79,8 @@ Ct softmax_times_v(Context& c, const std::vector<Ct>& probs, const KV& cache);
 
 // --- prefill (kv_attention.cpp:119-129, 245-376; vmm.cpp:30-43, 417-467) ------
 Ct inner_rotate(Context& c, const Ct& x, int r, int block, bool hoisted);
-std::unique_ptr<VmmPlan> make_vmm_batch_plan(Context& c, const double* W, int rows, int cols, int level, bool bsgs);
+std::unique_ptr<VmmPlan> make_vmm_batch_plan(Context& c, const double* W, int rows, int cols, int level, bool bsgs,
+                                             bool encode = true);
 Ct vmm_batch(Context& c, const Ct& x, VmmPlan& plan);
 Ct rope_apply_batch(Context& c, const Ct& x, const AttnCfg& cfg, long long first_pos, double base);
 // prefill up to the caller's softmax: the cache and the score maps [p][g][rho]
@@ -91,5 +92,13 @@ PrefillScores prefill_scores(Context& c, const std::vector<Ct>& xs, VmmPlan& wq,
                              const AttnCfg& cfg, double base);
 // the probability-weighted values per prompt ct (after the caller's softmax)
 std::vector<Ct> prefill_attend(Context& c, const std::vector<std::vector<std::vector<Ct>>>& probs, const KV& cache);
+
+// --- wire / on-disk formats (wire.cpp) ---------------------------------------
+std::vector<double> load_weight(const std::string& dir, const std::string& name, int* rows, int* cols);
+size_t ct_wire_size(const Context& c, const Ct& a);
+void ct_serialize(Context& c, const Ct& a, uint8_t* out);
+Ct ct_deserialize(Context& c, const uint8_t* in, size_t len);
+void vmm_plan_save(Context& c, VmmPlan& p, const std::string& path);
+std::unique_ptr<VmmPlan> vmm_plan_load(Context& c, const std::string& path);
 
 }  // namespace sf

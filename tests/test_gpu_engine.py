@@ -194,3 +194,40 @@ def test_vmm_multi_equals_separate_calls_and_ledger():
     (d0, l0, y0), (d1, l1, y1) = res
     assert all(np.array_equal(a, b) for a, b in zip(d0, d1))
     assert l0 == l1 and y0 == y1
+
+
+def test_wire_formats_round_trip(tmp_path):
+    # reference weight files -> plan, encoded-plan cache, ciphertext wire format
+    import paper_2602_11470_b200 as sf
+    from oracle.layout import make_interleaved
+    N, L = 4096, 3
+    be = sf.Backend(N, L, alpha=2)
+    rng = np.random.default_rng(2)
+    W = rng.normal(size=(100, 60)) / 10
+    sf.save_weight(str(tmp_path), "w_test", W)
+    assert np.array_equal(np.fromfile(tmp_path / "w_test.bin").reshape(100, 60), W)
+    ly = make_interleaved(128, N, 0)
+    s = np.zeros(N)
+    s[np.arange(100) * ly.t] = rng.normal(size=100)
+    x = be.encrypt(s, L, ly, seed=4)
+    p_mem = sf.VmmPlan(be, W, 100, 60, L, 0, 0, True)
+    p_file = sf.vmm_plan_from_file(be, str(tmp_path), "w_test", L)
+    y0 = sf.vmm_interleaved(be, x, None, plan=p_mem, mask_output=True)
+    y1 = sf.vmm_interleaved(be, x, None, plan=p_file, mask_output=True)
+    assert np.array_equal(y0.data(), y1.data())
+    p_mem.save(str(tmp_path / "plan.sfvp"))
+    p_back = sf.vmm_plan_load(be, str(tmp_path / "plan.sfvp"))
+    y2 = sf.vmm_interleaved(be, x, None, plan=p_back, mask_output=True)
+    assert np.array_equal(y0.data(), y2.data())
+    wire = be.serialize(y0)
+    z = be.deserialize(wire)
+    assert np.array_equal(z.data(), y0.data()) and z.level == y0.level and z.layout == y0.layout
+    assert abs(z.scale - y0.scale) == 0.0
+    zero = be.zeros(2)
+    zz = be.deserialize(be.serialize(zero))
+    assert zz.level == 2
+    with pytest.raises(sf.ShapeMismatch):
+        be.deserialize(wire[:-8])
+    other = sf.Backend(N, L + 1, alpha=2)
+    with pytest.raises(sf.ShapeMismatch):
+        other.deserialize(wire)
