@@ -194,12 +194,15 @@ __global__ void __launch_bounds__(kWarps * 32) ntt_col_pass(LimbBatch B, Tabs T)
 // NTT -> store), so shared memory does not grow with nd and every phase keeps
 // all warps busy. TCF = 8 gives 64-byte row segments for big batches; TCF = 2
 // gives 4x more CTAs for single-ciphertext launches.
-template <int LOGR, int LOGC, int TCF>
-__global__ void __launch_bounds__(TCF * 32, TCF == 8 ? 3 : 8) fused_col_kernel(FusedColArgs A, Tabs T) {
+template <int LOGR, int LOGC, int TCF, int CPW>
+__global__ void __launch_bounds__(TCF / CPW * 32, TCF / CPW == 8 ? (CPW == 1 ? 3 : 2) : 8)
+    fused_col_kernel(FusedColArgs A, Tabs T) {
+  // CPW columns per warp (TCF / CPW warps): the column transforms of one warp
+  // run interleaved (shared twiddles, CPW x the independent butterflies)
   constexpr int R = 1 << LOGR, C = 1 << LOGC, E = R / 32, LOGN = LOGR + LOGC;
   constexpr int PAD = R + 1;
   constexpr int tiles = C / TCF;
-  constexpr int NT = TCF * 32;
+  constexpr int NT = TCF / CPW * 32;
   extern __shared__ u64 sm_all[];  // [ns][TCF][PAD] sources, [TCF][PAD] destination
   // blockIdx.x = (job * dgroups + dgroup) * tiles + tile; a CTA converts the
   // destinations [dgroup * dpc, +dpc) (dpc = nd: all of them)
@@ -232,16 +235,22 @@ __global__ void __launch_bounds__(TCF * 32, TCF == 8 ? 3 : 8) fused_col_kernel(F
       w = W[i];
       ws = Ws[i];
     };
-    u64* sm = region(s, warp);
-    u64 x[E];
+    u64* sm[CPW];
+    u64 x[CPW][E];
 #pragma unroll
-    for (int k = 0; k < E; ++k) x[k] = sm[swz(lane + 32 * k)];
+    for (int c = 0; c < CPW; ++c) {
+      sm[c] = region(s, warp * CPW + c);
+#pragma unroll
+      for (int k = 0; k < E; ++k) x[c][k] = sm[c][swz(lane + 32 * k)];
+    }
     __syncwarp();
-    warp_inv<LOGR>(x, sm, lane, q, tw);
+    warp_inv_n<LOGR, CPW>(x, sm, lane, q, tw);
     // canonical y_s: the basis conversion's [x q^_s^-1]_{q_s} (and the centred lift) need it
     const u64 ym = A.mode == 0 ? A.ymul[s] : T.ninv[p], yms = A.mode == 0 ? A.ymul_s[s] : T.ninv_s[p];
 #pragma unroll
-    for (int k = 0; k < E; ++k) sm[swz(lane + 32 * k)] = mul_shoup(x[k], ym, yms, q);
+    for (int c = 0; c < CPW; ++c)
+#pragma unroll
+      for (int k = 0; k < E; ++k) sm[c][swz(lane + 32 * k)] = mul_shoup(x[c][k], ym, yms, q);
     __syncwarp();
   }
   __syncthreads();
@@ -290,14 +299,20 @@ __global__ void __launch_bounds__(TCF * 32, TCF == 8 ? 3 : 8) fused_col_kernel(F
         w = W[i];
         ws = Ws[i];
       };
-      u64* sm = out + (size_t)warp * PAD;
-      u64 x[E];
+      u64* sm[CPW];
+      u64 x[CPW][E];
 #pragma unroll
-      for (int k = 0; k < E; ++k) x[k] = sm[swz(lane + 32 * k)];
+      for (int c = 0; c < CPW; ++c) {
+        sm[c] = out + (size_t)(warp * CPW + c) * PAD;
+#pragma unroll
+        for (int k = 0; k < E; ++k) x[c][k] = sm[c][swz(lane + 32 * k)];
+      }
       __syncwarp();
-      warp_fwd<LOGR>(x, sm, lane, q, tw);
+      warp_fwd_n<LOGR, CPW>(x, sm, lane, q, tw);
 #pragma unroll
-      for (int k = 0; k < E; ++k) sm[swz(lane + 32 * k)] = x[k];
+      for (int c = 0; c < CPW; ++c)
+#pragma unroll
+        for (int k = 0; k < E; ++k) sm[c][swz(lane + 32 * k)] = x[c][k];
     }
     __syncthreads();
     // 5. store (lazy [0, 4q) values; the row pass accepts them); one
@@ -600,26 +615,29 @@ void run_epi(Context& c, const EpiBatch& e) {
   ntt_row_epi<LOGR, LOGC><<<grid, kWarps * 32, 0, c.stream>>>(e, c.tabs);
 }
 
-template <int LOGR, int LOGC, int TCF>
+template <int LOGR, int LOGC, int TCF, int CPW>
 void run_fused_t(Context& c, const FusedColArgs& a) {
   constexpr int R = 1 << LOGR;
   const size_t sm = (size_t)(a.ns + 1) * TCF * (R + 1) * sizeof(u64);
   static int configured = 0;
   if (!configured) {
-    SF_CUDA(cudaFuncSetAttribute(fused_col_kernel<LOGR, LOGC, TCF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 200 * 1024));
+    SF_CUDA(cudaFuncSetAttribute(fused_col_kernel<LOGR, LOGC, TCF, CPW>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     configured = 1;
   }
   require(sm <= 200 * 1024, kInternal, "fused column stage: too many source limbs for shared memory");
   const int dpc = a.d_per_cta > 0 ? a.d_per_cta : a.nd;
   const unsigned grid = (unsigned)a.count * ((a.nd + dpc - 1) / dpc) * ((1u << LOGC) / TCF);
-  fused_col_kernel<LOGR, LOGC, TCF><<<grid, TCF * 32, sm, c.stream>>>(a, c.tabs);
+  fused_col_kernel<LOGR, LOGC, TCF, CPW><<<grid, TCF / CPW * 32, sm, c.stream>>>(a, c.tabs);
 }
 
 template <int LOGR, int LOGC>
 void run_fused(Context& c, const FusedColArgs& a) {
   if ((size_t)a.count * ((1u << LOGC) / 8) >= 444) {
-    run_fused_t<LOGR, LOGC, 8>(c, a);
+    if (c.fused_cpw == 2 && (1 << LOGC) >= 16)
+      run_fused_t<LOGR, LOGC, 16, 2>(c, a);
+    else
+      run_fused_t<LOGR, LOGC, 8, 1>(c, a);
     return;
   }
   // small launch (single ciphertexts): 2-column CTAs, and the destinations
@@ -627,7 +645,7 @@ void run_fused(Context& c, const FusedColArgs& a) {
   // chain of per-destination transforms does not serialise inside one warp
   FusedColArgs b = a;
   b.d_per_cta = 1;
-  run_fused_t<LOGR, LOGC, 2>(c, b);
+  run_fused_t<LOGR, LOGC, 2, 1>(c, b);
 }
 
 template <int LOGR, int LOGC>

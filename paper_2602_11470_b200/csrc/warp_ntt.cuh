@@ -104,6 +104,94 @@ __device__ __forceinline__ void warp_inv(u64 (&x)[1 << (LOGM - 5)], u64* sm, int
   relayout<LOGE>(x, sm, lane, s0, LOGM - LOGE);
 }
 
+// NC independent sub-transforms of the same prime in one warp (e.g. NC adjacent
+// columns of a column pass): every butterfly of a stage is issued for all NC
+// columns with one twiddle fetch, doubling the warp's independent work (ILP).
+template <int LOGE, int NC>
+__device__ __forceinline__ void relayout_n(u64 (&x)[NC][1 << LOGE], u64* const (&sm)[NC], int lane, int from, int to) {
+  if (from == to) return;
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+#pragma unroll
+    for (int k = 0; k < (1 << LOGE); ++k) sm[c][swz(lay<LOGE>(lane, k, from))] = x[c][k];
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+#pragma unroll
+    for (int k = 0; k < (1 << LOGE); ++k) x[c][k] = sm[c][swz(lay<LOGE>(lane, k, to))];
+  __syncwarp();
+}
+
+template <int LOGM, int NC, class TW>
+__device__ __forceinline__ void warp_fwd_n(u64 (&x)[NC][1 << (LOGM - 5)], u64* const (&sm)[NC], int lane, u64 q,
+                                           const TW& tw) {
+  constexpr int LOGE = LOGM - 5;
+  constexpr int E = 1 << LOGE;
+  const u64 q2 = 2 * q;
+  int s0 = LOGM - LOGE;
+#pragma unroll
+  for (int hi = LOGM; hi > 0; hi -= LOGE) {
+    const int lo = hi - LOGE > 0 ? hi - LOGE : 0;
+    relayout_n<LOGE, NC>(x, sm, lane, s0, lo);
+    s0 = lo;
+#pragma unroll
+    for (int b = hi - 1; b >= lo; --b) {
+      const int rb = b - s0;
+#pragma unroll
+      for (int k = 0; k < E; ++k) {
+        if (k & (1 << rb)) continue;
+        const int idx = lay<LOGE>(lane, k, s0);
+        u64 w, ws;
+        tw(b, idx >> (b + 1), w, ws);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          u64 U = x[c][k];
+          U = U >= q2 ? U - q2 : U;
+          const u64 T = mul_shoup_lazy(x[c][k | (1 << rb)], w, ws, q);
+          x[c][k] = U + T;
+          x[c][k | (1 << rb)] = U - T + q2;
+        }
+      }
+    }
+  }
+  relayout_n<LOGE, NC>(x, sm, lane, s0, LOGM - LOGE);
+}
+
+template <int LOGM, int NC, class TW>
+__device__ __forceinline__ void warp_inv_n(u64 (&x)[NC][1 << (LOGM - 5)], u64* const (&sm)[NC], int lane, u64 q,
+                                           const TW& tw) {
+  constexpr int LOGE = LOGM - 5;
+  constexpr int E = 1 << LOGE;
+  const u64 q2 = 2 * q;
+  int s0 = LOGM - LOGE;
+#pragma unroll
+  for (int lo = 0; lo < LOGM; lo += LOGE) {
+    const int hi = lo + LOGE < LOGM ? lo + LOGE : LOGM;
+    const int ns0 = hi - LOGE > 0 ? hi - LOGE : 0;
+    relayout_n<LOGE, NC>(x, sm, lane, s0, ns0);
+    s0 = ns0;
+#pragma unroll
+    for (int b = lo; b < hi; ++b) {
+      const int rb = b - s0;
+#pragma unroll
+      for (int k = 0; k < E; ++k) {
+        if (k & (1 << rb)) continue;
+        const int idx = lay<LOGE>(lane, k, s0);
+        u64 w, ws;
+        tw(b, idx >> (b + 1), w, ws);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          const u64 U = x[c][k], V = x[c][k | (1 << rb)];
+          const u64 S = U + V;
+          x[c][k] = S >= q2 ? S - q2 : S;
+          x[c][k | (1 << rb)] = mul_shoup_lazy(U - V + q2, w, ws, q);
+        }
+      }
+    }
+  }
+  relayout_n<LOGE, NC>(x, sm, lane, s0, LOGM - LOGE);
+}
+
 __device__ __forceinline__ u64 canon4(u64 v, u64 q) {  // [0, 4q) -> [0, q)
   v = v >= 2 * q ? v - 2 * q : v;
   return v >= q ? v - q : v;
