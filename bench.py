@@ -212,6 +212,90 @@ class LlamaLayer:
         return [q, k, v, maps[0], att, o, g, u, dn]
 
 
+    def step_sharded(self, sh, inputs=None):
+        """One decode token split over the ranks of `sh` (paper_2602_11470_b200.shard,
+        DESIGN.md §7): VMM giant groups, QK^T key-ct groups and Score*V pairs per
+        rank, partial ciphertexts all-gathered over NCCL and mod-added on the GPU;
+        RoPE, the appends and the replicated tails (reduce ladders, lane fold) on
+        every rank. Word-identical to step() for any world size."""
+        be, sf = self.be, self.sf
+        x, h7, h3, h1, p0, p1 = inputs or self.inputs
+        q, k, v = sh.vmm(x, self.wq), sh.vmm(x, self.wk), sh.vmm(x, self.wv)
+        qr = sf.rope_apply(be, q, self.cfg, self.pos)
+        kr = sf.rope_apply(be, k, self.cfg, self.pos)
+        cache = sf.v_append(be, self.cache, sf.make_v_pieces(be, self.cache, v, self.pos))
+        cache = sf.k_append(be, cache, kr)
+        maps = sh.qk_dot(qr, cache)
+        att = sh.softmax_times_v([p0, p1], cache)
+        o = sh.vmm(h7, self.wo)
+        g, u = sh.vmm(h3, self.wg), sh.vmm(h3, self.wu)
+        dn = sh.vmm(h1, self.wd)
+        return [q, k, v, maps[0], att, o, g, u, dn]
+
+
+def run_sharded(args, be, sf, layer, dist, rank, world, clk):
+    """--shard: strong scaling of ONE token over the ranks (latency), eager."""
+    from paper_2602_11470_b200 import shard
+    import torch
+    sh = shard.Sharded(be)
+    ref = layer.step()  # the single-device step on every rank, for the bit-exactness check
+    got = layer.step_sharded(sh)
+    exact = all(np.array_equal(a.data(), b.data()) for a, b in zip(ref, got))
+    for _ in range(args.warmup):
+        layer.step_sharded(sh)
+    be.synchronize()
+    torch.cuda.synchronize()
+    dist.barrier()
+    clk.mark()
+    be.event_record(0)
+    t_w = time.perf_counter()
+    for _ in range(args.steps):
+        outs = layer.step_sharded(sh)
+    be.event_record(1)
+    ms = be.event_elapsed_ms(0, 1) / args.steps
+    be.synchronize()
+    wall = (time.perf_counter() - t_w) * 1e3 / args.steps
+    clk.__exit__()
+    t = torch.tensor([ms], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    ex = torch.tensor([1 if exact else 0], device="cuda")
+    dist.all_reduce(ex, op=dist.ReduceOp.MIN)
+    host_in = [(c.data(), c.level, c.scale, c.layout) for c in layer.inputs]
+    be.synchronize()
+    dist.barrier()
+    t_e = time.perf_counter()
+    for _ in range(args.steps):
+        for slot, (w, *_r) in zip(layer.inputs, host_in):
+            be.refill(slot, w)
+        outs = layer.step_sharded(sh)
+        res = [outs[4].data(), outs[8].data()]
+    be.synchronize()
+    e2e = (time.perf_counter() - t_e) * 1e3 / args.steps
+    t = torch.tensor([e2e], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e = float(t.item())
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(ms, 3), "unit": "ms/token", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic: reference bench weights sin(0.001(31r+c)+0.25), N(0,1) activations/cache, seeded",
+            "config": {"workload": "llama3-8b-layer-decode@n'=2048", "ring_degree": 2 * SLOTS, "slots": SLOTS,
+                       "d": D, "heads": H, "ffn": FF, "context": NP, "levels": LEVELS, "L": 7, "alpha": args.alpha,
+                       "parallelism": f"sharded{world} (giant / key-ct / pair groups, NCCL all-gather + mod-add)",
+                       "l2": "working set >> 126 MB L2; no flush needed"},
+            "sharded_bit_exact_vs_single_device": bool(ex.item()),
+            "wall_ms_per_step_rank0": round(wall, 3),
+            "e2e": {"value": round(e2e, 3), "unit": "ms/token",
+                    "h2d_bytes_per_step": int(sum(w.nbytes for w, *_ in host_in)),
+                    "d2h_bytes_per_step": int(sum(r.nbytes for r in res))},
+            "gpu_launches": None, "clocks": clk.summary(), "cpu_baseline": None,
+            "execution": "eager (host-issued; NCCL exchanges on torch's stream between library launches)",
+        }
+        print(json.dumps(line), flush=True)
+
+
 # ---------------------------------------------------------------- reference arm
 def run_reference(args, rank):
     if rank != 0:
@@ -266,17 +350,27 @@ def main():
     ap.add_argument("--nvtx-step", action="store_true", help="run one NVTX-ranged step after warm-up and exit")
     ap.add_argument("--alpha", type=int, default=2, help="special primes per key-switching digit")
     ap.add_argument("--quiet", action="store_true")
+    ap.add_argument("--shard", action="store_true",
+                    help="strong scaling: split ONE token over the ranks (default: one replica per GPU)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dist = None
-    if world > 1:
+    if world > 1 or args.shard:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        if world > 1:
+            dist.init_process_group("nccl")
+        else:  # --shard on one GPU: a world of one (exercises the exchange path)
+            import socket
+            sk = socket.socket()
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+            sk.close()
+            dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
     if args.impl == "reference":
         run_reference(args, rank)
         if dist:
@@ -293,6 +387,11 @@ def main():
 
     clk = Clocks(local).__enter__()  # sampling starts before the warm-up
     clk.wait_first()
+    if args.shard:
+        run_sharded(args, be, sf, layer, dist, rank, world, clk)
+        dist.barrier()
+        dist.destroy_process_group()
+        return
     for _ in range(args.warmup):
         layer.step()
     be.synchronize()

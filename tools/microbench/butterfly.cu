@@ -13,7 +13,7 @@ __device__ __forceinline__ u64 hi_approx(u64 x, u64 wp) {
 __device__ __forceinline__ u64 shoup_approx(u64 x, u64 w, u64 wp, u64 q) { return x * w - hi_approx(x, wp) * q; }
 
 template <int V>
-__global__ void bench(u64* out, const u64* in, u64 q, u64 w0, u64 wp0, int iters) {
+__global__ void bench(u64* out, const u64* in, u64 q, u64 w0, u64 wp0, int iters, double wq0) {
   u64 x[8];
   for (int k = 0; k < 8; ++k) x[k] = in[(threadIdx.x + blockIdx.x * blockDim.x) * 8 + k] % q;
   const u64 q2 = 2 * q;
@@ -32,6 +32,11 @@ __global__ void bench(u64* out, const u64* in, u64 q, u64 w0, u64 wp0, int iters
         } else if (V == 1) {
           T = shoup_approx(x[k | (1 << b)], w, wp, q);
           T = T >= q2 ? T - q2 : T;
+        } else if (V == 3) {  // FP64 quotient (q < 2^42 primes): qt = floor(x * (w / q)) +- 1
+          const u64 V_ = x[k | (1 << b)];
+          const u64 qt = (u64)(__ull2double_rn(V_) * wq0);
+          u64 r = V_ * w - qt * q;
+          T = (long long)r < 0 ? r + q : r;
         } else {  // V2: [0, 8q) invariant, approximate high product, one correction
           U = x[k];
           U = U >= 2 * q2 ? U - 2 * q2 : U;
@@ -64,12 +69,17 @@ int main() {
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  for (int v = 0; v < 3; ++v) {
+  const u64 q40 = 1099511480321ull;  // a 40-bit NTT prime (any q < 2^42 works for V3)
+  const u64 w40 = 123456789123ull % q40;
+  const u64 wp40 = (u64)(((unsigned __int128)w40 << 64) / q40);
+  const double wq40 = (double)w40 / (double)q40;
+  for (int v = 0; v < 4; ++v) {
     for (int rep = 0; rep < 2; ++rep) {
       cudaEventRecord(a);
-      if (v == 0) bench<0><<<blocks, threads>>>(out, in, q, w, wp, iters);
-      else if (v == 1) bench<1><<<blocks, threads>>>(out, in, q, w, wp, iters);
-      else bench<2><<<blocks, threads>>>(out, in, q, w, wp, iters);
+      if (v == 0) bench<0><<<blocks, threads>>>(out, in, q40, w40, wp40, iters, wq40);
+      else if (v == 1) bench<1><<<blocks, threads>>>(out, in, q40, w40, wp40, iters, wq40);
+      else if (v == 2) bench<2><<<blocks, threads>>>(out, in, q40, w40, wp40, iters, wq40);
+      else bench<3><<<blocks, threads>>>(out, in, q40, w40, wp40, iters, wq40);
       cudaEventRecord(b);
       cudaEventSynchronize(b);
       float ms;
