@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(kWarps * 32) ntt_col_pass(LimbBatch B, Tabs T)
 // all warps busy. TCF = 8 gives 64-byte row segments for big batches; TCF = 2
 // gives 4x more CTAs for single-ciphertext launches.
 template <int LOGR, int LOGC, int TCF, int CPW>
-__global__ void __launch_bounds__(TCF / CPW * 32, TCF / CPW == 8 ? (CPW == 1 ? 3 : 2) : 8)
+__global__ void __launch_bounds__(TCF / CPW * 32, TCF / CPW == 8 ? (CPW == 1 ? 3 : 2) : (TCF / CPW == 4 ? 6 : 8))
     fused_col_kernel(FusedColArgs A, Tabs T) {
   // CPW columns per warp (TCF / CPW warps): the column transforms of one warp
   // run interleaved (shared twiddles, CPW x the independent butterflies)
@@ -636,6 +636,8 @@ void run_fused(Context& c, const FusedColArgs& a) {
   if ((size_t)a.count * ((1u << LOGC) / 8) >= 444) {
     if (c.fused_cpw == 2 && (1 << LOGC) >= 16)
       run_fused_t<LOGR, LOGC, 16, 2>(c, a);
+    else if (c.fused_cpw == 4)  // A/B: 4-column, 4-warp CTAs
+      run_fused_t<LOGR, LOGC, 4, 1>(c, a);
     else
       run_fused_t<LOGR, LOGC, 8, 1>(c, a);
     return;
