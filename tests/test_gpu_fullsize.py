@@ -115,3 +115,90 @@ def test_llama_attention_context_2048_matches_float64():
     p /= p.sum(axis=1, keepdims=True)
     ref = np.concatenate([p[h] @ V[:, h * dh:(h + 1) * dh] for h in range(H)])
     assert np.max(np.abs(out - ref)) < 1e-3
+
+
+def _vmm_check(sf, be, N, rows, cols, level, seed, want_rot, want_ctpt):
+    rng = np.random.default_rng(seed)
+    W = rng.normal(size=(rows, cols)) / np.sqrt(rows)
+    x = rng.normal(size=rows)
+    d_in = 1 << (rows - 1).bit_length()
+    t_in = N // d_in
+    s = np.zeros(N)
+    s[np.arange(rows) * t_in] = x
+    ct = be.encrypt(s, level, sf.make_interleaved(d_in, N, 0), seed=seed)
+    be.ledger.reset()
+    y = sf.vmm_interleaved(be, ct, W, bsgs=True)
+    t_out = N // (1 << (cols - 1).bit_length())
+    got = be.decrypt(y)[np.arange(cols) * t_out]
+    assert np.max(np.abs(got - x @ W)) < 1e-3
+    c = be.ledger.totals()
+    assert (c.rotations, c.ct_pt_mults) == (want_rot, want_ctpt)
+
+
+def test_c1_gpt2_vmm_768_ring_2_15():
+    # BASELINE configs[0]: 1x768 x 768x768 at N = 2^15 (2^14 slots): 22 rot / 64 ct-pt
+    import paper_2602_11470_b200 as sf
+    be = sf.Backend(16384, 4, alpha=2, seed=1)
+    _vmm_check(sf, be, 16384, 768, 768, 4, 11, 22, 64)
+
+
+def test_c3_gpt2_layer_linear_path_ring_2_16():
+    # BASELINE configs[2]: QKV + out-proj 768^2, FFN 768 -> 3072 -> 768 at N = 2^16
+    import paper_2602_11470_b200 as sf
+    be = sf.Backend(SLOTS, 4, alpha=2, seed=2)
+    for i in range(4):
+        _vmm_check(sf, be, SLOTS, 768, 768, 4, 20 + i, 20, 32)
+    _vmm_check(sf, be, SLOTS, 768, 3072, 4, 30, 29, 128)
+    _vmm_check(sf, be, SLOTS, 3072, 768, 4, 31, 29, 128)
+
+
+def test_c2_gpt2_attention_grown_by_appends_ring_2_15():
+    # BASELINE configs[1]: 12 heads x 64 (run as H = 16 with 4 zero heads),
+    # the cache grown token by token through k_append / make_v_pieces / v_append, one
+    # decode query at n' = 128 and at n' = 1024 (SURVEY App. A counts at 2^14 slots)
+    import paper_2602_11470_b200 as sf
+    N, d, H, real = 16384, 1024, 16, 12
+    cfg = sf.AttentionConfig(N, d, H, 0, 1024)
+    be = sf.Backend(N, 5, alpha=2, seed=3)
+    t, gt, dh = cfg.t, cfg.group_tokens, cfg.d_head
+    rng = np.random.default_rng(4)
+    K = np.zeros((1024, d))
+    V = np.zeros((1024, d))
+    K[:, :real * dh] = rng.normal(size=(1024, real * dh)) * 0.15
+    V[:, :real * dh] = rng.normal(size=(1024, real * dh))
+    q = np.zeros(d)
+    q[:real * dh] = rng.normal(size=real * dh) * 0.15
+    cache = sf.KVCache(be, cfg)
+    qs = np.zeros(N)
+    qs[np.arange(d) * t] = q
+    qc = be.encrypt(qs, 3, sf.make_interleaved(d, N, 0, H), seed=5)
+    want_counts = {128: ((8, 8, 59), (71, 74, 1)), 1024: ((64, 64, 451), (127, 130, 1))}
+    for u in range(1024):
+        vs = np.full(N, 0.5)  # deferred garbage outside the token's lane
+        vs[np.arange(d) * t + u % t] = V[u]
+        vly = sf.make_interleaved(d, N, u % t, H).with_(deferred_mask=True)
+        cache = sf.v_append(be, cache, sf.make_v_pieces(be, cache, be.encrypt(vs, 4, vly, seed=100 + u), u))
+        ks = np.zeros(N)
+        ks[np.arange(d) * t + u % t] = K[u]
+        cache = sf.k_append(be, cache, be.encrypt(ks, 3, sf.make_interleaved(d, N, u % t, H), seed=3000 + u))
+        n = u + 1
+        if n not in want_counts:
+            continue
+        be.ledger.reset()
+        maps = sf.qk_dot(be, qc, cache)
+        c1 = be.ledger.totals()
+        probs = [be.bootstrap(p_, 3) for p_ in sf.exact_softmax_maps(be, maps, cfg, n)]
+        be.ledger.reset()
+        att = sf.softmax_times_v(be, probs, cache)
+        c2 = be.ledger.totals()
+        (a, b_, c_), (e, f, g) = want_counts[n]
+        assert (c1.ct_ct_mults, c1.ct_pt_mults, c1.rotations) == (a, b_, c_)
+        assert (c2.ct_ct_mults, c2.rotations, c2.ct_pt_mults) == (e, f, g)
+        out = be.decrypt(att)[np.arange(d) * t]
+        ref = np.zeros(d)
+        for h in range(H):
+            sc = K[:n, h * dh:(h + 1) * dh] @ q[h * dh:(h + 1) * dh]
+            p = np.exp(sc - sc.max())
+            p /= p.sum()
+            ref[h * dh:(h + 1) * dh] = p @ V[:n, h * dh:(h + 1) * dh]
+        assert np.max(np.abs(out - ref)) < 1e-3
