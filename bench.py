@@ -220,7 +220,7 @@ class LlamaLayer:
         every rank. Word-identical to step() for any world size."""
         be, sf = self.be, self.sf
         x, h7, h3, h1, p0, p1 = inputs or self.inputs
-        q, k, v = sh.vmm(x, self.wq), sh.vmm(x, self.wk), sh.vmm(x, self.wv)
+        q, k, v = sh.vmm_multi(x, [self.wq, self.wk, self.wv])
         qr = sf.rope_apply(be, q, self.cfg, self.pos)
         kr = sf.rope_apply(be, k, self.cfg, self.pos)
         cache = sf.v_append(be, self.cache, sf.make_v_pieces(be, self.cache, v, self.pos))
@@ -228,16 +228,20 @@ class LlamaLayer:
         maps = sh.qk_dot(qr, cache)
         att = sh.softmax_times_v([p0, p1], cache)
         o = sh.vmm(h7, self.wo)
-        g, u = sh.vmm(h3, self.wg), sh.vmm(h3, self.wu)
+        g, u = sh.vmm_multi(h3, [self.wg, self.wu])
         dn = sh.vmm(h1, self.wd)
         return [q, k, v, maps[0], att, o, g, u, dn]
 
 
 def run_sharded(args, be, sf, layer, dist, rank, world, clk):
-    """--shard: strong scaling of ONE token over the ranks (latency), eager."""
+    """--shard: strong scaling of ONE token over the ranks (latency). Default:
+    the exchange on the library stream (shard.StreamSharded, csrc/comm.cpp) and
+    the whole sharded step captured into one CUDA graph; --shard-host: the
+    torch-stream exchange (shard.Sharded), eager."""
     from paper_2602_11470_b200 import shard
     import torch
-    sh = shard.Sharded(be)
+    stream = not args.shard_host
+    sh = shard.StreamSharded(be) if stream else shard.Sharded(be)
     ref = layer.step()  # the single-device step on every rank, for the bit-exactness check
     got = layer.step_sharded(sh)
     exact = all(np.array_equal(a.data(), b.data()) for a, b in zip(ref, got))
@@ -245,36 +249,62 @@ def run_sharded(args, be, sf, layer, dist, rank, world, clk):
         layer.step_sharded(sh)
     be.synchronize()
     torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        t = torch.tensor([v], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # eager (host-issued) timing, for the record
     dist.barrier()
-    clk.mark()
     be.event_record(0)
     t_w = time.perf_counter()
     for _ in range(args.steps):
-        outs = layer.step_sharded(sh)
+        layer.step_sharded(sh)
     be.event_record(1)
-    ms = be.event_elapsed_ms(0, 1) / args.steps
+    ms_eager = max_over_ranks(be.event_elapsed_ms(0, 1) / args.steps)
     be.synchronize()
     wall = (time.perf_counter() - t_w) * 1e3 / args.steps
+
+    graph = None
+    if stream:  # the whole sharded step (NCCL all-gathers included) in one graph
+        graph, gouts = be.capture(layer.step_sharded, sh)
+        graph.launch()
+        be.synchronize()
+        exact = exact and all(np.array_equal(a.data(), b.data()) for a, b in zip(ref, gouts))
+    run = graph.launch if graph else (lambda: layer.step_sharded(sh))
+    be.synchronize()
+    torch.cuda.synchronize()
+    dist.barrier()
+    clk.mark()
+    l0 = be.kernel_launches()
+    be.event_record(0)
+    for _ in range(args.steps):
+        run()
+    be.event_record(1)
+    ms = max_over_ranks(be.event_elapsed_ms(0, 1) / args.steps)
+    be.synchronize()
+    launches = (be.kernel_launches() - l0) // args.steps
     clk.__exit__()
-    t = torch.tensor([ms], device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
     ex = torch.tensor([1 if exact else 0], device="cuda")
     dist.all_reduce(ex, op=dist.ReduceOp.MIN)
-    host_in = [(c.data(), c.level, c.scale, c.layout) for c in layer.inputs]
+
+    # e2e: inputs from host memory every step, results read back
+    host_in = [c.data() for c in layer.inputs]
+    outs = gouts if graph else None
     be.synchronize()
     dist.barrier()
     t_e = time.perf_counter()
     for _ in range(args.steps):
-        for slot, (w, *_r) in zip(layer.inputs, host_in):
+        for slot, w in zip(layer.inputs, host_in):
             be.refill(slot, w)
-        outs = layer.step_sharded(sh)
+        if graph:
+            graph.launch()
+        else:
+            outs = layer.step_sharded(sh)
         res = [outs[4].data(), outs[8].data()]
     be.synchronize()
-    e2e = (time.perf_counter() - t_e) * 1e3 / args.steps
-    t = torch.tensor([e2e], device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    e2e = float(t.item())
+    e2e = max_over_ranks((time.perf_counter() - t_e) * 1e3 / args.steps)
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(ms, 3), "unit": "ms/token", "n_gpus": world, "steps": args.steps,
@@ -286,14 +316,17 @@ def run_sharded(args, be, sf, layer, dist, rank, world, clk):
                        "parallelism": f"sharded{world} (giant / key-ct / pair groups, NCCL all-gather + mod-add)",
                        "l2": "working set >> 126 MB L2; no flush needed"},
             "sharded_bit_exact_vs_single_device": bool(ex.item()),
-            "wall_ms_per_step_rank0": round(wall, 3),
+            "eager_ms_per_step": round(ms_eager, 3), "wall_ms_per_step_rank0_eager": round(wall, 3),
             "e2e": {"value": round(e2e, 3), "unit": "ms/token",
-                    "h2d_bytes_per_step": int(sum(w.nbytes for w, *_ in host_in)),
+                    "h2d_bytes_per_step": int(sum(w.nbytes for w in host_in)),
                     "d2h_bytes_per_step": int(sum(r.nbytes for r in res))},
-            "gpu_launches": None, "clocks": clk.summary(), "cpu_baseline": None,
-            "execution": "eager (host-issued; NCCL exchanges on torch's stream between library launches)",
+            "gpu_launches": int(launches) if graph else None, "clocks": clk.summary(), "cpu_baseline": None,
+            "execution": ("one CUDA graph per step; NCCL all-gathers on the library stream inside it" if graph else
+                          "eager (host-issued; NCCL exchanges on torch's stream between library launches)"),
         }
         print(json.dumps(line), flush=True)
+    if stream:
+        sh.close()
 
 
 # ---------------------------------------------------------------- reference arm
@@ -352,6 +385,8 @@ def main():
     ap.add_argument("--quiet", action="store_true")
     ap.add_argument("--shard", action="store_true",
                     help="strong scaling: split ONE token over the ranks (default: one replica per GPU)")
+    ap.add_argument("--shard-host", action="store_true",
+                    help="with --shard: exchange on torch's stream (eager) instead of the library stream + graph")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))

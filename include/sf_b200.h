@@ -256,6 +256,31 @@ sf_status sf_softmax_times_v_partial(sf_context* ctx, const sf_ct* const* probs,
 sf_status sf_softmax_times_v_finish(sf_context* ctx, const sf_ct* const* parts01, const sf_ct* const* parts2,
                                     int n, const sf_kvcache* cache, sf_ct** out);
 sf_status sf_sum_partials(sf_context* ctx, const sf_ct* const* parts, int n, sf_ct** out);
+/* multi-VMM of one input (sf_vmm_interleaved_multi) split the same way: one
+ * partial accumulator per plan; finish = batched reduce ladders + masks */
+sf_status sf_vmm_multi_partial(sf_context* ctx, const sf_ct* x, sf_vmm_plan* const* plans, int k, int rank,
+                               int world, sf_ct** outs);
+sf_status sf_vmm_multi_finish(sf_context* ctx, const sf_ct* const* accs, sf_vmm_plan* const* plans, int k,
+                              int mask_output, sf_ct** outs);
+/* Sharded operators with the exchange on the library stream: NCCL (resolved at
+ * run time from the process's libnccl.so.2) all-gathers the partials on the
+ * context's stream, so partial -> exchange -> mod-add -> tail is one stream of
+ * work and a whole sharded step can be captured by sf_graph_begin/end (run the
+ * step once eagerly first: the exchange caches each call site's metadata).
+ * sf_comm_unique_id (rank 0) fills 128 bytes the caller broadcasts; every
+ * rank then calls sf_comm_init with its rank and the world size.
+ * Results are bit-identical to the unsharded sf_vmm / sf_qk_dot /
+ * sf_softmax_times_v. */
+sf_status sf_comm_unique_id(uint8_t id_out[128]);
+sf_status sf_comm_init(sf_context* ctx, const uint8_t id[128], int rank, int world);
+sf_status sf_comm_destroy(sf_context* ctx);
+sf_status sf_vmm_sharded(sf_context* ctx, const sf_ct* x, const sf_vmm_plan* plan, int mask_output, sf_ct** out);
+sf_status sf_vmm_multi_sharded(sf_context* ctx, const sf_ct* x, sf_vmm_plan* const* plans, int k, int mask_output,
+                               sf_ct** outs);
+sf_status sf_qk_dot_sharded(sf_context* ctx, const sf_ct* q, const sf_kvcache* cache, sf_ct** maps_out,
+                            int* n_maps);
+sf_status sf_softmax_times_v_sharded(sf_context* ctx, const sf_ct* const* probs, int n_probs,
+                                     const sf_kvcache* cache, sf_ct** out);
 /* device words of a ciphertext for peer/NCCL exchange: c0 and c1 each
  * (level+1)*n words; the view stays valid while the handle is alive */
 sf_status sf_ct_device_view(const sf_ct* ct, uint64_t** c0, uint64_t** c1, size_t* words_per_poly);

@@ -120,6 +120,15 @@ SIGNATURES = {
     "sf_softmax_times_v_partial": (st, [vp, vpp, C.c_int, vp, C.c_int, C.c_int, vpp]),
     "sf_softmax_times_v_finish": (st, [vp, vpp, vpp, C.c_int, vp, vpp]),
     "sf_sum_partials": (st, [vp, vpp, C.c_int, vpp]),
+    "sf_vmm_multi_partial": (st, [vp, vp, vpp, C.c_int, C.c_int, C.c_int, vpp]),
+    "sf_vmm_multi_finish": (st, [vp, vpp, vpp, C.c_int, C.c_int, vpp]),
+    "sf_vmm_multi_sharded": (st, [vp, vp, vpp, C.c_int, C.c_int, vpp]),
+    "sf_comm_unique_id": (st, [C.c_char_p]),
+    "sf_comm_init": (st, [vp, C.c_char_p, C.c_int, C.c_int]),
+    "sf_comm_destroy": (st, [vp]),
+    "sf_vmm_sharded": (st, [vp, vp, vp, C.c_int, vpp]),
+    "sf_qk_dot_sharded": (st, [vp, vp, vp, vpp, ip]),
+    "sf_softmax_times_v_sharded": (st, [vp, vpp, C.c_int, vp, vpp]),
     "sf_ct_device_view": (st, [vp, C.POINTER(u64p), C.POINTER(u64p), C.POINTER(C.c_size_t)]),
     "sf_ct_from_device": (st, [vp, C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_int, C.POINTER(SfLayout), vpp]),
     "sf_event_record": (st, [vp, C.c_int]),

@@ -409,6 +409,35 @@ sf_status sf_vmm_interleaved_multi(sf_context* ctx, const sf_ct* x, sf_vmm_plan*
   });
 }
 
+sf_status sf_vmm_multi_partial(sf_context* ctx, const sf_ct* x, sf_vmm_plan* const* plans, int k, int rank,
+                               int world, sf_ct** outs) {
+  return guard([&] {
+    std::vector<sf::VmmPlan*> ps(k);
+    for (int i = 0; i < k; ++i) ps[i] = plans[i]->p.get();
+    auto v = sf::vmm_multi_partial(*ctx->c, x->v, ps, rank, world);
+    for (int i = 0; i < k; ++i) outs[i] = wrap(std::move(v[i]));
+  });
+}
+sf_status sf_vmm_multi_finish(sf_context* ctx, const sf_ct* const* accs, sf_vmm_plan* const* plans, int k,
+                              int mask_output, sf_ct** outs) {
+  return guard([&] {
+    std::vector<sf::VmmPlan*> ps(k);
+    std::vector<sf::Ct> a;
+    for (int i = 0; i < k; ++i) ps[i] = plans[i]->p.get(), a.push_back(accs[i]->v);
+    auto v = sf::vmm_multi_finish(*ctx->c, a, ps, mask_output != 0);
+    for (int i = 0; i < k; ++i) outs[i] = wrap(std::move(v[i]));
+  });
+}
+sf_status sf_vmm_multi_sharded(sf_context* ctx, const sf_ct* x, sf_vmm_plan* const* plans, int k, int mask_output,
+                               sf_ct** outs) {
+  return guard([&] {
+    std::vector<sf::VmmPlan*> ps(k);
+    for (int i = 0; i < k; ++i) ps[i] = plans[i]->p.get();
+    auto v = sf::vmm_multi_sharded(*ctx->c, x->v, ps, mask_output != 0);
+    for (int i = 0; i < k; ++i) outs[i] = wrap(std::move(v[i]));
+  });
+}
+
 // --- wire / on-disk formats (wire.cpp)
 sf_status sf_vmm_plan_create_from_file(sf_context* ctx, const char* dir, const char* name, int level, int in_offset,
                                        int out_offset, int bsgs, sf_vmm_plan** out) {
@@ -673,6 +702,44 @@ sf_status sf_sum_partials(sf_context* ctx, const sf_ct* const* parts, int n, sf_
     std::vector<const sf::Ct*> p;
     for (int i = 0; i < n; ++i) p.push_back(&parts[i]->v);
     *out = wrap(sf::sum_partials(*ctx->c, p));
+  });
+}
+sf_status sf_comm_unique_id(uint8_t id_out[128]) {
+  return guard([&] {
+    need(id_out, "id_out");
+    sf::comm_unique_id(id_out);
+  });
+}
+sf_status sf_comm_init(sf_context* ctx, const uint8_t id[128], int rank, int world) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(id, "id");
+    sf::comm_init(*ctx->c, id, rank, world);
+  });
+}
+sf_status sf_comm_destroy(sf_context* ctx) {
+  return guard([&] {
+    need(ctx, "ctx");
+    sf::comm_destroy(*ctx->c);
+  });
+}
+sf_status sf_vmm_sharded(sf_context* ctx, const sf_ct* x, const sf_vmm_plan* plan, int mask_output, sf_ct** out) {
+  return guard([&] { *out = wrap(sf::vmm_sharded(*ctx->c, x->v, *plan->p, mask_output != 0)); });
+}
+sf_status sf_qk_dot_sharded(sf_context* ctx, const sf_ct* q, const sf_kvcache* cache, sf_ct** maps_out,
+                            int* n_maps) {
+  return guard([&] {
+    auto maps = sf::qk_dot_sharded(*ctx->c, q->v, cache->kv);
+    *n_maps = (int)maps.size();
+    for (size_t i = 0; i < maps.size(); ++i) maps_out[i] = wrap(std::move(maps[i]));
+  });
+}
+sf_status sf_softmax_times_v_sharded(sf_context* ctx, const sf_ct* const* probs, int n_probs,
+                                     const sf_kvcache* cache, sf_ct** out) {
+  return guard([&] {
+    std::vector<sf::Ct> p;
+    for (int i = 0; i < n_probs; ++i) p.push_back(probs[i]->v);
+    *out = wrap(sf::softmax_times_v_sharded(*ctx->c, p, cache->kv));
   });
 }
 sf_status sf_ct_device_view(const sf_ct* ct, uint64_t** c0, uint64_t** c1, size_t* words_per_poly) {

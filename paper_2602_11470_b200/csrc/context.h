@@ -161,6 +161,10 @@ struct Context {
   // capturing become graph memory nodes; frees of older buffers are deferred
   // to graph destruction (a replay still reads them).
   bool capturing = false;
+  // sharded ops (comm.cpp): NCCL communicator on this context's stream
+  void* comm = nullptr;
+  int rank = 0, world = 1;
+  std::map<std::string, std::vector<u64>> comm_hdr, comm_meta;
   std::vector<std::pair<u64*, size_t>> capture_deferred;
   long long graph_launch_base = 0;
   bool ks_row = true;  // fused key-switch row stage

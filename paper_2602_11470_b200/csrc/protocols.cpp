@@ -265,11 +265,8 @@ Ct vmm_finish(Context& c, const Ct& acc_in, VmmPlan& plan, bool mask_output) {
 // the preprocess ladder and the hoisted baby steps, which depend on x, t_in,
 // t_out and b alone -- runs once, and the per-call work (MACs, rescales, giant
 // rotation sums, reduce ladders, masks) runs as batched launches.
-std::vector<Ct> vmm_interleaved_multi(Context& c, const Ct& x, const std::vector<VmmPlan*>& plans, bool mask_output) {
-  SF_HPROF("vmm_interleaved_multi");
-  const int P = (int)plans.size();
-  std::vector<Ct> out;
-  require(P >= 1, kShapeMismatch, "vmm_multi: no plans");
+static bool vmm_multi_shares(Context& c, const Ct& x, const std::vector<VmmPlan*>& plans) {
+  require(!plans.empty(), kShapeMismatch, "vmm_multi: no plans");
   bool share = !x.zero;
   for (VmmPlan* p : plans) {
     vmm_check_input(c, x, *p);
@@ -278,47 +275,69 @@ std::vector<Ct> vmm_interleaved_multi(Context& c, const Ct& x, const std::vector
             a.k == b0.k && p->bg.baby == plans[0]->bg.baby && p->bg.giant == plans[0]->bg.giant &&
             !(p->bg.baby > 64 || p->bg.giant > 64 || a.k > 2048 || c.n < 64);
   }
-  if (!share) {
-    for (VmmPlan* p : plans) out.push_back(vmm_interleaved(c, x, *p, mask_output));
+  return share;
+}
+
+// Steps 1-4 of every call (ladder, babies, MACs, giant rotation sums) for the
+// giant groups rank owns; the ladder and babies are input-only (shared by the
+// calls, replicated on every rank and charged on rank 0).
+std::vector<Ct> vmm_multi_partial(Context& c, const Ct& x, const std::vector<VmmPlan*>& plans, int rank, int world) {
+  SF_HPROF("vmm_multi_partial");
+  require(world >= 1 && rank >= 0 && rank < world, kInvalidTarget, "vmm: bad rank/world");
+  const int P = (int)plans.size();
+  std::vector<Ct> out;
+  if (!vmm_multi_shares(c, x, plans)) {
+    for (VmmPlan* p : plans) out.push_back(vmm_partial(c, x, *p, rank, world));
     return out;
   }
+  const bool lead = rank == 0;
   const VmmShape& s0 = plans[0]->s;
   const long long unit = (long long)s0.t_in * s0.t_out;
   const int limbs = x.limbs, b = plans[0]->bg.baby, giants = plans[0]->bg.giant;
   // 1. ladder (vmm.cpp:190-193), charged once per call
   const std::vector<int> lr = ladder_rots(s0);
-  for (int r : lr)
-    if (pos_mod(r, c.slots) != 0) c.ledger.rot(false, P);
-  c.ledger.add((long long)P * lr.size());
+  if (lead) {
+    for (int r : lr)
+      if (pos_mod(r, c.slots) != 0) c.ledger.rot(false, P);
+    c.ledger.add((long long)P * lr.size());
+  }
   Ct stair = fold_steps_batch(c, {&x}, {lr}, false)[0];
   // 2. hoisted babies (vmm.cpp:208-209), charged once per call
   std::vector<RotJob> jobs;
   for (int g1 = 1; g1 < b; ++g1) {
     jobs.push_back({0, (int)(g1 * unit)});
-    if (pos_mod(g1 * unit, c.slots) != 0) c.ledger.rot(true, P);
+    if (lead && pos_mod(g1 * unit, c.slots) != 0) c.ledger.rot(true, P);
+  }
+  std::vector<int> mine;  // whole giant groups r = g2 mod kGiantGroups with r mod world == rank
+  for (int g2 = 0; g2 < giants; ++g2)
+    if ((g2 % kGiantGroups) % world == rank) mine.push_back(g2);
+  if (mine.empty()) {
+    for (int pi = 0; pi < P; ++pi) out.push_back(zeros(c, x.level() - 1));
+    return out;
   }
   std::vector<Ct> baby{stair};
   for (Ct& r : rotate_batch(c, {&stair}, jobs, true, false)) baby.push_back(std::move(r));
-  // 3. every call's fused MAC over all giants, then one batched rescale
-  std::vector<Ct> partial((size_t)P * giants);
+  // 3. every call's fused MAC over the owned giants, then one batched rescale
+  const int G = (int)mine.size();
+  std::vector<Ct> partial((size_t)P * G);
   for (int pi = 0; pi < P; ++pi) {
     const std::vector<Pt>& diag = plans[pi]->diagonals(limbs);
     VmmMacArgs A;
     A.n = c.n;
     A.b = b;
-    A.giants = giants;
+    A.giants = G;
     A.k = (int)s0.k;
     for (int g1 = 0; g1 < b; ++g1) A.baby0[g1] = baby[g1].c0(), A.baby1[g1] = baby[g1].c1(c.n);
     for (long long g = 0; g < s0.k; ++g) A.pt[g] = diag[g].buf->p;
-    for (int g2 = 0; g2 < giants; ++g2) {
-      const int cnt = (int)std::min<long long>(b, s0.k - (long long)g2 * b);
+    for (int i = 0; i < G; ++i) {
+      const int cnt = (int)std::min<long long>(b, s0.k - (long long)mine[i] * b);
       c.ledger.ctpt(cnt);
       c.ledger.add(cnt - 1);
-      Ct& pt = partial[(size_t)pi * giants + g2];
+      Ct& pt = partial[(size_t)pi * G + i];
       pt = alloc_ct(c, limbs, stair.scale * (double)c.primes[limbs - 1]);
-      A.gidx[g2] = g2;
-      A.out0[g2] = pt.c0();
-      A.out1[g2] = pt.c1(c.n);
+      A.gidx[i] = mine[i];
+      A.out0[i] = pt.c0();
+      A.out1[i] = pt.c1(c.n);
     }
     b_vmm_mac(c, A, limbs);
   }
@@ -326,33 +345,42 @@ std::vector<Ct> vmm_interleaved_multi(Context& c, const Ct& x, const std::vector
   for (auto& p : partial) pp.push_back(&p);
   std::vector<Ct> resc = rescale_batch(c, pp);
   for (auto& r : resc) r.scale = stair.scale, r.layout.reset();
-  // 4. giant alignment + sum: the groups of every call in one batch
+  // 4. giant alignment + sum: the owned groups of every call in one batch
   std::vector<std::vector<SumTerm>> groups;
   std::vector<int> gowner;
   for (int pi = 0; pi < P; ++pi)
     for (int r = 0; r < std::min(kGiantGroups, giants); ++r) {
+      if (r % world != rank) continue;
       groups.emplace_back();
       gowner.push_back(pi);
-      for (int g2 = r; g2 < giants; g2 += kGiantGroups)
-        groups.back().push_back({&resc[(size_t)pi * giants + g2], (int)(((long long)g2 * b * unit) % c.slots)});
+      for (int i = 0; i < G; ++i)
+        if (mine[i] % kGiantGroups == r)
+          groups.back().push_back({&resc[(size_t)pi * G + i], (int)(((long long)mine[i] * b * unit) % c.slots)});
     }
   std::vector<Ct> gs = rot_sum_batch(c, groups, false);
-  std::vector<Ct> acc(P);
   for (int pi = 0; pi < P; ++pi) {
     std::vector<const Ct*> ap;
     for (size_t i = 0; i < gs.size(); ++i)
       if (gowner[i] == pi) ap.push_back(&gs[i]);
-    acc[pi] = sum_cts(c, ap);
+    out.push_back(sum_cts(c, ap));
   }
-  // 5. reduce ladders (vmm.cpp:226-230), one batched rotation + addition per step
-  {
+  return out;
+}
+
+// Steps 5-6 of every call on the summed partials: batched reduce ladders, masks.
+std::vector<Ct> vmm_multi_finish(Context& c, const std::vector<Ct>& accs, const std::vector<VmmPlan*>& plans,
+                                 bool mask_output) {
+  SF_HPROF("vmm_multi_finish");
+  const int P = (int)plans.size();
+  require((int)accs.size() == P, kShapeMismatch, "vmm_multi_finish: one accumulator per plan");
+  std::vector<Ct> acc;
+  {  // reduce ladders (vmm.cpp:226-230), one batched rotation + addition per step
     std::vector<const Ct*> src;
     std::vector<std::vector<int>> rr;
-    for (int pi = 0; pi < P; ++pi) src.push_back(&acc[pi]), rr.push_back(reduce_rots(plans[pi]->s));
+    for (int pi = 0; pi < P; ++pi) src.push_back(&accs[pi]), rr.push_back(reduce_rots(plans[pi]->s));
     acc = fold_steps_batch(c, src, rr);
   }
-  // 6. masks (vmm.cpp:233) and layouts
-  if (mask_output) {
+  if (mask_output) {  // masks (vmm.cpp:233)
     std::vector<Pt> mk;
     std::vector<const Ct*> xs;
     for (int pi = 0; pi < P; ++pi) {
@@ -372,6 +400,22 @@ std::vector<Ct> vmm_interleaved_multi(Context& c, const Ct& x, const std::vector
     acc[pi].layout = Layout{LayoutKind::Interleaved, sp.d_out, sp.t_out, sp.tau_out, 1, !mask_output};
   }
   return acc;
+}
+
+// Several VMMs of the SAME input x (the decode step's Q/K/V and gate/up
+// projections): identical to separate vmm_interleaved calls word for word and
+// in the ledger (each call's charges are applied), but the input-only work --
+// the preprocess ladder and the hoisted baby steps, which depend on x, t_in,
+// t_out and b alone -- runs once, and the per-call work (MACs, rescales, giant
+// rotation sums, reduce ladders, masks) runs as batched launches.
+std::vector<Ct> vmm_interleaved_multi(Context& c, const Ct& x, const std::vector<VmmPlan*>& plans, bool mask_output) {
+  SF_HPROF("vmm_interleaved_multi");
+  if (!vmm_multi_shares(c, x, plans)) {
+    std::vector<Ct> out;
+    for (VmmPlan* p : plans) out.push_back(vmm_interleaved(c, x, *p, mask_output));
+    return out;
+  }
+  return vmm_multi_finish(c, vmm_multi_partial(c, x, plans, 0, 1), plans, mask_output);
 }
 
 // vmm.cpp:179-236: the whole VMM on one GPU.

@@ -40,6 +40,9 @@ std::unique_ptr<VmmPlan> make_vmm_plan(Context& c, const double* W, int rows, in
                                        int out_offset, bool bsgs, bool encode = true);
 Ct vmm_interleaved(Context& c, const Ct& x, VmmPlan& plan, bool mask_output);
 // several VMMs of the same input (shared ladder + babies, batched tails)
+std::vector<Ct> vmm_multi_partial(Context& c, const Ct& x, const std::vector<VmmPlan*>& plans, int rank, int world);
+std::vector<Ct> vmm_multi_finish(Context& c, const std::vector<Ct>& accs, const std::vector<VmmPlan*>& plans,
+                                 bool mask_output);
 std::vector<Ct> vmm_interleaved_multi(Context& c, const Ct& x, const std::vector<VmmPlan*>& plans, bool mask_output);
 // sharded form: partial over the giant steps g2 = rank mod world, then (after
 // the exchange's modular sum) the reduce ladder + mask
@@ -92,6 +95,15 @@ PrefillScores prefill_scores(Context& c, const std::vector<Ct>& xs, VmmPlan& wq,
                              const AttnCfg& cfg, double base);
 // the probability-weighted values per prompt ct (after the caller's softmax)
 std::vector<Ct> prefill_attend(Context& c, const std::vector<std::vector<std::vector<Ct>>>& probs, const KV& cache);
+
+// --- sharded ops with the exchange on the library stream (comm.cpp) ------------
+void comm_unique_id(uint8_t* out128);
+void comm_init(Context& c, const uint8_t* id128, int rank, int world);
+void comm_destroy(Context& c);
+Ct vmm_sharded(Context& c, const Ct& x, VmmPlan& plan, bool mask_output);
+std::vector<Ct> vmm_multi_sharded(Context& c, const Ct& x, const std::vector<VmmPlan*>& plans, bool mask_output);
+std::vector<Ct> qk_dot_sharded(Context& c, const Ct& q, const KV& cache);
+Ct softmax_times_v_sharded(Context& c, const std::vector<Ct>& probs, const KV& cache);
 
 // --- wire / on-disk formats (wire.cpp) ---------------------------------------
 std::vector<double> load_weight(const std::string& dir, const std::string& name, int* rows, int* cols);

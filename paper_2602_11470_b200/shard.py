@@ -129,6 +129,23 @@ def sum_partials(be: Backend, parts: List[Ciphertext]) -> Ciphertext:
     return _ct(be, _native.lib().sf_sum_partials, arr, len(parts))
 
 
+def vmm_multi_partial(be: Backend, x: Ciphertext, plans, rank: int, world: int) -> List[Ciphertext]:
+    k = len(plans)
+    arr = (C.c_void_p * k)(*[p.h for p in plans])
+    outs = (C.c_void_p * k)()
+    _check(_native.lib().sf_vmm_multi_partial(be.ctx, x.h, arr, k, rank, world, outs))
+    return [Ciphertext(be, outs[i]) for i in range(k)]
+
+
+def vmm_multi_finish(be: Backend, accs: List[Ciphertext], plans, mask_output: bool = False) -> List[Ciphertext]:
+    k = len(plans)
+    a = (C.c_void_p * k)(*[x.h for x in accs])
+    arr = (C.c_void_p * k)(*[p.h for p in plans])
+    outs = (C.c_void_p * k)()
+    _check(_native.lib().sf_vmm_multi_finish(be.ctx, a, arr, k, int(mask_output), outs))
+    return [Ciphertext(be, outs[i]) for i in range(k)]
+
+
 def qk_dot_partial(be: Backend, q: Ciphertext, cache: KVCache, rank: int, world: int) -> List[Ciphertext]:
     gt = cache.cfg.group_tokens
     cap = max(1, (max(cache.n_prime, 1) + gt - 1) // gt)
@@ -166,6 +183,12 @@ class Sharded:
         parts = [p[0] for p in allgather_cts(self.be, [part], self.group)]
         return vmm_finish(self.be, sum_partials(self.be, parts), plan, mask_output)
 
+    def vmm_multi(self, x: Ciphertext, plans, mask_output: bool = False) -> List[Ciphertext]:
+        parts = vmm_multi_partial(self.be, x, plans, self.rank, self.world)
+        got = allgather_cts(self.be, parts, self.group)
+        accs = [sum_partials(self.be, [got[r][i] for r in range(self.world)]) for i in range(len(plans))]
+        return vmm_multi_finish(self.be, accs, plans, mask_output)
+
     def qk_dot(self, q: Ciphertext, cache: KVCache) -> List[Ciphertext]:
         maps = qk_dot_partial(self.be, q, cache, self.rank, self.world)
         got = allgather_cts(self.be, maps, self.group)
@@ -174,3 +197,49 @@ class Sharded:
     def softmax_times_v(self, probs, cache: KVCache) -> Ciphertext:
         part = softmax_times_v_partial(self.be, probs, cache, self.rank, self.world)
         return softmax_times_v_finish(self.be, allgather_cts(self.be, part, self.group), cache)
+
+
+class StreamSharded:
+    """The sharded operators with the exchange on the library stream
+    (csrc/comm.cpp): NCCL's all-gather is issued on the context stream, so a
+    sharded step has no host synchronisation and can be captured whole into a
+    CUDA graph (Backend.capture). The communicator is bootstrapped over the
+    torch.distributed group (rank 0's NCCL unique id is broadcast); run each
+    step once eagerly before capturing it (the exchange caches the call sites'
+    ciphertext metadata on that first call)."""
+
+    def __init__(self, be: Backend, group=None):
+        import torch.distributed as dist
+        self.be, self.group = be, group
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        uid = C.create_string_buffer(128)
+        if self.rank == 0:
+            _check(_native.lib().sf_comm_unique_id(uid))
+        box = [uid.raw]
+        dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        _check(_native.lib().sf_comm_init(be.ctx, box[0], self.rank, self.world))
+
+    def close(self) -> None:
+        _check(_native.lib().sf_comm_destroy(self.be.ctx))
+
+    def vmm(self, x: Ciphertext, plan: VmmPlan, mask_output: bool = False) -> Ciphertext:
+        return _ct(self.be, _native.lib().sf_vmm_sharded, x.h, plan.h, int(mask_output))
+
+    def vmm_multi(self, x: Ciphertext, plans, mask_output: bool = False) -> List[Ciphertext]:
+        k = len(plans)
+        arr = (C.c_void_p * k)(*[p.h for p in plans])
+        outs = (C.c_void_p * k)()
+        _check(_native.lib().sf_vmm_multi_sharded(self.be.ctx, x.h, arr, k, int(mask_output), outs))
+        return [Ciphertext(self.be, outs[i]) for i in range(k)]
+
+    def qk_dot(self, q: Ciphertext, cache: KVCache) -> List[Ciphertext]:
+        gt = cache.cfg.group_tokens
+        cap = max(1, (max(cache.n_prime, 1) + gt - 1) // gt)
+        maps = (C.c_void_p * cap)()
+        n = C.c_int()
+        _check(_native.lib().sf_qk_dot_sharded(self.be.ctx, q.h, cache.h, maps, C.byref(n)))
+        return [Ciphertext(self.be, maps[i]) for i in range(n.value)]
+
+    def softmax_times_v(self, probs, cache: KVCache) -> Ciphertext:
+        arr = (C.c_void_p * len(probs))(*[p.h for p in probs])
+        return _ct(self.be, _native.lib().sf_softmax_times_v_sharded, arr, len(probs), cache.h)

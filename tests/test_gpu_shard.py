@@ -30,6 +30,31 @@ def test_sharded_vmm_emulated(world):
     assert y.layout == full.layout
 
 
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_sharded_vmm_multi_emulated(world):
+    """Q/K/V-style multi-VMM of one input: shared ladder + babies, per-rank giant groups."""
+    import paper_2602_11470_b200 as sf
+    from paper_2602_11470_b200 import shard
+    N, L = 2048, 5
+    rng = np.random.default_rng(40 + world)
+    xs = np.zeros(N)
+    xs[np.arange(256) * 8] = rng.normal(size=256)
+    be = sf.Backend(N, L, alpha=2)
+    x = be.encrypt(xs, L, sf.make_interleaved(256, N, 0), seed=5)
+    plans = [sf.VmmPlan(be, rng.normal(size=(256, 128)) / 16, 256, 128, L, 0, 3, True) for _ in range(3)]
+    be.ledger.reset()
+    full = sf.vmm_interleaved_multi(be, x, plans)
+    want = be.ledger.totals()
+    be.ledger.reset()
+    parts = [shard.vmm_multi_partial(be, x, plans, r, world) for r in range(world)]
+    accs = [shard.sum_partials(be, [parts[r][i] for r in range(world)]) for i in range(3)]
+    ys = shard.vmm_multi_finish(be, accs, plans)
+    for y, f in zip(ys, full):
+        assert np.array_equal(y.data(), f.data())
+        assert y.layout == f.layout
+    assert be.ledger.totals() == want
+
+
 @pytest.mark.parametrize("world", [2, 4])
 def test_sharded_attention_emulated(world):
     import paper_2602_11470_b200 as sf
