@@ -453,11 +453,42 @@ void check_scales(const Ct* a, const Ct* b) {
   if (std::fabs(a->scale / b->scale - 1.0) > 1e-9) throw std::runtime_error("ScaleMismatch: add: operand scales differ");
 }
 
+Ct* rescale(const Ctx& c, const Ct* a);
+
+// bring a (at more limbs) to `limbs` limbs and scale `target`
+// -- drop to limbs+1, multiply by the integer m = round(target q / scale)
+// (a constant polynomial), rescale by q = primes[limbs]. Part of add/sub's
+// implicit level drop; no ledger charge.
+Ct* align_scale(const Ctx& c, const Ct* a, int limbs, double target) {
+  const u64 q = c.primes[limbs];
+  const u64 m = (u64)std::llround(target * (double)q / a->scale);
+  Ct* t = new_ct(c, limbs + 1, a->scale);
+  for (int p = 0; p < 2; ++p)
+    for (int l = 0; l <= limbs; ++l) {
+      const u64 ql = c.primes[l], ml = m % ql;
+      const u64* x = poly(c, a, p, l);
+      u64* o = poly(c, t, p, l);
+      for (int k = 0; k < c.n; ++k) o[k] = mulmod(x[k], ml, ql);
+    }
+  Ct* r = rescale(c, t);
+  delete t;
+  r->scale = a->scale * (double)m / (double)q;
+  return r;
+}
+
 Ct* addsub(const Ctx& c, const Ct* a, const Ct* b, bool sub) {
   const int limbs = std::min(a->limbs, b->limbs);
   if (a->zero && b->zero) {
     Ct* r = new_ct(c, limbs, 0.0);
     r->zero = true;
+    return r;
+  }
+  if (!a->zero && !b->zero && std::fabs(a->scale / b->scale - 1.0) > 1e-9 && a->limbs != b->limbs &&
+      a->d2.empty() && b->d2.empty()) {
+    const bool a_hi = a->limbs > b->limbs;
+    Ct* al = align_scale(c, a_hi ? a : b, limbs, a_hi ? b->scale : a->scale);
+    Ct* r = a_hi ? addsub(c, al, b, sub) : addsub(c, a, al, sub);
+    delete al;
     return r;
   }
   check_scales(a, b);

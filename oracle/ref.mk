@@ -2,7 +2,7 @@
 # from where they lie under /root/reference, into oracle/_ref/ (git-ignored,
 # NOT gpurun-ignored). TEST INFRASTRUCTURE: oracle/_ref is the checker and the
 # `--impl reference` CPU arm, never the product.
-#   make -f oracle/ref.mk            -> libslotforge_ref.so + 4 test binaries + golden dumper
+#   make -f oracle/ref.mk            -> libslotforge_ref.so + 5 test binaries + golden dumper
 #   make -f oracle/ref.mk check      -> runs the reference's own tests
 REF      ?= /root/reference/proj
 OUT      ?= oracle/_ref
@@ -10,9 +10,9 @@ JSON_INC ?= $(shell python3 -c "import os,sys; p=os.path.join(sys.prefix,'lib','
 CXX      ?= g++
 CXXFLAGS ?= -std=c++20 -O2 -fPIC -ffp-contract=off -w
 INC      := -I$(REF)/include -Ioracle/shim -I$(JSON_INC)
-SRCS     := engine layouts vmm kv_attention
+SRCS     := engine layouts vmm kv_attention nonlinear placement harness
 OBJS     := $(SRCS:%=$(OUT)/%.o)
-TESTS    := test_engine test_layouts test_vmm test_kv
+TESTS    := test_engine test_layouts test_vmm test_kv test_harness
 
 all: $(OUT)/libslotforge_ref.so $(TESTS:%=$(OUT)/%) $(OUT)/ref_golden $(OUT)/ref_bench
 

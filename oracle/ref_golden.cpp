@@ -12,6 +12,9 @@
 //   exact_softmax_maps         proj/src/kv_attention.cpp:395-412
 //   prefill (vmm_batch, rope_apply_batch, inner_rotate, exact_softmax_prefill_maps)
 //                              proj/src/kv_attention.cpp:119-129, 245-376, 414-454; vmm.cpp:30-43, 417-467
+//   harness ("harness" set): make_weights / seeded_prompt / plaintext_reference /
+//   plan_decode / run_generation (prefill_prompt + run_decode_step)
+//                              proj/src/harness.cpp:197-352, 425-659, 712-857, 943-1053
 #include <nlohmann/json.hpp>
 
 #include <cstdio>
@@ -21,6 +24,7 @@
 #include <vector>
 
 #include "slotforge/engine.hpp"
+#include "slotforge/harness.hpp"
 #include "slotforge/kv_attention.hpp"
 #include "slotforge/layouts.hpp"
 #include "slotforge/vmm.hpp"
@@ -256,6 +260,56 @@ json engine_case() {
               {"counted", be.ledger().totals().rotations}};
 }
 
+json mat_stats(const Matrix& m) {
+  double s = 0, s2 = 0;
+  for (long i = 0; i < m.size(); ++i) s += m.data()[i], s2 += m.data()[i] * m.data()[i];
+  return json{{"rows", m.rows()}, {"cols", m.cols()}, {"sum", s}, {"sumsq", s2},
+              {"head", vec_json(m.data(), std::min<long>(4, m.size()))},
+              {"last", m.data()[m.size() - 1]}};
+}
+json vec_stats(const Vector& v) {
+  double s = 0;
+  for (long i = 0; i < v.size(); ++i) s += v[i];
+  return json{{"n", v.size()}, {"sum", s}, {"head", vec_json(v.data(), std::min<long>(4, v.size()))}};
+}
+
+// One seeded generation run of the reference harness: the config, weight
+// fingerprints (Python port check), prompt, plaintext trace, the solver's plan
+// (the harness port takes the plan as input), the full Report (tokens, level
+// trace, per-phase ledger) and the prefill's final-block states.
+json harness_case(const ModelConfig& cfg, int n0, int gen_len) {
+  const ModelWeights w = make_weights(cfg);
+  const std::vector<int> prompt = seeded_prompt(cfg, n0);
+  const ReferenceTrace ref = plaintext_reference(cfg, w, prompt, gen_len);
+  const PlacementPlan plan = plan_decode(cfg, w, n0 + gen_len);
+  const Report rep = run_generation(cfg, w, prompt, gen_len, nullptr);
+  json wj;
+  wj["embedding"] = mat_stats(w.embedding);
+  json blocks = json::array();
+  for (const auto& b : w.blocks)
+    blocks.push_back(json{{"wq", mat_stats(b.wq)},         {"wk", mat_stats(b.wk)},
+                          {"wv", mat_stats(b.wv)},         {"wo", mat_stats(b.wo)},
+                          {"w_gate", mat_stats(b.w_gate)}, {"w_up", mat_stats(b.w_up)},
+                          {"w_down", mat_stats(b.w_down)}, {"gamma1", vec_stats(b.gamma1)},
+                          {"beta1", vec_stats(b.beta1)},   {"gamma2", vec_stats(b.gamma2)},
+                          {"beta2", vec_stats(b.beta2)}});
+  wj["blocks"] = blocks;
+  json states = json::array();
+  for (const auto& v : ref.final_states) states.push_back(v_json(v));
+  return json{{"kind", "harness"},
+              {"config", json::parse(cfg.to_json())},
+              {"n0", n0},
+              {"gen_len", gen_len},
+              {"weights", wj},
+              {"prompt", prompt},
+              {"ref_tokens", ref.tokens},
+              {"ref_final_states", states},
+              {"plan", json::parse(plan.to_json())},
+              {"plan_terminal_level", plan.terminal_level},
+              {"plan_bootstrap_count", plan.bootstrap_count},
+              {"report", json::parse(rep.to_json())}};
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -299,6 +353,20 @@ int main(int argc, char** argv) {
     cases.push_back(prefill_case(16, 8, 2, 11, seed++));
     cases.push_back(prefill_case(16, 4, 1, 1, seed++));
     cases.push_back(prefill_case(64, 16, 4, 13, seed++));
+  } else if (which == "harness") {
+    // test_harness.cpp: desk_config (d 64, H 4, 2 blocks, vocab 32, N 256, L 13)
+    // exact mode seeds 3 / 9 (prompt 8 + 8 generated; single-token prompt),
+    // and tiny_config (d 8, H 2, 1 block, N 32)
+    ModelConfig desk;
+    desk.mode = NonlinearMode::Exact;
+    desk.seed = 3;
+    cases.push_back(harness_case(desk, 8, 8));
+    desk.seed = 9;
+    cases.push_back(harness_case(desk, 1, 1));
+    ModelConfig tiny;
+    tiny.d = 8, tiny.H = 2, tiny.n_layers = 1, tiny.ffn_alpha = 2, tiny.vocab = 8, tiny.N = 32, tiny.L = 13;
+    tiny.seed = 11;
+    cases.push_back(harness_case(tiny, 5, 3));
   } else if (which == "medium") {
     // N = 2048 slots (ring degree 4096): the GPU parity size
     cases.push_back(vmm_case(2048, 64, 64, 0, 0, true, false, 7001));

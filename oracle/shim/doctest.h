@@ -181,6 +181,18 @@ inline int run_all() {
     }                                                                                   \
     doctest::detail::report(doctest_ok_, "CHECK_THROWS_AS", #expr, __FILE__, __LINE__); \
   } while (0)
+#define CHECK_NOTHROW(expr)                                                           \
+  do {                                                                                \
+    bool doctest_ok_ = true;                                                          \
+    try {                                                                             \
+      expr;                                                                           \
+    } catch (...) {                                                                   \
+      doctest_ok_ = false;                                                            \
+    }                                                                                 \
+    doctest::detail::report(doctest_ok_, "CHECK_NOTHROW", #expr, __FILE__, __LINE__); \
+  } while (0)
+#define CHECK_MESSAGE(cond, msg) \
+  doctest::detail::report(static_cast<bool>(cond), "CHECK_MESSAGE", #cond, __FILE__, __LINE__)
 #define CAPTURE(x) \
   const doctest::detail::Capture DOCTEST_UNIQUE(doctest_cap_)(std::string(#x " := ") + doctest::detail::to_str(x))
 

@@ -168,6 +168,7 @@ struct Context {
   std::vector<std::pair<u64*, size_t>> capture_deferred;
   long long graph_launch_base = 0;
   bool ks_row = true;  // fused key-switch row stage
+  int variant = 0;     // SF_VARIANT bit mask: kernel variants under A/B evaluation
   int fused_cpw = 1;   // columns per warp in batched fused column stages (SF_FUSED_CPW=1|2, for A/B timing) (SF_KS_ROW=0: separate passes, for A/B timing)
   std::vector<u64> primes;  // q0..qL, p0..p_{alpha-1}
   cudaStream_t stream = nullptr;

@@ -83,6 +83,7 @@ std::unique_ptr<Context> make_context(int slots, int L, int log_n, int alpha, in
   c->device = device;
   if (const char* e = std::getenv("SF_KS_ROW")) c->ks_row = std::atoi(e) != 0;
   if (const char* e = std::getenv("SF_FUSED_CPW")) c->fused_cpw = std::atoi(e);
+  if (const char* e = std::getenv("SF_VARIANT")) c->variant = std::atoi(e);
   c->delta = std::ldexp(1.0, scale_bits > 0 ? scale_bits : 40);
   c->primes = generate_primes(c->logn, L, q0_bits > 0 ? q0_bits : 60, scale_bits > 0 ? scale_bits : 40, c->alpha,
                               special_bits > 0 ? special_bits : 60);
@@ -328,11 +329,54 @@ void decrypt(Context& c, const Ct& a, double* out) {
 }
 
 // ------------------------------------------------------------------ evaluator
+// bring a (at more limbs) to `limbs` limbs and scale
+// `target`: drop to limbs+1, multiply by the integer m = round(target q /
+// scale) (a constant polynomial: m mod q_i at every NTT point), rescale by
+// q = primes[limbs]. Part of add/sub's implicit level drop (no ledger charge);
+// it lets the residual adds of a decoder block combine a fresh chain input
+// with a projection output whose scale went through ct x ct products.
+Ct align_scale(Context& c, const Ct& a, int limbs, double target) {
+  SF_HPROF("align_scale");
+  require(a.limbs > limbs, kScaleMismatch, "ScaleMismatch: align needs a spare level");
+  const u64 q = c.primes[limbs];
+  const u64 m = (u64)std::llround(target * (double)q / a.scale);
+  const std::string key = "const:" + std::to_string(m) + "@" + std::to_string(limbs + 1);
+  Pt p;
+  {
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto it = c.pt_cache.find(key);
+    if (it != c.pt_cache.end()) p = it->second;
+  }
+  if (!p.buf) {  // first use: upload the constant once (cached like the mask plaintexts)
+    std::vector<u64> h((size_t)(limbs + 1) * c.n);
+    for (int l = 0; l <= limbs; ++l)
+      std::fill(h.begin() + (size_t)l * c.n, h.begin() + (size_t)(l + 1) * c.n, m % c.primes[l]);
+    p.limbs = limbs + 1;
+    p.scale = (double)m;
+    p.buf = buf(c, h.size());
+    SF_CUDA(cudaMemcpyAsync(p.buf->p, h.data(), h.size() * 8, cudaMemcpyHostToDevice, c.stream));
+    SF_CUDA(cudaStreamSynchronize(c.stream));  // h is pageable and goes out of scope
+    std::lock_guard<std::mutex> lk(c.mu);
+    c.pt_cache[key] = p;
+  }
+  Ct t = view(a, limbs + 1);
+  t.layout.reset();
+  Ct r = mac_plain(c, {&t}, {&p}, false);
+  r.scale = a.scale * (double)m / (double)q;
+  r.layout = a.layout;
+  return r;
+}
+
 Ct add(Context& c, const Ct& a, const Ct& b, bool sub, bool count) {
   SF_HPROF("add");
   check_ct(c, a, sub ? "sub" : "add");
   check_ct(c, b, sub ? "sub" : "add");
   const int limbs = std::min(a.limbs, b.limbs);
+  if (!a.zero && !b.zero && std::fabs(a.scale / b.scale - 1.0) > 1e-9 && a.limbs != b.limbs) {
+    const bool a_hi = a.limbs > b.limbs;
+    const Ct al = align_scale(c, a_hi ? a : b, limbs, a_hi ? b.scale : a.scale);
+    return a_hi ? add(c, al, b, sub, count) : add(c, a, al, sub, count);
+  }
   if (count) c.ledger.add();
   OptLayout ly = merge_layouts(a, b);
   if (a.zero && b.zero) {

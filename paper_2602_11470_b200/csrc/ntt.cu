@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) ks_row_kernel(KsRowArgs A, Tab
 // destination row rd and walks the jobs of o: each non-identity job reads its
 // source rows rs = perm_g(rd) (digit ext rows / own c1 row and the c0 row),
 // staged through the warp's shared row buffer for the in-row permutation.
-template <int LOGR, int LOGC>
+template <int LOGR, int LOGC, bool PF>
 __global__ void __launch_bounds__(kWarps * 32, 2) ks_sum_kernel(KsSumArgs A, Tabs T) {
   constexpr int C = 1 << LOGC, E = C / 32, LOGN = LOGR + LOGC;
   auto rbr = [](uint32_t col) { return __brev(col) >> (32 - LOGC); };
@@ -519,6 +519,16 @@ __global__ void __launch_bounds__(kWarps * 32, 2) ks_sum_kernel(KsSumArgs A, Tab
       const int lo = j * A.alpha, hi = min(lo + A.alpha, A.limbs);
       const u64* src = (t >= lo && t < hi) ? A.c1[s] + (size_t)t * n + (size_t)rs * C
                                            : A.ext[s] + ((size_t)j * A.nt + t) * n + (size_t)rs * C;
+      const u64* kb = A.key[jb] + ((size_t)(j * 2 + 0) * A.np + m) * n + rowoff;
+      const u64* ka = A.key[jb] + ((size_t)(j * 2 + 1) * A.np + m) * n + rowoff;
+      ulonglong2 kv[PF ? E : 1];  // PF: the key words are in flight while the row is staged
+      if constexpr (PF) {
+#pragma unroll
+        for (int k = 0; k < E; k += 2) {
+          kv[k] = reinterpret_cast<const ulonglong2*>(kb)[k / 2];
+          kv[k + 1] = reinterpret_cast<const ulonglong2*>(ka)[k / 2];
+        }
+      }
 #pragma unroll
       for (int k = 0; k < E; k += 2) {
         const ulonglong2 v = reinterpret_cast<const ulonglong2*>(src + lane * E)[k / 2];
@@ -526,12 +536,15 @@ __global__ void __launch_bounds__(kWarps * 32, 2) ks_sum_kernel(KsSumArgs A, Tab
         buf[rbr(lane * E + k + 1)] = v.y;
       }
       __syncwarp();
-      const u64* kb = A.key[jb] + ((size_t)(j * 2 + 0) * A.np + m) * n + rowoff;
-      const u64* ka = A.key[jb] + ((size_t)(j * 2 + 1) * A.np + m) * n + rowoff;
 #pragma unroll
       for (int k = 0; k < E; k += 2) {
-        const ulonglong2 vb = reinterpret_cast<const ulonglong2*>(kb)[k / 2];
-        const ulonglong2 va = reinterpret_cast<const ulonglong2*>(ka)[k / 2];
+        ulonglong2 vb, va;
+        if constexpr (PF) {
+          vb = kv[k], va = kv[k + 1];
+        } else {
+          vb = reinterpret_cast<const ulonglong2*>(kb)[k / 2];
+          va = reinterpret_cast<const ulonglong2*>(ka)[k / 2];
+        }
         const u64 x0 = buf[sc[k]], x1 = buf[sc[k + 1]];
         mac128(sb[k], x0, vb.x);
         mac128(sa[k], x0, va.x);
@@ -668,7 +681,10 @@ void run_ks_row(Context& c, const KsRowArgs& a) {
 template <int LOGR, int LOGC>
 void run_ks_sum(Context& c, const KsSumArgs& a) {
   const unsigned grid = (unsigned)(a.nout * a.nt * ((1 << LOGR) / kWarps));
-  ks_sum_kernel<LOGR, LOGC><<<grid, kWarps * 32, 0, c.stream>>>(a, c.tabs);
+  if (c.variant & 1)
+    ks_sum_kernel<LOGR, LOGC, true><<<grid, kWarps * 32, 0, c.stream>>>(a, c.tabs);
+  else
+    ks_sum_kernel<LOGR, LOGC, false><<<grid, kWarps * 32, 0, c.stream>>>(a, c.tabs);
 }
 
 #define SF_NTT_DISPATCH(FN, ...)                        \

@@ -7,4 +7,5 @@ cd "$(dirname "$0")/../.."
 make -s -f oracle/ref.mk oracle/_ref/ref_golden
 ./oracle/_ref/ref_golden small  | gzip -9n > tests/golden/ref_small.json.gz
 ./oracle/_ref/ref_golden medium | gzip -9n > tests/golden/ref_medium.json.gz
+./oracle/_ref/ref_golden harness | gzip -9n > tests/golden/ref_harness.json.gz
 ls -la tests/golden/
