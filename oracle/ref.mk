@@ -12,7 +12,7 @@ CXXFLAGS ?= -std=c++20 -O2 -fPIC -ffp-contract=off -w
 INC      := -I$(REF)/include -Ioracle/shim -I$(JSON_INC)
 SRCS     := engine layouts vmm kv_attention nonlinear placement harness
 OBJS     := $(SRCS:%=$(OUT)/%.o)
-TESTS    := test_engine test_layouts test_vmm test_kv test_harness
+TESTS    := test_engine test_layouts test_vmm test_kv test_harness test_nonlinear test_placement
 
 all: $(OUT)/libslotforge_ref.so $(TESTS:%=$(OUT)/%) $(OUT)/ref_golden $(OUT)/ref_bench
 

@@ -12,19 +12,24 @@
 //   exact_softmax_maps         proj/src/kv_attention.cpp:395-412
 //   prefill (vmm_batch, rope_apply_batch, inner_rotate, exact_softmax_prefill_maps)
 //                              proj/src/kv_attention.cpp:119-129, 245-376, 414-454; vmm.cpp:30-43, 417-467
+//   nonlinear ("nonlinear" set): eval_cheb, goldschmidt, approx_exp, approx_softmax,
+//   approx_norm, approx_silu   proj/src/nonlinear.cpp:312-549
 //   harness ("harness" set): make_weights / seeded_prompt / plaintext_reference /
 //   plan_decode / run_generation (prefill_prompt + run_decode_step)
 //                              proj/src/harness.cpp:197-352, 425-659, 712-857, 943-1053
 #include <nlohmann/json.hpp>
 
 #include <cstdio>
+#include <functional>
 #include <iostream>
+#include <optional>
 #include <random>
 #include <string>
 #include <vector>
 
 #include "slotforge/engine.hpp"
 #include "slotforge/harness.hpp"
+#include "slotforge/nonlinear.hpp"
 #include "slotforge/kv_attention.hpp"
 #include "slotforge/layouts.hpp"
 #include "slotforge/vmm.hpp"
@@ -310,6 +315,136 @@ json harness_case(const ModelConfig& cfg, int n0, int gen_len) {
               {"report", json::parse(rep.to_json())}};
 }
 
+SlotVector uniform_slots(std::mt19937_64& rng, int N, double lo, double hi) {
+  std::uniform_real_distribution<double> u(lo, hi);
+  SlotVector s(N);
+  for (int i = 0; i < N; ++i) s[i] = u(rng);
+  return s;
+}
+
+json spec_json(const ApproxSpec& s) { return json::parse(approx_spec_to_json(s)); }
+
+// one nonlinear call on a fresh SimBackend: inputs, outputs, levels, ledger
+json nl_case(const std::string& op, int N, int L, const std::vector<SlotVector>& ins, const ApproxSpec* spec,
+             const std::function<std::vector<Ciphertext>(SimBackend&, const std::vector<Ciphertext>&)>& fn,
+             json extra, const std::optional<Layout>& ly = std::nullopt) {
+  SimBackend be({N, L});
+  std::vector<Ciphertext> cts;
+  json jin = json::array();
+  for (const auto& s : ins) {
+    cts.push_back(ly ? be.encrypt(s, L, *ly) : be.encrypt(s, L));
+    jin.push_back(sv_json(s));
+  }
+  be.ledger().reset();
+  auto outs = fn(be, cts);
+  json jout = json::array(), lv = json::array();
+  for (const auto& o : outs) {
+    jout.push_back(sv_json(o.slots));
+    lv.push_back(o.level);
+  }
+  json j{{"kind", "nonlinear"}, {"op", op},        {"N", N},
+         {"L", L},              {"inputs", jin},   {"outputs", jout},
+         {"out_levels", lv},    {"counts", counts_json(be.ledger().totals())},
+         {"extra", extra},      {"layout", layout_json(ly)}};
+  if (spec) j["spec"] = spec_json(*spec);
+  return j;
+}
+
+json nonlinear_cases() {
+  json cases = json::array();
+  std::mt19937_64 rng(11);
+  // eval_cheb at the degrees of test_nonlinear.cpp:49-70
+  for (int deg : {1, 2, 3, 5, 8, 13, 20, 31}) {
+    auto f = [](double x) { return std::sin(3.0 * x) + 0.25 * x; };
+    auto coeffs = fit_cheb_ls(f, -2.0, 1.5, deg);
+    cases.push_back(nl_case("eval_cheb", 64, 20, {uniform_slots(rng, 64, -2.0, 1.5)}, nullptr,
+                            [&](SimBackend& be, const std::vector<Ciphertext>& x) {
+                              return std::vector<Ciphertext>{eval_cheb(be, x[0], -2.0, 1.5, coeffs)};
+                            },
+                            json{{"lo", -2.0}, {"hi", 1.5}, {"coeffs", coeffs}, {"deg", deg}}));
+  }
+  {  // coefficient mask (test_nonlinear.cpp:72-88)
+    auto silu = [](double x) { return x / (1.0 + std::exp(-x)); };
+    auto coeffs = fit_cheb_ls(silu, -4.0, 4.0, 15);
+    SlotVector mask = SlotVector::Zero(32);
+    for (int i = 0; i < 32; i += 2) mask[i] = 1.0;
+    cases.push_back(nl_case("eval_cheb_masked", 32, 12, {uniform_slots(rng, 32, -4.0, 4.0)}, nullptr,
+                            [&](SimBackend& be, const std::vector<Ciphertext>& x) {
+                              return std::vector<Ciphertext>{eval_cheb(be, x[0], -4.0, 4.0, coeffs, &mask)};
+                            },
+                            json{{"lo", -4.0}, {"hi", 4.0}, {"coeffs", coeffs}, {"mask", sv_json(mask)}}));
+  }
+  for (const char* preset : {"desk-default", "desk-shallow"}) {
+    const ApproxSpec inv = desk_spec(preset, "inverse");
+    cases.push_back(nl_case("inverse", 64, 24, {uniform_slots(rng, 64, 1.0 / 64.0, 1.0)}, &inv,
+                            [&](SimBackend& be, const std::vector<Ciphertext>& x) {
+                              return std::vector<Ciphertext>{goldschmidt(be, x[0], GoldschmidtKind::Inverse, inv)};
+                            },
+                            json{{"preset", preset}}));
+    const ApproxSpec rs = desk_spec(preset, "rsqrt");
+    cases.push_back(nl_case("rsqrt", 64, 24, {uniform_slots(rng, 64, 1.0 / 16.0, 1.0)}, &rs,
+                            [&](SimBackend& be, const std::vector<Ciphertext>& x) {
+                              return std::vector<Ciphertext>{goldschmidt(be, x[0], GoldschmidtKind::Rsqrt, rs)};
+                            },
+                            json{{"preset", preset}}));
+    const ApproxSpec ex = desk_spec(preset, "exp");
+    cases.push_back(nl_case("exp", 64, 24, {uniform_slots(rng, 64, -8.0, 4.0)}, &ex,
+                            [&](SimBackend& be, const std::vector<Ciphertext>& x) {
+                              return std::vector<Ciphertext>{approx_exp(be, x[0], ex)};
+                            },
+                            json{{"preset", preset}}));
+    const ApproxSpec sm = desk_spec(preset, "softmax");
+    for (auto [heads, n] : std::vector<std::pair<int, int>>{{1, 20}, {2, 13}, {4, 19}}) {
+      const int gt = 32 / heads;
+      const int nm = (n + gt - 1) / gt;
+      std::vector<SlotVector> maps;
+      for (int m = 0; m < nm; ++m) {
+        SlotVector s = SlotVector::Zero(32);
+        const int cnt = std::min(gt, n - m * gt);
+        for (int h = 0; h < heads; ++h) {
+          SlotVector u = uniform_slots(rng, cnt, -6.0, 3.0);
+          for (int k = 0; k < cnt; ++k) s[h * gt + k] = u[k];
+        }
+        maps.push_back(s);
+      }
+      cases.push_back(nl_case("softmax", 32, 26, maps, &sm,
+                              [&](SimBackend& be, const std::vector<Ciphertext>& x) {
+                                return approx_softmax(be, x, n, heads, sm);
+                              },
+                              json{{"preset", preset}, {"heads", heads}, {"n_prime", n}}));
+    }
+    const ApproxSpec nm = desk_spec(preset, "norm");
+    for (int d : {16, 8}) {
+      const Layout ly = make_interleaved(d, 64, 1, 1);
+      SlotVector s = SlotVector::Zero(64);
+      SlotVector u = uniform_slots(rng, d, -1.5, 2.0);
+      for (int e = 0; e < d; ++e) s[e * ly.t + ly.offset] = u[e];
+      const SlotVector gs = uniform_slots(rng, d, 0.5, 1.5), bs = uniform_slots(rng, d, -0.2, 0.2);
+      Vector gamma(d), beta(d);
+      for (int e = 0; e < d; ++e) gamma[e] = gs[e], beta[e] = bs[e];
+      cases.push_back(nl_case("norm", 64, 32, {s}, &nm,
+                              [&](SimBackend& be, const std::vector<Ciphertext>& x) {
+                                return std::vector<Ciphertext>{approx_norm(be, x[0], gamma, beta, 1e-5, nm)};
+                              },
+                              json{{"preset", preset}, {"gamma", v_json(gamma)}, {"beta", v_json(beta)},
+                                   {"eps", 1e-5}},
+                              ly));
+    }
+    for (const char* fn : {"silu", "gelu"}) {
+      const ApproxSpec si = desk_spec(preset, fn);
+      Layout ly = make_interleaved(16, 64, 2, 1);
+      ly.deferred_mask = true;  // vmm garbage on the invalid slots
+      SlotVector s = uniform_slots(rng, 64, -10.0, 10.0);
+      cases.push_back(nl_case("silu", 64, 16, {s}, &si,
+                              [&](SimBackend& be, const std::vector<Ciphertext>& x) {
+                                return std::vector<Ciphertext>{approx_silu(be, x[0], si)};
+                              },
+                              json{{"preset", preset}, {"function", fn}}, ly));
+    }
+  }
+  return cases;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -353,6 +488,8 @@ int main(int argc, char** argv) {
     cases.push_back(prefill_case(16, 8, 2, 11, seed++));
     cases.push_back(prefill_case(16, 4, 1, 1, seed++));
     cases.push_back(prefill_case(64, 16, 4, 13, seed++));
+  } else if (which == "nonlinear") {
+    cases = nonlinear_cases();
   } else if (which == "harness") {
     // test_harness.cpp: desk_config (d 64, H 4, 2 blocks, vocab 32, N 256, L 13)
     // exact mode seeds 3 / 9 (prompt 8 + 8 generated; single-token prompt),

@@ -681,10 +681,10 @@ void run_ks_row(Context& c, const KsRowArgs& a) {
 template <int LOGR, int LOGC>
 void run_ks_sum(Context& c, const KsSumArgs& a) {
   const unsigned grid = (unsigned)(a.nout * a.nt * ((1 << LOGR) / kWarps));
-  if (c.variant & 1)
-    ks_sum_kernel<LOGR, LOGC, true><<<grid, kWarps * 32, 0, c.stream>>>(a, c.tabs);
-  else
+  if (c.variant & 1)  // A/B: key words loaded after the row is staged
     ks_sum_kernel<LOGR, LOGC, false><<<grid, kWarps * 32, 0, c.stream>>>(a, c.tabs);
+  else  // default: key loads issued first, in flight while the row is staged (-4% family time)
+    ks_sum_kernel<LOGR, LOGC, true><<<grid, kWarps * 32, 0, c.stream>>>(a, c.tabs);
 }
 
 #define SF_NTT_DISPATCH(FN, ...)                        \

@@ -8,4 +8,5 @@ make -s -f oracle/ref.mk oracle/_ref/ref_golden
 ./oracle/_ref/ref_golden small  | gzip -9n > tests/golden/ref_small.json.gz
 ./oracle/_ref/ref_golden medium | gzip -9n > tests/golden/ref_medium.json.gz
 ./oracle/_ref/ref_golden harness | gzip -9n > tests/golden/ref_harness.json.gz
+./oracle/_ref/ref_golden nonlinear | gzip -9n > tests/golden/ref_nonlinear.json.gz
 ls -la tests/golden/
