@@ -504,6 +504,13 @@ int main(int argc, char** argv) {
     tiny.d = 8, tiny.H = 2, tiny.n_layers = 1, tiny.ffn_alpha = 2, tiny.vocab = 8, tiny.N = 32, tiny.L = 13;
     tiny.seed = 11;
     cases.push_back(harness_case(tiny, 5, 3));
+    // approx mode: homomorphic softmax / norm / SiLU under the solver's plan
+    ModelConfig ap;
+    ap.mode = NonlinearMode::Approx;
+    ap.seed = 5;
+    cases.push_back(harness_case(ap, 4, 2));
+    tiny.mode = NonlinearMode::Approx;
+    cases.push_back(harness_case(tiny, 3, 2));
   } else if (which == "medium") {
     // N = 2048 slots (ring degree 4096): the GPU parity size
     cases.push_back(vmm_case(2048, 64, 64, 0, 0, true, false, 7001));

@@ -99,8 +99,8 @@ def validate_model_config(cfg: ModelConfig) -> None:
         raise ShapeMismatch("model config: level budget must be at least 1")
     if not cfg.rope_base > 1.0:
         raise ShapeMismatch("model config: rope_base must exceed 1")
-    if cfg.mode != "exact":
-        raise ShapeMismatch("model config: only exact-mode nonlinearities run here (approx mode is out of scope)")
+    if cfg.mode not in ("exact", "approx"):
+        raise ShapeMismatch(f'model config: mode must be "exact" or "approx", got "{cfg.mode}"')
 
 
 # ------------------------------------------------------------ seeded generators
@@ -342,6 +342,29 @@ class PlacementPlan:
                             "bootstrap_to": e.bootstrap_to, "drop_to": e.drop_to} for e in self.entries])
 
 
+# ------------------------------------------------------------ nonlinear schedule
+@dataclass
+class NonlinearSchedule:
+    softmax: object
+    norm: object
+    silu: object
+
+
+def nonlinear_schedule(cfg: ModelConfig) -> NonlinearSchedule:
+    """harness.cpp:353-374: desk-shallow specs; exact mode marks them exact;
+    approx mode trims the norm to 3 Goldschmidt iterations and clamps."""
+    from . import nonlinear as NL
+    s = NonlinearSchedule(NL.desk_spec("desk-shallow", "softmax"), NL.desk_spec("desk-shallow", "norm"),
+                          NL.desk_spec("desk-shallow", "silu"))
+    if cfg.mode == "exact":
+        s.softmax.exact = s.norm.exact = s.silu.exact = True
+        return s
+    s.norm.iterations = 3
+    s.norm.depth_budget = 0
+    s.softmax.strict_domain = s.norm.strict_domain = s.silu.strict_domain = False
+    return s
+
+
 # ----------------------------------------------------------------- GPU operators
 class GpuOps:
     """The harness's operator set on the GPU backend. VMM diagonals are encoded
@@ -416,6 +439,10 @@ class GpuOps:
         att, cache = self._m["prefill"](self.be, xs, wq, wk, wv, acfg, self._m["exact_softmax_prefill_maps"], base)
         dec = self._m["AttentionConfig"](acfg.N, acfg.d, acfg.H, 0, acfg.n_max)  # decode-side view of the cache
         return att, self._m["kv_from_cts"](self.be, dec, cache.n_prime, cache.k_cts, cache.v_cts)
+
+    def fused_extract_norm(self, x):
+        from . import fused_extract_mask
+        return fused_extract_mask(self.be, x)
 
     def n_prime(self, cache):
         return cache.n_prime
@@ -511,6 +538,14 @@ def run_decode_step(be, ops, cfg: ModelConfig, w: ModelWeights, plan: Optional[P
     acfg = ops.attention_config(cfg, state.n_max)
     t = acfg.t
     pos = state.position
+    from . import nonlinear as NL
+    sched = nonlinear_schedule(cfg)
+    exact = cfg.mode == "exact"
+
+    def norm(v, gamma, beta):  # stages 6 / 10
+        if exact:
+            return exact_norm(be, exact_apply(be, v, lambda z: z), gamma, beta)
+        return NL.approx_norm(be, ops.fused_extract_norm(v), gamma, beta, NORM_EPS, sched.norm)
     ffn_layout = ops.layout(padded_dim(cfg.ffn_alpha * cfg.d))
     x = state.x
     if plan is not None and x.level > plan.entries[0].input_level:
@@ -588,7 +623,8 @@ def run_decode_step(be, ops, cfg: ModelConfig, w: ModelWeights, plan: Optional[P
         # [3] softmax (exact oracle hook; records no ops)
         begin(maps[0], base + 3)
         with be.phase(STAGE_NAMES[3]):
-            probs = ops.exact_softmax(maps, acfg, ops.n_prime(state.caches[b]))
+            probs = (ops.exact_softmax(maps, acfg, ops.n_prime(state.caches[b])) if exact else
+                     NL.approx_softmax(be, maps, ops.n_prime(state.caches[b]), cfg.H, sched.softmax))
         end(b, 3, probs[0])
         live = post(base + 3, probs + [x], False, True, b)
         probs, x = live[:-1], live[-1]
@@ -613,7 +649,7 @@ def run_decode_step(be, ops, cfg: ModelConfig, w: ModelWeights, plan: Optional[P
         # [6] first norm
         begin(s, base + 6)
         with be.phase(STAGE_NAMES[6]):
-            y = exact_norm(be, exact_apply(be, s, lambda v: v), blk.gamma1, blk.beta1)
+            y = norm(s, blk.gamma1, blk.beta1)
         end(b, 6, y)
         (y,) = post(base + 6, [y])
 
@@ -628,7 +664,7 @@ def run_decode_step(be, ops, cfg: ModelConfig, w: ModelWeights, plan: Optional[P
         # [8] gated activation (exact SiLU hook) times the up projection
         begin(gate_o, base + 8)
         with be.phase(STAGE_NAMES[8]):
-            act = exact_apply(be, gate_o, silu)
+            act = exact_apply(be, gate_o, silu) if exact else NL.approx_silu(be, gate_o, sched.silu)
             prod = be.with_layout(be.mul(act, up_o), ffn_layout)
         end(b, 8, prod)
         prod, y = post(base + 8, [prod, y])
@@ -646,7 +682,7 @@ def run_decode_step(be, ops, cfg: ModelConfig, w: ModelWeights, plan: Optional[P
         # [10] second norm -> next block's input
         begin(s2, base + 10)
         with be.phase(STAGE_NAMES[6]):
-            x = exact_norm(be, exact_apply(be, s2, lambda v: v), blk.gamma2, blk.beta2)
+            x = norm(s2, blk.gamma2, blk.beta2)
         end(b, 10, x)
         (x,) = post(base + 10, [x])
 
@@ -671,6 +707,9 @@ def prefill_prompt(be, ops, cfg: ModelConfig, w: ModelWeights, tokens: List[int]
     ffn_layout = ops.layout(padded_dim(cfg.ffn_alpha * cfg.d))
     state.caches, state.n_max = [], n_max
     L = be.L
+    from . import nonlinear as NL
+    sched = nonlinear_schedule(cfg)
+    exact = cfg.mode == "exact"
 
     def ensure(c, need):
         return be.bootstrap(c, L) if c.level < need else c
@@ -700,17 +739,30 @@ def prefill_prompt(be, ops, cfg: ModelConfig, w: ModelWeights, tokens: List[int]
                     mk = np.zeros(cfg.N)
                     mk[tau::t] = 1.0
                     lane = be.with_layout(be.mul_plain(s, mk), ops.layout(cfg.d, tau, 1))
-                    y = exact_norm(be, lane, blk.gamma1, blk.beta1)
+                    if exact:
+                        y = exact_norm(be, lane, blk.gamma1, blk.beta1)
+                    else:
+                        lane = ensure(lane, NL.norm_depth(sched.norm))
+                        y = NL.approx_norm(be, lane, blk.gamma1, blk.beta1, NORM_EPS, sched.norm)
                     y = ensure(y, 1)
                     gate_o = ops.vmm(y, blk.w_gate)
                     up_o = ops.vmm(y, blk.w_up)
-                    act = ensure(exact_apply(be, gate_o, silu), 1)
+                    if exact:
+                        act = ensure(exact_apply(be, gate_o, silu), 1)
+                    else:
+                        gate_o = ensure(gate_o, NL.silu_depth(sched.silu) + 1)
+                        act = NL.approx_silu(be, gate_o, sched.silu)
                     up_o = ensure(up_o, 1)
                     prod = be.with_layout(be.mul(act, up_o), ffn_layout)
                     prod = ensure(prod, 1)
                     down = ops.vmm(prod, blk.w_down, tau)
                     s2 = be.with_layout(be.add(y, down), down.layout)
-                    z = exact_norm(be, exact_apply(be, s2, lambda v: v), blk.gamma2, blk.beta2)
+                    if exact:
+                        z = exact_norm(be, exact_apply(be, s2, lambda v: v), blk.gamma2, blk.beta2)
+                    else:
+                        s2 = ensure(s2, 1 + NL.norm_depth(sched.norm))
+                        z = NL.approx_norm(be, ops.fused_extract_norm(s2), blk.gamma2, blk.beta2, NORM_EPS,
+                                           sched.norm)
                     acc = z if acc is None else be.add(acc, z)
                     acc = be.with_layout(acc, batch_layout)
                 nxt.append(acc)

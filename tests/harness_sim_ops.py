@@ -61,6 +61,9 @@ class SimOps:
         att, cache = P.prefill(self.be, xs, wq, wk, wv, acfg, P.exact_softmax_prefill_maps, base)
         return att, self._tag(cache, P.AttentionConfig(acfg.N, acfg.d, acfg.H, 0, acfg.n_max))
 
+    def fused_extract_norm(self, x):
+        return P.fused_extract(self.be, x, "norm_mask")
+
     def n_prime(self, cache):
         return cache.n_prime
 

@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden", "ref_harness.json.gz")
 
 
-@pytest.mark.parametrize("ci", [0, 1, 2])
+@pytest.mark.parametrize("ci", [0, 1, 2, 3, 4])
 def test_gpu_generation_matches_reference(ci):
     import paper_2602_11470_b200 as sf
     from paper_2602_11470_b200 import harness as Hn
@@ -34,9 +34,13 @@ def test_gpu_generation_matches_reference(ci):
         [(e["step"], e["block"], e["phase"], e["level_in"], e["level_out"], e["bootstrap_to"])
          for e in want["level_trace"]]
     assert rep.phase_rows() == want["phases"]
-    # CKKS at scale 2^40: states and logits of the whole generation within 1e-6
-    # of the exact double-precision model (the reference's own bound)
-    assert rep.max_abs_error < 1e-6, rep.max_abs_error
+    if cfg.mode == "exact":
+        # CKKS at scale 2^40: states and logits of the whole generation within
+        # 1e-6 of the exact double-precision model (the reference's own bound)
+        assert rep.max_abs_error < 1e-6, rep.max_abs_error
+    else:  # approx mode: the reference's approximation error, plus CKKS noise
+        ref_err = want["max_abs_error"]
+        assert abs(rep.max_abs_error - ref_err) <= 1e-4 * max(1.0, ref_err)
     # and word-for-word the CPU CKKS twin (same keys and encryption seeds):
     # every decrypted hidden state identical to the last bit
     import sys

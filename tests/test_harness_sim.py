@@ -31,7 +31,7 @@ def _seq_sum(a):
     return s
 
 
-@pytest.mark.parametrize("ci", range(3))
+@pytest.mark.parametrize("ci", range(5))
 def test_weights_prompt_and_plaintext_reference(ci):
     c = cases()[ci]
     cfg = Hn.ModelConfig.from_json(c["config"])
@@ -54,7 +54,7 @@ def test_weights_prompt_and_plaintext_reference(ci):
         np.testing.assert_allclose(got, want, rtol=0, atol=1e-12)
 
 
-@pytest.mark.parametrize("ci", range(3))
+@pytest.mark.parametrize("ci", range(5))
 def test_generation_matches_reference_report(ci):
     c = cases()[ci]
     cfg = Hn.ModelConfig.from_json(c["config"])
@@ -70,7 +70,10 @@ def test_generation_matches_reference_report(ci):
                   for e in want["level_trace"]]
     assert got_trace == want_trace
     assert [p for p in rep.phase_rows()] == want["phases"]
-    assert rep.max_abs_error < 1e-9
+    if cfg.mode == "exact":
+        assert rep.max_abs_error < 1e-9
+    else:  # approx mode: the approximation error itself, as the reference measured it
+        assert abs(rep.max_abs_error - want["max_abs_error"]) <= 1e-6 * max(1.0, want["max_abs_error"])
 
 
 def test_plan_levels_and_block_budget():
@@ -93,7 +96,7 @@ def test_plan_levels_and_block_budget():
     assert len(lv) == 8 * 2 and set(lv.values()) == {5}
 
 
-@pytest.mark.parametrize("ci", range(3))
+@pytest.mark.parametrize("ci", range(5))
 def test_generation_over_ckks_oracle(ci):
     """The same harness over the bit-exact CPU CKKS twin (real RNS-CKKS): the
     reference's tokens, level trace and ledger, within CKKS precision."""
@@ -105,4 +108,8 @@ def test_generation_over_ckks_oracle(ci):
     rep = Hn.run_generation(be, SimOps(be), cfg, w, c["prompt"], c["gen_len"], Hn.PlacementPlan.from_json(c["plan"]))
     assert rep.generated == c["report"]["generated"]
     assert rep.phase_rows() == c["report"]["phases"]
-    assert rep.max_abs_error < 1e-6, rep.max_abs_error
+    if cfg.mode == "exact":
+        assert rep.max_abs_error < 1e-6, rep.max_abs_error
+    else:  # CKKS noise on top of the approximation error the reference measured
+        ref_err = c["report"]["max_abs_error"]
+        assert abs(rep.max_abs_error - ref_err) <= 1e-4 * max(1.0, ref_err)
