@@ -312,7 +312,8 @@ json harness_case(const ModelConfig& cfg, int n0, int gen_len) {
               {"plan", json::parse(plan.to_json())},
               {"plan_terminal_level", plan.terminal_level},
               {"plan_bootstrap_count", plan.bootstrap_count},
-              {"report", json::parse(rep.to_json())}};
+              {"report", json::parse(rep.to_json())},
+              {"report_csv", rep.to_csv()}};
 }
 
 SlotVector uniform_slots(std::mt19937_64& rng, int N, double lo, double hi) {

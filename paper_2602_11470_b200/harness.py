@@ -801,6 +801,20 @@ class Report:
         return [dict({keys[k]: v for k, v in p["ops"].items()}, name=p["name"], levels_in=p["levels_in"],
                      levels_out=p["levels_out"]) for p in self.phases]
 
+    def to_csv(self) -> str:
+        """harness.cpp:901-922 (pinned columns)."""
+        def field_(v):
+            if not any(ch in v for ch in ',"\n'):
+                return v
+            return '"' + v.replace('"', '""') + '"'
+        out = "phase,rotations,hoisted,ctpt_mult,ctct_mult,adds,bootstraps,levels_in,levels_out\n"
+        for r in self.phase_rows():
+            cells = [field_(r["name"])] + [str(r[k]) for k in ("rotations", "hoisted", "ctpt_mult", "ctct_mult",
+                                                                 "adds", "bootstraps")]
+            cells += ["" if r[k] < 0 else str(r[k]) for k in ("levels_in", "levels_out")]
+            out += ",".join(cells) + "\n"
+        return out
+
     def to_json(self) -> str:
         return json.dumps({"config": asdict(self.config), "prompt": self.prompt, "generated": self.generated,
                            "phases": self.phase_rows(), "level_trace": [asdict(e) for e in self.level_trace],

@@ -70,6 +70,7 @@ def test_generation_matches_reference_report(ci):
                   for e in want["level_trace"]]
     assert got_trace == want_trace
     assert [p for p in rep.phase_rows()] == want["phases"]
+    assert rep.to_csv() == c["report_csv"]
     if cfg.mode == "exact":
         assert rep.max_abs_error < 1e-9
     else:  # approx mode: the approximation error itself, as the reference measured it
