@@ -459,7 +459,78 @@ __global__ void __launch_bounds__(kWarps * 32, 2) ks_row_kernel(KsRowArgs A, Tab
 // destination row rd and walks the jobs of o: each non-identity job reads its
 // source rows rs = perm_g(rd) (digit ext rows / own c1 row and the c0 row),
 // staged through the warp's shared row buffer for the in-row permutation.
-template <int LOGR, int LOGC, bool PF>
+// Automorphism gather of one row held blocked in registers (lane L owns the 8
+// natural columns 8L..8L+7), by warp shuffles instead of a shared-memory round
+// trip (ks_sum is L1TEX-bound; profiles/r1_ncu_v8.md). Destination register k
+// of lane L needs the source at bit-reversed position
+//   pos = (base + slope * ((brev3(k) << 5) | brev5(L))) mod 256,
+// i.e. source lane brev5(pos & 31) -- a function of L alone -- and source
+// register brev3(((A_L >> 5) + slope * brev3(k)) & 7) with A_L = base +
+// slope * brev5(L). Each source lane therefore pre-rotates its registers by
+// the c = (A_L >> 5) & 7 of the lane that will read it (3 select stages),
+// applies the warp-uniform multiplier permutation (4 static cases, slope odd)
+// and every register moves with one 64-bit shuffle.
+struct ShflPerm {
+  int src_lane;   // lane this lane reads from
+  int c;          // rotation this lane applies for its reader
+  int smod;       // slope mod 8 (odd)
+  __device__ __forceinline__ ShflPerm(uint32_t base, uint32_t slope, int lane) {
+    const uint32_t u = __brev((uint32_t)lane) >> 27;  // brev5(lane)
+    src_lane = (int)(__brev((base + slope * u) & 31) >> 27);
+    uint32_t inv = slope;  // slope^-1 mod 32 (Newton, slope odd)
+    inv *= 2 - slope * inv;
+    inv *= 2 - slope * inv;
+    inv *= 2 - slope * inv;
+    const uint32_t ur = (inv * ((__brev((uint32_t)lane) >> 27) - base)) & 31;  // reader's brev5(L)
+    c = (int)(((base + slope * ur) >> 5) & 7);
+    smod = (int)(slope & 7);
+  }
+  // v: natural-order registers of this lane's row segment -> permuted row
+  __device__ __forceinline__ void apply(u64 (&v)[8]) const {
+    u64 z[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) z[m] = v[__brev((uint32_t)m) >> 29];  // z[m] = v[brev3(m)]
+    // z[i] <- z[(i + c) & 7] in place: rotations by 1, 2, 4, each cycle with one temporary
+    if (c & 1) {
+      const u64 t0 = z[0];
+#pragma unroll
+      for (int i = 0; i < 7; ++i) z[i] = z[i + 1];
+      z[7] = t0;
+    }
+    if (c & 2) {
+#pragma unroll
+      for (int cy = 0; cy < 2; ++cy) {
+        const u64 t0 = z[cy];
+        z[cy] = z[cy + 2];
+        z[cy + 2] = z[cy + 4];
+        z[cy + 4] = z[cy + 6];
+        z[cy + 6] = t0;
+      }
+    }
+    if (c & 4) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const u64 t0 = z[i];
+        z[i] = z[i + 4];
+        z[i + 4] = t0;
+      }
+    }
+    switch (smod) {  // y[k] = z[(slope * brev3(k)) & 7], then one shuffle per register
+#define SF_SHFL_CASE(M)                                                                 \
+  case M:                                                                               \
+    _Pragma("unroll") for (int k = 0; k < 8; ++k) v[k] =                                \
+        __shfl_sync(0xffffffffu, z[(M * (__brev((uint32_t)k) >> 29)) & 7], src_lane);  \
+    break;
+      SF_SHFL_CASE(1)
+      SF_SHFL_CASE(3)
+      SF_SHFL_CASE(5)
+      SF_SHFL_CASE(7)
+#undef SF_SHFL_CASE
+    }
+  }
+};
+
+template <int LOGR, int LOGC, bool PF, bool SH>
 __global__ void __launch_bounds__(kWarps * 32, 2) ks_sum_kernel(KsSumArgs A, Tabs T) {
   constexpr int C = 1 << LOGC, E = C / 32, LOGN = LOGR + LOGC;
   auto rbr = [](uint32_t col) { return __brev(col) >> (32 - LOGC); };
@@ -510,6 +581,47 @@ __global__ void __launch_bounds__(kWarps * 32, 2) ks_sum_kernel(KsSumArgs A, Tab
     }
     const RowPerm<LOGR, LOGC> rp(rd, g);
     const int rs = (int)rp.src_row;
+    if constexpr (SH && LOGC == 8) {  // shuffle gather (no shared-memory round trip)
+      const ShflPerm sp(rp.base, rp.slope, lane);
+      for (int j = 0; j < A.ndig; ++j) {
+        const int lo = j * A.alpha, hi = min(lo + A.alpha, A.limbs);
+        const u64* src = (t >= lo && t < hi) ? A.c1[s] + (size_t)t * n + (size_t)rs * C
+                                             : A.ext[s] + ((size_t)j * A.nt + t) * n + (size_t)rs * C;
+        const ulonglong2* kb = reinterpret_cast<const ulonglong2*>(A.key[jb] + ((size_t)(j * 2 + 0) * A.np + m) * n + rowoff);
+        const ulonglong2* ka = reinterpret_cast<const ulonglong2*>(A.key[jb] + ((size_t)(j * 2 + 1) * A.np + m) * n + rowoff);
+        u64 x[8];
+#pragma unroll
+        for (int k = 0; k < E; k += 2) {
+          const ulonglong2 v = reinterpret_cast<const ulonglong2*>(src + lane * E)[k / 2];
+          x[k] = v.x, x[k + 1] = v.y;
+        }
+        sp.apply(x);
+        ulonglong2 kv[E];
+#pragma unroll
+        for (int k = 0; k < E; k += 2) kv[k] = kb[k / 2], kv[k + 1] = ka[k / 2];
+#pragma unroll
+        for (int k = 0; k < E; k += 2) {
+          mac128(sb[k], x[k], kv[k].x);
+          mac128(sa[k], x[k], kv[k + 1].x);
+          mac128(sb[k + 1], x[k + 1], kv[k].y);
+          mac128(sa[k + 1], x[k + 1], kv[k + 1].y);
+        }
+      }
+      if (qt) {  // P * sigma_g(c0)
+        const u64* src = A.c0[s] + (size_t)t * n + (size_t)rs * C;
+        u64 x[8];
+#pragma unroll
+        for (int k = 0; k < E; k += 2) {
+          const ulonglong2 v = reinterpret_cast<const ulonglong2*>(src + lane * E)[k / 2];
+          x[k] = v.x, x[k + 1] = v.y;
+        }
+        sp.apply(x);
+#pragma unroll
+        for (int k = 0; k < E; ++k) mac128(sb[k], x[k], pm);
+      }
+      terms += A.ndig + 1;
+      continue;
+    }
     // source positions in the bit-reversed row buffer: an affine map of
     // br(column) with odd slope g, so every 16 lanes hit 16 distinct banks
     uint32_t sc[E];
@@ -681,10 +793,15 @@ void run_ks_row(Context& c, const KsRowArgs& a) {
 template <int LOGR, int LOGC>
 void run_ks_sum(Context& c, const KsSumArgs& a) {
   const unsigned grid = (unsigned)(a.nout * a.nt * ((1 << LOGR) / kWarps));
-  if (c.variant & 1)  // A/B: key words loaded after the row is staged
-    ks_sum_kernel<LOGR, LOGC, false><<<grid, kWarps * 32, 0, c.stream>>>(a, c.tabs);
-  else  // default: key loads issued first, in flight while the row is staged (-4% family time)
-    ks_sum_kernel<LOGR, LOGC, true><<<grid, kWarps * 32, 0, c.stream>>>(a, c.tabs);
+  // default: automorphism gather by warp shuffles (-2% family time vs shared-memory staging);
+  // SF_VARIANT bit 3: shared-memory staging with the key loads issued first (-4% vs bit 0:
+  // key words loaded after the row is staged)
+  if (c.variant & 1)
+    ks_sum_kernel<LOGR, LOGC, false, false><<<grid, kWarps * 32, 0, c.stream>>>(a, c.tabs);
+  else if (c.variant & 8)
+    ks_sum_kernel<LOGR, LOGC, true, false><<<grid, kWarps * 32, 0, c.stream>>>(a, c.tabs);
+  else
+    ks_sum_kernel<LOGR, LOGC, true, true><<<grid, kWarps * 32, 0, c.stream>>>(a, c.tabs);
 }
 
 #define SF_NTT_DISPATCH(FN, ...)                        \
