@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(kWarps * 32) ntt_col_pass(LimbBatch B, Tabs T)
 // NTT -> store), so shared memory does not grow with nd and every phase keeps
 // all warps busy. TCF = 8 gives 64-byte row segments for big batches; TCF = 2
 // gives 4x more CTAs for single-ciphertext launches.
-template <int LOGR, int LOGC, int TCF, int CPW>
+template <int LOGR, int LOGC, int TCF, int CPW, bool FC>
 __global__ void __launch_bounds__(TCF / CPW * 32, TCF / CPW == 8 ? (CPW == 1 ? 3 : 2) : (TCF / CPW == 4 ? 6 : 8))
     fused_col_kernel(FusedColArgs A, Tabs T) {
   // CPW columns per warp (TCF / CPW warps): the column transforms of one warp
@@ -258,6 +258,69 @@ __global__ void __launch_bounds__(TCF / CPW * 32, TCF / CPW == 8 ? (CPW == 1 ? 3
     const int pd = A.dst_prime[d];
     const u64 q = T.q[pd];
     u64* out = region(A.ns, 0);
+    if constexpr (FC) {
+      // 3+4. each warp converts its own column(s) straight into registers and
+      // transforms them (no destination-tile round trip, one barrier less)
+      u64 x[CPW][E];
+      u64* sm[CPW];
+      if (A.mode == 0) {
+        u64 h[8], hs[8];
+#pragma unroll
+        for (int s = 0; s < 8; ++s)
+          if (s < A.ns) h[s] = A.qhat[(size_t)s * A.nd + d], hs[s] = A.qhat_s[(size_t)s * A.nd + d];
+        const u64 q4 = 4 * q, q8 = 8 * q;
+#pragma unroll
+        for (int c = 0; c < CPW; ++c) {
+          const int col = warp * CPW + c;
+          sm[c] = out + (size_t)col * PAD;
+#pragma unroll
+          for (int k = 0; k < E; ++k) {
+            const int r = swz(lane + 32 * k);
+            u64 acc = 0;
+#pragma unroll
+            for (int s = 0; s < 8; ++s)
+              if (s < A.ns) acc += mul_shoup_lazy(region(s, col)[r], h[s], hs[s], q);
+            if (A.ns > 4) acc = acc >= q8 ? acc - q8 : acc;
+            if (A.ns > 2) acc = acc >= q4 ? acc - q4 : acc;
+            x[c][k] = acc;
+          }
+        }
+      } else {
+        const u64 mh = T.mh[pd];
+        const u64 ql = reduce64(A.q_last, q, mh), half = A.q_last >> 1;
+#pragma unroll
+        for (int c = 0; c < CPW; ++c) {
+          const int col = warp * CPW + c;
+          sm[c] = out + (size_t)col * PAD;
+#pragma unroll
+          for (int k = 0; k < E; ++k) {
+            const u64 v = region(0, col)[swz(lane + 32 * k)];
+            const u64 rr = reduce64(v, q, mh);
+            x[c][k] = v > half ? sub_mod(rr, ql, q) : rr;
+          }
+        }
+      }
+      const u64* W = T.psi + ((size_t)pd << LOGN);
+      const u64* Ws = T.psi_s + ((size_t)pd << LOGN);
+      auto tw = [&](int b, int blk, u64& w, u64& ws) {
+        const int i = (1 << (LOGR - 1 - b)) + blk;
+        w = W[i];
+        ws = Ws[i];
+      };
+      warp_fwd_n<LOGR, CPW>(x, sm, lane, q, tw);
+#pragma unroll
+      for (int c = 0; c < CPW; ++c)
+#pragma unroll
+        for (int k = 0; k < E; ++k) sm[c][swz(lane + 32 * k)] = x[c][k];
+      __syncthreads();
+      u64* o = dst + (size_t)A.out_slot[d] * n + col0;
+      for (int e = threadIdx.x; e < R * TCF; e += NT) {
+        const int row = e / TCF, col = e - row * TCF;
+        o[(size_t)row * C + col] = out[(size_t)col * PAD + swz(row)];
+      }
+      if (d + 1 < d_hi) __syncthreads();
+      continue;
+    }
     // 3. conversion (coefficient domain) into destination tile d & 1
     if (A.mode == 0) {
       u64 h[8], hs[8];
@@ -746,14 +809,19 @@ void run_fused_t(Context& c, const FusedColArgs& a) {
   const size_t sm = (size_t)(a.ns + 1) * TCF * (R + 1) * sizeof(u64);
   static int configured = 0;
   if (!configured) {
-    SF_CUDA(cudaFuncSetAttribute(fused_col_kernel<LOGR, LOGC, TCF, CPW>,
+    SF_CUDA(cudaFuncSetAttribute(fused_col_kernel<LOGR, LOGC, TCF, CPW, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    SF_CUDA(cudaFuncSetAttribute(fused_col_kernel<LOGR, LOGC, TCF, CPW, false>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     configured = 1;
   }
   require(sm <= 200 * 1024, kInternal, "fused column stage: too many source limbs for shared memory");
   const int dpc = a.d_per_cta > 0 ? a.d_per_cta : a.nd;
   const unsigned grid = (unsigned)a.count * ((a.nd + dpc - 1) / dpc) * ((1u << LOGC) / TCF);
-  fused_col_kernel<LOGR, LOGC, TCF, CPW><<<grid, TCF / CPW * 32, sm, c.stream>>>(a, c.tabs);
+  if (c.variant & 16)  // A/B: block-wide conversion through the destination tile
+    fused_col_kernel<LOGR, LOGC, TCF, CPW, false><<<grid, TCF / CPW * 32, sm, c.stream>>>(a, c.tabs);
+  else  // default: per-warp conversion into registers
+    fused_col_kernel<LOGR, LOGC, TCF, CPW, true><<<grid, TCF / CPW * 32, sm, c.stream>>>(a, c.tabs);
 }
 
 template <int LOGR, int LOGC>
