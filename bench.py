@@ -372,6 +372,41 @@ def cpu_baseline_sample():
         return {"value": None, "unit": "ms/token", "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
 
 
+def cpu_twin_sample(gpu_qkt_ms):
+    """the bit-exact CPU CKKS twin (oracle/ckks_oracle.cpp,
+    OpenMP over limbs and ciphertexts on every host core) on a bounded sample
+    of the same step: qk_dot over 8 of its 256 K-cts (ring 2^16, level 2),
+    rotation keys warm (one untimed call first). Reported beside the GPU's
+    QK^T phase; the per-token figure is the sample x 32, labelled extrapolated."""
+    try:
+        sys.path.insert(0, ROOT)
+        from oracle.ckks import CkksOracle
+        from oracle import protocols as P
+        from oracle.layout import make_interleaved
+        be = CkksOracle(SLOTS, 7, alpha=2, seed=1)
+        cfg = P.AttentionConfig(SLOTS, D, H, 0, NP)
+        t, rng = cfg.t, np.random.default_rng(7)
+        ly = make_interleaved(D, SLOTS, 0, H)
+        cache = P.KVCache()
+        for _ in range(8):
+            cache.k_cts.append(be.encrypt(rng.normal(size=SLOTS), LEVELS["cache"], ly))
+        cache.n_prime = 8 * t
+        qs = np.zeros(SLOTS)
+        qs[np.arange(D) * t] = rng.normal(size=D)
+        q = be.encrypt(qs, LEVELS["cache"], ly)
+        P.qk_dot(be, q, cache, cfg)  # rotation keys generated here, untimed
+        t0 = time.perf_counter()
+        P.qk_dot(be, q, cache, cfg)
+        sec = time.perf_counter() - t0
+        return {"kind": "port", "cores": os.cpu_count(), "sample": "qk_dot over 8 of the step's 256 K-cts "
+                "(ring 2^16, level 2, keys warm) on the bit-exact CPU CKKS twin, OpenMP on all host cores",
+                "value": round(sec * 1e3, 1), "unit": "ms per sample",
+                "qkt_per_token_extrapolated_ms": round(sec * 32e3, 1), "gpu_qkt_ms": gpu_qkt_ms,
+                "gpu_speedup_qkt_extrapolated": round(sec * 32e3 / gpu_qkt_ms, 1) if gpu_qkt_ms else None}
+    except Exception as e:  # pragma: no cover
+        return {"kind": "port", "sample": f"failed: {e}"}
+
+
 # ----------------------------------------------------------------------------- main
 def main():
     ap = argparse.ArgumentParser()
@@ -585,6 +620,7 @@ def main():
 
     phases = layer.phase_ms(args.steps)  # last: its graph's memory must not disturb the timed graph
     cpu = None if (args.no_cpu_baseline or rank != 0) else cpu_baseline_sample()
+    twin = None if (args.no_cpu_baseline or rank != 0) else cpu_twin_sample(phases.get("QK^T"))
     vmm_per_step = 7
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "ms/token", "n_gpus": world, "steps": args.steps,
@@ -599,6 +635,7 @@ def main():
         "roofline": roofline,
         "int_roofline": int_roofline,
         "cpu_baseline": cpu,
+        "cpu_baseline_ckks_twin": twin,
         "e2e": {"value": round(e2e_ms / world, 3), "unit": "ms/token", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "breakdown": e2e_parts},
         "gpu_launches": int(launches),
