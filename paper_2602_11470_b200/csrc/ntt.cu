@@ -818,9 +818,12 @@ void run_fused_t(Context& c, const FusedColArgs& a) {
   require(sm <= 200 * 1024, kInternal, "fused column stage: too many source limbs for shared memory");
   const int dpc = a.d_per_cta > 0 ? a.d_per_cta : a.nd;
   const unsigned grid = (unsigned)a.count * ((a.nd + dpc - 1) / dpc) * ((1u << LOGC) / TCF);
-  if (c.variant & 16)  // A/B: block-wide conversion through the destination tile
+  // per-warp conversion into registers for the batched 8-column CTAs (-4% family
+  // time); the 2-column single-ciphertext CTAs keep the block-wide conversion
+  // (measured faster there: 1.49 vs 1.69 ms/step); SF_VARIANT bit 4 forces it everywhere
+  if ((c.variant & 16) || TCF < 8)
     fused_col_kernel<LOGR, LOGC, TCF, CPW, false><<<grid, TCF / CPW * 32, sm, c.stream>>>(a, c.tabs);
-  else  // default: per-warp conversion into registers
+  else
     fused_col_kernel<LOGR, LOGC, TCF, CPW, true><<<grid, TCF / CPW * 32, sm, c.stream>>>(a, c.tabs);
 }
 
