@@ -574,6 +574,13 @@ def main():
                     "peak": bpk, "unit": "G butterfly/s",
                     "frac": round(bf_tot / (nt_ms * 1e-3) / 1e9 / bpk, 4) if (nt_ms > 0 and bpk) else None,
                     "peak_source": "profiles/r1_butterfly_peak.json (tools/microbench/butterfly.cu on B200)"}
+    try:  # the same kernels' FMA-heavy pipe utilisation from the committed ncu capture
+        pu = json.load(open(os.path.join(ROOT, "profiles", "r1_pipe_util.json")))
+        int_roofline["fmaheavy_pipe_pct_share_weighted"] = pu["share_weighted_fmaheavy_pct"]
+        int_roofline["fmaheavy_pipe_source"] = "profiles/r1_pipe_util.json (ncu, top-5 kernels, %.1f%% of the step)" % \
+            pu["covered_step_share_pct"]
+    except Exception:
+        pass
 
     # ---- e2e: public API with host buffers (import inputs from pinned host
     # memory, read the results back), host wall clock around whole steps
