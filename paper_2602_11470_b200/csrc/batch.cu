@@ -216,8 +216,12 @@ __global__ void subscale_batch_kernel(SubScaleBatch B, int limbs, int logn, cons
 // A CTA owns 64 coefficients of one limb: it stages the b babies' (c0, c1)
 // words for those coefficients in shared memory once, then each warp streams
 // the plaintext diagonals of its giants (16-byte loads, 512 B per warp row).
+// D > 0: each lane streams its 16-byte share of the diagonal tiles through a
+// private D+1-slot shared-memory ring with cp.async (no registers held by the
+// in-flight loads; every lane reads back only what it copied, so no barrier).
+template <int D>
 __global__ void vmm_mac_kernel(VmmMacArgs A, const u64* Q, const u64* MH, const u64* ML) {
-  extern __shared__ u64 sb[];  // [b][2][64]
+  extern __shared__ u64 sb[];  // [b][2][64] babies, then (D > 0) [warps][D + 1][64] diagonal ring
   const int n = A.n;
   const int tiles_per_limb = n / 64;
   const int l = blockIdx.x / tiles_per_limb;
@@ -234,8 +238,26 @@ __global__ void vmm_mac_kernel(VmmMacArgs A, const u64* Q, const u64* MH, const 
     U128 a0{0, 0}, a1{0, 0}, b0{0, 0}, b1{0, 0};
     const int gbase = A.gidx[g2] * A.b;
     const int cnt = min(A.b, A.k - gbase);
+    u64* ring = sb + (size_t)A.b * 128 + (size_t)warp * (D + 1) * 64;
+    auto issue = [&](int g1) {
+      if (g1 < cnt) {
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(ring + (g1 % (D + 1)) * 64 + 2 * lane);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(A.pt[gbase + g1] + base + 2 * lane)
+                     : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if constexpr (D > 0)
+      for (int u = 0; u < D; ++u) issue(u);
     for (int g1 = 0; g1 < cnt; ++g1) {
-      const ulonglong2 p = reinterpret_cast<const ulonglong2*>(A.pt[gbase + g1] + base)[lane];
+      ulonglong2 p;
+      if constexpr (D > 0) {
+        issue(g1 + D);
+        asm volatile("cp.async.wait_group %0;" ::"n"(D) : "memory");
+        p = reinterpret_cast<const ulonglong2*>(ring + (g1 % (D + 1)) * 64)[lane];
+      } else {
+        p = reinterpret_cast<const ulonglong2*>(A.pt[gbase + g1] + base)[lane];
+      }
       const u64* s = sb + g1 * 128;
       mac128(a0, s[2 * lane], p.x);
       mac128(b0, s[2 * lane + 1], p.y);
@@ -466,15 +488,28 @@ void b_subscale(Context& c, const SubScaleBatch& B, int limbs, const u64* inv, c
 
 void b_vmm_mac(Context& c, const VmmMacArgs& A, int limbs) {
   SF_HPROF("b_vmm_mac");
-  const size_t sm = (size_t)A.b * 2 * 64 * sizeof(u64);
+  // diagonal ring depth: 4 (measured best: 6.1 -> 5.8 ms/step vs direct loads; 8 and 12 lose
+  // occupancy); SF_VARIANT bits 5-6 select 0 / 8 / 12 for A/B
+  static const int kDepth[4] = {4, 0, 8, 12};
+  const int D = kDepth[(c.variant >> 5) & 3];
+  const size_t sm = (size_t)A.b * 2 * 64 * sizeof(u64) + (D ? (size_t)8 * (D + 1) * 64 * sizeof(u64) : 0);
   // algorithmic bytes: every diagonal once, babies once, partials once
   ProfScope prof(c, kFamMac, 8.0 * c.n * limbs * ((double)A.k + 2.0 * A.b + 2.0 * A.giants));
   static bool attr = false;
   if (!attr) {
-    SF_CUDA(cudaFuncSetAttribute(vmm_mac_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    SF_CUDA(cudaFuncSetAttribute(vmm_mac_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    SF_CUDA(cudaFuncSetAttribute(vmm_mac_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    SF_CUDA(cudaFuncSetAttribute(vmm_mac_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    SF_CUDA(cudaFuncSetAttribute(vmm_mac_kernel<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
-  vmm_mac_kernel<<<(unsigned)(limbs * (c.n / 64)), 256, sm, c.stream>>>(A, c.tabs.q, c.tabs.mh, c.tabs.ml);
+  const unsigned grid = (unsigned)(limbs * (c.n / 64));
+  switch (D) {
+    case 4: vmm_mac_kernel<4><<<grid, 256, sm, c.stream>>>(A, c.tabs.q, c.tabs.mh, c.tabs.ml); break;
+    case 8: vmm_mac_kernel<8><<<grid, 256, sm, c.stream>>>(A, c.tabs.q, c.tabs.mh, c.tabs.ml); break;
+    case 12: vmm_mac_kernel<12><<<grid, 256, sm, c.stream>>>(A, c.tabs.q, c.tabs.mh, c.tabs.ml); break;
+    default: vmm_mac_kernel<0><<<grid, 256, sm, c.stream>>>(A, c.tabs.q, c.tabs.mh, c.tabs.ml);
+  }
   post(c);
 }
 
