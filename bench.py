@@ -241,7 +241,12 @@ def run_sharded(args, be, sf, layer, dist, rank, world, clk):
     from paper_2602_11470_b200 import shard
     import torch
     stream = not args.shard_host
-    sh = shard.StreamSharded(be) if stream else shard.Sharded(be)
+    if args.shard_host:
+        sh = shard.Sharded(be)
+    elif args.shard_nccl:
+        sh = shard.StreamSharded(be)
+    else:  # default: the fused peer-memory exchange (csrc/p2p.cu)
+        sh = shard.PeerSharded(be)
     ref = layer.step()  # the single-device step on every rank, for the bit-exactness check
     got = layer.step_sharded(sh)
     exact = all(np.array_equal(a.data(), b.data()) for a, b in zip(ref, got))
@@ -313,7 +318,10 @@ def run_sharded(args, be, sf, layer, dist, rank, world, clk):
             "data": "synthetic: reference bench weights sin(0.001(31r+c)+0.25), N(0,1) activations/cache, seeded",
             "config": {"workload": "llama3-8b-layer-decode@n'=2048", "ring_degree": 2 * SLOTS, "slots": SLOTS,
                        "d": D, "heads": H, "ffn": FF, "context": NP, "levels": LEVELS, "L": 7, "alpha": args.alpha,
-                       "parallelism": f"sharded{world} (giant / key-ct / pair groups, NCCL all-gather + mod-add)",
+                       "parallelism": f"sharded{world} (giant / key-ct / pair groups; exchange: " +
+                                      ("torch-stream NCCL all-gather + mod-add" if args.shard_host else
+                                       "NCCL all-gather on the library stream + mod-add" if args.shard_nccl else
+                                       "fused peer-memory read + mod-add kernel (CUDA IPC / NVLink)") + ")",
                        "l2": "working set >> 126 MB L2; no flush needed"},
             "sharded_bit_exact_vs_single_device": bool(ex.item()),
             "eager_ms_per_step": round(ms_eager, 3), "wall_ms_per_step_rank0_eager": round(wall, 3),
@@ -321,7 +329,7 @@ def run_sharded(args, be, sf, layer, dist, rank, world, clk):
                     "h2d_bytes_per_step": int(sum(w.nbytes for w in host_in)),
                     "d2h_bytes_per_step": int(sum(r.nbytes for r in res))},
             "gpu_launches": int(launches) if graph else None, "clocks": clk.summary(), "cpu_baseline": None,
-            "execution": ("one CUDA graph per step; NCCL all-gathers on the library stream inside it" if graph else
+            "execution": ("one CUDA graph per step; the exchanges on the library stream inside it" if graph else
                           "eager (host-issued; NCCL exchanges on torch's stream between library launches)"),
         }
         print(json.dumps(line), flush=True)
@@ -422,8 +430,13 @@ def main():
                     help="strong scaling: split ONE token over the ranks (default: one replica per GPU)")
     ap.add_argument("--shard-host", action="store_true",
                     help="with --shard: exchange on torch's stream (eager) instead of the library stream + graph")
+    ap.add_argument("--shard-nccl", action="store_true",
+                    help="with --shard: NCCL all-gather on the library stream instead of the peer-memory exchange")
     args = ap.parse_args()
 
+    # NCCL announces its version on stdout at communicator creation unless told
+    # otherwise; rank 0's stdout must carry exactly one JSON line
+    os.environ.setdefault("NCCL_DEBUG", "WARN")
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))

@@ -271,6 +271,17 @@ sf_status sf_vmm_multi_finish(sf_context* ctx, const sf_ct* const* accs, sf_vmm_
  * rank then calls sf_comm_init with its rank and the world size.
  * Results are bit-identical to the unsharded sf_vmm / sf_qk_dot /
  * sf_softmax_times_v. */
+/* Exchange over peer memory instead of NCCL (SURVEY §8(e) "fused P2P"): each
+ * rank allocates a symmetric buffer of 2 x cap_words words (sf_p2p_init returns
+ * its 64-byte CUDA IPC handle), the caller all-gathers the handles (any
+ * transport) and passes world x 64 bytes to sf_p2p_open. The sharded
+ * operators then publish their partials into the buffer and ONE kernel per
+ * exchange reads every rank's partial over NVLink and sums them mod q --
+ * graph-capturable (device-side epochs, release/acquire flags). Takes
+ * precedence over sf_comm_init when both are set. */
+sf_status sf_p2p_init(sf_context* ctx, int rank, int world, size_t cap_words, uint8_t handle_out[64]);
+sf_status sf_p2p_open(sf_context* ctx, const uint8_t* handles, int world);
+sf_status sf_p2p_destroy(sf_context* ctx);
 sf_status sf_comm_unique_id(uint8_t id_out[128]);
 sf_status sf_comm_init(sf_context* ctx, const uint8_t id[128], int rank, int world);
 sf_status sf_comm_destroy(sf_context* ctx);

@@ -123,6 +123,9 @@ SIGNATURES = {
     "sf_vmm_multi_partial": (st, [vp, vp, vpp, C.c_int, C.c_int, C.c_int, vpp]),
     "sf_vmm_multi_finish": (st, [vp, vpp, vpp, C.c_int, C.c_int, vpp]),
     "sf_vmm_multi_sharded": (st, [vp, vp, vpp, C.c_int, C.c_int, vpp]),
+    "sf_p2p_init": (st, [vp, C.c_int, C.c_int, C.c_size_t, C.c_char_p]),
+    "sf_p2p_open": (st, [vp, C.c_char_p, C.c_int]),
+    "sf_p2p_destroy": (st, [vp]),
     "sf_comm_unique_id": (st, [C.c_char_p]),
     "sf_comm_init": (st, [vp, C.c_char_p, C.c_int, C.c_int]),
     "sf_comm_destroy": (st, [vp]),

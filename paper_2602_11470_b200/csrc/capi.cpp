@@ -704,6 +704,29 @@ sf_status sf_sum_partials(sf_context* ctx, const sf_ct* const* parts, int n, sf_
     *out = wrap(sf::sum_partials(*ctx->c, p));
   });
 }
+sf_status sf_p2p_init(sf_context* ctx, int rank, int world, size_t cap_words, uint8_t handle_out[64]) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(handle_out, "handle_out");
+    sf::p2p_init(*ctx->c, rank, world, cap_words, handle_out);
+  });
+}
+sf_status sf_p2p_open(sf_context* ctx, const uint8_t* handles, int world) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(handles, "handles");
+    int r, w;
+    sf::p2p_rank_world(*ctx->c, r, w);
+    sf::require(w == world, sf::kShapeMismatch, "p2p_open: world size differs from sf_p2p_init");
+    sf::p2p_open(*ctx->c, handles);
+  });
+}
+sf_status sf_p2p_destroy(sf_context* ctx) {
+  return guard([&] {
+    need(ctx, "ctx");
+    sf::p2p_destroy(*ctx->c);
+  });
+}
 sf_status sf_comm_unique_id(uint8_t id_out[128]) {
   return guard([&] {
     need(id_out, "id_out");

@@ -133,6 +133,16 @@ std::vector<std::vector<Ct>> allgather_cts(Context& c, const std::vector<const C
 
 }  // namespace
 
+static void rank_world(Context& c, int& rank, int& world) {
+  if (c.p2p) {
+    p2p_rank_world(c, rank, world);
+    return;
+  }
+  require(c.comm != nullptr, kInvalidTarget, "sharded ops: initialise an exchange (sf_comm_init or sf_p2p_init)");
+  rank = c.rank;
+  world = c.world;
+}
+
 void comm_unique_id(uint8_t* out) {
   ncclUniqueId id;
   nccl_check(nccl().get_unique_id(&id), "ncclGetUniqueId");
@@ -156,11 +166,17 @@ void comm_destroy(Context& c) {
   c.comm = nullptr;
 }
 
+// rank / world of the active exchange: peer memory (p2p.cu) when initialised, else NCCL
+static void rank_world(Context& c, int& rank, int& world);
+
 Ct vmm_sharded(Context& c, const Ct& x, VmmPlan& plan, bool mask_output) {
   SF_HPROF("vmm_sharded");
-  Ct part = vmm_partial(c, x, plan, c.rank, c.world);
+  int rank, world;
+  rank_world(c, rank, world);
+  Ct part = vmm_partial(c, x, plan, rank, world);
   char tag[64];
   std::snprintf(tag, sizeof tag, "vmm:%p", (const void*)&plan);
+  if (c.p2p) return vmm_finish(c, p2p_sum_cts(c, {&part}, tag)[0], plan, mask_output);
   auto got = allgather_cts(c, {&part}, tag);
   std::vector<const Ct*> ps;
   for (int r = 0; r < c.world; ++r) ps.push_back(&got[r][0]);
@@ -169,11 +185,14 @@ Ct vmm_sharded(Context& c, const Ct& x, VmmPlan& plan, bool mask_output) {
 
 std::vector<Ct> vmm_multi_sharded(Context& c, const Ct& x, const std::vector<VmmPlan*>& plans, bool mask_output) {
   SF_HPROF("vmm_multi_sharded");
-  std::vector<Ct> parts = vmm_multi_partial(c, x, plans, c.rank, c.world);
+  int rank, world;
+  rank_world(c, rank, world);
+  std::vector<Ct> parts = vmm_multi_partial(c, x, plans, rank, world);
   std::vector<const Ct*> pp;
   for (auto& p : parts) pp.push_back(&p);
   char tag[64];
   std::snprintf(tag, sizeof tag, "vmm_multi:%p", (const void*)plans[0]);
+  if (c.p2p) return vmm_multi_finish(c, p2p_sum_cts(c, pp, tag), plans, mask_output);
   auto got = allgather_cts(c, pp, tag);
   std::vector<Ct> accs;
   for (size_t i = 0; i < parts.size(); ++i) {
@@ -186,9 +205,12 @@ std::vector<Ct> vmm_multi_sharded(Context& c, const Ct& x, const std::vector<Vmm
 
 std::vector<Ct> qk_dot_sharded(Context& c, const Ct& q, const KV& cache) {
   SF_HPROF("qk_dot_sharded");
-  std::vector<Ct> maps = qk_dot_partial(c, q, cache, c.rank, c.world);
+  int rank, world;
+  rank_world(c, rank, world);
+  std::vector<Ct> maps = qk_dot_partial(c, q, cache, rank, world);
   std::vector<const Ct*> mp;
   for (auto& m : maps) mp.push_back(&m);
+  if (c.p2p) return p2p_sum_cts(c, mp, "qk:" + std::to_string(cache.n_prime));
   auto got = allgather_cts(c, mp, "qk:" + std::to_string(cache.n_prime));
   std::vector<Ct> out;
   for (size_t m = 0; m < maps.size(); ++m) {
@@ -201,8 +223,20 @@ std::vector<Ct> qk_dot_sharded(Context& c, const Ct& q, const KV& cache) {
 
 Ct softmax_times_v_sharded(Context& c, const std::vector<Ct>& probs, const KV& cache) {
   SF_HPROF("softmax_times_v_sharded");
-  Ct3 part = softmax_times_v_partial(c, probs, cache, c.rank, c.world);
+  int rank, world;
+  rank_world(c, rank, world);
+  Ct3 part = softmax_times_v_partial(c, probs, cache, rank, world);
   part.d01.zero = part.d2.zero = part.zero;
+  if (c.p2p) {  // the parts' sum over peer memory; finish charges the exchange additions once
+    std::vector<int> live;
+    std::vector<Ct> sum = p2p_sum_cts(c, {&part.d01, &part.d2}, "sv:" + std::to_string(cache.n_prime), false, &live);
+    Ct3 tot;
+    tot.d01 = sum[0];
+    tot.d2 = sum[1];
+    tot.zero = live[0] == 0;
+    if (live[0] > 1) c.ledger.add(live[0] - 1);
+    return softmax_times_v_finish(c, {&tot}, cache);
+  }
   auto got = allgather_cts(c, {&part.d01, &part.d2}, "sv:" + std::to_string(cache.n_prime));
   std::vector<Ct3> parts(c.world);
   std::vector<const Ct3*> pp;

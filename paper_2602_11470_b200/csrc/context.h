@@ -165,6 +165,7 @@ struct Context {
   void* comm = nullptr;
   int rank = 0, world = 1;
   std::map<std::string, std::vector<u64>> comm_hdr, comm_meta;
+  void* p2p = nullptr;  // peer-memory exchange state (p2p.cu)
   std::vector<std::pair<u64*, size_t>> capture_deferred;
   long long graph_launch_base = 0;
   bool ks_row = true;  // fused key-switch row stage
@@ -237,6 +238,7 @@ void ntt_list(Context& c, const std::vector<std::pair<u64*, int>>& limbs, bool i
 // --- evaluator (evaluator.cu) -------------------------------------------------
 BufPtr make_buf(Context& c, size_t words);
 Ct alloc_ct(Context& c, int limbs, double scale);
+void p2p_destroy(Context& c);  // p2p.cu
 Pt encode_pt(Context& c, const double* slots, double scale, int limbs);
 std::vector<Pt> encode_many(Context& c, const std::function<void(int, double*)>& gen, int count, double scale,
                             int limbs);

@@ -47,6 +47,7 @@ static BufPtr buf(Context& c, size_t words) { return make_buf(c, words); }
 
 Context::~Context() {
   if (stream) cudaStreamSynchronize(stream);
+  p2p_destroy(*this);
   keys.clear();
   conv_plans.clear();
   pt_cache.clear();

@@ -105,6 +105,14 @@ std::vector<Ct> vmm_multi_sharded(Context& c, const Ct& x, const std::vector<Vmm
 std::vector<Ct> qk_dot_sharded(Context& c, const Ct& q, const KV& cache);
 Ct softmax_times_v_sharded(Context& c, const std::vector<Ct>& probs, const KV& cache);
 
+// --- sharded ops with the exchange over peer memory (p2p.cu) --------------------
+void p2p_init(Context& c, int rank, int world, size_t cap_words, uint8_t* handle_out64);
+void p2p_open(Context& c, const uint8_t* handles);  // world x 64 bytes
+void p2p_destroy(Context& c);
+void p2p_rank_world(Context& c, int& rank, int& world);
+std::vector<Ct> p2p_sum_cts(Context& c, const std::vector<const Ct*>& cts, const std::string& tag, bool charge = true,
+                            std::vector<int>* live_out = nullptr);
+
 // --- wire / on-disk formats (wire.cpp) ---------------------------------------
 std::vector<double> load_weight(const std::string& dir, const std::string& name, int* rows, int* cols);
 size_t ct_wire_size(const Context& c, const Ct& a);

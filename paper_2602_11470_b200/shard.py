@@ -243,3 +243,27 @@ class StreamSharded:
     def softmax_times_v(self, probs, cache: KVCache) -> Ciphertext:
         arr = (C.c_void_p * len(probs))(*[p.h for p in probs])
         return _ct(self.be, _native.lib().sf_softmax_times_v_sharded, arr, len(probs), cache.h)
+
+
+class PeerSharded(StreamSharded):
+    """The sharded operators with the exchange over peer memory
+    (csrc/p2p.cu): every rank publishes its partial ciphertexts into a
+    symmetric buffer exported with CUDA IPC, and one kernel per exchange reads
+    all ranks' partials over NVLink and sums them mod q (the all-gather and the
+    mod-add fused; no collective library). The IPC handles travel once over
+    the torch.distributed group. `cap_words` sizes each of the two slots (the
+    largest exchange of a decode step at ring 2^16 is two degree-2 Score*V
+    parts at 3 limbs: ~1.6 M words)."""
+
+    def __init__(self, be: Backend, group=None, cap_words: int = 1 << 21):
+        import torch.distributed as dist
+        self.be, self.group = be, group
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        h = C.create_string_buffer(64)
+        _check(_native.lib().sf_p2p_init(be.ctx, self.rank, self.world, cap_words, h))
+        got: list = [None] * self.world
+        dist.all_gather_object(got, h.raw, group=group)
+        _check(_native.lib().sf_p2p_open(be.ctx, b"".join(got), self.world))
+
+    def close(self) -> None:
+        _check(_native.lib().sf_p2p_destroy(self.be.ctx))

@@ -39,13 +39,16 @@ def _cache(sf, be, cfg, n, L, rng):
     return cache
 
 
-def test_stream_sharded_ops_world1(world1):
+@pytest.mark.parametrize("kind", ["nccl", "peer"])
+def test_stream_sharded_ops_world1(world1, kind):
+    """kind "nccl": NCCL all-gather on the library stream; "peer": the fused
+    peer-memory exchange (csrc/p2p.cu; with one rank the peer is itself)."""
     import paper_2602_11470_b200 as sf
     from paper_2602_11470_b200 import shard
     N, L, d, H, n = 2048, 6, 128, 4, 40
     rng = np.random.default_rng(5)
     be = sf.Backend(N, L, alpha=2)
-    sh = shard.StreamSharded(be)
+    sh = shard.StreamSharded(be) if kind == "nccl" else shard.PeerSharded(be, cap_words=1 << 17)
     try:
         # VMM
         W = rng.normal(size=(256, 128)) / 16
