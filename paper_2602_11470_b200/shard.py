@@ -266,4 +266,8 @@ class PeerSharded(StreamSharded):
         _check(_native.lib().sf_p2p_open(be.ctx, b"".join(got), self.world))
 
     def close(self) -> None:
+        """Free the symmetric buffer once every rank is done reading it."""
+        import torch.distributed as dist
+        self.be.synchronize()
+        dist.barrier(group=self.group)
         _check(_native.lib().sf_p2p_destroy(self.be.ctx))
