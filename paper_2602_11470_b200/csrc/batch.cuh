@@ -134,6 +134,7 @@ struct EpiBatch {
   u64 g[kJobsWide];
   u64 inv[kJobsWide], inv_s[kJobsWide];
   uint8_t prime[kJobsWide];
+  bool nomul = false;  // out = acc - v (+ addend): P^-1 already folded in (rotation sums)
 };
 
 // Fused key-switch row stage (ntt.cu ks_row_kernel): per (source, target prime
@@ -172,6 +173,7 @@ struct KsSumArgs {
   int nout = 0, limbs = 0, nt = 0, ndig = 0, alpha = 0, np = 0;
   int tprime[kMaxPrimes];
   u64 pm[kMaxPrimes];  // P mod q_t, t < limbs
+  bool pm_one = false;  // keys carry P^-1 on the Q limbs (get_key_pinv): pm == 1, ModDown without P^-1
   int out_begin[kSumOuts + 1];
   u64* acc[kSumOuts];  // [2][nt][n]
   int jsrc[kSumJobs];

@@ -187,6 +187,7 @@ struct Context {
   BufPtr sk;  // [np][n] NTT domain
   std::map<u64, BufPtr> keys;  // galois element (0 = relin) -> [beta][2][np][n]
   std::map<std::string, ConvPlan> conv_plans;
+  std::map<u64, BufPtr> keys_pinv;  // switching keys with the Q limbs times P^-1 (get_key_pinv)
   std::map<std::string, Pt> pt_cache;  // semantic-key plaintext cache (masks)
   std::map<int, BufPtr> level_consts;  // per-limb-count rescale / moddown constants
   std::map<int, std::vector<u64>> level_consts_h;
@@ -258,6 +259,7 @@ Ct level_drop(Context& c, const Ct& a, int target);
 Ct bootstrap(Context& c, const Ct& a, int target);
 u64 galois_elt(const Context& c, int r);
 const BufPtr& get_key(Context& c, u64 g);
+const BufPtr& get_key_pinv(Context& c, u64 g);  // Q limbs times P^-1 (rotation sums)
 void check_ct(const Context& c, const Ct& a, const char* what);
 void check_scales(const Ct& a, const Ct& b, const char* what);
 

@@ -49,6 +49,7 @@ Context::~Context() {
   if (stream) cudaStreamSynchronize(stream);
   p2p_destroy(*this);
   keys.clear();
+  keys_pinv.clear();
   conv_plans.clear();
   pt_cache.clear();
   level_consts.clear();
@@ -202,12 +203,13 @@ const u64* level_consts(Context& c, int limbs) {
   return b->p;
 }
 
-const ConvPlan& conv_plan(Context& c, const std::vector<int>& src, const std::vector<int>& dst) {
+const ConvPlan& conv_plan(Context& c, const std::vector<int>& src, const std::vector<int>& dst, bool pinv) {
   SF_HPROF("conv_plan");
   std::string key;
   for (int s : src) key += std::to_string(s) + ",";
   key += ">";
   for (int d : dst) key += std::to_string(d) + ",";
+  if (pinv) key += ":pinv";  // destination constants times (prod src)^-1: ModDown with the P^-1 folded in
   std::lock_guard<std::mutex> lk(c.mu);
   auto it = c.conv_plans.find(key);
   if (it != c.conv_plans.end()) return it->second;
@@ -232,6 +234,7 @@ const ConvPlan& conv_plan(Context& c, const std::vector<int>& src, const std::ve
       u64 hm = 1 % pd;
       for (int k = 0; k < p.nsrc; ++k)
         if (k != i) hm = mulmod_h(hm, c.primes[src[k]] % pd, pd);
+      if (pinv) hm = invmod_h(c.primes[src[i]] % pd, pd);  // qhat_i * (prod src)^-1 = src_i^-1
       h[2 * p.nsrc + (size_t)i * p.ndst + d] = hm;
       h[base2 + 2 * p.nsrc + (size_t)i * p.ndst + d] = shoup_h(hm, pd);
     }
@@ -516,6 +519,37 @@ const BufPtr& get_key(Context& c, u64 g) {
   }
   std::lock_guard<std::mutex> lk(c.mu);
   return c.keys.emplace(g, key).first->second;
+}
+
+// get_key with the Q-prime limbs multiplied by P^-1: the
+// rotation-sum inner products then land already divided by P on the Q
+// primes, the P*sigma(c0) terms become plain additions and ModDown's final
+// multiply disappears. The special-prime limbs are unchanged (ModDown's
+// conversion input). Results are bit-identical (exact modular identities).
+const BufPtr& get_key_pinv(Context& c, u64 g) {
+  SF_HPROF("get_key_pinv");
+  {
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto it = c.keys_pinv.find(g);
+    if (it != c.keys_pinv.end()) return it->second;
+  }
+  const BufPtr& k = get_key(c, g);
+  const size_t words = (size_t)c.beta * 2 * c.np * c.n;
+  BufPtr out = buf(c, words);
+  SF_CUDA(cudaMemcpyAsync(out->p, k->p, words * sizeof(u64), cudaMemcpyDeviceToDevice, c.stream));
+  std::vector<u64> f(c.np, 1);
+  for (int m = 0; m <= c.L; ++m) {
+    const u64 q = c.primes[m];
+    u64 pm = 1 % q;
+    for (int kk = 0; kk < c.alpha; ++kk) pm = mulmod_h(pm, c.primes[c.P_index(kk)] % q, q);
+    f[m] = invmod_h(pm, q);
+  }
+  BufPtr fd = buf(c, f.size());
+  SF_CUDA(cudaMemcpyAsync(fd->p, f.data(), f.size() * sizeof(u64), cudaMemcpyHostToDevice, c.stream));
+  k_scale_limbs(c, out->p, c.beta * 2, fd->p);
+  SF_CUDA(cudaStreamSynchronize(c.stream));  // f is pageable; keys are built once, off the timed path
+  std::lock_guard<std::mutex> lk(c.mu);
+  return c.keys_pinv.emplace(g, out).first->second;
 }
 
 Ct level_drop(Context& c, const Ct& a, int target) {

@@ -360,6 +360,16 @@ __global__ void dec_combine_kernel(u64* out, const u64* c0, const u64* c1, const
     out[i] = add_mod(c0[i], mulmod(c1[i], s[i], Q[0], MH[0], ML[0]), Q[0]);
 }
 
+// data[blk][m][n] *= F[m] (mod prime m) for the primes with F[m] != 1 (blk = nblk blocks of np primes)
+__global__ void scale_limbs_kernel(u64* data, size_t total, int np, int n, const u64* F, const u64* Q, const u64* MH,
+                                   const u64* ML) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const int m = (int)((i / n) % np);
+    const u64 f = F[m];
+    if (f != 1) data[i] = mulmod(data[i], f, Q[m], MH[m], ML[m]);
+  }
+}
+
 __global__ void square_kernel(u64* out, const u64* s, int limbs, int n, const u64* Q, const u64* MH,
                               const u64* ML) {
   const size_t total = (size_t)limbs * n;
@@ -557,6 +567,13 @@ void k_enc_combine(Context& c, u64* c0, const u64* a, const u64* s, const u64* e
 
 void k_dec_combine(Context& c, u64* out, const u64* c0, const u64* c1, const u64* s) {
   dec_combine_kernel<<<grid_cap(c.n), kThreads, 0, c.stream>>>(out, c0, c1, s, c.n, QP(c), c.tabs.mh, c.tabs.ml);
+  post_launch(c);
+}
+
+void k_scale_limbs(Context& c, u64* data, int nblk, const u64* F_dev) {
+  const size_t total = (size_t)nblk * c.np * c.n;
+  scale_limbs_kernel<<<grid_cap(total), kThreads, 0, c.stream>>>(data, total, c.np, c.n, F_dev, c.tabs.q, c.tabs.mh,
+                                                                 c.tabs.ml);
   post_launch(c);
 }
 

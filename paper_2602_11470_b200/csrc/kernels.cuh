@@ -54,5 +54,6 @@ void k_enc_combine(Context& c, u64* c0, const u64* a, const u64* s, const u64* e
 void k_dec_combine(Context& c, u64* out, const u64* c0, const u64* c1, const u64* s);
 // sk' = sigma_g(s) or s*s over all primes
 void k_square(Context& c, u64* out, const u64* s, int limbs);
+void k_scale_limbs(Context& c, u64* data, int nblk, const u64* F_dev);  // data[blk][m][n] *= F[m] mod prime m
 
 }  // namespace sf

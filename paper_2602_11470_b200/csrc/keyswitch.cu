@@ -18,7 +18,7 @@ namespace sf {
 
 BufPtr make_buf(Context& c, size_t words);
 const u64* level_consts(Context& c, int limbs);
-const ConvPlan& conv_plan(Context& c, const std::vector<int>& src, const std::vector<int>& dst);
+const ConvPlan& conv_plan(Context& c, const std::vector<int>& src, const std::vector<int>& dst, bool pinv = false);
 OptLayout merge_layouts(const Ct& a, const Ct& b);
 
 namespace {
@@ -496,13 +496,16 @@ void ks_jobs(Context& c, const ExtB& x, const std::vector<KsJob>& jobs, bool mer
 // extended-basis polynomials acc = [nt][n]. p_rowpassed: the P limbs already
 // had ModDown's inverse row pass (fused path); otherwise they are NTT domain.
 
-void mod_down_polys(Context& c, int limbs, const std::vector<MdPoly>& P, bool p_rowpassed) {
+void mod_down_polys(Context& c, int limbs, const std::vector<MdPoly>& P, bool p_rowpassed, bool prescaled = false) {
   SF_HPROF("mod_down_polys");
   const size_t n = c.n;
   std::vector<int> pidx, qidx;
   for (int k = 0; k < c.alpha; ++k) pidx.push_back(c.P_index(k));
   for (int l = 0; l < limbs; ++l) qidx.push_back(l);
-  const ConvPlan& down = conv_plan(c, pidx, qidx);
+  require(!prescaled || fused_path(c), kInternal, "mod_down_polys: P^-1-prescaled input needs the fused path");
+  // prescaled: the Q limbs of acc already carry P^-1, so the conversion constants
+  // do too and the combine is a plain subtraction
+  const ConvPlan& down = conv_plan(c, pidx, qidx, prescaled);
   const u64* kc = level_consts(c, limbs);
   for (size_t s0 = 0; s0 < P.size(); s0 += kJobsWide) {
     const int J = (int)std::min<size_t>(kJobsWide, P.size() - s0);
@@ -530,6 +533,7 @@ void mod_down_polys(Context& c, int limbs, const std::vector<MdPoly>& P, bool p_
       }
       b_fused_col(c, A);
       EpiBatch E;
+      E.nomul = prescaled;
       for (int j = 0; j < J; ++j) {
         const MdPoly& m = P[s0 + j];
         for (int l = 0; l < limbs; ++l) {
@@ -622,10 +626,12 @@ std::vector<Ct> rot_sum_batch(Context& c, const std::vector<std::vector<SumTerm>
   const size_t n = c.n;
   for (auto& [limbs, gidx] : by_limbs) {
     std::vector<u64> pm(limbs);
+    // fused path: keys with P^-1 on the Q limbs (bit-identical results, fewer products)
+    const bool pre = fused_path(c);
     for (int l = 0; l < limbs; ++l) {
       u64 r = 1 % c.primes[l];
       for (int k = 0; k < c.alpha; ++k) r = mulmod_h(r, c.primes[c.P_index(k)] % c.primes[l], c.primes[l]);
-      pm[l] = r;
+      pm[l] = pre ? 1 : r;
     }
     size_t gpos = 0;
     while (gpos < gidx.size()) {
@@ -661,6 +667,7 @@ std::vector<Ct> rot_sum_batch(Context& c, const std::vector<std::vector<SumTerm>
       A.np = c.np;
       for (int t = 0; t < nt; ++t) A.tprime[t] = x.tprime[t];
       for (int l = 0; l < limbs; ++l) A.pm[l] = pm[l];
+      A.pm_one = pre;
       for (size_t s = 0; s < srcv.size(); ++s) {
         A.c0[s] = srcv[s]->c0();
         A.c1[s] = srcv[s]->c1(c.n);
@@ -676,7 +683,7 @@ std::vector<Ct> rot_sum_batch(Context& c, const std::vector<std::vector<SumTerm>
           const int r = pos_mod(tm.r, c.slots);
           A.jsrc[jb] = src[tm.ct];
           A.g[jb] = r == 0 ? 1 : galois_elt(c, r);
-          A.key[jb] = r == 0 ? nullptr : get_key(c, A.g[jb])->p;
+          A.key[jb] = r == 0 ? nullptr : (pre ? get_key_pinv(c, A.g[jb]) : get_key(c, A.g[jb]))->p;
           ++jb;
         }
         const Ct& y = out[chunk[o]];
@@ -686,7 +693,7 @@ std::vector<Ct> rot_sum_batch(Context& c, const std::vector<std::vector<SumTerm>
       A.out_begin[chunk.size()] = jb;
       A.nout = (int)chunk.size();
       b_ks_sum(c, A);
-      mod_down_polys(c, limbs, md, fused_path(c));
+      mod_down_polys(c, limbs, md, fused_path(c), pre);
     }
   }
   return out;

@@ -80,8 +80,9 @@ __global__ void __launch_bounds__(kWarps * 32) ntt_row_pass(LimbBatch B, Tabs T)
   }
 }
 
-// Forward row pass + combine epilogue (EpiBatch): out = (acc - v) * inv (+ addend).
-template <int LOGR, int LOGC>
+// Forward row pass + combine epilogue (EpiBatch): out = (acc - v) * inv (+ addend);
+// NOMUL: out = acc - v (+ addend) (ModDown with P^-1 folded into the keys and the conversion).
+template <int LOGR, int LOGC, bool NOMUL>
 __global__ void __launch_bounds__(kWarps * 32) ntt_row_epi(EpiBatch B, Tabs T) {
   constexpr int C = 1 << LOGC, E = C / 32, LOGN = LOGR + LOGC;
   constexpr int tiles = (1 << LOGR) / kWarps;
@@ -113,8 +114,12 @@ __global__ void __launch_bounds__(kWarps * 32) ntt_row_epi(EpiBatch B, Tabs T) {
 #pragma unroll
   for (int k = 0; k < E; k += 2) {
     const ulonglong2 av = *reinterpret_cast<const ulonglong2*>(acc + base + k);
-    u64 v0 = mul_shoup(sub_mod(av.x, canon4(x[k], q), q), inv, inv_s, q);
-    u64 v1 = mul_shoup(sub_mod(av.y, canon4(x[k + 1], q), q), inv, inv_s, q);
+    u64 v0 = sub_mod(av.x, canon4(x[k], q), q);
+    u64 v1 = sub_mod(av.y, canon4(x[k + 1], q), q);
+    if constexpr (!NOMUL) {
+      v0 = mul_shoup(v0, inv, inv_s, q);
+      v1 = mul_shoup(v1, inv, inv_s, q);
+    }
     if (addend) {
       if (g > 1) {
         v0 = add_mod(v0, addend[auto_perm((uint32_t)(base + k), g, LOGN)], q);
@@ -593,7 +598,13 @@ struct ShflPerm {
   }
 };
 
-template <int LOGR, int LOGC, bool PF, bool SH>
+__device__ __forceinline__ void add128(U128& acc, uint64_t a) {
+  asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, 0;" : "+l"(acc.lo), "+l"(acc.hi) : "l"(a));
+}
+
+// PM1: the keys' Q limbs carry P^-1 (get_key_pinv), so the P * sigma(c0) and
+// P * (c0, c1) terms are plain additions
+template <int LOGR, int LOGC, bool PF, bool SH, bool PM1>
 __global__ void __launch_bounds__(kWarps * 32, 2) ks_sum_kernel(KsSumArgs A, Tabs T) {
   constexpr int C = 1 << LOGC, E = C / 32, LOGN = LOGR + LOGC;
   auto rbr = [](uint32_t col) { return __brev(col) >> (32 - LOGC); };
@@ -634,10 +645,17 @@ __global__ void __launch_bounds__(kWarps * 32, 2) ks_sum_kernel(KsSumArgs A, Tab
       for (int k = 0; k < E; k += 2) {
         const ulonglong2 v0 = reinterpret_cast<const ulonglong2*>(a0)[k / 2];
         const ulonglong2 v1 = reinterpret_cast<const ulonglong2*>(a1)[k / 2];
-        mac128(sb[k], v0.x, pm);
-        mac128(sb[k + 1], v0.y, pm);
-        mac128(sa[k], v1.x, pm);
-        mac128(sa[k + 1], v1.y, pm);
+        if constexpr (PM1) {
+          add128(sb[k], v0.x);
+          add128(sb[k + 1], v0.y);
+          add128(sa[k], v1.x);
+          add128(sa[k + 1], v1.y);
+        } else {
+          mac128(sb[k], v0.x, pm);
+          mac128(sb[k + 1], v0.y, pm);
+          mac128(sa[k], v1.x, pm);
+          mac128(sa[k + 1], v1.y, pm);
+        }
       }
       ++terms;
       continue;
@@ -680,7 +698,12 @@ __global__ void __launch_bounds__(kWarps * 32, 2) ks_sum_kernel(KsSumArgs A, Tab
         }
         sp.apply(x);
 #pragma unroll
-        for (int k = 0; k < E; ++k) mac128(sb[k], x[k], pm);
+        for (int k = 0; k < E; ++k) {
+          if constexpr (PM1)
+            add128(sb[k], x[k]);
+          else
+            mac128(sb[k], x[k], pm);
+        }
       }
       terms += A.ndig + 1;
       continue;
@@ -738,7 +761,12 @@ __global__ void __launch_bounds__(kWarps * 32, 2) ks_sum_kernel(KsSumArgs A, Tab
       }
       __syncwarp();
 #pragma unroll
-      for (int k = 0; k < E; ++k) mac128(sb[k], buf[sc[k]], pm);
+      for (int k = 0; k < E; ++k) {
+        if constexpr (PM1)
+          add128(sb[k], buf[sc[k]]);
+        else
+          mac128(sb[k], buf[sc[k]], pm);
+      }
       __syncwarp();
     }
     terms += A.ndig + 1;
@@ -800,7 +828,10 @@ void run_row(Context& c, const LimbBatch& b, bool inverse) {
 template <int LOGR, int LOGC>
 void run_epi(Context& c, const EpiBatch& e) {
   const unsigned grid = (unsigned)e.count * ((1u << LOGR) / kWarps);
-  ntt_row_epi<LOGR, LOGC><<<grid, kWarps * 32, 0, c.stream>>>(e, c.tabs);
+  if (e.nomul)
+    ntt_row_epi<LOGR, LOGC, true><<<grid, kWarps * 32, 0, c.stream>>>(e, c.tabs);
+  else
+    ntt_row_epi<LOGR, LOGC, false><<<grid, kWarps * 32, 0, c.stream>>>(e, c.tabs);
 }
 
 template <int LOGR, int LOGC, int TCF, int CPW>
@@ -867,12 +898,14 @@ void run_ks_sum(Context& c, const KsSumArgs& a) {
   // default: automorphism gather by warp shuffles (-2% family time vs shared-memory staging);
   // SF_VARIANT bit 3: shared-memory staging with the key loads issued first (-4% vs bit 0:
   // key words loaded after the row is staged)
-  if (c.variant & 1)
-    ks_sum_kernel<LOGR, LOGC, false, false><<<grid, kWarps * 32, 0, c.stream>>>(a, c.tabs);
+  if (a.pm_one)
+    ks_sum_kernel<LOGR, LOGC, true, true, true><<<grid, kWarps * 32, 0, c.stream>>>(a, c.tabs);
+  else if (c.variant & 1)
+    ks_sum_kernel<LOGR, LOGC, false, false, false><<<grid, kWarps * 32, 0, c.stream>>>(a, c.tabs);
   else if (c.variant & 8)
-    ks_sum_kernel<LOGR, LOGC, true, false><<<grid, kWarps * 32, 0, c.stream>>>(a, c.tabs);
+    ks_sum_kernel<LOGR, LOGC, true, false, false><<<grid, kWarps * 32, 0, c.stream>>>(a, c.tabs);
   else
-    ks_sum_kernel<LOGR, LOGC, true, true><<<grid, kWarps * 32, 0, c.stream>>>(a, c.tabs);
+    ks_sum_kernel<LOGR, LOGC, true, true, false><<<grid, kWarps * 32, 0, c.stream>>>(a, c.tabs);
 }
 
 #define SF_NTT_DISPATCH(FN, ...)                        \
