@@ -291,7 +291,9 @@ void ks_jobs(Context& c, const ExtB& x, const std::vector<KsJob>& jobs, bool mer
   std::vector<int> pidx, qidx;
   for (int k = 0; k < c.alpha; ++k) pidx.push_back(c.P_index(k));
   for (int l = 0; l < limbs; ++l) qidx.push_back(l);
-  const ConvPlan& down = conv_plan(c, pidx, qidx);
+  // fused rotations: keys with P^-1 on the Q limbs, ModDown without the final multiply
+  const bool pre = fused_path(c) && x.col_only && !merged;
+  const ConvPlan& down = conv_plan(c, pidx, qidx, pre);
   for (size_t s0 = 0; s0 < jobs.size(); s0 += kJobs) {
     const int J = (int)std::min<size_t>(kJobs, jobs.size() - s0);
     BufPtr acc = make_buf(c, (size_t)J * 2 * nt * n);
@@ -344,7 +346,7 @@ void ks_jobs(Context& c, const ExtB& x, const std::vector<KsJob>& jobs, bool mer
           for (u64 e = (u64)n - 1, b = jb.g, m2 = 2ull * n - 1; e; e >>= 1, b = (b * b) & m2)
             if (e & 1) gi = (gi * b) & m2;
         ka.ginv[k] = gi;
-        ka.key[k] = get_key(c, jb.g <= 1 ? 0 : jb.g)->p;
+        ka.key[k] = (pre ? get_key_pinv(c, jb.g <= 1 ? 0 : jb.g) : get_key(c, jb.g <= 1 ? 0 : jb.g))->p;
         ka.acc[k] = accp(j, 0);
         ka.add0[k] = jb.add0;
         ka.add1[k] = jb.add1;
@@ -433,6 +435,7 @@ void ks_jobs(Context& c, const ExtB& x, const std::vector<KsJob>& jobs, bool mer
         }
       b_fused_col(c, A);
       EpiBatch E;
+      E.nomul = pre;
       for (int j = 0; j < J; ++j) {
         const KsJob& jb = jobs[s0 + j];
         for (int poly = 0; poly < 2; ++poly) {
