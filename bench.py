@@ -380,6 +380,39 @@ def cpu_baseline_sample():
         return {"value": None, "unit": "ms/token", "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
 
 
+def hevmm_c1(sf, steps):
+    """BASELINE.json configs[0] as a throughput number: independent 768x768 BSGS
+    HE-VMMs (encrypted 1x768 activation x plaintext weight) at ring 2^15,
+    level 4, 16 inputs per captured graph, outputs per second (SURVEY.md §8(d):
+    one output ciphertext per VMM)."""
+    slots, B = 1 << 14, int(os.environ.get("SF_HEVMM_BATCH", "16"))
+    be = sf.Backend(slots, 4, alpha=2, seed=7)
+    rng = np.random.default_rng(11)
+    W = rng.normal(size=(768, 768)) / np.sqrt(768.0)
+    ly = sf.make_interleaved(1024, slots, 0)
+    plan = sf.VmmPlan(be, W, 768, 768, 4, 0, 0, True)
+    xs = []
+    for i in range(B):
+        v = np.zeros(slots)
+        v[np.arange(768) * ly.t] = rng.normal(size=768)
+        xs.append(be.encrypt(v, 4, ly, seed=100 + i))
+    run = lambda: sf.vmm_interleaved_many(be, xs, plan)  # noqa: E731  (one batched VMM over the 16 inputs)
+    run()
+    be.synchronize()
+    graph, _ = be.capture(run)
+    graph.launch()
+    be.synchronize()
+    be.event_record(0)
+    for _ in range(steps):
+        graph.launch()
+    be.event_record(1)
+    ms = be.event_elapsed_ms(0, 1) / steps
+    be.synchronize()
+    return {"value": round(B / (ms * 1e-3), 1), "unit": "ciphertexts/s", "ms_per_vmm": round(ms / B, 4),
+            "config": f"768x768 BSGS HE-VMM (BASELINE configs[0]), ring 2^15, level 4, {B} independent inputs "
+                      "batched through sf_vmm_interleaved_many per graph replay, device-resident, CUDA events"}
+
+
 def cpu_twin_sample(gpu_qkt_ms):
     """the bit-exact CPU CKKS twin (oracle/ckks_oracle.cpp,
     OpenMP over limbs and ciphertexts on every host core) on a bounded sample
@@ -639,6 +672,10 @@ def main():
         e2e_ms = float(t.item())
 
     phases = layer.phase_ms(args.steps)  # last: its graph's memory must not disturb the timed graph
+    try:
+        hevmm = hevmm_c1(sf, args.steps)
+    except Exception as e:  # pragma: no cover
+        hevmm = {"value": None, "error": str(e)}
     cpu = None if (args.no_cpu_baseline or rank != 0) else cpu_baseline_sample()
     twin = None if (args.no_cpu_baseline or rank != 0) else cpu_twin_sample(phases.get("QK^T"))
     vmm_per_step = 7
@@ -652,6 +689,7 @@ def main():
                    "parallelism": f"replicas{world}" if world > 1 else "single",
                    "l2": "working set (plaintext diagonals + keys ~30 GB) >> 126 MB L2; no flush needed"},
         "hevmm_ct_per_s": round(vmm_per_step * world / (ms_step * 1e-3), 2),
+        "hevmm_c1": hevmm,
         "roofline": roofline,
         "int_roofline": int_roofline,
         "cpu_baseline": cpu,

@@ -171,6 +171,10 @@ sf_status sf_vmm_interleaved(sf_context* ctx, const sf_ct* x, const sf_vmm_plan*
    the input-only ladder and baby steps run once, the rest as batched launches. */
 sf_status sf_vmm_interleaved_multi(sf_context* ctx, const sf_ct* x, sf_vmm_plan* const* plans, int k,
                                    int mask_output, sf_ct** outs);
+/* [vmm_interleaved(x_i, plan) for each of k independent inputs], word for word
+ * and in the ledger, every stage batched across the inputs (HE-VMM throughput) */
+sf_status sf_vmm_interleaved_many(sf_context* ctx, const sf_ct* const* xs, int k, const sf_vmm_plan* plan,
+                                  int mask_output, sf_ct** outs);
 
 /* ---- wire and on-disk formats ---------------------------------
    Weights in the reference's files (layouts.cpp:158-184: <dir>/<name>.bin =

@@ -545,6 +545,17 @@ def vmm_interleaved_multi(be: Backend, x: Ciphertext, plans, mask_output: bool =
     return [Ciphertext(be, outs[i]) for i in range(k)]
 
 
+def vmm_interleaved_many(be: Backend, xs, plan: "VmmPlan", mask_output: bool = False):
+    """[vmm_interleaved(be, x, None, plan=plan, mask_output=mask_output) for x in xs]
+    word for word and in the ledger, every stage batched across the inputs
+    (sf_vmm_interleaved_many)."""
+    k = len(xs)
+    arr = (C.c_void_p * k)(*[x.h for x in xs])
+    outs = (C.c_void_p * k)()
+    _check(_native.lib().sf_vmm_interleaved_many(be.ctx, arr, k, plan.h, int(mask_output), outs))
+    return [Ciphertext(be, outs[i]) for i in range(k)]
+
+
 def vmm_interleaved(be: Backend, x: Ciphertext, W, bsgs: bool = False, out_offset: int = 0,
                     mask_output: bool = False, plan: Optional[VmmPlan] = None) -> Ciphertext:
     """vmm_interleaved (vmm.hpp:74-75). Pass `plan` to reuse pre-encoded

@@ -43,6 +43,7 @@ SIGNATURES = {
     "sf_host_profile": (st, [C.c_char_p, C.c_int, C.c_int]),
     "sf_rotate_many": (st, [vp, vpp, C.c_int, C.c_int, vpp]),
     "sf_vmm_interleaved_multi": (st, [vp, vp, vpp, C.c_int, C.c_int, vpp]),
+    "sf_vmm_interleaved_many": (st, [vp, vpp, C.c_int, vp, C.c_int, vpp]),
     "sf_vmm_batch_plan_create": (st, [vp, dp, C.c_int, C.c_int, C.c_int, C.c_int, vpp]),
     "sf_vmm_plan_create_from_file": (st, [vp, C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, vpp]),
     "sf_vmm_plan_save": (st, [vp, vp, C.c_char_p]),

@@ -409,6 +409,15 @@ sf_status sf_vmm_interleaved_multi(sf_context* ctx, const sf_ct* x, sf_vmm_plan*
   });
 }
 
+sf_status sf_vmm_interleaved_many(sf_context* ctx, const sf_ct* const* xs, int k, const sf_vmm_plan* plan,
+                                  int mask_output, sf_ct** outs) {
+  return guard([&] {
+    std::vector<const sf::Ct*> v;
+    for (int i = 0; i < k; ++i) v.push_back(&xs[i]->v);
+    auto r = sf::vmm_interleaved_many(*ctx->c, v, *plan->p, mask_output != 0);
+    for (int i = 0; i < k; ++i) outs[i] = wrap(std::move(r[i]));
+  });
+}
 sf_status sf_vmm_multi_partial(sf_context* ctx, const sf_ct* x, sf_vmm_plan* const* plans, int k, int rank,
                                int world, sf_ct** outs) {
   return guard([&] {

@@ -259,6 +259,94 @@ Ct vmm_finish(Context& c, const Ct& acc_in, VmmPlan& plan, bool mask_output) {
   return acc;
 }
 
+// The same VMM (one plan) of several independent inputs: identical to separate
+// vmm_interleaved calls word for word and in the ledger, with every stage
+// batched across the inputs (ladders, hoisted babies, rescales, giant rotation
+// sums, reduce ladders, masks) so small rings fill the GPU (the HE-VMM
+// throughput configuration, BASELINE configs[0]).
+std::vector<Ct> vmm_interleaved_many(Context& c, const std::vector<const Ct*>& xs, VmmPlan& plan, bool mask_output) {
+  SF_HPROF("vmm_interleaved_many");
+  require(!xs.empty(), kShapeMismatch, "vmm_many: no inputs");
+  bool batched = plan.bsgs && !(plan.bg.baby > 64 || plan.bg.giant > 64 || plan.s.k > 2048 || c.n < 64);
+  for (const Ct* x : xs) {
+    vmm_check_input(c, *x, plan);
+    batched = batched && !x->zero && x->limbs == xs[0]->limbs;
+  }
+  std::vector<Ct> out;
+  if (!batched) {
+    for (const Ct* x : xs) out.push_back(vmm_interleaved(c, *x, plan, mask_output));
+    return out;
+  }
+  const int B = (int)xs.size();
+  const VmmShape& s = plan.s;
+  const std::vector<Pt>& diag = plan.diagonals(xs[0]->limbs);
+  const long long unit = (long long)s.t_in * s.t_out;
+  const int limbs = xs[0]->limbs, b = plan.bg.baby, giants = plan.bg.giant;
+  // 1. ladders (vmm.cpp:190-193)
+  std::vector<Ct> stair = fold_steps_batch(c, xs, std::vector<std::vector<int>>(B, ladder_rots(s)), true, true);
+  // 2. hoisted babies (vmm.cpp:208-209), every input's in one batch
+  std::vector<const Ct*> sp;
+  for (auto& st : stair) sp.push_back(&st);
+  std::vector<RotJob> jobs;
+  for (int i = 0; i < B; ++i)
+    for (int g1 = 1; g1 < b; ++g1) jobs.push_back({i, (int)(g1 * unit)});
+  std::vector<Ct> rots = rotate_batch(c, sp, jobs, true, true);
+  // 3. per input: the fused MAC over all giants; then one batched rescale
+  std::vector<Ct> partial((size_t)B * giants);
+  for (int i = 0; i < B; ++i) {
+    VmmMacArgs A;
+    A.n = c.n;
+    A.b = b;
+    A.giants = giants;
+    A.k = (int)s.k;
+    A.baby0[0] = stair[i].c0(), A.baby1[0] = stair[i].c1(c.n);
+    for (int g1 = 1; g1 < b; ++g1) {
+      const Ct& r = rots[(size_t)i * (b - 1) + g1 - 1];
+      A.baby0[g1] = r.c0(), A.baby1[g1] = r.c1(c.n);
+    }
+    for (long long g = 0; g < s.k; ++g) A.pt[g] = diag[g].buf->p;
+    for (int g2 = 0; g2 < giants; ++g2) {
+      const int cnt = (int)std::min<long long>(b, s.k - (long long)g2 * b);
+      c.ledger.ctpt(cnt);
+      c.ledger.add(cnt - 1);
+      Ct& pt = partial[(size_t)i * giants + g2];
+      pt = alloc_ct(c, limbs, stair[i].scale * (double)c.primes[limbs - 1]);
+      A.gidx[g2] = g2;
+      A.out0[g2] = pt.c0();
+      A.out1[g2] = pt.c1(c.n);
+    }
+    b_vmm_mac(c, A, limbs);
+  }
+  std::vector<const Ct*> pp;
+  for (auto& p : partial) pp.push_back(&p);
+  std::vector<Ct> resc = rescale_batch(c, pp);
+  for (int i = 0; i < B; ++i)
+    for (int g2 = 0; g2 < giants; ++g2) {
+      Ct& r = resc[(size_t)i * giants + g2];
+      r.scale = stair[i].scale, r.layout.reset();
+    }
+  // 4. giant alignment + sum: every input's groups in one batch
+  std::vector<std::vector<SumTerm>> groups;
+  std::vector<int> gowner;
+  for (int i = 0; i < B; ++i)
+    for (int r = 0; r < std::min(kGiantGroups, giants); ++r) {
+      groups.emplace_back();
+      gowner.push_back(i);
+      for (int g2 = r; g2 < giants; g2 += kGiantGroups)
+        groups.back().push_back({&resc[(size_t)i * giants + g2], (int)(((long long)g2 * b * unit) % c.slots)});
+    }
+  std::vector<Ct> gs = rot_sum_batch(c, groups, false);
+  std::vector<Ct> acc;
+  for (int i = 0; i < B; ++i) {
+    std::vector<const Ct*> ap;
+    for (size_t k = 0; k < gs.size(); ++k)
+      if (gowner[k] == i) ap.push_back(&gs[k]);
+    acc.push_back(sum_cts(c, ap));
+  }
+  // 5-6. reduce ladders and masks, batched (the multi-plan finish with one plan per input)
+  return vmm_multi_finish(c, acc, std::vector<VmmPlan*>(B, &plan), mask_output);
+}
+
 // Several VMMs of the SAME input x (the decode step's Q/K/V and gate/up
 // projections): identical to separate vmm_interleaved calls word for word and
 // in the ledger (each call's charges are applied), but the input-only work --

@@ -43,6 +43,7 @@ Ct vmm_interleaved(Context& c, const Ct& x, VmmPlan& plan, bool mask_output);
 std::vector<Ct> vmm_multi_partial(Context& c, const Ct& x, const std::vector<VmmPlan*>& plans, int rank, int world);
 std::vector<Ct> vmm_multi_finish(Context& c, const std::vector<Ct>& accs, const std::vector<VmmPlan*>& plans,
                                  bool mask_output);
+std::vector<Ct> vmm_interleaved_many(Context& c, const std::vector<const Ct*>& xs, VmmPlan& plan, bool mask_output);
 std::vector<Ct> vmm_interleaved_multi(Context& c, const Ct& x, const std::vector<VmmPlan*>& plans, bool mask_output);
 // sharded form: partial over the giant steps g2 = rank mod world, then (after
 // the exchange's modular sum) the reduce ladder + mask

@@ -231,3 +231,30 @@ def test_wire_formats_round_trip(tmp_path):
     other = sf.Backend(N, L + 1, alpha=2)
     with pytest.raises(sf.ShapeMismatch):
         other.deserialize(wire)
+
+
+@pytest.mark.parametrize("mask", [False, True])
+def test_vmm_many_matches_separate_calls(mask):
+    """vmm_interleaved_many (one plan, several independent inputs, every stage
+    batched) == separate vmm_interleaved calls, word for word and in the ledger."""
+    import paper_2602_11470_b200 as sf
+    N, L = 2048, 4
+    rng = np.random.default_rng(21)
+    be = sf.Backend(N, L, alpha=2)
+    W = rng.normal(size=(192, 160)) / 16
+    ly = sf.make_interleaved(256, N, 0)
+    plan = sf.VmmPlan(be, W, 192, 160, L, 0, 2, True)
+    xs = []
+    for i in range(5):
+        v = np.zeros(N)
+        v[np.arange(192) * ly.t] = rng.normal(size=192)
+        xs.append(be.encrypt(v, L, ly, seed=30 + i))
+    be.ledger.reset()
+    want = [sf.vmm_interleaved(be, x, None, plan=plan, mask_output=mask) for x in xs]
+    counts = be.ledger.totals()
+    be.ledger.reset()
+    got = sf.vmm_interleaved_many(be, xs, plan, mask_output=mask)
+    assert be.ledger.totals() == counts
+    for a, b in zip(got, want):
+        assert np.array_equal(a.data(), b.data())
+        assert a.layout == b.layout
