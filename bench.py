@@ -413,6 +413,56 @@ def hevmm_c1(sf, steps):
                       "batched through sf_vmm_interleaved_many per graph replay, device-resident, CUDA events"}
 
 
+def prefill_c4(sf, be, steps, n0=64):
+    """SURVEY.md §8(f) rank 2 measured: the batched prefill of an n0-token
+    prompt at the C4 layer shape (d 4096, 32 heads, ring 2^16) -- token-batched
+    Q/K/V VMMs, batched RoPE, causal score maps, attention -- captured into one
+    graph and replayed. The softmax between scores and attention is the
+    reference's client hook; here it returns pre-made encrypted probability
+    maps, as the decode bench does, so the timed region is homomorphic work."""
+    cfg = sf.AttentionConfig(SLOTS, D, H, n0, NP)
+    t = cfg.t
+    P = (n0 + t - 1) // t
+    lvl = 6
+    r = np.arange(D, dtype=np.float64)[:, None]
+    cidx = np.arange(D, dtype=np.float64)[None, :]
+    Wm = np.sin(0.001 * (31.0 * r + cidx) + 0.25)  # the reference bench weight (slotforge_cli.cpp:88-92)
+    plans = [sf.VmmBatchPlan(be, Wm, lvl) for _ in range(3)]
+    rng = np.random.default_rng(13)
+    xs = []
+    for p in range(P):
+        v = np.zeros(SLOTS)
+        for tau in range(min(t, n0 - p * t)):
+            v[np.arange(D) * t + tau] = rng.normal(size=D) / 8
+        xs.append(be.encrypt(v, lvl, sf.make_interleaved(D, SLOTS, 0, H), seed=900 + p))
+    made = {}
+
+    def probs_fn(be_, maps, cfg_, n0_):
+        if "p" not in made:  # first (eager) call: synthetic probabilities at each map's level
+            made["p"] = [[[be_.encrypt(np.full(SLOTS, 1.0 / n0_), m.level, m.layout) for m in row] for row in mp]
+                         for mp in maps]
+        return made["p"]
+
+    run = lambda: sf.prefill(be, xs, plans[0], plans[1], plans[2], cfg, probs_fn)  # noqa: E731
+    run()
+    be.synchronize()
+    be.ledger.reset()
+    graph, _ = be.capture(run)
+    counts = be.ledger.totals().asdict()
+    graph.launch()
+    be.synchronize()
+    be.event_record(0)
+    for _ in range(steps):
+        graph.launch()
+    be.event_record(1)
+    ms = be.event_elapsed_ms(0, 1) / steps
+    be.synchronize()
+    return {"ms_per_prompt": round(ms, 3), "ms_per_prompt_token": round(ms / n0, 3), "n0": n0,
+            "config": f"prefill of {n0} tokens at the C4 layer shape (d {D}, {H} heads, ring 2^16, level {lvl}): "
+                      "vmm_batch Q/K/V, rope_apply_batch, causal score maps, attention; one graph, CUDA events",
+            "ledger": counts}
+
+
 def cpu_twin_sample(gpu_qkt_ms):
     """the bit-exact CPU CKKS twin (oracle/ckks_oracle.cpp,
     OpenMP over limbs and ciphertexts on every host core) on a bounded sample
@@ -676,6 +726,10 @@ def main():
         hevmm = hevmm_c1(sf, args.steps)
     except Exception as e:  # pragma: no cover
         hevmm = {"value": None, "error": str(e)}
+    try:
+        prefill = prefill_c4(sf, be, args.steps)
+    except Exception as e:  # pragma: no cover
+        prefill = {"ms_per_prompt": None, "error": str(e)}
     cpu = None if (args.no_cpu_baseline or rank != 0) else cpu_baseline_sample()
     twin = None if (args.no_cpu_baseline or rank != 0) else cpu_twin_sample(phases.get("QK^T"))
     vmm_per_step = 7
@@ -690,6 +744,7 @@ def main():
                    "l2": "working set (plaintext diagonals + keys ~30 GB) >> 126 MB L2; no flush needed"},
         "hevmm_ct_per_s": round(vmm_per_step * world / (ms_step * 1e-3), 2),
         "hevmm_c1": hevmm,
+        "prefill_c4": prefill,
         "roofline": roofline,
         "int_roofline": int_roofline,
         "cpu_baseline": cpu,
