@@ -463,6 +463,48 @@ def prefill_c4(sf, be, steps, n0=64):
             "ledger": counts}
 
 
+def nonlinear_c4(sf):
+    """SURVEY.md §8(f) rank 3 measured at the C4 shape (ring 2^16): the
+    homomorphic softmax over the two score maps of n' = 2048 (32 heads), the
+    layer norm of a 4096-wide hidden vector and the SiLU of the 14336-wide gate
+    projection, with the harness's desk-shallow schedules (nonlinear.py). Wall
+    clock around synchronised calls: the client-side domain guard decrypts."""
+    from paper_2602_11470_b200 import nonlinear as NL
+    be = sf.Backend(SLOTS, 14, alpha=2, seed=17)
+    rng = np.random.default_rng(19)
+    gt = SLOTS // H
+    maps = []
+    for m in range(2):
+        v = np.zeros(SLOTS)
+        for h in range(H):
+            v[h * gt:h * gt + gt] = rng.uniform(-8, -3, size=gt)  # normaliser inside the inverse domain
+        maps.append(be.encrypt(v, 14, seed=40 + m))
+    hid = np.zeros(SLOTS)
+    lyh = sf.make_interleaved(D, SLOTS, 0, 1)
+    hid[np.arange(D) * lyh.t] = rng.normal(size=D)
+    xh = be.encrypt(hid, 14, lyh, seed=50)
+    gate = be.encrypt(rng.uniform(-8, 8, size=SLOTS), 14, sf.make_interleaved(16384, SLOTS, 0, 1), seed=51)
+    sm, nm, si = (NL.desk_spec("desk-shallow", f) for f in ("softmax", "norm", "silu"))
+    nm.iterations, nm.depth_budget = 3, 0  # the harness's approx-mode norm (harness.cpp:353-374)
+    for spec in (sm, nm, si):
+        spec.strict_domain = False
+    gamma, beta = 1 + 0.1 * rng.normal(size=D), 0.01 * rng.normal(size=D)
+    ops = {"approx_softmax (2 maps, n'=2048, 32 heads)": lambda: NL.approx_softmax(be, maps, NP, H, sm),
+           "approx_norm (d 4096)": lambda: NL.approx_norm(be, xh, gamma, beta, 1e-5, nm),
+           "approx_silu (14336-wide gate, padded 16384)": lambda: NL.approx_silu(be, gate, si)}
+    out = {}
+    for name, fn in ops.items():
+        be.ledger.reset()
+        fn()
+        be.synchronize()
+        counts = be.ledger.totals().asdict()
+        t0 = time.perf_counter()
+        fn()
+        be.synchronize()
+        out[name] = {"ms": round((time.perf_counter() - t0) * 1e3, 2), "ledger": counts}
+    return out
+
+
 def cpu_twin_sample(gpu_qkt_ms):
     """the bit-exact CPU CKKS twin (oracle/ckks_oracle.cpp,
     OpenMP over limbs and ciphertexts on every host core) on a bounded sample
@@ -730,6 +772,10 @@ def main():
         prefill = prefill_c4(sf, be, args.steps)
     except Exception as e:  # pragma: no cover
         prefill = {"ms_per_prompt": None, "error": str(e)}
+    try:
+        nonlin = nonlinear_c4(sf)
+    except Exception as e:  # pragma: no cover
+        nonlin = {"error": str(e)}
     cpu = None if (args.no_cpu_baseline or rank != 0) else cpu_baseline_sample()
     twin = None if (args.no_cpu_baseline or rank != 0) else cpu_twin_sample(phases.get("QK^T"))
     vmm_per_step = 7
@@ -745,6 +791,7 @@ def main():
         "hevmm_ct_per_s": round(vmm_per_step * world / (ms_step * 1e-3), 2),
         "hevmm_c1": hevmm,
         "prefill_c4": prefill,
+        "nonlinear_c4": nonlin,
         "roofline": roofline,
         "int_roofline": int_roofline,
         "cpu_baseline": cpu,
