@@ -133,6 +133,7 @@ struct EpiBatch {
   u64* out[kJobsWide];
   u64 g[kJobsWide];
   u64 inv[kJobsWide], inv_s[kJobsWide];
+  const u64* post[kJobsWide] = {};  // optional NTT-domain plaintext limb multiplied into the output
   uint8_t prime[kJobsWide];
   bool nomul = false;  // out = acc - v (+ addend): P^-1 already folded in (rotation sums)
 };
@@ -235,13 +236,16 @@ struct SumTerm {
   int r;
 };
 std::vector<Ct> rot_sum_batch(Context& c, const std::vector<std::vector<SumTerm>>& groups, bool hoisted,
-                              bool count = true);
+                              bool count = true, const std::vector<const Pt*>* post = nullptr);
 // doubling chains x <- x + Rot(x, r) over rots[i] (radix rotation sums); charged
 // as the reference's rotate + add steps when count && lead
+// post (fused path only): per chain an NTT-domain plaintext multiplied into the
+// result in the last ModDown's epilogue (a fused ct x pt; the caller rescales)
 std::vector<Ct> fold_steps_batch(Context& c, const std::vector<const Ct*>& xs, const std::vector<std::vector<int>>& rots,
-                                 bool count = true, bool lead = true);
+                                 bool count = true, bool lead = true, const std::vector<const Pt*>* post = nullptr);
 // fold_within_head of every x (radix rotation sums), reference ledger charge
-std::vector<Ct> fold_batch(Context& c, const std::vector<const Ct*>& xs, int d_head, int t, bool count = true);
+std::vector<Ct> fold_batch(Context& c, const std::vector<const Ct*>& xs, int d_head, int t, bool count = true,
+                           const std::vector<const Pt*>* post = nullptr);
 // sum of k same-level ciphertexts, charged k-1 additions
 Ct sum_cts(Context& c, const std::vector<const Ct*>& xs, bool count = true);
 

@@ -39,6 +39,7 @@ struct MdPoly {
   const u64* addend;
   u64 g;
   u64* out;
+  const u64* post = nullptr;  // optional NTT-domain plaintext multiplied into the result (fused ct x pt)
 };
 
 void fill_conv(ConvBatch& B, Context& c, const ConvPlan& p) {
@@ -547,6 +548,7 @@ void mod_down_polys(Context& c, int limbs, const std::vector<MdPoly>& P, bool p_
           E.g[E.count] = m.g;
           E.inv[E.count] = kh[2 * limbs + l];
           E.inv_s[E.count] = kh[3 * limbs + l];
+          E.post[E.count] = m.post ? m.post + (size_t)l * n : nullptr;
           E.prime[E.count++] = (uint8_t)l;
           if (E.count == kJobsWide) b_row_epi(c, E), E.count = 0;
         }
@@ -555,6 +557,7 @@ void mod_down_polys(Context& c, int limbs, const std::vector<MdPoly>& P, bool p_
       continue;
     }
     require(!p_rowpassed, kInternal, "mod_down_polys: row-passed input on the generic path");
+    for (const MdPoly& m : P) require(m.post == nullptr, kInternal, "mod_down_polys: post multiplier needs the fused path");
     LimbBatch lb;
     for (int j = 0; j < J; ++j)
       for (int k = 0; k < c.alpha; ++k)
@@ -587,8 +590,10 @@ void mod_down_polys(Context& c, int limbs, const std::vector<MdPoly>& P, bool p_
 // sum_i Rot(a_i, r_i) accumulated in the extended basis and
 // brought back with one ModDown per part; the same function as the CPU
 // oracle's rot_sum, charged as the reference's rotate/add chain.
-std::vector<Ct> rot_sum_batch(Context& c, const std::vector<std::vector<SumTerm>>& groups, bool hoisted, bool count) {
+std::vector<Ct> rot_sum_batch(Context& c, const std::vector<std::vector<SumTerm>>& groups, bool hoisted, bool count,
+                              const std::vector<const Pt*>* post) {
   SF_HPROF("rot_sum_batch");
+  require(!post || (post->size() == groups.size() && fused_path(c)), kInternal, "rot_sum: post multipliers");
   std::vector<Ct> out(groups.size());
   std::map<int, std::vector<int>> by_limbs;
   for (size_t gi = 0; gi < groups.size(); ++gi) {
@@ -690,8 +695,9 @@ std::vector<Ct> rot_sum_batch(Context& c, const std::vector<std::vector<SumTerm>
           ++jb;
         }
         const Ct& y = out[chunk[o]];
-        md.push_back({A.acc[o], nullptr, 0, y.c0()});
-        md.push_back({A.acc[o] + (size_t)nt * n, nullptr, 0, y.c1(c.n)});
+        const u64* pp = post ? (*post)[chunk[o]]->buf->p : nullptr;
+        md.push_back({A.acc[o], nullptr, 0, y.c0(), pp});
+        md.push_back({A.acc[o] + (size_t)nt * n, nullptr, 0, y.c1(c.n), pp});
       }
       A.out_begin[chunk.size()] = jb;
       A.nout = (int)chunk.size();
@@ -709,8 +715,9 @@ std::vector<Ct> rot_sum_batch(Context& c, const std::vector<std::vector<SumTerm>
 // of DESIGN.md §3.8 (m <= 3 bits in one sum, else ceil(m/2) then floor(m/2));
 // charged as the reference's m rotate + add steps per ciphertext.
 std::vector<Ct> fold_steps_batch(Context& c, const std::vector<const Ct*>& xs, const std::vector<std::vector<int>>& rots,
-                                 bool count, bool lead) {
+                                 bool count, bool lead, const std::vector<const Pt*>* post) {
   SF_HPROF("fold_steps_batch");
+  std::vector<bool> posted(xs.size(), false);
   require(xs.size() == rots.size(), kShapeMismatch, "fold_steps: operand count");
   std::vector<Ct> cur;
   size_t mmax = 0;
@@ -735,7 +742,8 @@ std::vector<Ct> fold_steps_batch(Context& c, const std::vector<const Ct*>& xs, c
     else
       steps.push_back((m + 1) / 2), steps.push_back(m / 2);
     int lo = 0;
-    for (int bits : steps) {
+    for (size_t si = 0; si < steps.size(); ++si) {
+      const int bits = steps[si];
       std::vector<std::vector<SumTerm>> groups(idx.size());
       for (size_t g = 0; g < idx.size(); ++g) {
         const std::vector<int>& rs = rots[idx[g]];
@@ -746,7 +754,11 @@ std::vector<Ct> fold_steps_batch(Context& c, const std::vector<const Ct*>& xs, c
           groups[g].push_back({&cur[idx[g]], (int)pos_mod(r, c.slots)});
         }
       }
-      std::vector<Ct> nxt = rot_sum_batch(c, groups, false, false);
+      std::vector<const Pt*> pg;  // the post multipliers ride the last step's ModDown epilogue
+      const bool last = si + 1 == steps.size();
+      if (post && last)
+        for (int g : idx) pg.push_back((*post)[g]), posted[g] = true;
+      std::vector<Ct> nxt = rot_sum_batch(c, groups, false, false, (post && last) ? &pg : nullptr);
       for (size_t g = 0; g < idx.size(); ++g) cur[idx[g]] = std::move(nxt[g]);
       lo += bits;
     }
@@ -755,14 +767,16 @@ std::vector<Ct> fold_steps_batch(Context& c, const std::vector<const Ct*>& xs, c
     bool all0 = true;
     for (int r : rots[i]) all0 = all0 && pos_mod(r, c.slots) == 0;
     cur[i].layout = all0 ? xs[i]->layout : OptLayout();
+    require(!post || posted[i], kInternal, "fold_steps: post multiplier on an empty chain");
   }
   return cur;
 }
 
-std::vector<Ct> fold_batch(Context& c, const std::vector<const Ct*>& xs, int d_head, int t, bool count) {
+std::vector<Ct> fold_batch(Context& c, const std::vector<const Ct*>& xs, int d_head, int t, bool count,
+                           const std::vector<const Pt*>* post) {
   std::vector<int> rs;
   for (int l = 0; (1 << l) < d_head; ++l) rs.push_back((1 << l) * t);
-  return fold_steps_batch(c, xs, std::vector<std::vector<int>>(xs.size(), rs), count, true);
+  return fold_steps_batch(c, xs, std::vector<std::vector<int>>(xs.size(), rs), count, true, post);
 }
 
 // -------------------------------------------------------------------- rescale

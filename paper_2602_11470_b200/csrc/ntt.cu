@@ -108,6 +108,7 @@ __global__ void __launch_bounds__(kWarps * 32) ntt_row_epi(EpiBatch B, Tabs T) {
   warp_fwd<LOGC, kBlocked>(x, sm, lane, q, tw);
   const u64* acc = B.acc[entry];
   const u64* addend = B.addend[entry];
+  const u64* post = B.post[entry];
   const u64 g = B.g[entry], inv = B.inv[entry], inv_s = B.inv_s[entry];
   u64* out = B.out[entry];
   const int base = row * C + lane * E;  // blocked: this lane owns E consecutive outputs
@@ -129,6 +130,11 @@ __global__ void __launch_bounds__(kWarps * 32) ntt_row_epi(EpiBatch B, Tabs T) {
         v0 = add_mod(v0, dv.x, q);
         v1 = add_mod(v1, dv.y, q);
       }
+    }
+    if (post) {  // fused ct x pt (the plaintext product mul_plain_batch would apply next)
+      const ulonglong2 pv = *reinterpret_cast<const ulonglong2*>(post + base + k);
+      v0 = mulmod(v0, pv.x, q, T.mh[p], T.ml[p]);
+      v1 = mulmod(v1, pv.y, q, T.mh[p], T.ml[p]);
     }
     *reinterpret_cast<ulonglong2*>(out + base + k) = make_ulonglong2(v0, v1);
   }

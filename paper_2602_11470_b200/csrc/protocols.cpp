@@ -730,17 +730,41 @@ std::vector<Ct> qk_dot_partial(Context& c, const Ct& q, const KV& cache, int ran
   std::vector<Ct> prod0 = mul_batch(c, qs, ks);
   std::vector<const Ct*> pp0;
   for (auto& p : prod0) pp0.push_back(&p);
-  std::vector<Ct> prod = fold_batch(c, pp0, dh, t);  // fold_within_head (38-41), DESIGN.md §3.8
   const std::string hkey = "headmask:" + std::to_string(cfg.H) + ":" + std::to_string(t);
-  std::vector<const Ct*> pp;
-  std::vector<Pt> hm;
-  for (int i = 0; i < J; ++i) {
-    require(prod[i].level() > 0, kLevelUnderflow, "mul_plain: no multiplicative level left");
-    hm.push_back(cached_pt(c, hkey, head_mask.data(), (double)c.primes[prod[i].limbs - 1], prod[i].limbs));
+  std::vector<Ct> masked;
+  bool fused_mask = fused_path(c);
+  for (int i = 0; i < J; ++i) fused_mask = fused_mask && !prod0[i].zero && prod0[i].limbs == prod0[0].limbs;
+  if (fused_mask) {
+    // fold_within_head (38-41) with the ReplicateExtract mask (layouts.cpp:134-138)
+    // multiplied in the fold's last ModDown epilogue, then one batched rescale:
+    // the same words as fold -> mul_plain
+    const int lb = prod0[0].limbs;
+    require(lb - 1 > 0, kLevelUnderflow, "mul_plain: no multiplicative level left");
+    const Pt hm = cached_pt(c, hkey, head_mask.data(), (double)c.primes[lb - 1], lb);
+    std::vector<const Pt*> post(J, &hm);
+    std::vector<Ct> prod = fold_batch(c, pp0, dh, t, true, &post);
+    std::vector<const Ct*> pp;
+    std::vector<double> s0(J);
+    for (int i = 0; i < J; ++i) {
+      c.ledger.ctpt();
+      s0[i] = prod[i].scale;
+      prod[i].scale *= (double)c.primes[lb - 1];  // the product's scale before its rescale
+      pp.push_back(&prod[i]);
+    }
+    masked = rescale_batch(c, pp);
+    for (int i = 0; i < J; ++i) masked[i].scale = s0[i], masked[i].layout.reset();
+  } else {
+    std::vector<Ct> prod = fold_batch(c, pp0, dh, t);  // fold_within_head (38-41), DESIGN.md §3.8
+    std::vector<const Ct*> pp;
+    std::vector<Pt> hm;
+    for (int i = 0; i < J; ++i) {
+      require(prod[i].level() > 0, kLevelUnderflow, "mul_plain: no multiplicative level left");
+      hm.push_back(cached_pt(c, hkey, head_mask.data(), (double)c.primes[prod[i].limbs - 1], prod[i].limbs));
+    }
+    std::vector<const Pt*> hp;
+    for (int i = 0; i < J; ++i) pp.push_back(&prod[i]), hp.push_back(&hm[i]);
+    masked = mul_plain_batch(c, pp, hp);
   }
-  std::vector<const Pt*> hp;
-  for (int i = 0; i < J; ++i) pp.push_back(&prod[i]), hp.push_back(&hm[i]);
-  std::vector<Ct> masked = mul_plain_batch(c, pp, hp);
   // pack + accumulate (kv_attention.cpp:202-206): one rotation sum per (map,
   // key-ct group j mod kPackGroups), then the groups' sum
   std::vector<std::vector<SumTerm>> groups;
