@@ -166,6 +166,13 @@ struct Context {
   int rank = 0, world = 1;
   std::map<std::string, std::vector<u64>> comm_hdr, comm_meta;
   void* p2p = nullptr;  // peer-memory exchange state (p2p.cu)
+  // exact-size free lists of device buffers (eager path only): every kernel runs
+  // on `stream`, so a buffer released after its last use was enqueued can back
+  // the next same-size allocation (stream order); saves the per-op
+  // cudaMallocAsync / cudaFreeAsync host cost
+  std::mutex alloc_mu;
+  std::unordered_map<size_t, std::vector<u64*>> free_bufs;
+  size_t cached_words = 0, cache_cap_words = (size_t)1 << 30;  // 8 GiB
   std::vector<std::pair<u64*, size_t>> capture_deferred;
   long long graph_launch_base = 0;
   bool ks_row = true;  // fused key-switch row stage

@@ -25,8 +25,19 @@ void build_host_tables(Context& c, std::vector<u64>& psi, std::vector<u64>& psi_
 // ------------------------------------------------------------------ memory
 Buf::Buf(Context* c, size_t w) : words(w), ctx(c) {
   SF_HPROF("cudaMallocAsync");
-  if (w) SF_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), w * sizeof(u64), c->stream));
   graph_owned = c->capturing;
+  if (!w) return;
+  if (!c->capturing) {  // eager: reuse a released buffer of the same size (stream-ordered)
+    std::lock_guard<std::mutex> lk(c->alloc_mu);
+    auto it = c->free_bufs.find(w);
+    if (it != c->free_bufs.end() && !it->second.empty()) {
+      p = it->second.back();
+      it->second.pop_back();
+      c->cached_words -= w;
+      return;
+    }
+  }
+  SF_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), w * sizeof(u64), c->stream));
 }
 Buf::~Buf() {
   SF_HPROF("cudaFreeAsync");
@@ -39,6 +50,14 @@ Buf::~Buf() {
     return;
   }
   if (graph_owned) return;  // lives in the graph's memory (freed with the graph)
+  {
+    std::lock_guard<std::mutex> lk(ctx->alloc_mu);
+    if (ctx->cached_words + words <= ctx->cache_cap_words) {
+      ctx->free_bufs[words].push_back(p);
+      ctx->cached_words += words;
+      return;
+    }
+  }
   cudaFreeAsync(p, ctx->stream);
 }
 
@@ -57,6 +76,9 @@ Context::~Context() {
   sk.reset();
   tab_store.reset();
   for (auto e : events) cudaEventDestroy(e);
+  for (auto& [w, v] : free_bufs)
+    for (u64* q : v) cudaFreeAsync(q, stream);
+  free_bufs.clear();
   if (stream) {
     cudaStreamSynchronize(stream);
     cudaStreamDestroy(stream);
