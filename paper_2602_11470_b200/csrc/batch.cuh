@@ -113,11 +113,14 @@ struct FusedColArgs {
     ymul = tab + base2;
     ymul_s = tab + base2 + nsrc;
     qhat_s = tab + base2 + 2 * nsrc;
+    ymulw = tab + 2 * base2;
+    ymulw_s = tab + 2 * base2 + nsrc;
   }
   int count = 0, ns = 0, nd = 0, mode = 0;
   int src_prime[kMaxPrimes], dst_prime[kMaxPrimes], out_slot[kMaxPrimes];
   // mode 0 (ConvPlan tables): y_s = x_s * (n^-1 qhat_s^-1) (Shoup), out_d = sum_s y_s * qhat[s][d] (Shoup)
   const u64 *ymul = nullptr, *ymul_s = nullptr, *qhat = nullptr, *qhat_s = nullptr;
+  const u64 *ymulw = nullptr, *ymulw_s = nullptr;  // ymul * ipsi[1]: folded into the last inverse stage
   u64 q_last = 0;  // mode 1
   const u64* src[kJobsWide];
   u64* dst[kJobsWide];

@@ -114,6 +114,7 @@ struct Tabs {
   const u64 *psi, *psi_s;          // [np][n] psi^{br(k)} (+ Shoup)
   const u64 *ipsi, *ipsi_s;        // [np][n] psi^{-br(k)} (+ Shoup)
   const u64 *ninv, *ninv_s;        // [np]
+  const u64 *ninvw, *ninvw_s;      // [np] n^-1 * ipsi[1]: the last inverse column stage's twiddle with n^-1 folded in
   int n, logn;
 };
 
@@ -179,6 +180,7 @@ struct Context {
   int variant = 0;     // SF_VARIANT bit mask: kernel variants under A/B evaluation
   int fused_cpw = 1;   // columns per warp in batched fused column stages (SF_FUSED_CPW=1|2, for A/B timing) (SF_KS_ROW=0: separate passes, for A/B timing)
   std::vector<u64> primes;  // q0..qL, p0..p_{alpha-1}
+  std::vector<u64> ipsi1_h;  // per prime: ipsi table index 1 (the last inverse column stage's twiddle)
   cudaStream_t stream = nullptr;
   cudaMemPool_t pool = nullptr;
 

@@ -123,7 +123,14 @@ std::unique_ptr<Context> make_context(int slots, int L, int log_n, int alpha, in
   std::vector<u64> psi, psi_s, ipsi, ipsi_s, ninv, ninv_s;
   build_host_tables(*c, psi, psi_s, ipsi, ipsi_s, ninv, ninv_s);
   const size_t np = c->np, n = c->n;
-  const size_t words = 3 * np + 4 * np * n + 2 * np;
+  c->ipsi1_h.resize(np);
+  std::vector<u64> ninvw(np), ninvw_s(np);
+  for (size_t p = 0; p < np; ++p) {
+    c->ipsi1_h[p] = ipsi[p * n + 1];
+    ninvw[p] = mulmod_h(ninv[p], c->ipsi1_h[p], c->primes[p]);
+    ninvw_s[p] = shoup_h(ninvw[p], c->primes[p]);
+  }
+  const size_t words = 3 * np + 4 * np * n + 4 * np;
   c->tab_store = buf(*c, words);
   std::vector<u64> host(words);
   u64* h = host.data();
@@ -143,6 +150,8 @@ std::unique_ptr<Context> make_context(int slots, int L, int log_n, int alpha, in
   c->tabs.ipsi_s = put(ipsi_s);
   c->tabs.ninv = put(ninv);
   c->tabs.ninv_s = put(ninv_s);
+  c->tabs.ninvw = put(ninvw);
+  c->tabs.ninvw_s = put(ninvw_s);
   c->tabs.n = c->n;
   c->tabs.logn = c->logn;
   SF_CUDA(cudaMemcpyAsync(c->tab_store->p, host.data(), words * sizeof(u64), cudaMemcpyHostToDevice, c->stream));
@@ -243,7 +252,8 @@ const ConvPlan& conv_plan(Context& c, const std::vector<int>& src, const std::ve
   // [nsrc] qhat^-1, [nsrc] Shoup, [nsrc][ndst] qhat mod dst,
   // then for the fused column stage: [nsrc] n^-1 qhat^-1, [nsrc] Shoup, [nsrc][ndst] Shoup of qhat mod dst
   const size_t base2 = 2 * (size_t)p.nsrc + (size_t)p.nsrc * p.ndst;
-  std::vector<u64> h(2 * base2);
+  // + [nsrc] y-factor times the last inverse column stage's twiddle (ipsi[1]), [nsrc] Shoup
+  std::vector<u64> h(2 * base2 + 2 * (size_t)p.nsrc);
   for (int i = 0; i < p.nsrc; ++i) {
     const u64 qi = c.primes[src[i]];
     u64 hat = 1 % qi;
@@ -263,6 +273,8 @@ const ConvPlan& conv_plan(Context& c, const std::vector<int>& src, const std::ve
     const u64 ni = invmod_h((u64)c.n % qi, qi);
     h[base2 + i] = mulmod_h(ni, h[i], qi);
     h[base2 + p.nsrc + i] = shoup_h(h[base2 + i], qi);
+    h[2 * base2 + i] = mulmod_h(h[base2 + i], c.ipsi1_h[src[i]], qi);
+    h[2 * base2 + p.nsrc + i] = shoup_h(h[2 * base2 + i], qi);
   }
   p.tab = buf(c, h.size());
   SF_CUDA(cudaMemcpyAsync(p.tab->p, h.data(), h.size() * sizeof(u64), cudaMemcpyHostToDevice, c.stream));

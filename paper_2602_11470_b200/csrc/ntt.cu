@@ -255,13 +255,15 @@ __global__ void __launch_bounds__(TCF / CPW * 32, TCF / CPW == 8 ? (CPW == 1 ? 3
       for (int k = 0; k < E; ++k) x[c][k] = sm[c][swz(lane + 32 * k)];
     }
     __syncwarp();
-    warp_inv_n<LOGR, CPW>(x, sm, lane, q, tw);
-    // canonical y_s: the basis conversion's [x q^_s^-1]_{q_s} (and the centred lift) need it
+    // canonical y_s: the basis conversion's [x q^_s^-1]_{q_s} (and the centred lift) need it;
+    // the factor rides the last inverse stage (its twiddle is ipsi[1] for every butterfly)
     const u64 ym = A.mode == 0 ? A.ymul[s] : T.ninv[p], yms = A.mode == 0 ? A.ymul_s[s] : T.ninv_s[p];
+    const u64 ymw = A.mode == 0 ? A.ymulw[s] : T.ninvw[p], ymws = A.mode == 0 ? A.ymulw_s[s] : T.ninvw_s[p];
+    warp_inv_n<LOGR, CPW, decltype(tw), true>(x, sm, lane, q, tw, ym, yms, ymw, ymws);
 #pragma unroll
     for (int c = 0; c < CPW; ++c)
 #pragma unroll
-      for (int k = 0; k < E; ++k) sm[c][swz(lane + 32 * k)] = mul_shoup(x[c][k], ym, yms, q);
+      for (int k = 0; k < E; ++k) sm[c][swz(lane + 32 * k)] = x[c][k];
     __syncwarp();
   }
   __syncthreads();

@@ -157,9 +157,12 @@ __device__ __forceinline__ void warp_fwd_n(u64 (&x)[NC][1 << (LOGM - 5)], u64* c
   relayout_n<LOGE, NC>(x, sm, lane, s0, LOGM - LOGE);
 }
 
-template <int LOGM, int NC, class TW>
+// FS: the last stage also applies a constant factor f to every output (the
+// caller's post-transform scale, e.g. n^-1 times a conversion factor): the
+// sum gets f, the difference f * w (fw precomputed); outputs canonical
+template <int LOGM, int NC, class TW, bool FS = false>
 __device__ __forceinline__ void warp_inv_n(u64 (&x)[NC][1 << (LOGM - 5)], u64* const (&sm)[NC], int lane, u64 q,
-                                           const TW& tw) {
+                                           const TW& tw, u64 f = 0, u64 fs = 0, u64 fw = 0, u64 fws = 0) {
   constexpr int LOGE = LOGM - 5;
   constexpr int E = 1 << LOGE;
   const u64 q2 = 2 * q;
@@ -183,8 +186,13 @@ __device__ __forceinline__ void warp_inv_n(u64 (&x)[NC][1 << (LOGM - 5)], u64* c
         for (int c = 0; c < NC; ++c) {
           const u64 U = x[c][k], V = x[c][k | (1 << rb)];
           const u64 S = U + V;
-          x[c][k] = S >= q2 ? S - q2 : S;
-          x[c][k | (1 << rb)] = mul_shoup_lazy(U - V + q2, w, ws, q);
+          if (FS && b == LOGM - 1) {
+            x[c][k] = mul_shoup(S, f, fs, q);
+            x[c][k | (1 << rb)] = mul_shoup(U - V + q2, fw, fws, q);
+          } else {
+            x[c][k] = S >= q2 ? S - q2 : S;
+            x[c][k | (1 << rb)] = mul_shoup_lazy(U - V + q2, w, ws, q);
+          }
         }
       }
     }
