@@ -258,3 +258,28 @@ def test_vmm_many_matches_separate_calls(mask):
     for a, b in zip(got, want):
         assert np.array_equal(a.data(), b.data())
         assert a.layout == b.layout
+
+
+def test_vmm_many_fallback_paths():
+    """vmm_interleaved_many with a non-BSGS plan, and with a trivial-zero input
+    among the inputs, takes the per-input path and still equals separate calls."""
+    import paper_2602_11470_b200 as sf
+    N, L = 2048, 4
+    rng = np.random.default_rng(23)
+    be = sf.Backend(N, L, alpha=2)
+    W = rng.normal(size=(64, 96)) / 8
+    ly = sf.make_interleaved(64, N, 0)
+    plan = sf.VmmPlan(be, W, 64, 96, L, 0, 1, False)
+    xs = []
+    for i in range(3):
+        v = np.zeros(N)
+        v[np.arange(64) * ly.t] = rng.normal(size=64)
+        xs.append(be.encrypt(v, L, ly, seed=60 + i))
+    want = [sf.vmm_interleaved(be, x, None, plan=plan) for x in xs]
+    got = sf.vmm_interleaved_many(be, xs, plan)
+    for a, b in zip(got, want):
+        assert np.array_equal(a.data(), b.data())
+    bplan = sf.VmmPlan(be, W, 64, 96, L, 0, 1, True)
+    z = be.with_layout(be.zeros(L), ly)
+    got = sf.vmm_interleaved_many(be, [xs[0], z], bplan)
+    assert np.array_equal(got[0].data(), sf.vmm_interleaved(be, xs[0], None, plan=bplan).data())
