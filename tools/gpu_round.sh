@@ -22,7 +22,7 @@ if [[ $WHAT == all || $WHAT == *ncu* ]]; then
   timeout 900 ncu --nvtx --nvtx-include "sf_step/" --metrics gpu__time_duration.sum --clock-control none \
       --csv --log-file $OUT/launches.csv python bench.py --nvtx-step --warmup 3 --no-cpu-baseline > $OUT/ncu_launch.log 2>&1
   echo "launch list rc=$?"
-  for K in ${NCU_KERNELS:-ntt_row_pass ntt_col_pass ks_batch_kernel vmm_mac_kernel fused_col_kernel ntt_row_epi}; do
+  for K in ${NCU_KERNELS:-fused_col_kernel ks_sum_kernel ks_row_kernel ntt_row_epi vmm_mac_kernel}; do
     timeout 900 ncu --nvtx --nvtx-include "sf_step/" --set full --clock-control none --import-source on \
         -k regex:$K -c 2 -o $OUT/full_$K python bench.py --nvtx-step --warmup 3 --no-cpu-baseline > $OUT/ncu_$K.log 2>&1
     echo "ncu $K rc=$?"
