@@ -58,7 +58,8 @@ typedef struct {
 /* engine.hpp:19-22 (EngineParams{N, L}) extended with the CKKS parameters the
  * reference leaves "unhoused by design". slots = the reference N.
  * log_n = ring degree exponent (0: 2*slots). alpha = special primes per digit
- * (0: min(L+1, 5)). Bits of q0 / scale primes / special primes (0: 60/40/60). */
+ * (0: min(L+1, 5)). Bits of q0 / scale primes / special primes (0: 60/40/60),
+ * each in [20, 60] (the lazy kernels need q < 2^60; SF_ERR_DOMAIN otherwise). */
 typedef struct {
   int slots;
   int L;
@@ -336,6 +337,11 @@ void sf_graph_destroy(sf_graph* g);
 /* Overwrite a ciphertext's words from host memory (stream-ordered; pinned host
    memory makes it asynchronous): the input slots of a captured graph. */
 sf_status sf_ct_refill(sf_context* ctx, sf_ct* ct, const uint64_t* words);
+
+/* Device memory in use (diagnostics): bytes currently allocated by CUDA-graph
+   memory nodes on the context's device (outstanding step outputs of live
+   graphs) and by the context's stream-ordered pool (live buffers + free lists). */
+sf_status sf_mem_stats(sf_context* ctx, size_t* graph_bytes, size_t* pool_bytes);
 
 /* Host-side wall time per internal scope ("name total_us calls" lines), collected
    when SF_HOST_PROF=1 is set in the environment; diagnostics only. */

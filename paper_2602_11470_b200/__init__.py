@@ -294,16 +294,38 @@ class Backend:
         """Capture everything fn(*args, **kw) enqueues into one CUDA graph
         (nothing runs during the capture). Returns (graph, fn's result): the
         result's ciphertexts hold the latest replay's values; inputs created
-        before the capture are fed with refill() between replays."""
+        before the capture are fed with refill() between replays.
+
+        Lazily built tables / keys / cached plaintexts need one host upload on
+        first use, which a capture cannot contain: if fn hits one, the partial
+        capture is discarded, fn runs once eagerly (warming every cache) and
+        the capture is retried once."""
         lib = _native.lib()
-        _check(lib.sf_graph_capture_begin(self.ctx))
-        try:
-            res = fn(*args, **kw)
-        finally:
+        for attempt in range(2):
+            _check(lib.sf_graph_capture_begin(self.ctx))
+            err = None
+            try:
+                res = fn(*args, **kw)
+            except Exception as e:  # noqa: BLE001 - the capture must be ended whatever fn raised
+                err = e
             g = C.c_void_p()
             st = lib.sf_graph_capture_end(self.ctx, C.byref(g))
-        _check(st)
-        return StepGraph(self, g.value), res
+            if err is None:
+                _check(st)
+                return StepGraph(self, g.value), res
+            if g.value:
+                lib.sf_graph_destroy(g)
+            if attempt == 0 and isinstance(err, InvalidTarget) and "eagerly" in str(err):
+                fn(*args, **kw)  # warm-up run, then capture again
+                self.synchronize()
+                continue
+            raise err
+
+    def mem_stats(self):
+        """(graph-node bytes, pool bytes) currently allocated (sf_mem_stats)."""
+        g, p = C.c_size_t(), C.c_size_t()
+        _check(_native.lib().sf_mem_stats(self.ctx, C.byref(g), C.byref(p)))
+        return g.value, p.value
 
     def rotate_many(self, cts, r: int):
         """Rot(c, r) for every c, one batched key-switching pass (sf_rotate_many)."""

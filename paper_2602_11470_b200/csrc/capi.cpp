@@ -26,6 +26,7 @@ struct sf_graph {
   cudaGraphExec_t x = nullptr;
   long long launches = 0;  // library kernels per replay
   std::vector<std::pair<sf::u64*, size_t>> deferred;
+  std::shared_ptr<sf::GraphMem> gm;
 };
 struct sf_kvcache {
   std::atomic<int> rc{1};
@@ -860,6 +861,7 @@ sf_status sf_graph_capture_begin(sf_context* ctx) {
     sf::require(!c.capturing, sf::kInvalidTarget, "graph capture already in progress");
     SF_CUDA(cudaStreamSynchronize(c.stream));
     c.capture_deferred.clear();
+    c.capture_gm = std::make_shared<sf::GraphMem>();
     c.capturing = true;
     c.graph_launch_base = c.launches.load();
     const cudaError_t e = cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal);
@@ -877,9 +879,24 @@ sf_status sf_graph_capture_end(sf_context* ctx, sf_graph** out) {
     const cudaError_t e = cudaStreamEndCapture(c.stream, &g->g);
     c.capturing = false;
     g->deferred.swap(c.capture_deferred);
+    g->gm = std::move(c.capture_gm);
     g->launches = c.launches.load() - c.graph_launch_base;
+    cudaError_t ie = e;
+    if (e == cudaSuccess) ie = cudaGraphInstantiateWithFlags(&g->x, g->g, cudaGraphInstantiateFlagAutoFreeOnLaunch);
+    if (ie != cudaSuccess) {  // failed capture: nothing will replay; release what it deferred
+      cudaGetLastError();
+      if (g->g) cudaGraphDestroy(g->g);
+      g->g = nullptr;
+      {
+        std::lock_guard<std::mutex> lk(g->gm->mu);
+        g->gm->destroyed = true;  // never launched: its Bufs own nothing outstanding
+        g->gm->dead.clear();
+      }
+      for (auto& d : g->deferred) cudaFreeAsync(d.first, c.stream);
+      g->deferred.clear();
+    }
     SF_CUDA(e);
-    SF_CUDA(cudaGraphInstantiateWithFlags(&g->x, g->g, cudaGraphInstantiateFlagAutoFreeOnLaunch));
+    SF_CUDA(ie);
     *out = g.release();
   });
 }
@@ -889,6 +906,7 @@ sf_status sf_graph_launch(sf_context* ctx, sf_graph* g) {
     auto& c = *ctx->c;
     sf::require(g && g->ctx == ctx, sf::kInvalidTarget, "graph belongs to another context");
     SF_CUDA(cudaGraphLaunch(g->x, c.stream));
+    { std::lock_guard<std::mutex> lk(g->gm->mu); g->gm->launched = true; }
     c.launches.fetch_add(g->launches);
   });
 }
@@ -902,6 +920,13 @@ void sf_graph_destroy(sf_graph* g) {
   if (g->x) cudaGraphExecDestroy(g->x);
   if (g->g) cudaGraphDestroy(g->g);
   for (auto& d : g->deferred) cudaFreeAsync(d.first, c.stream);
+  {
+    std::lock_guard<std::mutex> lk(g->gm->mu);
+    g->gm->destroyed = true;
+    if (g->gm->launched)
+      for (sf::u64* p : g->gm->dead) cudaFreeAsync(p, c.stream);  // outstanding allocations of dead Bufs
+    g->gm->dead.clear();
+  }
   cudaStreamSynchronize(c.stream);
   delete g;
 }
@@ -914,6 +939,18 @@ sf_status sf_ct_refill(sf_context* ctx, sf_ct* ct, const uint64_t* words) {
     const size_t w = (size_t)v.limbs * c.n;
     SF_CUDA(cudaMemcpyAsync(v.c0(), words, w * 8, cudaMemcpyHostToDevice, c.stream));
     SF_CUDA(cudaMemcpyAsync(v.c1(c.n), words + w, w * 8, cudaMemcpyHostToDevice, c.stream));
+  });
+}
+
+sf_status sf_mem_stats(sf_context* ctx, size_t* graph_bytes, size_t* pool_bytes) {
+  return guard([&] {
+    auto& c = *ctx->c;
+    unsigned long long g = 0, p = 0;
+    SF_CUDA(cudaStreamSynchronize(c.stream));
+    SF_CUDA(cudaDeviceGetGraphMemAttribute(c.device, cudaGraphMemAttrUsedMemCurrent, &g));
+    SF_CUDA(cudaMemPoolGetAttribute(c.pool, cudaMemPoolAttrUsedMemCurrent, &p));
+    if (graph_bytes) *graph_bytes = (size_t)g;
+    if (pool_bytes) *pool_bytes = (size_t)p;
   });
 }
 

@@ -24,11 +24,21 @@ void cuda_check(cudaError_t e, const char* what);
 
 // Stream-ordered device allocation (cudaMallocAsync pool; frees are enqueued on
 // the context stream so in-flight kernels that still read a buffer are safe).
+// Allocations a captured graph owns (graph memory nodes). A graph instantiated
+// with AutoFreeOnLaunch frees and re-allocates them on every replay; those still
+// outstanding when the graph is destroyed are freed then (if their Buf already
+// died) or when their Buf dies (sf_graph_destroy / ~Buf).
+struct GraphMem {
+  std::mutex mu;
+  bool destroyed = false;
+  bool launched = false;
+  std::vector<u64*> dead;  // Bufs gone while the graph lives: free at destroy
+};
 struct Buf {
   u64* p = nullptr;
   size_t words = 0;
   Context* ctx = nullptr;
-  bool graph_owned = false;  // allocated while capturing a CUDA graph (a graph memory node)
+  std::shared_ptr<GraphMem> gm;  // set: allocated while capturing that graph (a graph memory node)
   Buf(Context* c, size_t w);
   ~Buf();
   Buf(const Buf&) = delete;
@@ -162,6 +172,7 @@ struct Context {
   // capturing become graph memory nodes; frees of older buffers are deferred
   // to graph destruction (a replay still reads them).
   bool capturing = false;
+  std::shared_ptr<GraphMem> capture_gm;  // the graph being captured
   // sharded ops (comm.cpp): NCCL communicator on this context's stream
   void* comm = nullptr;
   int rank = 0, world = 1;
@@ -271,5 +282,15 @@ const BufPtr& get_key(Context& c, u64 g);
 const BufPtr& get_key_pinv(Context& c, u64 g);  // Q limbs times P^-1 (rotation sums)
 void check_ct(const Context& c, const Ct& a, const char* what);
 void check_scales(const Ct& a, const Ct& b, const char* what);
+
+// Host synchronisation of the lazy builders (constant tables, keys, cached
+// plaintexts uploaded from pageable memory on first use). Not allowed inside a
+// graph capture: the caller must run the step once eagerly first.
+inline void host_sync(Context& c) {
+  require(!c.capturing, kInvalidTarget,
+          "graph capture: a lazily built table / key / plaintext is not warm yet; run the step once eagerly "
+          "before capturing it");
+  SF_CUDA(cudaStreamSynchronize(c.stream));
+}
 
 }  // namespace sf

@@ -25,7 +25,7 @@ void build_host_tables(Context& c, std::vector<u64>& psi, std::vector<u64>& psi_
 // ------------------------------------------------------------------ memory
 Buf::Buf(Context* c, size_t w) : words(w), ctx(c) {
   SF_HPROF("cudaMallocAsync");
-  graph_owned = c->capturing;
+  if (c->capturing) gm = c->capture_gm;
   if (!w) return;
   if (!c->capturing) {  // eager: reuse a released buffer of the same size (stream-ordered)
     std::lock_guard<std::mutex> lk(c->alloc_mu);
@@ -42,14 +42,23 @@ Buf::Buf(Context* c, size_t w) : words(w), ctx(c) {
 Buf::~Buf() {
   SF_HPROF("cudaFreeAsync");
   if (!p) return;
-  if (ctx->capturing) {
-    if (graph_owned)
-      cudaFreeAsync(p, ctx->stream);  // captured free node
-    else
-      ctx->capture_deferred.push_back({p, words});  // a replay still reads it
+  if (gm) {  // a graph memory node
+    if (ctx->capturing && ctx->capture_gm == gm) {
+      cudaFreeAsync(p, ctx->stream);  // allocated and freed inside the same capture: a free node
+      return;
+    }
+    std::lock_guard<std::mutex> lk(gm->mu);
+    if (!gm->destroyed) {
+      gm->dead.push_back(p);  // the graph still re-allocates it on replay; freed at sf_graph_destroy
+    } else if (gm->launched) {
+      cudaFreeAsync(p, ctx->stream);  // outstanding allocation of a destroyed graph
+    }
     return;
   }
-  if (graph_owned) return;  // lives in the graph's memory (freed with the graph)
+  if (ctx->capturing) {
+    ctx->capture_deferred.push_back({p, words});  // a replay still reads it
+    return;
+  }
   {
     std::lock_guard<std::mutex> lk(ctx->alloc_mu);
     if (ctx->cached_words + words <= ctx->cache_cap_words) {
@@ -228,7 +237,7 @@ const u64* level_consts(Context& c, int limbs) {
   }
   BufPtr b = buf(c, h.size());
   SF_CUDA(cudaMemcpyAsync(b->p, h.data(), h.size() * sizeof(u64), cudaMemcpyHostToDevice, c.stream));
-  SF_CUDA(cudaStreamSynchronize(c.stream));  // h goes out of scope
+  host_sync(c);  // h goes out of scope
   c.level_consts[limbs] = b;
   c.level_consts_h[limbs] = h;
   return b->p;
@@ -278,7 +287,7 @@ const ConvPlan& conv_plan(Context& c, const std::vector<int>& src, const std::ve
   }
   p.tab = buf(c, h.size());
   SF_CUDA(cudaMemcpyAsync(p.tab->p, h.data(), h.size() * sizeof(u64), cudaMemcpyHostToDevice, c.stream));
-  SF_CUDA(cudaStreamSynchronize(c.stream));
+  host_sync(c);
   return c.conv_plans.emplace(key, std::move(p)).first->second;
 }
 
@@ -293,7 +302,7 @@ static BufPtr coeffs_to_ntt(Context& c, const std::vector<i64>& co, int limbs, b
   k_small_rns(c, out->p, ekey, noise, reinterpret_cast<const i64*>(tmp->p), primes.data(), limbs);
   ntt_limbs(c, out->p, limbs, 0, false);
   // the host vector must outlive the async copy
-  SF_CUDA(cudaStreamSynchronize(c.stream));
+  host_sync(c);
   return out;
 }
 
@@ -359,7 +368,7 @@ void decrypt(Context& c, const Ct& a, double* out) {
   ntt_limbs(c, mu->p, 1, 0, true);
   std::vector<u64> h(c.n);
   SF_CUDA(cudaMemcpyAsync(h.data(), mu->p, c.n * sizeof(u64), cudaMemcpyDeviceToHost, c.stream));
-  SF_CUDA(cudaStreamSynchronize(c.stream));
+  host_sync(c);
   const u64 q = c.primes[0];
   std::vector<double> co(c.n);
   for (int k = 0; k < c.n; ++k) co[k] = h[k] > q / 2 ? -(double)(q - h[k]) : (double)h[k];
@@ -393,7 +402,7 @@ Ct align_scale(Context& c, const Ct& a, int limbs, double target) {
     p.scale = (double)m;
     p.buf = buf(c, h.size());
     SF_CUDA(cudaMemcpyAsync(p.buf->p, h.data(), h.size() * 8, cudaMemcpyHostToDevice, c.stream));
-    SF_CUDA(cudaStreamSynchronize(c.stream));  // h is pageable and goes out of scope
+    host_sync(c);  // h is pageable and goes out of scope
     std::lock_guard<std::mutex> lk(c.mu);
     c.pt_cache[key] = p;
   }
@@ -581,7 +590,7 @@ const BufPtr& get_key_pinv(Context& c, u64 g) {
   BufPtr fd = buf(c, f.size());
   SF_CUDA(cudaMemcpyAsync(fd->p, f.data(), f.size() * sizeof(u64), cudaMemcpyHostToDevice, c.stream));
   k_scale_limbs(c, out->p, c.beta * 2, fd->p);
-  SF_CUDA(cudaStreamSynchronize(c.stream));  // f is pageable; keys are built once, off the timed path
+  host_sync(c);  // f is pageable; keys are built once, off the timed path
   std::lock_guard<std::mutex> lk(c.mu);
   return c.keys_pinv.emplace(g, out).first->second;
 }
@@ -665,7 +674,7 @@ std::vector<Pt> encode_many(Context& c, const std::function<void(int, double*)>&
                                 cudaMemcpyDeviceToDevice, c.stream));
         out[s + i] = p;
       }
-      SF_CUDA(cudaStreamSynchronize(c.stream));  // pinned buffer reused next chunk
+      host_sync(c);  // pinned buffer reused next chunk
     }
   } catch (...) {
     cudaFreeHost(pinned);

@@ -55,7 +55,7 @@ struct U64Arr {
 inline void post_launch(Context& c) {
   c.launches.fetch_add(1, std::memory_order_relaxed);
 #ifdef SF_DEBUG_SYNC
-  SF_CUDA(cudaStreamSynchronize(c.stream));
+  host_sync(c);
 #endif
   SF_CUDA(cudaGetLastError());
 }

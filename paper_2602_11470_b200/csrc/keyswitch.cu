@@ -202,7 +202,7 @@ const std::vector<u64>& merged_consts(Context& c, int limbs, const u64** dev) {
     }
     BufPtr b = make_buf(c, h.size());
     SF_CUDA(cudaMemcpyAsync(b->p, h.data(), h.size() * sizeof(u64), cudaMemcpyHostToDevice, c.stream));
-    SF_CUDA(cudaStreamSynchronize(c.stream));
+    host_sync(c);
     c.merged_consts[limbs] = b;
     it = c.merged_consts_h.emplace(limbs, std::move(h)).first;
   }
@@ -400,7 +400,7 @@ void ks_jobs(Context& c, const ExtB& x, const std::vector<KsJob>& jobs, bool mer
             ab.d[ab.count++] = poly ? jobs[s0 + j].add1 : jobs[s0 + j].add0;
           }
         b_axpy_pm(c, ab, limbs, pmd->p);
-        SF_CUDA(cudaStreamSynchronize(c.stream));  // pmh outlives the copy (generic small-ring path only)
+        host_sync(c);  // pmh outlives the copy (generic small-ring path only)
       }
       for (int j = 0; j < J; ++j)
         for (int poly = 0; poly < 2; ++poly) md.push_back({accp(j, poly), nullptr, 0, poly ? jobs[s0 + j].out1 : jobs[s0 + j].out0});

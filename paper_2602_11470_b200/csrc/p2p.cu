@@ -119,6 +119,15 @@ __global__ void p2p_release_kernel(u64* region, size_t cap) {
   st_release_sys(cw + (e & 1), e);
 }
 
+__device__ __forceinline__ ulonglong2 ld_volatile2(const u64* p) {
+  ulonglong2 v;
+  asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p));
+  return v;
+}
+
+// One thread per PAIR of words (16-byte peer loads over NVLink): the slot
+// layout keeps every polynomial at an even word offset (header 4 words,
+// widths limbs*n), and a pair never straddles a limb (n is even).
 __global__ void p2p_reduce_kernel(ReduceArgs A, const u64* Q, u64* own_region) {
   const u64 e = ld_volatile(ctrl(own_region, A.cap) + 4) + 1, s = e & 1;
   if (threadIdx.x == 0)
@@ -126,25 +135,34 @@ __global__ void p2p_reduce_kernel(ReduceArgs A, const u64* Q, u64* own_region) {
       while (ld_acquire_sys(ctrl(const_cast<u64*>(A.peers[r]), A.cap) + s) < e) __nanosleep(64);
   __syncthreads();
   const int j = blockIdx.y;
-  const size_t w = A.words[j];
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < 2 * w; i += (size_t)gridDim.x * blockDim.x) {
-    const int poly = i >= w;
-    const size_t ii = i - poly * w;
+  const size_t w2 = A.words[j] >> 1;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < 2 * w2; i += (size_t)gridDim.x * blockDim.x) {
+    const int poly = i >= w2;
+    const size_t ii = 2 * (i - poly * w2);
     const u64 q = Q[ii / A.n];
-    u64 acc = 0;
-    for (int r = 0; r < A.world; ++r) {
-      acc += ld_volatile(A.peers[r] + s * A.cap + A.off[j] + kHdrW + poly * A.pw + ii);
-      acc = acc >= q ? acc - q : acc;
+    const size_t at = s * A.cap + A.off[j] + kHdrW + poly * A.pw + ii;
+    ulonglong2 acc = ld_volatile2(A.peers[0] + at);
+    for (int r = 1; r < A.world; ++r) {
+      const ulonglong2 v = ld_volatile2(A.peers[r] + at);
+      acc.x += v.x;
+      acc.x = acc.x >= q ? acc.x - q : acc.x;
+      acc.y += v.y;
+      acc.y = acc.y >= q ? acc.y - q : acc.y;
     }
-    (poly ? A.out1[j] : A.out0[j])[ii] = acc;
+    *reinterpret_cast<ulonglong2*>((poly ? A.out1[j] : A.out0[j]) + ii) = acc;
   }
 }
 
+// Release our reads of every peer's slot: the fence orders them before the
+// system-scope release atomics that let each peer overwrite the slot.
 __global__ void p2p_ack_kernel(ReduceArgs A, u64* own_region) {
   u64* cw = ctrl(own_region, A.cap);
   const u64 e = ld_volatile(cw + 4) + 1, s = e & 1;
-  for (int r = 0; r < A.world; ++r) atomicAdd((unsigned long long*)(ctrl(const_cast<u64*>(A.peers[r]), A.cap) + 2 + s), 1ull);
   __threadfence_system();
+  for (int r = 0; r < A.world; ++r) {
+    u64* ack = ctrl(const_cast<u64*>(A.peers[r]), A.cap) + 2 + s;
+    asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(ack) : "memory");
+  }
   cw[4] = e;
 }
 
@@ -255,7 +273,7 @@ std::vector<Ct> p2p_sum_cts(Context& c, const std::vector<const Ct*>& cts, const
   p2p_release_kernel<<<1, 1, 0, c.stream>>>(p.region, p.cap);
   launched(c);
   {
-    const unsigned gx = (unsigned)std::max<size_t>(1, std::min<size_t>(148 * 4, (2 * pw + 255) / 256));
+    const unsigned gx = (unsigned)std::max<size_t>(1, std::min<size_t>(148 * 4, (pw + 255) / 256));
     p2p_reduce_kernel<<<dim3(gx, k), 256, 0, c.stream>>>(R, c.tabs.q, p.region);
     launched(c);
   }

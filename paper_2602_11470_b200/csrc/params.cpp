@@ -76,7 +76,10 @@ std::vector<u64> generate_primes(int logn, int L, int q0_bits, int scale_bits, i
   const u64 m = 2ull << logn;
   std::vector<u64> used;
   auto take = [&](int bits, int count) {
-    require(bits >= 20 && bits <= 61, kDomain, "prime bits must be in [20, 61]");
+    // <= 60 bits: the lazy kernels keep sums of up to 8 Shoup products in [0, 2q)
+    // in one u64 (fused column conversion) and fold 128-bit inner products
+    // every 64+ terms (ks_sum); both bounds need q < 2^60.
+    require(bits >= 20 && bits <= 60, kDomain, "prime bits must be in [20, 60]");
     std::vector<u64> r;
     u64 c = ((1ull << bits) / m) * m + 1;
     if (c >= (1ull << bits)) c -= m;

@@ -6,6 +6,7 @@
 //  * the client <-> server ciphertext format: header + the RNS words.
 // All integers little-endian; every file / buffer starts with a magic and a
 // version and carries the ring fingerprint it was produced under.
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <fstream>
@@ -20,18 +21,31 @@ namespace {
 
 constexpr uint32_t kCtMagic = 0x54434653u;    // "SFCT"
 constexpr uint32_t kPlanMagic = 0x50564653u;  // "SFVP"
-constexpr uint32_t kVersion = 1;
+constexpr uint32_t kVersion = 2;
 
+// FNV-1a over the whole prime chain (q0..qL, p0..p_{alpha-1}) plus a key-material
+// id (a one-way mix of the key seed), so contexts that differ in any prime
+// (e.g. scale_bits) or in the keys reject each other's ciphertexts. Plans hold
+// plaintexts only and are key-independent: they carry key_id = 0.
+u64 mix64(u64 z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
 struct Fingerprint {
   uint32_t logn, np, alpha, L;
-  uint64_t q0, qlast;
+  uint64_t chain, key_id;
 };
-Fingerprint fingerprint(const Context& c) {
-  return Fingerprint{(uint32_t)c.logn, (uint32_t)c.np, (uint32_t)c.alpha, (uint32_t)c.L, c.primes.front(),
-                     c.primes.back()};
+Fingerprint fingerprint(const Context& c, bool with_key) {
+  u64 h = 0xCBF29CE484222325ull;
+  for (u64 q : c.primes)
+    for (int b = 0; b < 8; ++b) h = (h ^ ((q >> (8 * b)) & 0xFF)) * 0x100000001B3ull;
+  return Fingerprint{(uint32_t)c.logn, (uint32_t)c.np, (uint32_t)c.alpha, (uint32_t)c.L, h,
+                     with_key ? mix64(mix64(c.seed ^ 0x5F4B45595F494400ull) + 0x9E3779B97F4A7C15ull) : 0};
 }
 bool same(const Fingerprint& a, const Fingerprint& b) {
-  return a.logn == b.logn && a.np == b.np && a.alpha == b.alpha && a.L == b.L && a.q0 == b.q0 && a.qlast == b.qlast;
+  return a.logn == b.logn && a.np == b.np && a.alpha == b.alpha && a.L == b.L && a.chain == b.chain &&
+         a.key_id == b.key_id;
 }
 
 struct CtHeader {
@@ -79,7 +93,7 @@ void ct_serialize(Context& c, const Ct& a, uint8_t* out) {
   CtHeader h{};
   h.magic = kCtMagic;
   h.version = kVersion;
-  h.fp = fingerprint(c);
+  h.fp = fingerprint(c, true);
   h.limbs = a.limbs;
   h.zero = a.zero ? 1 : 0;
   h.scale = a.scale;
@@ -107,7 +121,8 @@ Ct ct_deserialize(Context& c, const uint8_t* in, size_t len) {
   std::memcpy(&h, in, sizeof h);
   require(h.magic == kCtMagic, kShapeMismatch, "ct_deserialize: not a ciphertext (bad magic)");
   require(h.version == kVersion, kShapeMismatch, "ct_deserialize: unsupported version");
-  require(same(h.fp, fingerprint(c)), kShapeMismatch, "ct_deserialize: produced under different parameters");
+  require(same(h.fp, fingerprint(c, true)), kShapeMismatch,
+          "ct_deserialize: produced under different parameters or keys");
   require(h.limbs >= 1 && h.limbs <= c.L + 1, kInvalidTarget, "ct_deserialize: level out of range");
   OptLayout ly;
   if (h.ly_valid) {
@@ -118,6 +133,8 @@ Ct ct_deserialize(Context& c, const uint8_t* in, size_t len) {
     l.offset = h.ly_offset;
     l.heads = h.ly_heads;
     l.deferred_mask = h.ly_deferred != 0;
+    require(h.ly_kind >= 0 && h.ly_kind <= 2, kShapeMismatch, "ct_deserialize: bad layout kind");
+    validate_layout(l, c.slots);  // untrusted header: same checks as Backend::encrypt (layouts.cpp:50-64)
     ly = l;
   }
   if (h.zero) {
@@ -128,6 +145,18 @@ Ct ct_deserialize(Context& c, const uint8_t* in, size_t len) {
   }
   const size_t w = (size_t)h.limbs * c.n;
   require(len == sizeof h + 2 * w * sizeof(u64), kShapeMismatch, "ct_deserialize: truncated words");
+  require(h.scale > 0 && std::isfinite(h.scale), kShapeMismatch, "ct_deserialize: bad scale");
+  {  // every residue must be canonical (< its prime): the kernels assume it
+    const u64* words = reinterpret_cast<const u64*>(in + sizeof h);
+    for (int part = 0; part < 2; ++part)
+      for (int i = 0; i < h.limbs; ++i) {
+        const u64 q = c.primes[i];
+        const u64* p = words + ((size_t)part * h.limbs + i) * c.n;
+        u64 bad = 0;
+        for (int j = 0; j < c.n; ++j) bad |= (u64)(p[j] >= q);
+        require(!bad, kDomain, "ct_deserialize: non-canonical residue (word >= its prime)");
+      }
+  }
   Ct r = alloc_ct(c, h.limbs, h.scale);
   r.layout = ly;
   SF_CUDA(cudaMemcpyAsync(r.c0(), in + sizeof h, 2 * w * sizeof(u64), cudaMemcpyHostToDevice, c.stream));
@@ -140,7 +169,7 @@ Ct ct_deserialize(Context& c, const uint8_t* in, size_t len) {
 void vmm_plan_save(Context& c, VmmPlan& p, const std::string& path) {
   std::ofstream f(path, std::ios::binary);
   require((bool)f, kInvalidTarget, "vmm_plan_save: cannot open " + path);
-  const Fingerprint fp = fingerprint(c);
+  const Fingerprint fp = fingerprint(c, false);
   const int32_t hdr[9] = {p.rows, p.cols, p.level, p.s.tau_in, p.s.tau_out, p.bsgs ? 1 : 0, p.batch ? 1 : 0,
                           (int32_t)p.s.k, (int32_t)p.pts.size()};
   f.write(reinterpret_cast<const char*>(&kPlanMagic), 4);
@@ -176,7 +205,7 @@ std::unique_ptr<VmmPlan> vmm_plan_load(Context& c, const std::string& path) {
   f.read(reinterpret_cast<char*>(hdr), sizeof hdr);
   require((bool)f && magic == kPlanMagic, kShapeMismatch, "vmm_plan_load: not a plan file (bad magic)");
   require(version == kVersion, kShapeMismatch, "vmm_plan_load: unsupported version");
-  require(same(fp, fingerprint(c)), kShapeMismatch, "vmm_plan_load: plan encoded under different parameters");
+  require(same(fp, fingerprint(c, false)), kShapeMismatch, "vmm_plan_load: plan encoded under different parameters");
   const int rows = hdr[0], cols = hdr[1], level = hdr[2];
   std::vector<double> w((size_t)rows * cols);
   f.read(reinterpret_cast<char*>(w.data()), (std::streamsize)(w.size() * sizeof(double)));

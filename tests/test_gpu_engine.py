@@ -169,6 +169,42 @@ def test_graph_capture_replays_the_step_bit_exactly():
         assert all(np.array_equal(g_, w_) for g_, w_ in zip(got, want))
 
 
+def test_capture_cold_caches_and_graph_memory_is_released():
+    """(1) Capturing a step whose lazy tables / keys are still cold: the capture
+    is retried after one eager warm-up run and replays bit-exactly. (2) Graph-
+    owned step outputs are freed when the graph and its handles are gone:
+    repeated capture / launch / destroy cycles do not grow device memory."""
+    import gc
+    import paper_2602_11470_b200 as sf
+    from oracle.layout import make_interleaved
+    N, L = 4096, 4
+    be = sf.Backend(N, L, alpha=2, seed=11)
+    ly = make_interleaved(64, N, 0)
+    s = np.zeros(N)
+    s[np.arange(64) * ly.t] = np.random.default_rng(0).normal(size=64)
+    x = be.encrypt(s, L, ly, seed=1)
+    plan = sf.VmmPlan(be, np.random.default_rng(1).normal(size=(64, 64)) / 8, 64, 64, L, 0, 0, True)
+
+    def step():
+        return [be.rotate(sf.vmm_interleaved(be, x, None, mask_output=True, plan=plan), 7)]
+
+    graph, outs = be.capture(step)  # cold: rotation key for 7, plan plaintexts, conversion tables
+    graph.launch()
+    want = step()[0].data()
+    assert np.array_equal(outs[0].data(), want)
+    del graph, outs
+    gc.collect()
+    g_base = be.mem_stats()[0]
+    for i in range(6):
+        g, o = be.capture(step)
+        g.launch()
+        assert np.array_equal(o[0].data(), want)
+        assert be.mem_stats()[0] > g_base  # the replay's outputs are graph memory
+        del g, o
+        gc.collect()
+        assert be.mem_stats()[0] <= g_base  # ... released with the graph and its handles
+
+
 def test_vmm_multi_equals_separate_calls_and_ledger():
     # Q/K/V-style: three plans on one input (different output offsets) must give
     # the separate calls' ciphertexts word for word and the same ledger totals
@@ -231,6 +267,29 @@ def test_wire_formats_round_trip(tmp_path):
     other = sf.Backend(N, L + 1, alpha=2)
     with pytest.raises(sf.ShapeMismatch):
         other.deserialize(wire)
+    # same shape, different scale primes / different keys: rejected (full-chain + key-id fingerprint)
+    with pytest.raises(sf.ShapeMismatch):
+        sf.Backend(N, L, alpha=2, scale_bits=39).deserialize(wire)
+    with pytest.raises(sf.ShapeMismatch):
+        sf.Backend(N, L, alpha=2, seed=99).deserialize(wire)
+    # plans are key-independent: a plan saved under one key seed loads under another
+    p_other = sf.vmm_plan_load(sf.Backend(N, L, alpha=2, seed=99), str(tmp_path / "plan.sfvp"))
+    assert p_other is not None
+    # non-canonical residue (word >= q) in an otherwise valid buffer: rejected
+    bad = bytearray(wire)
+    bad[-8:] = (2**64 - 1).to_bytes(8, "little")
+    with pytest.raises(sf.DomainViolation):
+        be.deserialize(bytes(bad))
+
+
+def test_prime_bits_clamped_to_60():
+    """The lazy kernels need q < 2^60 (8 lazy Shoup products per u64 in the
+    fused column stage); 61-bit primes are rejected up front."""
+    import paper_2602_11470_b200 as sf
+    with pytest.raises(sf.DomainViolation):
+        sf.Backend(1024, 2, q0_bits=61)
+    with pytest.raises(sf.DomainViolation):
+        sf.Backend(1024, 2, special_bits=61)
 
 
 @pytest.mark.parametrize("mask", [False, True])
