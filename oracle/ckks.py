@@ -75,6 +75,7 @@ def lib():
             "ock_ct_d2": (None, [vp, U64P]),
             "ock_ct_set_d2": (None, [vp, U64P]),
             "ock_level_drop": (vp, [vp, vp, C.c_int]),
+            "ock_bench_weight": (None, [C.c_int, C.c_int, DP]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -89,6 +90,14 @@ def _u64(a: np.ndarray):
 
 def _dp(a: np.ndarray):
     return a.ctypes.data_as(DP)
+
+
+def bench_weight(rows: int, cols: int) -> np.ndarray:
+    """The reference bench weight sin(0.001(31r+c)+0.25) (slotforge_cli.cpp:88-92),
+    computed in C with libm exactly as the product's W = NULL plans are."""
+    out = np.empty((rows, cols))
+    lib().ock_bench_weight(rows, cols, _dp(out))
+    return out
 
 
 def fold_radix(d_head: int):

@@ -1070,5 +1070,13 @@ void* ock_rescale(void* c, void* a) {
 void* ock_level_drop(void* c, void* a, int limbs) {
   return guard([&]() -> void* { return drop_to(*static_cast<Ctx*>(c), (Ct*)a, limbs); });
 }
+// The reference bench weight W[r][c] = sin(0.001 (31 r + c) + 0.25)
+// (slotforge_cli.cpp:88-92), row-major rows x cols, evaluated with the same
+// libm sin and operation order as the product's W = NULL plans.
+void ock_bench_weight(int rows, int cols, double* out) {
+#pragma omp parallel for
+  for (int r = 0; r < rows; ++r)
+    for (int cc = 0; cc < cols; ++cc) out[(size_t)r * cols + cc] = std::sin(0.001 * ((double)r * 31.0 + cc) + 0.25);
+}
 
 }  // extern "C"

@@ -194,15 +194,22 @@ def test_capture_cold_caches_and_graph_memory_is_released():
     assert np.array_equal(outs[0].data(), want)
     del graph, outs
     gc.collect()
+    # graph memory is reserved in 64 MiB chunks: make every capture's outputs
+    # ~32 MiB so six leaked generations would be visible
+    y = sf.vmm_interleaved(be, x, None, mask_output=True, plan=plan)
+
+    def big_step():
+        return [be.add(y, y) for _ in range(64)]
+
+    big_step()
     g_base = be.mem_stats()[0]
     for i in range(6):
-        g, o = be.capture(step)
+        g, o = be.capture(big_step)
         g.launch()
-        assert np.array_equal(o[0].data(), want)
-        assert be.mem_stats()[0] > g_base  # the replay's outputs are graph memory
+        assert np.array_equal(o[0].data(), o[63].data())
         del g, o
         gc.collect()
-        assert be.mem_stats()[0] <= g_base  # ... released with the graph and its handles
+    assert be.mem_stats()[0] <= g_base + (64 << 20)  # released with the graphs and their handles
 
 
 def test_vmm_multi_equals_separate_calls_and_ledger():
