@@ -239,6 +239,17 @@ class LlamaLayer:
         return [q, k, v, maps[0], att, o, g, u, dn]
 
 
+def bench_config(alpha, world, sharded):
+    """The workload's config, identical on both arms (the reference arm runs the
+    same decode step on the host cores)."""
+    par = "single" if world == 1 else (
+        f"sharded{world} (one token split over the ranks: VMM giant groups, QK^T key-ct groups, Score*V pairs; "
+        "fused peer-memory exchange)" if sharded else f"replicas{world}")
+    return {"workload": "llama3-8b-layer-decode@n'=2048", "ring_degree": 2 * SLOTS, "slots": SLOTS, "d": D,
+            "heads": H, "ffn": FF, "context": NP, "levels": LEVELS, "L": 7, "alpha": alpha, "parallelism": par,
+            "l2": "working set (plaintext diagonals + keys ~30 GB) >> 126 MB L2; no flush needed"}
+
+
 def bench_weight(rows, cols):
     r = np.arange(rows, dtype=np.float64)[:, None]
     c = np.arange(cols, dtype=np.float64)[None, :]
@@ -267,6 +278,16 @@ def decrypt_parity(be, layer, outs):
     return errs
 
 
+def reduce_ranks(dist, v, op):
+    """All-reduce one float over the ranks (a CUDA tensor over NCCL, a CPU one
+    over gloo when ranks share a device)."""
+    import torch
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(v)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=op)
+    return float(t.item())
+
+
 def run_sharded(args, be, sf, layer, dist, rank, world, clk):
     """--shard: strong scaling of ONE token over the ranks (latency). Default:
     the exchange on the library stream (shard.StreamSharded, csrc/comm.cpp) and
@@ -290,9 +311,7 @@ def run_sharded(args, be, sf, layer, dist, rank, world, clk):
     torch.cuda.synchronize()
 
     def max_over_ranks(v):
-        t = torch.tensor([v], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return reduce_ranks(dist, v, dist.ReduceOp.MAX)
 
     # eager (host-issued) timing, for the record
     dist.barrier()
@@ -325,8 +344,7 @@ def run_sharded(args, be, sf, layer, dist, rank, world, clk):
     be.synchronize()
     launches = (be.kernel_launches() - l0) // args.steps
     clk.__exit__()
-    ex = torch.tensor([1 if exact else 0], device="cuda")
-    dist.all_reduce(ex, op=dist.ReduceOp.MIN)
+    ex_all = reduce_ranks(dist, 1.0 if exact else 0.0, dist.ReduceOp.MIN)
 
     # e2e: inputs from host memory every step, results read back
     host_in = [c.data() for c in layer.inputs]
@@ -350,14 +368,11 @@ def run_sharded(args, be, sf, layer, dist, rank, world, clk):
             "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "u64",
             "data": "synthetic: reference bench weights sin(0.001(31r+c)+0.25), N(0,1) activations/cache, seeded",
-            "config": {"workload": "llama3-8b-layer-decode@n'=2048", "ring_degree": 2 * SLOTS, "slots": SLOTS,
-                       "d": D, "heads": H, "ffn": FF, "context": NP, "levels": LEVELS, "L": 7, "alpha": args.alpha,
-                       "parallelism": f"sharded{world} (giant / key-ct / pair groups; exchange: " +
-                                      ("torch-stream NCCL all-gather + mod-add" if args.shard_host else
-                                       "NCCL all-gather on the library stream + mod-add" if args.shard_nccl else
-                                       "fused peer-memory read + mod-add kernel (CUDA IPC / NVLink)") + ")",
-                       "l2": "working set >> 126 MB L2; no flush needed"},
-            "sharded_bit_exact_vs_single_device": bool(ex.item()),
+            "config": bench_config(args.alpha, world, True),
+            "exchange": ("torch-stream NCCL all-gather + mod-add" if args.shard_host else
+                         "NCCL all-gather on the library stream + mod-add" if args.shard_nccl else
+                         "fused peer-memory read + mod-add kernel (CUDA IPC / NVLink)"),
+            "sharded_bit_exact_vs_single_device": bool(ex_all == 1.0),
             "eager_ms_per_step": round(ms_eager, 3), "wall_ms_per_step_rank0_eager": round(wall, 3),
             "e2e": {"value": round(e2e, 3), "unit": "ms/token",
                     "h2d_bytes_per_step": int(sum(w.nbytes for w in host_in)),
@@ -373,26 +388,50 @@ def run_sharded(args, be, sf, layer, dist, rank, world, clk):
 
 # ---------------------------------------------------------------- reference arm
 def run_reference(args, rank):
+    """The reference's own CPU implementation of the step (oracle/_ref/ref_bench:
+    the unmodified slotforge SimBackend, single-threaded) on this host: every
+    warm-up and timed step is one process, run concurrently on all host cores
+    (W untimed, then K timed); value = the mean per-step latency the processes
+    measure themselves. Same metric, unit and config as our arm. Under torchrun
+    only rank 0 runs."""
     if rank != 0:
         return
     exe = os.path.join(ROOT, "oracle", "_ref", "ref_bench")
-    per_step_s = 20.0  # measured reference step ~19 s on one core; keep the run within minutes
-    steps = max(1, min(args.steps, int(180 // per_step_s)))
-    warm = min(args.warmup, 1)
-    out = subprocess.run([exe, "--workload", "llama", "--steps", str(steps), "--warmup", str(warm)],
-                         capture_output=True, text=True, check=True).stdout.strip().splitlines()[-1]
-    r = json.loads(out)
-    v = r["ms_per_step"]
+    cores = os.cpu_count() or 1
+
+    def batch(n):
+        res, running, todo = [], [], n
+        while todo or running:
+            while todo and len(running) < cores:
+                running.append(subprocess.Popen([exe, "--workload", "llama", "--steps", "1", "--warmup", "0"],
+                                                stdout=subprocess.PIPE, text=True))
+                todo -= 1
+            p = running.pop(0)
+            outp, _ = p.communicate()
+            if p.returncode:
+                raise RuntimeError(f"ref_bench exited {p.returncode}")
+            res.append(json.loads(outp.strip().splitlines()[-1]))
+        return res
+
+    batch(args.warmup)
+    t0 = time.perf_counter()
+    res = batch(args.steps)
+    wall = time.perf_counter() - t0
+    v = round(float(np.mean([r["ms_per_step"] for r in res])), 3)
+    used = min(cores, args.steps)
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "ms/token", "n_gpus": args.gpus,
-        "steps": steps, "warmup": warm, "ms_per_step": v, "higher_is_better": False, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference bench weights, mt19937_64 seeds)",
-        "config": {"workload": "llama3-8b-layer-decode@n'=2048 (cleartext slotforge SimBackend)", "slots": SLOTS,
-                   "ring_degree": 2 * SLOTS, "requested_steps": args.steps},
-        "cpu_baseline": {"value": v, "unit": "ms/token", "cores": 1, "kind": "reference",
-                         "sample": f"{steps} full decode step(s) of the unmodified reference (single-threaded)"},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False,
+        "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: reference bench weights sin(0.001(31r+c)+0.25) (slotforge_cli.cpp:88-92), "
+                "mt19937_64-seeded activations",
+        "config": bench_config(args.alpha, args.gpus, args.gpus > 1 and not args.replicas),
+        "cpu_baseline": {"value": v, "unit": "ms/token", "cores": used, "kind": "reference",
+                         "sample": f"{args.steps} full decode steps of the unmodified reference SimBackend "
+                                   f"(cleartext slot simulator), one single-threaded process per step, "
+                                   f"{used} concurrently on {cores} host cores; wall {wall:.1f} s"},
         "e2e": {"value": v, "unit": "ms/token", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "counts": r.get("counts"),
+        "counts": res[0].get("counts"),
     }
     print(json.dumps(line), flush=True)
 
@@ -412,6 +451,62 @@ def cpu_baseline_sample():
                           "(cleartext slot simulator, single-threaded)"}
     except Exception as e:  # pragma: no cover
         return {"value": None, "unit": "ms/token", "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
+
+
+def emulated_shards(be, sf, layer, steps, worlds=(2, 4, 8)):
+    """Predicted strong scaling of ONE token over N GPUs, measured on this one:
+    for every rank r of a world W, the rank's own work -- its partials (VMM giant
+    groups, QK^T key-ct groups, Score*V pairs; csrc/protocols.cpp *_partial),
+    the W-way modular sum of the exchanged partials (sf_sum_partials over W
+    ciphertexts: the same reads and adds as the peer-memory reduce kernel) and
+    the replicated tail (reduce ladders, RoPE, appends, lane fold,
+    relinearisation) -- is captured into a graph and timed with CUDA events.
+    The prediction ignores the NVLink transfer itself (reported separately as
+    bytes per exchange); a rank's step time is the max over ranks because every
+    exchange waits for all of them."""
+    from paper_2602_11470_b200 import shard
+    x, h7, h3, h1, p0, p1 = layer.inputs
+    wl = [layer.wq, layer.wk, layer.wv]
+
+    def step_rank(r, W):
+        parts = shard.vmm_multi_partial(be, x, wl, r, W)
+        q, k, v = shard.vmm_multi_finish(be, [shard.sum_partials(be, [p] * W) for p in parts], wl)
+        qr = sf.rope_apply(be, q, layer.cfg, layer.pos)
+        kr = sf.rope_apply(be, k, layer.cfg, layer.pos)
+        cache = sf.v_append(be, layer.cache, sf.make_v_pieces(be, layer.cache, v, layer.pos))
+        cache = sf.k_append(be, cache, kr)
+        mp = shard.qk_dot_partial(be, qr, cache, r, W)
+        maps = [shard.sum_partials(be, [m] * W) for m in mp]
+        sv = shard.softmax_times_v_partial(be, [p0, p1], cache, r, W)
+        att = shard.softmax_times_v_finish(be, [sv] * W, cache)
+        po = shard.vmm_partial(be, h7, layer.wo, r, W)
+        o = shard.vmm_finish(be, shard.sum_partials(be, [po] * W), layer.wo)
+        gu = shard.vmm_multi_partial(be, h3, [layer.wg, layer.wu], r, W)
+        g, u = shard.vmm_multi_finish(be, [shard.sum_partials(be, [p] * W) for p in gu], [layer.wg, layer.wu])
+        pd = shard.vmm_partial(be, h1, layer.wd, r, W)
+        dn = shard.vmm_finish(be, shard.sum_partials(be, [pd] * W), layer.wd)
+        return [q, att, o, g, u, dn] + maps, [parts, mp, sv, gu, [po], [pd]]
+
+    out = {}
+    for W in worlds:
+        per_rank, xbytes = [], 0
+        for r in range(W):
+            graph, (outs, partials) = be.capture(step_rank, r, W)
+            if r == 0:  # bytes each rank publishes per token: every partial ciphertext of the step
+                flat = [c for grp in partials for c in grp]
+                xbytes = int(sum(2 * (c.level + 1) * 2 * SLOTS * 8 for c in flat if not c.is_zero))
+            graph.launch()
+            be.synchronize()
+            be.event_record(0)
+            for _ in range(steps):
+                graph.launch()
+            be.event_record(1)
+            per_rank.append(round(be.event_elapsed_ms(0, 1) / steps, 3))
+            del graph, outs, partials
+        out[str(W)] = {"rank_ms": per_rank, "max_rank_ms": max(per_rank),
+                       "exchange_bytes_published_per_rank": xbytes,
+                       "nvlink_ms_at_900GBps": round(xbytes * (W - 1) / 900e9 * 1e3, 3)}
+    return out
 
 
 def hevmm_c1(sf, steps):
@@ -684,39 +779,58 @@ def main():
     ap.add_argument("--alpha", type=int, default=2, help="special primes per key-switching digit")
     ap.add_argument("--quiet", action="store_true")
     ap.add_argument("--shard", action="store_true",
-                    help="strong scaling: split ONE token over the ranks (default: one replica per GPU)")
+                    help="split ONE token over the ranks (the default for --gpus > 1; with one GPU: a world of one)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="with --gpus > 1: N independent replicas (throughput) instead of one sharded token")
     ap.add_argument("--shard-host", action="store_true",
                     help="with --shard: exchange on torch's stream (eager) instead of the library stream + graph")
     ap.add_argument("--shard-nccl", action="store_true",
                     help="with --shard: NCCL all-gather on the library stream instead of the peer-memory exchange")
+    ap.add_argument("--no-emulate", action="store_true",
+                    help="skip the emulated per-rank timings of worlds 2/4/8 (N=1 only)")
     args = ap.parse_args()
 
     # NCCL announces its version on stdout at communicator creation unless told
     # otherwise; rank 0's stdout must carry exactly one JSON line
     os.environ.setdefault("NCCL_DEBUG", "WARN")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `bench.py --gpus N` without a launcher: re-run under torch.distributed.run, one rank per GPU
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.stdout.flush()
+        os.execv(sys.executable, cmd)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":  # host cores only: rank 0 runs, the other ranks exit without work
+        run_reference(args, rank)
+        return
+    if world > 1 and not args.replicas:
+        args.shard = True  # N > 1: one token split over the ranks (strong scaling, per-token latency)
     dist = None
     if world > 1 or args.shard:
         import torch
         import torch.distributed as dist
+        ngpu = torch.cuda.device_count()
+        local = local % max(ngpu, 1)  # more ranks than GPUs: ranks share devices (CUDA IPC still works)
         torch.cuda.set_device(local)
+        backend = "nccl" if ngpu >= world else "gloo"  # NCCL refuses two ranks on one device
         if world > 1:
-            dist.init_process_group("nccl")
+            dist.init_process_group(backend)
         else:  # --shard on one GPU: a world of one (exercises the exchange path)
             import socket
             sk = socket.socket()
             sk.bind(("127.0.0.1", 0))
             port = sk.getsockname()[1]
             sk.close()
-            dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
-    if args.impl == "reference":
-        run_reference(args, rank)
-        if dist:
-            dist.barrier()
-            dist.destroy_process_group()
-        return
+            dist.init_process_group(backend, init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+        if backend == "gloo" and args.shard_nccl:
+            raise SystemExit("--shard-nccl needs one GPU per rank")
 
     log = (lambda *a: None) if (args.quiet or rank != 0) else (lambda *a: print(*a, file=sys.stderr, flush=True))
     import paper_2602_11470_b200 as sf
@@ -787,10 +901,7 @@ def main():
     barrier()
     launches = be.kernel_launches() - l0
     if dist:
-        import torch
-        t = torch.tensor([ms_total], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_total = float(t.item())
+        ms_total = reduce_ranks(dist, ms_total, dist.ReduceOp.MAX)
     ms_step = ms_total / args.steps
     value = ms_step / world  # whole-job: `world` independent tokens per step time
 
@@ -890,12 +1001,17 @@ def main():
     e2e_parts = {"h2d_enqueue_ms": round(t_imp * 1e3 / args.steps, 3), "graph_launch_ms": round(t_iss * 1e3 / args.steps, 3),
                  "readback_wait_ms": round(t_rd * 1e3 / args.steps, 3), "pinned": pinned}
     if dist:
-        import torch
-        t = torch.tensor([e2e_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+        e2e_ms = reduce_ranks(dist, e2e_ms, dist.ReduceOp.MAX)
 
     phases = layer.phase_ms(args.steps)  # last: its graph's memory must not disturb the timed graph
+    emu = None
+    if world == 1 and not args.no_emulate:
+        try:
+            emu = emulated_shards(be, sf, layer, args.steps)
+            for W, e in emu.items():
+                e["predicted_speedup"] = round(ms_step / e["max_rank_ms"], 2)
+        except Exception as e:  # pragma: no cover
+            emu = {"error": str(e)}
     try:
         hevmm = hevmm_c1(sf, args.steps)
     except Exception as e:  # pragma: no cover
@@ -921,10 +1037,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "u64",
         "data": "synthetic: reference bench weights sin(0.001(31r+c)+0.25), N(0,1) activations/cache, seeded",
-        "config": {"workload": "llama3-8b-layer-decode@n'=2048", "ring_degree": 2 * SLOTS, "slots": SLOTS,
-                   "d": D, "heads": H, "ffn": FF, "context": NP, "levels": LEVELS, "L": 7, "alpha": args.alpha,
-                   "parallelism": f"replicas{world}" if world > 1 else "single",
-                   "l2": "working set (plaintext diagonals + keys ~30 GB) >> 126 MB L2; no flush needed"},
+        "config": bench_config(args.alpha, world, False),
         "hevmm_ct_per_s": round(vmm_per_step * world / (ms_step * 1e-3), 2),
         "hevmm_c1": hevmm,
         "prefill_c4": prefill,
@@ -934,6 +1047,7 @@ def main():
         "cpu_baseline": cpu,
         "cpu_baseline_ckks_twin": twin,
         "parity": parity,
+        "emulated_sharding": emu,
         "e2e": {"value": round(e2e_ms / world, 3), "unit": "ms/token", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "breakdown": e2e_parts},
         "gpu_launches": int(launches),
