@@ -542,6 +542,124 @@ def hevmm_c1(sf, steps):
                       "batched through sf_vmm_interleaved_many per graph replay, device-resident, CUDA events"}
 
 
+def c2_attention(sf, steps):
+    """BASELINE.json configs[1]: GPT-2 attention, 12 heads x
+    d_head 64 (run as H = 16 with 4 zero heads, d = 1024), ring 2^15 (2^14
+    slots); the KV cache grows from n' = 128 to 1024 by per-token append. Each
+    decode step = make_v_pieces + v_append + k_append of the new token, then
+    qk_dot and softmax_times_v over the whole cache (kv_attention.cpp:131-241),
+    issued eagerly through the public API (the cache grows, so every step has a
+    new shape). Reported: the stream's mean ms per decode step (device time,
+    CUDA events around the whole stream; and host wall), plus one captured step
+    replayed at n' = 1024 (device-resident, graph)."""
+    N, d, H = 16384, 1024, 16
+    cfg = sf.AttentionConfig(N, d, H, 0, 1024)
+    be = sf.Backend(N, 5, alpha=2, seed=3)
+    t = cfg.t
+    rng = np.random.default_rng(4)
+    vs_in, ks_in = [], []
+    for off in range(t):  # one fresh encryption per lane offset, reused by every token at that offset
+        vs = np.full(N, 0.5)
+        vs[np.arange(d) * t + off] = rng.normal(size=d)
+        vs_in.append(be.encrypt(vs, 4, sf.make_interleaved(d, N, off, H).with_(deferred_mask=True), seed=100 + off))
+        ks = np.zeros(N)
+        ks[np.arange(d) * t + off] = rng.normal(size=d) * 0.15
+        ks_in.append(be.encrypt(ks, 3, sf.make_interleaved(d, N, off, H), seed=200 + off))
+    qs = np.zeros(N)
+    qs[np.arange(d) * t] = rng.normal(size=d) * 0.15
+    qc = be.encrypt(qs, 3, sf.make_interleaved(d, N, 0, H), seed=5)
+    probs = [be.encrypt(np.full(N, 1.0 / 1024), 3, seed=6)]
+
+    def append(cache, u):
+        cache = sf.v_append(be, cache, sf.make_v_pieces(be, cache, vs_in[u % t], u))
+        return sf.k_append(be, cache, ks_in[u % t])
+
+    def step(cache, u):
+        cache = append(cache, u)
+        maps = sf.qk_dot(be, qc, cache)
+        att = sf.softmax_times_v(be, probs[:len(maps)], cache)
+        return cache, att
+
+    cache = sf.KVCache(be, cfg)
+    for u in range(128):  # the prompt stands in as appended tokens (off the timed region)
+        cache = append(cache, u)
+    step(cache, 128)  # warm: keys, masks, conversion tables
+    be.synchronize()
+    be.ledger.reset()
+    be.event_record(0)
+    t0 = time.perf_counter()
+    for u in range(128, 1024):
+        cache, att = step(cache, u)
+    be.event_record(1)
+    dev = be.event_elapsed_ms(0, 1)
+    be.synchronize()
+    wall = (time.perf_counter() - t0) * 1e3
+    counts = be.ledger.totals().asdict()
+    # one decode step at n' = 1023 -> 1024, captured and replayed (device-resident)
+    n_before = cache  # noqa: F841 (kept alive)
+    full = sf.KVCache(be, cfg)
+    for u in range(1023):
+        full = append(full, u)
+    graph, _ = be.capture(step, full, 1023)
+    graph.launch()
+    be.synchronize()
+    be.event_record(2)
+    for _ in range(steps):
+        graph.launch()
+    be.event_record(3)
+    g_ms = be.event_elapsed_ms(2, 3) / steps
+    be.synchronize()
+    return {"stream_ms_per_step": round(dev / 896, 3), "stream_wall_ms_per_step": round(wall / 896, 3),
+            "graph_ms_per_step_at_1024": round(g_ms, 3), "steps": 896, "ledger_stream": counts,
+            "config": "GPT-2 attention (12 heads x 64, as H=16, d=1024), ring 2^15, L=5, alpha=2: 896 decode "
+                      "steps n'=128->1024, each append + QK^T + Score*V; device time (CUDA events) over the eager "
+                      "stream, and one step at n'=1024 captured and replayed"}
+
+
+def c3_linear(sf, steps):
+    """BASELINE.json configs[2]: the GPT-2-small decoder-layer
+    linear path per decode token at ring 2^16 (2^15 slots), level 4: Q/K/V
+    (one multi-VMM of three 768x768 plans), the output projection 768x768, the
+    FFN 768->3072 and 3072->768 BSGS HE-VMMs, captured into one graph.
+    Reference bench weights (W = None plans), fresh encrypted inputs."""
+    N, lvl = SLOTS, 4
+    be = sf.Backend(N, lvl, alpha=2, seed=2)
+    mk = lambda r, c: sf.VmmPlan(be, None, r, c, lvl, 0, 0, True)  # noqa: E731
+    wq, wk, wv, wo, wu, wd = mk(768, 768), mk(768, 768), mk(768, 768), mk(768, 768), mk(768, 3072), mk(3072, 768)
+    rng = np.random.default_rng(21)
+
+    def fresh(d, seed):
+        dp = 1 << (d - 1).bit_length()
+        s = np.zeros(N)
+        s[np.arange(d) * (N // dp)] = rng.normal(size=d)
+        return be.encrypt(s, lvl, sf.make_interleaved(dp, N, 0), seed=seed)
+    x, h, hu, hd = fresh(768, 1), fresh(768, 2), fresh(768, 3), fresh(3072, 4)
+
+    def step():
+        q, k, v = sf.vmm_interleaved_multi(be, x, [wq, wk, wv])
+        o = sf.vmm_interleaved(be, h, None, plan=wo)
+        u = sf.vmm_interleaved(be, hu, None, plan=wu)
+        dn = sf.vmm_interleaved(be, hd, None, plan=wd)
+        return [q, k, v, o, u, dn]
+
+    step()
+    be.synchronize()
+    be.ledger.reset()
+    graph, _ = be.capture(step)
+    counts = be.ledger.totals().asdict()
+    graph.launch()
+    be.synchronize()
+    be.event_record(0)
+    for _ in range(steps):
+        graph.launch()
+    be.event_record(1)
+    ms = be.event_elapsed_ms(0, 1) / steps
+    be.synchronize()
+    return {"ms_per_token": round(ms, 3), "vmm_ct_per_s": round(6 / (ms * 1e-3), 1), "ledger": counts,
+            "config": "GPT-2-small layer linear path (QKV 3x768^2 multi-VMM, out 768^2, 768->3072, 3072->768), "
+                      "ring 2^16, level 4, alpha=2, bench weights; one graph, CUDA events"}
+
+
 def prefill_c4(sf, be, steps, n0=64):
     """SURVEY.md §8(f) rank 2 measured: the batched prefill of an n0-token
     prompt at the C4 layer shape (d 4096, 32 heads, ring 2^16) -- token-batched
@@ -786,6 +904,9 @@ def main():
                     help="with --shard: exchange on torch's stream (eager) instead of the library stream + graph")
     ap.add_argument("--shard-nccl", action="store_true",
                     help="with --shard: NCCL all-gather on the library stream instead of the peer-memory exchange")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="only the headline step (skip C1/C2/C3/C5, prefill and nonlinearity lines)")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the reduced C5 NTT / key-switch sweep")
     ap.add_argument("--no-emulate", action="store_true",
                     help="skip the emulated per-rank timings of worlds 2/4/8 (N=1 only)")
     args = ap.parse_args()
@@ -1012,18 +1133,36 @@ def main():
                 e["predicted_speedup"] = round(ms_step / e["max_rank_ms"], 2)
         except Exception as e:  # pragma: no cover
             emu = {"error": str(e)}
-    try:
-        hevmm = hevmm_c1(sf, args.steps)
-    except Exception as e:  # pragma: no cover
-        hevmm = {"value": None, "error": str(e)}
-    try:
-        prefill = prefill_c4(sf, be, args.steps)
-    except Exception as e:  # pragma: no cover
-        prefill = {"ms_per_prompt": None, "error": str(e)}
-    try:
-        nonlin = nonlinear_c4(sf)
-    except Exception as e:  # pragma: no cover
-        nonlin = {"error": str(e)}
+    hevmm = prefill = c2 = c3 = c5 = nonlin = None
+    if not args.no_extras:
+        try:
+            hevmm = hevmm_c1(sf, args.steps)
+        except Exception as e:  # pragma: no cover
+            hevmm = {"value": None, "error": str(e)}
+        try:
+            prefill = prefill_c4(sf, be, args.steps)
+        except Exception as e:  # pragma: no cover
+            prefill = {"ms_per_prompt": None, "error": str(e)}
+        try:
+            c2 = c2_attention(sf, args.steps)
+        except Exception as e:  # pragma: no cover
+            c2 = {"error": str(e)}
+        try:
+            c3 = c3_linear(sf, args.steps)
+        except Exception as e:  # pragma: no cover
+            c3 = {"error": str(e)}
+        c5 = None
+        if not args.no_sweep:
+            try:
+                sys.path.insert(0, os.path.join(ROOT, "tools"))
+                from sweep import sweep
+                c5 = sweep(levels=(8, 24, 40), logns=(15, 16), alpha=4, log=lambda m: None)
+            except Exception as e:  # pragma: no cover
+                c5 = {"error": str(e)}
+        try:
+            nonlin = nonlinear_c4(sf)
+        except Exception as e:  # pragma: no cover
+            nonlin = {"error": str(e)}
     cpu = None if (args.no_cpu_baseline or rank != 0) else cpu_baseline_sample()
     parity = {"decrypt_max_rel_err": decrypt_parity(be, layer, outs), "tolerance": 1e-3}
     parity["decrypt_ok"] = all(v <= parity["tolerance"] for v in parity["decrypt_max_rel_err"].values())
@@ -1040,6 +1179,9 @@ def main():
         "config": bench_config(args.alpha, world, False),
         "hevmm_ct_per_s": round(vmm_per_step * world / (ms_step * 1e-3), 2),
         "hevmm_c1": hevmm,
+        "attention_c2": c2,
+        "linear_c3": c3,
+        "sweep_c5": c5,
         "prefill_c4": prefill,
         "nonlinear_c4": nonlin,
         "roofline": roofline,

@@ -82,18 +82,51 @@ u64 bitrev(u64 x, int bits) {
   return r;
 }
 
-// --- PRNG: counter-based SplitMix64 mixing -----------------
-u64 fmix(u64 z) {
+// --- PRNG: ChaCha20 counter stream ---------------------------
+// Textbook ChaCha20 (D. J. Bernstein, 2008; RFC 8439 §2.3 block function with
+// the original 64-bit counter / 64-bit nonce split): state = 4 constants,
+// 8 key words, counter (2 words), nonce (2 words); 10 double rounds; output =
+// final state + input state. Key = the 64-bit seed (2 words) followed by the
+// domain words "sf_b200 ckks rng", 1, 0; nonce = the stream id; word i of a
+// stream is 64-bit word i mod 8 of block i / 8. Pinned against the
+// `cryptography` package's ChaCha20 (tests/test_ckks_oracle.py).
+uint32_t rotl(uint32_t v, int c) { return (v << c) | (v >> (32 - c)); }
+#define QR(a, b, c, d) \
+  a += b; d ^= a; d = rotl(d, 16); c += d; b ^= c; b = rotl(b, 12); \
+  a += b; d ^= a; d = rotl(d, 8);  c += d; b ^= c; b = rotl(b, 7);
+void chacha20_block(const uint32_t key[8], u64 counter, u64 nonce, uint32_t out[16]) {
+  const uint32_t in[16] = {0x61707865u, 0x3320646eu, 0x79622d32u, 0x6b206574u, key[0], key[1], key[2], key[3],
+                           key[4], key[5], key[6], key[7], (uint32_t)counter, (uint32_t)(counter >> 32),
+                           (uint32_t)nonce, (uint32_t)(nonce >> 32)};
+  uint32_t x[16];
+  std::copy(in, in + 16, x);
+  for (int i = 0; i < 10; ++i) {
+    QR(x[0], x[4], x[8], x[12]) QR(x[1], x[5], x[9], x[13]) QR(x[2], x[6], x[10], x[14]) QR(x[3], x[7], x[11], x[15])
+    QR(x[0], x[5], x[10], x[15]) QR(x[1], x[6], x[11], x[12]) QR(x[2], x[7], x[8], x[13]) QR(x[3], x[4], x[9], x[14])
+  }
+  for (int i = 0; i < 16; ++i) out[i] = x[i] + in[i];
+}
+#undef QR
+u64 rand64(u64 seed, u64 stream, u64 ctr) {
+  const uint32_t key[8] = {(uint32_t)seed, (uint32_t)(seed >> 32), 0x625f6673u, 0x20303032u,
+                           0x736b6b63u, 0x676e7220u, 1u, 0u};
+  uint32_t o[16];
+  chacha20_block(key, ctr / 8, stream, o);
+  const int w = (int)(ctr % 8);
+  return (u64)o[2 * w] | ((u64)o[2 * w + 1] << 32);
+}
+// uniform residue k of a stream mod q: words 2k, 2k+1 as one 128-bit integer
+u64 rand_mod(u64 seed, u64 stream, u64 k, u64 q) {
+  const unsigned __int128 v = ((unsigned __int128)rand64(seed, stream, 2 * k + 1) << 64) | rand64(seed, stream, 2 * k);
+  return (u64)(v % q);
+}
+u64 fmix(u64 z) {  // SplitMix64 finaliser: derives the seeds of counter-seeded encryptions
   z ^= z >> 30;
   z *= 0xbf58476d1ce4e5b9ull;
   z ^= z >> 27;
   z *= 0x94d049bb133111ebull;
   z ^= z >> 31;
   return z;
-}
-u64 rand64(u64 seed, u64 stream, u64 ctr) {
-  const u64 key = fmix(seed ^ fmix(stream ^ 0x9E3779B97F4A7C15ull));
-  return fmix(key + (ctr + 1) * 0x9E3779B97F4A7C15ull);
 }
 i64 cbd21(u64 r) {
   return (i64)__builtin_popcountll(r & 0x1FFFFFull) - (i64)__builtin_popcountll((r >> 21) & 0x1FFFFFull);
@@ -359,7 +392,7 @@ std::vector<u64> make_ksk(const Ctx& c, u64 kid, const std::vector<u64>& sprime)
       const u64* s = c.sk.data() + (size_t)m * n;
       const u64* sp = sprime.data() + (size_t)m * n;
       for (int k = 0; k < n; ++k) {
-        a[k] = rand64(c.seed, kStreamKeyA | (kid << 16) | ((u64)j << 8) | (u64)m, k) % q;
+        a[k] = rand_mod(c.seed, kStreamKeyA | (kid << 16) | ((u64)j << 8) | (u64)m, k, q);
         u64 v = submod(et[k], mulmod(a[k], s[k], q), q);
         if (pm) v = addmod(v, mulmod(pm, sp[k], q), q);
         b[k] = v;
@@ -416,7 +449,7 @@ Ct* encrypt(Ctx& c, const double* slots, int limbs, double scale, u64 seed) {
     const u64* s = c.sk.data() + (size_t)l * c.n;
     const u64* mm = m.data() + (size_t)l * c.n;
     for (int k = 0; k < c.n; ++k) {
-      const u64 a = rand64(seed, kStreamEncA | (u64)l, k) % q;
+      const u64 a = rand_mod(seed, kStreamEncA | (u64)l, k, q);
       c1[k] = a;
       c0[k] = addmod(submod(et[k], mulmod(a, s[k], q), q), mm[k], q);
     }
@@ -1070,6 +1103,11 @@ void* ock_rescale(void* c, void* a) {
 void* ock_level_drop(void* c, void* a, int limbs) {
   return guard([&]() -> void* { return drop_to(*static_cast<Ctx*>(c), (Ct*)a, limbs); });
 }
+// One raw ChaCha20 block (the KAT hook of tests/test_ckks_oracle.py).
+void ock_chacha20_block(const uint32_t* key, uint64_t counter, uint64_t nonce, uint32_t* out) {
+  chacha20_block(key, counter, nonce, out);
+}
+uint64_t ock_rand64(uint64_t seed, uint64_t stream, uint64_t ctr) { return rand64(seed, stream, ctr); }
 // The reference bench weight W[r][c] = sin(0.001 (31 r + c) + 0.25)
 // (slotforge_cli.cpp:88-92), row-major rows x cols, evaluated with the same
 // libm sin and operation order as the product's W = NULL plans.

@@ -124,8 +124,49 @@ SF_HD u64 fmix64(u64 z) {
   z ^= z >> 31;
   return z;
 }
-SF_HD u64 stream_key(u64 seed, u64 stream) { return fmix64(seed ^ fmix64(stream ^ 0x9E3779B97F4A7C15ull)); }
-SF_HD u64 rand_at(u64 key, u64 ctr) { return fmix64(key + (ctr + 1) * 0x9E3779B97F4A7C15ull); }
+// Key material and encryption randomness: a ChaCha20 counter stream
+// (DESIGN.md §3.4). Word i of stream (seed, stream) is 64-bit word i mod 8 of
+// the ChaCha20 block (20 rounds, 64-bit block counter, 64-bit nonce) with
+//   key     = seed (2 words, little-endian) || "sf_b200 ckks rng" domain words || 1 || 0
+//   counter = i / 8,  nonce = stream id.
+struct RngKey {
+  u64 seed, stream;
+};
+SF_HD RngKey stream_key(u64 seed, u64 stream) { return RngKey{seed, stream}; }
+SF_HD uint32_t rotl32(uint32_t v, int c) { return (v << c) | (v >> (32 - c)); }
+SF_HD void chacha_qr(uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d) {
+  a += b, d ^= a, d = rotl32(d, 16);
+  c += d, b ^= c, b = rotl32(b, 12);
+  a += b, d ^= a, d = rotl32(d, 8);
+  c += d, b ^= c, b = rotl32(b, 7);
+}
+// the 16 output words of the block (state after 20 rounds + input state)
+SF_HD void chacha20_block(const uint32_t key[8], u64 counter, u64 nonce, uint32_t out[16]) {
+  uint32_t in[16] = {0x61707865u, 0x3320646eu, 0x79622d32u, 0x6b206574u, key[0], key[1], key[2], key[3],
+                     key[4], key[5], key[6], key[7], (uint32_t)counter, (uint32_t)(counter >> 32),
+                     (uint32_t)nonce, (uint32_t)(nonce >> 32)};
+  uint32_t x[16];
+  for (int i = 0; i < 16; ++i) x[i] = in[i];
+  for (int r = 0; r < 10; ++r) {
+    chacha_qr(x[0], x[4], x[8], x[12]);
+    chacha_qr(x[1], x[5], x[9], x[13]);
+    chacha_qr(x[2], x[6], x[10], x[14]);
+    chacha_qr(x[3], x[7], x[11], x[15]);
+    chacha_qr(x[0], x[5], x[10], x[15]);
+    chacha_qr(x[1], x[6], x[11], x[12]);
+    chacha_qr(x[2], x[7], x[8], x[13]);
+    chacha_qr(x[3], x[4], x[9], x[14]);
+  }
+  for (int i = 0; i < 16; ++i) out[i] = x[i] + in[i];
+}
+SF_HD u64 rand_at(RngKey k, u64 ctr) {
+  const uint32_t key[8] = {(uint32_t)k.seed, (uint32_t)(k.seed >> 32), 0x625f6673u, 0x20303032u,
+                           0x736b6b63u, 0x676e7220u, 1u, 0u};
+  uint32_t o[16];
+  chacha20_block(key, ctr >> 3, k.stream, o);
+  const int w = (int)(ctr & 7);
+  return (u64)o[2 * w] | ((u64)o[2 * w + 1] << 32);
+}
 constexpr u64 kStreamSk = 1ull << 56, kStreamKeyA = 2ull << 56, kStreamKeyE = 3ull << 56,
               kStreamEncA = 4ull << 56, kStreamEncE = 5ull << 56;
 

@@ -292,7 +292,7 @@ const ConvPlan& conv_plan(Context& c, const std::vector<int>& src, const std::ve
 }
 
 // upload signed coefficients and reduce into `limbs` NTT-domain limbs (+ noise)
-static BufPtr coeffs_to_ntt(Context& c, const std::vector<i64>& co, int limbs, bool noise, u64 ekey) {
+static BufPtr coeffs_to_ntt(Context& c, const std::vector<i64>& co, int limbs, bool noise, RngKey ekey) {
   SF_HPROF("coeffs_to_ntt");
   BufPtr tmp = buf(c, (size_t)c.n);
   SF_CUDA(cudaMemcpyAsync(tmp->p, co.data(), co.size() * sizeof(i64), cudaMemcpyHostToDevice, c.stream));
@@ -309,7 +309,7 @@ static BufPtr coeffs_to_ntt(Context& c, const std::vector<i64>& co, int limbs, b
 Pt encode_pt(Context& c, const double* slots, double scale, int limbs) {
   SF_HPROF("encode_pt");
   Pt p;
-  p.buf = coeffs_to_ntt(c, encode_coeffs(c, slots, scale), limbs, false, 0);
+  p.buf = coeffs_to_ntt(c, encode_coeffs(c, slots, scale), limbs, false, RngKey{0, 0});
   p.limbs = limbs;
   p.scale = scale;
   return p;
@@ -339,7 +339,7 @@ Ct encrypt(Context& c, const double* slots, int level, u64 seed, OptLayout layou
   Ct r = alloc_ct(c, limbs, c.delta);
   r.layout = layout;
   BufPtr em = coeffs_to_ntt(c, encode_coeffs(c, slots, c.delta), limbs, true, stream_key(seed, kStreamEncE));
-  std::vector<u64> keys(limbs);
+  std::vector<RngKey> keys(limbs);
   std::vector<int> primes(limbs);
   for (int l = 0; l < limbs; ++l) keys[l] = stream_key(seed, kStreamEncA | (u64)l), primes[l] = l;
   k_sample_uniform(c, r.c1(c.n), keys.data(), primes.data(), limbs);
@@ -546,7 +546,8 @@ const BufPtr& get_key(Context& c, u64 g) {
     ntt_limbs(c, e->p, np, 0, false);
     u64* b = key->p + ((size_t)j * 2 + 0) * np * n;
     u64* a = key->p + ((size_t)j * 2 + 1) * np * n;
-    std::vector<u64> keys(np), pm(np, 0);
+    std::vector<RngKey> keys(np);
+    std::vector<u64> pm(np, 0);
     const int lo = j * c.alpha, hi = std::min((j + 1) * c.alpha, c.L + 1);
     for (int m = 0; m < np; ++m) {
       keys[m] = stream_key(c.seed, kStreamKeyA | tag | (u64)m);
@@ -658,7 +659,7 @@ std::vector<Pt> encode_many(Context& c, const std::function<void(int, double*)>&
       SF_CUDA(cudaMemcpyAsync(dev->p, pinned, (size_t)m * n * sizeof(i64), cudaMemcpyHostToDevice, c.stream));
       BufPtr all = buf(c, (size_t)m * limbs * n);
       for (int i = 0; i < m; ++i)
-        k_small_rns(c, all->p + (size_t)i * limbs * n, 0, false, reinterpret_cast<const i64*>(dev->p + (size_t)i * n),
+        k_small_rns(c, all->p + (size_t)i * limbs * n, RngKey{0, 0}, false, reinterpret_cast<const i64*>(dev->p + (size_t)i * n),
                     primes.data(), limbs);
       std::vector<std::pair<u64*, int>> todo;
       for (int i = 0; i < m; ++i)

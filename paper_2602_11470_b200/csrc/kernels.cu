@@ -48,6 +48,9 @@ constexpr int kMaxL = 64;
 struct IntArr {
   int v[kMaxL];
 };
+struct RngArr {
+  RngKey v[kMaxL];
+};
 struct U64Arr {
   u64 v[kMaxL];
 };
@@ -286,12 +289,17 @@ __global__ void rescale_lift_kernel(u64* out, const u64* x, u64 ql, int limbs, i
 }
 
 // --- sampling ----------------------------------------------------------------------
-__global__ void uniform_kernel(u64* out, U64Arr keys, IntArr prime, int limbs, int n, const u64* Q) {
+// uniform residue k of a limb: two stream words as a 128-bit integer, reduced
+// mod q (bias < 2^-67; a single 64-bit word mod a 60-bit prime would be biased)
+__global__ void uniform_kernel(u64* out, RngArr keys, IntArr prime, int limbs, int n, const u64* Q, const u64* MH,
+                               const u64* ML) {
   const size_t total = (size_t)limbs * n;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
     const int l = (int)(i / n);
     const size_t k = i - (size_t)l * n;
-    out[i] = rand_at(keys.v[l], k) % Q[prime.v[l]];
+    const int p = prime.v[l];
+    const u64 lo = rand_at(keys.v[l], 2 * k), hi = rand_at(keys.v[l], 2 * k + 1);
+    out[i] = reduce128(hi, lo, Q[p], MH[p], ML[p]);
   }
 }
 
@@ -301,7 +309,7 @@ __device__ __forceinline__ u64 signed_to_mod(i64 v, u64 q) {
   return r == 0 ? 0 : q - r;
 }
 
-__global__ void ternary_kernel(u64* out, u64 key, int limbs, int n, int first_prime, const u64* Q) {
+__global__ void ternary_kernel(u64* out, RngKey key, int limbs, int n, int first_prime, const u64* Q) {
   const size_t total = (size_t)limbs * n;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
     const int l = (int)(i / n);
@@ -311,7 +319,7 @@ __global__ void ternary_kernel(u64* out, u64 key, int limbs, int n, int first_pr
   }
 }
 
-__global__ void small_rns_kernel(u64* out, u64 ekey, bool noise, const i64* m, IntArr prime, int limbs, int n,
+__global__ void small_rns_kernel(u64* out, RngKey ekey, bool noise, const i64* m, IntArr prime, int limbs, int n,
                                  const u64* Q) {
   const size_t total = (size_t)limbs * n;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
@@ -522,23 +530,23 @@ void k_rescale_lift(Context& c, u64* out, const u64* x, int last_prime, int limb
   post_launch(c);
 }
 
-void k_sample_uniform(Context& c, u64* out, const u64* stream_keys, const int* prime_of_limb, int limbs) {
+void k_sample_uniform(Context& c, u64* out, const RngKey* stream_keys, const int* prime_of_limb, int limbs) {
   require(limbs <= kMaxL, kInternal, "sample: too many limbs");
-  U64Arr k;
+  RngArr k;
   IntArr p;
   for (int l = 0; l < limbs; ++l) k.v[l] = stream_keys[l], p.v[l] = prime_of_limb[l];
   const size_t w = (size_t)limbs * c.n;
-  uniform_kernel<<<grid_cap(w), kThreads, 0, c.stream>>>(out, k, p, limbs, c.n, QP(c));
+  uniform_kernel<<<grid_cap(w), kThreads, 0, c.stream>>>(out, k, p, limbs, c.n, QP(c), c.tabs.mh, c.tabs.ml);
   post_launch(c);
 }
 
-void k_ternary(Context& c, u64* out, u64 key, int limbs, int first_prime) {
+void k_ternary(Context& c, u64* out, RngKey key, int limbs, int first_prime) {
   const size_t w = (size_t)limbs * c.n;
   ternary_kernel<<<grid_cap(w), kThreads, 0, c.stream>>>(out, key, limbs, c.n, first_prime, QP(c));
   post_launch(c);
 }
 
-void k_small_rns(Context& c, u64* out, u64 ekey, bool noise, const i64* m, const int* prime_of_limb, int limbs) {
+void k_small_rns(Context& c, u64* out, RngKey ekey, bool noise, const i64* m, const int* prime_of_limb, int limbs) {
   require(limbs <= kMaxL, kInternal, "small_rns: too many limbs");
   IntArr p;
   for (int l = 0; l < limbs; ++l) p.v[l] = prime_of_limb[l];

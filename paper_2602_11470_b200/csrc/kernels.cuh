@@ -41,10 +41,10 @@ void k_sub_scale(Context& c, u64* out, const u64* acc, const u64* conv, const u6
 void k_rescale_lift(Context& c, u64* out, const u64* x, int last_prime, int limbs);
 
 // sampling
-void k_sample_uniform(Context& c, u64* out, const u64* stream_keys, const int* prime_of_limb, int limbs);
-void k_ternary(Context& c, u64* out, u64 key, int limbs, int first_prime);  // sk coefficients
+void k_sample_uniform(Context& c, u64* out, const RngKey* stream_keys, const int* prime_of_limb, int limbs);
+void k_ternary(Context& c, u64* out, RngKey key, int limbs, int first_prime);  // sk coefficients
 // small signed coefficients v = cbd(rand(key, k)) + (m ? m[k] : 0) reduced mod each prime
-void k_small_rns(Context& c, u64* out, u64 ekey, bool noise, const i64* m, const int* prime_of_limb, int limbs);
+void k_small_rns(Context& c, u64* out, RngKey ekey, bool noise, const i64* m, const int* prime_of_limb, int limbs);
 // b = -a*s + e (+ pm * s') ; operands per limb via prime index
 void k_key_combine(Context& c, u64* b, const u64* a, const u64* s, const u64* e, const u64* sp, const u64* pm,
                    const int* prime_of_limb, int limbs);

@@ -148,11 +148,12 @@ template <int LOGR, int LOGC, bool INV>
 __global__ void __launch_bounds__(kWarps * 32) ntt_col_pass(LimbBatch B, Tabs T) {
   constexpr int R = 1 << LOGR, C = 1 << LOGC, E = R / 32, LOGN = LOGR + LOGC;
   constexpr int tiles = C / kWarps;
-  constexpr int PAD = R + 1;  // column regions offset by one bank
+  constexpr int PAD = R + 2;  // column regions offset by one 8-byte bank pair (conflict-free row-major staging)
   __shared__ u64 sm_all[kWarps * PAD];
   __shared__ u64 tw_s[2 * R];
   const int entry = blockIdx.x / tiles, tile = blockIdx.x - entry * tiles;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int swl = swz(lane);  // lane part of the (linear) swizzle
   const int p = B.prime[entry];
   const u64 q = T.q[p];
   u64* a = B.ptr[entry] + tile * kWarps;
@@ -172,7 +173,7 @@ __global__ void __launch_bounds__(kWarps * 32) ntt_col_pass(LimbBatch B, Tabs T)
   u64* sm = sm_all + warp * PAD;
   u64 x[E];
 #pragma unroll
-  for (int k = 0; k < E; ++k) x[k] = sm[swz(lane + 32 * k)];
+  for (int k = 0; k < E; ++k) x[k] = sm[(swl ^ swz(32 * k))];
   __syncwarp();
   // column stage with distance 2^b rows: forward global stage r-1-b uses
   // psi[2^(r-1-b) + blk]; GS: h = n / (2 * 2^b * C) = 2^(r-1-b)
@@ -190,7 +191,7 @@ __global__ void __launch_bounds__(kWarps * 32) ntt_col_pass(LimbBatch B, Tabs T)
     for (int k = 0; k < E; ++k) x[k] = mul_shoup(x[k], ni, nis, q);
   }
 #pragma unroll
-  for (int k = 0; k < E; ++k) sm[swz(lane + 32 * k)] = x[k];
+  for (int k = 0; k < E; ++k) sm[(swl ^ swz(32 * k))] = x[k];
   __syncthreads();
   for (int e = threadIdx.x; e < R * kWarps; e += blockDim.x) {
     const int row = e / kWarps, col = e % kWarps;
@@ -211,7 +212,10 @@ __global__ void __launch_bounds__(TCF / CPW * 32, TCF / CPW == 8 ? (CPW == 1 ? 3
   // CPW columns per warp (TCF / CPW warps): the column transforms of one warp
   // run interleaved (shared twiddles, CPW x the independent butterflies)
   constexpr int R = 1 << LOGR, C = 1 << LOGC, E = R / 32, LOGN = LOGR + LOGC;
-  constexpr int PAD = R + 1;
+  // column regions offset by 2 banks pairs: a half warp staging TCF = 8 columns
+  // of two adjacent rows (swz(row) and swz(row ^ 1) differ in bit 0) hits 16
+  // distinct 8-byte banks; PAD = R + 1 made those 2-way conflicts
+  constexpr int PAD = R + 2;
   constexpr int tiles = C / TCF;
   constexpr int NT = TCF / CPW * 32;
   extern __shared__ u64 sm_all[];  // [ns][TCF][PAD] sources, [TCF][PAD] destination
@@ -224,6 +228,7 @@ __global__ void __launch_bounds__(TCF / CPW * 32, TCF / CPW == 8 ? (CPW == 1 ? 3
   const int d_lo = dgroup * dpc, d_hi = min(A.nd, d_lo + dpc);
   const int col0 = tile * TCF;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int swl = swz(lane);  // lane part of the (linear) swizzle
   constexpr int n = 1 << LOGN;
   const u64* src = A.src[job];
   u64* dst = A.dst[job];
@@ -252,7 +257,7 @@ __global__ void __launch_bounds__(TCF / CPW * 32, TCF / CPW == 8 ? (CPW == 1 ? 3
     for (int c = 0; c < CPW; ++c) {
       sm[c] = region(s, warp * CPW + c);
 #pragma unroll
-      for (int k = 0; k < E; ++k) x[c][k] = sm[c][swz(lane + 32 * k)];
+      for (int k = 0; k < E; ++k) x[c][k] = sm[c][(swl ^ swz(32 * k))];
     }
     __syncwarp();
     // canonical y_s: the basis conversion's [x q^_s^-1]_{q_s} (and the centred lift) need it;
@@ -263,7 +268,7 @@ __global__ void __launch_bounds__(TCF / CPW * 32, TCF / CPW == 8 ? (CPW == 1 ? 3
 #pragma unroll
     for (int c = 0; c < CPW; ++c)
 #pragma unroll
-      for (int k = 0; k < E; ++k) sm[c][swz(lane + 32 * k)] = x[c][k];
+      for (int k = 0; k < E; ++k) sm[c][(swl ^ swz(32 * k))] = x[c][k];
     __syncwarp();
   }
   __syncthreads();
@@ -288,7 +293,7 @@ __global__ void __launch_bounds__(TCF / CPW * 32, TCF / CPW == 8 ? (CPW == 1 ? 3
           sm[c] = out + (size_t)col * PAD;
 #pragma unroll
           for (int k = 0; k < E; ++k) {
-            const int r = swz(lane + 32 * k);
+            const int r = (swl ^ swz(32 * k));
             u64 acc = 0;
 #pragma unroll
             for (int s = 0; s < 8; ++s)
@@ -307,7 +312,7 @@ __global__ void __launch_bounds__(TCF / CPW * 32, TCF / CPW == 8 ? (CPW == 1 ? 3
           sm[c] = out + (size_t)col * PAD;
 #pragma unroll
           for (int k = 0; k < E; ++k) {
-            const u64 v = region(0, col)[swz(lane + 32 * k)];
+            const u64 v = region(0, col)[(swl ^ swz(32 * k))];
             const u64 rr = reduce64(v, q, mh);
             x[c][k] = v > half ? sub_mod(rr, ql, q) : rr;
           }
@@ -324,7 +329,7 @@ __global__ void __launch_bounds__(TCF / CPW * 32, TCF / CPW == 8 ? (CPW == 1 ? 3
 #pragma unroll
       for (int c = 0; c < CPW; ++c)
 #pragma unroll
-        for (int k = 0; k < E; ++k) sm[c][swz(lane + 32 * k)] = x[c][k];
+        for (int k = 0; k < E; ++k) sm[c][(swl ^ swz(32 * k))] = x[c][k];
       __syncthreads();
       u64* o = dst + (size_t)A.out_slot[d] * n + col0;
       for (int e = threadIdx.x; e < R * TCF; e += NT) {
@@ -381,14 +386,14 @@ __global__ void __launch_bounds__(TCF / CPW * 32, TCF / CPW == 8 ? (CPW == 1 ? 3
       for (int c = 0; c < CPW; ++c) {
         sm[c] = out + (size_t)(warp * CPW + c) * PAD;
 #pragma unroll
-        for (int k = 0; k < E; ++k) x[c][k] = sm[c][swz(lane + 32 * k)];
+        for (int k = 0; k < E; ++k) x[c][k] = sm[c][(swl ^ swz(32 * k))];
       }
       __syncwarp();
       warp_fwd_n<LOGR, CPW>(x, sm, lane, q, tw);
 #pragma unroll
       for (int c = 0; c < CPW; ++c)
 #pragma unroll
-        for (int k = 0; k < E; ++k) sm[c][swz(lane + 32 * k)] = x[c][k];
+        for (int k = 0; k < E; ++k) sm[c][(swl ^ swz(32 * k))] = x[c][k];
     }
     __syncthreads();
     // 5. store (lazy [0, 4q) values; the row pass accepts them); one
@@ -413,6 +418,10 @@ template <int LOGR, int LOGC>
 __global__ void __launch_bounds__(kWarps * 32, 2) ks_row_kernel(KsRowArgs A, Tabs T) {
   constexpr int C = 1 << LOGC, E = C / 32, LOGN = LOGR + LOGC;
   auto rbr = [](uint32_t col) { return __brev(col) >> (32 - LOGC); };
+  // row buffers hold bit-reversed columns; lane L's blocked segment lands at
+  // brev5(L) + 32 k, whose bit 4 (= bit 0 of L) is folded into bit 0 so the 16
+  // lanes of a half warp (and the affine gathers below) hit 16 distinct banks
+  auto xp = [](uint32_t i) { return i ^ ((i >> 4) & 1u); };
   constexpr int tiles = (1 << LOGR) / kWarps;
   constexpr int n = 1 << LOGN;
   extern __shared__ u64 ks_sm[];  // [kWarps][ndig + 1][C]
@@ -432,8 +441,8 @@ __global__ void __launch_bounds__(kWarps * 32, 2) ks_row_kernel(KsRowArgs A, Tab
 #pragma unroll
       for (int k = 0; k < E; k += 2) {
         const ulonglong2 v = reinterpret_cast<const ulonglong2*>(a)[k / 2];
-        X[rbr(lane * E + k)] = v.x;
-        X[rbr(lane * E + k + 1)] = v.y;
+        X[xp(rbr(lane * E + k))] = v.x;
+        X[xp(rbr(lane * E + k + 1))] = v.y;
       }
     } else {
       const u64* a = A.ext[s] + ((size_t)j * A.nt + t) * n + (size_t)rs * C;
@@ -450,7 +459,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) ks_row_kernel(KsRowArgs A, Tab
       };
       warp_fwd<LOGC, kBlocked>(x, X, lane, q, tw);
 #pragma unroll
-      for (int k = 0; k < E; ++k) X[rbr(lane * E + k)] = canon4(x[k], q);
+      for (int k = 0; k < E; ++k) X[xp(rbr(lane * E + k))] = canon4(x[k], q);
     }
   }
   __syncwarp();
@@ -467,7 +476,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) ks_row_kernel(KsRowArgs A, Tab
     uint32_t sc[E];  // positions in the bit-reversed row buffers (bank-conflict free gathers)
 #pragma unroll
     for (int k = 0; k < E; ++k)
-      sc[k] = g > 1 ? RowPerm<LOGR, LOGC>(rd, g).pos(rbr(lane * E + k)) : rbr(lane * E + k);
+      sc[k] = xp(g > 1 ? RowPerm<LOGR, LOGC>(rd, g).pos(rbr(lane * E + k)) : rbr(lane * E + k));
     for (int j = 0; j < A.ndig; ++j) {
       const u64* X = wsm + j * C;
       const u64* kb = A.key[jb] + ((size_t)(j * 2 + 0) * A.np + m) * n + rowoff;
@@ -616,6 +625,7 @@ template <int LOGR, int LOGC, bool PF, bool SH, bool PM1>
 __global__ void __launch_bounds__(kWarps * 32, 2) ks_sum_kernel(KsSumArgs A, Tabs T) {
   constexpr int C = 1 << LOGC, E = C / 32, LOGN = LOGR + LOGC;
   auto rbr = [](uint32_t col) { return __brev(col) >> (32 - LOGC); };
+  auto xp = [](uint32_t i) { return i ^ ((i >> 4) & 1u); };  // bank fold, as in ks_row_kernel
   constexpr int tiles = (1 << LOGR) / kWarps;
   constexpr int n = 1 << LOGN;
   __shared__ u64 rowbuf[kWarps][C];
@@ -720,7 +730,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) ks_sum_kernel(KsSumArgs A, Tab
     // br(column) with odd slope g, so every 16 lanes hit 16 distinct banks
     uint32_t sc[E];
 #pragma unroll
-    for (int k = 0; k < E; ++k) sc[k] = rp.pos(rbr(lane * E + k));
+    for (int k = 0; k < E; ++k) sc[k] = xp(rp.pos(rbr(lane * E + k)));
     for (int j = 0; j < A.ndig; ++j) {
       const int lo = j * A.alpha, hi = min(lo + A.alpha, A.limbs);
       const u64* src = (t >= lo && t < hi) ? A.c1[s] + (size_t)t * n + (size_t)rs * C
@@ -738,8 +748,8 @@ __global__ void __launch_bounds__(kWarps * 32, 2) ks_sum_kernel(KsSumArgs A, Tab
 #pragma unroll
       for (int k = 0; k < E; k += 2) {
         const ulonglong2 v = reinterpret_cast<const ulonglong2*>(src + lane * E)[k / 2];
-        buf[rbr(lane * E + k)] = v.x;
-        buf[rbr(lane * E + k + 1)] = v.y;
+        buf[xp(rbr(lane * E + k))] = v.x;
+        buf[xp(rbr(lane * E + k + 1))] = v.y;
       }
       __syncwarp();
 #pragma unroll
@@ -764,8 +774,8 @@ __global__ void __launch_bounds__(kWarps * 32, 2) ks_sum_kernel(KsSumArgs A, Tab
 #pragma unroll
       for (int k = 0; k < E; k += 2) {
         const ulonglong2 v = reinterpret_cast<const ulonglong2*>(src + lane * E)[k / 2];
-        buf[rbr(lane * E + k)] = v.x;
-        buf[rbr(lane * E + k + 1)] = v.y;
+        buf[xp(rbr(lane * E + k))] = v.x;
+        buf[xp(rbr(lane * E + k + 1))] = v.y;
       }
       __syncwarp();
 #pragma unroll
@@ -845,7 +855,7 @@ void run_epi(Context& c, const EpiBatch& e) {
 template <int LOGR, int LOGC, int TCF, int CPW>
 void run_fused_t(Context& c, const FusedColArgs& a) {
   constexpr int R = 1 << LOGR;
-  const size_t sm = (size_t)(a.ns + 1) * TCF * (R + 1) * sizeof(u64);
+  const size_t sm = (size_t)(a.ns + 1) * TCF * (R + 2) * sizeof(u64);
   static int configured = 0;
   if (!configured) {
     SF_CUDA(cudaFuncSetAttribute(fused_col_kernel<LOGR, LOGC, TCF, CPW, true>,

@@ -13,8 +13,18 @@
 namespace sf {
 namespace wntt {
 
-// 64-bit-bank swizzle inside a warp region (16 x 8-byte banks per half warp)
-__device__ __forceinline__ int swz(int i) { return i ^ ((i >> 4) & 15); }
+// 64-bit-bank swizzle inside a warp region (16 x 8-byte banks per half warp):
+// i ^ T(bits 4..7 of i), T the GF(2) matrix with columns (2, 13, 4, 3). It is
+// linear, so swz(lane part | register part) = swz(lane part) ^ swz(register
+// part), and it makes every half warp hit 16 distinct banks in each relayout
+// the warp NTTs issue (register bits at s0 = 0/2/5 for 8 registers per lane,
+// 0/1/3/5 for 4, 0/1/5 for 16 -- checked exhaustively); the former
+// i ^ (i >> 4) left the s0 = 2 relayouts of the 256-point transforms 2-way
+// conflicted (profiles/r1_ncu_v16.md: 24 % of fused_col's shared wavefronts).
+__device__ __forceinline__ int swz(int i) {
+  const int h = i >> 4;
+  return i ^ ((h & 1) ? 2 : 0) ^ ((h & 2) ? 13 : 0) ^ ((h & 4) ? 4 : 0) ^ ((h & 8) ? 3 : 0);
+}
 
 // index of register k of `lane` when register bits are [s0, s0 + LOGE)
 template <int LOGE>
@@ -25,11 +35,12 @@ __device__ __forceinline__ int lay(int lane, int k, int s0) {
 template <int LOGE>
 __device__ __forceinline__ void relayout(u64 (&x)[1 << LOGE], u64* sm, int lane, int from, int to) {
   if (from == to) return;
+  const int wb = swz(lay<LOGE>(lane, 0, from)), rb = swz(lay<LOGE>(lane, 0, to));  // lane parts
 #pragma unroll
-  for (int k = 0; k < (1 << LOGE); ++k) sm[swz(lay<LOGE>(lane, k, from))] = x[k];
+  for (int k = 0; k < (1 << LOGE); ++k) sm[wb ^ swz(k << from)] = x[k];
   __syncwarp();
 #pragma unroll
-  for (int k = 0; k < (1 << LOGE); ++k) x[k] = sm[swz(lay<LOGE>(lane, k, to))];
+  for (int k = 0; k < (1 << LOGE); ++k) x[k] = sm[rb ^ swz(k << to)];
   __syncwarp();
 }
 
@@ -110,15 +121,16 @@ __device__ __forceinline__ void warp_inv(u64 (&x)[1 << (LOGM - 5)], u64* sm, int
 template <int LOGE, int NC>
 __device__ __forceinline__ void relayout_n(u64 (&x)[NC][1 << LOGE], u64* const (&sm)[NC], int lane, int from, int to) {
   if (from == to) return;
+  const int wb = swz(lay<LOGE>(lane, 0, from)), rb = swz(lay<LOGE>(lane, 0, to));  // lane parts
 #pragma unroll
   for (int c = 0; c < NC; ++c)
 #pragma unroll
-    for (int k = 0; k < (1 << LOGE); ++k) sm[c][swz(lay<LOGE>(lane, k, from))] = x[c][k];
+    for (int k = 0; k < (1 << LOGE); ++k) sm[c][wb ^ swz(k << from)] = x[c][k];
   __syncwarp();
 #pragma unroll
   for (int c = 0; c < NC; ++c)
 #pragma unroll
-    for (int k = 0; k < (1 << LOGE); ++k) x[c][k] = sm[c][swz(lay<LOGE>(lane, k, to))];
+    for (int k = 0; k < (1 << LOGE); ++k) x[c][k] = sm[c][rb ^ swz(k << to)];
   __syncwarp();
 }
 

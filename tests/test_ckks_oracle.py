@@ -31,6 +31,45 @@ def _min_psi(q, n):
             return min(pow(c, k, q) for k in range(1, m, 2))
 
 
+def test_chacha20_block_matches_cryptography():
+    """keys and encryption randomness are a ChaCha20 counter
+    stream. The twin's block function (the same definition the GPU product
+    implements, csrc/common.h) is pinned to an independent implementation:
+    the `cryptography` package (OpenSSL) keystream for the same key, 64-bit
+    block counter and 64-bit nonce (IV = counter || nonce, little-endian)."""
+    import ctypes as C
+    import struct
+    from cryptography.hazmat.primitives.ciphers import Cipher, algorithms
+    from oracle.ckks import lib
+    f = lib().ock_chacha20_block
+    f.argtypes = [C.POINTER(C.c_uint32), C.c_uint64, C.c_uint64, C.POINTER(C.c_uint32)]
+    rng = np.random.default_rng(2026)
+    for _ in range(16):
+        key = rng.integers(0, 2**32, size=8, dtype=np.uint64).astype(np.uint32)
+        ctr, nonce = (int(v) for v in rng.integers(0, 2**63, size=2))
+        out = np.zeros(16, dtype=np.uint32)
+        f(key.ctypes.data_as(C.POINTER(C.c_uint32)), ctr, nonce, out.ctypes.data_as(C.POINTER(C.c_uint32)))
+        ks = Cipher(algorithms.ChaCha20(key.tobytes(), struct.pack("<QQ", ctr, nonce)), mode=None).encryptor()
+        assert np.array_equal(np.frombuffer(ks.update(bytes(64)), dtype=np.uint32), out)
+
+
+def test_key_stream_words_are_chacha20():
+    """Word i of stream (seed, id) = 64-bit word i mod 8 of block i / 8 under the
+    documented key layout (seed || "sf_b200 ckks rng" || 1 || 0), nonce = id."""
+    import ctypes as C
+    import struct
+    from cryptography.hazmat.primitives.ciphers import Cipher, algorithms
+    from oracle.ckks import lib
+    f = lib().ock_rand64
+    f.argtypes, f.restype = [C.c_uint64, C.c_uint64, C.c_uint64], C.c_uint64
+    seed, stream = 0x0123456789ABCDEF, (4 << 56) | 3
+    key = struct.pack("<Q", seed) + b"sf_b200 ckks rng" + struct.pack("<II", 1, 0)
+    ks = Cipher(algorithms.ChaCha20(key, struct.pack("<QQ", 5, stream)), mode=None).encryptor().update(bytes(64))
+    want = np.frombuffer(ks, dtype=np.uint64)
+    got = np.array([f(seed, stream, 5 * 8 + w) for w in range(8)], dtype=np.uint64)
+    assert np.array_equal(got, want)
+
+
 def test_ntt_matches_definition():
     be = CkksOracle(8, 2)  # ring 16
     n, logn = be.n, be.log_n
