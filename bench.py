@@ -453,6 +453,71 @@ def cpu_baseline_sample():
         return {"value": None, "unit": "ms/token", "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
 
 
+def token_stream(be, sf, layer, T=16):
+    """A real decode stream through the public API: T consecutive tokens at
+    positions 2047, 2048, ... (n' grows 2047 -> 2047 + T): every token refills
+    the six stage inputs from pinned host words (H2D), runs Q/K/V with the K/V
+    plans of its lane offset pos mod t (vmm.cpp:66-83 out_offset), RoPE at its
+    own position (the three RoPE plaintexts are encoded on the host on first use
+    -- inside the timed region), appends k and v to the persistent cache (a new
+    K-ct every t tokens, a third V group and score map at n' = 2049), QK^T and
+    Score*V over the grown cache, the output / up / gate / down projections, and
+    reads the attention and down-projection outputs back (D2H). Eager (the cache
+    changes shape every token, so no single graph fits). Wall clock per token,
+    synchronised by the read-back."""
+    t = layer.cfg.t
+    mk = lambda off: sf.VmmPlan(be, None, D, D, LEVELS["qkv"], 0, off, True)  # noqa: E731
+    wk = {o: (layer.wk if o == layer.pos % t else mk(o)) for o in range(t)}
+    wv = {o: (layer.wv if o == layer.pos % t else mk(o)) for o in range(t)}
+    gt = layer.cfg.group_tokens
+    pmap = np.zeros(SLOTS)
+    for h in range(H):
+        pmap[h * gt:(h + 1) * gt] = 1.0 / (NP + T)
+    probs = [be.encrypt(pmap, LEVELS["probs"], seed=700 + i) for i in range(3)]
+    import torch
+    host_in = []
+    for c in layer.inputs[:4]:
+        w = c.data()
+        tt = torch.empty(w.shape, dtype=torch.uint64 if hasattr(torch, "uint64") else torch.int64, pin_memory=True)
+        a = tt.numpy().view(np.uint64)
+        a[...] = w
+        host_in.append((a, tt))
+    x, h7, h3, h1 = layer.inputs[:4]
+    cache = layer.cache
+    be.synchronize()
+    per_token = []
+    be.event_record(20)
+    t0 = time.perf_counter()
+    for i in range(T):
+        ti = time.perf_counter()
+        pos = layer.pos + i
+        for slot, (w, _) in zip(layer.inputs[:4], host_in):
+            be.refill(slot, w)
+        o = pos % t
+        q, k, v = sf.vmm_interleaved_multi(be, x, [layer.wq, wk[o], wv[o]])
+        qr = sf.rope_apply(be, q, layer.cfg, pos)
+        kr = sf.rope_apply(be, k, layer.cfg, pos)
+        cache = sf.v_append(be, cache, sf.make_v_pieces(be, cache, v, pos))
+        cache = sf.k_append(be, cache, kr)
+        maps = sf.qk_dot(be, qr, cache)
+        att = sf.softmax_times_v(be, probs[:len(maps)], cache)
+        sf.vmm_interleaved(be, h7, None, plan=layer.wo)
+        sf.vmm_interleaved_multi(be, h3, [layer.wg, layer.wu])
+        dn = sf.vmm_interleaved(be, h1, None, plan=layer.wd)
+        res = [att.data(), dn.data()]  # D2H: synchronises the token
+        per_token.append((time.perf_counter() - ti) * 1e3)
+    be.event_record(21)
+    wall = (time.perf_counter() - t0) * 1e3 / T
+    dev = be.event_elapsed_ms(20, 21) / T
+    return {"value": round(wall, 3), "unit": "ms/token", "tokens": T, "n_prime": [NP - 1, NP - 1 + T],
+            "device_ms_per_token": round(dev, 3), "first_token_ms": round(per_token[0], 3),
+            "median_token_ms": round(float(np.median(per_token)), 3),
+            "h2d_bytes_per_token": int(sum(w.nbytes for w, _ in host_in)),
+            "d2h_bytes_per_token": int(sum(r.nbytes for r in res)),
+            "maps_at_end": len(maps), "k_cts_at_end": cache.n_prime // t + (1 if cache.n_prime % t else 0),
+            "execution": "eager (host-issued); cache persists and grows; RoPE plaintexts encoded per position"}
+
+
 def emulated_shards(be, sf, layer, steps, worlds=(2, 4, 8)):
     """Predicted strong scaling of ONE token over N GPUs, measured on this one:
     for every rank r of a world W, the rank's own work -- its partials (VMM giant
@@ -906,6 +971,7 @@ def main():
                     help="with --shard: NCCL all-gather on the library stream instead of the peer-memory exchange")
     ap.add_argument("--no-extras", action="store_true",
                     help="only the headline step (skip C1/C2/C3/C5, prefill and nonlinearity lines)")
+    ap.add_argument("--no-stream", action="store_true", help="skip the T-token decode stream (e2e_stream)")
     ap.add_argument("--no-sweep", action="store_true", help="skip the reduced C5 NTT / key-switch sweep")
     ap.add_argument("--no-emulate", action="store_true",
                     help="skip the emulated per-rank timings of worlds 2/4/8 (N=1 only)")
@@ -1125,6 +1191,12 @@ def main():
         e2e_ms = reduce_ranks(dist, e2e_ms, dist.ReduceOp.MAX)
 
     phases = layer.phase_ms(args.steps)  # last: its graph's memory must not disturb the timed graph
+    stream = None
+    if not args.no_stream:
+        try:
+            stream = token_stream(be, sf, layer, max(16, args.steps))
+        except Exception as e:  # pragma: no cover
+            stream = {"error": str(e)}
     emu = None
     if world == 1 and not args.no_emulate:
         try:
@@ -1192,6 +1264,7 @@ def main():
         "emulated_sharding": emu,
         "e2e": {"value": round(e2e_ms / world, 3), "unit": "ms/token", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "breakdown": e2e_parts},
+        "e2e_stream": stream,
         "gpu_launches": int(launches),
         "host_issue_ms_per_step": round(t_host, 3),
         "eager_ms_per_step": round(ms_eager, 3),
