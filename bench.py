@@ -483,7 +483,9 @@ def token_stream(be, sf, layer, T=16):
         a[...] = w
         host_in.append((a, tt))
     x, h7, h3, h1 = layer.inputs[:4]
-    cache = layer.cache
+    # the same cache (n' = 2047) under a config with room for the T new tokens
+    cfg = sf.AttentionConfig(SLOTS, D, H, 0, NP + T)
+    cache = sf.kv_from_cts(be, cfg, layer.cache.n_prime, layer.cache.k_cts, layer.cache.v_cts)
     be.synchronize()
     per_token = []
     be.event_record(20)
@@ -495,8 +497,8 @@ def token_stream(be, sf, layer, T=16):
             be.refill(slot, w)
         o = pos % t
         q, k, v = sf.vmm_interleaved_multi(be, x, [layer.wq, wk[o], wv[o]])
-        qr = sf.rope_apply(be, q, layer.cfg, pos)
-        kr = sf.rope_apply(be, k, layer.cfg, pos)
+        qr = sf.rope_apply(be, q, cfg, pos)
+        kr = sf.rope_apply(be, k, cfg, pos)
         cache = sf.v_append(be, cache, sf.make_v_pieces(be, cache, v, pos))
         cache = sf.k_append(be, cache, kr)
         maps = sf.qk_dot(be, qr, cache)
@@ -1054,6 +1056,11 @@ def main():
             dist.barrier()
 
     # ---- eager reference timing (host-issued step, for the record)
+    hprof = None
+    if os.environ.get("SF_HOST_PROF"):
+        import ctypes as C
+        buf = C.create_string_buffer(1 << 16)
+        sf._native.lib().sf_host_profile(buf, len(buf), 1)  # reset: count only the timed eager steps
     be.ledger.reset()
     barrier()
     be.synchronize()
@@ -1066,6 +1073,11 @@ def main():
     ms_eager = be.event_elapsed_ms(0, 1) / args.steps
     counts = be.ledger.totals()
     be.synchronize()
+    if os.environ.get("SF_HOST_PROF"):  # host time per internal scope over the eager steps (diagnostics)
+        sf._native.lib().sf_host_profile(buf, len(buf), 1)
+        rows = [l.rsplit(" ", 2) for l in buf.value.decode().splitlines() if l.strip()]
+        hprof = {k: {"us_per_step": round(float(us) / args.steps, 1), "calls_per_step": int(n) // args.steps}
+                 for k, us, n in sorted(rows, key=lambda r: -float(r[1]))[:25]}
 
     # ---- capture the decode step once into a CUDA graph (nothing runs during
     # the capture); every replay re-executes all of the step's kernels
@@ -1267,6 +1279,7 @@ def main():
         "e2e_stream": stream,
         "gpu_launches": int(launches),
         "host_issue_ms_per_step": round(t_host, 3),
+        "host_profile": hprof,
         "eager_ms_per_step": round(ms_eager, 3),
         "execution": f"CUDA graph of the whole decode step ({graph.kernel_launches} kernels), replayed per token",
         "clocks": clk.summary(),

@@ -22,6 +22,8 @@ struct sf_vmm_plan {
 };
 struct sf_graph {
   sf_context* ctx = nullptr;
+  sf::Context* cp = nullptr;  // the context and its generation (sf_graph_destroy may run after it died)
+  sf::u64 gen = 0;
   cudaGraph_t g = nullptr;
   cudaGraphExec_t x = nullptr;
   long long launches = 0;  // library kernels per replay
@@ -876,6 +878,8 @@ sf_status sf_graph_capture_end(sf_context* ctx, sf_graph** out) {
     sf::require(c.capturing, sf::kInvalidTarget, "no graph capture in progress");
     auto g = std::make_unique<sf_graph>();
     g->ctx = ctx;
+    g->cp = ctx->c.get();
+    g->gen = ctx->c->gen;
     const cudaError_t e = cudaStreamEndCapture(c.stream, &g->g);
     c.capturing = false;
     g->deferred.swap(c.capture_deferred);
@@ -915,19 +919,21 @@ long long sf_graph_kernel_launches(const sf_graph* g) { return g ? g->launches :
 
 void sf_graph_destroy(sf_graph* g) {
   if (!g) return;
-  auto& c = *g->ctx->c;
-  cudaStreamSynchronize(c.stream);
+  const bool alive = sf::context_alive(g->cp, g->gen);
+  cudaStream_t st = alive ? g->cp->stream : nullptr;
+  if (alive) cudaStreamSynchronize(st);
   if (g->x) cudaGraphExecDestroy(g->x);
   if (g->g) cudaGraphDestroy(g->g);
-  for (auto& d : g->deferred) cudaFreeAsync(d.first, c.stream);
+  auto free_ = [&](sf::u64* p) { alive ? (void)cudaFreeAsync(p, st) : (void)cudaFree(p); };
+  for (auto& d : g->deferred) free_(d.first);
   {
     std::lock_guard<std::mutex> lk(g->gm->mu);
     g->gm->destroyed = true;
     if (g->gm->launched)
-      for (sf::u64* p : g->gm->dead) cudaFreeAsync(p, c.stream);  // outstanding allocations of dead Bufs
+      for (sf::u64* p : g->gm->dead) free_(p);  // outstanding allocations of dead Bufs
     g->gm->dead.clear();
   }
-  cudaStreamSynchronize(c.stream);
+  if (alive) cudaStreamSynchronize(st);
   delete g;
 }
 

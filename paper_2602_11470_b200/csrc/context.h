@@ -38,6 +38,7 @@ struct Buf {
   u64* p = nullptr;
   size_t words = 0;
   Context* ctx = nullptr;
+  u64 gen = 0;  // the context's generation: a Buf outliving its context frees itself directly
   std::shared_ptr<GraphMem> gm;  // set: allocated while capturing that graph (a graph memory node)
   Buf(Context* c, size_t w);
   ~Buf();
@@ -155,7 +156,13 @@ struct ProfRec {
   double bfly;  // radix-2 NTT butterflies the launch executes (0 for non-NTT kernels)
 };
 
+// Live-context registry: handles (ciphertexts, plans, caches, graphs) may be
+// released after their context (e.g. a garbage-collected cycle that finalises
+// the context first); their buffers then bypass the dead context.
+bool context_alive(const Context* c, u64 gen);
+
 struct Context {
+  u64 gen = 0;  // unique per context (context_alive)
   // profiling
   int prof_mask = 0;
   std::vector<ProfRec> prof_recs;

@@ -11,6 +11,7 @@
 #include <cstring>
 #include <functional>
 #include <thread>
+#include <unordered_map>
 
 #include <cstdlib>
 
@@ -23,7 +24,18 @@ void build_host_tables(Context& c, std::vector<u64>& psi, std::vector<u64>& psi_
                        std::vector<u64>& ipsi_s, std::vector<u64>& ninv, std::vector<u64>& ninv_s);
 
 // ------------------------------------------------------------------ memory
-Buf::Buf(Context* c, size_t w) : words(w), ctx(c) {
+namespace {
+std::mutex g_live_mu;
+std::unordered_map<const Context*, u64> g_live;
+std::atomic<u64> g_next_gen{1};
+}  // namespace
+bool context_alive(const Context* c, u64 gen) {
+  std::lock_guard<std::mutex> lk(g_live_mu);
+  auto it = g_live.find(c);
+  return it != g_live.end() && it->second == gen;
+}
+
+Buf::Buf(Context* c, size_t w) : words(w), ctx(c), gen(c->gen) {
   SF_HPROF("cudaMallocAsync");
   if (c->capturing) gm = c->capture_gm;
   if (!w) return;
@@ -42,6 +54,10 @@ Buf::Buf(Context* c, size_t w) : words(w), ctx(c) {
 Buf::~Buf() {
   SF_HPROF("cudaFreeAsync");
   if (!p) return;
+  if (!context_alive(ctx, gen)) {  // released after its context: no stream, no free lists
+    cudaFree(p);
+    return;
+  }
   if (gm) {  // a graph memory node
     if (ctx->capturing && ctx->capture_gm == gm) {
       cudaFreeAsync(p, ctx->stream);  // allocated and freed inside the same capture: a free node
@@ -88,6 +104,10 @@ Context::~Context() {
   for (auto& [w, v] : free_bufs)
     for (u64* q : v) cudaFreeAsync(q, stream);
   free_bufs.clear();
+  {  // from here on, buffers still referenced elsewhere free themselves (Buf::~Buf)
+    std::lock_guard<std::mutex> lk(g_live_mu);
+    g_live.erase(this);
+  }
   if (stream) {
     cudaStreamSynchronize(stream);
     cudaStreamDestroy(stream);
@@ -104,6 +124,11 @@ std::unique_ptr<Context> make_context(int slots, int L, int log_n, int alpha, in
   require(is_pow2(slots), kShapeMismatch, "engine: N must be a power of two");
   require(L >= 1, kInvalidTarget, "engine: level budget L must be >= 1");
   auto c = std::make_unique<Context>();
+  c->gen = g_next_gen.fetch_add(1);
+  {
+    std::lock_guard<std::mutex> lk(g_live_mu);
+    g_live[c.get()] = c->gen;
+  }
   c->slots = slots;
   c->L = L;
   c->logn = log_n > 0 ? log_n : std::max(2, log2_exact(2LL * slots));

@@ -457,7 +457,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) ks_row_kernel(KsRowArgs A, Tab
         w = W[i];
         ws = Ws[i];
       };
-      warp_fwd<LOGC, kBlocked>(x, X, lane, q, tw);
+      warp_fwd<LOGC, kBlocked, decltype(tw), false>(x, X, lane, q, tw);
 #pragma unroll
       for (int k = 0; k < E; ++k) X[xp(rbr(lane * E + k))] = canon4(x[k], q);
     }
@@ -528,8 +528,8 @@ __global__ void __launch_bounds__(kWarps * 32, 2) ks_row_kernel(KsRowArgs A, Tab
         w = W[i];
         ws = Ws[i];
       };
-      warp_inv<LOGC, kBlocked>(vb, scratch, lane, q, tw);
-      warp_inv<LOGC, kBlocked>(va, scratch, lane, q, tw);
+      warp_inv<LOGC, kBlocked, decltype(tw), false>(vb, scratch, lane, q, tw);
+      warp_inv<LOGC, kBlocked, decltype(tw), false>(va, scratch, lane, q, tw);
 #pragma unroll
       for (int k = 0; k < E; ++k) {
         accb[(size_t)rd * C + lane + 32 * k] = vb[k];

@@ -25,6 +25,12 @@ __device__ __forceinline__ int swz(int i) {
   const int h = i >> 4;
   return i ^ ((h & 1) ? 2 : 0) ^ ((h & 2) ? 13 : 0) ^ ((h & 4) ? 4 : 0) ^ ((h & 8) ? 3 : 0);
 }
+// the round-1 swizzle (2-way conflicted at s0 = 2, but cheaper to address):
+// kept for the register-starved key-switch row stage, where the conflict-free
+// form's extra address registers spill (ks_row_kernel at 128 registers)
+__device__ __forceinline__ int swz1(int i) { return i ^ ((i >> 4) & 15); }
+template <bool XS>
+__device__ __forceinline__ int swzx(int i) { return XS ? swz(i) : swz1(i); }
 
 // index of register k of `lane` when register bits are [s0, s0 + LOGE)
 template <int LOGE>
@@ -32,15 +38,15 @@ __device__ __forceinline__ int lay(int lane, int k, int s0) {
   return (lane & ((1 << s0) - 1)) | (k << s0) | ((lane >> s0) << (s0 + LOGE));
 }
 
-template <int LOGE>
+template <int LOGE, bool XS = true>
 __device__ __forceinline__ void relayout(u64 (&x)[1 << LOGE], u64* sm, int lane, int from, int to) {
   if (from == to) return;
-  const int wb = swz(lay<LOGE>(lane, 0, from)), rb = swz(lay<LOGE>(lane, 0, to));  // lane parts
+  const int wb = swzx<XS>(lay<LOGE>(lane, 0, from)), rb = swzx<XS>(lay<LOGE>(lane, 0, to));  // lane parts
 #pragma unroll
-  for (int k = 0; k < (1 << LOGE); ++k) sm[wb ^ swz(k << from)] = x[k];
+  for (int k = 0; k < (1 << LOGE); ++k) sm[wb ^ swzx<XS>(k << from)] = x[k];
   __syncwarp();
 #pragma unroll
-  for (int k = 0; k < (1 << LOGE); ++k) x[k] = sm[rb ^ swz(k << to)];
+  for (int k = 0; k < (1 << LOGE); ++k) x[k] = sm[rb ^ swzx<XS>(k << to)];
   __syncwarp();
 }
 
@@ -52,7 +58,7 @@ enum : int { kStrided = 0, kBlocked = 1 };
 // Forward sub-NTT (Cooley-Tukey). Entry layout: strided. Exit layout: EXIT.
 // tw(b, blk, w, ws) gives the twiddle (and Shoup companion) of the stage with
 // butterfly distance 2^b for block blk.
-template <int LOGM, int EXIT = kStrided, class TW>
+template <int LOGM, int EXIT = kStrided, class TW, bool XS = true>
 __device__ __forceinline__ void warp_fwd(u64 (&x)[1 << (LOGM - 5)], u64* sm, int lane, u64 q, const TW& tw) {
   constexpr int LOGE = LOGM - 5;
   constexpr int E = 1 << LOGE;
@@ -61,7 +67,7 @@ __device__ __forceinline__ void warp_fwd(u64 (&x)[1 << (LOGM - 5)], u64* sm, int
 #pragma unroll
   for (int hi = LOGM; hi > 0; hi -= LOGE) {
     const int lo = hi - LOGE > 0 ? hi - LOGE : 0;
-    relayout<LOGE>(x, sm, lane, s0, lo);
+    relayout<LOGE, XS>(x, sm, lane, s0, lo);
     s0 = lo;
 #pragma unroll
     for (int b = hi - 1; b >= lo; --b) {
@@ -80,11 +86,11 @@ __device__ __forceinline__ void warp_fwd(u64 (&x)[1 << (LOGM - 5)], u64* sm, int
       }
     }
   }
-  relayout<LOGE>(x, sm, lane, s0, EXIT == kBlocked ? 0 : LOGM - LOGE);
+  relayout<LOGE, XS>(x, sm, lane, s0, EXIT == kBlocked ? 0 : LOGM - LOGE);
 }
 
 // Inverse sub-NTT (Gentleman-Sande). Entry layout: ENTRY. Exit layout: strided.
-template <int LOGM, int ENTRY = kStrided, class TW>
+template <int LOGM, int ENTRY = kStrided, class TW, bool XS = true>
 __device__ __forceinline__ void warp_inv(u64 (&x)[1 << (LOGM - 5)], u64* sm, int lane, u64 q, const TW& tw) {
   constexpr int LOGE = LOGM - 5;
   constexpr int E = 1 << LOGE;
@@ -94,7 +100,7 @@ __device__ __forceinline__ void warp_inv(u64 (&x)[1 << (LOGM - 5)], u64* sm, int
   for (int lo = 0; lo < LOGM; lo += LOGE) {
     const int hi = lo + LOGE < LOGM ? lo + LOGE : LOGM;
     const int ns0 = hi - LOGE > 0 ? hi - LOGE : 0;
-    relayout<LOGE>(x, sm, lane, s0, ns0);
+    relayout<LOGE, XS>(x, sm, lane, s0, ns0);
     s0 = ns0;
 #pragma unroll
     for (int b = lo; b < hi; ++b) {
@@ -112,7 +118,7 @@ __device__ __forceinline__ void warp_inv(u64 (&x)[1 << (LOGM - 5)], u64* sm, int
       }
     }
   }
-  relayout<LOGE>(x, sm, lane, s0, LOGM - LOGE);
+  relayout<LOGE, XS>(x, sm, lane, s0, LOGM - LOGE);
 }
 
 // NC independent sub-transforms of the same prime in one warp (e.g. NC adjacent
