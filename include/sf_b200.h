@@ -228,6 +228,11 @@ sf_status sf_kv_from_cts(sf_context* ctx, int d, int H, int n0, int n_max, int n
 /* rope_apply (kv_attention.cpp:111-117 -> fused_extract Rope, vmm.cpp:85-100) */
 sf_status sf_rope_apply(sf_context* ctx, const sf_ct* x, int d, int H, long long position, double base,
                         sf_ct** out);
+/* encode + upload (stream-ordered, no host wait) the RoPE plaintexts that
+ * sf_rope_apply will use for an input interleaved at `offset` with `level` at
+ * `position`: a decode loop issues it for the next token while the current one
+ * runs, taking the host encode off the token's critical path. No ledger charge. */
+sf_status sf_rope_prepare(sf_context* ctx, int d, int H, int offset, int level, long long position, double base);
 /* fused_extract with a mask successor (vmm.cpp:102-108); coeff may be NULL */
 sf_status sf_fused_extract_mask(sf_context* ctx, const sf_ct* x, const double* coeff, sf_ct** out);
 sf_status sf_k_append(sf_context* ctx, const sf_kvcache* cache, const sf_ct* k_new, sf_kvcache** out);

@@ -27,7 +27,7 @@ from ._native import SfLayout, SfOpCounts, SfParams
 __all__ = [
     "Error", "LevelUnderflow", "InvalidTarget", "ShapeMismatch", "LayoutMismatch", "CacheFull", "CacheEmpty",
     "DomainViolation", "ScaleMismatch", "Layout", "make_interleaved", "OpCounts", "Backend", "Ciphertext",
-    "VmmPlan", "vmm_interleaved", "predict_interleaved_cost", "AttentionConfig", "KVCache", "rope_apply",
+    "VmmPlan", "vmm_interleaved", "predict_interleaved_cost", "AttentionConfig", "KVCache", "rope_apply", "rope_prepare",
     "fused_extract_mask", "k_append", "make_v_pieces", "v_append", "qk_dot", "softmax_times_v",
     "exact_softmax_maps", "kv_from_cts",
 ]
@@ -668,6 +668,14 @@ def kv_from_cts(be: Backend, cfg: AttentionConfig, n_prime: int, k_cts, v_cts) -
 def rope_apply(be: Backend, x: Ciphertext, cfg: AttentionConfig, position: int, base: float = 10000.0):
     """kv_attention.cpp:111-117."""
     return be._ct(_native.lib().sf_rope_apply, x.h, cfg.d, cfg.H, position, base)
+
+
+def rope_prepare(be: Backend, cfg: AttentionConfig, position: int, level: int, offset: int = 0,
+                 base: float = 10000.0) -> None:
+    """Encode the RoPE plaintexts rope_apply will need for an input interleaved
+    at `offset` with `level` at `position` ahead of time (stream-ordered upload,
+    no host wait): a decode loop prepares token p+1 while token p runs."""
+    _check(_native.lib().sf_rope_prepare(be.ctx, cfg.d, cfg.H, offset, level, int(position), base))
 
 
 def fused_extract_mask(be: Backend, x: Ciphertext, coeff=None):

@@ -110,6 +110,7 @@ SIGNATURES = {
     "sf_kv_get": (st, [vp, C.c_int, C.c_int, C.c_int, vpp]),
     "sf_kv_from_cts": (st, [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vpp, C.c_int, vpp, C.c_int, vpp]),
     "sf_rope_apply": (st, [vp, vp, C.c_int, C.c_int, C.c_longlong, C.c_double, vpp]),
+    "sf_rope_prepare": (st, [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_longlong, C.c_double]),
     "sf_fused_extract_mask": (st, [vp, vp, dp, vpp]),
     "sf_k_append": (st, [vp, vp, vp, vpp]),
     "sf_make_v_pieces": (st, [vp, vp, vp, C.c_int, vpp]),

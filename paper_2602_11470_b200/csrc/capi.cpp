@@ -629,6 +629,12 @@ sf_status sf_rope_apply(sf_context* ctx, const sf_ct* x, int d, int H, long long
     *out = wrap(sf::rope_apply(*ctx->c, x->v, cfg, position, base));
   });
 }
+sf_status sf_rope_prepare(sf_context* ctx, int d, int H, int offset, int level, long long position, double base) {
+  return guard([&] {
+    sf::AttnCfg cfg{ctx->c->slots, d, H, 0, 1};
+    sf::rope_prepare(*ctx->c, cfg, offset, level, position, base);
+  });
+}
 sf_status sf_fused_extract_mask(sf_context* ctx, const sf_ct* x, const double* coeff, sf_ct** out) {
   return guard([&] { *out = wrap(sf::fused_extract_mask(*ctx->c, x->v, coeff)); });
 }
@@ -901,6 +907,7 @@ sf_status sf_graph_capture_end(sf_context* ctx, sf_graph** out) {
     }
     SF_CUDA(e);
     SF_CUDA(ie);
+    ++c.live_graphs;
     *out = g.release();
   });
 }
@@ -922,6 +929,7 @@ void sf_graph_destroy(sf_graph* g) {
   const bool alive = sf::context_alive(g->cp, g->gen);
   cudaStream_t st = alive ? g->cp->stream : nullptr;
   if (alive) cudaStreamSynchronize(st);
+  if (alive && g->x) --g->cp->live_graphs;
   if (g->x) cudaGraphExecDestroy(g->x);
   if (g->g) cudaGraphDestroy(g->g);
   auto free_ = [&](sf::u64* p) { alive ? (void)cudaFreeAsync(p, st) : (void)cudaFree(p); };

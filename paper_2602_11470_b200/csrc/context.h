@@ -221,6 +221,19 @@ struct Context {
   std::map<int, BufPtr> merged_consts;               // (q_top P)^-1 per limb count (merged relin + rescale)
   std::map<int, std::vector<u64>> merged_consts_h;  // host copies (row-pass epilogue parameters)
 
+  // pinned staging ring for host -> device uploads of fresh plaintexts and
+  // encryptions (upload_async): the copy is stream-ordered and the host returns
+  // at once; a slot is reused only after its previous copy has completed
+  struct StageSlot {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaEvent_t ev = nullptr;
+    bool pending = false;
+  };
+  std::vector<StageSlot> stage;
+  size_t stage_next = 0;
+  int live_graphs = 0;  // instantiated graphs of this context (they may read cached plaintexts)
+
   Ledger ledger;
   u64 enc_counter = 0;
   std::atomic<long long> launches{0};
@@ -271,6 +284,7 @@ Pt encode_pt(Context& c, const double* slots, double scale, int limbs);
 std::vector<Pt> encode_many(Context& c, const std::function<void(int, double*)>& gen, int count, double scale,
                             int limbs);
 Pt cached_pt(Context& c, const std::string& key, const double* slots, double scale, int limbs);
+bool lookup_pt(Context& c, const std::string& key, int limbs, Pt* out);  // cached_pt's cache, no encode
 Ct encrypt(Context& c, const double* slots, int level, u64 seed, OptLayout layout);
 Ct zeros(Context& c, int level);
 void decrypt(Context& c, const Ct& a, double* out);
@@ -293,6 +307,11 @@ void check_scales(const Ct& a, const Ct& b, const char* what);
 // Host synchronisation of the lazy builders (constant tables, keys, cached
 // plaintexts uploaded from pageable memory on first use). Not allowed inside a
 // graph capture: the caller must run the step once eagerly first.
+// Stream-ordered upload of `bytes` host bytes to device memory through the
+// pinned staging ring (no stream synchronisation; `src` may be released on
+// return). Not allowed inside a graph capture (the staging slot is reused).
+void upload_async(Context& c, void* dst, const void* src, size_t bytes);
+
 inline void host_sync(Context& c) {
   require(!c.capturing, kInvalidTarget,
           "graph capture: a lazily built table / key / plaintext is not warm yet; run the step once eagerly "

@@ -101,6 +101,11 @@ Context::~Context() {
   sk.reset();
   tab_store.reset();
   for (auto e : events) cudaEventDestroy(e);
+  for (auto& st : stage) {
+    if (st.ev) cudaEventDestroy(st.ev);
+    if (st.p) cudaFreeHost(st.p);
+  }
+  stage.clear();
   for (auto& [w, v] : free_bufs)
     for (u64* q : v) cudaFreeAsync(q, stream);
   free_bufs.clear();
@@ -316,18 +321,37 @@ const ConvPlan& conv_plan(Context& c, const std::vector<int>& src, const std::ve
   return c.conv_plans.emplace(key, std::move(p)).first->second;
 }
 
+void upload_async(Context& c, void* dst, const void* src, size_t bytes) {
+  require(!c.capturing, kInvalidTarget,
+          "graph capture: a fresh plaintext / encryption upload is not capturable; run the step once eagerly "
+          "before capturing it");
+  constexpr size_t kSlots = 16;
+  if (c.stage.empty()) c.stage.resize(kSlots);
+  Context::StageSlot& st = c.stage[c.stage_next++ % kSlots];
+  if (st.pending) SF_CUDA(cudaEventSynchronize(st.ev));  // the slot's previous copy has landed
+  if (st.cap < bytes) {
+    if (st.p) SF_CUDA(cudaFreeHost(st.p));
+    st.p = nullptr;
+    SF_CUDA(cudaMallocHost(&st.p, bytes));
+    st.cap = bytes;
+  }
+  if (!st.ev) SF_CUDA(cudaEventCreateWithFlags(&st.ev, cudaEventDisableTiming));
+  std::memcpy(st.p, src, bytes);
+  SF_CUDA(cudaMemcpyAsync(dst, st.p, bytes, cudaMemcpyHostToDevice, c.stream));
+  SF_CUDA(cudaEventRecord(st.ev, c.stream));
+  st.pending = true;
+}
+
 // upload signed coefficients and reduce into `limbs` NTT-domain limbs (+ noise)
 static BufPtr coeffs_to_ntt(Context& c, const std::vector<i64>& co, int limbs, bool noise, RngKey ekey) {
   SF_HPROF("coeffs_to_ntt");
   BufPtr tmp = buf(c, (size_t)c.n);
-  SF_CUDA(cudaMemcpyAsync(tmp->p, co.data(), co.size() * sizeof(i64), cudaMemcpyHostToDevice, c.stream));
+  upload_async(c, tmp->p, co.data(), co.size() * sizeof(i64));
   BufPtr out = buf(c, (size_t)limbs * c.n);
   std::vector<int> primes(limbs);
   for (int l = 0; l < limbs; ++l) primes[l] = l;
   k_small_rns(c, out->p, ekey, noise, reinterpret_cast<const i64*>(tmp->p), primes.data(), limbs);
   ntt_limbs(c, out->p, limbs, 0, false);
-  // the host vector must outlive the async copy
-  host_sync(c);
   return out;
 }
 
@@ -338,6 +362,14 @@ Pt encode_pt(Context& c, const double* slots, double scale, int limbs) {
   p.limbs = limbs;
   p.scale = scale;
   return p;
+}
+
+bool lookup_pt(Context& c, const std::string& key, int limbs, Pt* out) {
+  std::lock_guard<std::mutex> lk(c.mu);
+  auto it = c.pt_cache.find(key + "@" + std::to_string(limbs));
+  if (it == c.pt_cache.end()) return false;
+  *out = it->second;
+  return true;
 }
 
 Pt cached_pt(Context& c, const std::string& key, const double* slots, double scale, int limbs) {

@@ -19,11 +19,14 @@ struct U128 {
   uint64_t lo, hi;
 };
 
+// The product is written as one 128-bit multiply: ptxas then emits the four
+// 32x32 partial products (IMAD.WIDE.U32 with carry chaining) once, where the
+// separate `a * b` and `__umul64hi(a, b)` recompute the low partials (5
+// IMAD.WIDE + 2 IMAD per term instead of 4 IMAD.WIDE).
 __device__ __forceinline__ void mac128(U128& acc, uint64_t a, uint64_t b) {
-  const uint64_t lo = a * b;
-  const uint64_t hi = __umul64hi(a, b);
-  // add with carry (compiles to IADD3 + IADD3.X chains)
-  asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(acc.lo), "+l"(acc.hi) : "l"(lo), "l"(hi));
+  const unsigned __int128 s = (((unsigned __int128)acc.hi << 64) | acc.lo) + (unsigned __int128)a * b;
+  acc.lo = (uint64_t)s;
+  acc.hi = (uint64_t)(s >> 64);
 }
 
 __device__ __forceinline__ uint64_t reduce128(uint64_t hi, uint64_t lo, uint64_t q, uint64_t mh, uint64_t ml) {

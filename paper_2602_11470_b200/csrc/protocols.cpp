@@ -8,6 +8,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 
 #include "batch.cuh"
 
@@ -577,15 +578,37 @@ static std::vector<double> valid_mask(const Layout& ly, int N) {  // vmm.cpp:45-
   return m;
 }
 
-// fused_extract, Rope successor (vmm.cpp:85-100) via rope_apply
-// (kv_attention.cpp:111-117): y = x.p0 + Rot(x.p1, -s) + Rot(x.p2, s), s = t.
-Ct rope_apply(Context& c, const Ct& x, const AttnCfg& cfg, long long position, double base) {
-  SF_HPROF("rope_apply");
-  require(x.layout && x.layout->kind == LayoutKind::Interleaved && x.layout->d == cfg.d, kLayoutMismatch,
-          "rope_apply: input must be interleaved at the configured width");
-  const Layout ly = *x.layout;
-  const int dh = cfg.d_head(), N = c.slots;
+// The RoPE plaintexts depend on the token position, so a decode stream encodes
+// fresh ones every token; keep those of the last few positions only (a graph
+// may read cached plaintexts, so nothing is dropped while one is alive).
+static void prune_rope_plaintexts(Context& c, long long position) {
+  constexpr long long kKeep = 8;
+  std::lock_guard<std::mutex> lk(c.mu);
+  if (c.live_graphs > 0 || c.capturing) return;
+  for (auto it = c.pt_cache.lower_bound("rope:"); it != c.pt_cache.end() && it->first.compare(0, 5, "rope:") == 0;) {
+    const long long p = std::atoll(it->first.c_str() + 5);
+    if (p < position - kKeep || p > position + kKeep)
+      it = c.pt_cache.erase(it);
+    else
+      ++it;
+  }
+}
+
+// The three RoPE plaintexts of (layout, limb count, position) (vmm.cpp:66-83),
+// encoded once at scale q_top and cached (pruned to recent positions).
+static std::vector<Pt> rope_plaintexts(Context& c, const Layout& ly, int limbs, int dh, long long position,
+                                       double base) {
+  SF_HPROF("rope_plaintexts");
   require(dh > 0 && dh % 2 == 0, kShapeMismatch, "rope_plaintexts: d_head must be positive and even");
+  require(limbs > 1, kLevelUnderflow, "mul_plain: no multiplicative level left");
+  prune_rope_plaintexts(c, position);
+  char key[160];
+  std::snprintf(key, sizeof key, "rope:%lld:%d:%d:%d:%d:%a:", position, ly.d, ly.t, ly.offset, dh, base);
+  std::vector<Pt> pts(3);
+  bool warm = true;
+  for (int i = 0; i < 3 && warm; ++i) warm = lookup_pt(c, key + std::to_string(i), limbs, &pts[i]);
+  if (warm) return pts;
+  const int N = c.slots;
   std::vector<double> p0(N, 0.0), p1(N, 0.0), p2(N, 0.0);
   for (int e = 0; e < ly.d; ++e) {  // vmm.cpp:66-83
     const int pair = (e % dh) / 2;
@@ -597,16 +620,41 @@ Ct rope_apply(Context& c, const Ct& x, const AttnCfg& cfg, long long position, d
     else
       p2[i] = -std::sin(angle);
   }
+  const double* v[3] = {p0.data(), p1.data(), p2.data()};
+  for (int i = 0; i < 3; ++i) pts[i] = cached_pt(c, key + std::to_string(i), v[i], (double)c.primes[limbs - 1], limbs);
+  return pts;
+}
+
+// fused_extract, Rope successor (vmm.cpp:85-100) via rope_apply
+// (kv_attention.cpp:111-117): y = x.p0 + Rot(x.p1, -s) + Rot(x.p2, s), s = t.
+Ct rope_apply(Context& c, const Ct& x, const AttnCfg& cfg, long long position, double base) {
+  SF_HPROF("rope_apply");
+  require(x.layout && x.layout->kind == LayoutKind::Interleaved && x.layout->d == cfg.d, kLayoutMismatch,
+          "rope_apply: input must be interleaved at the configured width");
+  const Layout ly = *x.layout;
+  const int dh = cfg.d_head();
+  check_ct(c, x, "mul_plain");
+  require(x.level() > 0, kLevelUnderflow, "mul_plain: no multiplicative level left");
+  const std::vector<Pt> pts = rope_plaintexts(c, ly, x.limbs, dh, position, base);
   const int s = cfg.t();
-  char key[160];
-  std::snprintf(key, sizeof key, "rope:%lld:%d:%d:%d:%d:%a:", position, ly.d, ly.t, ly.offset, dh, base);
-  Ct y = mul_plain_cached(c, x, std::string(key) + "0", p0);
-  y = add(c, y, rotate(c, mul_plain_cached(c, x, std::string(key) + "1", p1), -s, false));
-  y = add(c, y, rotate(c, mul_plain_cached(c, x, std::string(key) + "2", p2), s, false));
+  Ct y = mac_plain(c, {&x}, {&pts[0]});
+  y = add(c, y, rotate(c, mac_plain(c, {&x}, {&pts[1]}), -s, false));
+  y = add(c, y, rotate(c, mac_plain(c, {&x}, {&pts[2]}), s, false));
   Layout out = ly;
   out.deferred_mask = false;
   y.layout = out;
   return y;
+}
+
+// Encode (and upload, stream-ordered) the RoPE plaintexts rope_apply will use
+// for an input of this layout and level at `position`, ahead of time: a decode
+// loop calls it for the next token while the current one runs on the GPU, so
+// the host encode leaves the token's critical path. No ledger charge.
+void rope_prepare(Context& c, const AttnCfg& cfg, int offset, int level, long long position, double base) {
+  SF_HPROF("rope_prepare");
+  require(level >= 0 && level <= c.L, kInvalidTarget, "rope_prepare: level outside [0, L]");
+  Layout ly = make_interleaved(cfg.d, c.slots, offset, cfg.H);
+  rope_plaintexts(c, ly, level + 1, cfg.d_head(), position, base);
 }
 
 Ct fused_extract_mask(Context& c, const Ct& x, const double* coeff) {  // vmm.cpp:102-108
@@ -652,11 +700,16 @@ std::vector<Ct> make_v_pieces(Context& c, const KV& cache, const Ct& v_open, int
   require(v_open.level() > 0, kLevelUnderflow, "mul_plain: no multiplicative level left");
   std::vector<Pt> masks;
   for (int e = 0; e < dh; ++e) {  // fused_extract(VcacheMask) with the piece mask (vmm.cpp:102-108)
+    char key[96];
+    std::snprintf(key, sizeof key, "vpiece:%d:%d:%d:%d:%d", cfg.d, cfg.H, t, e, j0);
+    Pt hit;
+    if (lookup_pt(c, key, v_open.limbs, &hit)) {  // warm: no host mask synthesis
+      masks.push_back(std::move(hit));
+      continue;
+    }
     std::fill(m.begin(), m.end(), 0.0);
     for (int h = 0; h < cfg.H; ++h) m[(h * dh + e) * t + j0] = 1.0;
     for (int i = 0; i < c.slots; ++i) m[i] *= valid[i];
-    char key[96];
-    std::snprintf(key, sizeof key, "vpiece:%d:%d:%d:%d:%d", cfg.d, cfg.H, t, e, j0);
     masks.push_back(cached_pt(c, key, m.data(), (double)c.primes[v_open.limbs - 1], v_open.limbs));
   }
   std::vector<const Ct*> xs(dh, &v_open);

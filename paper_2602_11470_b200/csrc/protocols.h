@@ -71,6 +71,7 @@ int v_variant_index(const AttnCfg& cfg, int w);
 int v_variant_of(const AttnCfg& cfg, int e, int u_local);
 
 Ct rope_apply(Context& c, const Ct& x, const AttnCfg& cfg, long long position, double base);
+void rope_prepare(Context& c, const AttnCfg& cfg, int offset, int level, long long position, double base);
 Ct fused_extract_mask(Context& c, const Ct& x, const double* coeff);
 KV k_append(Context& c, const KV& cache, const Ct& k_new);
 std::vector<Ct> make_v_pieces(Context& c, const KV& cache, const Ct& v_open, int position);

@@ -237,6 +237,32 @@ def test_rope_bit_exact_and_matches_reference():
         assert g.ledger.totals().asdict() == c["counts"]
 
 
+def test_rope_prepare_then_apply_is_identical():
+    """sf_rope_prepare encodes the plaintexts ahead of time (stream-ordered, no
+    host wait); the following rope_apply must produce the same words as a cold
+    one and charge the same ledger (prepare itself charges nothing)."""
+    from oracle import protocols as P
+    from oracle.layout import make_interleaved
+    import paper_2602_11470_b200 as sf
+    c = cases("medium", "rope")[0]
+    N, L = c["N"], c["L"]
+    g, o = _pair(N, L)
+    ly = make_interleaved(c["d"], N, c["offset"]).with_(deferred_mask=True)
+    xg = g.encrypt(np.array(c["x_slots"]), L, ly, seed=5)
+    xo = o.encrypt(np.array(c["x_slots"]), L, ly, seed=5)
+    cfg = sf.AttentionConfig(N, c["d"], c["d"] // c["d_head"], 0, 1)
+    sf.rope_prepare(g, cfg, c["pos"], L, c["offset"])
+    assert g.ledger.totals().asdict() == sf.OpCounts().asdict()
+    yg = sf.rope_apply(g, xg, cfg, c["pos"])
+    yo = P.fused_extract(o, xo, "rope", dict(n=c["pos"], d_head=c["d_head"], s=ly.t))
+    _eq(yg, yo)
+    assert g.ledger.totals().asdict() == c["counts"]
+    # a stream of positions: the cache of old positions is pruned, results stay exact
+    for pos in range(c["pos"] + 1, c["pos"] + 12):
+        sf.rope_prepare(g, cfg, pos, L, c["offset"])
+        _eq(sf.rope_apply(g, xg, cfg, pos), P.fused_extract(o, xo, "rope", dict(n=pos, d_head=c["d_head"], s=ly.t)))
+
+
 def test_full_ring_ntt_and_rotation_parity():
     # ring 2^16 (the north-star N): encryption, mul_plain (rescale) and a
     # rotation (ModUp / key switch / ModDown) word-identical to the oracle
