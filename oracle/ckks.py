@@ -70,6 +70,8 @@ def lib():
             "ock_rescale": (vp, [vp, vp]),
             "ock_tensor_sum": (vp, [vp, C.POINTER(vp), C.POINTER(vp), C.c_int]),
             "ock_rot_sum": (vp, [vp, C.POINTER(vp), C.POINTER(C.c_int), C.c_int]),
+            "ock_rot_sum_rescale": (vp, [vp, C.POINTER(vp), C.POINTER(C.c_int), C.c_int]),
+            "ock_mac_plain_lazy": (vp, [vp, C.POINTER(vp), DP, C.c_int]),
             "ock_relin_rescale": (vp, [vp, vp]),
             "ock_ct_is_three": (C.c_int, [vp]),
             "ock_ct_d2": (None, [vp, U64P]),
@@ -349,6 +351,36 @@ class CkksOracle:
                 if c.layout != layout:
                     layout = None
         return OCt(self, lib().ock_mac_plain(self.ptr, arr, _dp(pts), len(terms)), lvl - 1, layout)
+
+    def mul_plain_lazy(self, a, p):
+        """a * p WITHOUT the rescale: the raw product at scale * q_top on the
+        same limbs, charged as the reference's mul_plain; the rescale happens in
+        a later rot_sum_rescale (the QK^T pack)."""
+        self._check(a, "mul_plain")
+        if a.level <= 0:
+            raise LevelUnderflow("mul_plain: no multiplicative level left")
+        self.ledger.count_ct_pt()
+        pts = np.ascontiguousarray(self._slots(p, "mul_plain")[None, :])
+        arr = (C.c_void_p * 1)(a.ptr)
+        return OCt(self, lib().ock_mac_plain_lazy(self.ptr, arr, _dp(pts), 1), a.level, a.layout)
+
+    def rot_sum_rescale(self, terms, hoisted: bool = False):
+        """rot_sum of unrescaled products (mul_plain_lazy) with the pending
+        rescale merged into the sum's ModDown (one basis conversion from
+        {q_top} u P); same charge as rot_sum, one level lower."""
+        for a, _ in terms:
+            self._check(a, "rotate")
+        for i, (a, r) in enumerate(terms):
+            if r % self.N:
+                self.ledger.count_rotation(hoisted)
+        for _ in range(len(terms) - 1):
+            self.ledger.count_add()
+        arr = (C.c_void_p * len(terms))(*[a.ptr for a, _ in terms])
+        rr = (C.c_int * len(terms))(*[int(r) for _, r in terms])
+        lvl = min(a.level for a, _ in terms)
+        if lvl <= 0:
+            raise LevelUnderflow("mul_plain: no multiplicative level left")
+        return OCt(self, lib().ock_rot_sum_rescale(self.ptr, arr, rr, len(terms)), lvl - 1, None)
 
     def rotate(self, a, r: int, hoisted: bool = False):
         self._check(a, "rotate")

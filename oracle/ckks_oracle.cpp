@@ -676,6 +676,36 @@ void mod_down(Ctx& c, std::vector<u64>& acc, int limbs, u64* out) {
   }
 }
 
+// ModDown and the rescale by the top prime as ONE fast basis conversion
+// (DESIGN.md §3.6): X = [limbs + alpha][n] (NTT domain, Q limbs then P limbs;
+// the M limbs are consumed); out (limbs - 1 limbs) =
+// (X_i - conv_{M -> q_i}(X_M)) * M^-1 mod q_i, M = q_{limbs-1} * P.
+void mod_down_rescale(Ctx& c, std::vector<u64>& X, int limbs, u64* out) {
+  const int n = c.n;
+  std::vector<int> M{limbs - 1};
+  for (int k = 0; k < c.alpha; ++k) M.push_back((int)c.P_index(k));
+  // coefficient forms of the M limbs: slot limbs-1 (q_top), then the P slots
+  std::vector<u64> coef((size_t)M.size() * n);
+#pragma omp parallel for
+  for (int j = 0; j < (int)M.size(); ++j) {
+    std::memcpy(coef.data() + (size_t)j * n, X.data() + (size_t)(limbs - 1 + j) * n, sizeof(u64) * n);
+    ntt_inv(c, M[j], coef.data() + (size_t)j * n);
+  }
+  std::vector<const u64*> in;
+  for (size_t j = 0; j < M.size(); ++j) in.push_back(coef.data() + j * n);
+#pragma omp parallel for
+  for (int l = 0; l < limbs - 1; ++l) {
+    const u64 q = c.primes[l];
+    std::vector<u64> t(n);
+    conv_basis(c, M, in, l, t.data());
+    ntt_fwd(c, l, t.data());
+    const u64 minv = invmod(mulmod(P_mod(c, q), c.primes[limbs - 1] % q, q), q);
+    const u64* x = X.data() + (size_t)l * n;
+    u64* o = out + (size_t)l * n;
+    for (int k = 0; k < n; ++k) o[k] = mulmod(submod(x[k], t[k], q), minv, q);
+  }
+}
+
 // Relinearise-and-rescale in one basis conversion: for the
 // degree-2 ciphertext (d0, d1, d2) at `limbs` limbs, (kb, ka) = the key-switch
 // inner products of d2 under the relinearisation key (extended basis), and
@@ -688,8 +718,6 @@ Ct* relin_rescale_merged(Ctx& c, const u64* d0, const u64* d1, const u64* d2, in
   std::vector<u64> acc[2] = {std::vector<u64>(nt * n, 0), std::vector<u64>(nt * n, 0)};
   key_switch_ext(c, d2, limbs, 0, acc[0], acc[1]);
   const u64* dd[2] = {d0, d1};
-  std::vector<int> M{limbs - 1};
-  for (int k = 0; k < c.alpha; ++k) M.push_back((int)c.P_index(k));
   Ct* out = new_ct(c, limbs - 1, scale);
   for (int part = 0; part < 2; ++part) {
     std::vector<u64>& X = acc[part];
@@ -700,26 +728,7 @@ Ct* relin_rescale_merged(Ctx& c, const u64* d0, const u64* d1, const u64* d2, in
       const u64* d = dd[part] + (size_t)l * n;
       for (int k = 0; k < n; ++k) x[k] = addmod(x[k], mulmod(d[k], pm, q), q);
     }
-    // coefficient forms of the M limbs: slot limbs-1 (q_top), then the P slots
-    std::vector<u64> coef((size_t)M.size() * n);
-#pragma omp parallel for
-    for (int j = 0; j < (int)M.size(); ++j) {
-      std::memcpy(coef.data() + (size_t)j * n, X.data() + (size_t)(limbs - 1 + j) * n, sizeof(u64) * n);
-      ntt_inv(c, M[j], coef.data() + (size_t)j * n);
-    }
-    std::vector<const u64*> in;
-    for (size_t j = 0; j < M.size(); ++j) in.push_back(coef.data() + j * n);
-#pragma omp parallel for
-    for (int l = 0; l < limbs - 1; ++l) {
-      const u64 q = c.primes[l];
-      std::vector<u64> t(n);
-      conv_basis(c, M, in, l, t.data());
-      ntt_fwd(c, l, t.data());
-      const u64 minv = invmod(mulmod(P_mod(c, q), c.primes[limbs - 1] % q, q), q);
-      const u64* x = X.data() + (size_t)l * n;
-      u64* o = poly(c, out, part, l);
-      for (int k = 0; k < n; ++k) o[k] = mulmod(submod(x[k], t[k], q), minv, q);
-    }
+    mod_down_rescale(c, X, limbs, poly(c, out, part, 0));
   }
   return out;
 }
@@ -740,7 +749,9 @@ void key_switch(Ctx& c, const u64* d, int limbs, u64 g, u64* kb, u64* ka) {
 // the Q limbs, a zero rotation contributes P * (c0, c1) -- and the sum is
 // brought back to Q_l once. Same value as the op-by-op sum up to the ModDown
 // rounding of one instead of k terms.
-Ct* rot_sum(Ctx& c, const Ct* const* a, const int* rots, int k) {
+// rescale: the sum is also rescaled by its top prime, in the ModDown's basis
+// conversion (mod_down_rescale; the QK^T pack).
+Ct* rot_sum(Ctx& c, const Ct* const* a, const int* rots, int k, bool rescale = false) {
   int limbs = 1 << 30;
   double scale = 0.0;
   bool any = false;
@@ -752,7 +763,8 @@ Ct* rot_sum(Ctx& c, const Ct* const* a, const int* rots, int k) {
     else if (std::fabs(a[i]->scale / scale - 1.0) > 1e-9)
       throw std::runtime_error("ScaleMismatch: add: operand scales differ");
   }
-  if (!any) return drop_to(c, a[0], limbs);
+  if (rescale && limbs < 2) throw std::runtime_error("LevelUnderflow: mul_plain: no multiplicative level left");
+  if (!any) return drop_to(c, a[0], rescale ? limbs - 1 : limbs);
   const int n = c.n;
   const size_t nt = (size_t)limbs + c.alpha;
   std::vector<u64> accb(nt * n, 0), acca(nt * n, 0);
@@ -778,6 +790,12 @@ Ct* rot_sum(Ctx& c, const Ct* const* a, const int* rots, int k) {
         for (int j = 0; j < n; ++j) oa[j] = addmod(oa[j], mulmod(s1[j], pm, q), q);
       }
     }
+  }
+  if (rescale) {
+    Ct* out = new_ct(c, limbs - 1, scale / (double)c.primes[limbs - 1]);
+    mod_down_rescale(c, accb, limbs, poly(c, out, 0, 0));
+    mod_down_rescale(c, acca, limbs, poly(c, out, 1, 0));
+    return out;
   }
   Ct* out = new_ct(c, limbs, scale);
   mod_down(c, accb, limbs, poly(c, out, 0, 0));
@@ -885,7 +903,7 @@ Ct* relin_rescale(Ctx& c, const Ct* x) {
 
 // sum_k ct_k (*) pt_k with plaintexts encoded at scale q_top (so the scale is
 // preserved), one rescale at the end (lazy rescale of a MAC).
-Ct* mac_plain(Ctx& c, const Ct* const* cts, const double* slots, int k) {
+Ct* mac_plain(Ctx& c, const Ct* const* cts, const double* slots, int k, bool rescale_out = true) {
   int limbs = 1 << 30;
   for (int i = 0; i < k; ++i) limbs = std::min(limbs, cts[i]->limbs);
   const u64 qtop = c.primes[limbs - 1];
@@ -916,6 +934,10 @@ Ct* mac_plain(Ctx& c, const Ct* const* cts, const double* slots, int k) {
     }
   }
   acc->zero = !any;
+  if (!rescale_out) {  // the raw products at scale * q_top (the caller rescales later)
+    if (acc->zero) acc->scale = 0.0;
+    return acc;
+  }
   Ct* r = rescale(c, acc);
   r->scale = acc->zero ? 0.0 : scale;
   delete acc;
@@ -1081,6 +1103,12 @@ void* ock_rotate(void* c, void* a, int r) {
 }
 void* ock_rot_sum(void* c, void** a, const int* rots, int k) {
   return guard([&]() -> void* { return rot_sum(*static_cast<Ctx*>(c), (Ct* const*)a, rots, k); });
+}
+void* ock_rot_sum_rescale(void* c, void** a, const int* rots, int k) {
+  return guard([&]() -> void* { return rot_sum(*static_cast<Ctx*>(c), (Ct* const*)a, rots, k, true); });
+}
+void* ock_mac_plain_lazy(void* c, void** cts, const double* slots, int k) {
+  return guard([&]() -> void* { return mac_plain(*static_cast<Ctx*>(c), (Ct* const*)cts, slots, k, false); });
 }
 void* ock_tensor_sum(void* c, void** a, void** b, int k) {
   return guard([&]() -> void* { return tensor_sum(*static_cast<Ctx*>(c), (Ct* const*)a, (Ct* const*)b, k); });

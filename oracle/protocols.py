@@ -437,23 +437,33 @@ def qk_dot(be, q, cache: KVCache, cfg):
     for j, kc in enumerate(cache.k_cts):
         prod = be.mul(q_rep, kc)
         prod = fold_within_head(be, prod, dh, t)
-        masked = be.mul_plain(prod, head_mask)
+        masked = mask_lazy(be, prod, head_mask)
         terms[(j * t) // gt][j % PACK_GROUPS].append((masked, -((j * t) % gt)))
     # pack + accumulate (kv_attention.cpp:202-206) as rotation sums, one per
     # (map, key-ct group j mod PACK_GROUPS)
     return [be.with_layout(pack_sum(be, grp), None) for grp in terms]
 
 
+def mask_lazy(be, x, mask):
+    """The QK^T head mask (layouts.cpp:134-138) with its rescale deferred to the
+    pack rotation sum (CKKS backends: mul_plain_lazy + rot_sum_rescale, one
+    rescale per sum instead of one per key ciphertext)."""
+    f = getattr(be, "mul_plain_lazy", None)
+    return f(x, mask) if f else be.mul_plain(x, mask)
+
+
 PACK_GROUPS = 8  # key-ct groups of the QK^T pack sums (DESIGN.md §3.8)
 
 
 def pack_sum(be, groups):
-    """sum over non-empty groups of rot_sum(group), accumulated in group order."""
+    """sum over non-empty groups of rot_sum(group), accumulated in group order
+    (rot_sum_rescale where the backend deferred the mask's rescale)."""
+    rs = getattr(be, "rot_sum_rescale", None) if getattr(be, "mul_plain_lazy", None) else None
     acc = None
     for grp in groups:
         if not grp:
             continue
-        s = be.rot_sum(grp)
+        s = rs(grp) if rs else be.rot_sum(grp)
         acc = s if acc is None else be.add(acc, s)
     return acc
 

@@ -66,7 +66,7 @@ def qk_dot_partial(be, q, cache, cfg, rank, world):
         if (j % G) % world != rank:  # whole pack groups per rank
             continue
         prod = P.fold_within_head(be, be.mul(q_rep, cache.k_cts[j]), dh, t)
-        masked = be.mul_plain(prod, head_mask)
+        masked = P.mask_lazy(be, prod, head_mask)
         terms[(j * t) // gt][j % G].append((masked, -((j * t) % gt)))
     maps = [P.pack_sum(be, grp) for grp in terms]
     return [be.with_layout(m, None) if m is not None else be.zeros(q.level - 2) for m in maps]

@@ -210,6 +210,16 @@ class SimBackend:
             acc = t if acc is None else self.add(acc, t)
         return acc
 
+    def mul_plain_lazy(self, a, p):
+        """CKKS backends defer this product's rescale to rot_sum_rescale; at
+        slot level it is mul_plain (same charge, same level bookkeeping)."""
+        return self.mul_plain(a, p)
+
+    def rot_sum_rescale(self, terms, hoisted: bool = False):
+        """rot_sum of mul_plain_lazy products (the deferred rescale is invisible
+        at slot level)."""
+        return self.rot_sum(terms, hoisted)
+
     def rot_sum(self, terms, hoisted: bool = False):
         """sum_i Rot(a_i, r_i) as the reference's rotate/add chain."""
         acc = None

@@ -178,6 +178,9 @@ struct KsSumArgs {
   int tprime[kMaxPrimes];
   u64 pm[kMaxPrimes];  // P mod q_t, t < limbs
   bool pm_one = false;  // keys carry P^-1 on the Q limbs (get_key_pinv): pm == 1, ModDown without P^-1
+  // targets t >= inv_from (and all special primes) are written inverse-row-passed:
+  // inv_from = limbs - 1 feeds the merged ModDown + rescale (M = {q_top} u P)
+  int inv_from = 1 << 30;
   int out_begin[kSumOuts + 1];
   u64* acc[kSumOuts];  // [2][nt][n]
   int jsrc[kSumJobs];
@@ -229,8 +232,9 @@ std::vector<Ct> mul_batch(Context& c, const std::vector<const Ct*>& a, const std
                           bool count = true);
 std::vector<Ct> rescale_batch(Context& c, const std::vector<const Ct*>& xs);
 // x_i (.) p_i, rescaled (scale preserved: p_i encoded at q_top)
+// rescale = false: the raw products at scale * q_top, same limbs (the caller rescales)
 std::vector<Ct> mul_plain_batch(Context& c, const std::vector<const Ct*>& xs, const std::vector<const Pt*>& ps,
-                                bool count = true);
+                                bool count = true, bool rescale = true);
 std::vector<Ct> add_batch(Context& c, const std::vector<const Ct*>& a, const std::vector<const Ct*>& b,
                           bool count = true);
 // sum_i Rot(a_i, r_i) per group with one ModDown per part
@@ -238,8 +242,10 @@ struct SumTerm {
   const Ct* ct;
   int r;
 };
+// rescale: the sum is rescaled by its top prime in the same basis conversion as
+// its ModDown (merged): one conversion from {q_top} u P
 std::vector<Ct> rot_sum_batch(Context& c, const std::vector<std::vector<SumTerm>>& groups, bool hoisted,
-                              bool count = true, const std::vector<const Pt*>* post = nullptr);
+                              bool count = true, const std::vector<const Pt*>* post = nullptr, bool rescale = false);
 // doubling chains x <- x + Rot(x, r) over rots[i] (radix rotation sums); charged
 // as the reference's rotate + add steps when count && lead
 // post (fused path only): per chain an NTT-domain plaintext multiplied into the

@@ -591,9 +591,10 @@ void mod_down_polys(Context& c, int limbs, const std::vector<MdPoly>& P, bool p_
 // brought back with one ModDown per part; the same function as the CPU
 // oracle's rot_sum, charged as the reference's rotate/add chain.
 std::vector<Ct> rot_sum_batch(Context& c, const std::vector<std::vector<SumTerm>>& groups, bool hoisted, bool count,
-                              const std::vector<const Pt*>* post) {
+                              const std::vector<const Pt*>* post, bool rescale) {
   SF_HPROF("rot_sum_batch");
   require(!post || (post->size() == groups.size() && fused_path(c)), kInternal, "rot_sum: post multipliers");
+  require(!(post && rescale), kInternal, "rot_sum: post multipliers with a merged rescale");
   std::vector<Ct> out(groups.size());
   std::map<int, std::vector<int>> by_limbs;
   for (size_t gi = 0; gi < groups.size(); ++gi) {
@@ -620,22 +621,25 @@ std::vector<Ct> rot_sum_batch(Context& c, const std::vector<std::vector<SumTerm>
         check_scales(*first, a, "add");
     }
     if (count) c.ledger.add((long long)G.size() - 1);
+    if (rescale) require(limbs > 1, kLevelUnderflow, "mul_plain: no multiplicative level left");
     if (!first) {
       Ct z = *G[0].ct;
-      z.limbs = limbs;
+      z.limbs = rescale ? limbs - 1 : limbs;
       z.layout = ly;
       out[gi] = z;
       continue;
     }
-    out[gi] = alloc_ct(c, limbs, first->scale);
+    out[gi] = rescale ? alloc_ct(c, limbs - 1, first->scale / (double)c.primes[limbs - 1])
+                      : alloc_ct(c, limbs, first->scale);
     out[gi].layout = ly;
     by_limbs[limbs].push_back((int)gi);
   }
   const size_t n = c.n;
   for (auto& [limbs, gidx] : by_limbs) {
     std::vector<u64> pm(limbs);
-    // fused path: keys with P^-1 on the Q limbs (bit-identical results, fewer products)
-    const bool pre = fused_path(c);
+    // fused path: keys with P^-1 on the Q limbs (bit-identical results, fewer products);
+    // the merged ModDown + rescale converts the unscaled sum
+    const bool pre = fused_path(c) && !rescale;
     for (int l = 0; l < limbs; ++l) {
       u64 r = 1 % c.primes[l];
       for (int k = 0; k < c.alpha; ++k) r = mulmod_h(r, c.primes[c.P_index(k)] % c.primes[l], c.primes[l]);
@@ -676,6 +680,7 @@ std::vector<Ct> rot_sum_batch(Context& c, const std::vector<std::vector<SumTerm>
       for (int t = 0; t < nt; ++t) A.tprime[t] = x.tprime[t];
       for (int l = 0; l < limbs; ++l) A.pm[l] = pm[l];
       A.pm_one = pre;
+      if (rescale) A.inv_from = limbs - 1;
       for (size_t s = 0; s < srcv.size(); ++s) {
         A.c0[s] = srcv[s]->c0();
         A.c1[s] = srcv[s]->c1(c.n);
@@ -702,7 +707,10 @@ std::vector<Ct> rot_sum_batch(Context& c, const std::vector<std::vector<SumTerm>
       A.out_begin[chunk.size()] = jb;
       A.nout = (int)chunk.size();
       b_ks_sum(c, A);
-      mod_down_polys(c, limbs, md, fused_path(c), pre);
+      if (rescale)
+        mod_down_rescale_polys(c, limbs, md, fused_path(c));
+      else
+        mod_down_polys(c, limbs, md, fused_path(c), pre);
     }
   }
   return out;
@@ -1085,7 +1093,7 @@ Ct relin_rescale(Context& c, const Ct3& x) {
 
 // ------------------------------------------------------------- ct x pt mult
 std::vector<Ct> mul_plain_batch(Context& c, const std::vector<const Ct*>& xs, const std::vector<const Pt*>& ps,
-                                bool count) {
+                                bool count, bool rescale) {
   require(xs.size() == ps.size(), kShapeMismatch, "mul_plain_batch: operand count");
   std::vector<Ct> out(xs.size());
   std::vector<Ct> tmp(xs.size());
@@ -1099,11 +1107,12 @@ std::vector<Ct> mul_plain_batch(Context& c, const std::vector<const Ct*>& xs, co
     require(ps[i]->limbs >= x.limbs, kShapeMismatch, "mul_plain: plaintext has too few limbs");
     if (count) c.ledger.ctpt();
     if (x.zero) {
-      out[i] = zeros(c, x.level() - 1);
+      out[i] = zeros(c, rescale ? x.level() - 1 : x.level());
       out[i].layout = x.layout;
       continue;
     }
     tmp[i] = alloc_ct(c, x.limbs, x.scale * (double)c.primes[x.limbs - 1]);
+    tmp[i].layout = x.layout;
     MulPtBatch& B = by_limbs[x.limbs];
     B.c0[B.count] = x.c0(), B.c1[B.count] = x.c1(c.n), B.pt[B.count] = ps[i]->buf->p;
     B.o0[B.count] = tmp[i].c0(), B.o1[B.count] = tmp[i].c1(c.n);
@@ -1112,6 +1121,10 @@ std::vector<Ct> mul_plain_batch(Context& c, const std::vector<const Ct*>& xs, co
     where.push_back((int)i);
   }
   for (auto& [limbs, B] : by_limbs) b_mulpt(c, B, limbs);
+  if (!rescale) {  // the caller rescales later (e.g. merged into a rotation sum's ModDown)
+    for (size_t k = 0; k < todo.size(); ++k) out[where[k]] = std::move(tmp[where[k]]);
+    return out;
+  }
   auto r = rescale_batch(c, todo);
   for (size_t k = 0; k < r.size(); ++k) {
     const Ct& x = *xs[where[k]];

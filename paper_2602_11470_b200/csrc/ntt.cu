@@ -797,13 +797,13 @@ __global__ void __launch_bounds__(kWarps * 32, 2) ks_sum_kernel(KsSumArgs A, Tab
   }
   u64* accb = A.acc[o] + (size_t)t * n;
   u64* acca = A.acc[o] + (size_t)(A.nt + t) * n;
-  if (qt) {
+  if (qt && t < A.inv_from) {
 #pragma unroll
     for (int k = 0; k < E; k += 2) {
       reinterpret_cast<ulonglong2*>(accb + rowoff)[k / 2] = make_ulonglong2(vb[k], vb[k + 1]);
       reinterpret_cast<ulonglong2*>(acca + rowoff)[k / 2] = make_ulonglong2(va[k], va[k + 1]);
     }
-  } else {  // special prime: ModDown's inverse row pass, strided stores
+  } else {  // special prime (or merged q_top): ModDown's inverse row pass, strided stores
     const u64* W = T.ipsi + ((size_t)m << LOGN);
     const u64* Ws = T.ipsi_s + ((size_t)m << LOGN);
     auto tw = [&](int b, int blk, u64& w, u64& ws) {

@@ -787,25 +787,22 @@ std::vector<Ct> qk_dot_partial(Context& c, const Ct& q, const KV& cache, int ran
   std::vector<Ct> masked;
   bool fused_mask = fused_path(c);
   for (int i = 0; i < J; ++i) fused_mask = fused_mask && !prod0[i].zero && prod0[i].limbs == prod0[0].limbs;
+  // the masked products stay unrescaled (scale * q_top): each pack rotation sum
+  // rescales once in its ModDown's basis conversion (merged)
+  // instead of J separate rescales
   if (fused_mask) {
     // fold_within_head (38-41) with the ReplicateExtract mask (layouts.cpp:134-138)
-    // multiplied in the fold's last ModDown epilogue, then one batched rescale:
-    // the same words as fold -> mul_plain
+    // multiplied in the fold's last ModDown epilogue (a fused ct x pt)
     const int lb = prod0[0].limbs;
     require(lb - 1 > 0, kLevelUnderflow, "mul_plain: no multiplicative level left");
     const Pt hm = cached_pt(c, hkey, head_mask.data(), (double)c.primes[lb - 1], lb);
     std::vector<const Pt*> post(J, &hm);
-    std::vector<Ct> prod = fold_batch(c, pp0, dh, t, true, &post);
-    std::vector<const Ct*> pp;
-    std::vector<double> s0(J);
+    masked = fold_batch(c, pp0, dh, t, true, &post);
     for (int i = 0; i < J; ++i) {
       c.ledger.ctpt();
-      s0[i] = prod[i].scale;
-      prod[i].scale *= (double)c.primes[lb - 1];  // the product's scale before its rescale
-      pp.push_back(&prod[i]);
+      masked[i].scale *= (double)c.primes[lb - 1];  // the product's scale before its rescale
+      masked[i].layout.reset();
     }
-    masked = rescale_batch(c, pp);
-    for (int i = 0; i < J; ++i) masked[i].scale = s0[i], masked[i].layout.reset();
   } else {
     std::vector<Ct> prod = fold_batch(c, pp0, dh, t);  // fold_within_head (38-41), DESIGN.md §3.8
     std::vector<const Ct*> pp;
@@ -816,7 +813,8 @@ std::vector<Ct> qk_dot_partial(Context& c, const Ct& q, const KV& cache, int ran
     }
     std::vector<const Pt*> hp;
     for (int i = 0; i < J; ++i) pp.push_back(&prod[i]), hp.push_back(&hm[i]);
-    masked = mul_plain_batch(c, pp, hp);
+    masked = mul_plain_batch(c, pp, hp, true, false);
+    for (auto& m : masked) m.layout.reset();
   }
   // pack + accumulate (kv_attention.cpp:202-206): one rotation sum per (map,
   // key-ct group j mod kPackGroups), then the groups' sum
@@ -828,7 +826,7 @@ std::vector<Ct> qk_dot_partial(Context& c, const Ct& q, const KV& cache, int ran
     if (!where.count(key)) where[key] = (int)groups.size(), groups.emplace_back(), gid.push_back(key);
     groups[where[key]].push_back({&masked[i], -((own[i] * t) % gt)});
   }
-  std::vector<Ct> gs = rot_sum_batch(c, groups, false);
+  std::vector<Ct> gs = rot_sum_batch(c, groups, false, true, nullptr, true);
   std::vector<std::vector<const Ct*>> per_map(n_maps);
   for (int m = 0; m < n_maps; ++m)
     for (int r = 0; r < kPackGroups; ++r) {
