@@ -569,36 +569,27 @@ struct ShflPerm {
     const uint32_t ur = (inv * ((__brev((uint32_t)lane) >> 27) - base)) & 31;  // reader's brev5(L)
     c = (int)(((base + slope * ur) >> 5) & 7);
     smod = (int)(slope & 7);
+#pragma unroll
+    for (int b = 0; b < 3; ++b) rm[b] = 0ull - (u64)((c >> b) & 1);
   }
+  u64 rm[3];  // all-ones where rotation stage b applies (bit b of c)
   // v: natural-order registers of this lane's row segment -> permuted row
   __device__ __forceinline__ void apply(u64 (&v)[8]) const {
     u64 z[8];
 #pragma unroll
     for (int m = 0; m < 8; ++m) z[m] = v[__brev((uint32_t)m) >> 29];  // z[m] = v[brev3(m)]
-    // z[i] <- z[(i + c) & 7] in place: rotations by 1, 2, 4, each cycle with one temporary
-    if (c & 1) {
-      const u64 t0 = z[0];
+    // z[i] <- z[(i + c) & 7]: a barrel rotation by 1, 2, 4 as bitwise blends
+    // x ^ ((x ^ y) & m) (one LOP3 per 32-bit half on the ALU pipe; the branchy
+    // in-place form compiled to predicated IMAD.MOVs on the FMA-heavy pipe that
+    // the key-switch products saturate)
 #pragma unroll
-      for (int i = 0; i < 7; ++i) z[i] = z[i + 1];
-      z[7] = t0;
-    }
-    if (c & 2) {
+    for (int b = 0; b < 3; ++b) {
+      const u64 m = rm[b];
+      u64 t[8];
 #pragma unroll
-      for (int cy = 0; cy < 2; ++cy) {
-        const u64 t0 = z[cy];
-        z[cy] = z[cy + 2];
-        z[cy + 2] = z[cy + 4];
-        z[cy + 4] = z[cy + 6];
-        z[cy + 6] = t0;
-      }
-    }
-    if (c & 4) {
+      for (int i = 0; i < 8; ++i) t[i] = z[i] ^ ((z[i] ^ z[(i + (1 << b)) & 7]) & m);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const u64 t0 = z[i];
-        z[i] = z[i + 4];
-        z[i + 4] = t0;
-      }
+      for (int i = 0; i < 8; ++i) z[i] = t[i];
     }
     switch (smod) {  // y[k] = z[(slope * brev3(k)) & 7], then one shuffle per register
 #define SF_SHFL_CASE(M)                                                                 \

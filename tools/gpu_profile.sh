@@ -17,6 +17,7 @@ for r in $OUT/*.ncu-rep; do
   b=${r%.ncu-rep}
   ncu -i $r --page raw --csv > $b.raw.csv 2>/dev/null
   ncu -i $r --page details --csv --print-details all > $b.details.csv 2>/dev/null
+  ncu -i $r --page source --csv --print-source sass > $b.sass.csv 2>/dev/null; gzip -f $b.sass.csv
   rm -f $r
 done
 du -sh $OUT
