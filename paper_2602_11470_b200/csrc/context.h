@@ -122,6 +122,7 @@ struct Ledger {
 // Device-side prime / twiddle tables (one array per quantity, indexed by prime).
 struct Tabs {
   const u64 *q, *mh, *ml;          // prime, Barrett mu = floor(2^128 / q)
+  const u64 *qn, *r64;             // Montgomery: -q^-1 mod 2^64, R = 2^64 mod q
   const u64 *psi, *psi_s;          // [np][n] psi^{br(k)} (+ Shoup)
   const u64 *ipsi, *ipsi_s;        // [np][n] psi^{-br(k)} (+ Shoup)
   const u64 *ninv, *ninv_s;        // [np]
@@ -205,7 +206,7 @@ struct Context {
   // device tables
   BufPtr tab_store;  // owns all table memory below
   Tabs tabs{};
-  std::vector<u64> mu_hi, mu_lo;
+  std::vector<u64> mu_hi, mu_lo, qneg_inv, r64;
 
   // host copies needed by the encoder
   std::vector<double> fft_re, fft_im;  // zeta^{br(k)}
@@ -214,7 +215,9 @@ struct Context {
   BufPtr sk;  // [np][n] NTT domain
   std::map<u64, BufPtr> keys;  // galois element (0 = relin) -> [beta][2][np][n]
   std::map<std::string, ConvPlan> conv_plans;
-  std::map<u64, BufPtr> keys_pinv;  // switching keys with the Q limbs times P^-1 (get_key_pinv)
+  // Montgomery copies of the switching keys for the fused kernels (get_key_mont):
+  // every limb times R = 2^64, the Q limbs of the rotation-sum copy also times P^-1
+  std::map<u64, BufPtr> keys_pinv, keys_r;
   std::map<std::string, Pt> pt_cache;  // semantic-key plaintext cache (masks)
   std::map<int, BufPtr> level_consts;  // per-limb-count rescale / moddown constants
   std::map<int, std::vector<u64>> level_consts_h;
@@ -300,7 +303,9 @@ Ct level_drop(Context& c, const Ct& a, int target);
 Ct bootstrap(Context& c, const Ct& a, int target);
 u64 galois_elt(const Context& c, int r);
 const BufPtr& get_key(Context& c, u64 g);
-const BufPtr& get_key_pinv(Context& c, u64 g);  // Q limbs times P^-1 (rotation sums)
+// Montgomery key copy: limbs times R = 2^64 mod q, and with
+// pinv the Q limbs also times P^-1 (rotation sums / hoisted rotations, §3.7a)
+const BufPtr& get_key_mont(Context& c, u64 g, bool pinv);
 void check_ct(const Context& c, const Ct& a, const char* what);
 void check_scales(const Ct& a, const Ct& b, const char* what);
 

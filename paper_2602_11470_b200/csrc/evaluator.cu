@@ -94,6 +94,7 @@ Context::~Context() {
   p2p_destroy(*this);
   keys.clear();
   keys_pinv.clear();
+  keys_r.clear();
   conv_plans.clear();
   pt_cache.clear();
   level_consts.clear();
@@ -169,7 +170,7 @@ std::unique_ptr<Context> make_context(int slots, int L, int log_n, int alpha, in
     ninvw[p] = mulmod_h(ninv[p], c->ipsi1_h[p], c->primes[p]);
     ninvw_s[p] = shoup_h(ninvw[p], c->primes[p]);
   }
-  const size_t words = 3 * np + 4 * np * n + 4 * np;
+  const size_t words = 5 * np + 4 * np * n + 4 * np;
   c->tab_store = buf(*c, words);
   std::vector<u64> host(words);
   u64* h = host.data();
@@ -183,6 +184,8 @@ std::unique_ptr<Context> make_context(int slots, int L, int log_n, int alpha, in
   c->tabs.q = put(c->primes);
   c->tabs.mh = put(c->mu_hi);
   c->tabs.ml = put(c->mu_lo);
+  c->tabs.qn = put(c->qneg_inv);
+  c->tabs.r64 = put(c->r64);
   c->tabs.psi = put(psi);
   c->tabs.psi_s = put(psi_s);
   c->tabs.ipsi = put(ipsi);
@@ -579,13 +582,9 @@ Ct mul_plain(Context& c, const Ct& a, const double* slots) {
 }
 
 // ---------------------------------------------------------------- key switching
-const BufPtr& get_key(Context& c, u64 g) {
-  SF_HPROF("get_key");
-  {
-    std::lock_guard<std::mutex> lk(c.mu);
-    auto it = c.keys.find(g);
-    if (it != c.keys.end()) return it->second;
-  }
+// The switching key for galois element g (0: relinearisation), DESIGN.md §3.4;
+// deterministic in (seed, g), so it can be rebuilt instead of kept.
+static BufPtr build_key(Context& c, u64 g) {
   const int np = c.np;
   const size_t n = c.n;
   BufPtr key = buf(c, (size_t)c.beta * 2 * np * n);
@@ -618,39 +617,71 @@ const BufPtr& get_key(Context& c, u64 g) {
     k_sample_uniform(c, a, keys.data(), primes.data(), np);
     k_key_combine(c, b, a, c.sk->p, e->p, sp->p, pm.data(), primes.data(), np);
   }
+  return key;
+}
+
+const BufPtr& get_key(Context& c, u64 g) {
+  SF_HPROF("get_key");
+  {
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto it = c.keys.find(g);
+    if (it != c.keys.end()) return it->second;
+  }
+  BufPtr key = build_key(c, g);
   std::lock_guard<std::mutex> lk(c.mu);
   return c.keys.emplace(g, key).first->second;
 }
 
-// get_key with the Q-prime limbs multiplied by P^-1: the
-// rotation-sum inner products then land already divided by P on the Q
-// primes, the P*sigma(c0) terms become plain additions and ModDown's final
-// multiply disappears. The special-prime limbs are unchanged (ModDown's
-// conversion input). Results are bit-identical (exact modular identities).
-const BufPtr& get_key_pinv(Context& c, u64 g) {
-  SF_HPROF("get_key_pinv");
+// Montgomery copies of the switching keys for the fused key-switch kernels
+// (DESIGN.md §3.7b): every limb times R = 2^64 mod q, so the kernels' 128-bit
+// inner-product sums T finish with one Montgomery reduction T R^-1 (a 64-bit
+// low product and one high product) instead of a 128-bit Barrett reduction.
+// With pinv the Q-prime limbs also carry P^-1: the
+// rotation-sum inner products then land already divided by P on the Q primes,
+// the P*sigma(c0) terms become plain additions and ModDown's final multiply
+// disappears; the special-prime limbs (ModDown's conversion input) carry R
+// only. Exact modular identities: results are bit-identical. The unscaled key
+// is rebuilt (deterministic) rather than kept, unless something cached it.
+const BufPtr& get_key_mont(Context& c, u64 g, bool pinv) {
+  SF_HPROF("get_key_mont");
+  auto& cache = pinv ? c.keys_pinv : c.keys_r;
   {
     std::lock_guard<std::mutex> lk(c.mu);
-    auto it = c.keys_pinv.find(g);
-    if (it != c.keys_pinv.end()) return it->second;
+    auto it = cache.find(g);
+    if (it != cache.end()) return it->second;
   }
-  const BufPtr& k = get_key(c, g);
-  const size_t words = (size_t)c.beta * 2 * c.np * c.n;
-  BufPtr out = buf(c, words);
-  SF_CUDA(cudaMemcpyAsync(out->p, k->p, words * sizeof(u64), cudaMemcpyDeviceToDevice, c.stream));
-  std::vector<u64> f(c.np, 1);
-  for (int m = 0; m <= c.L; ++m) {
+  BufPtr out;
+  {
+    BufPtr cached;
+    {
+      std::lock_guard<std::mutex> lk(c.mu);
+      auto it = c.keys.find(g);
+      if (it != c.keys.end()) cached = it->second;
+    }
+    if (cached) {
+      const size_t words = (size_t)c.beta * 2 * c.np * c.n;
+      out = buf(c, words);
+      SF_CUDA(cudaMemcpyAsync(out->p, cached->p, words * sizeof(u64), cudaMemcpyDeviceToDevice, c.stream));
+    } else {
+      out = build_key(c, g);
+    }
+  }
+  std::vector<u64> f(c.np);
+  for (int m = 0; m < c.np; ++m) {
     const u64 q = c.primes[m];
-    u64 pm = 1 % q;
-    for (int kk = 0; kk < c.alpha; ++kk) pm = mulmod_h(pm, c.primes[c.P_index(kk)] % q, q);
-    f[m] = invmod_h(pm, q);
+    f[m] = c.r64[m];
+    if (pinv && m <= c.L) {
+      u64 pm = 1 % q;
+      for (int kk = 0; kk < c.alpha; ++kk) pm = mulmod_h(pm, c.primes[c.P_index(kk)] % q, q);
+      f[m] = mulmod_h(f[m], invmod_h(pm, q), q);
+    }
   }
   BufPtr fd = buf(c, f.size());
   SF_CUDA(cudaMemcpyAsync(fd->p, f.data(), f.size() * sizeof(u64), cudaMemcpyHostToDevice, c.stream));
   k_scale_limbs(c, out->p, c.beta * 2, fd->p);
   host_sync(c);  // f is pageable; keys are built once, off the timed path
   std::lock_guard<std::mutex> lk(c.mu);
-  return c.keys_pinv.emplace(g, out).first->second;
+  return cache.emplace(g, out).first->second;
 }
 
 Ct level_drop(Context& c, const Ct& a, int target) {

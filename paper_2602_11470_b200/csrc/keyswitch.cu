@@ -347,7 +347,7 @@ void ks_jobs(Context& c, const ExtB& x, const std::vector<KsJob>& jobs, bool mer
           for (u64 e = (u64)n - 1, b = jb.g, m2 = 2ull * n - 1; e; e >>= 1, b = (b * b) & m2)
             if (e & 1) gi = (gi * b) & m2;
         ka.ginv[k] = gi;
-        ka.key[k] = (pre ? get_key_pinv(c, jb.g <= 1 ? 0 : jb.g) : get_key(c, jb.g <= 1 ? 0 : jb.g))->p;
+        ka.key[k] = get_key_mont(c, jb.g <= 1 ? 0 : jb.g, pre)->p;  // the row stage reduces by REDC
         ka.acc[k] = accp(j, 0);
         ka.add0[k] = jb.add0;
         ka.add1[k] = jb.add1;
@@ -356,7 +356,7 @@ void ks_jobs(Context& c, const ExtB& x, const std::vector<KsJob>& jobs, bool mer
       if (merged) {
         ka.merged = 1;
         for (int l = 0; l < limbs; ++l) {
-          u64 r = 1 % c.primes[l];
+          u64 r = c.r64[l];  // P * R mod q (Montgomery-scaled like the keys)
           for (int k = 0; k < c.alpha; ++k) r = mulmod_h(r, c.primes[c.P_index(k)] % c.primes[l], c.primes[l]);
           ka.pm[l] = r;
         }
@@ -637,11 +637,13 @@ std::vector<Ct> rot_sum_batch(Context& c, const std::vector<std::vector<SumTerm>
   const size_t n = c.n;
   for (auto& [limbs, gidx] : by_limbs) {
     std::vector<u64> pm(limbs);
-    // fused path: keys with P^-1 on the Q limbs (bit-identical results, fewer products);
-    // the merged ModDown + rescale converts the unscaled sum
-    const bool pre = fused_path(c) && !rescale;
+    // fused path: Montgomery keys (R-scaled) with P^-1 on the
+    // Q limbs (bit-identical results, fewer products); the merged ModDown +
+    // rescale converts the unscaled sum (keys and pm times R only)
+    const bool fused = fused_path(c);
+    const bool pre = fused && !rescale;
     for (int l = 0; l < limbs; ++l) {
-      u64 r = 1 % c.primes[l];
+      u64 r = fused ? c.r64[l] : 1 % c.primes[l];
       for (int k = 0; k < c.alpha; ++k) r = mulmod_h(r, c.primes[c.P_index(k)] % c.primes[l], c.primes[l]);
       pm[l] = pre ? 1 : r;
     }
@@ -696,7 +698,7 @@ std::vector<Ct> rot_sum_batch(Context& c, const std::vector<std::vector<SumTerm>
           const int r = pos_mod(tm.r, c.slots);
           A.jsrc[jb] = src[tm.ct];
           A.g[jb] = r == 0 ? 1 : galois_elt(c, r);
-          A.key[jb] = r == 0 ? nullptr : (pre ? get_key_pinv(c, A.g[jb]) : get_key(c, A.g[jb]))->p;
+          A.key[jb] = r == 0 ? nullptr : (fused ? get_key_mont(c, A.g[jb], pre) : get_key(c, A.g[jb]))->p;
           ++jb;
         }
         const Ct& y = out[chunk[o]];

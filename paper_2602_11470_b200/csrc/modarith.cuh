@@ -53,6 +53,23 @@ __device__ __forceinline__ uint64_t reduce64(uint64_t x, uint64_t q, uint64_t mh
   return r;
 }
 
+// Montgomery reduction, R = 2^64: (hi:lo) R^-1 mod q for hi < q (any lo), with
+// qn = -q^-1 mod 2^64. m = lo qn makes lo + m q = 0 mod 2^64 (a carry of 1
+// unless lo = 0), so (T + m q) / 2^64 = hi + mulhi(m, q) + (lo != 0) < 2q.
+// One 64-bit low product and one high product (reduce128: three high products).
+__device__ __forceinline__ uint64_t redc128(uint64_t hi, uint64_t lo, uint64_t q, uint64_t qn) {
+  const uint64_t m = lo * qn;
+  const uint64_t r = hi + __umul64hi(m, q) + (lo != 0 ? 1u : 0u);
+  return r >= q ? r - q : r;
+}
+
+// Montgomery-domain finish of a 128-bit sum T = sum x_i (k_i R) (R-scaled
+// multipliers): T R^-1 mod q = sum x_i k_i mod q. The high word is first
+// brought below q (T changes by a multiple of q 2^64), which bounds T < q 2^64.
+__device__ __forceinline__ uint64_t mont_finish(const U128& t, uint64_t q, uint64_t mh, uint64_t qn) {
+  return redc128(reduce64(t.hi, q, mh), t.lo, q, qn);
+}
+
 __device__ __forceinline__ uint64_t mulmod(uint64_t a, uint64_t b, uint64_t q, uint64_t mh, uint64_t ml) {
   return reduce128(__umul64hi(a, b), a * b, q, mh, ml);
 }

@@ -207,7 +207,8 @@ __global__ void __launch_bounds__(kWarps * 32) ntt_col_pass(LimbBatch B, Tabs T)
 // all warps busy. TCF = 8 gives 64-byte row segments for big batches; TCF = 2
 // gives 4x more CTAs for single-ciphertext launches.
 template <int LOGR, int LOGC, int TCF, int CPW, bool FC>
-__global__ void __launch_bounds__(TCF / CPW * 32, TCF / CPW == 8 ? (CPW == 1 ? 3 : 2) : (TCF / CPW == 4 ? 6 : 8))
+__global__ void __launch_bounds__(TCF / CPW * 32, TCF / CPW == 8 ? (CPW == 1 && LOGR + LOGC < 17 ? 3 : 2)
+                                                                  : (TCF / CPW == 4 ? (LOGR + LOGC < 17 ? 6 : 4) : 8))
     fused_col_kernel(FusedColArgs A, Tabs T) {
   // CPW columns per warp (TCF / CPW warps): the column transforms of one warp
   // run interleaved (shared twiddles, CPW x the independent butterflies)
@@ -415,7 +416,8 @@ __global__ void __launch_bounds__(TCF / CPW * 32, TCF / CPW == 8 ? (CPW == 1 ? 3
 // job reads exactly one source row: rd = perm_{g^-1}(rs), and within it the
 // column perm_g(rd*C + c) mod C.
 template <int LOGR, int LOGC>
-__global__ void __launch_bounds__(kWarps * 32, 2) ks_row_kernel(KsRowArgs A, Tabs T) {
+// ring 2^17 rows hold 16 residues per lane: one CTA per SM lifts the register cap (no spills)
+__global__ void __launch_bounds__(kWarps * 32, LOGC >= 9 ? 1 : 2) ks_row_kernel(KsRowArgs A, Tabs T) {
   constexpr int C = 1 << LOGC, E = C / 32, LOGN = LOGR + LOGC;
   auto rbr = [](uint32_t col) { return __brev(col) >> (32 - LOGC); };
   // row buffers hold bit-reversed columns; lane L's blocked segment lands at
@@ -463,7 +465,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) ks_row_kernel(KsRowArgs A, Tab
     }
   }
   __syncwarp();
-  const u64 mh = T.mh[m], ml = T.ml[m];
+  const u64 mh = T.mh[m], qn = T.qn[m];  // keys (and pm) are Montgomery-scaled: get_key_mont
   u64* scratch = wsm + A.ndig * C;
   // 2. every job of this source: permuted inner product with its key
   for (int jb = A.job_begin[s]; jb < A.job_begin[s + 1]; ++jb) {
@@ -509,8 +511,8 @@ __global__ void __launch_bounds__(kWarps * 32, 2) ks_row_kernel(KsRowArgs A, Tab
     u64 vb[E], va[E];
 #pragma unroll
     for (int k = 0; k < E; ++k) {
-      vb[k] = reduce128(sb[k].hi, sb[k].lo, q, mh, ml);
-      va[k] = reduce128(sa[k].hi, sa[k].lo, q, mh, ml);
+      vb[k] = mont_finish(sb[k], q, mh, qn);
+      va[k] = mont_finish(sa[k], q, mh, qn);
     }
     u64* accb = A.acc[jb] + (size_t)t * n;
     u64* acca = A.acc[jb] + (size_t)(A.nt + t) * n;
@@ -613,7 +615,7 @@ __device__ __forceinline__ void add128(U128& acc, uint64_t a) {
 // PM1: the keys' Q limbs carry P^-1 (get_key_pinv), so the P * sigma(c0) and
 // P * (c0, c1) terms are plain additions
 template <int LOGR, int LOGC, bool PF, bool SH, bool PM1>
-__global__ void __launch_bounds__(kWarps * 32, 2) ks_sum_kernel(KsSumArgs A, Tabs T) {
+__global__ void __launch_bounds__(kWarps * 32, LOGC >= 9 ? 1 : 2) ks_sum_kernel(KsSumArgs A, Tabs T) {
   constexpr int C = 1 << LOGC, E = C / 32, LOGN = LOGR + LOGC;
   auto rbr = [](uint32_t col) { return __brev(col) >> (32 - LOGC); };
   auto xp = [](uint32_t i) { return i ^ ((i >> 4) & 1u); };  // bank fold, as in ks_row_kernel
@@ -625,7 +627,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) ks_sum_kernel(KsSumArgs A, Tab
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rd = tile * kWarps + warp;
   const int m = A.tprime[t];
-  const u64 q = T.q[m], mh = T.mh[m], ml = T.ml[m];
+  const u64 q = T.q[m], mh = T.mh[m], qn = T.qn[m];
   const bool qt = t < A.limbs;
   const u64 pm = qt ? A.pm[t] : 0;
   u64* buf = rowbuf[warp];
@@ -633,19 +635,24 @@ __global__ void __launch_bounds__(kWarps * 32, 2) ks_sum_kernel(KsSumArgs A, Tab
   U128 sb[E], sa[E];
 #pragma unroll
   for (int k = 0; k < E; ++k) sb[k] = U128{0, 0}, sa[k] = U128{0, 0};
-  int terms = 0;  // products accumulated since the last partial reduction (< 2^120 each)
+  // Montgomery-domain sums (keys and pm carry R = 2^64: get_key_mont): a product
+  // adds < 2^56 to the high word, a plain term c (P * sigma(c0) with P^-1 folded
+  // into the keys) enters as c R = c * 2^64, i.e. c added to the high word. A job
+  // raises the high word by < 2^61, so it is brought back below q every 7 jobs
+  // (T changes by multiples of q 2^64) and the sum finishes with one REDC.
+  int terms = 0;  // jobs since the last high-word reduction
   auto fold = [&]() {
 #pragma unroll
     for (int k = 0; k < E; ++k) {
-      sb[k] = U128{reduce128(sb[k].hi, sb[k].lo, q, mh, ml), 0};
-      sa[k] = U128{reduce128(sa[k].hi, sa[k].lo, q, mh, ml), 0};
+      sb[k].hi = reduce64(sb[k].hi, q, mh);
+      sa[k].hi = reduce64(sa[k].hi, q, mh);
     }
     terms = 0;
   };
   for (int jb = A.out_begin[o]; jb < A.out_begin[o + 1]; ++jb) {
     const int s = A.jsrc[jb];
     const u64 g = A.g[jb];
-    if (terms > 200) fold();
+    if (terms >= 7) fold();
     if (g <= 1) {  // identity term: P * (c0, c1) on the Q primes
       if (!qt) continue;
       const u64* a0 = A.c0[s] + (size_t)t * n + rowoff;
@@ -655,10 +662,10 @@ __global__ void __launch_bounds__(kWarps * 32, 2) ks_sum_kernel(KsSumArgs A, Tab
         const ulonglong2 v0 = reinterpret_cast<const ulonglong2*>(a0)[k / 2];
         const ulonglong2 v1 = reinterpret_cast<const ulonglong2*>(a1)[k / 2];
         if constexpr (PM1) {
-          add128(sb[k], v0.x);
-          add128(sb[k + 1], v0.y);
-          add128(sa[k], v1.x);
-          add128(sa[k + 1], v1.y);
+          sb[k].hi += v0.x;
+          sb[k + 1].hi += v0.y;
+          sa[k].hi += v1.x;
+          sa[k + 1].hi += v1.y;
         } else {
           mac128(sb[k], v0.x, pm);
           mac128(sb[k + 1], v0.y, pm);
@@ -709,12 +716,12 @@ __global__ void __launch_bounds__(kWarps * 32, 2) ks_sum_kernel(KsSumArgs A, Tab
 #pragma unroll
         for (int k = 0; k < E; ++k) {
           if constexpr (PM1)
-            add128(sb[k], x[k]);
+            sb[k].hi += x[k];
           else
             mac128(sb[k], x[k], pm);
         }
       }
-      terms += A.ndig + 1;
+      ++terms;
       continue;
     }
     // source positions in the bit-reversed row buffer: an affine map of
@@ -772,19 +779,19 @@ __global__ void __launch_bounds__(kWarps * 32, 2) ks_sum_kernel(KsSumArgs A, Tab
 #pragma unroll
       for (int k = 0; k < E; ++k) {
         if constexpr (PM1)
-          add128(sb[k], buf[sc[k]]);
+          sb[k].hi += buf[sc[k]];
         else
           mac128(sb[k], buf[sc[k]], pm);
       }
       __syncwarp();
     }
-    terms += A.ndig + 1;
+    ++terms;
   }
   u64 vb[E], va[E];
 #pragma unroll
   for (int k = 0; k < E; ++k) {
-    vb[k] = reduce128(sb[k].hi, sb[k].lo, q, mh, ml);
-    va[k] = reduce128(sa[k].hi, sa[k].lo, q, mh, ml);
+    vb[k] = mont_finish(sb[k], q, mh, qn);
+    va[k] = mont_finish(sa[k], q, mh, qn);
   }
   u64* accb = A.acc[o] + (size_t)t * n;
   u64* acca = A.acc[o] + (size_t)(A.nt + t) * n;

@@ -223,6 +223,8 @@ void build_host_tables(Context& c, std::vector<u64>& psi, std::vector<u64>& psi_
   ninv_s.resize(np);
   c.mu_hi.resize(np);
   c.mu_lo.resize(np);
+  c.qneg_inv.resize(np);
+  c.r64.resize(np);
   std::vector<uint32_t> br(n);
   for (int k = 0; k < n; ++k) br[k] = (uint32_t)bitrev_h(k, c.logn);
   for (int m = 0; m < np; ++m) {
@@ -230,6 +232,10 @@ void build_host_tables(Context& c, std::vector<u64>& psi, std::vector<u64>& psi_
     const u128 mu = (~(u128)0) / q;  // floor((2^128 - 1) / q) == floor(2^128 / q), q odd
     c.mu_hi[m] = (u64)(mu >> 64);
     c.mu_lo[m] = (u64)mu;
+    u64 inv = q;  // q^-1 mod 2^64 by Newton (q odd: correct to 3 bits, doubling per step)
+    for (int it = 0; it < 5; ++it) inv *= 2 - q * inv;
+    c.qneg_inv[m] = 0 - inv;
+    c.r64[m] = (u64)(((u128)1 << 64) % q);
     const u64 psi1 = min_primitive_root(q, n), ipsi1 = invmod_h(psi1, q);
     std::vector<u64> pw(n), ipw(n);
     pw[0] = ipw[0] = 1;
