@@ -608,6 +608,74 @@ struct ShflPerm {
   }
 };
 
+// Automorphism gather for the pair-strided row layout of ks_sum (C = 256):
+// register k = 2a + b of lane L holds column 64a + 2L + b, so every row load
+// and store is one fully coalesced 16-byte access per lane per quarter a (the
+// blocked layout's 64-byte lane stride cost 4x the L1 wavefronts: ks_sum was
+// L1TEX-bound). In bit-reversed positions, brev8(64a + 2L + b) = brev2(a) +
+// 4 brev5(L) + 128 b, so destination (L, a, b) reads position
+//   p = (S_a + 4 slope brev5(L) + 128 b) mod 256,  S_a = base + slope brev2(a),
+// i.e. source lane brev5((p >> 2) & 31) -- the same for b = 0, 1 -- source
+// quarter brev2(S_a & 3) -- warp-uniform: 8 static cases of (base & 3, slope & 3)
+// -- and source pair element b ^ (bit 7 of p at b = 0). Each source lane swaps
+// its pair for the lane that reads it (one blend per quarter) and every
+// register moves with one 64-bit shuffle.
+struct ShflPermQ {
+  int sl[4];        // per destination quarter: the lane this lane reads from
+  uint32_t fm[4];   // per quarter: all-ones when this lane's reader needs the pair swapped
+  int cs;           // quarter map case: (base & 3) | (slope & 2) << 1
+  __device__ __forceinline__ ShflPermQ(uint32_t base, uint32_t slope, int lane) {
+    const uint32_t u = __brev((uint32_t)lane) >> 27;  // brev5(lane)
+    uint32_t inv = slope;  // slope^-1 mod 32 (Newton, slope odd)
+    inv *= 2 - slope * inv;
+    inv *= 2 - slope * inv;
+    inv *= 2 - slope * inv;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const uint32_t S = (base + slope * (uint32_t)(((a & 1) << 1) | (a >> 1))) & 255;
+      sl[a] = (int)(__brev(((S >> 2) + slope * u) & 31) >> 27);
+      const uint32_t ur = (inv * (u - (S >> 2))) & 31;  // brev5 of the lane reading this one
+      fm[a] = 0u - ((((S >> 2) + slope * ur) >> 5) & 1u);
+    }
+    cs = (int)((base & 3) | ((slope & 2) << 1));
+  }
+  __device__ __forceinline__ static u64 blend(u64 x, u64 y, uint32_t m) {  // m ? y : x, per 32-bit half
+    const uint32_t lo = (uint32_t)x ^ (((uint32_t)x ^ (uint32_t)y) & m);
+    const uint32_t hi = (uint32_t)(x >> 32) ^ (((uint32_t)(x >> 32) ^ (uint32_t)(y >> 32)) & m);
+    return ((u64)hi << 32) | lo;
+  }
+  __device__ __forceinline__ void apply(u64 (&v)[8]) const {
+    u64 y[8];
+    switch (cs) {
+#define SF_Q_CASE(K)                                                                          \
+  case K:                                                                                     \
+    _Pragma("unroll") for (int a = 0; a < 4; ++a) {                                           \
+      constexpr int b3 = K & 3, s3 = (K & 4) ? 3 : 1;                                         \
+      const int al = ((a & 1) << 1) | (a >> 1);                                               \
+      const int pa = (b3 + s3 * al) & 3;                                                      \
+      const int ap = ((pa & 1) << 1) | (pa >> 1);                                            \
+      y[2 * a] = blend(v[2 * ap], v[2 * ap + 1], fm[a]);                                      \
+      y[2 * a + 1] = blend(v[2 * ap + 1], v[2 * ap], fm[a]);                                  \
+    }                                                                                         \
+    break;
+      SF_Q_CASE(0)
+      SF_Q_CASE(1)
+      SF_Q_CASE(2)
+      SF_Q_CASE(3)
+      SF_Q_CASE(4)
+      SF_Q_CASE(5)
+      SF_Q_CASE(6)
+      SF_Q_CASE(7)
+#undef SF_Q_CASE
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      v[2 * a] = __shfl_sync(0xffffffffu, y[2 * a], sl[a]);
+      v[2 * a + 1] = __shfl_sync(0xffffffffu, y[2 * a + 1], sl[a]);
+    }
+  }
+};
+
 __device__ __forceinline__ void add128(U128& acc, uint64_t a) {
   asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, 0;" : "+l"(acc.lo), "+l"(acc.hi) : "l"(a));
 }
@@ -631,7 +699,12 @@ __global__ void __launch_bounds__(kWarps * 32, LOGC >= 9 ? 1 : 2) ks_sum_kernel(
   const bool qt = t < A.limbs;
   const u64 pm = qt ? A.pm[t] : 0;
   u64* buf = rowbuf[warp];
-  const size_t rowoff = (size_t)rd * C + lane * E;
+  // register layout of a row: pair-strided on the shuffle path at C = 256
+  // (register pair k of lane L = columns 64 (k/2) + 2L, +1: coalesced), blocked
+  // otherwise (lane L owns columns E L .. E L + E - 1)
+  constexpr bool PS = SH && LOGC == 8;
+  auto eoff = [&](int k) { return PS ? 64 * (k >> 1) + 2 * lane : lane * E + k; };
+  const size_t rowoff = (size_t)rd * C;
   U128 sb[E], sa[E];
 #pragma unroll
   for (int k = 0; k < E; ++k) sb[k] = U128{0, 0}, sa[k] = U128{0, 0};
@@ -659,8 +732,8 @@ __global__ void __launch_bounds__(kWarps * 32, LOGC >= 9 ? 1 : 2) ks_sum_kernel(
       const u64* a1 = A.c1[s] + (size_t)t * n + rowoff;
 #pragma unroll
       for (int k = 0; k < E; k += 2) {
-        const ulonglong2 v0 = reinterpret_cast<const ulonglong2*>(a0)[k / 2];
-        const ulonglong2 v1 = reinterpret_cast<const ulonglong2*>(a1)[k / 2];
+        const ulonglong2 v0 = *reinterpret_cast<const ulonglong2*>(a0 + eoff(k));
+        const ulonglong2 v1 = *reinterpret_cast<const ulonglong2*>(a1 + eoff(k));
         if constexpr (PM1) {
           sb[k].hi += v0.x;
           sb[k + 1].hi += v0.y;
@@ -678,24 +751,26 @@ __global__ void __launch_bounds__(kWarps * 32, LOGC >= 9 ? 1 : 2) ks_sum_kernel(
     }
     const RowPerm<LOGR, LOGC> rp(rd, g);
     const int rs = (int)rp.src_row;
-    if constexpr (SH && LOGC == 8) {  // shuffle gather (no shared-memory round trip)
-      const ShflPerm sp(rp.base, rp.slope, lane);
+    if constexpr (PS) {  // shuffle gather (no shared-memory round trip)
+      const ShflPermQ sp(rp.base, rp.slope, lane);
       for (int j = 0; j < A.ndig; ++j) {
         const int lo = j * A.alpha, hi = min(lo + A.alpha, A.limbs);
         const u64* src = (t >= lo && t < hi) ? A.c1[s] + (size_t)t * n + (size_t)rs * C
                                              : A.ext[s] + ((size_t)j * A.nt + t) * n + (size_t)rs * C;
-        const ulonglong2* kb = reinterpret_cast<const ulonglong2*>(A.key[jb] + ((size_t)(j * 2 + 0) * A.np + m) * n + rowoff);
-        const ulonglong2* ka = reinterpret_cast<const ulonglong2*>(A.key[jb] + ((size_t)(j * 2 + 1) * A.np + m) * n + rowoff);
+        const u64* kb = A.key[jb] + ((size_t)(j * 2 + 0) * A.np + m) * n + rowoff;
+        const u64* ka = A.key[jb] + ((size_t)(j * 2 + 1) * A.np + m) * n + rowoff;
         u64 x[8];
 #pragma unroll
         for (int k = 0; k < E; k += 2) {
-          const ulonglong2 v = reinterpret_cast<const ulonglong2*>(src + lane * E)[k / 2];
+          const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(src + eoff(k));
           x[k] = v.x, x[k + 1] = v.y;
         }
         sp.apply(x);
         ulonglong2 kv[E];
 #pragma unroll
-        for (int k = 0; k < E; k += 2) kv[k] = kb[k / 2], kv[k + 1] = ka[k / 2];
+        for (int k = 0; k < E; k += 2)
+          kv[k] = *reinterpret_cast<const ulonglong2*>(kb + eoff(k)),
+          kv[k + 1] = *reinterpret_cast<const ulonglong2*>(ka + eoff(k));
 #pragma unroll
         for (int k = 0; k < E; k += 2) {
           mac128(sb[k], x[k], kv[k].x);
@@ -709,7 +784,7 @@ __global__ void __launch_bounds__(kWarps * 32, LOGC >= 9 ? 1 : 2) ks_sum_kernel(
         u64 x[8];
 #pragma unroll
         for (int k = 0; k < E; k += 2) {
-          const ulonglong2 v = reinterpret_cast<const ulonglong2*>(src + lane * E)[k / 2];
+          const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(src + eoff(k));
           x[k] = v.x, x[k + 1] = v.y;
         }
         sp.apply(x);
@@ -733,8 +808,8 @@ __global__ void __launch_bounds__(kWarps * 32, LOGC >= 9 ? 1 : 2) ks_sum_kernel(
       const int lo = j * A.alpha, hi = min(lo + A.alpha, A.limbs);
       const u64* src = (t >= lo && t < hi) ? A.c1[s] + (size_t)t * n + (size_t)rs * C
                                            : A.ext[s] + ((size_t)j * A.nt + t) * n + (size_t)rs * C;
-      const u64* kb = A.key[jb] + ((size_t)(j * 2 + 0) * A.np + m) * n + rowoff;
-      const u64* ka = A.key[jb] + ((size_t)(j * 2 + 1) * A.np + m) * n + rowoff;
+      const u64* kb = A.key[jb] + ((size_t)(j * 2 + 0) * A.np + m) * n + rowoff + lane * E;
+      const u64* ka = A.key[jb] + ((size_t)(j * 2 + 1) * A.np + m) * n + rowoff + lane * E;
       ulonglong2 kv[PF ? E : 1];  // PF: the key words are in flight while the row is staged
       if constexpr (PF) {
 #pragma unroll
@@ -798,8 +873,8 @@ __global__ void __launch_bounds__(kWarps * 32, LOGC >= 9 ? 1 : 2) ks_sum_kernel(
   if (qt && t < A.inv_from) {
 #pragma unroll
     for (int k = 0; k < E; k += 2) {
-      reinterpret_cast<ulonglong2*>(accb + rowoff)[k / 2] = make_ulonglong2(vb[k], vb[k + 1]);
-      reinterpret_cast<ulonglong2*>(acca + rowoff)[k / 2] = make_ulonglong2(va[k], va[k + 1]);
+      *reinterpret_cast<ulonglong2*>(accb + rowoff + eoff(k)) = make_ulonglong2(vb[k], vb[k + 1]);
+      *reinterpret_cast<ulonglong2*>(acca + rowoff + eoff(k)) = make_ulonglong2(va[k], va[k + 1]);
     }
   } else {  // special prime (or merged q_top): ModDown's inverse row pass, strided stores
     const u64* W = T.ipsi + ((size_t)m << LOGN);
@@ -809,8 +884,23 @@ __global__ void __launch_bounds__(kWarps * 32, LOGC >= 9 ? 1 : 2) ks_sum_kernel(
       w = W[i];
       ws = Ws[i];
     };
-    warp_inv<LOGC, kBlocked>(vb, buf, lane, q, tw);
-    warp_inv<LOGC, kBlocked>(va, buf, lane, q, tw);
+    if constexpr (PS) {  // pair-strided -> strided (lane + 32 k) through the row buffer, then the transform
+      auto restride = [&](u64 (&v)[E]) {
+#pragma unroll
+        for (int k = 0; k < E; ++k) buf[xp(eoff(k & ~1) + (k & 1))] = v[k];
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < E; ++k) v[k] = buf[xp(lane + 32 * k)];
+        __syncwarp();
+      };
+      restride(vb);
+      warp_inv<LOGC, kStrided>(vb, buf, lane, q, tw);
+      restride(va);
+      warp_inv<LOGC, kStrided>(va, buf, lane, q, tw);
+    } else {
+      warp_inv<LOGC, kBlocked>(vb, buf, lane, q, tw);
+      warp_inv<LOGC, kBlocked>(va, buf, lane, q, tw);
+    }
 #pragma unroll
     for (int k = 0; k < E; ++k) {
       accb[(size_t)rd * C + lane + 32 * k] = vb[k];
