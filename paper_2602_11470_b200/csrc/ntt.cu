@@ -417,7 +417,7 @@ __global__ void __launch_bounds__(TCF / CPW * 32, TCF / CPW == 8 ? (CPW == 1 && 
 // column perm_g(rd*C + c) mod C.
 template <int LOGR, int LOGC>
 // ring 2^17 rows hold 16 residues per lane: one CTA per SM lifts the register cap (no spills)
-__global__ void __launch_bounds__(kWarps * 32, LOGC >= 9 ? 1 : 2) ks_row_kernel(KsRowArgs A, Tabs T) {
+__global__ void __launch_bounds__(kWarps * 32, LOGC >= 9 ? 1 : 3) ks_row_kernel(KsRowArgs A, Tabs T) {
   constexpr int C = 1 << LOGC, E = C / 32, LOGN = LOGR + LOGC;
   auto rbr = [](uint32_t col) { return __brev(col) >> (32 - LOGC); };
   // row buffers hold bit-reversed columns; lane L's blocked segment lands at
@@ -472,70 +472,56 @@ __global__ void __launch_bounds__(kWarps * 32, LOGC >= 9 ? 1 : 2) ks_row_kernel(
     const u64 g = A.g[jb];
     const int rd = g > 1 ? (int)RowPerm<LOGR, LOGC>(rs, A.ginv[jb]).src_row : rs;
     const size_t rowoff = (size_t)rd * C + lane * E;
-    U128 sb[E], sa[E];
-#pragma unroll
-    for (int k = 0; k < E; ++k) sb[k] = U128{0, 0}, sa[k] = U128{0, 0};
     uint32_t sc[E];  // positions in the bit-reversed row buffers (bank-conflict free gathers)
 #pragma unroll
     for (int k = 0; k < E; ++k)
       sc[k] = xp(g > 1 ? RowPerm<LOGR, LOGC>(rd, g).pos(rbr(lane * E + k)) : rbr(lane * E + k));
-    for (int j = 0; j < A.ndig; ++j) {
-      const u64* X = wsm + j * C;
-      const u64* kb = A.key[jb] + ((size_t)(j * 2 + 0) * A.np + m) * n + rowoff;
-      const u64* ka = A.key[jb] + ((size_t)(j * 2 + 1) * A.np + m) * n + rowoff;
+    // the b and a parts one after the other: half the accumulator registers
+    // (3 CTAs per SM instead of 2); the gathered words are re-read from shared memory
+#pragma unroll 1
+    for (int part = 0; part < 2; ++part) {
+      U128 acc[E];
 #pragma unroll
-      for (int k = 0; k < E; k += 2) {
-        const ulonglong2 vb = reinterpret_cast<const ulonglong2*>(kb)[k / 2];
-        const ulonglong2 va = reinterpret_cast<const ulonglong2*>(ka)[k / 2];
-        const u64 x0 = X[sc[k]], x1 = X[sc[k + 1]];
-        mac128(sb[k], x0, vb.x);
-        mac128(sa[k], x0, va.x);
-        mac128(sb[k + 1], x1, vb.y);
-        mac128(sa[k + 1], x1, va.y);
+      for (int k = 0; k < E; ++k) acc[k] = U128{0, 0};
+      for (int j = 0; j < A.ndig; ++j) {
+        const u64* X = wsm + j * C;
+        const u64* kp = A.key[jb] + ((size_t)(j * 2 + part) * A.np + m) * n + rowoff;
+#pragma unroll
+        for (int k = 0; k < E; k += 2) {
+          const ulonglong2 kv = reinterpret_cast<const ulonglong2*>(kp)[k / 2];
+          mac128(acc[k], X[sc[k]], kv.x);
+          mac128(acc[k + 1], X[sc[k + 1]], kv.y);
+        }
       }
-    }
-    if (A.merged && t < A.limbs) {  // + P * (d0, d1): the relinearised pair in the extended basis
-      const u64 pmt = A.pm[t];
-      const u64* a0 = A.add0[jb] + (size_t)t * n + rowoff;
-      const u64* a1 = A.add1[jb] + (size_t)t * n + rowoff;
+      if (A.merged && t < A.limbs) {  // + P * (d0, d1): the relinearised pair in the extended basis
+        const u64 pmt = A.pm[t];
+        const u64* ad = (part ? A.add1[jb] : A.add0[jb]) + (size_t)t * n + rowoff;
 #pragma unroll
-      for (int k = 0; k < E; k += 2) {
-        const ulonglong2 v0 = reinterpret_cast<const ulonglong2*>(a0)[k / 2];
-        const ulonglong2 v1 = reinterpret_cast<const ulonglong2*>(a1)[k / 2];
-        mac128(sb[k], v0.x, pmt);
-        mac128(sb[k + 1], v0.y, pmt);
-        mac128(sa[k], v1.x, pmt);
-        mac128(sa[k + 1], v1.y, pmt);
+        for (int k = 0; k < E; k += 2) {
+          const ulonglong2 v = reinterpret_cast<const ulonglong2*>(ad)[k / 2];
+          mac128(acc[k], v.x, pmt);
+          mac128(acc[k + 1], v.y, pmt);
+        }
       }
-    }
-    u64 vb[E], va[E];
+      u64 v[E];
 #pragma unroll
-    for (int k = 0; k < E; ++k) {
-      vb[k] = mont_finish(sb[k], q, mh, qn);
-      va[k] = mont_finish(sa[k], q, mh, qn);
-    }
-    u64* accb = A.acc[jb] + (size_t)t * n;
-    u64* acca = A.acc[jb] + (size_t)(A.nt + t) * n;
-    if (t < A.limbs && !(A.merged && t == A.limbs - 1)) {
+      for (int k = 0; k < E; ++k) v[k] = mont_finish(acc[k], q, mh, qn);
+      u64* out = A.acc[jb] + (size_t)(part * A.nt + t) * n;
+      if (t < A.limbs && !(A.merged && t == A.limbs - 1)) {
 #pragma unroll
-      for (int k = 0; k < E; k += 2) {
-        reinterpret_cast<ulonglong2*>(accb + rowoff)[k / 2] = make_ulonglong2(vb[k], vb[k + 1]);
-        reinterpret_cast<ulonglong2*>(acca + rowoff)[k / 2] = make_ulonglong2(va[k], va[k + 1]);
-      }
-    } else {  // special prime: ModDown's inverse row pass, strided stores
-      const u64* W = T.ipsi + ((size_t)m << LOGN);
-      const u64* Ws = T.ipsi_s + ((size_t)m << LOGN);
-      auto tw = [&](int b, int blk, u64& w, u64& ws) {
-        const int i = (1 << (LOGN - 1 - b)) + (rd << (LOGC - 1 - b)) + blk;
-        w = W[i];
-        ws = Ws[i];
-      };
-      warp_inv<LOGC, kBlocked, decltype(tw), false>(vb, scratch, lane, q, tw);
-      warp_inv<LOGC, kBlocked, decltype(tw), false>(va, scratch, lane, q, tw);
+        for (int k = 0; k < E; k += 2)
+          reinterpret_cast<ulonglong2*>(out + rowoff)[k / 2] = make_ulonglong2(v[k], v[k + 1]);
+      } else {  // special prime: ModDown's inverse row pass, strided stores
+        const u64* W = T.ipsi + ((size_t)m << LOGN);
+        const u64* Ws = T.ipsi_s + ((size_t)m << LOGN);
+        auto tw = [&](int b, int blk, u64& w, u64& ws) {
+          const int i = (1 << (LOGN - 1 - b)) + (rd << (LOGC - 1 - b)) + blk;
+          w = W[i];
+          ws = Ws[i];
+        };
+        warp_inv<LOGC, kBlocked, decltype(tw), false>(v, scratch, lane, q, tw);
 #pragma unroll
-      for (int k = 0; k < E; ++k) {
-        accb[(size_t)rd * C + lane + 32 * k] = vb[k];
-        acca[(size_t)rd * C + lane + 32 * k] = va[k];
+        for (int k = 0; k < E; ++k) out[(size_t)rd * C + lane + 32 * k] = v[k];
       }
     }
   }
