@@ -85,6 +85,10 @@ __device__ __forceinline__ uint64_t mul_shoup_lazy(uint64_t x, uint64_t w, uint6
   return x * w - __umul64hi(x, wp) * q;
 }
 
+// L1 prefetch of one 128-byte line (no register result: the load latency of the
+// next work item overlaps this one's arithmetic)
+__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
 __device__ __forceinline__ uint64_t add_mod(uint64_t a, uint64_t b, uint64_t q) {
   const uint64_t s = a + b;
   return s >= q ? s - q : s;

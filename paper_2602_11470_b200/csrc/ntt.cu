@@ -234,10 +234,22 @@ __global__ void __launch_bounds__(TCF / CPW * 32, TCF / CPW == 8 ? (CPW == 1 && 
   const u64* src = A.src[job];
   u64* dst = A.dst[job];
   auto region = [&](int limb, int col) { return sm_all + (size_t)(limb * TCF + col) * PAD; };
-  // 1. stage the source tiles (TCF*8-byte row segments)
-  for (int e = threadIdx.x; e < A.ns * R * TCF; e += NT) {
-    const int s = e / (R * TCF), rem = e - s * R * TCF, row = rem / TCF, col = rem - row * TCF;
-    region(s, col)[swz(row)] = src[(size_t)s * n + (size_t)row * C + col0 + col];
+  // 1. stage the source tiles (TCF*8-byte row segments): per source limb, all
+  //    of a thread's loads are issued before its shared-memory stores (R*TCF/NT
+  //    loads in flight per thread instead of one)
+  constexpr int kStage = R * TCF / NT;
+  for (int s = 0; s < A.ns; ++s) {
+    u64 v[kStage];
+#pragma unroll
+    for (int i = 0; i < kStage; ++i) {
+      const int e = threadIdx.x + i * NT, row = e / TCF, col = e - row * TCF;
+      v[i] = src[(size_t)s * n + (size_t)row * C + col0 + col];
+    }
+#pragma unroll
+    for (int i = 0; i < kStage; ++i) {
+      const int e = threadIdx.x + i * NT, row = e / TCF, col = e - row * TCF;
+      region(s, col)[swz(row)] = v[i];
+    }
   }
   __syncthreads();
   // 2. inverse column NTT of every (source limb, column); the epilogue applies
@@ -434,6 +446,14 @@ __global__ void __launch_bounds__(kWarps * 32, LOGC >= 9 ? 1 : 3) ks_row_kernel(
   const int m = A.tprime[t];
   const u64 q = T.q[m];
   u64* wsm = ks_sm + (size_t)warp * (A.ndig + 1) * C;
+  if (lane < C / 16 && A.job_begin[s] < A.job_begin[s + 1]) {  // the first job's key rows: in flight during the row NTTs
+    const int j0 = A.job_begin[s];
+    const u64 g0 = A.g[j0];
+    const int rd0 = g0 > 1 ? (int)RowPerm<LOGR, LOGC>(rs, A.ginv[j0]).src_row : rs;
+    for (int j = 0; j < A.ndig; ++j)
+      for (int part = 0; part < 2; ++part)
+        prefetch_l1(A.key[j0] + ((size_t)(j * 2 + part) * A.np + m) * n + (size_t)rd0 * C + (size_t)lane * 16);
+  }
   // 1. row rs of every digit's extended polynomial, NTT domain, natural order
   for (int j = 0; j < A.ndig; ++j) {
     u64* X = wsm + j * C;
@@ -708,9 +728,28 @@ __global__ void __launch_bounds__(kWarps * 32, LOGC >= 9 ? 1 : 2) ks_sum_kernel(
     }
     terms = 0;
   };
+  // L1 prefetch of a job's rows (source digit rows, key rows, c0 row): lanes
+  // 0..C/16-1 each touch one 128-byte line of every row
+  auto prefetch_job = [&](int j2) {
+    const int s2 = A.jsrc[j2];
+    const u64 g2 = A.g[j2];
+    if (g2 <= 1 || lane >= C / 16) return;
+    const int rs2 = (int)RowPerm<LOGR, LOGC>(rd, g2).src_row;
+    const size_t lo16 = (size_t)lane * 16;
+    for (int j = 0; j < A.ndig; ++j) {
+      const int lo = j * A.alpha, hi = min(lo + A.alpha, A.limbs);
+      prefetch_l1(((t >= lo && t < hi) ? A.c1[s2] + (size_t)t * n : A.ext[s2] + ((size_t)j * A.nt + t) * n) +
+                  (size_t)rs2 * C + lo16);
+      prefetch_l1(A.key[j2] + ((size_t)(j * 2 + 0) * A.np + m) * n + rowoff + lo16);
+      prefetch_l1(A.key[j2] + ((size_t)(j * 2 + 1) * A.np + m) * n + rowoff + lo16);
+    }
+    if (qt) prefetch_l1(A.c0[s2] + (size_t)t * n + (size_t)rs2 * C + lo16);
+  };
+  if (A.out_begin[o] < A.out_begin[o + 1]) prefetch_job(A.out_begin[o]);
   for (int jb = A.out_begin[o]; jb < A.out_begin[o + 1]; ++jb) {
     const int s = A.jsrc[jb];
     const u64 g = A.g[jb];
+    if (jb + 1 < A.out_begin[o + 1]) prefetch_job(jb + 1);
     if (terms >= 7) fold();
     if (g <= 1) {  // identity term: P * (c0, c1) on the Q primes
       if (!qt) continue;
