@@ -728,28 +728,9 @@ __global__ void __launch_bounds__(kWarps * 32, LOGC >= 9 ? 1 : 2) ks_sum_kernel(
     }
     terms = 0;
   };
-  // L1 prefetch of a job's rows (source digit rows, key rows, c0 row): lanes
-  // 0..C/16-1 each touch one 128-byte line of every row
-  auto prefetch_job = [&](int j2) {
-    const int s2 = A.jsrc[j2];
-    const u64 g2 = A.g[j2];
-    if (g2 <= 1 || lane >= C / 16) return;
-    const int rs2 = (int)RowPerm<LOGR, LOGC>(rd, g2).src_row;
-    const size_t lo16 = (size_t)lane * 16;
-    for (int j = 0; j < A.ndig; ++j) {
-      const int lo = j * A.alpha, hi = min(lo + A.alpha, A.limbs);
-      prefetch_l1(((t >= lo && t < hi) ? A.c1[s2] + (size_t)t * n : A.ext[s2] + ((size_t)j * A.nt + t) * n) +
-                  (size_t)rs2 * C + lo16);
-      prefetch_l1(A.key[j2] + ((size_t)(j * 2 + 0) * A.np + m) * n + rowoff + lo16);
-      prefetch_l1(A.key[j2] + ((size_t)(j * 2 + 1) * A.np + m) * n + rowoff + lo16);
-    }
-    if (qt) prefetch_l1(A.c0[s2] + (size_t)t * n + (size_t)rs2 * C + lo16);
-  };
-  if (A.out_begin[o] < A.out_begin[o + 1]) prefetch_job(A.out_begin[o]);
   for (int jb = A.out_begin[o]; jb < A.out_begin[o + 1]; ++jb) {
     const int s = A.jsrc[jb];
     const u64 g = A.g[jb];
-    if (jb + 1 < A.out_begin[o + 1]) prefetch_job(jb + 1);
     if (terms >= 7) fold();
     if (g <= 1) {  // identity term: P * (c0, c1) on the Q primes
       if (!qt) continue;
@@ -934,6 +915,215 @@ __global__ void __launch_bounds__(kWarps * 32, LOGC >= 9 ? 1 : 2) ks_sum_kernel(
   }
 }
 
+// ------------------------------------------ rotation-sum row, TMA pipelined
+// Single-digit rotation sums at C = 256 (the QK^T folds and pack at level 1,
+// two thirds of the rotation-sum time): ks_sum_kernel's pair-strided register
+// math, but every row a job reads (its digit row, the two key rows, the c0 row;
+// 2 KB each, contiguous) arrives in shared memory by 1D bulk copies
+// (cp.async.bulk, the TMA engine) on a per-warp double-buffered mbarrier ring:
+// lane 0 issues job i+1's copies before the warp computes job i, so the L2
+// latency that left ks_sum long-scoreboard bound (profiles/r2_ncu: 3.4 stall
+// cycles per issue) overlaps the previous job's arithmetic, with no registers
+// held for the prefetch. Four warps (rows) per CTA, 72 KB of shared memory.
+namespace tma1d {
+__device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(saddr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   saddr(dst)),
+               "l"(src), "r"(bytes), "r"(saddr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+}  // namespace tma1d
+
+constexpr int kTmaWarps = 4;
+constexpr int kTmaRows = 4;  // per stage: digit row, key b row, key a row, c0 row
+template <int LOGR, bool PM1>
+__global__ void __launch_bounds__(kTmaWarps * 32, 3) ks_sum_tma_kernel(KsSumArgs A, Tabs T) {
+  constexpr int LOGC = 8, C = 1 << LOGC, E = 8, LOGN = LOGR + LOGC;
+  constexpr int tiles = (1 << LOGR) / kTmaWarps;
+  constexpr int n = 1 << LOGN;
+  extern __shared__ __align__(128) u64 tma_sm[];  // [warp][2 stages][kTmaRows][C], [warp][C], mbarriers
+  const int tile = blockIdx.x % tiles, rest = blockIdx.x / tiles;
+  const int t = rest % A.nt, o = rest / A.nt;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rd = tile * kTmaWarps + warp;
+  const int m = A.tprime[t];
+  const u64 q = T.q[m], mh = T.mh[m], qn = T.qn[m];
+  const bool qt = t < A.limbs;
+  const u64 pm = qt ? A.pm[t] : 0;
+  u64* stage_base = tma_sm + (size_t)warp * 2 * kTmaRows * C;
+  u64* buf = tma_sm + (size_t)kTmaWarps * 2 * kTmaRows * C + (size_t)warp * C;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(tma_sm + (size_t)kTmaWarps * (2 * kTmaRows + 1) * C) + warp * 2;
+  auto eoff = [&](int k) { return 64 * (k >> 1) + 2 * lane; };
+  auto xp = [](uint32_t i) { return i ^ ((i >> 4) & 1u); };
+  const size_t rowoff = (size_t)rd * C;
+  const int b0 = A.out_begin[o], b1 = A.out_begin[o + 1];
+  if (lane == 0) {
+    tma1d::mbar_init(&bars[0], 1);
+    tma1d::mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const uint32_t row_bytes = C * sizeof(u64);
+  // lane 0: arm stage st's barrier and copy job jb's rows into it
+  auto issue = [&](int jb, int st) {
+    if (lane != 0) return;
+    const int s = A.jsrc[jb];
+    const int rs = (int)RowPerm<LOGR, LOGC>(rd, A.g[jb]).src_row;
+    u64* dst = stage_base + (size_t)st * kTmaRows * C;
+    tma1d::fence_proxy_async();  // the warp's earlier shared-memory reads of this stage come first
+    tma1d::mbar_expect_tx(&bars[st], (qt ? 4 : 3) * row_bytes);
+    const u64* src = (t < A.alpha && t < A.limbs) ? A.c1[s] + (size_t)t * n : A.ext[s] + (size_t)t * n;
+    tma1d::bulk_g2s(dst, src + (size_t)rs * C, row_bytes, &bars[st]);
+    tma1d::bulk_g2s(dst + C, A.key[jb] + (size_t)m * n + rowoff, row_bytes, &bars[st]);
+    tma1d::bulk_g2s(dst + 2 * C, A.key[jb] + ((size_t)A.np + m) * n + rowoff, row_bytes, &bars[st]);
+    if (qt) tma1d::bulk_g2s(dst + 3 * C, A.c0[s] + (size_t)t * n + (size_t)rs * C, row_bytes, &bars[st]);
+  };
+  auto next_rot = [&](int jb) {  // first non-identity job at or after jb
+    while (jb < b1 && A.g[jb] <= 1) ++jb;
+    return jb;
+  };
+  U128 sb[E], sa[E];
+#pragma unroll
+  for (int k = 0; k < E; ++k) sb[k] = U128{0, 0}, sa[k] = U128{0, 0};
+  int terms = 0;  // jobs since the last high-word reduction (see ks_sum_kernel)
+  auto fold = [&]() {
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      sb[k].hi = reduce64(sb[k].hi, q, mh);
+      sa[k].hi = reduce64(sa[k].hi, q, mh);
+    }
+    terms = 0;
+  };
+  int cur = next_rot(b0), st = 0;
+  uint32_t phase = 0;  // bit st: parity of stage st's next completion
+  if (cur < b1) issue(cur, 0);
+  for (int jb = b0; jb < b1; ++jb) {
+    const int s = A.jsrc[jb];
+    const u64 g = A.g[jb];
+    if (terms >= 7) fold();
+    if (g <= 1) {  // identity term: P * (c0, c1) on the Q primes, straight from global memory
+      if (!qt) continue;
+#pragma unroll
+      for (int k = 0; k < E; k += 2) {
+        const ulonglong2 v0 = *reinterpret_cast<const ulonglong2*>(A.c0[s] + (size_t)t * n + rowoff + eoff(k));
+        const ulonglong2 v1 = *reinterpret_cast<const ulonglong2*>(A.c1[s] + (size_t)t * n + rowoff + eoff(k));
+        if constexpr (PM1) {
+          sb[k].hi += v0.x;
+          sb[k + 1].hi += v0.y;
+          sa[k].hi += v1.x;
+          sa[k + 1].hi += v1.y;
+        } else {
+          mac128(sb[k], v0.x, pm);
+          mac128(sb[k + 1], v0.y, pm);
+          mac128(sa[k], v1.x, pm);
+          mac128(sa[k + 1], v1.y, pm);
+        }
+      }
+      ++terms;
+      continue;
+    }
+    // jb == cur: its rows are in (or on their way to) stage st; start the next job's copies
+    const int nxt = next_rot(jb + 1);
+    if (nxt < b1) issue(nxt, st ^ 1);
+    tma1d::mbar_wait(&bars[st], (phase >> st) & 1);
+    phase ^= 1u << st;
+    const u64* X = stage_base + (size_t)st * kTmaRows * C;
+    const RowPerm<LOGR, LOGC> rp(rd, g);
+    const ShflPermQ sp(rp.base, rp.slope, lane);
+    u64 x[E];
+#pragma unroll
+    for (int k = 0; k < E; k += 2) {
+      const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(X + eoff(k));
+      x[k] = v.x, x[k + 1] = v.y;
+    }
+    sp.apply(x);
+#pragma unroll
+    for (int k = 0; k < E; k += 2) {
+      const ulonglong2 kb = *reinterpret_cast<const ulonglong2*>(X + C + eoff(k));
+      const ulonglong2 ka = *reinterpret_cast<const ulonglong2*>(X + 2 * C + eoff(k));
+      mac128(sb[k], x[k], kb.x);
+      mac128(sa[k], x[k], ka.x);
+      mac128(sb[k + 1], x[k + 1], kb.y);
+      mac128(sa[k + 1], x[k + 1], ka.y);
+    }
+    if (qt) {  // P * sigma_g(c0)
+#pragma unroll
+      for (int k = 0; k < E; k += 2) {
+        const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(X + 3 * C + eoff(k));
+        x[k] = v.x, x[k + 1] = v.y;
+      }
+      sp.apply(x);
+#pragma unroll
+      for (int k = 0; k < E; ++k) {
+        if constexpr (PM1)
+          sb[k].hi += x[k];
+        else
+          mac128(sb[k], x[k], pm);
+      }
+    }
+    __syncwarp();  // every lane is done with stage st before lane 0 refills it
+    st ^= 1;
+    ++terms;
+  }
+  u64 vb[E], va[E];
+#pragma unroll
+  for (int k = 0; k < E; ++k) {
+    vb[k] = mont_finish(sb[k], q, mh, qn);
+    va[k] = mont_finish(sa[k], q, mh, qn);
+  }
+  u64* accb = A.acc[o] + (size_t)t * n;
+  u64* acca = A.acc[o] + (size_t)(A.nt + t) * n;
+  if (qt && t < A.inv_from) {
+#pragma unroll
+    for (int k = 0; k < E; k += 2) {
+      *reinterpret_cast<ulonglong2*>(accb + rowoff + eoff(k)) = make_ulonglong2(vb[k], vb[k + 1]);
+      *reinterpret_cast<ulonglong2*>(acca + rowoff + eoff(k)) = make_ulonglong2(va[k], va[k + 1]);
+    }
+  } else {  // special prime (or merged q_top): ModDown's inverse row pass, strided stores
+    const u64* W = T.ipsi + ((size_t)m << LOGN);
+    const u64* Ws = T.ipsi_s + ((size_t)m << LOGN);
+    auto tw = [&](int b, int blk, u64& w, u64& ws) {
+      const int i = (1 << (LOGN - 1 - b)) + (rd << (LOGC - 1 - b)) + blk;
+      w = W[i];
+      ws = Ws[i];
+    };
+    auto restride = [&](u64 (&v)[E]) {
+#pragma unroll
+      for (int k = 0; k < E; ++k) buf[xp(eoff(k & ~1) + (k & 1))] = v[k];
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < E; ++k) v[k] = buf[xp(lane + 32 * k)];
+      __syncwarp();
+    };
+    restride(vb);
+    warp_inv<LOGC, kStrided>(vb, buf, lane, q, tw);
+    restride(va);
+    warp_inv<LOGC, kStrided>(va, buf, lane, q, tw);
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      accb[(size_t)rd * C + lane + 32 * k] = vb[k];
+      acca[(size_t)rd * C + lane + 32 * k] = va[k];
+    }
+  }
+}
+
 template <int LOGR, int LOGC>
 void run_two_pass(Context& c, const LimbBatch& b, bool inverse) {
   const unsigned rows_grid = (unsigned)b.count * ((1u << LOGR) / kWarps);
@@ -1025,6 +1215,24 @@ void run_ks_row(Context& c, const KsRowArgs& a) {
 
 template <int LOGR, int LOGC>
 void run_ks_sum(Context& c, const KsSumArgs& a) {
+  if constexpr (LOGC == 8) {
+    // single-digit sums: the TMA-pipelined row stage (SF_VARIANT bit 6: off, for A/B)
+    if (a.ndig == 1 && !(c.variant & 64)) {
+      constexpr size_t sm = (size_t)kTmaWarps * (2 * kTmaRows + 1) * 256 * sizeof(u64) + kTmaWarps * 2 * sizeof(u64);
+      static bool attr = false;
+      if (!attr) {
+        SF_CUDA(cudaFuncSetAttribute(ks_sum_tma_kernel<LOGR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        SF_CUDA(cudaFuncSetAttribute(ks_sum_tma_kernel<LOGR, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        attr = true;
+      }
+      const unsigned grid = (unsigned)(a.nout * a.nt * ((1 << LOGR) / kTmaWarps));
+      if (a.pm_one)
+        ks_sum_tma_kernel<LOGR, true><<<grid, kTmaWarps * 32, sm, c.stream>>>(a, c.tabs);
+      else
+        ks_sum_tma_kernel<LOGR, false><<<grid, kTmaWarps * 32, sm, c.stream>>>(a, c.tabs);
+      return;
+    }
+  }
   const unsigned grid = (unsigned)(a.nout * a.nt * ((1 << LOGR) / kWarps));
   // default: automorphism gather by warp shuffles (-2% family time vs shared-memory staging);
   // SF_VARIANT bit 3: shared-memory staging with the key loads issued first (-4% vs bit 0:
