@@ -1241,6 +1241,9 @@ def main():
     if dist:
         e2e_ms = reduce_ranks(dist, e2e_ms, dist.ReduceOp.MAX)
 
+    graph_kernels = graph.kernel_launches
+    del graph, gouts, res  # the timed graph's memory is not the stream's to fight over
+    be.synchronize()
     phases = layer.phase_ms(args.steps)  # last: its graph's memory must not disturb the timed graph
     stream = None
     if not args.no_stream:
@@ -1321,7 +1324,7 @@ def main():
         "host_issue_ms_per_step_queued": round(t_host, 3),
         "host_profile": hprof,
         "eager_ms_per_step": round(ms_eager, 3),
-        "execution": f"CUDA graph of the whole decode step ({graph.kernel_launches} kernels), replayed per token",
+        "execution": f"CUDA graph of the whole decode step ({graph_kernels} kernels), replayed per token",
         "clocks": clk.summary(),
         "ledger_per_step": {k: v // args.steps for k, v in counts.asdict().items()},
         "kernel_families": prof,

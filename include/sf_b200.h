@@ -257,14 +257,14 @@ sf_status sf_vmm_partial(sf_context* ctx, const sf_ct* x, const sf_vmm_plan* pla
 sf_status sf_vmm_finish(sf_context* ctx, const sf_ct* acc, const sf_vmm_plan* plan, int mask_output, sf_ct** out);
 sf_status sf_qk_dot_partial(sf_context* ctx, const sf_ct* q, const sf_kvcache* cache, int rank, int world,
                             sf_ct** maps_out, int* n_maps);
-/* Score*V partial = the rank's lazily relinearised product sum, a degree-2
- * ciphertext returned as two handles: out2[0] = (d0, d1), out2[1] = (d2, 0).
- * finish sums the n ranks' partials, relinearises + rescales once, folds the
- * lanes and masks (kv_attention.cpp:230-238). */
+/* Score*V partial = the rank's share of the baby-step / giant-step product
+ * sum (whole giant groups G mod 8 with (G mod 8) mod world ==
+ * rank), one relinearised ciphertext one level below the maps. finish sums the
+ * n ranks' partials, folds the lanes and masks (kv_attention.cpp:227-238). */
 sf_status sf_softmax_times_v_partial(sf_context* ctx, const sf_ct* const* probs, int n_probs,
-                                     const sf_kvcache* cache, int rank, int world, sf_ct** out2);
-sf_status sf_softmax_times_v_finish(sf_context* ctx, const sf_ct* const* parts01, const sf_ct* const* parts2,
-                                    int n, const sf_kvcache* cache, sf_ct** out);
+                                     const sf_kvcache* cache, int rank, int world, sf_ct** out);
+sf_status sf_softmax_times_v_finish(sf_context* ctx, const sf_ct* const* parts, int n, const sf_kvcache* cache,
+                                    sf_ct** out);
 sf_status sf_sum_partials(sf_context* ctx, const sf_ct* const* parts, int n, sf_ct** out);
 /* multi-VMM of one input (sf_vmm_interleaved_multi) split the same way: one
  * partial accumulator per plan; finish = batched reduce ladders + masks */

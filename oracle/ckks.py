@@ -73,6 +73,7 @@ def lib():
             "ock_rot_sum_rescale": (vp, [vp, C.POINTER(vp), C.POINTER(C.c_int), C.c_int]),
             "ock_mac_plain_lazy": (vp, [vp, C.POINTER(vp), DP, C.c_int]),
             "ock_relin_rescale": (vp, [vp, vp]),
+            "ock_relin": (vp, [vp, vp]),
             "ock_ct_is_three": (C.c_int, [vp]),
             "ock_ct_d2": (None, [vp, U64P]),
             "ock_ct_set_d2": (None, [vp, U64P]),
@@ -195,6 +196,8 @@ class CkksParams:
 class CkksOracle:
     """slotforge-shaped backend over the CPU CKKS oracle."""
 
+    sv_bsgs = True  # Score*V as the product's baby-step / giant-step sum (DESIGN.md §3.9)
+
     def __init__(self, N: int, L: int, **kw):
         if not is_pow2(N):
             raise ShapeMismatch("engine: N must be a power of two")
@@ -299,6 +302,16 @@ class CkksOracle:
 
     def relin_rescale(self, x) -> OCt:
         return OCt(self, lib().ock_relin_rescale(self.ptr, x.ptr), x.level - 1, None)
+
+    def relin(self, x) -> OCt:
+        """Relinearise a degree-2 ciphertext without rescaling."""
+        return OCt(self, lib().ock_relin(self.ptr, x.ptr), x.level, None)
+
+    def rescale(self, x) -> OCt:
+        """Rescale by the top prime (off-ledger)."""
+        if x.level <= 0:
+            raise LevelUnderflow("rescale: no level left")
+        return OCt(self, lib().ock_rescale(self.ptr, x.ptr), x.level - 1, x.layout)
 
     def mul_sum(self, pairs) -> OCt:
         return self.relin_rescale(self.tensor_sum(pairs))

@@ -901,6 +901,32 @@ Ct* relin_rescale(Ctx& c, const Ct* x) {
                               x->scale / (double)c.primes[limbs - 1]);
 }
 
+// Relinearisation without the rescale (the Score*V giants):
+// (d0, d1) + the hybrid key switch of d2 under the relinearisation key, same
+// limbs and scale.
+Ct* relin(Ctx& c, const Ct* x) {
+  const int limbs = x->limbs, n = c.n;
+  Ct* out = new_ct(c, limbs, x->scale);
+  if (x->zero) {
+    out->zero = true;
+    return out;
+  }
+  if (x->d2.empty()) throw std::runtime_error("relin: not a degree-2 ciphertext");
+  std::vector<u64> kb((size_t)limbs * n), ka((size_t)limbs * n);
+  key_switch(c, x->d2.data(), limbs, 0, kb.data(), ka.data());
+  for (int part = 0; part < 2; ++part) {
+    const u64* k = part ? ka.data() : kb.data();
+#pragma omp parallel for
+    for (int l = 0; l < limbs; ++l) {
+      const u64 q = c.primes[l];
+      const u64* d = poly(c, x, part, l);
+      u64* o = poly(c, out, part, l);
+      for (int i = 0; i < n; ++i) o[i] = addmod(d[i], k[(size_t)l * n + i], q);
+    }
+  }
+  return out;
+}
+
 // sum_k ct_k (*) pt_k with plaintexts encoded at scale q_top (so the scale is
 // preserved), one rescale at the end (lazy rescale of a MAC).
 Ct* mac_plain(Ctx& c, const Ct* const* cts, const double* slots, int k, bool rescale_out = true) {
@@ -1115,6 +1141,9 @@ void* ock_tensor_sum(void* c, void** a, void** b, int k) {
 }
 void* ock_relin_rescale(void* c, void* a) {
   return guard([&]() -> void* { return relin_rescale(*static_cast<Ctx*>(c), (Ct*)a); });
+}
+void* ock_relin(void* c, void* a) {
+  return guard([&]() -> void* { return relin(*static_cast<Ctx*>(c), (Ct*)a); });
 }
 int ock_ct_is_three(void* ct) { return static_cast<Ct*>(ct)->d2.empty() ? 0 : 1; }
 void ock_ct_d2(void* ct, uint64_t* out) {

@@ -478,6 +478,9 @@ def softmax_times_v(be, probs, cache: KVCache, cfg):
         raise ShapeMismatch(f"softmax_times_v: expected {n_maps} probability maps, got {len(probs)}")
     if len(cache.v_cts) < n_maps:
         raise ShapeMismatch("softmax_times_v: value cache is missing groups")
+    if getattr(be, "sv_bsgs", False):
+        # CKKS backends: the baby-step / giant-step form
+        return sv_finish(be, [sv_partial(be, probs, cache, cfg, 0, 1)], cfg)
     pairs = []
     for g in range(n_maps):
         tokens = min(gt, cache.n_prime - g * gt)
@@ -485,11 +488,99 @@ def softmax_times_v(be, probs, cache: KVCache, cfg):
         for w in range(lo, hi):
             scores = be.rotate(probs[g], -w * t) if w else probs[g]
             pairs.append((scores, cache.v_cts[g][v_variant_index(cfg, w)]))
-    # sum of the products (kv_attention.cpp:230-235); CKKS backends evaluate it
-    # with one lazy relinearisation, same ledger charge
+    # sum of the products (kv_attention.cpp:230-235)
     acc = be.mul_sum(pairs)
     folded = fold_lanes(be, acc, t)
     out = be.mul_plain(folded, stride_mask(cfg.N, t, 0))
+    return be.with_layout(out, make_interleaved(cfg.d, cfg.N, 0, cfg.H))
+
+
+SV_GROUPS = 8  # giant groups of the Score*V giant rotation sums
+
+
+def sv_baby(cfg):
+    """Baby-step count B: the least power of two with B^2 >= #variants."""
+    b, nv = 1, v_variant_count(cfg)
+    while b * b < nv:
+        b <<= 1
+    return b
+
+
+def sv_partial(be, probs, cache: KVCache, cfg, rank, world):
+    """Score*V over the giant groups a rank owns, as a baby-step / giant-step
+    sum (mirrors csrc/protocols.cpp softmax_times_v_partial):
+    with w = G B + b,  sum_(g,w) Rot(P_g, -w t) (x) V[g][w]
+      = sum_G Rot( sum_(g,b) Rot(P_g, -b t) (x) Rot(V[g][w], G B t), -G B t ),
+    inner sums lazily relinearised (one relinearisation per giant), giants as
+    one rotation sum per group G mod SV_GROUPS at the products' scale (the
+    rescale happens once, in sv_finish). Charged as the reference's
+    rotations / ct-ct mults / additions of the owned (g, w) pairs
+    (kv_attention.cpp:227-235)."""
+    t, gt, N = cfg.t, cfg.group_tokens, cfg.N
+    B = sv_baby(cfg)
+    own = []
+    for g in range(len(probs)):
+        tokens = min(gt, cache.n_prime - g * gt)
+        lo, hi = touched_variants(cfg, tokens)
+        for w in range(lo, hi):
+            G = w // B
+            if (G % SV_GROUPS) % world == rank:
+                own.append((g, w, G, w - G * B))
+    for g, w, _, _ in own:
+        if (-w * t) % N:
+            be.ledger.count_rotation(False)
+    for _ in own:
+        be.ledger.count_ct_ct()
+    for _ in range(len(own) - 1):
+        be.ledger.count_add()
+    lvl = min(probs[0].level, cache.v_cts[0][0].level)
+    if not own:
+        return be.zeros(lvl)
+    led, be.ledger = be.ledger, type(be.ledger)()
+    try:
+        babies = {}
+        inner = {}
+        for g, w, G, b in own:
+            if (g, b) not in babies:
+                babies[(g, b)] = be.rotate(probs[g], -b * t, hoisted=True) if b else probs[g]
+            v = cache.v_cts[g][v_variant_index(cfg, w)]
+            if not v.is_zero and (G * B * t) % N:
+                v = be.rotate(v, G * B * t)
+            inner.setdefault(G, []).append((babies[(g, b)], v))
+        rel = {}
+        for G in sorted(inner):
+            live = [(a, v) for a, v in inner[G] if not (a.is_zero or v.is_zero)]
+            if live:
+                rel[G] = be.relin(be.tensor_sum(live))
+        if not rel:
+            return be.zeros(lvl)
+        acc = None
+        for r in range(SV_GROUPS):
+            terms = [(rel[G], -G * B * t) for G in sorted(rel) if G % SV_GROUPS == r]
+            if terms:
+                s = be.rot_sum(terms)
+                acc = s if acc is None else be.add(acc, s)
+    finally:
+        be.ledger = led
+    return be.with_layout(acc, None)
+
+
+def sv_finish(be, parts, cfg):
+    """Sum of the ranks' Score*V partials (charged live - 1 additions), one
+    rescale, then fold_lanes and the stride mask (kv_attention.cpp:236-240)."""
+    live = [p for p in parts if not p.is_zero]
+    for _ in range(len(live) - 1):
+        be.ledger.count_add()
+    led, be.ledger = be.ledger, type(be.ledger)()
+    try:
+        acc = parts[0] if not live else live[0]
+        for p in live[1:]:
+            acc = be.add(acc, p)
+        acc = be.rescale(acc) if live else be.zeros(acc.level - 1)
+    finally:
+        be.ledger = led
+    folded = fold_lanes(be, acc, cfg.t)
+    out = be.mul_plain(folded, stride_mask(cfg.N, cfg.t, 0))
     return be.with_layout(out, make_interleaved(cfg.d, cfg.N, 0, cfg.H))
 
 

@@ -5,8 +5,8 @@ qk_dot_partial, softmax_times_v_partial / _finish) over any slotforge-shaped
 backend, so the multi-process tests can check on CPU (gloo, world_size 2) that
 partial results exchanged between ranks and summed mod q reproduce the
 single-device ciphertexts bit for bit. Ownership rules: VMM giant steps
-g2 = rank mod world; K ciphertexts j = rank mod world; Score*V (group, variant)
-pairs by running index mod world.
+g2 = rank mod world; K ciphertexts j = rank mod world; Score*V whole giant groups
+(G mod 8) mod world == rank.
 """
 from __future__ import annotations
 
@@ -73,27 +73,13 @@ def qk_dot_partial(be, q, cache, cfg, rank, world):
 
 
 def softmax_times_v_partial(be, probs, cache, cfg, rank, world):
-    """The rank's degree-2 (lazily relinearised) product sum."""
-    t, gt = cfg.t, cfg.group_tokens
-    pairs, idx = [], 0
-    for g in range(len(probs)):
-        tokens = min(gt, cache.n_prime - g * gt)
-        lo, hi = P.touched_variants(cfg, tokens)
-        for w in range(lo, hi):
-            if idx % world == rank:
-                scores = be.rotate(probs[g], -w * t) if w else probs[g]
-                pairs.append((scores, cache.v_cts[g][P.v_variant_index(cfg, w)]))
-            idx += 1
-    if not pairs:
-        return be.zeros(min(probs[0].level, cache.v_cts[0][0].level))
-    return be.tensor_sum(pairs)
+    """The rank's share of the baby-step / giant-step Score*V sum (whole giant groups)."""
+    return P.sv_partial(be, probs, cache, cfg, rank, world)
 
 
 def softmax_times_v_finish(be, parts, cfg):
-    """Sum the degree-2 partials, relinearise + rescale once, fold, mask."""
-    folded = P.fold_lanes(be, be.relin_rescale(sum_partials(be, parts)), cfg.t)
-    out = be.mul_plain(folded, stride_mask(cfg.N, cfg.t, 0))
-    return be.with_layout(out, make_interleaved(cfg.d, cfg.N, 0, cfg.H))
+    """Sum the partials, fold the lanes, mask."""
+    return P.sv_finish(be, parts, cfg)
 
 
 def sum_partials(be, parts):

@@ -121,7 +121,7 @@ SIGNATURES = {
     "sf_vmm_finish": (st, [vp, vp, vp, C.c_int, vpp]),
     "sf_qk_dot_partial": (st, [vp, vp, vp, C.c_int, C.c_int, vpp, ip]),
     "sf_softmax_times_v_partial": (st, [vp, vpp, C.c_int, vp, C.c_int, C.c_int, vpp]),
-    "sf_softmax_times_v_finish": (st, [vp, vpp, vpp, C.c_int, vp, vpp]),
+    "sf_softmax_times_v_finish": (st, [vp, vpp, C.c_int, vp, vpp]),
     "sf_sum_partials": (st, [vp, vpp, C.c_int, vpp]),
     "sf_vmm_multi_partial": (st, [vp, vp, vpp, C.c_int, C.c_int, C.c_int, vpp]),
     "sf_vmm_multi_finish": (st, [vp, vpp, vpp, C.c_int, C.c_int, vpp]),

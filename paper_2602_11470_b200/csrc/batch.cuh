@@ -271,5 +271,8 @@ Ct3 tensor_sum(Context& c, const std::vector<const Ct*>& a, const std::vector<co
 Ct3 add_ct3(Context& c, const std::vector<const Ct3*>& xs);
 // relinearise (key switch d2 under s^2) and rescale
 Ct relin_rescale(Context& c, const Ct3& x);
+// relinearise many degree-2 ciphertexts (one batched ModUp and key switch),
+// rescaled in the ModDown's conversion (merged) or not (same level and scale)
+std::vector<Ct> relin_batch(Context& c, const std::vector<const Ct3*>& xs, bool rescale);
 
 }  // namespace sf

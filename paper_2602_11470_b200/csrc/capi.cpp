@@ -689,28 +689,19 @@ sf_status sf_qk_dot_partial(sf_context* ctx, const sf_ct* q, const sf_kvcache* c
   });
 }
 sf_status sf_softmax_times_v_partial(sf_context* ctx, const sf_ct* const* probs, int n_probs,
-                                     const sf_kvcache* cache, int rank, int world, sf_ct** out2) {
+                                     const sf_kvcache* cache, int rank, int world, sf_ct** out) {
   return guard([&] {
     std::vector<sf::Ct> p;
     for (int i = 0; i < n_probs; ++i) p.push_back(probs[i]->v);
-    sf::Ct3 r = sf::softmax_times_v_partial(*ctx->c, p, cache->kv, rank, world);
-    r.d01.zero = r.d2.zero = r.zero;
-    out2[0] = wrap(std::move(r.d01));
-    out2[1] = wrap(std::move(r.d2));
+    *out = wrap(sf::softmax_times_v_partial(*ctx->c, p, cache->kv, rank, world));
   });
 }
-sf_status sf_softmax_times_v_finish(sf_context* ctx, const sf_ct* const* parts01, const sf_ct* const* parts2,
-                                    int n, const sf_kvcache* cache, sf_ct** out) {
+sf_status sf_softmax_times_v_finish(sf_context* ctx, const sf_ct* const* parts, int n, const sf_kvcache* cache,
+                                    sf_ct** out) {
   return guard([&] {
     sf::require(n >= 1, sf::kShapeMismatch, "softmax_times_v_finish: need at least one part");
-    std::vector<sf::Ct3> parts(n);
-    std::vector<const sf::Ct3*> pp;
-    for (int i = 0; i < n; ++i) {
-      parts[i].d01 = parts01[i]->v;
-      parts[i].d2 = parts2[i]->v;
-      parts[i].zero = parts01[i]->v.zero;
-      pp.push_back(&parts[i]);
-    }
+    std::vector<const sf::Ct*> pp;
+    for (int i = 0; i < n; ++i) pp.push_back(&parts[i]->v);
     *out = wrap(sf::softmax_times_v_finish(*ctx->c, pp, cache->kv));
   });
 }

@@ -225,27 +225,16 @@ Ct softmax_times_v_sharded(Context& c, const std::vector<Ct>& probs, const KV& c
   SF_HPROF("softmax_times_v_sharded");
   int rank, world;
   rank_world(c, rank, world);
-  Ct3 part = softmax_times_v_partial(c, probs, cache, rank, world);
-  part.d01.zero = part.d2.zero = part.zero;
+  Ct part = softmax_times_v_partial(c, probs, cache, rank, world);
   if (c.p2p) {  // the parts' sum over peer memory; finish charges the exchange additions once
     std::vector<int> live;
-    std::vector<Ct> sum = p2p_sum_cts(c, {&part.d01, &part.d2}, "sv:" + std::to_string(cache.n_prime), false, &live);
-    Ct3 tot;
-    tot.d01 = sum[0];
-    tot.d2 = sum[1];
-    tot.zero = live[0] == 0;
+    std::vector<Ct> sum = p2p_sum_cts(c, {&part}, "sv:" + std::to_string(cache.n_prime), false, &live);
     if (live[0] > 1) c.ledger.add(live[0] - 1);
-    return softmax_times_v_finish(c, {&tot}, cache);
+    return softmax_times_v_finish(c, {&sum[0]}, cache);
   }
-  auto got = allgather_cts(c, {&part.d01, &part.d2}, "sv:" + std::to_string(cache.n_prime));
-  std::vector<Ct3> parts(c.world);
-  std::vector<const Ct3*> pp;
-  for (int r = 0; r < c.world; ++r) {
-    parts[r].d01 = got[r][0];
-    parts[r].d2 = got[r][1];
-    parts[r].zero = got[r][0].zero && got[r][1].zero;
-    pp.push_back(&parts[r]);
-  }
+  auto got = allgather_cts(c, {&part}, "sv:" + std::to_string(cache.n_prime));
+  std::vector<const Ct*> pp;
+  for (int r = 0; r < c.world; ++r) pp.push_back(&got[r][0]);
   return softmax_times_v_finish(c, pp, cache);
 }
 

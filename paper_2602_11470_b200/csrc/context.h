@@ -223,6 +223,15 @@ struct Context {
   std::map<int, std::vector<u64>> level_consts_h;
   std::map<int, BufPtr> merged_consts;               // (q_top P)^-1 per limb count (merged relin + rescale)
   std::map<int, std::vector<u64>> merged_consts_h;  // host copies (row-pass epilogue parameters)
+  // Rot(V, r) of value-cache ciphertexts for the BSGS Score*V:
+  // kept while the source buffer lives (a completed cache group's variants are
+  // rotated once, not once per decode step); never filled while capturing
+  struct RotMemo {
+    std::weak_ptr<Buf> src;
+    int limbs, r;
+    Ct out;
+  };
+  std::unordered_multimap<const Buf*, RotMemo> rot_memo;
 
   // pinned staging ring for host -> device uploads of fresh plaintexts and
   // encryptions (upload_async): the copy is stream-ordered and the host returns

@@ -97,6 +97,7 @@ Context::~Context() {
   keys_r.clear();
   conv_plans.clear();
   pt_cache.clear();
+  rot_memo.clear();
   level_consts.clear();
   merged_consts.clear();
   sk.reset();

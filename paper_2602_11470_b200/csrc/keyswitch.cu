@@ -1093,6 +1093,36 @@ Ct relin_rescale(Context& c, const Ct3& x) {
   return t;
 }
 
+std::vector<Ct> relin_batch(Context& c, const std::vector<const Ct3*>& xs, bool rescale) {
+  SF_HPROF("relin_batch");
+  std::vector<Ct> out(xs.size());
+  std::map<int, std::vector<int>> by_limbs;
+  for (size_t i = 0; i < xs.size(); ++i) {
+    if (xs[i]->zero)
+      out[i] = zeros(c, xs[i]->d01.level() - (rescale ? 1 : 0));
+    else
+      by_limbs[std::min(xs[i]->d01.limbs, xs[i]->d2.limbs)].push_back((int)i);
+  }
+  for (auto& [limbs, idx] : by_limbs) {
+    for (size_t s0 = 0; s0 < idx.size(); s0 += kJobs) {
+      const int J = (int)std::min<size_t>(kJobs, idx.size() - s0);
+      std::vector<const u64*> d2;
+      for (int j = 0; j < J; ++j) d2.push_back(xs[idx[s0 + j]]->d2.c0());
+      ExtB e = mod_up_batch(c, d2, limbs);
+      std::vector<KsJob> kj;
+      for (int j = 0; j < J; ++j) {
+        const Ct3& x = *xs[idx[s0 + j]];
+        Ct t = rescale ? alloc_ct(c, limbs - 1, x.d01.scale / (double)c.primes[limbs - 1])
+                       : alloc_ct(c, limbs, x.d01.scale);
+        kj.push_back({j, 0, x.d01.c0(), x.d01.c1(c.n), t.c0(), t.c1(c.n)});
+        out[idx[s0 + j]] = std::move(t);
+      }
+      ks_jobs(c, e, kj, rescale);
+    }
+  }
+  return out;
+}
+
 // ------------------------------------------------------------- ct x pt mult
 std::vector<Ct> mul_plain_batch(Context& c, const std::vector<const Ct*>& xs, const std::vector<const Pt*>& ps,
                                 bool count, bool rescale) {

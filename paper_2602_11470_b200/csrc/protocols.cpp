@@ -847,13 +847,78 @@ std::vector<Ct> qk_dot_partial(Context& c, const Ct& q, const KV& cache, int ran
 
 std::vector<Ct> qk_dot(Context& c, const Ct& q, const KV& cache) { return qk_dot_partial(c, q, cache, 0, 1); }
 
-// kv_attention.cpp:216-241 (before the lane fold) for the (group, variant)
-// pairs this rank owns: all score alignments of one probability map share its
-// ModUp (hoisting), the rotations run as one batch, and the products are
-// accumulated as degree-2 tensors without relinearisation (lazy relin): the
-// reference's 510 ct-ct mults + 509 additions (kv_attention.cpp:230-235) cost
-// one key switch and one rescale in softmax_times_v_finish instead of 510.
-Ct3 softmax_times_v_partial(Context& c, const std::vector<Ct>& probs, const KV& cache, int rank, int world) {
+// Score*V as a baby-step / giant-step sum. The reference's
+// sum over (group g, variant w) of Rot(P_g, -w t) (x) V[g][w]
+// (kv_attention.cpp:216-241) is regrouped with w = G B + b (G = floor(w / B),
+// 0 <= b < B) and Rot(X, -G B t) (x) V = Rot(X (x) Rot(V, G B t), -G B t):
+//   sum_G Rot( sum_(g, b) Rot(P_g, -b t) (x) Rot(V[g][G B + b], G B t), -G B t ).
+// The babies Rot(P_g, -b t) share one hoisted ModUp per map, the inner sums are
+// lazily relinearised degree-2 accumulations (one relinearisation per giant,
+// both maps together), and the giants run as rotation sums, one per giant
+// group G mod kSvGroups, at the products' scale (one rescale in finish, so the
+// groups' ModDown roundings are divided by q_top): B + #giants key switches per map instead of one
+// per variant (255 at d_head 128). Rot(V, G B t) of a cache ciphertext is kept
+// with the ciphertext (Context::rot_memo): a completed group's variants are
+// rotated once. A rank owns whole giant groups (group mod world == rank), so
+// the partials summed mod q are the single-device result for any world size
+// dividing kSvGroups; each rank charges the reference's rotations / ct-ct
+// mults / additions of the (group, variant) pairs it owns.
+constexpr int kSvGroups = 8;
+
+int sv_baby(const AttnCfg& cfg) {
+  const int nv = v_variant_count(cfg);
+  int b = 1;
+  while ((long long)b * b < nv) b <<= 1;
+  return b;
+}
+
+static int floor_div(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+
+// Rot(x, r) of value-cache ciphertexts through the context's memo; results are
+// kept only where keep[i] (a completed group's variants: the growing group's
+// change with every append)
+static std::vector<Ct> rotate_memo(Context& c, const std::vector<const Ct*>& xs, const std::vector<int>& rs,
+                                   const std::vector<char>& keep) {
+  std::vector<Ct> out(xs.size());
+  for (auto it = c.rot_memo.begin(); it != c.rot_memo.end();)  // drop entries of dead sources
+    it = it->second.src.expired() ? c.rot_memo.erase(it) : std::next(it);
+  std::vector<const Ct*> miss;
+  std::vector<RotJob> jobs;
+  std::vector<int> where;
+  for (size_t i = 0; i < xs.size(); ++i) {
+    const Ct& x = *xs[i];
+    if (x.zero || pos_mod(rs[i], c.slots) == 0 || !x.buf) {
+      out[i] = x;
+      continue;
+    }
+    bool hit = false;
+    auto range = c.rot_memo.equal_range(x.buf.get());
+    for (auto it = range.first; it != range.second; ++it) {
+      const Context::RotMemo& m = it->second;
+      if (m.limbs == x.limbs && m.r == rs[i] && m.src.lock() == x.buf && m.out.scale == x.scale) {
+        out[i] = m.out;
+        hit = true;
+        break;
+      }
+    }
+    if (hit) continue;
+    where.push_back((int)i);
+    jobs.push_back({(int)miss.size(), rs[i]});
+    miss.push_back(xs[i]);
+  }
+  if (!miss.empty()) {
+    std::vector<Ct> r = rotate_batch(c, miss, jobs, false, false);
+    for (size_t k = 0; k < r.size(); ++k) {
+      const Ct& x = *xs[where[k]];
+      if (!c.capturing && keep[where[k]])
+        c.rot_memo.emplace(x.buf.get(), Context::RotMemo{x.buf, x.limbs, jobs[k].r, r[k]});
+      out[where[k]] = std::move(r[k]);
+    }
+  }
+  return out;
+}
+
+Ct softmax_times_v_partial(Context& c, const std::vector<Ct>& probs, const KV& cache, int rank, int world) {
   SF_HPROF("softmax_times_v_partial");
   const AttnCfg& cfg = cache.cfg;
   require(cache.n_prime != 0, kCacheEmpty, "softmax_times_v: no cached values");
@@ -864,42 +929,98 @@ Ct3 softmax_times_v_partial(Context& c, const std::vector<Ct>& probs, const KV& 
           "softmax_times_v: expected " + std::to_string(n_maps) + " probability maps, got " +
               std::to_string(probs.size()));
   require((int)cache.v.size() >= n_maps, kShapeMismatch, "softmax_times_v: value cache is missing groups");
-  std::vector<const Ct*> src;
-  for (const Ct& p : probs) src.push_back(&p);
-  std::vector<RotJob> jobs;
-  std::vector<std::pair<int, int>> gw;
-  int idx = 0;
+  const int B = sv_baby(cfg);
+  struct Pair {
+    int g, w, G, b;
+  };
+  std::vector<Pair> own;
+  int limbs = 1 << 30;
   for (int g = 0; g < n_maps; ++g) {
     const int tokens = std::min(gt, cache.n_prime - g * gt);
     const int u_max = (tokens - 1) / t;  // touched_variants (53-57)
     const int w_lo = cfg.H == 1 ? 0 : -u_max, w_hi = cfg.d_head();
-    for (int w = w_lo; w < w_hi; ++w, ++idx)
-      if (idx % world == rank) gw.push_back({g, w}), jobs.push_back({g, -w * t});
+    for (int w = w_lo; w < w_hi; ++w) {
+      const int G = floor_div(w, B);
+      if ((int)pos_mod(G, kSvGroups) % world != rank) continue;
+      own.push_back({g, w, G, w - G * B});
+      const Ct& v = cache.v[g][v_variant_index(cfg, w)];
+      check_ct(c, probs[g], "mul");
+      check_ct(c, v, "mul");
+      const int l = std::min(probs[g].limbs, v.limbs);
+      require(l - 1 > 0, kLevelUnderflow, "mul: no multiplicative level left");
+      limbs = std::min(limbs, l);
+    }
   }
-  if (gw.empty()) {
-    Ct3 z;
-    z.d01 = z.d2 = zeros(c, std::min(probs[0].level(), cache.v[0][0].level()));
-    return z;
+  // the reference's charges for the owned pairs (kv_attention.cpp:227-235)
+  for (const Pair& p : own)
+    if (pos_mod((long long)-p.w * t, c.slots)) c.ledger.rot(false);
+  c.ledger.ctct((long long)own.size());
+  if (own.size() > 1) c.ledger.add((long long)own.size() - 1);
+  if (own.empty()) return zeros(c, std::min(probs[0].level(), cache.v[0][0].level()));
+  // babies: Rot(P_g, -b t), one hoisted ModUp per map
+  std::vector<const Ct*> src;
+  for (const Ct& p : probs) src.push_back(&p);
+  std::map<std::pair<int, int>, int> baby_of;
+  std::vector<RotJob> bj;
+  for (const Pair& p : own)
+    if (!baby_of.count({p.g, p.b})) baby_of[{p.g, p.b}] = (int)bj.size(), bj.push_back({p.g, -p.b * t});
+  std::vector<Ct> babies = rotate_batch(c, src, bj, true, false);
+  // giant-aligned values Rot(V, G B t)
+  std::vector<const Ct*> vs;
+  std::vector<int> vr;
+  std::vector<char> keep;
+  for (const Pair& p : own) {
+    vs.push_back(&cache.v[p.g][v_variant_index(cfg, p.w)]);
+    vr.push_back(p.G * B * t);
+    keep.push_back(cache.n_prime - p.g * gt >= gt);
   }
-  std::vector<Ct> scores = rotate_batch(c, src, jobs, false);
-  std::vector<const Ct*> sa, vb;
-  for (size_t i = 0; i < gw.size(); ++i) {
-    sa.push_back(&scores[i]);
-    vb.push_back(&cache.v[gw[i].first][v_variant_index(cfg, gw[i].second)]);
+  std::vector<Ct> va = rotate_memo(c, vs, vr, keep);
+  // inner sums per giant (both maps), lazily relinearised
+  std::map<int, std::pair<std::vector<const Ct*>, std::vector<const Ct*>>> inner;
+  for (size_t i = 0; i < own.size(); ++i) {
+    auto& [a, b] = inner[own[i].G];
+    a.push_back(&babies[baby_of[{own[i].g, own[i].b}]]);
+    b.push_back(&va[i]);
   }
-  return tensor_sum(c, sa, vb);
+  std::vector<int> giants;
+  std::vector<Ct3> sums;
+  for (auto& [G, ab] : inner) {
+    Ct3 s = tensor_sum(c, ab.first, ab.second, false);
+    if (s.zero) continue;
+    giants.push_back(G);
+    sums.push_back(std::move(s));
+  }
+  if (giants.empty()) return zeros(c, limbs - 1);
+  std::vector<const Ct3*> sp;
+  for (auto& s : sums) sp.push_back(&s);
+  std::vector<Ct> rel = relin_batch(c, sp, false);
+  // giant rotation sums, one per giant group, still at the products' scale:
+  // their ModDown roundings are then divided by q_top in finish's single rescale
+  std::map<int, std::vector<SumTerm>> grp;
+  for (size_t i = 0; i < giants.size(); ++i)
+    grp[(int)pos_mod(giants[i], kSvGroups)].push_back({&rel[i], -giants[i] * B * t});
+  std::vector<std::vector<SumTerm>> groups;
+  for (auto& [r, terms] : grp) groups.push_back(terms);
+  std::vector<Ct> gs = rot_sum_batch(c, groups, false, false);
+  std::vector<const Ct*> gp;
+  for (auto& x : gs) gp.push_back(&x);
+  Ct acc = sum_cts(c, gp, false);
+  acc.layout.reset();
+  return acc;
 }
 
-// Sum of the ranks' degree-2 partials, one relinearisation + rescale, then
-// fold_lanes (44-47) and the final stride mask (238).
-Ct softmax_times_v_finish(Context& c, const std::vector<const Ct3*>& parts, const KV& cache) {
+// Sum of the ranks' partials, the rescale, then fold_lanes
+// (kv_attention.cpp:44-47) and the final stride mask (238).
+Ct softmax_times_v_finish(Context& c, const std::vector<const Ct*>& parts, const KV& cache) {
   SF_HPROF("softmax_times_v_finish");
   const AttnCfg& cfg = cache.cfg;
   const int t = cfg.t();
   long long live = 0;
-  for (const Ct3* p : parts) live += p->zero ? 0 : 1;
+  for (const Ct* p : parts) live += p->zero ? 0 : 1;
   if (live > 1) c.ledger.add(live - 1);
-  Ct folded = relin_rescale(c, add_ct3(c, parts));
+  Ct folded = sum_cts(c, parts, false);
+  if (!folded.zero) folded = rescale(c, folded);
+  else folded = zeros(c, folded.level() - 1);
   {
     std::vector<int> fl;  // fold_lanes (44-47)
     for (int step = 1; step < t; step <<= 1) fl.push_back(step);
@@ -914,7 +1035,7 @@ Ct softmax_times_v_finish(Context& c, const std::vector<const Ct3*>& parts, cons
 
 Ct softmax_times_v(Context& c, const std::vector<Ct>& probs, const KV& cache) {
   SF_HPROF("softmax_times_v");
-  Ct3 p = softmax_times_v_partial(c, probs, cache, 0, 1);
+  Ct p = softmax_times_v_partial(c, probs, cache, 0, 1);
   return softmax_times_v_finish(c, {&p}, cache);
 }
 

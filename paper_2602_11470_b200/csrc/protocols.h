@@ -78,8 +78,11 @@ std::vector<Ct> make_v_pieces(Context& c, const KV& cache, const Ct& v_open, int
 KV v_append(Context& c, const KV& cache, const std::vector<Ct>& parts);
 std::vector<Ct> qk_dot(Context& c, const Ct& q, const KV& cache);
 std::vector<Ct> qk_dot_partial(Context& c, const Ct& q, const KV& cache, int rank, int world);
-Ct3 softmax_times_v_partial(Context& c, const std::vector<Ct>& probs, const KV& cache, int rank, int world);
-Ct softmax_times_v_finish(Context& c, const std::vector<const Ct3*>& parts, const KV& cache);
+// Score*V: the rank's baby-step / giant-step partial (whole
+// giant groups), then the sum of the partials, fold_lanes and the stride mask
+int sv_baby(const AttnCfg& cfg);
+Ct softmax_times_v_partial(Context& c, const std::vector<Ct>& probs, const KV& cache, int rank, int world);
+Ct softmax_times_v_finish(Context& c, const std::vector<const Ct*>& parts, const KV& cache);
 Ct softmax_times_v(Context& c, const std::vector<Ct>& probs, const KV& cache);
 
 // --- prefill (kv_attention.cpp:119-129, 245-376; vmm.cpp:30-43, 417-467) ------

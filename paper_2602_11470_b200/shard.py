@@ -1,8 +1,8 @@
 """Sharded decode-step hot path: one process per GPU.
 
 Each rank computes its share of a VMM (giant steps g2 = rank mod world), of
-QK^T (key ciphertexts j = rank mod world) or of Score*V ((group, variant)
-pairs by index mod world) through the C ABI's *_partial entry points; the
+QK^T (key ciphertexts j = rank mod world) or of Score*V (whole giant groups of
+its baby-step / giant-step sum) through the C ABI's *_partial entry points; the
 partial ciphertexts are all-gathered (NCCL over NVLink for device tensors; the
 same code moves host tensors over gloo) and summed mod q on the GPU
 (sf_sum_partials; NCCL has no mod-q reduction); the replicated tail (VMM
@@ -40,9 +40,23 @@ def own_keys(n_k: int, rank: int, world: int) -> List[int]:
     return [j for j in range(n_k) if (j % PACK_GROUPS) % world == rank]
 
 
-def own_pairs(n_pairs: int, rank: int, world: int) -> List[int]:
-    """Indices of the (group, variant) pairs a rank multiplies (softmax_times_v_partial)."""
-    return [i for i in range(n_pairs) if i % world == rank]
+SV_GROUPS = 8  # Score*V giants G = r mod 8 share one rotation sum
+
+
+def sv_baby(n_variants: int) -> int:
+    """Baby-step count B of the Score*V sum: the least power of two with B^2 >= #variants."""
+    b = 1
+    while b * b < n_variants:
+        b <<= 1
+    return b
+
+
+def own_variants(n_variants: int, w_lo: int, w_hi: int, rank: int, world: int) -> List[int]:
+    """Variants w of a cache group whose Score*V products a rank computes
+    (csrc/protocols.cpp:softmax_times_v_partial): whole giant groups
+    r = floor(w / B) mod SV_GROUPS with r mod world == rank."""
+    B = sv_baby(n_variants)
+    return [w for w in range(w_lo, w_hi) if ((w // B) % SV_GROUPS) % world == rank]
 
 
 # --------------------------------------------------------------------- exchange
@@ -156,18 +170,15 @@ def qk_dot_partial(be: Backend, q: Ciphertext, cache: KVCache, rank: int, world:
 
 
 def softmax_times_v_partial(be: Backend, probs, cache: KVCache, rank: int, world: int) -> List[Ciphertext]:
-    """The rank's lazily relinearised Score*V product sum: [(d0, d1), (d2, 0)]."""
+    """The rank's share of the baby-step / giant-step Score*V sum (one ciphertext)."""
     arr = (C.c_void_p * len(probs))(*[p.h for p in probs])
-    out = (C.c_void_p * 2)()
-    _check(_native.lib().sf_softmax_times_v_partial(be.ctx, arr, len(probs), cache.h, rank, world, out))
-    return [Ciphertext(be, out[0]), Ciphertext(be, out[1])]
+    return [_ct(be, _native.lib().sf_softmax_times_v_partial, arr, len(probs), cache.h, rank, world)]
 
 
 def softmax_times_v_finish(be: Backend, parts: List[List[Ciphertext]], cache: KVCache) -> Ciphertext:
-    """Sum the ranks' degree-2 partials, relinearise + rescale once, fold, mask."""
+    """Sum the ranks' partials, fold the lanes, mask."""
     a = (C.c_void_p * len(parts))(*[p[0].h for p in parts])
-    b = (C.c_void_p * len(parts))(*[p[1].h for p in parts])
-    return _ct(be, _native.lib().sf_softmax_times_v_finish, a, b, len(parts), cache.h)
+    return _ct(be, _native.lib().sf_softmax_times_v_finish, a, len(parts), cache.h)
 
 
 class Sharded:

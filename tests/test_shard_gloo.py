@@ -89,7 +89,9 @@ def _worker(rank, world, port, out):
         from paper_2602_11470_b200 import shard
         res["own"] = all(
             sorted(sum((f(m, r, world) for r in range(world)), [])) == list(range(m))
-            for f in (shard.own_giants, shard.own_keys, shard.own_pairs) for m in (1, 7, 45, 256))
+            for f in (shard.own_giants, shard.own_keys) for m in (1, 7, 45, 256)) and all(
+            sorted(sum((shard.own_variants(nv, lo, dh, r, world) for r in range(world)), [])) == list(range(lo, dh))
+            for nv, lo, dh in ((255, -127, 128), (255, -3, 128), (127, -63, 64), (8, 0, 8), (3, -1, 2)))
         out.put((rank, res))
     except Exception as e:  # pragma: no cover - surfaced through the queue
         out.put((rank, {"error": repr(e)}))

@@ -26,6 +26,9 @@ if os.environ.get("SF_HOST_PROF"):
 t0 = time.perf_counter()
 r = bench.token_stream(be, sf, layer, T)
 print(f"stream: {r}")
+if os.environ.get("SF_STREAM_TWICE"):  # first-use effects: a second pass from the same cache
+    r2 = bench.token_stream(be, sf, layer, T)
+    print(f"second pass: {r2['token_ms']}")
 print(f"wall {1e3 * (time.perf_counter() - t0) / T:.1f} ms/token")
 if os.environ.get("SF_HOST_PROF"):
     lib.sf_host_profile(buf, len(buf), 1)
