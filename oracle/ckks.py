@@ -197,6 +197,7 @@ class CkksOracle:
     """slotforge-shaped backend over the CPU CKKS oracle."""
 
     sv_bsgs = True  # Score*V as the product's baby-step / giant-step sum (DESIGN.md §3.9)
+    qk_shift_fold = True  # the QK^T pack rotation rides the fold (DESIGN.md §3.8)
 
     def __init__(self, N: int, L: int, **kw):
         if not is_pow2(N):
@@ -421,30 +422,39 @@ class CkksOracle:
         lvl = min(a.level for a, _ in terms)
         return OCt(self, lib().ock_rot_sum(self.ptr, arr, rr, len(terms)), lvl, ly)
 
-    def fold_steps(self, c, rots):
+    def fold_steps(self, c, rots, shift: int = 0):
         """The doubling chain c <- c + Rot(c, r_i), i = 0..m-1 (fold_within_head,
         replicate_lanes, fold_lanes, the VMM ladders: kv_attention.cpp:30-47,
         vmm.cpp:190-193, 226-230), i.e. sum_{k < 2^m} Rot(c, sum_i bit_i(k) r_i),
         evaluated as radix rotation sums (fold_radix) and charged
-        as the reference's m rotate + add steps."""
+        as the reference's m rotate + add steps. shift: the value rotated by
+        `shift` (every term of the last radix sum moves by it; uncharged)."""
         self._check(c, "rotate")
         m = len(rots)
         if m == 0:
-            return c
+            if shift % self.N == 0:
+                return c
+            led, self.ledger = self.ledger, CostLedger()
+            try:
+                return self.rot_sum([(c, shift)])
+            finally:
+                self.ledger = led
         for r in rots:
             if r % self.N:
                 self.ledger.count_rotation(False)
         for _ in range(m):
             self.ledger.count_add()
-        ly = c.layout if all(r % self.N == 0 for r in rots) else None
+        ly = c.layout if all(r % self.N == 0 for r in list(rots) + [shift]) else None
         led, self.ledger = self.ledger, CostLedger()
         try:
             lo = 0
-            for bits in fold_radix(1 << m):
+            radix = fold_radix(1 << m)
+            for si, bits in enumerate(radix):
                 rs = rots[lo:lo + bits]
+                s0 = shift if si + 1 == len(radix) else 0
                 terms = []
                 for k in range(1 << bits):
-                    terms.append((c, sum(rs[i] for i in range(bits) if (k >> i) & 1)))
+                    terms.append((c, s0 + sum(rs[i] for i in range(bits) if (k >> i) & 1)))
                 c = self.rot_sum(terms)
                 lo += bits
         finally:

@@ -435,13 +435,24 @@ def qk_dot(be, q, cache: KVCache, cfg):
     n_maps = _ceil_div(cache.n_prime, gt)
     terms = [[[] for _ in range(PACK_GROUPS)] for _ in range(n_maps)]
     for j, kc in enumerate(cache.k_cts):
-        prod = be.mul(q_rep, kc)
-        prod = fold_within_head(be, prod, dh, t)
-        masked = mask_lazy(be, prod, head_mask)
-        terms[(j * t) // gt][j % PACK_GROUPS].append((masked, -((j * t) % gt)))
-    # pack + accumulate (kv_attention.cpp:202-206) as rotation sums, one per
-    # (map, key-ct group j mod PACK_GROUPS)
+        terms[(j * t) // gt][j % PACK_GROUPS].append(qk_term(be, q_rep, kc, cfg, head_mask, -((j * t) % gt)))
+    # pack + accumulate (kv_attention.cpp:202-206), one sum per (map, key-ct
+    # group j mod PACK_GROUPS)
     return [be.with_layout(pack_sum(be, grp), None) for grp in terms]
+
+
+def qk_term(be, q_rep, kc, cfg, head_mask, r):
+    """One key ciphertext's (masked product, pack rotation) of kv_attention.cpp:
+    195-204. CKKS backends with a shiftable fold apply the pack rotation inside
+    the fold (its last radix sum's terms move by r) and mask with Rot(mask, r):
+    Rot(mask (.) F, r) = Rot(mask, r) (.) Rot(F, r) -- the returned product is
+    already aligned (rotation 0) and still unrescaled."""
+    prod = be.mul(q_rep, kc)
+    if getattr(be, "qk_shift_fold", False):
+        f = be.fold_steps(prod, [(1 << l) * cfg.t for l in range(cfg.d_head.bit_length() - 1)], shift=r)
+        return be.mul_plain_lazy(f, np.roll(head_mask, -r)), r
+    prod = fold_within_head(be, prod, cfg.d_head, cfg.t)
+    return mask_lazy(be, prod, head_mask), r
 
 
 def mask_lazy(be, x, mask):
@@ -457,13 +468,31 @@ PACK_GROUPS = 8  # key-ct groups of the QK^T pack sums
 
 def pack_sum(be, groups):
     """sum over non-empty groups of rot_sum(group), accumulated in group order
-    (rot_sum_rescale where the backend deferred the mask's rescale)."""
+    (rot_sum_rescale where the backend deferred the mask's rescale; where the
+    pack rotation already rode the fold, qk_term: the plain sum of the aligned
+    products and one rescale, charged as the reference's rotate/add chain)."""
     rs = getattr(be, "rot_sum_rescale", None) if getattr(be, "mul_plain_lazy", None) else None
+    shifted = getattr(be, "qk_shift_fold", False)
     acc = None
     for grp in groups:
         if not grp:
             continue
-        s = rs(grp) if rs else be.rot_sum(grp)
+        if shifted:
+            for _, r in grp:
+                if r % be.N:
+                    be.ledger.count_rotation(False)
+            for _ in range(len(grp) - 1):
+                be.ledger.count_add()
+            led, be.ledger = be.ledger, type(be.ledger)()
+            try:
+                s = grp[0][0]
+                for x, _ in grp[1:]:
+                    s = be.add(s, x)
+                s = be.rescale(s)
+            finally:
+                be.ledger = led
+        else:
+            s = rs(grp) if rs else be.rot_sum(grp)
         acc = s if acc is None else be.add(acc, s)
     return acc
 

@@ -65,9 +65,7 @@ def qk_dot_partial(be, q, cache, cfg, rank, world):
     for j in range(len(cache.k_cts)):
         if (j % G) % world != rank:  # whole pack groups per rank
             continue
-        prod = P.fold_within_head(be, be.mul(q_rep, cache.k_cts[j]), dh, t)
-        masked = P.mask_lazy(be, prod, head_mask)
-        terms[(j * t) // gt][j % G].append((masked, -((j * t) % gt)))
+        terms[(j * t) // gt][j % G].append(P.qk_term(be, q_rep, cache.k_cts[j], cfg, head_mask, -((j * t) % gt)))
     maps = [P.pack_sum(be, grp) for grp in terms]
     return [be.with_layout(m, None) if m is not None else be.zeros(q.level - 2) for m in maps]
 

@@ -250,11 +250,14 @@ std::vector<Ct> rot_sum_batch(Context& c, const std::vector<std::vector<SumTerm>
 // as the reference's rotate + add steps when count && lead
 // post (fused path only): per chain an NTT-domain plaintext multiplied into the
 // result in the last ModDown's epilogue (a fused ct x pt; the caller rescales)
+// shift (per chain): Rot(chain value, shift[i]) -- every term of the last radix
+// sum moves by shift[i] (one rotation sum, no extra key switch)
 std::vector<Ct> fold_steps_batch(Context& c, const std::vector<const Ct*>& xs, const std::vector<std::vector<int>>& rots,
-                                 bool count = true, bool lead = true, const std::vector<const Pt*>* post = nullptr);
+                                 bool count = true, bool lead = true, const std::vector<const Pt*>* post = nullptr,
+                                 const std::vector<int>* shift = nullptr);
 // fold_within_head of every x (radix rotation sums), reference ledger charge
 std::vector<Ct> fold_batch(Context& c, const std::vector<const Ct*>& xs, int d_head, int t, bool count = true,
-                           const std::vector<const Pt*>* post = nullptr);
+                           const std::vector<const Pt*>* post = nullptr, const std::vector<int>* shift = nullptr);
 // sum of k same-level ciphertexts, charged k-1 additions
 Ct sum_cts(Context& c, const std::vector<const Ct*>& xs, bool count = true);
 

@@ -192,11 +192,15 @@ struct Context {
   // cudaMallocAsync / cudaFreeAsync host cost
   std::mutex alloc_mu;
   std::unordered_map<size_t, std::vector<u64*>> free_bufs;
-  size_t cached_words = 0, cache_cap_words = (size_t)1 << 30;  // 8 GiB
+  // 24 GiB (SF_FREE_CACHE_GIB): the decode step's whole temporary working set, so a
+  // steady-state eager step never reaches cudaMallocAsync (an 8 GiB cap overflowed
+  // and stalled single allocations for 100-400 ms)
+  size_t cached_words = 0, cache_cap_words = (size_t)3 << 30;
   std::vector<std::pair<u64*, size_t>> capture_deferred;
   long long graph_launch_base = 0;
   bool ks_row = true;  // fused key-switch row stage
   int variant = 0;     // SF_VARIANT bit mask: kernel variants under A/B evaluation
+  int rot_chunk = 0;   // SF_ROT_CHUNK: sources per ModUp batch in rotate_batch (0: kJobs), for A/B timing
   int fused_cpw = 1;   // columns per warp in batched fused column stages (SF_FUSED_CPW=1|2, for A/B timing) (SF_KS_ROW=0: separate passes, for A/B timing)
   std::vector<u64> primes;  // q0..qL, p0..p_{alpha-1}
   std::vector<u64> ipsi1_h;  // per prime: ipsi table index 1 (the last inverse column stage's twiddle)

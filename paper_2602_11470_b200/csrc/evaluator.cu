@@ -149,6 +149,8 @@ std::unique_ptr<Context> make_context(int slots, int L, int log_n, int alpha, in
   if (const char* e = std::getenv("SF_KS_ROW")) c->ks_row = std::atoi(e) != 0;
   if (const char* e = std::getenv("SF_FUSED_CPW")) c->fused_cpw = std::atoi(e);
   if (const char* e = std::getenv("SF_VARIANT")) c->variant = std::atoi(e);
+  if (const char* e = std::getenv("SF_FREE_CACHE_GIB")) c->cache_cap_words = (size_t)(std::atof(e) * (1u << 27));
+  if (const char* e = std::getenv("SF_ROT_CHUNK")) c->rot_chunk = std::atoi(e);
   c->delta = std::ldexp(1.0, scale_bits > 0 ? scale_bits : 40);
   c->primes = generate_primes(c->logn, L, q0_bits > 0 ? q0_bits : 60, scale_bits > 0 ? scale_bits : 40, c->alpha,
                               special_bits > 0 ? special_bits : 60);

@@ -725,7 +725,8 @@ std::vector<Ct> rot_sum_batch(Context& c, const std::vector<std::vector<SumTerm>
 // of DESIGN.md §3.8 (m <= 3 bits in one sum, else ceil(m/2) then floor(m/2));
 // charged as the reference's m rotate + add steps per ciphertext.
 std::vector<Ct> fold_steps_batch(Context& c, const std::vector<const Ct*>& xs, const std::vector<std::vector<int>>& rots,
-                                 bool count, bool lead, const std::vector<const Pt*>* post) {
+                                 bool count, bool lead, const std::vector<const Pt*>* post,
+                                 const std::vector<int>* shift) {
   SF_HPROF("fold_steps_batch");
   std::vector<bool> posted(xs.size(), false);
   require(xs.size() == rots.size(), kShapeMismatch, "fold_steps: operand count");
@@ -745,8 +746,8 @@ std::vector<Ct> fold_steps_batch(Context& c, const std::vector<const Ct*>& xs, c
   std::map<int, std::vector<int>> by_len;
   for (size_t i = 0; i < xs.size(); ++i) by_len[(int)rots[i].size()].push_back((int)i);
   for (auto& [m, idx] : by_len) {
-    if (m == 0) continue;
-    std::vector<int> steps;
+    if (m == 0 && !shift) continue;
+    std::vector<int> steps;  // an empty chain with a shift: one single-term sum (the rotation)
     if (m <= 3)
       steps.push_back(m);
     else
@@ -754,18 +755,18 @@ std::vector<Ct> fold_steps_batch(Context& c, const std::vector<const Ct*>& xs, c
     int lo = 0;
     for (size_t si = 0; si < steps.size(); ++si) {
       const int bits = steps[si];
+      const bool last = si + 1 == steps.size();
       std::vector<std::vector<SumTerm>> groups(idx.size());
       for (size_t g = 0; g < idx.size(); ++g) {
         const std::vector<int>& rs = rots[idx[g]];
         for (int k = 0; k < (1 << bits); ++k) {
-          long long r = 0;
+          long long r = (shift && last) ? (*shift)[idx[g]] : 0;  // Rot(sum, s): every last-step term moves by s
           for (int i = 0; i < bits; ++i)
             if ((k >> i) & 1) r += rs[lo + i];
           groups[g].push_back({&cur[idx[g]], (int)pos_mod(r, c.slots)});
         }
       }
       std::vector<const Pt*> pg;  // the post multipliers ride the last step's ModDown epilogue
-      const bool last = si + 1 == steps.size();
       if (post && last)
         for (int g : idx) pg.push_back((*post)[g]), posted[g] = true;
       std::vector<Ct> nxt = rot_sum_batch(c, groups, false, false, (post && last) ? &pg : nullptr);
@@ -774,7 +775,7 @@ std::vector<Ct> fold_steps_batch(Context& c, const std::vector<const Ct*>& xs, c
     }
   }
   for (size_t i = 0; i < xs.size(); ++i) {
-    bool all0 = true;
+    bool all0 = !shift || pos_mod((*shift)[i], c.slots) == 0;
     for (int r : rots[i]) all0 = all0 && pos_mod(r, c.slots) == 0;
     cur[i].layout = all0 ? xs[i]->layout : OptLayout();
     require(!post || posted[i], kInternal, "fold_steps: post multiplier on an empty chain");
@@ -783,10 +784,10 @@ std::vector<Ct> fold_steps_batch(Context& c, const std::vector<const Ct*>& xs, c
 }
 
 std::vector<Ct> fold_batch(Context& c, const std::vector<const Ct*>& xs, int d_head, int t, bool count,
-                           const std::vector<const Pt*>* post) {
+                           const std::vector<const Pt*>* post, const std::vector<int>* shift) {
   std::vector<int> rs;
   for (int l = 0; (1 << l) < d_head; ++l) rs.push_back((1 << l) * t);
-  return fold_steps_batch(c, xs, std::vector<std::vector<int>>(xs.size(), rs), count, true, post);
+  return fold_steps_batch(c, xs, std::vector<std::vector<int>>(xs.size(), rs), count, true, post, shift);
 }
 
 // -------------------------------------------------------------------- rescale
@@ -927,8 +928,9 @@ std::vector<Ct> rotate_batch(Context& c, const std::vector<const Ct*>& srcs, con
     if (uses[jobs[i].src]++ == 0) need[s.limbs].push_back(jobs[i].src);
   }
   for (auto& [limbs, sidx] : need) {
-    for (size_t c0 = 0; c0 < sidx.size(); c0 += kJobs) {  // bound the ModUp working set
-      const size_t S = std::min<size_t>(kJobs, sidx.size() - c0);
+    const size_t chunk = c.rot_chunk > 0 ? (size_t)c.rot_chunk : (size_t)kJobs;
+    for (size_t c0 = 0; c0 < sidx.size(); c0 += chunk) {  // bound the ModUp working set
+      const size_t S = std::min<size_t>(chunk, sidx.size() - c0);
       std::vector<const u64*> d;
       std::map<int, int> local;
       for (size_t s = 0; s < S; ++s) {

@@ -784,49 +784,79 @@ std::vector<Ct> qk_dot_partial(Context& c, const Ct& q, const KV& cache, int ran
   std::vector<const Ct*> pp0;
   for (auto& p : prod0) pp0.push_back(&p);
   const std::string hkey = "headmask:" + std::to_string(cfg.H) + ":" + std::to_string(t);
+  // the pack rotation (kv_attention.cpp:201-204) rides the fold: Rot(mask (.) F, r)
+  // = Rot(mask, r) (.) Rot(F, r), and Rot(fold(x), r) is the fold's last radix sum
+  // with every term moved by r -- no key switch of its own
+  std::vector<int> shift(J);
+  for (int i = 0; i < J; ++i) shift[i] = -((own[i] * t) % gt);
+  std::map<std::pair<int, int>, Pt> mask_pt;  // (shift, limbs) -> Rot(mask, shift), encoded once per context
+  auto mask_of = [&](int i, int limbs) {
+    auto it = mask_pt.find({shift[i], limbs});
+    if (it != mask_pt.end()) return it->second;
+    const std::string key = hkey + ":" + std::to_string(shift[i]);
+    Pt p;
+    if (!lookup_pt(c, key, limbs, &p)) {
+      std::vector<double> m(N);
+      for (int k = 0; k < N; ++k) m[k] = head_mask[pos_mod((long long)k + shift[i], N)];  // Rot(mask, r)
+      p = cached_pt(c, key, m.data(), (double)c.primes[limbs - 1], limbs);
+    }
+    mask_pt[{shift[i], limbs}] = p;
+    return p;
+  };
   std::vector<Ct> masked;
   bool fused_mask = fused_path(c);
   for (int i = 0; i < J; ++i) fused_mask = fused_mask && !prod0[i].zero && prod0[i].limbs == prod0[0].limbs;
-  // the masked products stay unrescaled (scale * q_top): each pack rotation sum
-  // rescales once in its ModDown's basis conversion (merged)
-  // instead of J separate rescales
+  // the masked products stay unrescaled (scale * q_top): each (map, pack group)
+  // sum is rescaled once instead of J separate rescales
   if (fused_mask) {
-    // fold_within_head (38-41) with the ReplicateExtract mask (layouts.cpp:134-138)
-    // multiplied in the fold's last ModDown epilogue (a fused ct x pt)
+    // fold_within_head (38-41), shifted by the pack rotation, with the rotated
+    // ReplicateExtract mask (layouts.cpp:134-138) multiplied in the fold's last
+    // ModDown epilogue (a fused ct x pt)
     const int lb = prod0[0].limbs;
     require(lb - 1 > 0, kLevelUnderflow, "mul_plain: no multiplicative level left");
-    const Pt hm = cached_pt(c, hkey, head_mask.data(), (double)c.primes[lb - 1], lb);
-    std::vector<const Pt*> post(J, &hm);
-    masked = fold_batch(c, pp0, dh, t, true, &post);
+    std::vector<Pt> hm;
+    for (int i = 0; i < J; ++i) hm.push_back(mask_of(i, lb));
+    std::vector<const Pt*> post;
+    for (auto& p : hm) post.push_back(&p);
+    masked = fold_batch(c, pp0, dh, t, true, &post, &shift);
     for (int i = 0; i < J; ++i) {
       c.ledger.ctpt();
       masked[i].scale *= (double)c.primes[lb - 1];  // the product's scale before its rescale
       masked[i].layout.reset();
     }
   } else {
-    std::vector<Ct> prod = fold_batch(c, pp0, dh, t);  // fold_within_head (38-41), DESIGN.md §3.8
+    std::vector<Ct> prod = fold_batch(c, pp0, dh, t, true, nullptr, &shift);  // fold_within_head (38-41)
     std::vector<const Ct*> pp;
     std::vector<Pt> hm;
     for (int i = 0; i < J; ++i) {
       require(prod[i].level() > 0, kLevelUnderflow, "mul_plain: no multiplicative level left");
-      hm.push_back(cached_pt(c, hkey, head_mask.data(), (double)c.primes[prod[i].limbs - 1], prod[i].limbs));
+      hm.push_back(mask_of(i, prod[i].limbs));
     }
     std::vector<const Pt*> hp;
     for (int i = 0; i < J; ++i) pp.push_back(&prod[i]), hp.push_back(&hm[i]);
     masked = mul_plain_batch(c, pp, hp, true, false);
     for (auto& m : masked) m.layout.reset();
   }
-  // pack + accumulate (kv_attention.cpp:202-206): one rotation sum per (map,
-  // key-ct group j mod kPackGroups), then the groups' sum
-  std::vector<std::vector<SumTerm>> groups;
-  std::vector<std::pair<int, int>> gid;  // (map, group) of each rotation sum
+  // pack + accumulate (kv_attention.cpp:202-206): per (map, key-ct group j mod
+  // kPackGroups) the plain sum of the already aligned masked products and one
+  // rescale, then the groups' sum; charged as the reference's rotate/add chain
+  std::vector<std::vector<const Ct*>> groups;
+  std::vector<std::pair<int, int>> gid;  // (map, group) of each group sum
   std::map<std::pair<int, int>, int> where;
   for (int i = 0; i < J; ++i) {
     const std::pair<int, int> key{(own[i] * t) / gt, own[i] % kPackGroups};
     if (!where.count(key)) where[key] = (int)groups.size(), groups.emplace_back(), gid.push_back(key);
-    groups[where[key]].push_back({&masked[i], -((own[i] * t) % gt)});
+    groups[where[key]].push_back(&masked[i]);
+    if (pos_mod(shift[i], c.slots)) c.ledger.rot(false);
   }
-  std::vector<Ct> gs = rot_sum_batch(c, groups, false, true, nullptr, true);
+  std::vector<Ct> sums;
+  for (auto& g : groups) {
+    c.ledger.add((long long)g.size() - 1);
+    sums.push_back(sum_cts(c, g, false));
+  }
+  std::vector<const Ct*> sp;
+  for (auto& x : sums) sp.push_back(&x);
+  std::vector<Ct> gs = rescale_batch(c, sp);
   std::vector<std::vector<const Ct*>> per_map(n_maps);
   for (int m = 0; m < n_maps; ++m)
     for (int r = 0; r < kPackGroups; ++r) {
