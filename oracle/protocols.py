@@ -265,9 +265,13 @@ class KVCache:
     n_prime: int = 0
     k_cts: list = field(default_factory=list)
     v_cts: list = field(default_factory=list)  # [group][variant]
+    # CKKS backends: giant-aligned variants Rot(v, G B t) kept by v_append (None:
+    # not tracked)
+    v_aligned: list = field(default_factory=list)
 
     def copy(self):
-        return KVCache(self.n_prime, list(self.k_cts), [list(g) for g in self.v_cts])
+        return KVCache(self.n_prime, list(self.k_cts), [list(g) for g in self.v_cts],
+                       [list(g) if g is not None else None for g in self.v_aligned])
 
 
 def v_variant_count(cfg):
@@ -394,8 +398,46 @@ def make_v_pieces(be, v_open, cfg, position):
         raise LayoutMismatch("make_v_pieces: input must be interleaved at the configured width")
     if v_open.layout.offset != position % cfg.t:
         raise LayoutMismatch("make_v_pieces: value ct offset does not match the token position")
-    return [fused_extract(be, v_open, "vcache_mask", coeff=v_piece_mask(cfg, e, position))
-            for e in range(cfg.d_head)]
+    parts = [fused_extract(be, v_open, "vcache_mask", coeff=v_piece_mask(cfg, e, position))
+             for e in range(cfg.d_head)]
+    if getattr(be, "sv_bsgs", False):
+        _attach_aligned(be, v_open, parts, cfg, position)
+    return parts
+
+
+def _giant_shift(cfg, w):
+    B = sv_baby(cfg)
+    return (w // B) * B * cfg.t
+
+
+def _attach_aligned(be, v_open, parts, cfg, position):
+    """Aligned companions of the value pieces (mirrors csrc/protocols.cpp
+    make_v_pieces): piece e lands in variant w of giant
+    G = floor(w / B); its companion Rot(piece, G B t) is computed as
+    RS(Rot(mask_e, G B t) (.) Rot(v_open, G B t)) with Rot(mask_e, G B t) =
+    mask_{(e - G B) mod d_head} (valid slots invariant under a lane-block
+    shift). Off-ledger."""
+    N, t, dh = be.N, cfg.t, cfg.d_head
+    valid = valid_mask(v_open.layout, N)
+    if not np.array_equal(valid, np.roll(valid, -t)) or v_open.is_zero:
+        return
+    B = sv_baby(cfg)
+    u_local = position % cfg.group_tokens
+    led, be.ledger = be.ledger, type(be.ledger)()
+    try:
+        rot = {}
+        for e in range(dh):
+            w = v_variant_of(cfg, e, u_local)
+            G = w // B
+            r = G * B * t
+            if r % N == 0:
+                continue
+            if r not in rot:
+                rot[r] = be.rotate(v_open, r, hoisted=True)
+            m = valid * v_piece_mask(cfg, (e - G * B) % dh, position)
+            parts[e]._aligned = (be.mul_plain(rot[r], m), r)
+    finally:
+        be.ledger = led
 
 
 def v_append(be, cache: KVCache, parts, cfg):
@@ -412,10 +454,42 @@ def v_append(be, cache: KVCache, parts, cfg):
     if g == len(out.v_cts):
         z = be.zeros()
         out.v_cts.append([z] * v_variant_count(cfg))
+    if getattr(be, "sv_bsgs", False):
+        _append_aligned(be, cache, out, parts, cfg, g, u_local)
     for e in range(dh):
         idx = v_variant_index(cfg, v_variant_of(cfg, e, u_local))
         out.v_cts[g][idx] = be.add(out.v_cts[g][idx], parts[e])
     return out
+
+
+def _append_aligned(be, cache, out, parts, cfg, g, u_local):
+    """Giant-aligned variants (mirrors csrc/protocols.cpp v_append): aligned' =
+    (aligned, or Rot(V_old) when untracked, or 0 for an empty variant) + the
+    piece's aligned companion; untracked when a piece has none. Off-ledger."""
+    N, nv = be.N, v_variant_count(cfg)
+    while len(out.v_aligned) <= g:
+        out.v_aligned.append(None)
+    al = list(out.v_aligned[g]) if out.v_aligned[g] is not None else [None] * nv
+    led, be.ledger = be.ledger, type(be.ledger)()
+    try:
+        for e in range(cfg.d_head):
+            w = v_variant_of(cfg, e, u_local)
+            idx = v_variant_index(cfg, w)
+            r = _giant_shift(cfg, w)
+            comp = getattr(parts[e], "_aligned", None)
+            if r % N == 0 or comp is None or comp[1] != r or parts[e].is_zero:
+                al[idx] = None
+                continue
+            if al[idx] is None:
+                old = cache.v_cts[g][idx] if g < len(cache.v_cts) else None
+                if old is None or old.is_zero:
+                    al[idx] = comp[0]
+                    continue
+                al[idx] = be.rotate(old, r)
+            al[idx] = be.add(al[idx], comp[0])
+    finally:
+        be.ledger = led
+    out.v_aligned[g] = al
 
 
 def _ceil_div(a, b):
@@ -572,8 +646,13 @@ def sv_partial(be, probs, cache: KVCache, cfg, rank, world):
         for g, w, G, b in own:
             if (g, b) not in babies:
                 babies[(g, b)] = be.rotate(probs[g], -b * t, hoisted=True) if b else probs[g]
-            v = cache.v_cts[g][v_variant_index(cfg, w)]
-            if not v.is_zero and (G * B * t) % N:
+            vi = v_variant_index(cfg, w)
+            v = cache.v_cts[g][vi]
+            tracked = (cache.v_aligned[g][vi] if G and g < len(cache.v_aligned) and cache.v_aligned[g] is not None
+                       else None)
+            if tracked is not None:
+                v = tracked
+            elif not v.is_zero and (G * B * t) % N:
                 v = be.rotate(v, G * B * t)
             inner.setdefault(G, []).append((babies[(g, b)], v))
         rel = {}

@@ -56,6 +56,10 @@ struct Ct {
   double scale = 0.0;
   bool zero = false;  // trivial (0, 0) ciphertext: Backend::zeros (engine.cpp:123)
   OptLayout layout;
+  // value-cache piece only (make_v_pieces): Rot(this, aligned_r), computed from the
+  // rotated input, for v_append's giant-aligned variants
+  std::shared_ptr<const Ct> aligned;
+  int aligned_r = 0;
   int level() const { return limbs - 1; }
   u64* c0() const { return buf ? buf->p : nullptr; }
   u64* c1(int n) const { return buf ? buf->p + (size_t)stride * n : nullptr; }

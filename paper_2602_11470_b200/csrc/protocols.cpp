@@ -682,6 +682,17 @@ KV k_append(Context& c, const KV& cache, const Ct& k_new) {  // kv_attention.cpp
   return out;
 }
 
+static std::vector<Ct> rotate_memo(Context& c, const std::vector<const Ct*>& xs, const std::vector<int>& rs,
+                                   const std::vector<char>& keep);
+static bool cache_v_zero(const KV& cache, int g, int idx) {
+  return g >= (int)cache.v.size() || cache.v[g][idx].zero;
+}
+// the tracked giant-aligned copy of v[g][idx], or null
+static const Ct* aligned_of(const KV& cache, int g, int idx) {
+  if (g >= (int)cache.va_ok.size() || idx >= (int)cache.va_ok[g].size() || !cache.va_ok[g][idx]) return nullptr;
+  return &cache.va[g][idx];
+}
+
 std::vector<Ct> make_v_pieces(Context& c, const KV& cache, const Ct& v_open, int position) {  // :145-163
   const AttnCfg& cfg = cache.cfg;
   require(position >= 0 && position < cfg.n_max, kShapeMismatch, "make_v_pieces: position outside cache capacity");
@@ -717,6 +728,41 @@ std::vector<Ct> make_v_pieces(Context& c, const KV& cache, const Ct& v_open, int
   for (auto& p : masks) ps.push_back(&p);
   parts = mul_plain_batch(c, xs, ps);
   for (auto& y : parts) y.layout = out;
+  // aligned companions: piece e lands in variant w of giant
+  // G = floor(w / B); Rot(piece, G B t) = RS(Rot(mask_e, G B t) (.) Rot(v_open, G B t))
+  // and Rot(mask_e, G B t) = mask_{(e - G B) mod d_head} when the valid slots are
+  // invariant under a lane-block shift -- one hoisted rotation of v_open per giant
+  bool periodic = true;
+  for (int i = 0; i < c.slots && periodic; ++i) periodic = valid[i] == valid[(i + t) % c.slots];
+  if (periodic && !v_open.zero) {
+    const int B = sv_baby(cfg), gt = cfg.group_tokens(), u_local = position % gt;
+    std::vector<int> shift(dh), esrc(dh);
+    std::vector<RotJob> jobs;
+    std::map<int, int> job_of;
+    for (int e = 0; e < dh; ++e) {
+      const int w = v_variant_of(cfg, e, u_local);
+      const int G = w >= 0 ? w / B : -((-w + B - 1) / B);
+      shift[e] = G * B * t;
+      esrc[e] = (int)pos_mod(e - G * B, dh);
+      if (pos_mod(shift[e], c.slots) && !job_of.count(shift[e]))
+        job_of[shift[e]] = (int)jobs.size(), jobs.push_back({0, shift[e]});
+    }
+    std::vector<Ct> rv = rotate_batch(c, {&v_open}, jobs, true, false);
+    std::vector<const Ct*> ax;
+    std::vector<const Pt*> ap;
+    std::vector<int> which;
+    for (int e = 0; e < dh; ++e) {
+      if (!pos_mod(shift[e], c.slots)) continue;  // giant 0: the piece itself
+      ax.push_back(&rv[job_of[shift[e]]]);
+      ap.push_back(&masks[esrc[e]]);
+      which.push_back(e);
+    }
+    std::vector<Ct> al = mul_plain_batch(c, ax, ap, false);
+    for (size_t k = 0; k < which.size(); ++k) {
+      parts[which[k]].aligned = std::make_shared<const Ct>(std::move(al[k]));
+      parts[which[k]].aligned_r = shift[which[k]];
+    }
+  }
   return parts;
 }
 
@@ -738,8 +784,52 @@ KV v_append(Context& c, const KV& cache, const std::vector<Ct>& parts) {  // kv_
     a.push_back(&out.v[g][idx[e]]);
     b.push_back(&parts[e]);
   }
+  // giant-aligned variants: aligned' = (aligned, or Rot(V_old)
+  // when untracked, or 0 for an empty variant) + the piece's aligned companion
+  const int B = sv_baby(cfg), t = cfg.t();
+  if ((int)out.va.size() <= g) out.va.resize(g + 1), out.va_ok.resize(g + 1);
+  out.va[g].resize(v_variant_count(cfg));
+  out.va_ok[g].resize(v_variant_count(cfg), 0);
+  std::vector<const Ct*> base_rot;
+  std::vector<int> base_r, base_e;
+  std::vector<int> r_of(dh, 0);
+  for (int e = 0; e < dh; ++e) {
+    const int w = v_variant_of(cfg, e, u_local);
+    const int G = w >= 0 ? w / B : -((-w + B - 1) / B);
+    r_of[e] = G * B * t;
+    const Ct* p = &parts[e];
+    const bool comp = pos_mod(r_of[e], c.slots) && p->aligned && p->aligned_r == r_of[e] &&
+                      p->aligned->limbs == p->limbs && !p->zero;
+    if (!comp) {
+      out.va_ok[g][idx[e]] = 0;
+      r_of[e] = 0;
+      continue;
+    }
+    if (!out.va_ok[g][idx[e]] && !cache_v_zero(cache, g, idx[e]))
+      base_rot.push_back(&cache.v[g][idx[e]]), base_r.push_back(r_of[e]), base_e.push_back(e);
+  }
+  std::vector<Ct> based = rotate_memo(c, base_rot, base_r, std::vector<char>(base_rot.size(), 1));
+  std::vector<const Ct*> xa, xb;
+  std::vector<int> tgt;
+  for (size_t k = 0; k < base_e.size(); ++k) out.va[g][idx[base_e[k]]] = std::move(based[k]), out.va_ok[g][idx[base_e[k]]] = 1;
+  for (int e = 0; e < dh; ++e) {
+    if (!r_of[e]) continue;
+    if (!out.va_ok[g][idx[e]]) {  // empty variant: the companion alone
+      out.va[g][idx[e]] = *parts[e].aligned;
+      out.va_ok[g][idx[e]] = 1;
+      continue;
+    }
+    xa.push_back(&out.va[g][idx[e]]);
+    xb.push_back(parts[e].aligned.get());
+    tgt.push_back(idx[e]);
+  }
+  std::vector<Ct> asum = add_batch(c, xa, xb, false);
+  for (size_t k = 0; k < tgt.size(); ++k) out.va[g][tgt[k]] = std::move(asum[k]);
   std::vector<Ct> sums = add_batch(c, a, b);
-  for (int e = 0; e < dh; ++e) out.v[g][idx[e]] = std::move(sums[e]);
+  for (int e = 0; e < dh; ++e) {
+    out.v[g][idx[e]] = std::move(sums[e]);
+    out.v[g][idx[e]].aligned.reset();
+  }
   return out;
 }
 
@@ -999,12 +1089,23 @@ Ct softmax_times_v_partial(Context& c, const std::vector<Ct>& probs, const KV& c
   std::vector<const Ct*> vs;
   std::vector<int> vr;
   std::vector<char> keep;
-  for (const Pair& p : own) {
-    vs.push_back(&cache.v[p.g][v_variant_index(cfg, p.w)]);
+  std::vector<const Ct*> vsel(own.size(), nullptr);
+  std::vector<int> vpos;
+  for (size_t i = 0; i < own.size(); ++i) {  // tracked aligned copies first, else Rot(V) (memo)
+    const Pair& p = own[i];
+    const int vi = v_variant_index(cfg, p.w);
+    if (p.G != 0) vsel[i] = aligned_of(cache, p.g, vi);
+    if (vsel[i]) continue;
+    vs.push_back(&cache.v[p.g][vi]);
     vr.push_back(p.G * B * t);
     keep.push_back(cache.n_prime - p.g * gt >= gt);
+    vpos.push_back((int)i);
   }
-  std::vector<Ct> va = rotate_memo(c, vs, vr, keep);
+  std::vector<Ct> vrot = rotate_memo(c, vs, vr, keep);
+  std::vector<Ct> va(own.size());
+  for (size_t i = 0; i < own.size(); ++i)
+    if (vsel[i]) va[i] = *vsel[i];
+  for (size_t k = 0; k < vpos.size(); ++k) va[vpos[k]] = std::move(vrot[k]);
   // inner sums per giant (both maps), lazily relinearised
   std::map<int, std::pair<std::vector<const Ct*>, std::vector<const Ct*>>> inner;
   for (size_t i = 0; i < own.size(); ++i) {

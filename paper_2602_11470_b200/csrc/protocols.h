@@ -65,6 +65,11 @@ struct KV {
   int n_prime = 0;
   std::vector<Ct> k;
   std::vector<std::vector<Ct>> v;  // [group][variant]
+  // giant-aligned variants Rot(v[g][w], G B t) for the BSGS Score*V (DESIGN.md
+  // §3.9), kept current by v_append from the pieces' aligned companions;
+  // va_ok[g][w] = 0: not tracked (softmax_times_v rotates v[g][w] itself)
+  std::vector<std::vector<Ct>> va;
+  std::vector<std::vector<char>> va_ok;
 };
 int v_variant_count(const AttnCfg& cfg);
 int v_variant_index(const AttnCfg& cfg, int w);
