@@ -861,6 +861,9 @@ std::vector<Ct> qk_dot_partial(Context& c, const Ct& q, const KV& cache, int ran
   std::vector<int> own;  // whole pack groups r = j mod kPackGroups with r mod world == rank
   for (int j = 0; j < (int)cache.k.size(); ++j)
     if ((j % kPackGroups) % world == rank) own.push_back(j);
+  // key ciphertexts with the same pack shift (j t mod gt) use the same shifted
+  // fold keys: processed next to each other, their key rows are L2 hits
+  std::stable_sort(own.begin(), own.end(), [&](int a, int b) { return (a * t) % gt < (b * t) % gt; });
   const int J = (int)own.size();
   const int n_maps = ceil_div(cache.n_prime, gt);
   std::vector<Ct> out;

@@ -96,12 +96,17 @@ __device__ __forceinline__ void warp_inv(u64 (&x)[1 << (LOGM - 5)], u64* sm, int
   constexpr int E = 1 << LOGE;
   const u64 q2 = 2 * q;
   int s0 = ENTRY == kBlocked ? 0 : LOGM - LOGE;
+  // the forward transform's register groups in reverse ([0,2), [2,5), [5,8) at
+  // 256 points): the relayouts use the register offsets s0 the swizzle is
+  // conflict-free for (0/2/5, 0/1/5, 0/1/3/5); the former [0,3), [3,6), [6,8)
+  // put s0 = 3 in between (2-way conflicts, profiles/r2_ncu_v2)
+  constexpr int NG = (LOGM + LOGE - 1) / LOGE;
 #pragma unroll
-  for (int lo = 0; lo < LOGM; lo += LOGE) {
-    const int hi = lo + LOGE < LOGM ? lo + LOGE : LOGM;
-    const int ns0 = hi - LOGE > 0 ? hi - LOGE : 0;
-    relayout<LOGE, XS>(x, sm, lane, s0, ns0);
-    s0 = ns0;
+  for (int gi = NG - 1; gi >= 0; --gi) {
+    const int hi = LOGM - gi * LOGE;
+    const int lo = hi - LOGE > 0 ? hi - LOGE : 0;
+    relayout<LOGE, XS>(x, sm, lane, s0, lo);
+    s0 = lo;
 #pragma unroll
     for (int b = lo; b < hi; ++b) {
       const int rb = b - s0;
@@ -185,12 +190,13 @@ __device__ __forceinline__ void warp_inv_n(u64 (&x)[NC][1 << (LOGM - 5)], u64* c
   constexpr int E = 1 << LOGE;
   const u64 q2 = 2 * q;
   int s0 = LOGM - LOGE;
+  constexpr int NG = (LOGM + LOGE - 1) / LOGE;  // forward groups reversed (see warp_inv)
 #pragma unroll
-  for (int lo = 0; lo < LOGM; lo += LOGE) {
-    const int hi = lo + LOGE < LOGM ? lo + LOGE : LOGM;
-    const int ns0 = hi - LOGE > 0 ? hi - LOGE : 0;
-    relayout_n<LOGE, NC>(x, sm, lane, s0, ns0);
-    s0 = ns0;
+  for (int gi = NG - 1; gi >= 0; --gi) {
+    const int hi = LOGM - gi * LOGE;
+    const int lo = hi - LOGE > 0 ? hi - LOGE : 0;
+    relayout_n<LOGE, NC>(x, sm, lane, s0, lo);
+    s0 = lo;
 #pragma unroll
     for (int b = lo; b < hi; ++b) {
       const int rb = b - s0;
