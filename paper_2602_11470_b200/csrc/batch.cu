@@ -133,6 +133,47 @@ __global__ void tensor_sum_kernel(TensorSumArgs A, int limbs, int n, const u64* 
   }
 }
 
+// One block = 128 threads x 2 adjacent coefficients of one limb (16-byte loads);
+// the block walks all outputs, so the operands shared between outputs stay in L1.
+__global__ void __launch_bounds__(128) tensor_sum_multi_kernel(TensorSumMultiArgs A, int limbs, int n, const u64* Q,
+                                                              const u64* MH, const u64* ML) {
+  const size_t i = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 2;
+  if (i >= (size_t)limbs * n) return;
+  const int l = (int)(i / n);
+  const u64 q = Q[l], mh = MH[l], ml = ML[l];
+  for (int o = 0; o < A.nout; ++o) {
+    U128 s0[2] = {{0, 0}, {0, 0}}, s1[2] = {{0, 0}, {0, 0}}, s2[2] = {{0, 0}, {0, 0}};
+    for (int k = A.begin[o], c = 0; k < A.begin[o + 1]; ++k, ++c) {
+      const ulonglong2 x0 = *reinterpret_cast<const ulonglong2*>(A.a0[k] + i);
+      const ulonglong2 x1 = *reinterpret_cast<const ulonglong2*>(A.a1[k] + i);
+      const ulonglong2 y0 = *reinterpret_cast<const ulonglong2*>(A.b0[k] + i);
+      const ulonglong2 y1 = *reinterpret_cast<const ulonglong2*>(A.b1[k] + i);
+      mac128(s0[0], x0.x, y0.x);
+      mac128(s1[0], x0.x, y1.x);
+      mac128(s1[0], x1.x, y0.x);
+      mac128(s2[0], x1.x, y1.x);
+      mac128(s0[1], x0.y, y0.y);
+      mac128(s1[1], x0.y, y1.y);
+      mac128(s1[1], x1.y, y0.y);
+      mac128(s2[1], x1.y, y1.y);
+      if ((c & 15) == 15) {  // 16 * 2 * q^2 < 2^127 for q < 2^61
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          s0[h] = {reduce128(s0[h].hi, s0[h].lo, q, mh, ml), 0};
+          s1[h] = {reduce128(s1[h].hi, s1[h].lo, q, mh, ml), 0};
+          s2[h] = {reduce128(s2[h].hi, s2[h].lo, q, mh, ml), 0};
+        }
+      }
+    }
+    *reinterpret_cast<ulonglong2*>(A.d0[o] + i) =
+        make_ulonglong2(reduce128(s0[0].hi, s0[0].lo, q, mh, ml), reduce128(s0[1].hi, s0[1].lo, q, mh, ml));
+    *reinterpret_cast<ulonglong2*>(A.d1[o] + i) =
+        make_ulonglong2(reduce128(s1[0].hi, s1[0].lo, q, mh, ml), reduce128(s1[1].hi, s1[1].lo, q, mh, ml));
+    *reinterpret_cast<ulonglong2*>(A.d2[o] + i) =
+        make_ulonglong2(reduce128(s2[0].hi, s2[0].lo, q, mh, ml), reduce128(s2[1].hi, s2[1].lo, q, mh, ml));
+  }
+}
+
 __global__ void lift_batch_kernel(LiftBatch B, int limbs, int n, u64 ql, const u64* Q, const u64* MH) {
   const int j = blockIdx.y;
   const size_t total = (size_t)limbs * n;
@@ -409,6 +450,16 @@ void b_tensor_sum(Context& c, const TensorSumArgs& A, int limbs) {
   ProfScope prof(c, kFamMac, 8.0 * limbs * c.n * (4.0 * A.k + 3));
   tensor_sum_kernel<<<grid2((size_t)limbs * c.n, 1), kT, 0, c.stream>>>(A, limbs, c.n, c.tabs.q, c.tabs.mh,
                                                                         c.tabs.ml);
+  post(c);
+}
+
+void b_tensor_sum_multi(Context& c, const TensorSumMultiArgs& A, int limbs) {
+  SF_HPROF("b_tensor_sum_multi");
+  if (!A.nout) return;
+  ProfScope prof(c, kFamMac, 8.0 * limbs * c.n * (4.0 * A.begin[A.nout] + 3.0 * A.nout));
+  const size_t threads = (size_t)limbs * c.n / 2;
+  tensor_sum_multi_kernel<<<(unsigned)((threads + 127) / 128), 128, 0, c.stream>>>(A, limbs, c.n, c.tabs.q,
+                                                                                    c.tabs.mh, c.tabs.ml);
   post(c);
 }
 

@@ -99,6 +99,19 @@ struct TensorSumArgs {  // (D0, D1, D2) = sum_i tensor(a_i, b_i), no relinearisa
   bool accumulate = false;  // add into existing (D0, D1, D2)
 };
 
+// Several lazily relinearised sums at once (the Score*V giants):
+// output o = sum over terms [begin[o], begin[o+1]) of tensor(a_i, b_i). A block
+// walks every output for one coefficient tile, so operands shared by several
+// outputs (the babies) are re-read from L1 / L2 and each distinct operand
+// streams from HBM about once.
+constexpr int kTsmTerms = 600, kTsmOuts = 32;
+struct TensorSumMultiArgs {
+  int nout = 0;
+  int begin[kTsmOuts + 1];
+  u64 *d0[kTsmOuts], *d1[kTsmOuts], *d2[kTsmOuts];
+  const u64 *a0[kTsmTerms], *a1[kTsmTerms], *b0[kTsmTerms], *b1[kTsmTerms];
+};
+
 // Fused column stage of ModUp / ModDown / rescale (fused.cu): per job, the
 // inverse column NTT of ns source limbs (already inverse-row-passed), the
 // basis conversion (mode 0) or rescale lift (mode 1) into nd destination limbs
@@ -207,6 +220,7 @@ void b_ks_sum(Context& c, const KsSumArgs& A);
 
 void b_copy(Context& c, const CopyBatch& B, size_t words);
 void b_tensor_sum(Context& c, const TensorSumArgs& A, int limbs);
+void b_tensor_sum_multi(Context& c, const TensorSumMultiArgs& A, int limbs);
 void b_add(Context& c, const AddBatch& B, int limbs);
 void b_sum(Context& c, const SumArgs& A, int limbs);
 void b_mulpt(Context& c, const MulPtBatch& B, int limbs);
@@ -270,6 +284,10 @@ struct Ct3 {
 };
 // sum_i a_i (x) b_i without relinearisation; charged k ct-ct mults and k-1 additions
 Ct3 tensor_sum(Context& c, const std::vector<const Ct*>& a, const std::vector<const Ct*>& b, bool count = true);
+// several such sums in one pass (operands shared between sums read once); charged like
+// separate tensor_sum calls when count
+std::vector<Ct3> tensor_sum_multi(Context& c, const std::vector<std::vector<const Ct*>>& a,
+                                  const std::vector<std::vector<const Ct*>>& b, bool count = true);
 // component-wise sum of degree-2 partials (no ledger charge)
 Ct3 add_ct3(Context& c, const std::vector<const Ct3*>& xs);
 // relinearise (key switch d2 under s^2) and rescale

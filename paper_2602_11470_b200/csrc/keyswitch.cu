@@ -1072,6 +1072,77 @@ Ct3 tensor_sum(Context& c, const std::vector<const Ct*>& a, const std::vector<co
   return r;
 }
 
+std::vector<Ct3> tensor_sum_multi(Context& c, const std::vector<std::vector<const Ct*>>& a,
+                                  const std::vector<std::vector<const Ct*>>& b, bool count) {
+  SF_HPROF("tensor_sum_multi");
+  require(a.size() == b.size(), kShapeMismatch, "tensor_sum: operand count");
+  std::vector<Ct3> out(a.size());
+  std::vector<std::vector<int>> live(a.size());
+  int limbs_all = 1 << 30;
+  for (size_t o = 0; o < a.size(); ++o) {
+    require(a[o].size() == b[o].size() && !a[o].empty(), kShapeMismatch, "tensor_sum: operand count");
+    int limbs = 1 << 30;
+    double scale = 0.0;
+    for (size_t i = 0; i < a[o].size(); ++i) {
+      check_ct(c, *a[o][i], "mul");
+      check_ct(c, *b[o][i], "mul");
+      const int l = std::min(a[o][i]->limbs, b[o][i]->limbs);
+      require(l - 1 > 0, kLevelUnderflow, "mul: no multiplicative level left");
+      limbs = std::min(limbs, l);
+      if (a[o][i]->zero || b[o][i]->zero) continue;
+      const double sc = a[o][i]->scale * b[o][i]->scale;
+      if (scale == 0.0)
+        scale = sc;
+      else if (std::fabs(sc / scale - 1.0) > 1e-9)
+        fail(kScaleMismatch, "ScaleMismatch: add: operand scales differ");
+      live[o].push_back((int)i);
+    }
+    if (count) {
+      c.ledger.ctct((long long)a[o].size());
+      c.ledger.add((long long)a[o].size() - 1);
+    }
+    if (live[o].empty()) {
+      out[o].d01 = zeros(c, limbs - 1);
+      out[o].d2 = zeros(c, limbs - 1);
+      continue;
+    }
+    out[o].zero = false;
+    out[o].d01 = alloc_ct(c, limbs, scale);
+    out[o].d2 = alloc_ct(c, limbs, scale);
+    limbs_all = std::min(limbs_all, limbs);
+  }
+  // one launch per run of same-limb outputs that fits the parameter block
+  std::map<int, std::vector<int>> by_limbs;
+  for (size_t o = 0; o < a.size(); ++o)
+    if (!out[o].zero) by_limbs[out[o].d01.limbs].push_back((int)o);
+  (void)limbs_all;
+  for (auto& [limbs_run, todo] : by_limbs) {
+  size_t at = 0;
+  while (at < todo.size()) {
+    TensorSumMultiArgs A;
+    int terms = 0;
+    for (; at < todo.size() && A.nout < kTsmOuts; ++at) {
+      const int o = todo[at];
+      if (terms + (int)live[o].size() > kTsmTerms) break;
+      require((int)live[o].size() <= kTsmTerms, kInternal, "tensor_sum_multi: too many terms");
+      A.begin[A.nout] = terms;
+      A.d0[A.nout] = out[o].d01.c0();
+      A.d1[A.nout] = out[o].d01.c1(c.n);
+      A.d2[A.nout] = out[o].d2.c0();
+      for (int i : live[o]) {
+        A.a0[terms] = a[o][i]->c0(), A.a1[terms] = a[o][i]->c1(c.n);
+        A.b0[terms] = b[o][i]->c0(), A.b1[terms] = b[o][i]->c1(c.n);
+        ++terms;
+      }
+      ++A.nout;
+    }
+    A.begin[A.nout] = terms;
+    b_tensor_sum_multi(c, A, limbs_run);
+  }
+  }
+  return out;
+}
+
 Ct3 add_ct3(Context& c, const std::vector<const Ct3*>& xs) {
   SF_HPROF("add_ct3");
   std::vector<const Ct*> a, b;

@@ -1118,11 +1118,16 @@ Ct softmax_times_v_partial(Context& c, const std::vector<Ct>& probs, const KV& c
   }
   std::vector<int> giants;
   std::vector<Ct3> sums;
-  for (auto& [G, ab] : inner) {
-    Ct3 s = tensor_sum(c, ab.first, ab.second, false);
-    if (s.zero) continue;
-    giants.push_back(G);
-    sums.push_back(std::move(s));
+  {
+    std::vector<int> gs;
+    std::vector<std::vector<const Ct*>> ta, tb;
+    for (auto& [G, ab] : inner) gs.push_back(G), ta.push_back(ab.first), tb.push_back(ab.second);
+    std::vector<Ct3> all = tensor_sum_multi(c, ta, tb, false);
+    for (size_t i = 0; i < all.size(); ++i) {
+      if (all[i].zero) continue;
+      giants.push_back(gs[i]);
+      sums.push_back(std::move(all[i]));
+    }
   }
   if (giants.empty()) return zeros(c, limbs - 1);
   std::vector<const Ct3*> sp;
