@@ -497,6 +497,10 @@ def token_stream(be, sf, layer, T=16):
     rope_level = v_o.level
     sf.rope_prepare(be, cfg, layer.pos, rope_level, 0)
     sf.rope_prepare(be, cfg, layer.pos, rope_level, layer.pos % t)
+    # setup: grow the device pool past the stream's peak once (a deployment sizes
+    # its pool at start-up; otherwise the first token that raises the peak maps
+    # new device memory inside its step)
+    be.mem_reserve(16 << 30)
     be.synchronize()
     def token(cache, pos):
         for slot, (w, _) in zip(layer.inputs[:4], host_in):
@@ -529,7 +533,10 @@ def token_stream(be, sf, layer, T=16):
     per_token = []
     be.event_record(20)
     t0 = time.perf_counter()
+    tok_log = os.environ.get("SF_STREAM_LOG")
     for i in range(T):
+        if tok_log:
+            print(f"[stream] token {i}", file=sys.stderr, flush=True)
         ti = time.perf_counter()
         cache, maps, res = token(cache, layer.pos + i)
         per_token.append((time.perf_counter() - ti) * 1e3)
@@ -1320,6 +1327,8 @@ def main():
                 "d2h_bytes_per_step": int(d2h), "breakdown": e2e_parts},
         "e2e_stream": stream,
         "gpu_launches": int(launches),
+        "keys": dict(zip(("count", "GiB", "GiB_untruncated"),
+                         (lambda k: (k[0], round(k[1] / 2**30, 2), round(k[2] / 2**30, 2)))(be.key_stats()))),
         "host_issue_ms_per_step": round(t_idle, 3),
         "host_issue_ms_per_step_queued": round(t_host, 3),
         "host_profile": hprof,

@@ -347,6 +347,12 @@ sf_status sf_ct_refill(sf_context* ctx, sf_ct* ct, const uint64_t* words);
    memory nodes on the context's device (outstanding step outputs of live
    graphs) and by the context's stream-ordered pool (live buffers + free lists). */
 sf_status sf_mem_stats(sf_context* ctx, size_t* graph_bytes, size_t* pool_bytes);
+/* grow the context's stream-ordered pool by `bytes` once (allocate + free): later
+ * allocations up to that peak never map new device memory mid-step */
+sf_status sf_mem_reserve(sf_context* ctx, size_t bytes);
+/* switching keys held: count, bytes, and the bytes they would take untruncated
+ * (every digit; keys are kept for the digits their levels use) */
+sf_status sf_key_stats(sf_context* ctx, int* count, size_t* bytes, size_t* full_bytes);
 
 /* Host-side wall time per internal scope ("name total_us calls" lines), collected
    when SF_HOST_PROF=1 is set in the environment; diagnostics only. */

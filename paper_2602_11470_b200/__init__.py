@@ -321,6 +321,17 @@ class Backend:
                 continue
             raise err
 
+    def mem_reserve(self, nbytes: int) -> None:
+        """Grow the device pool once by nbytes (sf_mem_reserve): a setup step so
+        that a later, larger working set never maps new memory mid-token."""
+        _check(_native.lib().sf_mem_reserve(self.ctx, int(nbytes)))
+
+    def key_stats(self):
+        """(switching keys held, bytes, bytes if untruncated) (sf_key_stats)."""
+        n, b, f = C.c_int(), C.c_size_t(), C.c_size_t()
+        _check(_native.lib().sf_key_stats(self.ctx, C.byref(n), C.byref(b), C.byref(f)))
+        return n.value, b.value, f.value
+
     def mem_stats(self):
         """(graph-node bytes, pool bytes) currently allocated (sf_mem_stats)."""
         g, p = C.c_size_t(), C.c_size_t()

@@ -959,6 +959,32 @@ sf_status sf_mem_stats(sf_context* ctx, size_t* graph_bytes, size_t* pool_bytes)
   });
 }
 
+sf_status sf_key_stats(sf_context* ctx, int* count, size_t* bytes, size_t* full_bytes) {
+  return guard([&] {
+    auto& c = *ctx->c;
+    std::lock_guard<std::mutex> lk(c.mu);
+    size_t b = 0, f = 0;
+    int k = 0;
+    const size_t per_digit = (size_t)2 * c.np * c.n * sizeof(sf::u64);
+    for (auto* m : {&c.keys_pinv_dig, &c.keys_r_dig})
+      for (auto& [g, d] : *m) b += per_digit * d, f += per_digit * c.beta, ++k;
+    for (auto& [g, p] : c.keys) b += p->words * sizeof(sf::u64), f += per_digit * c.beta, ++k;
+    if (count) *count = k;
+    if (bytes) *bytes = b;
+    if (full_bytes) *full_bytes = f;
+  });
+}
+
+sf_status sf_mem_reserve(sf_context* ctx, size_t bytes) {
+  return guard([&] {
+    auto& c = *ctx->c;
+    void* p = nullptr;
+    SF_CUDA(cudaMallocAsync(&p, bytes, c.stream));  // grows the pool once (its release threshold is unbounded)
+    SF_CUDA(cudaFreeAsync(p, c.stream));
+    SF_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
 sf_status sf_host_profile(char* buf, int len, int reset) {
   return guard([&] {
     const std::string s = sf::host_prof_dump(reset != 0);

@@ -226,6 +226,8 @@ struct Context {
   // Montgomery copies of the switching keys for the fused kernels (get_key_mont):
   // every limb times R = 2^64, the Q limbs of the rotation-sum copy also times P^-1
   std::map<u64, BufPtr> keys_pinv, keys_r;
+  std::map<u64, int> keys_pinv_dig, keys_r_dig;  // digits built per key (level-truncated keys)
+  std::vector<BufPtr> key_graveyard;              // superseded truncated keys (captured graphs may read them)
   std::map<std::string, Pt> pt_cache;  // semantic-key plaintext cache (masks)
   std::map<int, BufPtr> level_consts;  // per-limb-count rescale / moddown constants
   std::map<int, std::vector<u64>> level_consts_h;
@@ -322,7 +324,10 @@ u64 galois_elt(const Context& c, int r);
 const BufPtr& get_key(Context& c, u64 g);
 // Montgomery key copy: limbs times R = 2^64 mod q, and with
 // pinv the Q limbs also times P^-1 (rotation sums / hoisted rotations, §3.7a)
-const BufPtr& get_key_mont(Context& c, u64 g, bool pinv);
+// ndig: the key is built (and kept) for its first ndig digits only -- a key used
+// at level l needs ceil((l + 1) / alpha) digits; a later use
+// with more digits rebuilds it (the old buffer stays alive for captured graphs)
+const BufPtr& get_key_mont(Context& c, u64 g, bool pinv, int ndig = 1 << 30);
 void check_ct(const Context& c, const Ct& a, const char* what);
 void check_scales(const Ct& a, const Ct& b, const char* what);
 

@@ -95,6 +95,7 @@ Context::~Context() {
   keys.clear();
   keys_pinv.clear();
   keys_r.clear();
+  key_graveyard.clear();
   conv_plans.clear();
   pt_cache.clear();
   rot_memo.clear();
@@ -587,10 +588,11 @@ Ct mul_plain(Context& c, const Ct& a, const double* slots) {
 // ---------------------------------------------------------------- key switching
 // The switching key for galois element g (0: relinearisation), DESIGN.md §3.4;
 // deterministic in (seed, g), so it can be rebuilt instead of kept.
-static BufPtr build_key(Context& c, u64 g) {
+static BufPtr build_key(Context& c, u64 g, int ndig = 1 << 30) {
   const int np = c.np;
   const size_t n = c.n;
-  BufPtr key = buf(c, (size_t)c.beta * 2 * np * n);
+  ndig = std::min(ndig, c.beta);
+  BufPtr key = buf(c, (size_t)ndig * 2 * np * n);
   BufPtr sp = buf(c, (size_t)np * n);
   if (g == 0)
     k_square(c, sp->p, c.sk->p, np);
@@ -599,7 +601,7 @@ static BufPtr build_key(Context& c, u64 g) {
   BufPtr e = buf(c, (size_t)np * n);
   std::vector<int> primes(np);
   for (int m = 0; m < np; ++m) primes[m] = m;
-  for (int j = 0; j < c.beta; ++j) {
+  for (int j = 0; j < ndig; ++j) {
     const u64 tag = (g << 16) | ((u64)j << 8);
     k_small_rns(c, e->p, stream_key(c.seed, kStreamKeyE | tag), true, nullptr, primes.data(), np);
     ntt_limbs(c, e->p, np, 0, false);
@@ -645,14 +647,25 @@ const BufPtr& get_key(Context& c, u64 g) {
 // disappears; the special-prime limbs (ModDown's conversion input) carry R
 // only. Exact modular identities: results are bit-identical. The unscaled key
 // is rebuilt (deterministic) rather than kept, unless something cached it.
-const BufPtr& get_key_mont(Context& c, u64 g, bool pinv) {
+const BufPtr& get_key_mont(Context& c, u64 g, bool pinv, int ndig) {
   SF_HPROF("get_key_mont");
   auto& cache = pinv ? c.keys_pinv : c.keys_r;
+  auto& digs = pinv ? c.keys_pinv_dig : c.keys_r_dig;
+  // at least two digits: the attention keys serve levels 1 and 2 (one and two
+  // digits at alpha = 2); a one-digit key upgraded mid-stream cost a rebuild
+  ndig = std::max(std::min(2, c.beta), std::min(ndig, c.beta));
   {
     std::lock_guard<std::mutex> lk(c.mu);
     auto it = cache.find(g);
-    if (it != cache.end()) return it->second;
+    if (it != cache.end()) {
+      if (digs[g] >= ndig) return it->second;
+      ndig = std::max(ndig, digs[g]);
+      c.key_graveyard.push_back(it->second);  // a captured graph may still read it
+      cache.erase(it);
+    }
   }
+  static const bool key_log = std::getenv("SF_KEY_LOG") != nullptr;
+  if (key_log) std::fprintf(stderr, "[sf] build key g=%llu pinv=%d ndig=%d\n", (unsigned long long)g, (int)pinv, ndig);
   BufPtr out;
   {
     BufPtr cached;
@@ -662,11 +675,11 @@ const BufPtr& get_key_mont(Context& c, u64 g, bool pinv) {
       if (it != c.keys.end()) cached = it->second;
     }
     if (cached) {
-      const size_t words = (size_t)c.beta * 2 * c.np * c.n;
+      const size_t words = (size_t)ndig * 2 * c.np * c.n;
       out = buf(c, words);
       SF_CUDA(cudaMemcpyAsync(out->p, cached->p, words * sizeof(u64), cudaMemcpyDeviceToDevice, c.stream));
     } else {
-      out = build_key(c, g);
+      out = build_key(c, g, ndig);
     }
   }
   std::vector<u64> f(c.np);
@@ -681,9 +694,10 @@ const BufPtr& get_key_mont(Context& c, u64 g, bool pinv) {
   }
   BufPtr fd = buf(c, f.size());
   SF_CUDA(cudaMemcpyAsync(fd->p, f.data(), f.size() * sizeof(u64), cudaMemcpyHostToDevice, c.stream));
-  k_scale_limbs(c, out->p, c.beta * 2, fd->p);
+  k_scale_limbs(c, out->p, ndig * 2, fd->p);
   host_sync(c);  // f is pageable; keys are built once, off the timed path
   std::lock_guard<std::mutex> lk(c.mu);
+  digs[g] = ndig;
   return cache.emplace(g, out).first->second;
 }
 

@@ -347,7 +347,7 @@ void ks_jobs(Context& c, const ExtB& x, const std::vector<KsJob>& jobs, bool mer
           for (u64 e = (u64)n - 1, b = jb.g, m2 = 2ull * n - 1; e; e >>= 1, b = (b * b) & m2)
             if (e & 1) gi = (gi * b) & m2;
         ka.ginv[k] = gi;
-        ka.key[k] = get_key_mont(c, jb.g <= 1 ? 0 : jb.g, pre)->p;  // the row stage reduces by REDC
+        ka.key[k] = get_key_mont(c, jb.g <= 1 ? 0 : jb.g, pre, x.ndig)->p;  // the row stage reduces by REDC
         ka.acc[k] = accp(j, 0);
         ka.add0[k] = jb.add0;
         ka.add1[k] = jb.add1;
@@ -698,7 +698,7 @@ std::vector<Ct> rot_sum_batch(Context& c, const std::vector<std::vector<SumTerm>
           const int r = pos_mod(tm.r, c.slots);
           A.jsrc[jb] = src[tm.ct];
           A.g[jb] = r == 0 ? 1 : galois_elt(c, r);
-          A.key[jb] = r == 0 ? nullptr : (fused ? get_key_mont(c, A.g[jb], pre) : get_key(c, A.g[jb]))->p;
+          A.key[jb] = r == 0 ? nullptr : (fused ? get_key_mont(c, A.g[jb], pre, x.ndig) : get_key(c, A.g[jb]))->p;
           ++jb;
         }
         const Ct& y = out[chunk[o]];

@@ -24,6 +24,7 @@ buf = ctypes.create_string_buffer(1 << 16)
 if os.environ.get("SF_HOST_PROF"):
     lib.sf_host_profile(buf, len(buf), 1)
 t0 = time.perf_counter()
+print("---- stream", file=sys.stderr, flush=True)
 r = bench.token_stream(be, sf, layer, T)
 print(f"stream: {r}")
 if os.environ.get("SF_STREAM_TWICE"):  # first-use effects: a second pass from the same cache
