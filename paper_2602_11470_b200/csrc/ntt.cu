@@ -479,7 +479,7 @@ __global__ void __launch_bounds__(kWarps * 32, LOGC >= 9 ? 1 : 3) ks_row_kernel(
         w = W[i];
         ws = Ws[i];
       };
-      warp_fwd<LOGC, kBlocked, decltype(tw), false>(x, X, lane, q, tw);
+      warp_fwd<LOGC, kBlocked, decltype(tw), true>(x, X, lane, q, tw);
 #pragma unroll
       for (int k = 0; k < E; ++k) X[xp(rbr(lane * E + k))] = canon4(x[k], q);
     }
@@ -539,7 +539,7 @@ __global__ void __launch_bounds__(kWarps * 32, LOGC >= 9 ? 1 : 3) ks_row_kernel(
           w = W[i];
           ws = Ws[i];
         };
-        warp_inv<LOGC, kBlocked, decltype(tw), false>(v, scratch, lane, q, tw);
+        warp_inv<LOGC, kBlocked, decltype(tw), true>(v, scratch, lane, q, tw);
 #pragma unroll
         for (int k = 0; k < E; ++k) out[(size_t)rd * C + lane + 32 * k] = v[k];
       }

@@ -25,9 +25,10 @@ __device__ __forceinline__ int swz(int i) {
   const int h = i >> 4;
   return i ^ ((h & 1) ? 2 : 0) ^ ((h & 2) ? 13 : 0) ^ ((h & 4) ? 4 : 0) ^ ((h & 8) ? 3 : 0);
 }
-// the round-1 swizzle (2-way conflicted at s0 = 2, but cheaper to address):
-// kept for the register-starved key-switch row stage, where the conflict-free
-// form's extra address registers spill (ks_row_kernel at 128 registers)
+// the round-1 swizzle (2-way conflicted at s0 = 2, but cheaper to address);
+// ks_row_kernel used it while it ran at 128 registers (the conflict-free form
+// spilled there); at 80 registers it takes the conflict-free form (smem bank
+// conflicts 26.6 % -> 5.6 % of shared wavefronts, same time: profiles/r2_ncu_v3_raw)
 __device__ __forceinline__ int swz1(int i) { return i ^ ((i >> 4) & 15); }
 template <bool XS>
 __device__ __forceinline__ int swzx(int i) { return XS ? swz(i) : swz1(i); }
