@@ -571,6 +571,7 @@ def emulated_shards(be, sf, layer, steps, worlds=(2, 4, 8)):
     wl = [layer.wq, layer.wk, layer.wv]
 
     def step_rank(r, W):
+        be.set_value_shard(r, W)  # this rank's aligned companions only
         parts = shard.vmm_multi_partial(be, x, wl, r, W)
         q, k, v = shard.vmm_multi_finish(be, [shard.sum_partials(be, [p] * W) for p in parts], wl)
         qr = sf.rope_apply(be, q, layer.cfg, layer.pos)
@@ -608,6 +609,7 @@ def emulated_shards(be, sf, layer, steps, worlds=(2, 4, 8)):
         out[str(W)] = {"rank_ms": per_rank, "max_rank_ms": max(per_rank),
                        "exchange_bytes_published_per_rank": xbytes,
                        "nvlink_ms_at_900GBps": round(xbytes * (W - 1) / 900e9 * 1e3, 3)}
+    be.set_value_shard(0, 1)
     return out
 
 

@@ -321,6 +321,12 @@ class Backend:
                 continue
             raise err
 
+    def set_value_shard(self, rank: int, world: int) -> None:
+        """Score*V giant groups this process owns (sf_set_value_shard): the appends build
+        aligned companions for those only (automatic with the library-stream / peer
+        exchanges)."""
+        _check(_native.lib().sf_set_value_shard(self.ctx, rank, world))
+
     def mem_reserve(self, nbytes: int) -> None:
         """Grow the device pool once by nbytes (sf_mem_reserve): a setup step so
         that a later, larger working set never maps new memory mid-token."""

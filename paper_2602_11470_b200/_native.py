@@ -65,6 +65,7 @@ SIGNATURES = {
     "sf_graph_destroy": (None, [vp]),
     "sf_mem_stats": (st, [vp, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
     "sf_mem_reserve": (st, [vp, C.c_size_t]),
+    "sf_set_value_shard": (st, [vp, C.c_int, C.c_int]),
     "sf_key_stats": (st, [vp, ip, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
     "sf_ct_refill": (st, [vp, vp, u64p]),
     "sf_context_create": (st, [C.POINTER(SfParams), vpp]),

@@ -975,6 +975,14 @@ sf_status sf_key_stats(sf_context* ctx, int* count, size_t* bytes, size_t* full_
   });
 }
 
+sf_status sf_set_value_shard(sf_context* ctx, int rank, int world) {
+  return guard([&] {
+    sf::require(world >= 1 && rank >= 0 && rank < world, sf::kInvalidTarget, "set_value_shard: bad rank/world");
+    ctx->c->sv_rank = rank;
+    ctx->c->sv_world = world;
+  });
+}
+
 sf_status sf_mem_reserve(sf_context* ctx, size_t bytes) {
   return guard([&] {
     auto& c = *ctx->c;

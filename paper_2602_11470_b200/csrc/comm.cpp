@@ -159,6 +159,8 @@ void comm_init(Context& c, const uint8_t* id_bytes, int rank, int world) {
   c.comm = comm;
   c.rank = rank;
   c.world = world;
+  c.sv_rank = rank;
+  c.sv_world = world;
 }
 
 void comm_destroy(Context& c) {

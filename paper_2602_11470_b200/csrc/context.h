@@ -188,6 +188,10 @@ struct Context {
   // sharded ops (comm.cpp): NCCL communicator on this context's stream
   void* comm = nullptr;
   int rank = 0, world = 1;
+  // the Score*V giant groups this process owns ((G mod 8) mod sv_world == sv_rank,
+  // DESIGN.md §3.9): make_v_pieces builds aligned companions for those only (set by
+  // sf_comm_init / sf_p2p_init / sf_set_value_shard)
+  int sv_rank = 0, sv_world = 1;
   std::map<std::string, std::vector<u64>> comm_hdr, comm_meta;
   void* p2p = nullptr;  // peer-memory exchange state (p2p.cu)
   // exact-size free lists of device buffers (eager path only): every kernel runs

@@ -174,6 +174,7 @@ void p2p_init(Context& c, int rank, int world, size_t cap_words, uint8_t* handle
   require(c.p2p == nullptr, kInvalidTarget, "p2p_init: already initialised");
   auto* p = new P2P;
   p->rank = rank, p->world = world, p->cap = cap_words;
+  c.sv_rank = rank, c.sv_world = world;
   SF_CUDA(cudaSetDevice(c.device));
   SF_CUDA(cudaMalloc(&p->region, (2 * cap_words + kCtrlW) * sizeof(u64)));  // plain allocation: IPC-exportable
   SF_CUDA(cudaMemset(p->region, 0, (2 * cap_words + kCtrlW) * sizeof(u64)));

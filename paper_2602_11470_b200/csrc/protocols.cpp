@@ -682,6 +682,7 @@ KV k_append(Context& c, const KV& cache, const Ct& k_new) {  // kv_attention.cpp
   return out;
 }
 
+constexpr int kSvGroups = 8;  // Score*V giant groups
 static std::vector<Ct> rotate_memo(Context& c, const std::vector<const Ct*>& xs, const std::vector<int>& rs,
                                    const std::vector<char>& keep);
 static bool cache_v_zero(const KV& cache, int g, int idx) {
@@ -742,7 +743,9 @@ std::vector<Ct> make_v_pieces(Context& c, const KV& cache, const Ct& v_open, int
     for (int e = 0; e < dh; ++e) {
       const int w = v_variant_of(cfg, e, u_local);
       const int G = w >= 0 ? w / B : -((-w + B - 1) / B);
-      shift[e] = G * B * t;
+      // a sharded process builds companions for its own giant groups only (the
+      // others' aligned variants are never read here): the appends shard too
+      shift[e] = (int)pos_mod(G, kSvGroups) % c.sv_world == c.sv_rank ? G * B * t : 0;
       esrc[e] = (int)pos_mod(e - G * B, dh);
       if (pos_mod(shift[e], c.slots) && !job_of.count(shift[e]))
         job_of[shift[e]] = (int)jobs.size(), jobs.push_back({0, shift[e]});
@@ -986,8 +989,6 @@ std::vector<Ct> qk_dot(Context& c, const Ct& q, const KV& cache) { return qk_dot
 // the partials summed mod q are the single-device result for any world size
 // dividing kSvGroups; each rank charges the reference's rotations / ct-ct
 // mults / additions of the (group, variant) pairs it owns.
-constexpr int kSvGroups = 8;
-
 int sv_baby(const AttnCfg& cfg) {
   const int nv = v_variant_count(cfg);
   int b = 1;

@@ -188,6 +188,7 @@ class Sharded:
         import torch.distributed as dist
         self.be, self.group = be, group
         self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        be.set_value_shard(self.rank, self.world)
 
     def vmm(self, x: Ciphertext, plan: VmmPlan, mask_output: bool = False) -> Ciphertext:
         part = vmm_partial(self.be, x, plan, self.rank, self.world)
