@@ -243,7 +243,7 @@ def bench_config(alpha, world, sharded):
     """The workload's config, identical on both arms (the reference arm runs the
     same decode step on the host cores)."""
     par = "single" if world == 1 else (
-        f"sharded{world} (one token split over the ranks: VMM giant groups, QK^T key-ct groups, Score*V pairs; "
+        f"sharded{world} (one token split over the ranks: VMM giant groups, QK^T key-ct groups, Score*V giant groups; "
         "fused peer-memory exchange)" if sharded else f"replicas{world}")
     return {"workload": "llama3-8b-layer-decode@n'=2048", "ring_degree": 2 * SLOTS, "slots": SLOTS, "d": D,
             "heads": H, "ffn": FF, "context": NP, "levels": LEVELS, "L": 7, "alpha": alpha, "parallelism": par,
@@ -296,13 +296,16 @@ def run_sharded(args, be, sf, layer, dist, rank, world, clk):
     from paper_2602_11470_b200 import shard
     import torch
     stream = not args.shard_host
+    # the single-device step on every rank, for the bit-exactness check -- before the
+    # exchange is set up (that restricts the appends' aligned companions to the rank's
+    # own Score*V giant groups, sf_set_value_shard)
+    ref = layer.step()
     if args.shard_host:
         sh = shard.Sharded(be)
     elif args.shard_nccl:
         sh = shard.StreamSharded(be)
     else:  # default: the fused peer-memory exchange (csrc/p2p.cu)
         sh = shard.PeerSharded(be)
-    ref = layer.step()  # the single-device step on every rank, for the bit-exactness check
     got = layer.step_sharded(sh)
     exact = all(np.array_equal(a.data(), b.data()) for a, b in zip(ref, got))
     for _ in range(args.warmup):

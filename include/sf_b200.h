@@ -351,8 +351,10 @@ sf_status sf_mem_stats(sf_context* ctx, size_t* graph_bytes, size_t* pool_bytes)
  * allocations up to that peak never map new device memory mid-step */
 sf_status sf_mem_reserve(sf_context* ctx, size_t bytes);
 /* the Score*V giant groups this process owns ((G mod 8) mod world == rank): sf_make_v_pieces
- * builds aligned companions for those only (set automatically by sf_comm_init / sf_p2p_init;
- * results are word-identical either way) */
+ * builds aligned companions for those only (set automatically by sf_comm_init / sf_p2p_init).
+ * Sharded results stay word-identical to the single-device ones; a single-device
+ * sf_softmax_times_v on such a process rotates the other giants' variants instead
+ * (same decryption, other words) */
 sf_status sf_set_value_shard(sf_context* ctx, int rank, int world);
 /* switching keys held: count, bytes, and the bytes they would take untruncated
  * (every digit; keys are kept for the digits their levels use) */
