@@ -220,7 +220,7 @@ class LlamaLayer:
 
     def step_sharded(self, sh, inputs=None):
         """One decode token split over the ranks of `sh` (paper_2602_11470_b200.shard,
-        DESIGN.md §7): VMM giant groups, QK^T key-ct groups and Score*V pairs per
+        DESIGN.md §7): VMM giant groups, QK^T key-ct groups and Score*V giant groups per
         rank, partial ciphertexts all-gathered over NCCL and mod-added on the GPU;
         RoPE, the appends and the replicated tails (reduce ladders, lane fold) on
         every rank. Word-identical to step() for any world size."""
@@ -561,7 +561,7 @@ def token_stream(be, sf, layer, T=16):
 def emulated_shards(be, sf, layer, steps, worlds=(2, 4, 8)):
     """Predicted strong scaling of ONE token over N GPUs, measured on this one:
     for every rank r of a world W, the rank's own work -- its partials (VMM giant
-    groups, QK^T key-ct groups, Score*V pairs; csrc/protocols.cpp *_partial),
+    groups, QK^T key-ct groups, Score*V giant groups; csrc/protocols.cpp *_partial),
     the W-way modular sum of the exchanged partials (sf_sum_partials over W
     ciphertexts: the same reads and adds as the peer-memory reduce kernel) and
     the replicated tail (reduce ladders, RoPE, appends, lane fold,
