@@ -717,7 +717,9 @@ __global__ void __launch_bounds__(kWarps * 32, LOGC >= 9 ? 1 : 2) ks_sum_kernel(
   // Montgomery-domain sums (keys and pm carry R = 2^64: get_key_mont): a product
   // adds < 2^56 to the high word, a plain term c (P * sigma(c0) with P^-1 folded
   // into the keys) enters as c R = c * 2^64, i.e. c added to the high word. A job
-  // raises the high word by < 2^61, so it is brought back below q every 7 jobs
+  // raises the high word by at most 2^60 + 2^56 (q < 2^60: one product's high word
+  // <= 2^56, one plain c < 2^60), so from a reduced high word (< q) 14 jobs stay
+  // below 2^60 (1 + 14 * 1.0625) < 2^64: it is brought back below q every 14 jobs
   // (T changes by multiples of q 2^64) and the sum finishes with one REDC.
   int terms = 0;  // jobs since the last high-word reduction
   auto fold = [&]() {
@@ -731,7 +733,7 @@ __global__ void __launch_bounds__(kWarps * 32, LOGC >= 9 ? 1 : 2) ks_sum_kernel(
   for (int jb = A.out_begin[o]; jb < A.out_begin[o + 1]; ++jb) {
     const int s = A.jsrc[jb];
     const u64 g = A.g[jb];
-    if (terms >= 7) fold();
+    if (terms >= 14) fold();
     if (g <= 1) {  // identity term: P * (c0, c1) on the Q primes
       if (!qt) continue;
       const u64* a0 = A.c0[s] + (size_t)t * n + rowoff;
@@ -1017,7 +1019,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) ks_sum_tma_kernel(KsSumArgs
   for (int jb = b0; jb < b1; ++jb) {
     const int s = A.jsrc[jb];
     const u64 g = A.g[jb];
-    if (terms >= 7) fold();
+    if (terms >= 14) fold();
     if (g <= 1) {  // identity term: P * (c0, c1) on the Q primes, straight from global memory
       if (!qt) continue;
 #pragma unroll
