@@ -372,14 +372,28 @@ u64 P_mod(const Ctx& c, u64 q) {
   return r;
 }
 
-// key for target s' (NTT domain over all primes): [beta][2 (b,a)][np][n]
+constexpr u64 kRelinWide = 1;  // the single-digit relinearisation key
+
+// digit size of a relinearisation at `limbs` limbs: ONE digit over all limbs when
+// log2(Q_l / P) <= 30 (the switch runs at the product scale), else alpha
+int relin_digit(const Ctx& c, int limbs) {
+  double lq = 0.0, lp = 0.0;
+  for (int l = 0; l < limbs; ++l) lq += std::log2((double)c.primes[l]);
+  for (int k = 0; k < c.alpha; ++k) lp += std::log2((double)c.primes[c.P_index(k)]);
+  return (limbs > c.alpha && limbs <= 8 && lq - lp <= 30.0) ? limbs : c.alpha;
+}
+
+// key for target s' (NTT domain over all primes): [ndig][2 (b,a)][np][n], digits of
+// `dig` Q primes (alpha; all Q primes for the wide relinearisation key)
 std::vector<u64> make_ksk(const Ctx& c, u64 kid, const std::vector<u64>& sprime) {
   const int np = c.np(), n = c.n;
-  std::vector<u64> key((size_t)c.beta * 2 * np * n);
-  for (int j = 0; j < c.beta; ++j) {
+  const int dig = kid == kRelinWide ? c.nq() : c.alpha;
+  const int ndig = (c.nq() + dig - 1) / dig;
+  std::vector<u64> key((size_t)ndig * 2 * np * n);
+  for (int j = 0; j < ndig; ++j) {
     std::vector<i64> e(n);
     for (int k = 0; k < n; ++k) e[k] = cbd21(rand64(c.seed, kStreamKeyE | (kid << 16) | ((u64)j << 8), k));
-    const int lo = j * c.alpha, hi = std::min((j + 1) * c.alpha, c.nq());
+    const int lo = j * dig, hi = std::min((j + 1) * dig, c.nq());
 #pragma omp parallel for
     for (int m = 0; m < np; ++m) {
       const u64 q = c.primes[m];
@@ -410,7 +424,7 @@ const std::vector<u64>& get_key(Ctx& c, u64 g) {
   for (int m = 0; m < c.np(); ++m) {
     const u64* s = c.sk.data() + (size_t)m * c.n;
     u64* o = sp.data() + (size_t)m * c.n;
-    if (g == 0) {
+    if (g == 0 || g == kRelinWide) {
       for (int k = 0; k < c.n; ++k) o[k] = mulmod(s[k], s[k], c.primes[m]);
     } else {
       automorph(c, s, o, g);
@@ -605,7 +619,8 @@ void conv_basis(const Ctx& c, const std::vector<int>& src, const std::vector<con
 // each over Q_l u P, NTT domain.
 void key_switch_ext(Ctx& c, const u64* d, int limbs, u64 g, std::vector<u64>& accb, std::vector<u64>& acca) {
   const int n = c.n, np = c.np();
-  const auto& key = get_key(c, g);
+  const int dig = g == 0 ? relin_digit(c, limbs) : c.alpha;  // relinearisation: maybe one wide digit
+  const auto& key = get_key(c, (g == 0 && dig != c.alpha) ? kRelinWide : g);
   std::vector<int> T;  // extended basis, key limb indices
   for (int l = 0; l < limbs; ++l) T.push_back(l);
   for (int k = 0; k < c.alpha; ++k) T.push_back((int)c.P_index(k));
@@ -613,9 +628,9 @@ void key_switch_ext(Ctx& c, const u64* d, int limbs, u64 g, std::vector<u64>& ac
   std::vector<u64> dcoef(d, d + (size_t)limbs * n);
 #pragma omp parallel for
   for (int l = 0; l < limbs; ++l) ntt_inv(c, l, dcoef.data() + (size_t)l * n);
-  const int ndig = (limbs + c.alpha - 1) / c.alpha;
+  const int ndig = (limbs + dig - 1) / dig;
   for (int j = 0; j < ndig; ++j) {
-    const int lo = j * c.alpha, hi = std::min((j + 1) * c.alpha, limbs);
+    const int lo = j * dig, hi = std::min((j + 1) * dig, limbs);
     std::vector<int> src;
     std::vector<const u64*> in;
     for (int i = lo; i < hi; ++i) src.push_back(i), in.push_back(dcoef.data() + (size_t)i * n);

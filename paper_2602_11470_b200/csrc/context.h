@@ -332,6 +332,13 @@ const BufPtr& get_key(Context& c, u64 g);
 // at level l needs ceil((l + 1) / alpha) digits; a later use
 // with more digits rebuilds it (the old buffer stays alive for captured graphs)
 const BufPtr& get_key_mont(Context& c, u64 g, bool pinv, int ndig = 1 << 30);
+// Key id of the single-digit relinearisation key (target s^2, ONE digit over all
+// Q primes; galois element 1 is never a rotation key). A relinearisation at limbs
+// l uses it when log2(Q_l / P) <= 30 (relin_digit): the switch runs at the product
+// scale (>= 2^80), where Q_l / P * e * n is far below the rescale rounding
+// -- half the ModUp NTTs and inner products at levels 1-2.
+constexpr u64 kRelinWide = 1;
+int relin_digit(const Context& c, int limbs);  // digit size of a relinearisation at `limbs` limbs
 void check_ct(const Context& c, const Ct& a, const char* what);
 void check_scales(const Ct& a, const Ct& b, const char* what);
 

@@ -591,10 +591,11 @@ Ct mul_plain(Context& c, const Ct& a, const double* slots) {
 static BufPtr build_key(Context& c, u64 g, int ndig = 1 << 30) {
   const int np = c.np;
   const size_t n = c.n;
-  ndig = std::min(ndig, c.beta);
+  const int dig = g == kRelinWide ? c.L + 1 : c.alpha;  // digit size: one digit over all Q primes for the wide key
+  ndig = std::min(ndig, (c.L + 1 + dig - 1) / dig);
   BufPtr key = buf(c, (size_t)ndig * 2 * np * n);
   BufPtr sp = buf(c, (size_t)np * n);
-  if (g == 0)
+  if (g == 0 || g == kRelinWide)
     k_square(c, sp->p, c.sk->p, np);
   else
     k_automorph(c, sp->p, c.sk->p, nullptr, g, np);
@@ -609,7 +610,7 @@ static BufPtr build_key(Context& c, u64 g, int ndig = 1 << 30) {
     u64* a = key->p + ((size_t)j * 2 + 1) * np * n;
     std::vector<RngKey> keys(np);
     std::vector<u64> pm(np, 0);
-    const int lo = j * c.alpha, hi = std::min((j + 1) * c.alpha, c.L + 1);
+    const int lo = j * dig, hi = std::min((j + 1) * dig, c.L + 1);
     for (int m = 0; m < np; ++m) {
       keys[m] = stream_key(c.seed, kStreamKeyA | tag | (u64)m);
       if (m >= lo && m < hi) {
@@ -653,7 +654,7 @@ const BufPtr& get_key_mont(Context& c, u64 g, bool pinv, int ndig) {
   auto& digs = pinv ? c.keys_pinv_dig : c.keys_r_dig;
   // at least two digits: the attention keys serve levels 1 and 2 (one and two
   // digits at alpha = 2); a one-digit key upgraded mid-stream cost a rebuild
-  ndig = std::max(std::min(2, c.beta), std::min(ndig, c.beta));
+  ndig = g == kRelinWide ? 1 : std::max(std::min(2, c.beta), std::min(ndig, c.beta));
   {
     std::lock_guard<std::mutex> lk(c.mu);
     auto it = cache.find(g);

@@ -16,6 +16,14 @@
 
 namespace sf {
 
+int relin_digit(const Context& c, int limbs) {
+  double lq = 0.0, lp = 0.0;
+  for (int l = 0; l < limbs; ++l) lq += std::log2((double)c.primes[l]);
+  for (int k = 0; k < c.alpha; ++k) lp += std::log2((double)c.primes[c.P_index(k)]);
+  return (limbs > c.alpha && limbs <= 8 && lq - lp <= 30.0) ? limbs : c.alpha;
+}
+
+
 BufPtr make_buf(Context& c, size_t words);
 const u64* level_consts(Context& c, int limbs);
 const ConvPlan& conv_plan(Context& c, const std::vector<int>& src, const std::vector<int>& dst, bool pinv = false);
@@ -25,7 +33,7 @@ namespace {
 
 struct ExtB {
   BufPtr buf;
-  int S = 0, ndig = 0, nt = 0, limbs = 0;
+  int S = 0, ndig = 0, nt = 0, limbs = 0, dig = 0;  // dig: limbs per digit
   bool col_only = false;        // ext holds column-pass output; ks_row_kernel finishes it
   std::vector<const u64*> src;  // the NTT-domain sources (own-prime rows)
   std::vector<int> tprime;
@@ -69,13 +77,15 @@ void ntt_push(Context& c, LimbBatch& b, u64* p, int prime, bool inverse) {
 // full_ext: the ext limbs are fully NTT'd (forward row pass run here) and the
 // digit's own limbs are not copied (the consumer reads the source) -- the
 // layout ks_sum_kernel expects; otherwise ks_row_kernel's column-only layout.
-ExtB mod_up_batch(Context& c, const std::vector<const u64*>& d, int limbs, bool full_ext = false) {
+// dig: digit size of the decomposition (0: alpha; a wide relinearisation: all limbs)
+ExtB mod_up_batch(Context& c, const std::vector<const u64*>& d, int limbs, bool full_ext = false, int dig = 0) {
   SF_HPROF("mod_up_batch");
   ExtB x;
   const size_t n = c.n;
   x.S = (int)d.size();
   x.limbs = limbs;
-  x.ndig = (limbs + c.alpha - 1) / c.alpha;
+  x.dig = dig > 0 ? dig : c.alpha;
+  x.ndig = (limbs + x.dig - 1) / x.dig;
   x.nt = limbs + c.alpha;
   for (int t = 0; t < x.nt; ++t) x.tprime.push_back(t < limbs ? t : c.P_index(t - limbs));
   x.per = (size_t)x.ndig * x.nt * n;
@@ -94,7 +104,7 @@ ExtB mod_up_batch(Context& c, const std::vector<const u64*>& d, int limbs, bool 
     if (lb.count) b_row(c, lb, true), lb.count = 0;
     x.buf = make_buf(c, (size_t)x.S * x.per);
     for (int j = 0; j < x.ndig; ++j) {
-      const int lo = j * c.alpha, hi = std::min((j + 1) * c.alpha, limbs);
+      const int lo = j * x.dig, hi = std::min((j + 1) * x.dig, limbs);
       std::vector<int> src, dst, slot;
       for (int i = lo; i < hi; ++i) src.push_back(i);
       for (int t = 0; t < x.nt; ++t)
@@ -146,7 +156,7 @@ ExtB mod_up_batch(Context& c, const std::vector<const u64*>& d, int limbs, bool 
   x.buf = make_buf(c, (size_t)x.S * x.per);
   LimbBatch lb;
   for (int j = 0; j < x.ndig; ++j) {
-    const int lo = j * c.alpha, hi = std::min((j + 1) * c.alpha, limbs);
+    const int lo = j * x.dig, hi = std::min((j + 1) * x.dig, limbs);
     std::vector<int> src, dst, slot;
     for (int i = lo; i < hi; ++i) src.push_back(i);
     for (int t = 0; t < x.nt; ++t)
@@ -306,7 +316,7 @@ void ks_jobs(Context& c, const ExtB& x, const std::vector<KsJob>& jobs, bool mer
       ka.limbs = limbs;
       ka.nt = nt;
       ka.ndig = x.ndig;
-      ka.alpha = c.alpha;
+      ka.alpha = x.dig;  // digit size (own-prime rows of each digit)
       ka.np = c.np;
       for (int t = 0; t < nt; ++t) ka.tprime[t] = x.tprime[t];
       std::vector<int> order(J);
@@ -347,7 +357,7 @@ void ks_jobs(Context& c, const ExtB& x, const std::vector<KsJob>& jobs, bool mer
           for (u64 e = (u64)n - 1, b = jb.g, m2 = 2ull * n - 1; e; e >>= 1, b = (b * b) & m2)
             if (e & 1) gi = (gi * b) & m2;
         ka.ginv[k] = gi;
-        ka.key[k] = get_key_mont(c, jb.g <= 1 ? 0 : jb.g, pre, x.ndig)->p;  // the row stage reduces by REDC
+        ka.key[k] = get_key_mont(c, jb.g <= 1 ? (x.dig != c.alpha ? kRelinWide : 0) : jb.g, pre, x.ndig)->p;
         ka.acc[k] = accp(j, 0);
         ka.add0[k] = jb.add0;
         ka.add1[k] = jb.add1;
@@ -372,7 +382,7 @@ void ks_jobs(Context& c, const ExtB& x, const std::vector<KsJob>& jobs, bool mer
     for (int j = 0; j < J; ++j) {
       const KsJob& jb = jobs[s0 + j];
       kb.ext[j] = x.ext(jb.src);
-      kb.key[j] = get_key(c, jb.g <= 1 ? 0 : jb.g)->p;
+      kb.key[j] = get_key(c, jb.g <= 1 ? (x.dig != c.alpha ? kRelinWide : 0) : jb.g)->p;
       kb.g[j] = jb.g;
       kb.accb[j] = accp(j, 0);
       kb.acca[j] = accp(j, 1);
@@ -1000,7 +1010,7 @@ std::vector<Ct> mul_batch(Context& c, const std::vector<const Ct*>& a, const std
       }
       tb.count = J;
       b_tensor(c, tb, limbs);
-      ExtB x = mod_up_batch(c, d2, limbs);
+      ExtB x = mod_up_batch(c, d2, limbs, false, relin_digit(c, limbs));
       std::vector<Ct> t(J);
       std::vector<KsJob> kj;
       for (int j = 0; j < J; ++j) {  // relinearise + rescale in one conversion
@@ -1160,7 +1170,7 @@ Ct relin_rescale(Context& c, const Ct3& x) {
   SF_HPROF("relin_rescale");
   if (x.zero) return zeros(c, x.d01.level() - 1);
   const int limbs = std::min(x.d01.limbs, x.d2.limbs);
-  ExtB e = mod_up_batch(c, {x.d2.c0()}, limbs);
+  ExtB e = mod_up_batch(c, {x.d2.c0()}, limbs, false, relin_digit(c, limbs));
   Ct t = alloc_ct(c, limbs - 1, x.d01.scale / (double)c.primes[limbs - 1]);
   ks_jobs(c, e, {KsJob{0, 0, x.d01.c0(), x.d01.c1(c.n), t.c0(), t.c1(c.n)}}, true);
   return t;
@@ -1181,7 +1191,7 @@ std::vector<Ct> relin_batch(Context& c, const std::vector<const Ct3*>& xs, bool 
       const int J = (int)std::min<size_t>(kJobs, idx.size() - s0);
       std::vector<const u64*> d2;
       for (int j = 0; j < J; ++j) d2.push_back(xs[idx[s0 + j]]->d2.c0());
-      ExtB e = mod_up_batch(c, d2, limbs);
+      ExtB e = mod_up_batch(c, d2, limbs, false, relin_digit(c, limbs));
       std::vector<KsJob> kj;
       for (int j = 0; j < J; ++j) {
         const Ct3& x = *xs[idx[s0 + j]];
