@@ -127,10 +127,12 @@ class LlamaLayer:
         gt, dh = cfg.group_tokens, cfg.d_head
         k_cts = []
         self.v_sum = np.zeros(D)  # sum over cached tokens of V[u, h*dh+e] (the attention parity check)
+        self.k_vals = np.zeros((n, D))  # cached keys (the QK^T parity check)
         for j in range((n + t - 1) // t):
             s = np.zeros(SLOTS)
             for tau in range(min(t, n - j * t)):
-                s[np.arange(D) * t + tau] = rng.normal(size=D)
+                self.k_vals[j * t + tau] = rng.normal(size=D)
+                s[np.arange(D) * t + tau] = self.k_vals[j * t + tau]
             k_cts.append(be.encrypt(s, LEVELS["cache"]))
         nv = 2 * dh - 1
         v_cts = []
@@ -215,7 +217,7 @@ class LlamaLayer:
         with be.phase("Down projection"):
             dn = sf.vmm_interleaved(be, h1, None, plan=self.wd)
         mark(7)
-        return [q, k, v, maps[0], att, o, g, u, dn]
+        return [q, k, v, maps[0], att, o, g, u, dn, qr]
 
 
     def step_sharded(self, sh, inputs=None):
@@ -236,7 +238,7 @@ class LlamaLayer:
         o = sh.vmm(h7, self.wo)
         g, u = sh.vmm_multi(h3, [self.wg, self.wu])
         dn = sh.vmm(h1, self.wd)
-        return [q, k, v, maps[0], att, o, g, u, dn]
+        return [q, k, v, maps[0], att, o, g, u, dn, qr]
 
 
 def bench_config(alpha, world, sharded):
@@ -262,7 +264,7 @@ def decrypt_parity(be, layer, outs):
     output (uniform probabilities over the n' = 2048 cached + appended values),
     the output / gate / down projections. Relative max error over the valid
     lanes of each output."""
-    q, _k, _v, _maps, att, o, g, _u, dn = outs
+    q, _k, _v, maps0, att, o, g, _u, dn, qr = outs[:10]
     Wdd = bench_weight(D, D)
     x, h7, h3, h1 = (layer.vals[k] for k in ("x", "h7", "h3", "h1"))
     xw = x @ Wdd
@@ -275,6 +277,14 @@ def decrypt_parity(be, layer, outs):
     for name, (ct, w, t) in want.items():
         got = be.decrypt(ct)[np.arange(len(w)) * t]
         errs[name] = float(np.max(np.abs(got - w)) / max(np.max(np.abs(w)), 1e-30))
+    # QK^T: score map 0 (tokens 0..gt-1, slot h*gt + u) against float64 dot products of
+    # the decrypted RoPE'd query with the cached keys, per head
+    gt, dh = SLOTS // H, D // H
+    qv = be.decrypt(qr)[np.arange(D) * (SLOTS // D)]
+    kk = layer.k_vals[:gt]
+    want_s = np.stack([kk[:, h * dh:(h + 1) * dh] @ qv[h * dh:(h + 1) * dh] for h in range(H)])  # [H, gt]
+    got_s = be.decrypt(maps0).reshape(H, gt)
+    errs["scores"] = float(np.max(np.abs(got_s - want_s)) / max(np.max(np.abs(want_s)), 1e-30))
     return errs
 
 
