@@ -198,6 +198,7 @@ class CkksOracle:
 
     sv_bsgs = True  # Score*V as the product's baby-step / giant-step sum
     qk_shift_fold = True  # the QK^T pack rotation rides the fold
+    rope_fused = True  # RoPE as one rotation sum with a merged rescale
 
     def __init__(self, N: int, L: int, **kw):
         if not is_pow2(N):

@@ -211,6 +211,13 @@ def fused_extract(be, x, succ: str, rope: Optional[dict] = None, coeff=None):
             raise ShapeMismatch("fused_extract: rope successor needs RoPEParams")
         p0, p1, p2 = rope_plaintexts(rope["n"], rope["d_head"], ly, N, rope.get("base", 10000.0))
         s = rope["s"]
+        if getattr(be, "rope_fused", False):
+            # CKKS backends: ONE rotation sum of the unrescaled products with the
+            # rescale merged into its ModDown (mirrors csrc/protocols.cpp rope_apply;
+            # same charge: 3 ct-pt mults, 2 rotations, 2 additions)
+            u = [be.with_layout(be.mul_plain_lazy(x, p), None) for p in (p0, p1, p2)]
+            y = be.rot_sum_rescale([(u[0], 0), (u[1], -s), (u[2], s)])
+            return be.with_layout(y, ly.with_(deferred_mask=False))
         y = be.mul_plain(x, p0)
         y = be.add(y, be.rotate(be.mul_plain(x, p1), -s))
         y = be.add(y, be.rotate(be.mul_plain(x, p2), s))

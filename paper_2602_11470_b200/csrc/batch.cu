@@ -80,6 +80,19 @@ __global__ void sum_kernel(SumArgs A, int limbs, int n, const u64* Q) {
   }
 }
 
+__global__ void sum_multi_kernel(SumMultiArgs A, int limbs, int n, const u64* Q) {
+  const int o = blockIdx.y;
+  const size_t total = (size_t)limbs * n;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < 2 * total; i += (size_t)gridDim.x * blockDim.x) {
+    const int poly = i >= total;
+    const size_t w = i - poly * total;
+    const u64 q = Q[w / n];
+    u64 acc = 0;
+    for (int k = A.begin[o]; k < A.begin[o + 1]; ++k) acc = add_mod(acc, (poly ? A.in1[k] : A.in0[k])[w], q);
+    (poly ? A.out1[o] : A.out0[o])[w] = acc;
+  }
+}
+
 __global__ void mulpt_batch_kernel(MulPtBatch B, int limbs, int n, const u64* Q, const u64* MH, const u64* ML) {
   const int j = blockIdx.y;
   const size_t total = (size_t)limbs * n;
@@ -395,6 +408,14 @@ void b_sum(Context& c, const SumArgs& A, int limbs) {
   SF_HPROF("b_sum");
   ProfScope prof(c, kFamElem, 16.0 * limbs * c.n * (A.k + 1));
   sum_kernel<<<grid2((size_t)limbs * c.n * 2, 1), kT, 0, c.stream>>>(A, limbs, c.n, c.tabs.q);
+  post(c);
+}
+
+void b_sum_multi(Context& c, const SumMultiArgs& A, int limbs) {
+  SF_HPROF("b_sum_multi");
+  if (!A.nout) return;
+  ProfScope prof(c, kFamElem, 16.0 * limbs * c.n * (A.begin[A.nout] + A.nout));
+  sum_multi_kernel<<<grid2((size_t)limbs * c.n * 2, A.nout), kT, 0, c.stream>>>(A, limbs, c.n, c.tabs.q);
   post(c);
 }
 

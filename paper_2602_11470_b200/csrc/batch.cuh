@@ -29,6 +29,13 @@ struct SumArgs {  // out = sum of k ciphertexts
   u64 *out0, *out1;
 };
 
+struct SumMultiArgs {  // out_o = sum of the inputs [begin[o], begin[o+1]) (several sums, one launch)
+  int nout = 0;
+  int begin[65];
+  const u64 *in0[512], *in1[512];
+  u64 *out0[64], *out1[64];
+};
+
 struct MulPtBatch {  // (c0, c1) (.) pt, reduced, no rescale
   int count = 0;
   const u64 *c0[kJobsWide], *c1[kJobsWide], *pt[kJobsWide];
@@ -223,6 +230,7 @@ void b_tensor_sum(Context& c, const TensorSumArgs& A, int limbs);
 void b_tensor_sum_multi(Context& c, const TensorSumMultiArgs& A, int limbs);
 void b_add(Context& c, const AddBatch& B, int limbs);
 void b_sum(Context& c, const SumArgs& A, int limbs);
+void b_sum_multi(Context& c, const SumMultiArgs& A, int limbs);
 void b_mulpt(Context& c, const MulPtBatch& B, int limbs);
 void b_tensor(Context& c, const TensorBatch& B, int limbs);
 void b_lift(Context& c, const LiftBatch& B, int limbs, int last_prime);
@@ -274,6 +282,8 @@ std::vector<Ct> fold_batch(Context& c, const std::vector<const Ct*>& xs, int d_h
                            const std::vector<const Pt*>* post = nullptr, const std::vector<int>* shift = nullptr);
 // sum of k same-level ciphertexts, charged k-1 additions
 Ct sum_cts(Context& c, const std::vector<const Ct*>& xs, bool count = true);
+// several such sums in one launch (uncharged; the caller charges)
+std::vector<Ct> sum_cts_multi(Context& c, const std::vector<std::vector<const Ct*>>& groups);
 
 // Degree-2 ciphertext (d0, d1, d2) decrypting under (1, s, s^2): the lazily
 // relinearised sum of ct x ct products. d01 holds (d0, d1); d2 lives in the

@@ -1291,6 +1291,51 @@ std::vector<Ct> add_batch(Context& c, const std::vector<const Ct*>& a, const std
   return out;
 }
 
+std::vector<Ct> sum_cts_multi(Context& c, const std::vector<std::vector<const Ct*>>& groups) {
+  SF_HPROF("sum_cts_multi");
+  std::vector<Ct> out(groups.size());
+  std::map<int, std::vector<int>> by_limbs;  // groups needing a kernel, by limb count
+  std::vector<std::vector<const Ct*>> live(groups.size());
+  for (size_t g = 0; g < groups.size(); ++g) {
+    require(!groups[g].empty(), kShapeMismatch, "sum: empty");
+    int limbs = 1 << 30;
+    for (const Ct* x : groups[g]) {
+      check_ct(c, *x, "add");
+      limbs = std::min(limbs, x->limbs);
+      if (!x->zero) live[g].push_back(x);
+    }
+    for (const Ct* x : live[g]) check_scales(*live[g][0], *x, "add");
+    if (live[g].size() <= 1) {  // as sum_cts: nothing to add
+      Ct r = live[g].empty() ? *groups[g][0] : *live[g][0];
+      r.limbs = limbs;
+      r.layout.reset();
+      out[g] = r;
+      continue;
+    }
+    out[g] = alloc_ct(c, limbs, live[g][0]->scale);
+    by_limbs[limbs].push_back((int)g);
+  }
+  for (auto& [limbs, gs] : by_limbs) {
+    size_t at = 0;
+    while (at < gs.size()) {
+      SumMultiArgs A;
+      int k = 0;
+      for (; at < gs.size() && A.nout < 64; ++at) {
+        const int g = gs[at];
+        if (k + (int)live[g].size() > 512) break;
+        A.begin[A.nout] = k;
+        for (const Ct* x : live[g]) A.in0[k] = x->c0(), A.in1[k] = x->c1(c.n), ++k;
+        A.out0[A.nout] = out[g].c0();
+        A.out1[A.nout] = out[g].c1(c.n);
+        ++A.nout;
+      }
+      A.begin[A.nout] = k;
+      b_sum_multi(c, A, limbs);
+    }
+  }
+  return out;
+}
+
 Ct sum_cts(Context& c, const std::vector<const Ct*>& xs, bool count) {
   SF_HPROF("sum_cts");
   require(!xs.empty(), kShapeMismatch, "sum: empty");

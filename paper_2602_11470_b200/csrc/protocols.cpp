@@ -637,9 +637,21 @@ Ct rope_apply(Context& c, const Ct& x, const AttnCfg& cfg, long long position, d
   require(x.level() > 0, kLevelUnderflow, "mul_plain: no multiplicative level left");
   const std::vector<Pt> pts = rope_plaintexts(c, ly, x.limbs, dh, position, base);
   const int s = cfg.t();
-  Ct y = mac_plain(c, {&x}, {&pts[0]});
-  y = add(c, y, rotate(c, mac_plain(c, {&x}, {&pts[1]}), -s, false));
-  y = add(c, y, rotate(c, mac_plain(c, {&x}, {&pts[2]}), s, false));
+  // p0 x + Rot(p1 x, -s) + Rot(p2 x, s) as ONE rotation sum of the unrescaled
+  // products with the rescale merged into its ModDown: one
+  // conversion instead of three rescales and two ModDowns; charged as the
+  // reference's 3 mul_plain + 2 rotations + 2 additions
+  Ct y;
+  if (!x.zero) {
+    std::vector<Ct> u = mul_plain_batch(c, {&x, &x, &x}, {&pts[0], &pts[1], &pts[2]}, false, false);
+    for (auto& v : u) v.layout.reset();
+    y = rot_sum_batch(c, {{{&u[0], 0}, {&u[1], -s}, {&u[2], s}}}, false, false, nullptr, true)[0];
+  } else {
+    y = zeros(c, x.level() - 1);
+  }
+  c.ledger.ctpt(3);
+  c.ledger.rot(false, 2);
+  c.ledger.add(2);
   Layout out = ly;
   out.deferred_mask = false;
   y.layout = out;
@@ -945,11 +957,8 @@ std::vector<Ct> qk_dot_partial(Context& c, const Ct& q, const KV& cache, int ran
     groups[where[key]].push_back(&masked[i]);
     if (pos_mod(shift[i], c.slots)) c.ledger.rot(false);
   }
-  std::vector<Ct> sums;
-  for (auto& g : groups) {
-    c.ledger.add((long long)g.size() - 1);
-    sums.push_back(sum_cts(c, g, false));
-  }
+  for (auto& g : groups) c.ledger.add((long long)g.size() - 1);
+  std::vector<Ct> sums = sum_cts_multi(c, groups);  // every group's sum in one launch
   std::vector<const Ct*> sp;
   for (auto& x : sums) sp.push_back(&x);
   std::vector<Ct> gs = rescale_batch(c, sp);
