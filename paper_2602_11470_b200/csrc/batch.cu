@@ -104,6 +104,41 @@ __global__ void mulpt_batch_kernel(MulPtBatch B, int limbs, int n, const u64* Q,
   }
 }
 
+// Shoup companions floor(a 2^64 / q) of `polys` polynomials of `limbs` limbs (contiguous)
+__global__ void shoup_companion_kernel(const u64* a, u64* out, int limbs, int n, int polys, const u64* Q) {
+  const size_t total = (size_t)polys * limbs * n;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const u64 q = Q[(i / n) % limbs];
+    out[i] = (u64)(((unsigned __int128)a[i] << 64) / q);
+  }
+}
+
+// the shared-a form: d0 = b0 a0, d1 = b0 a1 + b1 a0, d2 = b1 a1 as Shoup products
+// (a's companions precomputed once for the batch); two coefficients per thread
+__global__ void tensor_shared_kernel(TensorBatch B, int limbs, int n, const u64* Q) {
+  const int j = blockIdx.y;
+  const size_t total = (size_t)limbs * n;
+  const u64* a0s = B.as;
+  const u64* a1s = B.as + total;
+  for (size_t i = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) * 2; i < total;
+       i += (size_t)gridDim.x * blockDim.x * 2) {
+    const u64 q = Q[i / n];
+    const ulonglong2 x0 = *reinterpret_cast<const ulonglong2*>(B.a0[j] + i);
+    const ulonglong2 x1 = *reinterpret_cast<const ulonglong2*>(B.a1[j] + i);
+    const ulonglong2 w0 = *reinterpret_cast<const ulonglong2*>(a0s + i);
+    const ulonglong2 w1 = *reinterpret_cast<const ulonglong2*>(a1s + i);
+    const ulonglong2 y0 = *reinterpret_cast<const ulonglong2*>(B.b0[j] + i);
+    const ulonglong2 y1 = *reinterpret_cast<const ulonglong2*>(B.b1[j] + i);
+    *reinterpret_cast<ulonglong2*>(B.d0[j] + i) =
+        make_ulonglong2(mul_shoup(y0.x, x0.x, w0.x, q), mul_shoup(y0.y, x0.y, w0.y, q));
+    *reinterpret_cast<ulonglong2*>(B.d1[j] + i) =
+        make_ulonglong2(add_mod(mul_shoup(y1.x, x0.x, w0.x, q), mul_shoup(y0.x, x1.x, w1.x, q), q),
+                        add_mod(mul_shoup(y1.y, x0.y, w0.y, q), mul_shoup(y0.y, x1.y, w1.y, q), q));
+    *reinterpret_cast<ulonglong2*>(B.d2[j] + i) =
+        make_ulonglong2(mul_shoup(y1.x, x1.x, w1.x, q), mul_shoup(y1.y, x1.y, w1.y, q));
+  }
+}
+
 __global__ void tensor_batch_kernel(TensorBatch B, int limbs, int n, const u64* Q, const u64* MH, const u64* ML) {
   const int j = blockIdx.y;
   const size_t total = (size_t)limbs * n;
@@ -432,8 +467,18 @@ void b_tensor(Context& c, const TensorBatch& B, int limbs) {
   SF_HPROF("b_tensor");
   if (!B.count) return;
   ProfScope prof(c, kFamElem, 56.0 * limbs * c.n * B.count);
-  tensor_batch_kernel<<<grid2((size_t)limbs * c.n, B.count), kT, 0, c.stream>>>(B, limbs, c.n, c.tabs.q, c.tabs.mh,
-                                                                                  c.tabs.ml);
+  if (B.as)
+    tensor_shared_kernel<<<grid2((size_t)limbs * c.n / 2, B.count), kT, 0, c.stream>>>(B, limbs, c.n, c.tabs.q);
+  else
+    tensor_batch_kernel<<<grid2((size_t)limbs * c.n, B.count), kT, 0, c.stream>>>(B, limbs, c.n, c.tabs.q,
+                                                                                    c.tabs.mh, c.tabs.ml);
+  post(c);
+}
+
+void b_shoup_companion(Context& c, const u64* a, u64* out, int limbs, int polys) {
+  SF_HPROF("b_shoup_companion");
+  shoup_companion_kernel<<<grid2((size_t)polys * limbs * c.n, 1), kT, 0, c.stream>>>(a, out, limbs, c.n, polys,
+                                                                                      c.tabs.q);
   post(c);
 }
 

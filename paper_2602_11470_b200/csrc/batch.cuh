@@ -46,6 +46,9 @@ struct TensorBatch {
   int count = 0;
   const u64 *a0[kJobs], *a1[kJobs], *b0[kJobs], *b1[kJobs];
   u64 *d0[kJobs], *d1[kJobs], *d2[kJobs];
+  // every job's a is the same ciphertext (QK^T: the replicated query): its Shoup
+  // companions floor(a 2^64 / q) ([2][limbs][n]) turn the four products into Shoup products
+  const u64* as = nullptr;
 };
 
 struct LiftBatch {  // rescale lift of one coefficient-domain limb into `limbs` limbs
@@ -233,6 +236,7 @@ void b_sum(Context& c, const SumArgs& A, int limbs);
 void b_sum_multi(Context& c, const SumMultiArgs& A, int limbs);
 void b_mulpt(Context& c, const MulPtBatch& B, int limbs);
 void b_tensor(Context& c, const TensorBatch& B, int limbs);
+void b_shoup_companion(Context& c, const u64* a, u64* out, int limbs, int polys);  // out = floor(a 2^64 / q_l)
 void b_lift(Context& c, const LiftBatch& B, int limbs, int last_prime);
 void b_conv(Context& c, const ConvBatch& A);
 void b_ks(Context& c, const KsBatch& A);

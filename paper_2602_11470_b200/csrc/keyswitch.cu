@@ -996,6 +996,20 @@ std::vector<Ct> mul_batch(Context& c, const std::vector<const Ct*>& a, const std
   }
   const size_t n = c.n;
   for (auto& [limbs, idx] : by_limbs) {
+    // one shared left operand (the QK^T query against every key ciphertext): its
+    // Shoup companions once, then Shoup products (canonical, bit-identical)
+    bool shared = idx.size() > 1;
+    for (int i : idx) shared = shared && a[i] == a[idx[0]];
+    BufPtr as;
+    if (shared) {
+      const Ct& x = *a[idx[0]];
+      BufPtr ac = make_buf(c, (size_t)2 * limbs * n);  // c0, c1 at `limbs` limbs, contiguous
+      SF_CUDA(cudaMemcpyAsync(ac->p, x.c0(), (size_t)limbs * n * 8, cudaMemcpyDeviceToDevice, c.stream));
+      SF_CUDA(cudaMemcpyAsync(ac->p + (size_t)limbs * n, x.c1(c.n), (size_t)limbs * n * 8, cudaMemcpyDeviceToDevice,
+                              c.stream));
+      as = make_buf(c, (size_t)2 * limbs * n);
+      b_shoup_companion(c, ac->p, as->p, limbs, 2);
+    }
     for (size_t s0 = 0; s0 < idx.size(); s0 += kJobs) {
       const int J = (int)std::min<size_t>(kJobs, idx.size() - s0);
       BufPtr d = make_buf(c, (size_t)J * 3 * limbs * n);
@@ -1009,6 +1023,7 @@ std::vector<Ct> mul_batch(Context& c, const std::vector<const Ct*>& a, const std
         d2.push_back(dp(j, 2));
       }
       tb.count = J;
+      tb.as = as ? as->p : nullptr;
       b_tensor(c, tb, limbs);
       ExtB x = mod_up_batch(c, d2, limbs, false, relin_digit(c, limbs));
       std::vector<Ct> t(J);
