@@ -96,6 +96,22 @@ __global__ void sum_multi_kernel(SumMultiArgs A, int limbs, int n, const u64* Q)
 __global__ void mulpt_batch_kernel(MulPtBatch B, int limbs, int n, const u64* Q, const u64* MH, const u64* ML) {
   const int j = blockIdx.y;
   const size_t total = (size_t)limbs * n;
+  if (const u64* cs = B.cs[j]) {  // shared ciphertext: Shoup products, two coefficients per thread
+    for (size_t i = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) * 2; i < total;
+         i += (size_t)gridDim.x * blockDim.x * 2) {
+      const u64 q = Q[i / n];
+      const ulonglong2 p = *reinterpret_cast<const ulonglong2*>(B.pt[j] + i);
+      const ulonglong2 x0 = *reinterpret_cast<const ulonglong2*>(B.c0[j] + i);
+      const ulonglong2 x1 = *reinterpret_cast<const ulonglong2*>(B.c1[j] + i);
+      const ulonglong2 w0 = *reinterpret_cast<const ulonglong2*>(cs + i);
+      const ulonglong2 w1 = *reinterpret_cast<const ulonglong2*>(cs + total + i);
+      *reinterpret_cast<ulonglong2*>(B.o0[j] + i) =
+          make_ulonglong2(mul_shoup(p.x, x0.x, w0.x, q), mul_shoup(p.y, x0.y, w0.y, q));
+      *reinterpret_cast<ulonglong2*>(B.o1[j] + i) =
+          make_ulonglong2(mul_shoup(p.x, x1.x, w1.x, q), mul_shoup(p.y, x1.y, w1.y, q));
+    }
+    return;
+  }
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
     const int l = (int)(i / n);
     const u64 p = B.pt[j][i];

@@ -40,6 +40,9 @@ struct MulPtBatch {  // (c0, c1) (.) pt, reduced, no rescale
   int count = 0;
   const u64 *c0[kJobsWide], *c1[kJobsWide], *pt[kJobsWide];
   u64 *o0[kJobsWide], *o1[kJobsWide];
+  // per job: Shoup companions of (c0, c1) ([2][limbs][n]) when the ciphertext feeds
+  // several products of the batch (computed once; the products become Shoup products)
+  const u64* cs[kJobsWide] = {};
 };
 
 struct TensorBatch {

@@ -1230,6 +1230,25 @@ std::vector<Ct> mul_plain_batch(Context& c, const std::vector<const Ct*>& xs, co
   std::vector<const Ct*> todo;
   std::vector<int> where;
   std::map<int, MulPtBatch> by_limbs;
+  // ciphertexts feeding four or more products (value pieces of one v_open, RoPE):
+  // Shoup companions once per (buffer, limbs)
+  std::map<std::pair<const u64*, int>, int> uses;
+  for (const Ct* x : xs)
+    if (!x->zero) ++uses[{x->c0(), x->limbs}];
+  std::map<std::pair<const u64*, int>, BufPtr> comp;
+  for (auto& [key, cnt] : uses) {
+    if (cnt < 4) continue;
+    const Ct* x = nullptr;
+    for (const Ct* y : xs)
+      if (!y->zero && y->c0() == key.first && y->limbs == key.second) x = y;
+    const size_t w = (size_t)x->limbs * c.n;
+    BufPtr ac = make_buf(c, 2 * w);
+    SF_CUDA(cudaMemcpyAsync(ac->p, x->c0(), w * 8, cudaMemcpyDeviceToDevice, c.stream));
+    SF_CUDA(cudaMemcpyAsync(ac->p + w, x->c1(c.n), w * 8, cudaMemcpyDeviceToDevice, c.stream));
+    BufPtr cs = make_buf(c, 2 * w);
+    b_shoup_companion(c, ac->p, cs->p, x->limbs, 2);
+    comp[key] = cs;
+  }
   for (size_t i = 0; i < xs.size(); ++i) {
     const Ct& x = *xs[i];
     check_ct(c, x, "mul_plain");
@@ -1246,7 +1265,9 @@ std::vector<Ct> mul_plain_batch(Context& c, const std::vector<const Ct*>& xs, co
     MulPtBatch& B = by_limbs[x.limbs];
     B.c0[B.count] = x.c0(), B.c1[B.count] = x.c1(c.n), B.pt[B.count] = ps[i]->buf->p;
     B.o0[B.count] = tmp[i].c0(), B.o1[B.count] = tmp[i].c1(c.n);
-    if (++B.count == kJobsWide) b_mulpt(c, B, x.limbs), B.count = 0;
+    auto ci = comp.find({x.c0(), x.limbs});
+    B.cs[B.count] = ci != comp.end() ? ci->second->p : nullptr;
+    if (++B.count == kJobsWide) b_mulpt(c, B, x.limbs), B.count = 0, std::fill(B.cs, B.cs + kJobsWide, nullptr);
     todo.push_back(&tmp[i]);
     where.push_back((int)i);
   }
