@@ -1182,7 +1182,9 @@ def main():
     # 2 MACs, 3 fused column stages (ModUp / ModDown / rescale conversions), 4 elementwise, 5 sampling
     fams = ["ntt_rows", "keyswitch_rows", "ctpt_mac", "fused_col", "elementwise", "sampling"]
     prof = {f: {"ms_per_step": ms[i] / args.steps, "launches_per_step": nl[i] / args.steps,
-                "GBps": (by[i] / (ms[i] * 1e-3) / 1e9) if ms[i] > 0 else None} for i, f in enumerate(fams)}
+                # algorithmic-byte model (counts L2- and shared-memory-served re-reads: an
+                # upper bound on DRAM traffic; measured DRAM bytes: profiles/r2_traffic_v3.json)
+                "alg_GBps": (by[i] / (ms[i] * 1e-3) / 1e9) if ms[i] > 0 else None} for i, f in enumerate(fams)}
     dom = max(range(6), key=lambda i: ms[i])
     P = peaks()
     peak = P.get("hbm_gbs", 6650.0)
@@ -1325,7 +1327,9 @@ def main():
         "vs_baseline": None, "dtype": "u64",
         "data": "synthetic: reference bench weights sin(0.001(31r+c)+0.25), N(0,1) activations/cache, seeded",
         "config": bench_config(args.alpha, world, False),
-        "hevmm_ct_per_s": round(vmm_per_step * world / (ms_step * 1e-3), 2),
+        # the decode step's 7 VMMs over the WHOLE step time (attention included); the
+        # HE-VMM throughput proper is hevmm_c1
+        "step_vmms_per_s": round(vmm_per_step * world / (ms_step * 1e-3), 2),
         "hevmm_c1": hevmm,
         "attention_c2": c2,
         "linear_c3": c3,
