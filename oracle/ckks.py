@@ -71,6 +71,7 @@ def lib():
             "ock_tensor_sum": (vp, [vp, C.POINTER(vp), C.POINTER(vp), C.c_int]),
             "ock_rot_sum": (vp, [vp, C.POINTER(vp), C.POINTER(C.c_int), C.c_int]),
             "ock_rot_sum_rescale": (vp, [vp, C.POINTER(vp), C.POINTER(C.c_int), C.c_int]),
+            "ock_rot_sum_rescale_scaled": (vp, [vp, C.POINTER(vp), C.POINTER(C.c_int), C.c_int]),
             "ock_mac_plain_lazy": (vp, [vp, C.POINTER(vp), DP, C.c_int]),
             "ock_relin_rescale": (vp, [vp, vp]),
             "ock_relin": (vp, [vp, vp]),
@@ -199,6 +200,7 @@ class CkksOracle:
     sv_bsgs = True  # Score*V as the product's baby-step / giant-step sum
     qk_shift_fold = True  # the QK^T pack rotation rides the fold
     rope_fused = True  # RoPE as one rotation sum with a merged rescale
+    vmm_scaled_giants = True  # HE-VMM giants rotated before their rescale, wider digits
 
     def __init__(self, N: int, L: int, **kw):
         if not is_pow2(N):
@@ -367,6 +369,23 @@ class CkksOracle:
                     layout = None
         return OCt(self, lib().ock_mac_plain(self.ptr, arr, _dp(pts), len(terms)), lvl - 1, layout)
 
+    def mac_plain_lazy(self, terms):
+        """sum_k ct_k * p_k WITHOUT the rescale (scale * q_top, same limbs), charged
+        as the reference's k mul_plain + k - 1 additions (the HE-VMM giants, whose
+        rescale is merged into their rotation sum)."""
+        for c, _ in terms:
+            self._check(c, "mul_plain")
+            if c.level <= 0:
+                raise LevelUnderflow("mul_plain: no multiplicative level left")
+        for i, _ in enumerate(terms):
+            self.ledger.count_ct_pt()
+            if i:
+                self.ledger.count_add()
+        lvl = min(c.level for c, _ in terms)
+        pts = np.ascontiguousarray(np.stack([self._slots(p, "mul_plain") for _, p in terms]))
+        arr = (C.c_void_p * len(terms))(*[c.ptr for c, _ in terms])
+        return OCt(self, lib().ock_mac_plain_lazy(self.ptr, arr, _dp(pts), len(terms)), lvl, None)
+
     def mul_plain_lazy(self, a, p):
         """a * p WITHOUT the rescale: the raw product at scale * q_top on the
         same limbs, charged as the reference's mul_plain; the rescale happens in
@@ -379,10 +398,12 @@ class CkksOracle:
         arr = (C.c_void_p * 1)(a.ptr)
         return OCt(self, lib().ock_mac_plain_lazy(self.ptr, arr, _dp(pts), 1), a.level, a.layout)
 
-    def rot_sum_rescale(self, terms, hoisted: bool = False):
+    def rot_sum_rescale(self, terms, hoisted: bool = False, scaled: bool = False):
         """rot_sum of unrescaled products (mul_plain_lazy) with the pending
         rescale merged into the sum's ModDown (one basis conversion from
-        {q_top} u P); same charge as rot_sum, one level lower."""
+        {q_top} u P); same charge as rot_sum, one level lower. scaled: the
+        terms are still at scale >= 2^80, so their decomposition uses the wider
+        digits of scaled_digit (the HE-VMM giants)."""
         for a, _ in terms:
             self._check(a, "rotate")
         for i, (a, r) in enumerate(terms):
@@ -395,7 +416,8 @@ class CkksOracle:
         lvl = min(a.level for a, _ in terms)
         if lvl <= 0:
             raise LevelUnderflow("mul_plain: no multiplicative level left")
-        return OCt(self, lib().ock_rot_sum_rescale(self.ptr, arr, rr, len(terms)), lvl - 1, None)
+        fn = lib().ock_rot_sum_rescale_scaled if scaled else lib().ock_rot_sum_rescale
+        return OCt(self, fn(self.ptr, arr, rr, len(terms)), lvl - 1, None)
 
     def rotate(self, a, r: int, hoisted: bool = False):
         self._check(a, "rotate")

@@ -385,14 +385,36 @@ int relin_digit(const Ctx& c, int limbs) {
 
 // key for target s' (NTT domain over all primes): [ndig][2 (b,a)][np][n], digits of
 // `dig` Q primes (alpha; all Q primes for the wide relinearisation key)
+constexpr u64 kKeyGalMask = (1ull << 40) - 1;  // key id: galois element | digit size (other than alpha) << 40
+
+// largest digit size whose digits all stay within P 2^30 (at most 8 limbs): the key
+// switches of ciphertexts at scale >= 2^80 (the HE-VMM giants before their rescale)
+int scaled_digit(const Ctx& c, int limbs) {
+  double lp = 0.0;
+  for (int k = 0; k < c.alpha; ++k) lp += std::log2((double)c.primes[c.P_index(k)]);
+  int best = c.alpha;
+  for (int d = c.alpha + 1; d <= std::min(8, limbs); ++d) {
+    bool ok = true;
+    for (int lo = 0; lo < limbs && ok; lo += d) {
+      double lq = 0.0;
+      for (int l = lo; l < std::min(limbs, lo + d); ++l) lq += std::log2((double)c.primes[l]);
+      ok = lq - lp <= 30.0;
+    }
+    if (ok) best = d;
+  }
+  return best;
+}
+
 std::vector<u64> make_ksk(const Ctx& c, u64 kid, const std::vector<u64>& sprime) {
   const int np = c.np(), n = c.n;
-  const int dig = kid == kRelinWide ? c.nq() : c.alpha;
+  const u64 gal = kid & kKeyGalMask, kd = kid >> 40;
+  const int dig = kid == kRelinWide ? c.nq() : (kd ? (int)kd : c.alpha);
   const int ndig = (c.nq() + dig - 1) / dig;
   std::vector<u64> key((size_t)ndig * 2 * np * n);
   for (int j = 0; j < ndig; ++j) {
     std::vector<i64> e(n);
-    for (int k = 0; k < n; ++k) e[k] = cbd21(rand64(c.seed, kStreamKeyE | (kid << 16) | ((u64)j << 8), k));
+    const u64 tag = (gal << 16) | ((u64)j << 8) | (kd << 44);  // independent streams per digit layout
+    for (int k = 0; k < n; ++k) e[k] = cbd21(rand64(c.seed, kStreamKeyE | tag, k));
     const int lo = j * dig, hi = std::min((j + 1) * dig, c.nq());
 #pragma omp parallel for
     for (int m = 0; m < np; ++m) {
@@ -406,7 +428,7 @@ std::vector<u64> make_ksk(const Ctx& c, u64 kid, const std::vector<u64>& sprime)
       const u64* s = c.sk.data() + (size_t)m * n;
       const u64* sp = sprime.data() + (size_t)m * n;
       for (int k = 0; k < n; ++k) {
-        a[k] = rand_mod(c.seed, kStreamKeyA | (kid << 16) | ((u64)j << 8) | (u64)m, k, q);
+        a[k] = rand_mod(c.seed, kStreamKeyA | tag | (u64)m, k, q);
         u64 v = submod(et[k], mulmod(a[k], s[k], q), q);
         if (pm) v = addmod(v, mulmod(pm, sp[k], q), q);
         b[k] = v;
@@ -424,10 +446,11 @@ const std::vector<u64>& get_key(Ctx& c, u64 g) {
   for (int m = 0; m < c.np(); ++m) {
     const u64* s = c.sk.data() + (size_t)m * c.n;
     u64* o = sp.data() + (size_t)m * c.n;
-    if (g == 0 || g == kRelinWide) {
+    const u64 gal = g & kKeyGalMask;
+    if (gal == 0 || g == kRelinWide) {
       for (int k = 0; k < c.n; ++k) o[k] = mulmod(s[k], s[k], c.primes[m]);
     } else {
-      automorph(c, s, o, g);
+      automorph(c, s, o, gal);
     }
   }
   return c.keys.emplace(g, make_ksk(c, g, sp)).first->second;
@@ -617,10 +640,13 @@ void conv_basis(const Ctx& c, const std::vector<int>& src, const std::vector<con
 // (NTT, `limbs` limbs), the NTT-domain automorphism g applied to the ModUp
 // output, and the inner product with key g, ADDED into (accb, acca) = nt limbs
 // each over Q_l u P, NTT domain.
-void key_switch_ext(Ctx& c, const u64* d, int limbs, u64 g, std::vector<u64>& accb, std::vector<u64>& acca) {
+void key_switch_ext(Ctx& c, const u64* d, int limbs, u64 g, std::vector<u64>& accb, std::vector<u64>& acca,
+                    int dig_in = 0) {
   const int n = c.n, np = c.np();
-  const int dig = g == 0 ? relin_digit(c, limbs) : c.alpha;  // relinearisation: maybe one wide digit
-  const auto& key = get_key(c, (g == 0 && dig != c.alpha) ? kRelinWide : g);
+  // relinearisation: maybe one wide digit; rotations: alpha, or dig_in (scaled sums)
+  const int dig = g == 0 ? relin_digit(c, limbs) : (dig_in ? dig_in : c.alpha);
+  const u64 kid = g == 0 ? (dig != c.alpha ? kRelinWide : 0) : (dig != c.alpha ? g | ((u64)dig << 40) : g);
+  const auto& key = get_key(c, kid);
   std::vector<int> T;  // extended basis, key limb indices
   for (int l = 0; l < limbs; ++l) T.push_back(l);
   for (int k = 0; k < c.alpha; ++k) T.push_back((int)c.P_index(k));
@@ -766,7 +792,7 @@ void key_switch(Ctx& c, const u64* d, int limbs, u64 g, u64* kb, u64* ka) {
 // rounding of one instead of k terms.
 // rescale: the sum is also rescaled by its top prime, in the ModDown's basis
 // conversion (mod_down_rescale; the QK^T pack).
-Ct* rot_sum(Ctx& c, const Ct* const* a, const int* rots, int k, bool rescale = false) {
+Ct* rot_sum(Ctx& c, const Ct* const* a, const int* rots, int k, bool rescale = false, int dig = 0) {
   int limbs = 1 << 30;
   double scale = 0.0;
   bool any = false;
@@ -787,7 +813,7 @@ Ct* rot_sum(Ctx& c, const Ct* const* a, const int* rots, int k, bool rescale = f
     if (a[i]->zero) continue;
     const int r = (int)(((long long)rots[i] % c.slots + c.slots) % c.slots);
     const u64 g = r == 0 ? 1 : galois_elt(c, r);
-    if (r != 0) key_switch_ext(c, poly(c, a[i], 1, 0), limbs, g, accb, acca);
+    if (r != 0) key_switch_ext(c, poly(c, a[i], 1, 0), limbs, g, accb, acca, dig);
 #pragma omp parallel for
     for (int l = 0; l < limbs; ++l) {
       const u64 q = c.primes[l];
@@ -1147,6 +1173,16 @@ void* ock_rot_sum(void* c, void** a, const int* rots, int k) {
 }
 void* ock_rot_sum_rescale(void* c, void** a, const int* rots, int k) {
   return guard([&]() -> void* { return rot_sum(*static_cast<Ctx*>(c), (Ct* const*)a, rots, k, true); });
+}
+// rot_sum_rescale of products still at scale >= 2^80 (the HE-VMM giants): the
+// terms' decomposition uses scaled_digit(limbs)
+void* ock_rot_sum_rescale_scaled(void* c, void** a, const int* rots, int k) {
+  return guard([&]() -> void* {
+    Ctx& cx = *static_cast<Ctx*>(c);
+    int limbs = 1 << 30;
+    for (int i = 0; i < k; ++i) limbs = std::min(limbs, static_cast<Ct*>(a[i])->limbs);
+    return rot_sum(cx, (Ct* const*)a, rots, k, true, scaled_digit(cx, limbs));
+  });
 }
 void* ock_mac_plain_lazy(void* c, void** cts, const double* slots, int k) {
   return guard([&]() -> void* { return mac_plain(*static_cast<Ctx*>(c), (Ct* const*)cts, slots, k, false); });

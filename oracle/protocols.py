@@ -131,18 +131,9 @@ def vmm_interleaved(be, x, W: np.ndarray, bsgs: bool = False, out_offset: int = 
     else:
         b, giants = bsgs_split(s.k)
         baby = [stair] + [be.rotate(stair, g1 * unit, hoisted=True) for g1 in range(1, b)]
-        partials = []
-        for g2 in range(giants):
-            shift = g2 * b * unit
-            terms = [(baby[g1], interleaved_plain(s, W, g2 * b + g1, shift))
-                     for g1 in range(b) if g2 * b + g1 < s.k]
-            partials.append((be.mac_plain(terms), shift))
-        # giant alignment + sum (vmm.cpp:221-222) as GIANT_GROUPS rotation sums
-        # (DESIGN.md §3.8): giants g2 = r mod GIANT_GROUPS share one ModDown,
-        # so shards owning whole groups reproduce this sum exactly
         acc = None
         for r in range(min(GIANT_GROUPS, giants)):
-            grp = be.rot_sum(partials[r::GIANT_GROUPS])
+            grp = vmm_giant_group(be, s, W, baby, b, unit, range(r, giants, GIANT_GROUPS))
             acc = grp if acc is None else be.add(acc, grp)
     # 3. reduce (vmm.cpp:226-230)
     acc = _fold_steps(be, acc, reduce_rots(s))
@@ -150,6 +141,24 @@ def vmm_interleaved(be, x, W: np.ndarray, bsgs: bool = False, out_offset: int = 
     if mask_output:
         acc = be.mul_plain(acc, stride_mask(N, s.t_out, s.tau_out))
     return be.with_layout(acc, Layout("interleaved", s.d_out, s.t_out, s.tau_out, 1, not mask_output))
+
+
+def vmm_giant_group(be, s, W, baby, b, unit, giants):
+    """One giant group of vmm.cpp:206-222: every giant's partial MAC, aligned by its
+    giant rotation, summed as ONE rotation sum (giants g2 = r mod
+    GIANT_GROUPS share a ModDown, so shards owning whole groups reproduce the sum).
+    CKKS backends keep the partials unrescaled (scale * q_top) and merge the
+    rescale into the sum's ModDown, the rotations decomposed with the wider digits
+    a >= 2^80 scale allows (csrc/protocols.cpp vmm_partial)."""
+    scaled = getattr(be, "vmm_scaled_giants", False)
+    mac = be.mac_plain_lazy if scaled else be.mac_plain
+    partials = []
+    for g2 in giants:
+        shift = g2 * b * unit
+        terms = [(baby[g1], interleaved_plain(s, W, g2 * b + g1, shift))
+                 for g1 in range(b) if g2 * b + g1 < s.k]
+        partials.append((mac(terms), shift))
+    return be.rot_sum_rescale(partials, scaled=True) if scaled else be.rot_sum(partials)
 
 
 def predict_interleaved_cost(N: int, rows: int, cols: int, bsgs: bool = False, mask_output: bool = False):

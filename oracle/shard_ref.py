@@ -35,13 +35,7 @@ def vmm_partial(be, x, W, bsgs, out_offset, rank, world):
     baby = [stair] + [be.rotate(stair, g1 * unit, hoisted=True) for g1 in range(1, b)]
     acc = None
     for r in groups:
-        terms_r = []
-        for g2 in range(r, giants, G):
-            shift = g2 * b * unit
-            terms = [(baby[g1], P.interleaved_plain(s, W, g2 * b + g1, shift))
-                     for g1 in range(b) if g2 * b + g1 < s.k]
-            terms_r.append((be.mac_plain(terms), shift))
-        grp = be.rot_sum(terms_r)
+        grp = P.vmm_giant_group(be, s, W, baby, b, unit, range(r, giants, G))
         acc = grp if acc is None else be.add(acc, grp)
     return acc
 

@@ -273,8 +273,11 @@ struct SumTerm {
 };
 // rescale: the sum is rescaled by its top prime in the same basis conversion as
 // its ModDown (merged): one conversion from {q_top} u P
+// dig: digit size of the terms' decomposition (0: alpha; scaled_digit(limbs) for
+// sums of products still at scale >= 2^80, with the rescale merged)
 std::vector<Ct> rot_sum_batch(Context& c, const std::vector<std::vector<SumTerm>>& groups, bool hoisted,
-                              bool count = true, const std::vector<const Pt*>* post = nullptr, bool rescale = false);
+                              bool count = true, const std::vector<const Pt*>* post = nullptr, bool rescale = false,
+                              int dig = 0);
 // doubling chains x <- x + Rot(x, r) over rots[i] (radix rotation sums); charged
 // as the reference's rotate + add steps when count && lead
 // post (fused path only): per chain an NTT-domain plaintext multiplied into the

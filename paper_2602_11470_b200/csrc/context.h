@@ -317,7 +317,8 @@ void decrypt(Context& c, const Ct& a, double* out);
 Ct add(Context& c, const Ct& a, const Ct& b, bool sub = false, bool count = true);
 Ct add_plain(Context& c, const Ct& a, const double* slots);
 Ct rescale(Context& c, const Ct& a);
-Ct mac_plain(Context& c, const std::vector<const Ct*>& cts, const std::vector<const Pt*>& pts, bool count = true);
+Ct mac_plain(Context& c, const std::vector<const Ct*>& cts, const std::vector<const Pt*>& pts, bool count = true,
+              bool rescale_out = true);
 Ct mul_plain(Context& c, const Ct& a, const double* slots);
 Ct mul(Context& c, const Ct& a, const Ct& b, bool count = true);
 Ct rotate(Context& c, const Ct& a, int r, bool hoisted, bool count = true);
@@ -339,6 +340,14 @@ const BufPtr& get_key_mont(Context& c, u64 g, bool pinv, int ndig = 1 << 30);
 // -- half the ModUp NTTs and inner products at levels 1-2.
 constexpr u64 kRelinWide = 1;
 int relin_digit(const Context& c, int limbs);  // digit size of a relinearisation at `limbs` limbs
+// Switching-key ids: the galois element in the low 40 bits, a digit size other
+// than alpha in bits 40-47 (keys for key switches at a product scale >= 2^80,
+// e.g. the HE-VMM giant rotations before their rescale: DESIGN.md §3.6b)
+constexpr u64 kKeyGalMask = (1ull << 40) - 1;
+inline u64 key_id(u64 gal, int dig, int alpha) { return dig == alpha ? gal : gal | ((u64)dig << 40); }
+// largest digit size whose digits all stay within P 2^30 (at most 8 limbs): the
+// key switches of ciphertexts at scale >= 2^80 use it
+int scaled_digit(const Context& c, int limbs);
 void check_ct(const Context& c, const Ct& a, const char* what);
 void check_scales(const Ct& a, const Ct& b, const char* what);
 

@@ -521,7 +521,8 @@ Ct add_plain(Context& c, const Ct& a, const double* slots) {
   return r;
 }
 
-Ct mac_plain(Context& c, const std::vector<const Ct*>& cts, const std::vector<const Pt*>& pts, bool count) {
+Ct mac_plain(Context& c, const std::vector<const Ct*>& cts, const std::vector<const Pt*>& pts, bool count,
+              bool rescale_out) {
   SF_HPROF("mac_plain");
   require(!cts.empty() && cts.size() == pts.size(), kShapeMismatch, "mac_plain: term count");
   int limbs = 1 << 30;
@@ -546,7 +547,7 @@ Ct mac_plain(Context& c, const std::vector<const Ct*>& cts, const std::vector<co
   for (const Ct* x : cts)
     if (!(x->layout == ly)) ly.reset();
   if (scale == 0.0) {  // every term trivially zero
-    Ct z = zeros(c, limbs - 2);
+    Ct z = zeros(c, rescale_out ? limbs - 2 : limbs - 1);
     z.layout = ly;
     return z;
   }
@@ -571,6 +572,10 @@ Ct mac_plain(Context& c, const std::vector<const Ct*>& cts, const std::vector<co
       acc = add(c, acc, part, false, false);
     }
   }
+  if (!rescale_out) {  // the raw sum at scale * q_top (the caller's rotation sum rescales)
+    acc.layout = ly;
+    return acc;
+  }
   Ct r = rescale(c, acc);
   r.scale = scale;
   r.layout = ly;
@@ -591,19 +596,24 @@ Ct mul_plain(Context& c, const Ct& a, const double* slots) {
 static BufPtr build_key(Context& c, u64 g, int ndig = 1 << 30) {
   const int np = c.np;
   const size_t n = c.n;
-  const int dig = g == kRelinWide ? c.L + 1 : c.alpha;  // digit size: one digit over all Q primes for the wide key
+  const u64 gal = g & kKeyGalMask;
+  const int kd = (int)(g >> 40);  // digit size encoded in the key id (0: alpha)
+  // digit size: one digit over all Q primes for the wide relinearisation key
+  const int dig = g == kRelinWide ? c.L + 1 : (kd ? kd : c.alpha);
   ndig = std::min(ndig, (c.L + 1 + dig - 1) / dig);
   BufPtr key = buf(c, (size_t)ndig * 2 * np * n);
   BufPtr sp = buf(c, (size_t)np * n);
-  if (g == 0 || g == kRelinWide)
+  if (gal == 0 || g == kRelinWide)
     k_square(c, sp->p, c.sk->p, np);
   else
-    k_automorph(c, sp->p, c.sk->p, nullptr, g, np);
+    k_automorph(c, sp->p, c.sk->p, nullptr, gal, np);
   BufPtr e = buf(c, (size_t)np * n);
   std::vector<int> primes(np);
   for (int m = 0; m < np; ++m) primes[m] = m;
   for (int j = 0; j < ndig; ++j) {
-    const u64 tag = (g << 16) | ((u64)j << 8);
+    // independent streams per digit layout (two keys sharing a and e but not their
+    // gadgets would reveal the target)
+    const u64 tag = (gal << 16) | ((u64)j << 8) | ((u64)kd << 44);
     k_small_rns(c, e->p, stream_key(c.seed, kStreamKeyE | tag), true, nullptr, primes.data(), np);
     ntt_limbs(c, e->p, np, 0, false);
     u64* b = key->p + ((size_t)j * 2 + 0) * np * n;
@@ -654,7 +664,11 @@ const BufPtr& get_key_mont(Context& c, u64 g, bool pinv, int ndig) {
   auto& digs = pinv ? c.keys_pinv_dig : c.keys_r_dig;
   // at least two digits: the attention keys serve levels 1 and 2 (one and two
   // digits at alpha = 2); a one-digit key upgraded mid-stream cost a rebuild
-  ndig = g == kRelinWide ? 1 : std::max(std::min(2, c.beta), std::min(ndig, c.beta));
+  {
+    const int kd = (int)(g >> 40);
+    const int dmax = g == kRelinWide ? 1 : (c.L + 1 + (kd ? kd : c.alpha) - 1) / (kd ? kd : c.alpha);
+    ndig = g == kRelinWide ? 1 : std::max(std::min(2, dmax), std::min(ndig, dmax));
+  }
   {
     std::lock_guard<std::mutex> lk(c.mu);
     auto it = cache.find(g);

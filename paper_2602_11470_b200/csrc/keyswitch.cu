@@ -16,6 +16,22 @@
 
 namespace sf {
 
+int scaled_digit(const Context& c, int limbs) {
+  double lp = 0.0;
+  for (int k = 0; k < c.alpha; ++k) lp += std::log2((double)c.primes[c.P_index(k)]);
+  int best = c.alpha;
+  for (int d = c.alpha + 1; d <= std::min(8, limbs); ++d) {
+    bool ok = true;
+    for (int lo = 0; lo < limbs && ok; lo += d) {
+      double lq = 0.0;
+      for (int l = lo; l < std::min(limbs, lo + d); ++l) lq += std::log2((double)c.primes[l]);
+      ok = lq - lp <= 30.0;
+    }
+    if (ok) best = d;
+  }
+  return best;
+}
+
 int relin_digit(const Context& c, int limbs) {
   double lq = 0.0, lp = 0.0;
   for (int l = 0; l < limbs; ++l) lq += std::log2((double)c.primes[l]);
@@ -601,7 +617,7 @@ void mod_down_polys(Context& c, int limbs, const std::vector<MdPoly>& P, bool p_
 // brought back with one ModDown per part; the same function as the CPU
 // oracle's rot_sum, charged as the reference's rotate/add chain.
 std::vector<Ct> rot_sum_batch(Context& c, const std::vector<std::vector<SumTerm>>& groups, bool hoisted, bool count,
-                              const std::vector<const Pt*>* post, bool rescale) {
+                              const std::vector<const Pt*>* post, bool rescale, int dig) {
   SF_HPROF("rot_sum_batch");
   require(!post || (post->size() == groups.size() && fused_path(c)), kInternal, "rot_sum: post multipliers");
   require(!(post && rescale), kInternal, "rot_sum: post multipliers with a merged rescale");
@@ -680,14 +696,14 @@ std::vector<Ct> rot_sum_batch(Context& c, const std::vector<std::vector<SumTerm>
       }
       std::vector<const u64*> d;
       for (const Ct* a : srcv) d.push_back(a->c1(c.n));
-      ExtB x = mod_up_batch(c, d, limbs, true);
+      ExtB x = mod_up_batch(c, d, limbs, true, dig);
       const int nt = x.nt;
       BufPtr acc = make_buf(c, chunk.size() * 2 * nt * n);
       KsSumArgs A;
       A.limbs = limbs;
       A.nt = nt;
       A.ndig = x.ndig;
-      A.alpha = c.alpha;
+      A.alpha = x.dig;  // digit size
       A.np = c.np;
       for (int t = 0; t < nt; ++t) A.tprime[t] = x.tprime[t];
       for (int l = 0; l < limbs; ++l) A.pm[l] = pm[l];
@@ -708,7 +724,8 @@ std::vector<Ct> rot_sum_batch(Context& c, const std::vector<std::vector<SumTerm>
           const int r = pos_mod(tm.r, c.slots);
           A.jsrc[jb] = src[tm.ct];
           A.g[jb] = r == 0 ? 1 : galois_elt(c, r);
-          A.key[jb] = r == 0 ? nullptr : (fused ? get_key_mont(c, A.g[jb], pre, x.ndig) : get_key(c, A.g[jb]))->p;
+          const u64 kid = key_id(A.g[jb], x.dig, c.alpha);
+          A.key[jb] = r == 0 ? nullptr : (fused ? get_key_mont(c, kid, pre, x.ndig) : get_key(c, kid))->p;
           ++jb;
         }
         const Ct& y = out[chunk[o]];

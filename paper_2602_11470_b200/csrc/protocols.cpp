@@ -217,21 +217,21 @@ Ct vmm_partial(Context& c, const Ct& x, VmmPlan& plan, int rank, int world) {
       A.out1[i] = partial[i].c1(c.n);
     }
     b_vmm_mac(c, A, limbs);
-    std::vector<const Ct*> pp;
-    for (auto& p : partial) pp.push_back(&p);
-    resc = rescale_batch(c, pp);
-    for (auto& r : resc) r.scale = stair.scale, r.layout.reset();
+    resc = std::move(partial);  // unrescaled (scale * q_top): the group sums rescale
+    for (auto& r : resc) r.layout.reset();
   } else {
     for (int g2 : mine) {
       std::vector<const Ct*> cts;
       std::vector<const Pt*> pts;
       for (int g1 = 0; g1 < b && (long long)g2 * b + g1 < s.k; ++g1)
         cts.push_back(&baby[g1]), pts.push_back(&diag[(long long)g2 * b + g1]);
-      resc.push_back(mac_plain(c, cts, pts));
+      resc.push_back(mac_plain(c, cts, pts, true, false));
     }
   }
   // giant alignment + sum (vmm.cpp:221-222): one rotation sum per giant group
-  // (ModDown once per group instead of once per giant)
+  // (ModDown once per group instead of once per giant), on the
+  // unrescaled partials with the rescale merged into the ModDown: at scale >= 2^80
+  // the giant rotations decompose with the wider digits of scaled_digit (§3.6b)
   std::vector<std::vector<SumTerm>> groups;
   std::map<int, int> gpos;
   for (size_t i = 0; i < mine.size(); ++i) {
@@ -239,7 +239,7 @@ Ct vmm_partial(Context& c, const Ct& x, VmmPlan& plan, int rank, int world) {
     if (!gpos.count(r)) gpos[r] = (int)groups.size(), groups.emplace_back();
     groups[gpos[r]].push_back({&resc[i], (int)(((long long)mine[i] * b * unit) % c.slots)});
   }
-  std::vector<Ct> gs = rot_sum_batch(c, groups, false);
+  std::vector<Ct> gs = rot_sum_batch(c, groups, false, true, nullptr, true, scaled_digit(c, limbs));
   std::vector<const Ct*> ap;
   for (auto& a : gs) ap.push_back(&a);
   return sum_cts(c, ap);
@@ -318,14 +318,8 @@ std::vector<Ct> vmm_interleaved_many(Context& c, const std::vector<const Ct*>& x
     }
     b_vmm_mac(c, A, limbs);
   }
-  std::vector<const Ct*> pp;
-  for (auto& p : partial) pp.push_back(&p);
-  std::vector<Ct> resc = rescale_batch(c, pp);
-  for (int i = 0; i < B; ++i)
-    for (int g2 = 0; g2 < giants; ++g2) {
-      Ct& r = resc[(size_t)i * giants + g2];
-      r.scale = stair[i].scale, r.layout.reset();
-    }
+  std::vector<Ct> resc = std::move(partial);  // unrescaled: the group sums rescale (§3.6b)
+  for (auto& r : resc) r.layout.reset();
   // 4. giant alignment + sum: every input's groups in one batch
   std::vector<std::vector<SumTerm>> groups;
   std::vector<int> gowner;
@@ -336,7 +330,7 @@ std::vector<Ct> vmm_interleaved_many(Context& c, const std::vector<const Ct*>& x
       for (int g2 = r; g2 < giants; g2 += kGiantGroups)
         groups.back().push_back({&resc[(size_t)i * giants + g2], (int)(((long long)g2 * b * unit) % c.slots)});
     }
-  std::vector<Ct> gs = rot_sum_batch(c, groups, false);
+  std::vector<Ct> gs = rot_sum_batch(c, groups, false, true, nullptr, true, scaled_digit(c, limbs));
   std::vector<Ct> acc;
   for (int i = 0; i < B; ++i) {
     std::vector<const Ct*> ap;
@@ -430,10 +424,8 @@ std::vector<Ct> vmm_multi_partial(Context& c, const Ct& x, const std::vector<Vmm
     }
     b_vmm_mac(c, A, limbs);
   }
-  std::vector<const Ct*> pp;
-  for (auto& p : partial) pp.push_back(&p);
-  std::vector<Ct> resc = rescale_batch(c, pp);
-  for (auto& r : resc) r.scale = stair.scale, r.layout.reset();
+  std::vector<Ct> resc = std::move(partial);  // unrescaled: the group sums rescale (§3.6b)
+  for (auto& r : resc) r.layout.reset();
   // 4. giant alignment + sum: the owned groups of every call in one batch
   std::vector<std::vector<SumTerm>> groups;
   std::vector<int> gowner;
@@ -446,7 +438,7 @@ std::vector<Ct> vmm_multi_partial(Context& c, const Ct& x, const std::vector<Vmm
         if (mine[i] % kGiantGroups == r)
           groups.back().push_back({&resc[(size_t)pi * G + i], (int)(((long long)mine[i] * b * unit) % c.slots)});
     }
-  std::vector<Ct> gs = rot_sum_batch(c, groups, false);
+  std::vector<Ct> gs = rot_sum_batch(c, groups, false, true, nullptr, true, scaled_digit(c, limbs));
   for (int pi = 0; pi < P; ++pi) {
     std::vector<const Ct*> ap;
     for (size_t i = 0; i < gs.size(); ++i)
