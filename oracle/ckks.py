@@ -72,6 +72,7 @@ def lib():
             "ock_rot_sum": (vp, [vp, C.POINTER(vp), C.POINTER(C.c_int), C.c_int]),
             "ock_rot_sum_rescale": (vp, [vp, C.POINTER(vp), C.POINTER(C.c_int), C.c_int]),
             "ock_rot_sum_rescale_scaled": (vp, [vp, C.POINTER(vp), C.POINTER(C.c_int), C.c_int]),
+            "ock_rot_sum_scaled": (vp, [vp, C.POINTER(vp), C.POINTER(C.c_int), C.c_int]),
             "ock_mac_plain_lazy": (vp, [vp, C.POINTER(vp), DP, C.c_int]),
             "ock_relin_rescale": (vp, [vp, vp]),
             "ock_relin": (vp, [vp, vp]),
@@ -426,7 +427,7 @@ class CkksOracle:
         self.ledger.count_rotation(hoisted)
         return OCt(self, lib().ock_rotate(self.ptr, a.ptr, int(r)), a.level, None)
 
-    def rot_sum(self, terms, hoisted: bool = False):
+    def rot_sum(self, terms, hoisted: bool = False, scaled: bool = False):
         """sum_i Rot(a_i, r_i) (one ModDown for the whole sum),
         charged as the reference's rotate/add chain: one rotation per r_i != 0
         (mod N) and len(terms) - 1 additions; layouts merge as that chain's."""
@@ -443,7 +444,8 @@ class CkksOracle:
         arr = (C.c_void_p * len(terms))(*[a.ptr for a, _ in terms])
         rr = (C.c_int * len(terms))(*[int(r) for _, r in terms])
         lvl = min(a.level for a, _ in terms)
-        return OCt(self, lib().ock_rot_sum(self.ptr, arr, rr, len(terms)), lvl, ly)
+        fn = lib().ock_rot_sum_scaled if scaled else lib().ock_rot_sum  # scaled: terms at scale >= 2^80
+        return OCt(self, fn(self.ptr, arr, rr, len(terms)), lvl, ly)
 
     def fold_steps(self, c, rots, shift: int = 0):
         """The doubling chain c <- c + Rot(c, r_i), i = 0..m-1 (fold_within_head,

@@ -1174,6 +1174,15 @@ void* ock_rot_sum(void* c, void** a, const int* rots, int k) {
 void* ock_rot_sum_rescale(void* c, void** a, const int* rots, int k) {
   return guard([&]() -> void* { return rot_sum(*static_cast<Ctx*>(c), (Ct* const*)a, rots, k, true); });
 }
+// rot_sum of ciphertexts at scale >= 2^80 (the Score*V giants): scaled_digit digits
+void* ock_rot_sum_scaled(void* c, void** a, const int* rots, int k) {
+  return guard([&]() -> void* {
+    Ctx& cx = *static_cast<Ctx*>(c);
+    int limbs = 1 << 30;
+    for (int i = 0; i < k; ++i) limbs = std::min(limbs, static_cast<Ct*>(a[i])->limbs);
+    return rot_sum(cx, (Ct* const*)a, rots, k, false, scaled_digit(cx, limbs));
+  });
+}
 // rot_sum_rescale of products still at scale >= 2^80 (the HE-VMM giants): the
 // terms' decomposition uses scaled_digit(limbs)
 void* ock_rot_sum_rescale_scaled(void* c, void** a, const int* rots, int k) {

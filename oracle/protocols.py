@@ -225,7 +225,7 @@ def fused_extract(be, x, succ: str, rope: Optional[dict] = None, coeff=None):
             # rescale merged into its ModDown (mirrors csrc/protocols.cpp rope_apply;
             # same charge: 3 ct-pt mults, 2 rotations, 2 additions)
             u = [be.with_layout(be.mul_plain_lazy(x, p), None) for p in (p0, p1, p2)]
-            y = be.rot_sum_rescale([(u[0], 0), (u[1], -s), (u[2], s)])
+            y = be.rot_sum_rescale([(u[0], 0), (u[1], -s), (u[2], s)], scaled=True)
             return be.with_layout(y, ly.with_(deferred_mask=False))
         y = be.mul_plain(x, p0)
         y = be.add(y, be.rotate(be.mul_plain(x, p1), -s))
@@ -682,7 +682,7 @@ def sv_partial(be, probs, cache: KVCache, cfg, rank, world):
         for r in range(SV_GROUPS):
             terms = [(rel[G], -G * B * t) for G in sorted(rel) if G % SV_GROUPS == r]
             if terms:
-                s = be.rot_sum(terms)
+                s = be.rot_sum(terms, scaled=True)  # the relinearised sums are at scale >= 2^80
                 acc = s if acc is None else be.add(acc, s)
     finally:
         be.ledger = led

@@ -637,7 +637,8 @@ Ct rope_apply(Context& c, const Ct& x, const AttnCfg& cfg, long long position, d
   if (!x.zero) {
     std::vector<Ct> u = mul_plain_batch(c, {&x, &x, &x}, {&pts[0], &pts[1], &pts[2]}, false, false);
     for (auto& v : u) v.layout.reset();
-    y = rot_sum_batch(c, {{{&u[0], 0}, {&u[1], -s}, {&u[2], s}}}, false, false, nullptr, true)[0];
+    y = rot_sum_batch(c, {{{&u[0], 0}, {&u[1], -s}, {&u[2], s}}}, false, false, nullptr, true,
+                      scaled_digit(c, x.limbs))[0];  // products at scale >= 2^80: wider digits (§3.6b)
   } else {
     y = zeros(c, x.level() - 1);
   }
@@ -1142,7 +1143,8 @@ Ct softmax_times_v_partial(Context& c, const std::vector<Ct>& probs, const KV& c
     grp[(int)pos_mod(giants[i], kSvGroups)].push_back({&rel[i], -giants[i] * B * t});
   std::vector<std::vector<SumTerm>> groups;
   for (auto& [r, terms] : grp) groups.push_back(terms);
-  std::vector<Ct> gs = rot_sum_batch(c, groups, false, false);
+  // at the products' scale (>= 2^80): the wider digits of scaled_digit
+  std::vector<Ct> gs = rot_sum_batch(c, groups, false, false, nullptr, false, scaled_digit(c, limbs));
   std::vector<const Ct*> gp;
   for (auto& x : gs) gp.push_back(&x);
   Ct acc = sum_cts(c, gp, false);
