@@ -73,6 +73,7 @@ def lib():
             "ock_rot_sum_rescale": (vp, [vp, C.POINTER(vp), C.POINTER(C.c_int), C.c_int]),
             "ock_rot_sum_rescale_scaled": (vp, [vp, C.POINTER(vp), C.POINTER(C.c_int), C.c_int]),
             "ock_rot_sum_scaled": (vp, [vp, C.POINTER(vp), C.POINTER(C.c_int), C.c_int]),
+            "ock_fold2": (vp, [vp, vp, C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_int), C.c_int]),
             "ock_mac_plain_lazy": (vp, [vp, C.POINTER(vp), DP, C.c_int]),
             "ock_relin_rescale": (vp, [vp, vp]),
             "ock_relin": (vp, [vp, vp]),
@@ -202,6 +203,7 @@ class CkksOracle:
     qk_shift_fold = True  # the QK^T pack rotation rides the fold
     rope_fused = True  # RoPE as one rotation sum with a merged rescale
     vmm_scaled_giants = True  # HE-VMM giants rotated before their rescale, wider digits
+    fold_dh = True  # two-step folds double-hoisted: the first sum's b part stays extended
 
     def __init__(self, N: int, L: int, **kw):
         if not is_pow2(N):
@@ -474,6 +476,17 @@ class CkksOracle:
         try:
             lo = 0
             radix = fold_radix(1 << m)
+            if self.fold_dh and len(radix) == 2:
+                steps = []
+                for si, bits in enumerate(radix):
+                    rs = rots[lo:lo + bits]
+                    s0 = shift if si == 1 else 0
+                    steps.append([s0 + sum(rs[i] for i in range(bits) if (k >> i) & 1) for k in range(1 << bits)])
+                    lo += bits
+                a1 = (C.c_int * len(steps[0]))(*[int(r) for r in steps[0]])
+                a2 = (C.c_int * len(steps[1]))(*[int(r) for r in steps[1]])
+                out = OCt(self, lib().ock_fold2(self.ptr, c.ptr, a1, len(steps[0]), a2, len(steps[1])), c.level, None)
+                return OCt._alias(out, ly)
             for si, bits in enumerate(radix):
                 rs = rots[lo:lo + bits]
                 s0 = shift if si + 1 == len(radix) else 0

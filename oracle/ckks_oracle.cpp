@@ -792,7 +792,13 @@ void key_switch(Ctx& c, const u64* d, int limbs, u64 g, u64* kb, u64* ka) {
 // rounding of one instead of k terms.
 // rescale: the sum is also rescaled by its top prime, in the ModDown's basis
 // conversion (mod_down_rescale; the QK^T pack).
-Ct* rot_sum(Ctx& c, const Ct* const* a, const int* rots, int k, bool rescale = false, int dig = 0) {
+// Double hoisting (the two radix sums of fold_steps on the fused ring sizes,
+// keyswitch.cu fold_steps_batch): keep_b receives the sum's b part in the
+// extended basis (NTT domain, not ModDown'd; the returned b part is zero) and
+// ext_b supplies it back as the c0 of every term of the next sum, sigma_g
+// applied on all limbs with no P factor (it already carries it).
+Ct* rot_sum(Ctx& c, const Ct* const* a, const int* rots, int k, bool rescale = false, int dig = 0,
+            std::vector<u64>* keep_b = nullptr, const std::vector<u64>* ext_b = nullptr) {
   int limbs = 1 << 30;
   double scale = 0.0;
   bool any = false;
@@ -814,6 +820,27 @@ Ct* rot_sum(Ctx& c, const Ct* const* a, const int* rots, int k, bool rescale = f
     const int r = (int)(((long long)rots[i] % c.slots + c.slots) % c.slots);
     const u64 g = r == 0 ? 1 : galois_elt(c, r);
     if (r != 0) key_switch_ext(c, poly(c, a[i], 1, 0), limbs, g, accb, acca, dig);
+    if (ext_b) {
+#pragma omp parallel for
+      for (int l = 0; l < (int)nt; ++l) {
+        const u64 q = c.primes[l < limbs ? l : (int)c.P_index(l - limbs)];
+        std::vector<u64> s0(n);
+        const u64* e = ext_b->data() + (size_t)l * n;
+        if (r != 0)
+          automorph(c, e, s0.data(), g);
+        else
+          std::memcpy(s0.data(), e, sizeof(u64) * n);
+        u64* ob = accb.data() + (size_t)l * n;
+        for (int j = 0; j < n; ++j) ob[j] = addmod(ob[j], s0[j], q);
+        if (r == 0 && l < limbs) {
+          const u64 pm = P_mod(c, q);
+          const u64* s1 = poly(c, a[i], 1, l);
+          u64* oa = acca.data() + (size_t)l * n;
+          for (int j = 0; j < n; ++j) oa[j] = addmod(oa[j], mulmod(s1[j], pm, q), q);
+        }
+      }
+      continue;
+    }
 #pragma omp parallel for
     for (int l = 0; l < limbs; ++l) {
       const u64 q = c.primes[l];
@@ -839,8 +866,26 @@ Ct* rot_sum(Ctx& c, const Ct* const* a, const int* rots, int k, bool rescale = f
     return out;
   }
   Ct* out = new_ct(c, limbs, scale);
-  mod_down(c, accb, limbs, poly(c, out, 0, 0));
+  if (keep_b)
+    *keep_b = accb;
+  else
+    mod_down(c, accb, limbs, poly(c, out, 0, 0));
   mod_down(c, acca, limbs, poly(c, out, 1, 0));
+  return out;
+}
+
+// fold_steps' two radix sums with double hoisting (keyswitch.cu
+// fold_steps_batch): the first sum's b part never leaves the extended basis.
+// Ring sizes without the fused row kernels (logn < 12 or > 17, alpha > 7) and
+// zero inputs take the plain two sums, as on the GPU.
+Ct* fold2(Ctx& c, const Ct* a, const int* r1, int k1, const int* r2, int k2) {
+  const bool dh = c.logn >= 12 && c.logn <= 17 && c.alpha <= 7 && !a->zero;
+  std::vector<const Ct*> t1(k1, a);
+  std::vector<u64> kb;
+  Ct* mid = rot_sum(c, t1.data(), r1, k1, false, 0, dh ? &kb : nullptr);
+  std::vector<const Ct*> t2(k2, mid);
+  Ct* out = rot_sum(c, t2.data(), r2, k2, false, 0, nullptr, dh ? &kb : nullptr);
+  delete mid;
   return out;
 }
 
@@ -1170,6 +1215,9 @@ void* ock_rotate(void* c, void* a, int r) {
 }
 void* ock_rot_sum(void* c, void** a, const int* rots, int k) {
   return guard([&]() -> void* { return rot_sum(*static_cast<Ctx*>(c), (Ct* const*)a, rots, k); });
+}
+void* ock_fold2(void* c, void* a, const int* r1, int k1, const int* r2, int k2) {
+  return guard([&]() -> void* { return fold2(*static_cast<Ctx*>(c), (const Ct*)a, r1, k1, r2, k2); });
 }
 void* ock_rot_sum_rescale(void* c, void** a, const int* rots, int k) {
   return guard([&]() -> void* { return rot_sum(*static_cast<Ctx*>(c), (Ct* const*)a, rots, k, true); });

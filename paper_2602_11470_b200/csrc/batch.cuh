@@ -1,6 +1,8 @@
 // Job descriptors for the batched kernels (batch.cu). Each struct is passed by
 // value as the kernel parameter block (<= 32 KB, CUDA 12.1+).
 #pragma once
+#include <map>
+
 #include "context.h"
 
 namespace sf {
@@ -207,6 +209,12 @@ struct KsSumArgs {
   // targets t >= inv_from (and all special primes) are written inverse-row-passed:
   // inv_from = limbs - 1 feeds the merged ModDown + rescale (M = {q_top} u P)
   int inv_from = 1 << 30;
+  // double hoisting (fold_steps_batch; PM1 only):
+  // keep_b: the b part stays extended and NTT-domain on every target (the next
+  //   radix sum's c0 input), only the a part is inverse-row-passed for its ModDown
+  // ext_c0: c0[s] is such an extended b part ([nt][n]); sigma_g(c0) (identity: c0)
+  //   enters on every target, c1 on the Q targets only
+  bool keep_b = false, ext_c0 = false;
   int out_begin[kSumOuts + 1];
   u64* acc[kSumOuts];  // [2][nt][n]
   int jsrc[kSumJobs];
@@ -275,9 +283,18 @@ struct SumTerm {
 // its ModDown (merged): one conversion from {q_top} u P
 // dig: digit size of the terms' decomposition (0: alpha; scaled_digit(limbs) for
 // sums of products still at scale >= 2^80, with the rescale merged)
+// Double hoisting (fused path, PM1 sums, no rescale): keep_b (one entry per
+// group) receives each sum's b part extended and NTT-domain ([nt][n], the
+// buffer kept alive) and the returned Ct holds only the a part (c0 undefined);
+// ext_b feeds such kept b parts back as the c0 of their source ciphertexts.
+struct ExtPoly {
+  BufPtr buf;
+  const u64* p = nullptr;
+};
 std::vector<Ct> rot_sum_batch(Context& c, const std::vector<std::vector<SumTerm>>& groups, bool hoisted,
                               bool count = true, const std::vector<const Pt*>* post = nullptr, bool rescale = false,
-                              int dig = 0);
+                              int dig = 0, std::vector<ExtPoly>* keep_b = nullptr,
+                              const std::map<const Ct*, const u64*>* ext_b = nullptr);
 // doubling chains x <- x + Rot(x, r) over rots[i] (radix rotation sums); charged
 // as the reference's rotate + add steps when count && lead
 // post (fused path only): per chain an NTT-domain plaintext multiplied into the

@@ -617,8 +617,11 @@ void mod_down_polys(Context& c, int limbs, const std::vector<MdPoly>& P, bool p_
 // brought back with one ModDown per part; the same function as the CPU
 // oracle's rot_sum, charged as the reference's rotate/add chain.
 std::vector<Ct> rot_sum_batch(Context& c, const std::vector<std::vector<SumTerm>>& groups, bool hoisted, bool count,
-                              const std::vector<const Pt*>* post, bool rescale, int dig) {
+                              const std::vector<const Pt*>* post, bool rescale, int dig, std::vector<ExtPoly>* keep_b,
+                              const std::map<const Ct*, const u64*>* ext_b) {
   SF_HPROF("rot_sum_batch");
+  require(!(keep_b || ext_b) || (fused_path(c) && !rescale && dig == 0), kInternal, "rot_sum: double hoisting");
+  if (keep_b) keep_b->assign(groups.size(), ExtPoly());
   require(!post || (post->size() == groups.size() && fused_path(c)), kInternal, "rot_sum: post multipliers");
   require(!(post && rescale), kInternal, "rot_sum: post multipliers with a merged rescale");
   std::vector<Ct> out(groups.size());
@@ -709,8 +712,16 @@ std::vector<Ct> rot_sum_batch(Context& c, const std::vector<std::vector<SumTerm>
       for (int l = 0; l < limbs; ++l) A.pm[l] = pm[l];
       A.pm_one = pre;
       if (rescale) A.inv_from = limbs - 1;
+      A.keep_b = keep_b != nullptr;
+      A.ext_c0 = ext_b != nullptr;
       for (size_t s = 0; s < srcv.size(); ++s) {
-        A.c0[s] = srcv[s]->c0();
+        if (ext_b) {
+          auto e = ext_b->find(srcv[s]);
+          require(e != ext_b->end(), kInternal, "rot_sum: source without its extended b part");
+          A.c0[s] = e->second;
+        } else {
+          A.c0[s] = srcv[s]->c0();
+        }
         A.c1[s] = srcv[s]->c1(c.n);
         A.ext[s] = x.ext((int)s);
       }
@@ -730,7 +741,10 @@ std::vector<Ct> rot_sum_batch(Context& c, const std::vector<std::vector<SumTerm>
         }
         const Ct& y = out[chunk[o]];
         const u64* pp = post ? (*post)[chunk[o]]->buf->p : nullptr;
-        md.push_back({A.acc[o], nullptr, 0, y.c0(), pp});
+        if (keep_b)
+          (*keep_b)[chunk[o]] = ExtPoly{acc, A.acc[o]};
+        else
+          md.push_back({A.acc[o], nullptr, 0, y.c0(), pp});
         md.push_back({A.acc[o] + (size_t)nt * n, nullptr, 0, y.c1(c.n), pp});
       }
       A.out_begin[chunk.size()] = jb;
@@ -779,6 +793,13 @@ std::vector<Ct> fold_steps_batch(Context& c, const std::vector<const Ct*>& xs, c
       steps.push_back(m);
     else
       steps.push_back((m + 1) / 2), steps.push_back(m / 2);
+    // double hoisting: the first radix sum's b part stays in the
+    // extended basis and enters the second sum as its c0 terms -- one ModDown
+    // (the first sum's b part) fewer; SF_VARIANT bit 8 turns it off (A/B only:
+    // the CPU twin always hoists on this path)
+    const bool dh = steps.size() == 2 && fused_path(c) && !(c.variant & 256);
+    std::vector<ExtPoly> kept;
+    std::map<const Ct*, const u64*> ext;
     int lo = 0;
     for (size_t si = 0; si < steps.size(); ++si) {
       const int bits = steps[si];
@@ -796,8 +817,14 @@ std::vector<Ct> fold_steps_batch(Context& c, const std::vector<const Ct*>& xs, c
       std::vector<const Pt*> pg;  // the post multipliers ride the last step's ModDown epilogue
       if (post && last)
         for (int g : idx) pg.push_back((*post)[g]), posted[g] = true;
-      std::vector<Ct> nxt = rot_sum_batch(c, groups, false, false, (post && last) ? &pg : nullptr);
+      std::vector<Ct> nxt = rot_sum_batch(c, groups, false, false, (post && last) ? &pg : nullptr, false, 0,
+                                          (dh && si == 0) ? &kept : nullptr, (dh && si == 1) ? &ext : nullptr);
       for (size_t g = 0; g < idx.size(); ++g) cur[idx[g]] = std::move(nxt[g]);
+      if (dh && si == 0) {
+        ext.clear();
+        for (size_t g = 0; g < idx.size(); ++g)
+          if (kept[g].p) ext[&cur[idx[g]]] = kept[g].p;
+      }
       lo += bits;
     }
   }

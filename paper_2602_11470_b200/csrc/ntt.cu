@@ -703,6 +703,7 @@ __global__ void __launch_bounds__(kWarps * 32, LOGC >= 9 ? 1 : 2) ks_sum_kernel(
   const int m = A.tprime[t];
   const u64 q = T.q[m], mh = T.mh[m], qn = T.qn[m];
   const bool qt = t < A.limbs;
+  const bool c0t = qt || A.ext_c0;  // targets receiving the c0 (b part) terms
   const u64 pm = qt ? A.pm[t] : 0;
   u64* buf = rowbuf[warp];
   // register layout of a row: pair-strided on the shuffle path at C = 256
@@ -734,14 +735,14 @@ __global__ void __launch_bounds__(kWarps * 32, LOGC >= 9 ? 1 : 2) ks_sum_kernel(
     const int s = A.jsrc[jb];
     const u64 g = A.g[jb];
     if (terms >= 14) fold();
-    if (g <= 1) {  // identity term: P * (c0, c1) on the Q primes
-      if (!qt) continue;
+    if (g <= 1) {  // identity term: P * (c0, c1) on the Q primes (ext_c0: c0 on every target)
+      if (!c0t) continue;
       const u64* a0 = A.c0[s] + (size_t)t * n + rowoff;
       const u64* a1 = A.c1[s] + (size_t)t * n + rowoff;
 #pragma unroll
       for (int k = 0; k < E; k += 2) {
         const ulonglong2 v0 = *reinterpret_cast<const ulonglong2*>(a0 + eoff(k));
-        const ulonglong2 v1 = *reinterpret_cast<const ulonglong2*>(a1 + eoff(k));
+        const ulonglong2 v1 = qt ? *reinterpret_cast<const ulonglong2*>(a1 + eoff(k)) : make_ulonglong2(0, 0);
         if constexpr (PM1) {
           sb[k].hi += v0.x;
           sb[k + 1].hi += v0.y;
@@ -787,7 +788,7 @@ __global__ void __launch_bounds__(kWarps * 32, LOGC >= 9 ? 1 : 2) ks_sum_kernel(
           mac128(sa[k + 1], x[k + 1], kv[k + 1].y);
         }
       }
-      if (qt) {  // P * sigma_g(c0)
+      if (c0t) {  // P * sigma_g(c0)
         const u64* src = A.c0[s] + (size_t)t * n + (size_t)rs * C;
         u64 x[8];
 #pragma unroll
@@ -850,7 +851,7 @@ __global__ void __launch_bounds__(kWarps * 32, LOGC >= 9 ? 1 : 2) ks_sum_kernel(
       }
       __syncwarp();
     }
-    if (qt) {  // P * sigma_g(c0)
+    if (c0t) {  // P * sigma_g(c0)
       const u64* src = A.c0[s] + (size_t)t * n + (size_t)rs * C;
 #pragma unroll
       for (int k = 0; k < E; k += 2) {
@@ -878,13 +879,19 @@ __global__ void __launch_bounds__(kWarps * 32, LOGC >= 9 ? 1 : 2) ks_sum_kernel(
   }
   u64* accb = A.acc[o] + (size_t)t * n;
   u64* acca = A.acc[o] + (size_t)(A.nt + t) * n;
-  if (qt && t < A.inv_from) {
+  // NTT-domain stores on the Q targets; the special primes (and a merged q_top)
+  // get ModDown's inverse row pass and strided stores -- except a kept b part
+  const bool ntt_a = qt && t < A.inv_from, ntt_b = ntt_a || A.keep_b;
+  if (ntt_b) {
 #pragma unroll
-    for (int k = 0; k < E; k += 2) {
+    for (int k = 0; k < E; k += 2)
       *reinterpret_cast<ulonglong2*>(accb + rowoff + eoff(k)) = make_ulonglong2(vb[k], vb[k + 1]);
+  }
+  if (ntt_a) {
+#pragma unroll
+    for (int k = 0; k < E; k += 2)
       *reinterpret_cast<ulonglong2*>(acca + rowoff + eoff(k)) = make_ulonglong2(va[k], va[k + 1]);
-    }
-  } else {  // special prime (or merged q_top): ModDown's inverse row pass, strided stores
+  } else {
     const u64* W = T.ipsi + ((size_t)m << LOGN);
     const u64* Ws = T.ipsi_s + ((size_t)m << LOGN);
     auto tw = [&](int b, int blk, u64& w, u64& ws) {
@@ -901,19 +908,22 @@ __global__ void __launch_bounds__(kWarps * 32, LOGC >= 9 ? 1 : 2) ks_sum_kernel(
         for (int k = 0; k < E; ++k) v[k] = buf[xp(lane + 32 * k)];
         __syncwarp();
       };
-      restride(vb);
-      warp_inv<LOGC, kStrided>(vb, buf, lane, q, tw);
+      if (!ntt_b) {
+        restride(vb);
+        warp_inv<LOGC, kStrided>(vb, buf, lane, q, tw);
+      }
       restride(va);
       warp_inv<LOGC, kStrided>(va, buf, lane, q, tw);
     } else {
-      warp_inv<LOGC, kBlocked>(vb, buf, lane, q, tw);
+      if (!ntt_b) warp_inv<LOGC, kBlocked>(vb, buf, lane, q, tw);
       warp_inv<LOGC, kBlocked>(va, buf, lane, q, tw);
     }
+    if (!ntt_b) {
 #pragma unroll
-    for (int k = 0; k < E; ++k) {
-      accb[(size_t)rd * C + lane + 32 * k] = vb[k];
-      acca[(size_t)rd * C + lane + 32 * k] = va[k];
+      for (int k = 0; k < E; ++k) accb[(size_t)rd * C + lane + 32 * k] = vb[k];
     }
+#pragma unroll
+    for (int k = 0; k < E; ++k) acca[(size_t)rd * C + lane + 32 * k] = va[k];
   }
 }
 
@@ -968,6 +978,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) ks_sum_tma_kernel(KsSumArgs
   const int m = A.tprime[t];
   const u64 q = T.q[m], mh = T.mh[m], qn = T.qn[m];
   const bool qt = t < A.limbs;
+  const bool c0t = qt || A.ext_c0;  // targets receiving the c0 (b part) terms
   const u64 pm = qt ? A.pm[t] : 0;
   u64* stage_base = tma_sm + (size_t)warp * 2 * kTmaRows * C;
   u64* buf = tma_sm + (size_t)kTmaWarps * 2 * kTmaRows * C + (size_t)warp * C;
@@ -990,12 +1001,12 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) ks_sum_tma_kernel(KsSumArgs
     const int rs = (int)RowPerm<LOGR, LOGC>(rd, A.g[jb]).src_row;
     u64* dst = stage_base + (size_t)st * kTmaRows * C;
     tma1d::fence_proxy_async();  // the warp's earlier shared-memory reads of this stage come first
-    tma1d::mbar_expect_tx(&bars[st], (qt ? 4 : 3) * row_bytes);
+    tma1d::mbar_expect_tx(&bars[st], (c0t ? 4 : 3) * row_bytes);
     const u64* src = (t < A.alpha && t < A.limbs) ? A.c1[s] + (size_t)t * n : A.ext[s] + (size_t)t * n;
     tma1d::bulk_g2s(dst, src + (size_t)rs * C, row_bytes, &bars[st]);
     tma1d::bulk_g2s(dst + C, A.key[jb] + (size_t)m * n + rowoff, row_bytes, &bars[st]);
     tma1d::bulk_g2s(dst + 2 * C, A.key[jb] + ((size_t)A.np + m) * n + rowoff, row_bytes, &bars[st]);
-    if (qt) tma1d::bulk_g2s(dst + 3 * C, A.c0[s] + (size_t)t * n + (size_t)rs * C, row_bytes, &bars[st]);
+    if (c0t) tma1d::bulk_g2s(dst + 3 * C, A.c0[s] + (size_t)t * n + (size_t)rs * C, row_bytes, &bars[st]);
   };
   auto next_rot = [&](int jb) {  // first non-identity job at or after jb
     while (jb < b1 && A.g[jb] <= 1) ++jb;
@@ -1020,12 +1031,13 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) ks_sum_tma_kernel(KsSumArgs
     const int s = A.jsrc[jb];
     const u64 g = A.g[jb];
     if (terms >= 14) fold();
-    if (g <= 1) {  // identity term: P * (c0, c1) on the Q primes, straight from global memory
-      if (!qt) continue;
+    if (g <= 1) {  // identity term: P * (c0, c1) on the Q primes (ext_c0: c0 on every target), from global memory
+      if (!c0t) continue;
 #pragma unroll
       for (int k = 0; k < E; k += 2) {
         const ulonglong2 v0 = *reinterpret_cast<const ulonglong2*>(A.c0[s] + (size_t)t * n + rowoff + eoff(k));
-        const ulonglong2 v1 = *reinterpret_cast<const ulonglong2*>(A.c1[s] + (size_t)t * n + rowoff + eoff(k));
+        const ulonglong2 v1 = qt ? *reinterpret_cast<const ulonglong2*>(A.c1[s] + (size_t)t * n + rowoff + eoff(k))
+                                 : make_ulonglong2(0, 0);
         if constexpr (PM1) {
           sb[k].hi += v0.x;
           sb[k + 1].hi += v0.y;
@@ -1065,7 +1077,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) ks_sum_tma_kernel(KsSumArgs
       mac128(sb[k + 1], x[k + 1], kb.y);
       mac128(sa[k + 1], x[k + 1], ka.y);
     }
-    if (qt) {  // P * sigma_g(c0)
+    if (c0t) {  // P * sigma_g(c0)
 #pragma unroll
       for (int k = 0; k < E; k += 2) {
         const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(X + 3 * C + eoff(k));
@@ -1092,13 +1104,19 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) ks_sum_tma_kernel(KsSumArgs
   }
   u64* accb = A.acc[o] + (size_t)t * n;
   u64* acca = A.acc[o] + (size_t)(A.nt + t) * n;
-  if (qt && t < A.inv_from) {
+  // NTT-domain stores on the Q targets; the special primes (and a merged q_top)
+  // get ModDown's inverse row pass and strided stores -- except a kept b part
+  const bool ntt_a = qt && t < A.inv_from, ntt_b = ntt_a || A.keep_b;
+  if (ntt_b) {
 #pragma unroll
-    for (int k = 0; k < E; k += 2) {
+    for (int k = 0; k < E; k += 2)
       *reinterpret_cast<ulonglong2*>(accb + rowoff + eoff(k)) = make_ulonglong2(vb[k], vb[k + 1]);
+  }
+  if (ntt_a) {
+#pragma unroll
+    for (int k = 0; k < E; k += 2)
       *reinterpret_cast<ulonglong2*>(acca + rowoff + eoff(k)) = make_ulonglong2(va[k], va[k + 1]);
-    }
-  } else {  // special prime (or merged q_top): ModDown's inverse row pass, strided stores
+  } else {
     const u64* W = T.ipsi + ((size_t)m << LOGN);
     const u64* Ws = T.ipsi_s + ((size_t)m << LOGN);
     auto tw = [&](int b, int blk, u64& w, u64& ws) {
@@ -1114,15 +1132,16 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) ks_sum_tma_kernel(KsSumArgs
       for (int k = 0; k < E; ++k) v[k] = buf[xp(lane + 32 * k)];
       __syncwarp();
     };
-    restride(vb);
-    warp_inv<LOGC, kStrided>(vb, buf, lane, q, tw);
+    if (!ntt_b) {
+      restride(vb);
+      warp_inv<LOGC, kStrided>(vb, buf, lane, q, tw);
+#pragma unroll
+      for (int k = 0; k < E; ++k) accb[(size_t)rd * C + lane + 32 * k] = vb[k];
+    }
     restride(va);
     warp_inv<LOGC, kStrided>(va, buf, lane, q, tw);
 #pragma unroll
-    for (int k = 0; k < E; ++k) {
-      accb[(size_t)rd * C + lane + 32 * k] = vb[k];
-      acca[(size_t)rd * C + lane + 32 * k] = va[k];
-    }
+    for (int k = 0; k < E; ++k) acca[(size_t)rd * C + lane + 32 * k] = va[k];
   }
 }
 
