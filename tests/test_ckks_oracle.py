@@ -147,6 +147,27 @@ def test_sparse_packing_rotation():
     assert np.max(np.abs(y - np.roll(x, -3))) < TOL
 
 
+def test_double_hoisted_fold_matches_the_doubling_chain():
+    # fold_steps' two radix sums with the first sum's b part kept extended
+    # (fold2): on a fused ring (2^12) it decrypts to the
+    # rotate/add chain; below the fused range it is the plain two-sum path word
+    # for word; the ledger is the chain's either way
+    for log_n, hoisted in ((12, True), (11, False)):
+        n = 1 << (log_n - 1)
+        rots = [1, 2, 4, 8, 16]  # 5 doublings: radix 8 then 4
+        x = np.sin(np.arange(n) * 0.37)
+        want = sum(np.roll(x, -k) for k in range(32))
+        out = {}
+        for dh in (True, False):
+            ck = CkksOracle(n, 3, alpha=2)
+            ck.fold_dh = dh
+            y = ck.fold_steps(ck.encrypt(x), rots)
+            assert np.max(np.abs(ck.decrypt(y) - want)) < 32 * TOL
+            assert ck.ledger.totals().rotations == 5 and ck.ledger.totals().additions == 5
+            out[dh] = y.data()
+        assert np.array_equal(out[True], out[False]) != hoisted
+
+
 @pytest.mark.parametrize("which", ["small"])
 def test_vmm_protocol_decrypts_to_reference(which):
     for c in cases(which, "vmm")[::3]:
