@@ -188,11 +188,20 @@ class LlamaLayer:
         del graph
         return {p: round(t / steps, 3) for p, t in zip(self.PHASES, tot)}
 
-    def step(self, inputs=None, marks=False):
+    def step(self, inputs=None, marks=False, staged=None):
+        """One decode step. staged (e2e): the six inputs' pinned host words; their
+        uploads start at the step's beginning on a side stream (sf_ct_stage) and each
+        joins right before its stage, so the later stages' uploads overlap Q/K/V,
+        RoPE and QK^T (the stage inputs are independent client data)."""
         be, sf = self.be, self.sf
         x, h7, h3, h1, p0, p1 = inputs or self.inputs
+        wait = (lambda *slots: [be.stage_wait(i) for i in slots]) if staged else (lambda *slots: None)
+        if staged:
+            for i, (ct, w) in enumerate(zip((x, h7, h3, h1, p0, p1), staged)):
+                be.stage(ct, w, i)
         mark = (lambda i: be.event_record(10 + i)) if marks else (lambda i: None)
         mark(0)
+        wait(0)
         with be.phase("Q, K, V"):  # three VMMs of one input: shared ladder + babies
             q, k, v = sf.vmm_interleaved_multi(be, x, [self.wq, self.wk, self.wv])
         mark(1)
@@ -205,15 +214,19 @@ class LlamaLayer:
         with be.phase("QK^T"):
             maps = sf.qk_dot(be, qr, cache)
         mark(3)
+        wait(4, 5)
         with be.phase("Score*V"):
             att = sf.softmax_times_v(be, [p0, p1], cache)
         mark(4)
+        wait(1)
         with be.phase("Output projection"):
             o = sf.vmm_interleaved(be, h7, None, plan=self.wo)
         mark(5)
+        wait(2)
         with be.phase("Up & Gate projection"):
             g, u = sf.vmm_interleaved_multi(be, h3, [self.wg, self.wu])
         mark(6)
+        wait(3)
         with be.phase("Down projection"):
             dn = sf.vmm_interleaved(be, h1, None, plan=self.wd)
         mark(7)
@@ -1244,29 +1257,49 @@ def main():
     d2h = 0
     be.synchronize()
     barrier()
-    t_imp = t_iss = t_rd = 0.0
-    t_e = time.perf_counter()
-    for _ in range(args.steps):
-        t1 = time.perf_counter()
-        for slot, (w, *_r) in zip(layer.inputs, pinned_in):  # H2D into the step's input ciphertexts
-            be.refill(slot, w)
-        t2 = time.perf_counter()
-        graph.launch()
-        t3 = time.perf_counter()
-        res = [gouts[4].data(), gouts[8].data()]  # attention output and the layer's down-projection output
-        t4 = time.perf_counter()
-        t_imp, t_iss, t_rd = t_imp + t2 - t1, t_iss + t3 - t2, t_rd + t4 - t3
-        d2h = sum(r.nbytes for r in res)
-    be.synchronize()
-    barrier()
-    e2e_ms = (time.perf_counter() - t_e) * 1e3 / args.steps
-    e2e_parts = {"h2d_enqueue_ms": round(t_imp * 1e3 / args.steps, 3), "graph_launch_ms": round(t_iss * 1e3 / args.steps, 3),
+
+    def e2e_run(g, outs, refill):
+        t_imp = t_iss = t_rd = 0.0
+        t_e = time.perf_counter()
+        for _ in range(args.steps):
+            t1 = time.perf_counter()
+            if refill:
+                for slot, (w, *_r) in zip(layer.inputs, pinned_in):  # H2D into the step's input ciphertexts
+                    be.refill(slot, w)
+            t2 = time.perf_counter()
+            g.launch()
+            t3 = time.perf_counter()
+            res = [outs[4].data(), outs[8].data()]  # attention output and the layer's down-projection output
+            t4 = time.perf_counter()
+            t_imp, t_iss, t_rd = t_imp + t2 - t1, t_iss + t3 - t2, t_rd + t4 - t3
+        be.synchronize()
+        barrier()
+        ms = (time.perf_counter() - t_e) * 1e3 / args.steps
+        parts = {"h2d_enqueue_ms": round(t_imp * 1e3 / args.steps, 3), "graph_launch_ms": round(t_iss * 1e3 / args.steps, 3),
                  "readback_wait_ms": round(t_rd * 1e3 / args.steps, 3), "pinned": pinned}
+        return ms, parts, sum(r.nbytes for r in res)
+
+    # serial: all six uploads, then the step (the round-1 form, kept for comparison)
+    e2e_serial, serial_parts, d2h = e2e_run(graph, gouts, True)
+    graph_kernels = graph.kernel_launches
+    del graph, gouts  # the timed graph's memory is not the stream's to fight over
+    be.synchronize()
+    e2e_ms, e2e_parts = e2e_serial, dict(serial_parts, h2d="serial: six sf_ct_refill copies, then the step")
+    if pinned:
+        # staged: the uploads are part of the captured step (sf_ct_stage on a side stream,
+        # memcpy nodes re-reading the pinned words on every replay); each input joins
+        # right before its stage, so only x's upload precedes the first kernel
+        g_e2e, outs_e2e = be.capture(layer.step, staged=[w for w, *_r in pinned_in])
+        g_e2e.launch()
+        be.synchronize()
+        barrier()
+        e2e_ms, e2e_parts, d2h = e2e_run(g_e2e, outs_e2e, False)
+        e2e_parts["h2d"] = "staged: in-graph uploads overlapping the earlier stages (sf_ct_stage)"
+        e2e_parts["serial_ms"] = round(e2e_serial / world, 3)
+        del g_e2e, outs_e2e
+        be.synchronize()
     if dist:
         e2e_ms = reduce_ranks(dist, e2e_ms, dist.ReduceOp.MAX)
-
-    graph_kernels = graph.kernel_launches
-    del graph, gouts, res  # the timed graph's memory is not the stream's to fight over
     be.synchronize()
     phases = layer.phase_ms(args.steps)  # last: its graph's memory must not disturb the timed graph
     stream = None

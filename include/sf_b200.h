@@ -342,6 +342,13 @@ void sf_graph_destroy(sf_graph* g);
 /* Overwrite a ciphertext's words from host memory (stream-ordered; pinned host
    memory makes it asynchronous): the input slots of a captured graph. */
 sf_status sf_ct_refill(sf_context* ctx, sf_ct* ct, const uint64_t* words);
+/* The same copy issued on a side stream, forked from the library stream here:
+   it overlaps the work enqueued until sf_ct_stage_wait(slot) joins it (call the
+   wait before the ciphertext's first use; inside a capture, before the capture
+   ends). Host words must be pinned for the overlap (and stay valid for every
+   replay of a captured graph, which re-reads them). Slots 0..63. */
+sf_status sf_ct_stage(sf_context* ctx, sf_ct* ct, const uint64_t* words, int slot);
+sf_status sf_ct_stage_wait(sf_context* ctx, int slot);
 
 /* Device memory in use (diagnostics): bytes currently allocated by CUDA-graph
    memory nodes on the context's device (outstanding step outputs of live

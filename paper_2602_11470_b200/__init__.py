@@ -375,6 +375,19 @@ class Backend:
         w = np.ascontiguousarray(words, dtype=np.uint64)
         _check(_native.lib().sf_ct_refill(self.ctx, ct.h, w.ctypes.data_as(_native.u64p)))
 
+    def stage(self, ct: "Ciphertext", words: np.ndarray, slot: int):
+        """refill() issued on a side stream that overlaps the work enqueued until
+        stage_wait(slot) (sf_ct_stage). `words` is used in place (pinned, C-contiguous
+        uint64; a captured graph re-reads it on every replay), so it must outlive the
+        copy -- and the graph."""
+        if not (isinstance(words, np.ndarray) and words.dtype == np.uint64 and words.flags.c_contiguous):
+            raise TypeError("stage: words must be a C-contiguous uint64 array (used in place)")
+        _check(_native.lib().sf_ct_stage(self.ctx, ct.h, words.ctypes.data_as(_native.u64p), int(slot)))
+
+    def stage_wait(self, slot: int):
+        """Join the staged copy of `slot` back into the library stream (sf_ct_stage_wait)."""
+        _check(_native.lib().sf_ct_stage_wait(self.ctx, int(slot)))
+
     # --- client side (off-ledger)
     def encrypt(self, slots, level: int = -1, layout=None, seed: Optional[int] = None) -> Ciphertext:
         s = np.asarray(slots, dtype=np.float64)

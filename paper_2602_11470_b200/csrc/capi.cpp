@@ -947,6 +947,40 @@ sf_status sf_ct_refill(sf_context* ctx, sf_ct* ct, const uint64_t* words) {
   });
 }
 
+// Staged input upload: the copy runs on a side stream forked from the library
+// stream at this point, so it overlaps whatever the library stream runs until
+// sf_ct_stage_wait(slot) joins it back (inside a capture: memcpy nodes on a
+// parallel branch of the graph, re-read from the host words on every replay).
+sf_status sf_ct_stage(sf_context* ctx, sf_ct* ct, const uint64_t* words, int slot) {
+  return guard([&] {
+    auto& c = *ctx->c;
+    const sf::Ct& v = ct->v;
+    sf::require(v.buf && !v.zero, sf::kInvalidTarget, "stage: ciphertext has no device words");
+    sf::require(slot >= 0 && slot < 64, sf::kInvalidTarget, "stage: slot out of range");
+    if (!c.copy_stream) SF_CUDA(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
+    while ((int)c.stage_ev.size() <= slot) {
+      cudaEvent_t f, d;
+      SF_CUDA(cudaEventCreateWithFlags(&f, cudaEventDisableTiming));
+      SF_CUDA(cudaEventCreateWithFlags(&d, cudaEventDisableTiming));
+      c.stage_ev.push_back({f, d});
+    }
+    auto [fork, done] = c.stage_ev[slot];
+    const size_t w = (size_t)v.limbs * c.n;
+    SF_CUDA(cudaEventRecord(fork, c.stream));
+    SF_CUDA(cudaStreamWaitEvent(c.copy_stream, fork, 0));
+    SF_CUDA(cudaMemcpyAsync(v.c0(), words, w * 8, cudaMemcpyHostToDevice, c.copy_stream));
+    SF_CUDA(cudaMemcpyAsync(v.c1(c.n), words + w, w * 8, cudaMemcpyHostToDevice, c.copy_stream));
+    SF_CUDA(cudaEventRecord(done, c.copy_stream));
+  });
+}
+sf_status sf_ct_stage_wait(sf_context* ctx, int slot) {
+  return guard([&] {
+    auto& c = *ctx->c;
+    sf::require(slot >= 0 && slot < (int)c.stage_ev.size(), sf::kInvalidTarget, "stage_wait: slot never staged");
+    SF_CUDA(cudaStreamWaitEvent(c.stream, c.stage_ev[slot].second, 0));
+  });
+}
+
 sf_status sf_mem_stats(sf_context* ctx, size_t* graph_bytes, size_t* pool_bytes) {
   return guard([&] {
     auto& c = *ctx->c;

@@ -264,6 +264,10 @@ struct Context {
   u64 enc_counter = 0;
   std::atomic<long long> launches{0};
   std::vector<cudaEvent_t> events;
+  // sf_ct_stage: host->device input copies on a side stream (overlapping the
+  // stages before the input's first use); per slot: fork and done events
+  cudaStream_t copy_stream = nullptr;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> stage_ev;
 
   std::mutex mu;  // guards key / plan caches
 

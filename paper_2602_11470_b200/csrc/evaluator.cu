@@ -104,6 +104,8 @@ Context::~Context() {
   sk.reset();
   tab_store.reset();
   for (auto e : events) cudaEventDestroy(e);
+  for (auto& [f, d] : stage_ev) cudaEventDestroy(f), cudaEventDestroy(d);
+  if (copy_stream) cudaStreamSynchronize(copy_stream), cudaStreamDestroy(copy_stream);
   for (auto& st : stage) {
     if (st.ev) cudaEventDestroy(st.ev);
     if (st.p) cudaFreeHost(st.p);

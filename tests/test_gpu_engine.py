@@ -169,6 +169,57 @@ def test_graph_capture_replays_the_step_bit_exactly():
         assert all(np.array_equal(g_, w_) for g_, w_ in zip(got, want))
 
 
+def test_staged_uploads_inside_a_captured_step():
+    # sf_ct_stage: the inputs' uploads as a parallel graph branch re-reading
+    # pinned host words on every replay, each joined right before its first use;
+    # replays with new host words reproduce the eager ciphertexts word for word
+    import torch
+    import paper_2602_11470_b200 as sf
+    from oracle.layout import make_interleaved
+    N, L = 4096, 4
+    be = sf.Backend(N, L, alpha=2)
+    W = np.random.default_rng(6).normal(size=(64, 64)) / 8
+    ly = make_interleaved(64, N, 0)
+
+    def enc(seed):
+        s = np.zeros(N)
+        s[np.arange(64) * ly.t] = np.random.default_rng(seed).normal(size=64)
+        return be.encrypt(s, L, ly, seed=seed)
+
+    plan = sf.VmmPlan(be, W, 64, 64, L, 0, 0, True)
+
+    def step(x, y, staged=None):
+        if staged:
+            be.stage(x, staged[0], 0)
+            be.stage(y, staged[1], 1)
+            be.stage_wait(0)
+        v = sf.vmm_interleaved(be, x, None, mask_output=True, plan=plan)
+        if staged:
+            be.stage_wait(1)
+        m = be.mul(v, be.level_drop(y, v.level))
+        return [v, be.rotate(m, 5)]
+
+    xa, ya, xb, yb = enc(1), enc(2), enc(3), enc(4)
+    want_a = [c.data() for c in step(xa, ya)]
+    want_b = [c.data() for c in step(xb, yb)]
+    x_slot = be.import_ct(xa.data(), xa.level, xa.scale, xa.layout)
+    y_slot = be.import_ct(ya.data(), ya.level, ya.scale, ya.layout)
+    dt = torch.uint64 if hasattr(torch, "uint64") else torch.int64
+    pin = [torch.empty(xa.data().shape, dtype=dt, pin_memory=True).numpy().view(np.uint64) for _ in range(2)]
+    # eager staging first (overlap on the side stream, joined before use)
+    pin[0][...], pin[1][...] = xb.data(), yb.data()
+    got = [c.data() for c in step(x_slot, y_slot, staged=pin)]
+    assert all(np.array_equal(g_, w_) for g_, w_ in zip(got, want_b))
+    graph, outs = be.capture(step, x_slot, y_slot, staged=pin)
+    for wx, wy, want in ((xa.data(), ya.data(), want_a), (xb.data(), yb.data(), want_b)):
+        pin[0][...], pin[1][...] = wx, wy  # the graph re-reads the pinned words on replay
+        graph.launch()
+        got = [c.data() for c in outs]
+        assert all(np.array_equal(g_, w_) for g_, w_ in zip(got, want))
+    with pytest.raises(TypeError):
+        be.stage(x_slot, xa.data().astype(np.int64), 0)
+
+
 def test_capture_cold_caches_and_graph_memory_is_released():
     """(1) Capturing a step whose lazy tables / keys are still cold: the capture
     is retried after one eager warm-up run and replays bit-exactly. (2) Graph-
