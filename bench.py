@@ -481,8 +481,9 @@ def cpu_baseline_sample():
 
 def token_stream(be, sf, layer, T=16):
     """A real decode stream through the public API: T consecutive tokens at
-    positions 2047, 2048, ... (n' grows 2047 -> 2047 + T): every token refills
-    the six stage inputs from pinned host words (H2D), runs Q/K/V with the K/V
+    positions 2047, 2048, ... (n' grows 2047 -> 2047 + T): every token uploads
+    the stage inputs from pinned host words (H2D, staged: each overlaps the
+    stages before its first use), runs Q/K/V with the K/V
     plans of its lane offset pos mod t (vmm.cpp:66-83 out_offset), RoPE at its
     own position (its RoPE plaintexts are encoded on the host inside the timed
     region -- for token p+1 while token p runs, sf_rope_prepare), appends k and
@@ -529,9 +530,11 @@ def token_stream(be, sf, layer, T=16):
     be.mem_reserve(16 << 30)
     be.synchronize()
     def token(cache, pos):
-        for slot, (w, _) in zip(layer.inputs[:4], host_in):
-            be.refill(slot, w)
+        # uploads staged on the side stream (sf_ct_stage), each joined before its stage
+        for i, (slot, (w, _)) in enumerate(zip(layer.inputs[:4], host_in)):
+            be.stage(slot, w, i)
         o = pos % t
+        be.stage_wait(0)
         q, k, v = sf.vmm_interleaved_multi(be, x, [layer.wq, wk[o], wv[o]])
         qr = sf.rope_apply(be, q, cfg, pos)
         kr = sf.rope_apply(be, k, cfg, pos)
@@ -539,8 +542,11 @@ def token_stream(be, sf, layer, T=16):
         cache = sf.k_append(be, cache, kr)
         maps = sf.qk_dot(be, qr, cache)
         att = sf.softmax_times_v(be, probs[:len(maps)], cache)
+        be.stage_wait(1)
         sf.vmm_interleaved(be, h7, None, plan=layer.wo)
+        be.stage_wait(2)
         sf.vmm_interleaved_multi(be, h3, [layer.wg, layer.wu])
+        be.stage_wait(3)
         dn = sf.vmm_interleaved(be, h1, None, plan=layer.wd)
         # next token's RoPE plaintexts: encoded on the host while this token runs
         sf.rope_prepare(be, cfg, pos + 1, rope_level, 0)
