@@ -965,7 +965,12 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 
 constexpr int kTmaWarps = 4;
 constexpr int kTmaRows = 4;  // per stage: digit row, key b row, key a row, c0 row
-template <int LOGR, bool PM1>
+// GATHER: the automorphism read straight out of the staged rows -- register k
+// of lane L (natural column c = 64 (k/2) + 2L + (k & 1)) loads column
+// br8((base + slope br8(c)) mod 256) with one 8-byte shared load -- instead of
+// natural-order loads plus the ShflPermQ blend/shuffle network (the rows are in
+// shared memory anyway; ~2-way bank conflicts, far fewer instructions per job)
+template <int LOGR, bool PM1, bool GATHER>
 __global__ void __launch_bounds__(kTmaWarps * 32, 3) ks_sum_tma_kernel(KsSumArgs A, Tabs T) {
   constexpr int LOGC = 8, C = 1 << LOGC, E = 8, LOGN = LOGR + LOGC;
   constexpr int tiles = (1 << LOGR) / kTmaWarps;
@@ -1060,14 +1065,26 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) ks_sum_tma_kernel(KsSumArgs
     phase ^= 1u << st;
     const u64* X = stage_base + (size_t)st * kTmaRows * C;
     const RowPerm<LOGR, LOGC> rp(rd, g);
-    const ShflPermQ sp(rp.base, rp.slope, lane);
     u64 x[E];
+    // GATHER: source columns of this lane's registers (br8(c) = br8(2L) | br8 of
+    // the register's fixed bits: one product per job, a constant per register)
+    const uint32_t gb = rp.base + rp.slope * (__brev((uint32_t)(2 * lane)) >> 24);
+    auto src_col = [&](int k) {
+      const uint32_t kb = (__brev((uint32_t)(64 * (k >> 1) + (k & 1))) >> 24);
+      return __brev((gb + rp.slope * kb) & 255u) >> 24;
+    };
+    if constexpr (GATHER) {
 #pragma unroll
-    for (int k = 0; k < E; k += 2) {
-      const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(X + eoff(k));
-      x[k] = v.x, x[k + 1] = v.y;
+      for (int k = 0; k < E; ++k) x[k] = X[src_col(k)];
+    } else {
+      const ShflPermQ sp(rp.base, rp.slope, lane);
+#pragma unroll
+      for (int k = 0; k < E; k += 2) {
+        const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(X + eoff(k));
+        x[k] = v.x, x[k + 1] = v.y;
+      }
+      sp.apply(x);
     }
-    sp.apply(x);
 #pragma unroll
     for (int k = 0; k < E; k += 2) {
       const ulonglong2 kb = *reinterpret_cast<const ulonglong2*>(X + C + eoff(k));
@@ -1078,12 +1095,18 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) ks_sum_tma_kernel(KsSumArgs
       mac128(sa[k + 1], x[k + 1], ka.y);
     }
     if (c0t) {  // P * sigma_g(c0)
+      if constexpr (GATHER) {
 #pragma unroll
-      for (int k = 0; k < E; k += 2) {
-        const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(X + 3 * C + eoff(k));
-        x[k] = v.x, x[k + 1] = v.y;
+        for (int k = 0; k < E; ++k) x[k] = X[3 * C + src_col(k)];
+      } else {
+        const ShflPermQ sp(rp.base, rp.slope, lane);
+#pragma unroll
+        for (int k = 0; k < E; k += 2) {
+          const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(X + 3 * C + eoff(k));
+          x[k] = v.x, x[k + 1] = v.y;
+        }
+        sp.apply(x);
       }
-      sp.apply(x);
 #pragma unroll
       for (int k = 0; k < E; ++k) {
         if constexpr (PM1)
@@ -1242,15 +1265,23 @@ void run_ks_sum(Context& c, const KsSumArgs& a) {
       constexpr size_t sm = (size_t)kTmaWarps * (2 * kTmaRows + 1) * 256 * sizeof(u64) + kTmaWarps * 2 * sizeof(u64);
       static bool attr = false;
       if (!attr) {
-        SF_CUDA(cudaFuncSetAttribute(ks_sum_tma_kernel<LOGR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        SF_CUDA(cudaFuncSetAttribute(ks_sum_tma_kernel<LOGR, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        SF_CUDA(cudaFuncSetAttribute(ks_sum_tma_kernel<LOGR, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        SF_CUDA(cudaFuncSetAttribute(ks_sum_tma_kernel<LOGR, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        SF_CUDA(cudaFuncSetAttribute(ks_sum_tma_kernel<LOGR, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        SF_CUDA(cudaFuncSetAttribute(ks_sum_tma_kernel<LOGR, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         attr = true;
       }
       const unsigned grid = (unsigned)(a.nout * a.nt * ((1 << LOGR) / kTmaWarps));
-      if (a.pm_one)
-        ks_sum_tma_kernel<LOGR, true><<<grid, kTmaWarps * 32, sm, c.stream>>>(a, c.tabs);
+      // SF_VARIANT bit 10: the shuffle-network automorphism instead of the shared-memory gather (A/B)
+      const bool gather = !(c.variant & 1024);
+      if (a.pm_one && gather)
+        ks_sum_tma_kernel<LOGR, true, true><<<grid, kTmaWarps * 32, sm, c.stream>>>(a, c.tabs);
+      else if (a.pm_one)
+        ks_sum_tma_kernel<LOGR, true, false><<<grid, kTmaWarps * 32, sm, c.stream>>>(a, c.tabs);
+      else if (gather)
+        ks_sum_tma_kernel<LOGR, false, true><<<grid, kTmaWarps * 32, sm, c.stream>>>(a, c.tabs);
       else
-        ks_sum_tma_kernel<LOGR, false><<<grid, kTmaWarps * 32, sm, c.stream>>>(a, c.tabs);
+        ks_sum_tma_kernel<LOGR, false, false><<<grid, kTmaWarps * 32, sm, c.stream>>>(a, c.tabs);
       return;
     }
   }
