@@ -718,10 +718,13 @@ __global__ void __launch_bounds__(kWarps * 32, LOGC >= 9 ? 1 : 2) ks_sum_kernel(
   // Montgomery-domain sums (keys and pm carry R = 2^64: get_key_mont): a product
   // adds < 2^56 to the high word, a plain term c (P * sigma(c0) with P^-1 folded
   // into the keys) enters as c R = c * 2^64, i.e. c added to the high word. A job
-  // raises the high word by at most 2^60 + 2^56 (q < 2^60: one product's high word
-  // <= 2^56, one plain c < 2^60), so from a reduced high word (< q) 14 jobs stay
-  // below 2^60 (1 + 14 * 1.0625) < 2^64: it is brought back below q every 14 jobs
-  // (T changes by multiples of q 2^64) and the sum finishes with one REDC.
+  // raises the high word by at most 2^60 + ndig 2^56 (q < 2^60: one product's high
+  // word <= 2^56 per digit, one plain c < 2^60), so from a reduced high word (< q)
+  // J jobs stay below 2^60 (1 + J (1 + ndig / 16)) < 2^64 for J <= 239 / (16 + ndig)
+  // (14 single-digit jobs, 13 at two digits, 11 at four): the high word is brought
+  // back below q every fold_at jobs (T changes by multiples of q 2^64) and the sum
+  // finishes with one REDC.
+  const int fold_at = 239 / (16 + A.ndig);
   int terms = 0;  // jobs since the last high-word reduction
   auto fold = [&]() {
 #pragma unroll
@@ -734,7 +737,7 @@ __global__ void __launch_bounds__(kWarps * 32, LOGC >= 9 ? 1 : 2) ks_sum_kernel(
   for (int jb = A.out_begin[o]; jb < A.out_begin[o + 1]; ++jb) {
     const int s = A.jsrc[jb];
     const u64 g = A.g[jb];
-    if (terms >= 14) fold();
+    if (terms >= fold_at) fold();
     if (g <= 1) {  // identity term: P * (c0, c1) on the Q primes (ext_c0: c0 on every target)
       if (!c0t) continue;
       const u64* a0 = A.c0[s] + (size_t)t * n + rowoff;
@@ -970,7 +973,8 @@ constexpr int kTmaRows = 4;  // per stage: digit row, key b row, key a row, c0 r
 // br8((base + slope br8(c)) mod 256) with one 8-byte shared load -- instead of
 // natural-order loads plus the ShflPermQ blend/shuffle network (the rows are in
 // shared memory anyway; ~2-way bank conflicts, far fewer instructions per job)
-template <int LOGR, bool PM1, bool GATHER>
+// ONE: single-digit sums (the QKᵀ folds), the digit loop compiled away
+template <int LOGR, bool PM1, bool GATHER, bool ONE>
 __global__ void __launch_bounds__(kTmaWarps * 32, 3) ks_sum_tma_kernel(KsSumArgs A, Tabs T) {
   constexpr int LOGC = 8, C = 1 << LOGC, E = 8, LOGN = LOGR + LOGC;
   constexpr int tiles = (1 << LOGR) / kTmaWarps;
@@ -999,19 +1003,22 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) ks_sum_tma_kernel(KsSumArgs
   }
   __syncwarp();
   const uint32_t row_bytes = C * sizeof(u64);
-  // lane 0: arm stage st's barrier and copy job jb's rows into it
-  auto issue = [&](int jb, int st) {
+  // lane 0: arm stage st's barrier and copy the rows of job jb's digit j into it
+  // (the digit row, its two key rows; with digit 0, the c0 row)
+  auto issue = [&](int jb, int j, int st) {
     if (lane != 0) return;
     const int s = A.jsrc[jb];
     const int rs = (int)RowPerm<LOGR, LOGC>(rd, A.g[jb]).src_row;
     u64* dst = stage_base + (size_t)st * kTmaRows * C;
+    const bool wc0 = c0t && j == 0;
     tma1d::fence_proxy_async();  // the warp's earlier shared-memory reads of this stage come first
-    tma1d::mbar_expect_tx(&bars[st], (c0t ? 4 : 3) * row_bytes);
-    const u64* src = (t < A.alpha && t < A.limbs) ? A.c1[s] + (size_t)t * n : A.ext[s] + (size_t)t * n;
+    tma1d::mbar_expect_tx(&bars[st], (wc0 ? 4 : 3) * row_bytes);
+    const int lo = j * A.alpha, hi = min(lo + A.alpha, A.limbs);
+    const u64* src = (t >= lo && t < hi) ? A.c1[s] + (size_t)t * n : A.ext[s] + ((size_t)j * A.nt + t) * n;
     tma1d::bulk_g2s(dst, src + (size_t)rs * C, row_bytes, &bars[st]);
-    tma1d::bulk_g2s(dst + C, A.key[jb] + (size_t)m * n + rowoff, row_bytes, &bars[st]);
-    tma1d::bulk_g2s(dst + 2 * C, A.key[jb] + ((size_t)A.np + m) * n + rowoff, row_bytes, &bars[st]);
-    if (c0t) tma1d::bulk_g2s(dst + 3 * C, A.c0[s] + (size_t)t * n + (size_t)rs * C, row_bytes, &bars[st]);
+    tma1d::bulk_g2s(dst + C, A.key[jb] + ((size_t)(2 * j) * A.np + m) * n + rowoff, row_bytes, &bars[st]);
+    tma1d::bulk_g2s(dst + 2 * C, A.key[jb] + ((size_t)(2 * j + 1) * A.np + m) * n + rowoff, row_bytes, &bars[st]);
+    if (wc0) tma1d::bulk_g2s(dst + 3 * C, A.c0[s] + (size_t)t * n + (size_t)rs * C, row_bytes, &bars[st]);
   };
   auto next_rot = [&](int jb) {  // first non-identity job at or after jb
     while (jb < b1 && A.g[jb] <= 1) ++jb;
@@ -1020,6 +1027,8 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) ks_sum_tma_kernel(KsSumArgs
   U128 sb[E], sa[E];
 #pragma unroll
   for (int k = 0; k < E; ++k) sb[k] = U128{0, 0}, sa[k] = U128{0, 0};
+  const int ndig = ONE ? 1 : A.ndig;
+  const int fold_at = ONE ? 14 : 239 / (16 + ndig);  // see ks_sum_kernel
   int terms = 0;  // jobs since the last high-word reduction (see ks_sum_kernel)
   auto fold = [&]() {
 #pragma unroll
@@ -1031,11 +1040,11 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) ks_sum_tma_kernel(KsSumArgs
   };
   int cur = next_rot(b0), st = 0;
   uint32_t phase = 0;  // bit st: parity of stage st's next completion
-  if (cur < b1) issue(cur, 0);
+  if (cur < b1) issue(cur, 0, 0);
   for (int jb = b0; jb < b1; ++jb) {
     const int s = A.jsrc[jb];
     const u64 g = A.g[jb];
-    if (terms >= 14) fold();
+    if (terms >= fold_at) fold();
     if (g <= 1) {  // identity term: P * (c0, c1) on the Q primes (ext_c0: c0 on every target), from global memory
       if (!c0t) continue;
 #pragma unroll
@@ -1058,13 +1067,18 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) ks_sum_tma_kernel(KsSumArgs
       ++terms;
       continue;
     }
-    // jb == cur: its rows are in (or on their way to) stage st; start the next job's copies
-    const int nxt = next_rot(jb + 1);
-    if (nxt < b1) issue(nxt, st ^ 1);
+    const RowPerm<LOGR, LOGC> rp(rd, g);
+    for (int j = 0; j < ndig; ++j) {
+    // (jb, j): its rows are in (or on their way to) stage st; start the next step's copies
+    if (j + 1 < ndig) {
+      issue(jb, j + 1, st ^ 1);
+    } else {
+      const int nxt = next_rot(jb + 1);
+      if (nxt < b1) issue(nxt, 0, st ^ 1);
+    }
     tma1d::mbar_wait(&bars[st], (phase >> st) & 1);
     phase ^= 1u << st;
     const u64* X = stage_base + (size_t)st * kTmaRows * C;
-    const RowPerm<LOGR, LOGC> rp(rd, g);
     u64 x[E];
     // GATHER: source columns of this lane's registers (br8(c) = br8(2L) | br8 of
     // the register's fixed bits: one product per job, a constant per register)
@@ -1094,7 +1108,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) ks_sum_tma_kernel(KsSumArgs
       mac128(sb[k + 1], x[k + 1], kb.y);
       mac128(sa[k + 1], x[k + 1], ka.y);
     }
-    if (c0t) {  // P * sigma_g(c0)
+    if (c0t && j == 0) {  // P * sigma_g(c0)
       if constexpr (GATHER) {
 #pragma unroll
         for (int k = 0; k < E; ++k) x[k] = X[3 * C + src_col(k)];
@@ -1117,6 +1131,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) ks_sum_tma_kernel(KsSumArgs
     }
     __syncwarp();  // every lane is done with stage st before lane 0 refills it
     st ^= 1;
+    }
     ++terms;
   }
   u64 vb[E], va[E];
@@ -1260,28 +1275,38 @@ void run_ks_row(Context& c, const KsRowArgs& a) {
 template <int LOGR, int LOGC>
 void run_ks_sum(Context& c, const KsSumArgs& a) {
   if constexpr (LOGC == 8) {
-    // single-digit sums: the TMA-pipelined row stage (SF_VARIANT bit 6: off, for A/B)
-    if (a.ndig == 1 && !(c.variant & 64)) {
+    // the TMA-pipelined row stage, one (job, digit) step per stage (SF_VARIANT bit 6:
+    // ks_sum_kernel, for A/B; bit 11: TMA for single-digit sums only)
+    if ((a.ndig == 1 || !(c.variant & 2048)) && !(c.variant & 64)) {
       constexpr size_t sm = (size_t)kTmaWarps * (2 * kTmaRows + 1) * 256 * sizeof(u64) + kTmaWarps * 2 * sizeof(u64);
       static bool attr = false;
       if (!attr) {
-        SF_CUDA(cudaFuncSetAttribute(ks_sum_tma_kernel<LOGR, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        SF_CUDA(cudaFuncSetAttribute(ks_sum_tma_kernel<LOGR, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        SF_CUDA(cudaFuncSetAttribute(ks_sum_tma_kernel<LOGR, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        SF_CUDA(cudaFuncSetAttribute(ks_sum_tma_kernel<LOGR, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        SF_CUDA(cudaFuncSetAttribute(ks_sum_tma_kernel<LOGR, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        SF_CUDA(cudaFuncSetAttribute(ks_sum_tma_kernel<LOGR, false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        SF_CUDA(cudaFuncSetAttribute(ks_sum_tma_kernel<LOGR, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        SF_CUDA(cudaFuncSetAttribute(ks_sum_tma_kernel<LOGR, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        SF_CUDA(cudaFuncSetAttribute(ks_sum_tma_kernel<LOGR, true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        SF_CUDA(cudaFuncSetAttribute(ks_sum_tma_kernel<LOGR, false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         attr = true;
       }
       const unsigned grid = (unsigned)(a.nout * a.nt * ((1 << LOGR) / kTmaWarps));
       // SF_VARIANT bit 10: the shuffle-network automorphism instead of the shared-memory gather (A/B)
       const bool gather = !(c.variant & 1024);
-      if (a.pm_one && gather)
-        ks_sum_tma_kernel<LOGR, true, true><<<grid, kTmaWarps * 32, sm, c.stream>>>(a, c.tabs);
-      else if (a.pm_one)
-        ks_sum_tma_kernel<LOGR, true, false><<<grid, kTmaWarps * 32, sm, c.stream>>>(a, c.tabs);
-      else if (gather)
-        ks_sum_tma_kernel<LOGR, false, true><<<grid, kTmaWarps * 32, sm, c.stream>>>(a, c.tabs);
-      else
-        ks_sum_tma_kernel<LOGR, false, false><<<grid, kTmaWarps * 32, sm, c.stream>>>(a, c.tabs);
+      const dim3 blk(kTmaWarps * 32);
+      if (a.ndig == 1) {
+        if (a.pm_one && gather)
+          ks_sum_tma_kernel<LOGR, true, true, true><<<grid, blk, sm, c.stream>>>(a, c.tabs);
+        else if (a.pm_one)
+          ks_sum_tma_kernel<LOGR, true, false, true><<<grid, blk, sm, c.stream>>>(a, c.tabs);
+        else if (gather)
+          ks_sum_tma_kernel<LOGR, false, true, true><<<grid, blk, sm, c.stream>>>(a, c.tabs);
+        else
+          ks_sum_tma_kernel<LOGR, false, false, true><<<grid, blk, sm, c.stream>>>(a, c.tabs);
+      } else if (a.pm_one) {
+        ks_sum_tma_kernel<LOGR, true, true, false><<<grid, blk, sm, c.stream>>>(a, c.tabs);
+      } else {
+        ks_sum_tma_kernel<LOGR, false, true, false><<<grid, blk, sm, c.stream>>>(a, c.tabs);
+      }
       return;
     }
   }
