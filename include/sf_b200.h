@@ -349,6 +349,10 @@ sf_status sf_ct_refill(sf_context* ctx, sf_ct* ct, const uint64_t* words);
    replay of a captured graph, which re-reads them). Slots 0..63. */
 sf_status sf_ct_stage(sf_context* ctx, sf_ct* ct, const uint64_t* words, int slot);
 sf_status sf_ct_stage_wait(sf_context* ctx, int slot);
+/* Read-back counterpart: ct's words -> pinned host memory [2][limbs][n] on the side
+   stream, forked here (ct final at this point), overlapping the work enqueued until
+   sf_ct_stage_wait(slot); the host words are valid once the stream is synchronised. */
+sf_status sf_ct_stage_out(sf_context* ctx, const sf_ct* ct, uint64_t* words, int slot);
 
 /* Device memory in use (diagnostics): bytes currently allocated by CUDA-graph
    memory nodes on the context's device (outstanding step outputs of live

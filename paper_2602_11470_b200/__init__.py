@@ -384,6 +384,16 @@ class Backend:
             raise TypeError("stage: words must be a C-contiguous uint64 array (used in place)")
         _check(_native.lib().sf_ct_stage(self.ctx, ct.h, words.ctypes.data_as(_native.u64p), int(slot)))
 
+    def stage_out(self, ct: "Ciphertext", words: np.ndarray, slot: int):
+        """Read ct's words [2][level+1][n] into `words` (pinned, C-contiguous uint64,
+        used in place) on the side stream, overlapping the work enqueued until
+        stage_wait(slot) (sf_ct_stage_out); valid after synchronize()."""
+        if not (isinstance(words, np.ndarray) and words.dtype == np.uint64 and words.flags.c_contiguous):
+            raise TypeError("stage_out: words must be a C-contiguous uint64 array (used in place)")
+        if words.size != 2 * (ct.level + 1) * self.n:
+            raise ValueError("stage_out: words must hold [2][level+1][n] words")
+        _check(_native.lib().sf_ct_stage_out(self.ctx, ct.h, words.ctypes.data_as(_native.u64p), int(slot)))
+
     def stage_wait(self, slot: int):
         """Join the staged copy of `slot` back into the library stream (sf_ct_stage_wait)."""
         _check(_native.lib().sf_ct_stage_wait(self.ctx, int(slot)))

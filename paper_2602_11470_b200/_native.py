@@ -70,6 +70,7 @@ SIGNATURES = {
     "sf_ct_refill": (st, [vp, vp, u64p]),
     "sf_ct_stage": (st, [vp, vp, u64p, C.c_int]),
     "sf_ct_stage_wait": (st, [vp, C.c_int]),
+    "sf_ct_stage_out": (st, [vp, vp, u64p, C.c_int]),
     "sf_context_create": (st, [C.POINTER(SfParams), vpp]),
     "sf_context_destroy": (None, [vp]),
     "sf_context_info": (st, [vp, ip, ip, ip, ip, ip, u64p]),

@@ -973,6 +973,31 @@ sf_status sf_ct_stage(sf_context* ctx, sf_ct* ct, const uint64_t* words, int slo
     SF_CUDA(cudaEventRecord(done, c.copy_stream));
   });
 }
+// The read-back counterpart: device words -> (pinned) host memory on the side
+// stream, forked here (after everything enqueued so far, i.e. once ct is final),
+// overlapping what follows until sf_ct_stage_wait(slot).
+sf_status sf_ct_stage_out(sf_context* ctx, const sf_ct* ct, uint64_t* words, int slot) {
+  return guard([&] {
+    auto& c = *ctx->c;
+    const sf::Ct& v = ct->v;
+    sf::require(v.buf && !v.zero, sf::kInvalidTarget, "stage_out: ciphertext has no device words");
+    sf::require(slot >= 0 && slot < 64, sf::kInvalidTarget, "stage_out: slot out of range");
+    if (!c.copy_stream) SF_CUDA(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
+    while ((int)c.stage_ev.size() <= slot) {
+      cudaEvent_t f, d;
+      SF_CUDA(cudaEventCreateWithFlags(&f, cudaEventDisableTiming));
+      SF_CUDA(cudaEventCreateWithFlags(&d, cudaEventDisableTiming));
+      c.stage_ev.push_back({f, d});
+    }
+    auto [fork, done] = c.stage_ev[slot];
+    const size_t w = (size_t)v.limbs * c.n;
+    SF_CUDA(cudaEventRecord(fork, c.stream));
+    SF_CUDA(cudaStreamWaitEvent(c.copy_stream, fork, 0));
+    SF_CUDA(cudaMemcpyAsync(words, v.c0(), w * 8, cudaMemcpyDeviceToHost, c.copy_stream));
+    SF_CUDA(cudaMemcpyAsync(words + w, v.c1(c.n), w * 8, cudaMemcpyDeviceToHost, c.copy_stream));
+    SF_CUDA(cudaEventRecord(done, c.copy_stream));
+  });
+}
 sf_status sf_ct_stage_wait(sf_context* ctx, int slot) {
   return guard([&] {
     auto& c = *ctx->c;

@@ -188,15 +188,19 @@ def test_staged_uploads_inside_a_captured_step():
 
     plan = sf.VmmPlan(be, W, 64, 64, L, 0, 0, True)
 
-    def step(x, y, staged=None):
+    def step(x, y, staged=None, out=None):
         if staged:
             be.stage(x, staged[0], 0)
             be.stage(y, staged[1], 1)
             be.stage_wait(0)
         v = sf.vmm_interleaved(be, x, None, mask_output=True, plan=plan)
+        if out is not None:
+            be.stage_out(v, out, 2)  # read-back overlapping the rest of the step
         if staged:
             be.stage_wait(1)
         m = be.mul(v, be.level_drop(y, v.level))
+        if out is not None:
+            be.stage_wait(2)
         return [v, be.rotate(m, 5)]
 
     xa, ya, xb, yb = enc(1), enc(2), enc(3), enc(4)
@@ -210,10 +214,13 @@ def test_staged_uploads_inside_a_captured_step():
     pin[0][...], pin[1][...] = xb.data(), yb.data()
     got = [c.data() for c in step(x_slot, y_slot, staged=pin)]
     assert all(np.array_equal(g_, w_) for g_, w_ in zip(got, want_b))
-    graph, outs = be.capture(step, x_slot, y_slot, staged=pin)
+    out = torch.empty(want_a[0].shape, dtype=dt, pin_memory=True).numpy().view(np.uint64)
+    graph, outs = be.capture(step, x_slot, y_slot, staged=pin, out=out)
     for wx, wy, want in ((xa.data(), ya.data(), want_a), (xb.data(), yb.data(), want_b)):
         pin[0][...], pin[1][...] = wx, wy  # the graph re-reads the pinned words on replay
         graph.launch()
+        be.synchronize()
+        assert np.array_equal(out, want[0])  # staged read-back (sf_ct_stage_out)
         got = [c.data() for c in outs]
         assert all(np.array_equal(g_, w_) for g_, w_ in zip(got, want))
     with pytest.raises(TypeError):
