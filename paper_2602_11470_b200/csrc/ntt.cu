@@ -1049,9 +1049,17 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) ks_sum_tma_kernel(KsSumArgs
       if (!c0t) continue;
 #pragma unroll
       for (int k = 0; k < E; k += 2) {
-        const ulonglong2 v0 = *reinterpret_cast<const ulonglong2*>(A.c0[s] + (size_t)t * n + rowoff + eoff(k));
-        const ulonglong2 v1 = qt ? *reinterpret_cast<const ulonglong2*>(A.c1[s] + (size_t)t * n + rowoff + eoff(k))
-                                 : make_ulonglong2(0, 0);
+        ulonglong2 v0, v1;
+        if constexpr (GATHER) {  // strided: register k holds column 32 k + lane
+          const u64* a0 = A.c0[s] + (size_t)t * n + rowoff + lane;
+          const u64* a1 = A.c1[s] + (size_t)t * n + rowoff + lane;
+          v0 = make_ulonglong2(a0[32 * k], a0[32 * (k + 1)]);
+          v1 = qt ? make_ulonglong2(a1[32 * k], a1[32 * (k + 1)]) : make_ulonglong2(0, 0);
+        } else {
+          v0 = *reinterpret_cast<const ulonglong2*>(A.c0[s] + (size_t)t * n + rowoff + eoff(k));
+          v1 = qt ? *reinterpret_cast<const ulonglong2*>(A.c1[s] + (size_t)t * n + rowoff + eoff(k))
+                  : make_ulonglong2(0, 0);
+        }
         if constexpr (PM1) {
           sb[k].hi += v0.x;
           sb[k + 1].hi += v0.y;
@@ -1080,11 +1088,13 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) ks_sum_tma_kernel(KsSumArgs
     phase ^= 1u << st;
     const u64* X = stage_base + (size_t)st * kTmaRows * C;
     u64 x[E];
-    // GATHER: source columns of this lane's registers (br8(c) = br8(2L) | br8 of
-    // the register's fixed bits: one product per job, a constant per register)
-    const uint32_t gb = rp.base + rp.slope * (__brev((uint32_t)(2 * lane)) >> 24);
+    // GATHER: strided registers (register k of lane L = column c = 32 k + L);
+    // source column br8(base + slope br8(c)), br8(c) = br8(L) | br8(32 k): one
+    // product per job, a constant per register. The 16 lanes of a half warp then
+    // read 16 distinct banks (br8(c) varies in its top four bits)
+    const uint32_t gb = rp.base + rp.slope * (__brev((uint32_t)lane) >> 24);
     auto src_col = [&](int k) {
-      const uint32_t kb = (__brev((uint32_t)(64 * (k >> 1) + (k & 1))) >> 24);
+      const uint32_t kb = (__brev((uint32_t)(32 * k)) >> 24);
       return __brev((gb + rp.slope * kb) & 255u) >> 24;
     };
     if constexpr (GATHER) {
@@ -1101,8 +1111,14 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) ks_sum_tma_kernel(KsSumArgs
     }
 #pragma unroll
     for (int k = 0; k < E; k += 2) {
-      const ulonglong2 kb = *reinterpret_cast<const ulonglong2*>(X + C + eoff(k));
-      const ulonglong2 ka = *reinterpret_cast<const ulonglong2*>(X + 2 * C + eoff(k));
+      ulonglong2 kb, ka;
+      if constexpr (GATHER) {
+        kb = make_ulonglong2(X[C + 32 * k + lane], X[C + 32 * (k + 1) + lane]);
+        ka = make_ulonglong2(X[2 * C + 32 * k + lane], X[2 * C + 32 * (k + 1) + lane]);
+      } else {
+        kb = *reinterpret_cast<const ulonglong2*>(X + C + eoff(k));
+        ka = *reinterpret_cast<const ulonglong2*>(X + 2 * C + eoff(k));
+      }
       mac128(sb[k], x[k], kb.x);
       mac128(sa[k], x[k], ka.x);
       mac128(sb[k + 1], x[k + 1], kb.y);
@@ -1147,13 +1163,25 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) ks_sum_tma_kernel(KsSumArgs
   const bool ntt_a = qt && t < A.inv_from, ntt_b = ntt_a || A.keep_b;
   if (ntt_b) {
 #pragma unroll
-    for (int k = 0; k < E; k += 2)
-      *reinterpret_cast<ulonglong2*>(accb + rowoff + eoff(k)) = make_ulonglong2(vb[k], vb[k + 1]);
+    for (int k = 0; k < E; k += 2) {
+      if constexpr (GATHER) {
+        accb[rowoff + 32 * k + lane] = vb[k];
+        accb[rowoff + 32 * (k + 1) + lane] = vb[k + 1];
+      } else {
+        *reinterpret_cast<ulonglong2*>(accb + rowoff + eoff(k)) = make_ulonglong2(vb[k], vb[k + 1]);
+      }
+    }
   }
   if (ntt_a) {
 #pragma unroll
-    for (int k = 0; k < E; k += 2)
-      *reinterpret_cast<ulonglong2*>(acca + rowoff + eoff(k)) = make_ulonglong2(va[k], va[k + 1]);
+    for (int k = 0; k < E; k += 2) {
+      if constexpr (GATHER) {
+        acca[rowoff + 32 * k + lane] = va[k];
+        acca[rowoff + 32 * (k + 1) + lane] = va[k + 1];
+      } else {
+        *reinterpret_cast<ulonglong2*>(acca + rowoff + eoff(k)) = make_ulonglong2(va[k], va[k + 1]);
+      }
+    }
   } else {
     const u64* W = T.ipsi + ((size_t)m << LOGN);
     const u64* Ws = T.ipsi_s + ((size_t)m << LOGN);
@@ -1163,6 +1191,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) ks_sum_tma_kernel(KsSumArgs
       ws = Ws[i];
     };
     auto restride = [&](u64 (&v)[E]) {
+      if constexpr (GATHER) return;  // the registers are strided already
 #pragma unroll
       for (int k = 0; k < E; ++k) buf[xp(eoff(k & ~1) + (k & 1))] = v[k];
       __syncwarp();
