@@ -1208,21 +1208,21 @@ def main():
     fams = ["ntt_rows", "keyswitch_rows", "ctpt_mac", "fused_col", "elementwise", "sampling"]
     prof = {f: {"ms_per_step": ms[i] / args.steps, "launches_per_step": nl[i] / args.steps,
                 # algorithmic-byte model (counts L2- and shared-memory-served re-reads: an
-                # upper bound on DRAM traffic; measured DRAM bytes: profiles/r2_traffic_v6.json)
+                # upper bound on DRAM traffic; measured DRAM bytes: profiles/r2_traffic_v7.json)
                 "alg_GBps": (by[i] / (ms[i] * 1e-3) / 1e9) if ms[i] > 0 else None} for i, f in enumerate(fams)}
     dom = max(range(6), key=lambda i: ms[i])
     P = peaks()
     peak = P.get("hbm_gbs", 6650.0)
     achieved = by[dom] / (ms[dom] * 1e-3) / 1e9 if ms[dom] > 0 else 0.0
     traffic = None
-    try:  # ncu DRAM bytes per launch of the same family (profiles/r2_traffic_v6.json, tools/traffic.py)
-        traffic = json.load(open(os.path.join(ROOT, "profiles", "r2_traffic_v6.json")))["families"][fams[dom]][
+    try:  # ncu DRAM bytes per launch of the same family (profiles/r2_traffic_v7.json, tools/traffic.py)
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "r2_traffic_v7.json")))["families"][fams[dom]][
             "dram_bytes_per_launch"]
     except Exception:
         pass
     roofline = {"bound": "hbm", "kernel": fams[dom], "achieved": round(achieved, 1), "peak": peak,
                 "unit": "GB/s", "frac": round(achieved / peak, 4),
-                "traffic": traffic, "traffic_source": "profiles/r2_traffic_v6.json (ncu launch list, same family)",
+                "traffic": traffic, "traffic_source": "profiles/r2_traffic_v7.json (ncu launch list, same family)",
                 "peak_source": "measured" if not P.get("_fallback") else "fallback",
                 "algorithmic_bytes_per_launch": by[dom] / max(nl[dom], 1),
                 "avg_launch_us": ms[dom] * 1e3 / max(nl[dom], 1)}
@@ -1243,9 +1243,9 @@ def main():
                     "frac": round(bf_tot / (nt_ms * 1e-3) / 1e9 / bpk, 4) if (nt_ms > 0 and bpk) else None,
                     "peak_source": "profiles/r1_butterfly_peak.json (tools/microbench/butterfly.cu on B200)"}
     try:  # the same kernels' FMA-heavy pipe utilisation from the committed ncu capture
-        pu = json.load(open(os.path.join(ROOT, "profiles", "r2_pipe_util_v6.json")))
+        pu = json.load(open(os.path.join(ROOT, "profiles", "r2_pipe_util_v7.json")))
         int_roofline["fmaheavy_pipe_pct_share_weighted"] = pu["share_weighted_fmaheavy_pct"]
-        int_roofline["fmaheavy_pipe_source"] = "profiles/r2_pipe_util_v6.json (ncu, top-6 kernels, %.1f%% of the step)" % \
+        int_roofline["fmaheavy_pipe_source"] = "profiles/r2_pipe_util_v7.json (ncu, top-6 kernels, %.1f%% of the step)" % \
             pu["covered_step_share_pct"]
     except Exception:
         pass
